@@ -1,0 +1,67 @@
+"""Stand-in quantization schemes {(b_h, R_h)} as plain data.
+
+The paper's actual schemes live in an unavailable supplement,
+so these are the stand-ins of SURVEY.md §8(c) Q1 / DESIGN.md "Readings": bit
+widths follow the paper's compression figures (teaser P:85, T-large P:945-946),
+ranges are powers of two (so Delta = R 2^-b is exact) chosen as 2x the recorded
+magnitudes ("multiply the ranges by a factor (e.g., 2)").
+
+A scheme is a dict:
+  dim, material ("elastic" | "fluid"), rounding ("dither" | "rne"), seed,
+  fields: list of {attr: x|v|F|J|C, comp, kind: fixed|raw, frac_bits, range, offset}
+in PACKING order (bit pack).  Stored width of a fixed field is
+frac_bits + 1 (two's complement, reading Q2).  This module holds data only.
+"""
+
+DITHER_SEED = 0x9E3779B97F4A7C15
+
+
+def _fields(attr, n, kind, frac_bits=0, rng=1.0, offset=0.0):
+    return [dict(attr=attr, comp=c, kind=kind, frac_bits=frac_bits, range=rng, offset=offset)
+            for c in range(n)]
+
+
+def fp32(dim, material="elastic"):
+    """All fields RAW_F32: the uncompressed baseline (3D elastic W=24, fluid W=16, 2D W=12)."""
+    d = dim
+    f = _fields("x", d, "raw") + _fields("v", d, "raw")
+    f += _fields("J", 1, "raw") if material == "fluid" else _fields("F", d * d, "raw")
+    f += _fields("C", d * d, "raw")
+    return dict(dim=dim, material=material, rounding="dither", seed=DITHER_SEED, fields=f)
+
+
+def x16(v_range=8.0):
+    """C1 (2D elastic): x, v 16-bit fixed (b=15); F, C raw fp32 -> 320 bits, W=10."""
+    f = _fields("x", 2, "fixed", 15, 1.0) + _fields("v", 2, "fixed", 15, v_range)
+    f += _fields("F", 4, "raw") + _fields("C", 4, "raw")
+    return dict(dim=2, material="elastic", rounding="dither", seed=DITHER_SEED, fields=f)
+
+
+def e01():
+    """E0.1 (3D elastic, eps=0.1): x 3x19, v 3x15, F 9x14, C 9x13 = 345 bits, W=11."""
+    f = _fields("x", 3, "fixed", 18, 1.0) + _fields("v", 3, "fixed", 14, 8.0)
+    f += _fields("F", 9, "fixed", 13, 4.0) + _fields("C", 9, "fixed", 12, 256.0)
+    return dict(dim=3, material="elastic", rounding="dither", seed=DITHER_SEED, fields=f)
+
+
+def e001():
+    """E0.01 (3D elastic, eps=0.01): x 3x20, v 3x16, F 9x14, C 9x13 = 351 bits, W=11."""
+    f = _fields("x", 3, "fixed", 19, 1.0) + _fields("v", 3, "fixed", 15, 8.0)
+    f += _fields("F", 9, "fixed", 13, 4.0) + _fields("C", 9, "fixed", 12, 256.0)
+    return dict(dim=3, material="elastic", rounding="dither", seed=DITHER_SEED, fields=f)
+
+
+def f2():
+    """F2 (3D fluid): x 3x19, v 3x15, J 1x16 (offset 1), C 9x15 = 253 bits, W=8."""
+    f = _fields("x", 3, "fixed", 18, 1.0) + _fields("v", 3, "fixed", 14, 8.0)
+    f += _fields("J", 1, "fixed", 15, 0.25, 1.0) + _fields("C", 9, "fixed", 14, 256.0)
+    return dict(dim=3, material="fluid", rounding="dither", seed=DITHER_SEED, fields=f)
+
+
+def with_rounding(scheme, rounding):
+    s = dict(scheme)
+    s["rounding"] = rounding
+    return s
+
+
+BY_NAME = {"x16": x16, "e0.1": e01, "e0.01": e001, "f2": f2}

@@ -1,0 +1,300 @@
+"""Pins for the oracle's codec, bit pack and dither (CPU only).
+
+Each test pins the oracle to something other than itself: a worked example from
+the paper/SPEC, a closed form, an invariant, brute force against an independent
+Python big-integer bit vector, or a statistical property the paper states.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+
+def fixed_scheme(widths_b, ranges, offsets=None, rounding="dither", seed=1234):
+    offsets = offsets or [0.0] * len(widths_b)
+    return dict(dim=0, material="elastic", rounding=rounding, seed=seed,
+                fields=[dict(kind="fixed", frac_bits=b, range=r, offset=o)
+                        for b, r, o in zip(widths_b, ranges, offsets)])
+
+
+def raw_scheme(n):
+    return dict(dim=0, material="elastic", rounding="dither", seed=0,
+                fields=[dict(kind="raw") for _ in range(n)])
+
+
+# --------------------------------------------------------------- Eq. 3 examples
+def test_spec_worked_example_round_and_saturate():
+    """b=2, R=1 (Delta=0.25): v=0.6 -> u=2, decodes to 0.5 (error 0.1);
+    v=1.5 saturates at u=3 = 2^2-1 with one saturation counted; v=0 -> 0."""
+    s = fixed_scheme([2], [1.0], rounding="rne")
+    words, cnt = oracle.encode(s, np.array([[0.6]], np.float32))
+    assert words[0, 0] == 2
+    assert oracle.decode(s, words)[0, 0] == np.float32(0.5)
+    words, cnt = oracle.encode(s, np.array([[1.5]], np.float32))
+    assert words[0, 0] == 3 and cnt[0] == 1
+    words, cnt = oracle.encode(s, np.array([[0.0]], np.float32))
+    assert words[0, 0] == 0 and cnt[0] == 0
+
+
+def test_negative_codes_two_complement():
+    """Reading Q2: b+1-bit two's complement, range [-2^b, 2^b-1]."""
+    s = fixed_scheme([2], [1.0], rounding="rne")
+    words, cnt = oracle.encode(s, np.array([[-1.0], [-5.0], [-0.26]], np.float32))
+    assert list(words[:, 0]) == [0b100, 0b100, 0b111]  # -4, -4 (saturated), -1
+    assert cnt[0] == 1
+    assert list(oracle.decode(s, words)[:, 0]) == [-1.0, -1.0, -0.25]
+
+
+def test_round_half_even_ties():
+    """Reading Q6: undithered ties round half to even."""
+    s = fixed_scheme([4], [16.0], rounding="rne")  # Delta = 1
+    v = np.array([[0.5], [1.5], [2.5], [-0.5], [-1.5]], np.float32)
+    w, _ = oracle.encode(s, v)
+    u = oracle.decode(s, w)[:, 0]
+    assert list(u) == [0.0, 2.0, 2.0, 0.0, -2.0]
+
+
+def test_roundtrip_half_ulp_power_of_two_range():
+    """|decode(encode(v)) - v| <= Delta/2 for 1e5 random v in [-R+D, R-D]
+    (exact bound: Delta is a power of two, so t = v/Delta is exact)."""
+    rng = np.random.default_rng(0)
+    for b, R in [(7, 1.0), (15, 8.0), (19, 1.0), (12, 256.0)]:
+        D = R * 2.0 ** -b
+        v = rng.uniform(-R + D, R - D, size=(100_000, 1)).astype(np.float32)
+        s = fixed_scheme([b], [R], rounding="rne")
+        w, cnt = oracle.encode(s, v)
+        err = np.abs(oracle.decode(s, w).astype(np.float64) - v.astype(np.float64))
+        assert err.max() <= D / 2
+        assert cnt[0] == 0
+
+
+def test_roundtrip_general_range_bound():
+    """Non power-of-two R: error <= Delta/2 + 2^-23 |v| (one fp32 rounding of t)."""
+    rng = np.random.default_rng(1)
+    b, R = 13, 3.7
+    D = float(np.float32(R * 2.0 ** -b))
+    v = rng.uniform(-R + D, R - D, size=(50_000, 1)).astype(np.float32)
+    s = fixed_scheme([b], [R], rounding="rne")
+    w, _ = oracle.encode(s, v)
+    err = np.abs(oracle.decode(s, w).astype(np.float64) - v.astype(np.float64))
+    assert np.all(err[:, 0] <= D / 2 + 2.0 ** -23 * np.abs(v[:, 0]) * 2 + 1e-12)
+
+
+@pytest.mark.parametrize("b", [0, 1, 5, 11, 15])
+def test_exhaustive_idempotence(b):
+    """re-encoding a decoded value is the identity, for every code (b <= 16)."""
+    s = fixed_scheme([b], [2.0], rounding="rne")
+    codes = np.arange(-(2 ** b), 2 ** b, dtype=np.int64)
+    words = (codes & ((1 << (b + 1)) - 1)).astype(np.uint32).reshape(-1, 1)
+    vals = oracle.decode(s, words)
+    assert np.all(vals[:, 0] == codes * np.float32(2.0 * 2.0 ** -b))  # u * Delta exactly
+    w2, cnt = oracle.encode(s, vals)
+    assert np.array_equal(w2, words) and cnt[0] == 0
+    # dithered re-encode of an on-grid value never moves it (y = 0)
+    w3, cnt3 = oracle.encode(s, vals, keys=np.arange(len(vals), dtype=np.uint32), step=7)
+    assert np.array_equal(w3, words) and cnt3[64] == 0 and cnt3[128] == 0
+
+
+def test_offset_field():
+    """Reading Q21: value = offset + u*Delta."""
+    s = fixed_scheme([15], [0.25], offsets=[1.0], rounding="rne")
+    v = np.array([[1.0], [1.1], [0.95]], np.float32)
+    w, _ = oracle.encode(s, v)
+    d = oracle.decode(s, w)[:, 0]
+    assert d[0] == 1.0
+    assert np.all(np.abs(d - v[:, 0]) <= 0.25 * 2 ** -15 / 2 + 1e-7)
+
+
+def test_raw_f32_bitcast():
+    s = raw_scheme(3)
+    v = np.array([[1.5, -0.0, 3.4e38]], np.float32)
+    w, _ = oracle.encode(s, v)
+    assert np.array_equal(w.view(np.float32), v)
+    assert np.array_equal(oracle.decode(s, w).view(np.uint32), v.view(np.uint32))
+
+
+def test_nonfinite_counted():
+    """non-finite input is flagged (code 0 for fixed fields)."""
+    s = fixed_scheme([8, 8], [1.0, 1.0], rounding="rne")
+    w, cnt = oracle.encode(s, np.array([[np.nan, np.inf]], np.float32))
+    assert cnt[192] == 2 and w[0, 0] == 0
+
+
+# --------------------------------------------------------------- bit pack layout
+def test_layout_three_17bit_fields():
+    """Fig. bit_struct: three 17-bit elements fit into two 32-bit words;
+    S:119: offsets 0, 17, 34."""
+    s = fixed_scheme([16, 16, 16], [1.0] * 3)
+    offs, W, bits = oracle.layout(s)
+    assert list(offs) == [0, 17, 34] and W == 2 and bits == 51
+
+
+def test_cross_word_extraction_example():
+    """field at offset 17, width 17, word0 = 0xFFFE0000, word1 = 0x3 -> 0x1FFFF."""
+    rec = np.array([0xFFFE0000, 0x00000003], np.uint32)
+    L = oracle.lib()
+    assert L.oracle_get_bits(rec.ctypes.data, 17, 17) == 0x1FFFF
+
+
+def test_layout_rejects_bad_widths():
+    """width 0 or > 32 rejected."""
+    with pytest.raises(ValueError):
+        oracle.layout(fixed_scheme([32], [1.0]))  # width 33
+    assert oracle.layout(fixed_scheme([31], [1.0]))[1] == 1
+
+
+def _bigint_get(words, off, width):
+    v = int.from_bytes(np.asarray(words, np.uint32).tobytes(), "little")
+    return (v >> off) & ((1 << width) - 1)
+
+
+def _bigint_put(words, off, width, value):
+    v = int.from_bytes(np.asarray(words, np.uint32).tobytes(), "little")
+    mask = ((1 << width) - 1) << off
+    v = (v & ~mask) | ((value << off) & mask)
+    return np.frombuffer(v.to_bytes(4 * len(words), "little"), np.uint32).copy()
+
+
+def test_put_get_exhaustive_widths_offsets():
+    """round trip for every width 1..32 at every offset 0..31, neighbours
+    untouched; checked against an independent Python big-integer bit vector."""
+    rng = np.random.default_rng(2)
+    L = oracle.lib()
+    for width in range(1, 33):
+        for off in range(32):
+            rec = rng.integers(0, 2 ** 32, size=3, dtype=np.uint64).astype(np.uint32)
+            val = int(rng.integers(0, 2 ** width))
+            expect = _bigint_put(rec, off, width, val)
+            got = rec.copy()
+            L.oracle_put_bits(got.ctypes.data, off, width, val)
+            assert np.array_equal(got, expect), (width, off)
+            assert L.oracle_get_bits(got.ctypes.data, off, width) == _bigint_get(got, off, width) == val
+
+
+def test_sign_extension_boundaries():
+    """boundary codes +-2^(w-1) -+ 1 decode exactly (Delta = 1)."""
+    for b in range(1, 24):
+        w = b + 1
+        s = fixed_scheme([b], [float(2 ** b)], rounding="rne")
+        codes = np.array([2 ** (w - 1) - 1, -(2 ** (w - 1)) + 1, -(2 ** (w - 1)), -1, 0])
+        words = (codes & ((1 << w) - 1)).astype(np.uint32).reshape(-1, 1)
+        assert np.array_equal(oracle.decode(s, words)[:, 0], codes.astype(np.float32))
+
+
+def test_packed_record_matches_bigint_reference():
+    """Random multi-field records: every field lands at its layout offset LSB-first."""
+    rng = np.random.default_rng(3)
+    b = [18, 14, 13, 12, 19, 7, 30, 0, 21]
+    R = [1.0, 8.0, 4.0, 256.0, 2.0, 1.0, 16.0, 1.0, 0.5]
+    s = fixed_scheme(b, R, rounding="rne")
+    offs, W, bits = oracle.layout(s)
+    vals = np.stack([rng.uniform(-r, r, 500) for r in R], axis=1).astype(np.float32)
+    words, _ = oracle.encode(s, vals)
+    dec = oracle.decode(s, words)
+    for i in range(500):
+        for f in range(len(b)):
+            raw = _bigint_get(words[i], int(offs[f]), b[f] + 1)
+            u = raw - (1 << (b[f] + 1)) if raw >> b[f] else raw
+            assert dec[i, f] == np.float32(np.float32(u) * np.float32(R[f] * 2.0 ** -b[f]))
+
+
+# --------------------------------------------------------------- dithering (Eq. 11)
+def test_dither_round_up_probability_is_fraction():
+    """P(round up) = Y = v/Delta - floor(v/Delta); binomial 3-sigma at n=1e5."""
+    n = 100_000
+    for Y in [0.1, 0.25, 0.4, 0.5, 0.9]:
+        s = fixed_scheme([10], [1024.0])  # Delta = 1
+        v = np.full((n, 1), 37.0 + Y, np.float32)
+        w, cnt = oracle.encode(s, v, keys=np.arange(n, dtype=np.uint32), step=1)
+        u = oracle.decode(s, w)[:, 0]
+        assert set(np.unique(u)) <= {37.0, 38.0}
+        p = float(np.mean(u == 38.0))
+        yy = float(np.float32(37.0 + Y)) - 37.0
+        assert abs(p - yy) <= 3 * np.sqrt(yy * (1 - yy) / n)
+        assert cnt[64] == np.sum(u == 38.0) and cnt[128] == np.sum(u == 37.0)
+
+
+def test_dither_unbiased_and_within_one_ulp():
+    """bias < 4 Delta / sqrt(12 n) at n = 1e5; |err| < Delta (1 ulp)."""
+    n = 100_000
+    rng = np.random.default_rng(4)
+    b, R = 12, 8.0
+    D = R * 2.0 ** -b
+    for v0 in rng.uniform(-R + D, R - D, 5):
+        v = np.full((n, 1), v0, np.float32)
+        s = fixed_scheme([b], [R])
+        w, _ = oracle.encode(s, v, keys=rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32), step=3)
+        err = oracle.decode(s, w)[:, 0].astype(np.float64) - float(v[0, 0])
+        assert np.abs(err).max() < D
+        assert abs(err.mean()) < 4 * D / np.sqrt(12 * n)
+
+
+def test_drift_pathology():
+    """Fig. dithering_illustration (reading Q7): adding 1.4 Delta ten
+    times gives exactly 10 Delta with round-to-nearest, and 14 Delta +- 0.5 Delta on
+    average over 2000 dithered trials (wide type b = 16)."""
+    b, R = 16, 2.0 ** 16  # Delta = 1
+    s_rne = fixed_scheme([b], [R], rounding="rne")
+    s_dit = fixed_scheme([b], [R], rounding="dither")
+    trials = 2000
+    y_rne = np.zeros((1, 1), np.float32)
+    y_dit = np.zeros((trials, 1), np.float32)
+    keys = np.arange(trials, dtype=np.uint32)
+    for t in range(1, 11):
+        w, _ = oracle.encode(s_rne, y_rne + np.float32(1.4))
+        y_rne = oracle.decode(s_rne, w)
+        w, _ = oracle.encode(s_dit, y_dit + np.float32(1.4), keys=keys, step=t)
+        y_dit = oracle.decode(s_dit, w)
+    assert y_rne[0, 0] == 10.0
+    assert abs(float(y_dit.mean()) - 14.0) < 0.5
+
+
+def test_round_up_down_counts():
+    """T-dither-eff reports round-up/round-down counts.  With dithering
+    the expected ratio is sum(y)/sum(1-y) (P(up) = y), which is ~1 for
+    uniformly distributed fractional parts; round-to-nearest counts follow
+    numpy's round-half-even (np.rint)."""
+    rng = np.random.default_rng(5)
+    n = 200_000
+    s_dit = fixed_scheme([10], [1024.0])
+    s_rne = fixed_scheme([10], [1024.0], rounding="rne")
+    for frac in (rng.uniform(0.0, 1.0, n), rng.uniform(0.0, 0.45, n) ** 0.5):
+        v = (rng.integers(-100, 100, n) + frac).astype(np.float32).reshape(-1, 1)
+        y = v[:, 0].astype(np.float64) - np.floor(v[:, 0].astype(np.float64))
+        _, cd = oracle.encode(s_dit, v, keys=np.arange(n, dtype=np.uint32), step=1)
+        _, cr = oracle.encode(s_rne, v)
+        expect = y.sum() / (1 - y[y > 0]).sum()
+        assert abs(cd[64] / cd[128] / expect - 1.0) < 0.02
+        vv = v[:, 0].astype(np.float64)
+        assert cr[64] == np.sum(np.rint(vv) > vv) and cr[128] == np.sum(np.rint(vv) < vv)
+    # uniform fractional parts: dithered ratio ~ 1 (cf. 0.999976 in T-dither-eff)
+    frac = rng.uniform(0.0, 1.0, n)
+    v = (rng.integers(-100, 100, n) + frac).astype(np.float32).reshape(-1, 1)
+    _, cd = oracle.encode(s_dit, v, keys=np.arange(n, dtype=np.uint32), step=2)
+    assert abs(cd[64] / cd[128] - 1.0) < 0.02
+
+
+# --------------------------------------------------------------- RNG (reading Q5)
+def test_r24_uniform_chi_square_and_field_independence():
+    """The dither RNG is self-defined (parity unpinned beyond statistics): r24 is
+    uniform (chi^2 over 256 bins, 2^18 draws) and fields are uncorrelated."""
+    L = oracle.lib()
+    n = 1 << 18
+    r0 = np.array([L.oracle_r24(7, 5, k, 0) for k in range(n)], dtype=np.float64)
+    r1 = np.array([L.oracle_r24(7, 5, k, 1) for k in range(n)], dtype=np.float64)
+    assert r0.max() < 2 ** 24
+    hist = np.bincount((r0 / 2 ** 16).astype(np.int64), minlength=256)
+    chi2 = float(np.sum((hist - n / 256) ** 2 / (n / 256)))
+    assert chi2 < 255 + 5 * np.sqrt(2 * 255)
+    assert abs(np.corrcoef(r0, r1)[0, 1]) < 0.01
+    # steps decorrelate too
+    r2 = np.array([L.oracle_r24(7, 6, k, 0) for k in range(n)], dtype=np.float64)
+    assert abs(np.corrcoef(r0, r2)[0, 1]) < 0.01
+
+
+def test_mix32_is_a_bijection_on_a_sample():
+    L = oracle.lib()
+    xs = np.arange(0, 1 << 16, dtype=np.uint64) * 65537 + 12345
+    hs = {L.oracle_mix32(int(x) & 0xFFFFFFFF) for x in xs}
+    assert len(hs) == len(xs)
+    assert L.oracle_mix32(0) == 0
