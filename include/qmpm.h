@@ -1,0 +1,202 @@
+/*
+ * qmpm.h -- C ABI of libqmpm: the quantized MLS-MPM hot path of Liu et al.,
+ * "Automatic Quantization for Physics-Based Simulation" (arXiv 2207.04658), on B200.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
+ * readings Qn = DESIGN.md §2.
+ *
+ * Conventions for every entry point:
+ *   - Return value: qmpm_status, QMPM_OK (0) on success.  On failure a message
+ *     is available from qmpm_last_error(ctx) (ctx may be NULL: thread-local).
+ *   - Pointers marked "host or device" may be either; the library inspects them
+ *     with cudaPointerGetAttributes and copies through pinned staging if needed.
+ *     Pointers marked "device" must be device memory on the ctx's device.
+ *   - The caller owns every pointer it passes; the library never frees caller
+ *     memory.  The library allocates only in qmpm_create (records, sort scratch,
+ *     grid pool, counters, optional debug/id buffers), sized from max_particles.
+ *   - A ctx is single-owner and single-stream: all work is enqueued on the stream
+ *     given to qmpm_create; calls marked "synchronizes" block until it drains.
+ *   - Device-side conditions (non-finite values, out-of-domain particles, grid
+ *     pool overflow) are COUNTED on the device; pool overflow additionally sets a
+ *     sticky error that the next synchronizing call returns as QMPM_ECAPACITY.
+ *     Saturation of a fixed-point field is only counted.
+ */
+#ifndef QMPM_H
+#define QMPM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QMPM_ABI_VERSION 1
+#define QMPM_MAX_FIELDS 64
+
+typedef struct qmpm_ctx qmpm_ctx; /* opaque; owns all device pools */
+typedef int32_t qmpm_status;
+
+enum {
+    QMPM_OK = 0,
+    QMPM_EINVAL = 1,     /* bad argument (null pointer, size, dim, material...) */
+    QMPM_ELAYOUT = 2,    /* scheme cannot be laid out (width 0 or > 32; missing scalar) */
+    QMPM_ENOMEM = 3,     /* device allocation failed */
+    QMPM_ECUDA = 4,      /* CUDA runtime error */
+    QMPM_ENCCL = 5,      /* reserved: multi-GPU exchange */
+    QMPM_ENONFINITE = 6, /* reserved: non-finite values are counted in qmpm_stats */
+    QMPM_EDOMAIN = 7,    /* reserved: out-of-domain particles are counted in qmpm_stats */
+    QMPM_ECAPACITY = 8,  /* n > max_particles, or grid pool overflow during a step */
+    QMPM_ESTATE = 9      /* call not valid in the ctx's current state */
+};
+
+/* Field kinds.  FIXED: Eq. 3, u = round(v/Delta) stored as frac_bits+1-bit
+ * two's complement (reading Q2), Delta = range * 2^-frac_bits, value =
+ * offset + u*Delta (offset: reading Q21).  RAW_F32: the IEEE bits (32 bits).
+ * SHARED_EXP is reserved (reading Q4) and rejected with QMPM_ELAYOUT. */
+enum { QMPM_FIXED = 0, QMPM_RAW_F32 = 1, QMPM_SHARED_EXP = 2 };
+/* Attributes of a particle: position, velocity, deformation
+ * gradient (elastic), its determinant J (fluid), affine velocity C. */
+enum { QMPM_X = 0, QMPM_V = 1, QMPM_F = 2, QMPM_C = 3, QMPM_J = 4 };
+/* Rounding at every store of steps >= 1: Eq. 11 dithering or
+ * round-half-even (the undithered ablation, T-dither-perf P:767-786). */
+enum { QMPM_RNE = 0, QMPM_DITHER = 1 };
+/* Materials: fixed-corotated elastic, J-tracking fluid (reading Q15). */
+enum { QMPM_ELASTIC_FCR = 0, QMPM_FLUID_J = 1 };
+/* qmpm_params.flags */
+enum {
+    QMPM_TRACK_IDS = 1u << 0,       /* keep a u32 particle id alongside each record */
+    QMPM_DEBUG_PREENCODE = 1u << 1, /* keep the last step's fp32 state before encode */
+    QMPM_NO_ROUND_COUNTERS = 1u << 2 /* skip the per-field round-up/down counters */
+};
+
+/* One quantized quantity h: one scalar component of one attribute.
+ * Fields are bit-packed contiguously in array order, LSB-first, each particle
+ * record starting at a fresh 32-bit word (bit pack; reading Q10). */
+typedef struct {
+    uint8_t attr;      /* QMPM_X .. QMPM_J */
+    uint8_t comp;      /* component: 0..d-1 for x, v; row-major 0..d*d-1 for F, C; 0 for J */
+    uint8_t kind;      /* QMPM_FIXED | QMPM_RAW_F32 */
+    uint8_t frac_bits; /* b; FIXED width = b+1 in [1, 32] */
+    float range;       /* R > 0 (FIXED) */
+    float offset;      /* value = offset + u*Delta (FIXED) */
+    uint8_t exp_bits, group, pad[2]; /* reserved for SHARED_EXP */
+} qmpm_field;
+
+/* A quantization scheme {(b_h, R_h)} (Alg. 1 output) plus packing order. */
+typedef struct {
+    uint32_t dim;      /* 2 or 3 */
+    uint32_t material; /* QMPM_ELASTIC_FCR | QMPM_FLUID_J */
+    uint32_t n_fields; /* must cover every state scalar exactly once (see below) */
+    uint32_t rounding; /* QMPM_DITHER | QMPM_RNE */
+    const qmpm_field* fields; /* host pointer, n_fields entries, packing order */
+    uint64_t dither_seed;     /* seed of the content-keyed dither hash (reading Q5) */
+    uint32_t layout_policy;   /* 0 = bit pack (fields may straddle words) */
+    uint32_t pad;
+} qmpm_scheme;
+
+/* Scene parameters of the MLS-MPM step. */
+typedef struct {
+    int32_t grid_res[3]; /* nodes per axis (grid_res[2] ignored in 2D) */
+    float dx, dt;        /* cell size, time step */
+    float gravity[3];
+    float p_rho, p_vol;  /* particle density and volume; m_p = p_rho * p_vol */
+    float E, nu;         /* Young's modulus (fluid: bulk stiffness), Poisson ratio */
+    int32_t bound;       /* separating-wall thickness in nodes (reading Q13) */
+    uint32_t flags;      /* QMPM_TRACK_IDS | QMPM_DEBUG_PREENCODE | QMPM_NO_ROUND_COUNTERS */
+    uint64_t max_particles;
+    uint64_t pool_blocks; /* grid-pool capacity in blocks (4^3 nodes 3D, 8^2 2D); 0 = auto */
+} qmpm_params;
+
+typedef struct {
+    uint64_t step;          /* steps taken since set_state (set_words sets it) */
+    uint64_t n_particles;
+    uint64_t saturations[QMPM_MAX_FIELDS]; /* per field, cumulative */
+    uint64_t round_up[QMPM_MAX_FIELDS];    /* per field: u > v/Delta (T-dither-eff) */
+    uint64_t round_down[QMPM_MAX_FIELDS];  /* per field: u < v/Delta */
+    uint64_t nonfinite;     /* non-finite values met by the encoder */
+    uint64_t out_of_domain; /* particle-steps whose base was clamped (reading Q14) */
+    uint64_t active_blocks; /* grid blocks holding particles, last step */
+    uint64_t touched_blocks;/* grid blocks in the pool (active + their upper neighbours), last step */
+    uint64_t pool_overflow; /* steps whose touched blocks exceeded pool_blocks */
+} qmpm_stats_t;
+
+/*
+ * State scalar order used by qmpm_set_state / qmpm_read_state / qmpm_read_debug
+ * ("vals" as [n][n_scalars] fp32, row-major): x[d], v[d], then F[d*d] row-major
+ * (elastic) or J (fluid), then C[d*d] row-major.  n_scalars = 2d + 2d^2 (elastic)
+ * or 2d + 1 + d^2 (fluid): 3D elastic 24, 3D fluid 16, 2D elastic 12, 2D fluid 9.
+ * This order is independent of the packing order.
+ */
+
+/* Layout of a scheme (bit pack): words per particle record, bits used,
+ * and each field's bit offset (nullable; n_fields entries).  Pure host function.
+ * QMPM_ELAYOUT if a width is 0 or > 32 or a kind is unsupported. */
+qmpm_status qmpm_layout(const qmpm_scheme* scheme, uint32_t* words_per_particle,
+                        uint32_t* bits_used, uint32_t* bit_offsets);
+
+/* Create a single-GPU context on the current CUDA device; all work goes to
+ * cuda_stream (a cudaStream_t; NULL = legacy default stream).  Validates the
+ * scheme (every state scalar stored exactly once), uploads its constants and
+ * allocates every pool.  *out receives the ctx. */
+qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, void* cuda_stream,
+                        qmpm_ctx** out);
+qmpm_status qmpm_destroy(qmpm_ctx* ctx); /* synchronizes; NULL is a no-op */
+
+/* Replace the state with n particles given as fp32 scalars (host or device,
+ * [n][n_scalars]); encoded with round-half-even at step 0 (reading Q20); the
+ * step counter and all stats are reset; ids become 0..n-1. */
+qmpm_status qmpm_set_state(qmpm_ctx* ctx, uint64_t n, const float* vals);
+/* Append n particles (same encoding) after the current ones, for chunked
+ * creation of large scenes; ids continue.  QMPM_ECAPACITY past max_particles. */
+qmpm_status qmpm_append_state(qmpm_ctx* ctx, uint64_t n, const float* vals);
+/* Replace the state with n packed records (host or device, [n][W] u32) and set
+ * the step counter (resume; dithering is keyed by content and step, so a resumed
+ * run is bit-identical, reading Q5). */
+qmpm_status qmpm_set_words(qmpm_ctx* ctx, uint64_t n, const uint32_t* words, uint64_t step);
+
+/* Advance n_steps MLS-MPM steps (decode -> bin -> P2G -> grid update -> G2P ->
+ * dithered encode), asynchronously on the ctx stream; allocates nothing. */
+qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps);
+
+/* Read the current particles (synchronizes).  vals: [n][n_scalars] decoded fp32
+ * (nullable); words: [n][W] packed records (nullable); ids: [n] (nullable; needs
+ * QMPM_TRACK_IDS).  All host or device.  Particles are in the library's storage
+ * order (sorted by grid block after a step); use ids to match them.  *n_out = n;
+ * QMPM_ECAPACITY if capacity < n. */
+qmpm_status qmpm_read_state(qmpm_ctx* ctx, float* vals, uint32_t* words, uint32_t* ids,
+                            uint64_t capacity, uint64_t* n_out);
+/* The last step's fp32 state BEFORE the encode (needs QMPM_DEBUG_PREENCODE), in
+ * the same order as qmpm_read_state.  Synchronizes. */
+qmpm_status qmpm_read_debug(qmpm_ctx* ctx, float* pre_encode_vals, uint64_t capacity,
+                            uint64_t* n_out);
+qmpm_status qmpm_stats(qmpm_ctx* ctx, qmpm_stats_t* out); /* synchronizes */
+
+/* Standalone codec (Eq. 3 / Eq. 11 + bit pack) on device arrays, enqueued on
+ * cuda_stream.  vals: [n][n_fields] fp32 in PACKING order; words: [n][W].
+ * keys: nullable => round-half-even; else dithered with r24(seed, step, keys[i],
+ * field) when scheme->rounding == QMPM_DITHER.  The scheme's dim/material are not
+ * used and attr/comp are not checked.  counters (nullable, device, 3*64 u64,
+ * accumulated): saturations, round-ups, round-downs per field. */
+qmpm_status qmpm_encode(const qmpm_scheme* scheme, uint64_t n, const float* vals,
+                        const uint32_t* keys, uint64_t step, uint32_t* words,
+                        uint64_t* counters, void* cuda_stream);
+qmpm_status qmpm_decode(const qmpm_scheme* scheme, uint64_t n, const uint32_t* words, float* vals,
+                        void* cuda_stream);
+
+/* Per-kernel timing for the roofline: when enabled, qmpm_step brackets each
+ * kernel with CUDA events on the ctx stream.  qmpm_kernel_times (synchronizes)
+ * returns, for each of the QMPM_NUM_KERNELS kernels in the order of
+ * qmpm_kernel_name(i), the summed milliseconds and launch count since enabling. */
+#define QMPM_NUM_KERNELS 8
+qmpm_status qmpm_set_profiling(qmpm_ctx* ctx, int enabled);
+qmpm_status qmpm_kernel_times(qmpm_ctx* ctx, double* ms, uint64_t* launches);
+const char* qmpm_kernel_name(int i);
+/* Total kernels this ctx launched (all entry points), for the bench's claim. */
+uint64_t qmpm_launch_count(const qmpm_ctx* ctx);
+
+const char* qmpm_last_error(const qmpm_ctx* ctx);
+int qmpm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QMPM_H */

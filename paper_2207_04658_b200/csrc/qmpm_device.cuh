@@ -1,0 +1,249 @@
+// qmpm_device.cuh -- device-side building blocks of the quantized MLS-MPM step:
+// bit-pack field access, fixed-point decode/encode with non-subtractive dithering,
+// the content-keyed dither hash, B-spline weights and the polar decomposition.
+//
+// Paper passages (P:n = /root/reference/PAPER.md line n; readings Qn = DESIGN.md §2):
+//   decode    Eq. 3: value = u * Delta (+ offset, Q21), u sign-extended
+//             from b+1 bits (Q2); a field may straddle two words (bit pack).
+//   encode    Eq. 3 / Eq. 11: t = fl32(fl32(v - offset) * inv_Delta), no FMA
+//             (Q3); RNE (Q6) or u = floor(t) + [y >= 1 - r] (Q6), saturated.
+//   r24       reading Q5 (the paper's generator, is in an unavailable supplement).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace qmpm {
+
+constexpr int kMaxScalars = 24;   // 3D elastic: x3 v3 F9 C9
+constexpr int kMaxFields = 64;
+constexpr int kKindFixed = 0;
+constexpr int kKindRaw = 1;
+
+// One field as the kernels see it.  `idx` is the packing index (RNG stream and
+// counters); `col` is the column of the field's value in a vals row.
+struct FieldDev {
+  uint8_t word, shift, width, kind;
+  float delta, inv_delta, offset;
+  uint16_t idx, col;
+};
+
+// Layout for the MPM kernels: fields indexed by STATE SCALAR (x.., v.., F../J, C..).
+struct LayoutDev {
+  uint32_t W;           // words per record
+  uint32_t SW;          // shared-memory row stride (odd, >= W + 1)
+  uint32_t ns;          // number of state scalars
+  uint32_t xword_mask;  // record words holding any x bit (particle key, Q5)
+  uint32_t dither;      // 1 = Eq. 11 dithering, 0 = RNE
+  uint32_t counters;    // 1 = count round-ups/downs
+  uint32_t seed_lo, seed_hi;
+  FieldDev s[kMaxScalars];
+};
+
+// Layout for the standalone codec: fields in PACKING order.
+struct CodecDev {
+  uint32_t W, SW, nf, stride;  // stride = floats per vals row
+  uint32_t dither;
+  uint32_t seed_lo, seed_hi;
+  uint32_t pad;
+  FieldDev f[kMaxFields];
+};
+
+// Scene constants (DESIGN.md §2 Q12-Q15).
+struct SimDev {
+  int res[3];
+  int nb[3];          // grid blocks per axis
+  float dx, inv_dx, dt;
+  float g[3];
+  float p_mass;
+  float stress_scale; // -dt * p_vol * 4 * inv_dx^2
+  float mu, lambda;   // fixed corotated (elastic)
+  float E;            // fluid: P F^T = E (J - 1) I
+  int bound;
+  uint32_t nblocks;
+};
+
+// Device-side counters (accumulated across steps until set_state).
+struct DevCounters {
+  unsigned long long sat[kMaxFields];
+  unsigned long long up[kMaxFields];
+  unsigned long long down[kMaxFields];
+  unsigned long long nonfinite;
+  unsigned long long oob;
+  unsigned long long overflow;
+  unsigned int n_active;      // last step
+  unsigned int n_touched;     // last step (before clamping to the pool)
+  unsigned int n_touched_eff; // min(n_touched, pool)
+  unsigned int pad;
+};
+
+// ---------------------------------------------------------------- hashing (Q5)
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__host__ __device__ __forceinline__ uint32_t mix32_hd(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+// salt = mix(seed_lo ^ mix(seed_hi ^ mix(step)))  (step mod 2^32)
+__host__ __device__ __forceinline__ uint32_t step_salt(uint32_t seed_lo, uint32_t seed_hi,
+                                                       uint32_t step) {
+  return mix32_hd(seed_lo ^ mix32_hd(seed_hi ^ mix32_hd(step)));
+}
+
+// r24 for (particle hash h = mix(key ^ salt), field index f)
+__device__ __forceinline__ uint32_t r24_of(uint32_t h, uint32_t f) {
+  return mix32(h + f * 0x9E3779B9u) >> 8;
+}
+
+// ---------------------------------------------------------------- decode (Eq. 3)
+// `row` points at a record whose word W (one past the end) is readable.
+__device__ __forceinline__ float decode_field(const uint32_t* row, const FieldDev& f) {
+  const uint32_t lo = row[f.word];
+  const uint32_t hi = row[f.word + 1];
+  const uint32_t raw = __funnelshift_r(lo, hi, f.shift);
+  if (f.kind == kKindRaw) return __uint_as_float(raw);
+  const uint32_t sh = 32u - f.width;
+  const int u = ((int)(raw << sh)) >> sh;  // sign-extend b+1 bits (Q2)
+  float x = __fmul_rn(__int2float_rn(u), f.delta);
+  if (f.offset != 0.0f) x = __fadd_rn(x, f.offset);
+  return x;
+}
+
+// ---------------------------------------------------------------- encode (Eq. 3 / 11)
+struct EncStat {
+  int up, down, sat, nonfinite;
+};
+
+// Returns the field's raw bits (masked to its width).
+__device__ __forceinline__ uint32_t encode_field(float v, const FieldDev& f, bool dither,
+                                                 uint32_t r24, EncStat& st) {
+  st.up = st.down = st.sat = st.nonfinite = 0;
+  if (f.kind == kKindRaw) {
+    st.nonfinite = !isfinite(v);
+    return __float_as_uint(v);
+  }
+  if (!isfinite(v)) {
+    st.nonfinite = 1;
+    return 0u;
+  }
+  const float a = (f.offset != 0.0f) ? __fsub_rn(v, f.offset) : v;
+  const float t = __fmul_rn(a, f.inv_delta);  // no FMA (Q3)
+  float q;
+  if (dither) {
+    const float fl = floorf(t);
+    const float y = __fsub_rn(t, fl);  // exact
+    const float one_minus_r = __fmul_rn(__uint2float_rn(0x1000000u - r24), 0x1p-24f);  // exact
+    const bool up = y >= one_minus_r;
+    st.up = up;
+    st.down = (!up) && (y > 0.0f);
+    q = fl;
+    // q + up below, in integers (exact for any magnitude)
+    const float qc = fminf(fmaxf(q, -1099511627776.0f), 1099511627776.0f);  // +-2^40
+    long long u = __float2ll_rz(qc) + (up ? 1 : 0);
+    const long long hi = (1ll << (f.width - 1)) - 1, lo = -(1ll << (f.width - 1));
+    if (u > hi) { u = hi; st.sat = 1; }
+    if (u < lo) { u = lo; st.sat = 1; }
+    const uint32_t mask = (f.width == 32) ? 0xffffffffu : ((1u << f.width) - 1u);
+    return (uint32_t)u & mask;
+  }
+  q = rintf(t);  // round half to even (Q6)
+  st.up = q > t;
+  st.down = q < t;
+  const float qc = fminf(fmaxf(q, -1099511627776.0f), 1099511627776.0f);
+  long long u = __float2ll_rz(qc);
+  const long long hi = (1ll << (f.width - 1)) - 1, lo = -(1ll << (f.width - 1));
+  if (u > hi) { u = hi; st.sat = 1; }
+  if (u < lo) { u = lo; st.sat = 1; }
+  const uint32_t mask = (f.width == 32) ? 0xffffffffu : ((1u << f.width) - 1u);
+  return (uint32_t)u & mask;
+}
+
+// OR a field's bits into a record row (row owned by the calling thread; row has a
+// spare word at W so word + 1 is always writable).
+__device__ __forceinline__ void put_field(uint32_t* row, const FieldDev& f, uint32_t bits) {
+  const unsigned long long wide = (unsigned long long)bits << f.shift;
+  row[f.word] |= (uint32_t)wide;
+  const uint32_t hi = (uint32_t)(wide >> 32);
+  if (hi) row[f.word + 1] |= hi;
+}
+
+// ---------------------------------------------------------------- MLS-MPM helpers
+// base / fx of one axis with the out-of-domain clamp of Q14.  Identical arithmetic
+// wherever a base is computed (bin key, P2G, G2P, next-step key).
+__device__ __forceinline__ int base_fx(float x, float inv_dx, int n_axis, float& fx, bool& oob) {
+  const float X = __fmul_rn(x, inv_dx);
+  int b = (int)floorf(__fsub_rn(X, 0.5f));
+  oob = false;
+  if (b < 0) { b = 0; oob = true; }
+  if (b > n_axis - 3) { b = n_axis - 3; oob = true; }
+  float f = __fsub_rn(X, (float)b);
+  if (oob) f = fminf(fmaxf(f, 0.5f), 1.5f);
+  fx = f;
+  return b;
+}
+
+__device__ __forceinline__ void bspline_w(float fx, float w[3]) {
+  const float a = 1.5f - fx, b = fx - 1.0f, c = fx - 0.5f;
+  w[0] = 0.5f * a * a;
+  w[1] = 0.75f - b * b;
+  w[2] = 0.5f * c * c;
+}
+
+// 3x3 polar decomposition F = R S, det R = +1 for det F > 0, by Newton's iteration
+// R <- (g R + R^{-T}/g)/2 with Higham's determinant scaling g = |det R|^{-1/3}.
+__device__ __forceinline__ void polar3(const float F[9], float R[9]) {
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = F[i];
+  for (int it = 0; it < 12; ++it) {
+    // cofactor matrix (= det * R^{-T})
+    float c[9];
+    c[0] = R[4] * R[8] - R[5] * R[7];
+    c[1] = R[5] * R[6] - R[3] * R[8];
+    c[2] = R[3] * R[7] - R[4] * R[6];
+    c[3] = R[2] * R[7] - R[1] * R[8];
+    c[4] = R[0] * R[8] - R[2] * R[6];
+    c[5] = R[1] * R[6] - R[0] * R[7];
+    c[6] = R[1] * R[5] - R[2] * R[4];
+    c[7] = R[2] * R[3] - R[0] * R[5];
+    c[8] = R[0] * R[4] - R[1] * R[3];
+    const float det = R[0] * c[0] + R[1] * c[1] + R[2] * c[2];
+    const float ad = fabsf(det);
+    if (!(ad > 1e-30f)) break;
+    const float g = (it < 6) ? rcbrtf(ad) : 1.0f;
+    const float a = 0.5f * g, b = 0.5f / (g * det);
+    float delta = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      const float nr = a * R[i] + b * c[i];
+      delta = fmaxf(delta, fabsf(nr - R[i]));
+      R[i] = nr;
+    }
+    if (delta < 1e-7f) break;
+  }
+}
+
+// 2D polar: closed form (rotation by atan2(F10 - F01, F00 + F11)).
+__device__ __forceinline__ void polar2(const float F[4], float R[4]) {
+  const float x = F[0] + F[3], y = F[2] - F[1];
+  const float r2 = x * x + y * y;
+  float c = 1.0f, s = 0.0f;
+  if (r2 > 0.0f) {
+    const float ir = rsqrtf(r2);
+    c = x * ir;
+    s = y * ir;
+  }
+  R[0] = c; R[1] = -s; R[2] = s; R[3] = c;
+}
+
+}  // namespace qmpm

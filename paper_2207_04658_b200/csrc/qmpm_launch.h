@@ -1,0 +1,76 @@
+// qmpm_launch.h -- host-side launchers of the qmpm kernels (kernels.cu), used by
+// the runtime (api.cu).  Internal; not part of the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "qmpm_device.cuh"
+
+namespace qmpm {
+
+struct StepBuffers {
+  const uint32_t* rec_in;
+  uint32_t* rec_out;
+  const uint32_t* ids_in;  // nullable
+  uint32_t* ids_out;       // nullable
+  uint32_t* key;           // [n] block key of each record in rec_in order (in), rec_out order (out)
+  uint32_t* perm;          // [n] sorted slot -> rec_in index
+  uint32_t* block_count;   // [nblocks]
+  uint32_t* block_start;   // [nblocks + 1]
+  uint32_t* block_slot;    // [nblocks]
+  uint32_t* active_list;   // [nblocks]
+  uint32_t* touched_list;  // [pool]
+  uint4* tile_sums;        // [ntiles]
+  uint4* tile_off;         // [ntiles]
+  float4* mp;              // [pool * 64]  (m, p) -- zero between steps
+  float4* gv;              // [pool * 64]  (v, 0)
+  DevCounters* dc;
+  float* dbg;              // nullable [n][ns]
+  uint32_t n;
+  uint32_t pool;
+  uint32_t ntiles;
+};
+
+constexpr int kScanTile = 1024;  // grid blocks per scan tile
+
+// kernel ids for profiling (order = qmpm_kernel_name)
+enum KernelId {
+  KBinCount = 0,
+  KScanReduce,
+  KScanTiles,
+  KScanApply,
+  KBinScatter,
+  KP2G,
+  KGridUpdate,
+  KG2P,
+  KNumKernels
+};
+
+struct LaunchCfg {
+  int num_sms;
+  int p2g_ctas;
+  int g2p_ctas;
+  size_t p2g_smem;
+  size_t g2p_smem;
+};
+
+cudaError_t setup_kernels(int dim, int material, const LayoutDev& L, LaunchCfg& cfg);
+
+// one hook per kernel so the runtime can bracket launches with events
+typedef void (*KernelHook)(void* user, int kernel_id, int begin);
+
+cudaError_t launch_bin_count(int dim, const uint32_t* rec, uint32_t n, const LayoutDev& L,
+                             const SimDev& S, uint32_t* key, uint32_t* block_count,
+                             cudaStream_t st);
+cudaError_t launch_step(int dim, int material, const StepBuffers& B, const LayoutDev& L,
+                        const SimDev& S, uint32_t salt, const LaunchCfg& cfg, cudaStream_t st,
+                        KernelHook hook, void* user);
+
+cudaError_t launch_encode(const CodecDev& C, uint64_t n, const float* vals, const uint32_t* keys,
+                          uint32_t salt, uint32_t* words, unsigned long long* counters,
+                          cudaStream_t st);
+cudaError_t launch_decode(const CodecDev& C, uint64_t n, const uint32_t* words, float* vals,
+                          cudaStream_t st);
+cudaError_t launch_iota(uint32_t* ids, uint32_t n, uint32_t first, cudaStream_t st);
+
+}  // namespace qmpm

@@ -1,0 +1,75 @@
+"""CPU checks of the C-ABI library: it loads, exports every symbol include/qmpm.h
+declares, and its host-side layout function follows the bit-pack layout."""
+import re
+import subprocess
+import os
+
+import numpy as np
+import pytest
+
+from paper_2207_04658_b200 import qmpm, schemes
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "qmpm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(qmpm_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    path = qmpm.LIB_PATH
+    assert os.path.exists(path), "libqmpm.so not built"
+    out = subprocess.check_output(["nm", "-D", "--defined-only", path], text=True)
+    exported = set(l.split()[-1] for l in out.splitlines() if l.strip())
+    decl = declared_symbols()
+    assert len(decl) >= 15
+    missing = [s for s in decl if s not in exported]
+    assert not missing, missing
+    L = qmpm.lib()
+    for s in decl:
+        assert hasattr(L, s)
+    assert L.qmpm_abi_version() == 1
+
+
+def test_binding_names_match_header():
+    assert sorted(qmpm.EXPORTS) == declared_symbols()
+
+
+@pytest.mark.parametrize("name", ["x16", "e0.1", "e0.01", "f2"])
+def test_layout_of_stand_in_schemes(name):
+    sch = schemes.BY_NAME[name]()
+    offs, W, bits = qmpm.layout(sch)
+    widths = [32 if f["kind"] == "raw" else f["frac_bits"] + 1 for f in sch["fields"]]
+    assert offs == list(np.cumsum([0] + widths[:-1]))
+    assert bits == sum(widths) and W == (bits + 31) // 32
+    assert {"x16": 10, "e0.1": 11, "e0.01": 11, "f2": 8}[name] == W
+
+
+def test_layout_fig_bit_struct_and_errors():
+    s = dict(dim=3, material="elastic", rounding="dither", seed=0,
+             fields=[dict(kind="fixed", frac_bits=16, range=1.0) for _ in range(3)])
+    offs, W, bits = qmpm.layout(s)
+    assert offs == [0, 17, 34] and W == 2  # three 17-bit values in two words
+    bad = dict(s, fields=[dict(kind="fixed", frac_bits=32, range=1.0)])
+    with pytest.raises(qmpm.QmpmError) as e:
+        qmpm.layout(bad)
+    assert e.value.code == 2
+    bad = dict(s, fields=[dict(kind="shared_exp", frac_bits=8, range=1.0)])
+    with pytest.raises(qmpm.QmpmError):
+        qmpm.layout(bad)
+
+
+def test_create_without_gpu_fails_loudly_or_validates():
+    """Argument validation happens before any device work."""
+    from paper_2207_04658_b200 import scenes
+    sc = scenes.c1()
+    bad = dict(schemes.x16())
+    bad["fields"] = bad["fields"][:-1]  # a state scalar missing
+    cs = qmpm.CScheme(bad)
+    p = qmpm.make_params(sc.sim, 100)
+    import ctypes
+    h = ctypes.c_void_p()
+    rc = qmpm.lib().qmpm_create(ctypes.byref(p), cs.ref, None, ctypes.byref(h))
+    assert rc == 2
