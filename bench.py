@@ -1,0 +1,359 @@
+"""bench.py -- quantized MLS-MPM particle-steps/s and % HBM roofline on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--scheme e0.01]
+    python bench.py --impl reference ...   (the CPU oracle as it stands, host cores)
+
+Workload at N=1 (BASELINE.json configs[2], the paper's T-large elastic run):
+C3 = 295,280,208 particles of 3D elastic cubes on a 1024^3 block-sparse grid,
+dt 7.5e-5, stand-in scheme E0.01 (351 bits/particle, W = 11 words).  Inputs are
+generated on the device (seeded), encoded by qmpm_set_state, then advanced
+`scene_warmup` untimed steps so F != I and C != 0, then W warm-up steps, then K
+timed steps.  The state (13 GB) is far larger than L2 (126 MB), so no flush is
+needed between steps.
+
+One JSON line on rank 0 (see the contract in the task statement); the roofline
+object is for the dominant kernel, with algorithmic bytes per launch defined in
+DESIGN.md §6, duration from CUDA events on the ctx stream over the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_C3_PSTEPS = 295_280_208 * 128 / 63.5  # derived from T-large, RTX 3090: context
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="qmpm", choices=["qmpm", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--scheme", default=None, help="x16 | e0.1 | e0.01 | f2 | fp32")
+    ap.add_argument("--n", type=int, default=0, help="override particle count (reduced runs)")
+    ap.add_argument("--scene-warmup", type=int, default=50)
+    ap.add_argument("--rounding", default="dither", choices=["dither", "rne"])
+    ap.add_argument("--no-counters", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000)
+    ap.add_argument("--cpu-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def make_scene(args):
+    from paper_2207_04658_b200 import scenes, schemes
+    if args.config == "c1":
+        sc = scenes.c1()
+        sch = schemes.x16()
+    elif args.config == "c2":
+        sc = scenes.c2()
+        sch = schemes.e01()
+    elif args.config == "c3":
+        sc = scenes.c3(n_target=args.n or scenes.C3_PARTICLES)
+        sch = schemes.e001()
+    else:
+        sc = scenes.c4(n_target=args.n or 400_000_000)
+        sch = schemes.f2()
+    if args.scheme:
+        sch = schemes.fp32(sc.dim, sc.material) if args.scheme == "fp32" else schemes.BY_NAME[args.scheme]()
+    sch = schemes.with_rounding(sch, args.rounding)
+    return sc, sch
+
+
+def scheme_name(args):
+    return args.scheme or {"c1": "x16", "c2": "e0.1", "c3": "e0.01", "c4": "f2"}[args.config]
+
+
+def workload_name(args, sc, W, bits):
+    return (f"{sc.name}: {sc.dim}D {sc.material}, {sc.n_particles:,} particles, "
+            f"{'x'.join(str(r) for r in sc.sim['grid_res'][:sc.dim])} block-sparse grid, "
+            f"dt {sc.sim['dt']:g}, scheme {scheme_name(args)} ({bits} bits, W={W})")
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.splitlines():
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU oracle
+def cpu_oracle_rate(sc, sch, n_sample, steps):
+    """The oracle as it stands (single-threaded plain C, fp64), on the first n_sample
+    particles of the same workload; returns particle-steps/s."""
+    import oracle
+    n = min(n_sample, sc.n_particles)
+    st = sc.state_chunk(0, n)
+    w, _ = oracle.encode_state(sch, st)
+    t0 = time.perf_counter()
+    oracle.run(sc.sim, sch, w, 1, steps)
+    dt = time.perf_counter() - t0
+    return n * steps / dt, n, steps, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sc, sch = make_scene(args)
+    import oracle
+    _, W, bits = oracle.layout(sch)
+    n = min(args.cpu_sample, sc.n_particles)
+    st = sc.state_chunk(0, n)
+    w, _ = oracle.encode_state(sch, st)
+    for t in range(args.warmup):
+        w = oracle.step(sc.sim, sch, w, t + 1)[1]
+    times = []
+    for t in range(args.steps):
+        t0 = time.perf_counter()
+        w = oracle.step(sc.sim, sch, w, args.warmup + t + 1)[1]
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = n * args.steps / total
+    line = {
+        "impl": "reference", "metric": "quantized MPM particle-steps/sec", "value": value,
+        "unit": "particle-steps/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args, sc, W, bits), "sample_particles": n},
+        "cpu_baseline": {"value": value, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
+                         "sample": f"first {n:,} particles of the workload, {args.steps} steps (fp64 plain C, 1 thread)"},
+        "e2e": {"value": value, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU
+def algorithmic_bytes(S, nodes):
+    """Per launch: P2G reads each record once and reduces 16 B per
+    touched node; G2P reads + writes each record and reads 12 B per touched node."""
+    return {"p2g": lambda n: n * S + 16 * nodes, "g2p": lambda n: 2 * n * S + 12 * nodes,
+            "grid_update": lambda n: 28 * nodes}
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2207_04658_b200 import qmpm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sc, sch = make_scene(args)
+    _, W, bits = qmpm.layout(sch)
+    N = sc.n_particles
+    flags = qmpm.NO_ROUND_COUNTERS if args.no_counters else 0
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        sim = qmpm.Sim(sc.sim, sch, N, flags=flags, stream=stream)
+        chunk = 1 << 24
+        for s0 in range(0, N, chunk):
+            cnt = min(chunk, N - s0)
+            st = sc.state_chunk(s0, cnt, backend="torch", device="cuda")
+            if s0 == 0:
+                sim.set_state(st)
+            else:
+                sim.append_state(st)
+            stream.synchronize()
+            del st
+        torch.cuda.empty_cache()
+        sim.step(args.scene_warmup + args.warmup)
+        stream.synchronize()
+
+        # ---------------- timed region (device): K steps, per-kernel events on the ctx stream
+        sim.set_profiling(True)
+        launches0 = sim.launch_count()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local)
+        clocks.start()
+        time.sleep(0.3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sim.step(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        launches = sim.launch_count() - launches0
+        ms = e0.elapsed_time(e1)
+        ktimes = sim.kernel_times()
+        st = sim.stats()
+        sim.set_profiling(False)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        value = world * N * args.steps / (ms / 1e3)
+
+        # ---------------- end to end through the C ABI with pinned host buffers
+        e2e = None
+        if not args.no_e2e:
+            host = torch.empty((N, W), dtype=torch.int32, pin_memory=True)
+            sim.read_state(words=host)  # the current state, as a user would hold it on the host
+            step0 = st.step
+            k = args.steps
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            sim.set_words(host, step0)           # H2D of the inputs (pinned)
+            for _ in range(k):
+                sim.step(1)
+                sim.stats()                      # D2H of the step's metric (counters)
+            sim.read_state(words=host)           # D2H of the result
+            t1 = time.perf_counter()
+            e2e_s = t1 - t0
+            if world > 1:
+                t = torch.tensor([e2e_s], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                e2e_s = float(t.item())
+            stats_bytes = 8 * (2 + 3 * 64 + 5)
+            e2e = {"value": world * N * k / e2e_s, "unit": "particle-steps/s",
+                   "h2d_bytes_per_step": int(N * W * 4 / k),
+                   "d2h_bytes_per_step": int(N * W * 4 / k + stats_bytes),
+                   "note": f"timed: set_words(pinned host, {N*W*4/1e9:.2f} GB) + {k} x (qmpm_step + qmpm_stats D2H) "
+                           "+ read_state(words -> pinned host)"}
+            del host
+        sim.close()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel
+    import json as _json
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peaks = _json.load(open(peaks_path))
+        hbm_peak, peak_src = float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        hbm_peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    S = W * 4
+    nodes = 64 * int(st.touched_blocks)
+    ab = algorithmic_bytes(S, nodes)
+    dom = max(("p2g", "g2p", "grid_update"), key=lambda k: ktimes[k][0])
+    kms, kcnt = ktimes[dom]
+    avg_ms = kms / max(kcnt, 1)
+    achieved = ab[dom](N) / (avg_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = _json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+    step_ms = ms / args.steps
+    B_alg = 2 * S + 56.0 * nodes / N  # SURVEY §8(d) M3 per particle-step
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": ab[dom](N), "avg_launch_ms": avg_ms}
+    kshare = {k: {"ms_per_step": v[0] / max(v[1], 1) * (v[1] / args.steps), "launches": v[1]}
+              for k, v in ktimes.items()}
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1)
+    cpu = None
+    if world == 1:
+        rate, n_s, s_s, secs = cpu_oracle_rate(sc, sch, args.cpu_sample, args.cpu_steps)
+        cpu = {"value": rate, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {n_s:,} particles of the workload, {s_s} steps from the initial state "
+                         f"(fp64 plain C, single thread, {secs:.1f} s)", "cpu": os.cpu_count()}
+
+    line = {
+        "metric": "quantized MPM particle-steps/sec", "value": value, "unit": "particle-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": (value / PAPER_C3_PSTEPS) if (args.config == "c3" and not args.n
+                                                     and scheme_name(args) == "e0.01") else None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_name(args, sc, W, bits), "particles_per_gpu": N,
+                   "scheme": scheme_name(args), "record_bytes": S, "rounding": args.rounding,
+                   "round_counters": not args.no_counters, "scene_warmup_steps": args.scene_warmup,
+                   "l2": f"state {N * S / 1e9:.1f} GB per buffer >> 126 MB L2: no flush needed",
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (slab exchange not built)",
+                   "baseline_ref": "vs_baseline = value / 5.95e8 p-steps/s, the paper's RTX 3090 T-large elastic rate "
+                                   "(derived, P:945): context, not a target"},
+        "roofline": roofline,
+        "hbm_roofline_step": {"bytes_per_particle_step": B_alg,
+                              "achieved_GBps": value / world * B_alg / 1e9,
+                              "frac_of_8TBps": value / world * B_alg / 8e12,
+                              "frac_of_measured": value / world * B_alg / (hbm_peak * 1e9)},
+        "kernels": kshare,
+        "active_blocks": int(st.active_blocks), "touched_blocks": int(st.touched_blocks),
+        "out_of_domain": int(st.out_of_domain), "nonfinite": int(st.nonfinite), "pool_overflow": int(st.pool_overflow),
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()
