@@ -28,13 +28,36 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def scales(sim, o):
+def scales(sim, o, inp=None):
+    """Conditioning-aware scale per state scalar (DESIGN.md §5 "P2 tolerance").
+    fp32 summation error is bounded by eps * sum|terms|, so v is measured against the
+    magnitude of the P2G momentum terms in velocity units: |v|, |g| dt, |C| dx (APIC
+    term) and dt 4 (2 mu + d lambda) |F - I| / (rho dx) (stress term; fluid: E |J - 1|),
+    RMS over particles of the INPUT state.  C is a cancelling sum of node velocities
+    (C' = 4/dx sum w v_i (x) (i - fx)), so its scale is 4/dx * s_v."""
     d = sim["dim"]
     ns = o.shape[1]
     s = np.ones(ns)
     s[:d] = 1.0
     g = np.linalg.norm(sim["gravity"])
-    sv = max(float(np.sqrt(np.mean(o[:, d:2 * d] ** 2))), g * sim["dt"], 1e-12)
+    terms = [float(np.sqrt(np.mean(o[:, d:2 * d] ** 2))), g * sim["dt"], 1e-12]
+    if inp is not None:
+        inp = inp.astype(np.float64)
+        fluid = sim["material"] == "fluid"
+        C = inp[:, -d * d:]
+        terms.append(float(np.sqrt(np.mean(np.sum(C ** 2, 1)))) * sim["dx"])
+        E, nu = sim["E"], sim["nu"]
+        if fluid:
+            strain = np.abs(inp[:, 2 * d] - 1.0)
+            k = E
+        else:
+            F = inp[:, 2 * d:2 * d + d * d]
+            strain = np.sqrt(np.sum((F - np.eye(d).reshape(-1)) ** 2, 1))
+            mu = E / (2 * (1 + nu))
+            la = E * nu / ((1 + nu) * (1 - 2 * nu))
+            k = 2 * mu + d * la
+        terms.append(float(np.sqrt(np.mean(strain ** 2))) * sim["dt"] * 4 * k / (sim["p_rho"] * sim["dx"]))
+    sv = max(terms)
     s[d:2 * d] = sv
     s[-d * d:] = 4.0 / sim["dx"] * sv
     return s
@@ -77,7 +100,7 @@ def test_single_step_parity(case):
     o_pre, o_words, _ = oracle.step(sc.sim, sch, w_in, t, "f64")
     g_pre, g_words, st = run_gpu_step(sc, sch, w_in, t)
     assert st.pool_overflow == 0 and st.nonfinite == 0
-    s = scales(sc.sim, o_pre)
+    s = scales(sc.sim, o_pre, oracle.decode_state(sch, w_in))
     err = np.abs(g_pre.astype(np.float64) - o_pre) / np.maximum(np.abs(o_pre), s)
     worst = err.max(axis=0)
     assert worst.max() <= REL, (case, worst)
@@ -115,7 +138,7 @@ def test_fp32_oracle_agrees_too(case):
     o32, _, _ = oracle.step(sc.sim, sch, w_in, 6, "f32")
     o64, _, _ = oracle.step(sc.sim, sch, w_in, 6, "f64")
     g_pre, _, _ = run_gpu_step(sc, sch, w_in, 6)
-    s = scales(sc.sim, o64)
+    s = scales(sc.sim, o64, oracle.decode_state(sch, w_in))
     den = np.maximum(np.abs(o64), s)
     assert (np.abs(o32 - o64) / den).max() <= REL
     assert (np.abs(g_pre.astype(np.float64) - o64) / den).max() <= REL
