@@ -236,12 +236,13 @@ __device__ __forceinline__ void polar3(const float F[9], float R[9]) {
 // 2D polar: closed form (rotation by atan2(F10 - F01, F00 + F11)).
 __device__ __forceinline__ void polar2(const float F[4], float R[4]) {
   const float x = F[0] + F[3], y = F[2] - F[1];
-  const float r2 = x * x + y * y;
+  // IEEE sqrt and divisions: the stress depends on F - R, which for small strains is
+  // ~1e-6, so R must be as accurate as fp32 allows (an approximate rsqrt is not).
+  const float r = __fsqrt_rn(__fmaf_rn(x, x, y * y));
   float c = 1.0f, s = 0.0f;
-  if (r2 > 0.0f) {
-    const float ir = rsqrtf(r2);
-    c = x * ir;
-    s = y * ir;
+  if (r > 0.0f) {
+    c = __fdiv_rn(x, r);
+    s = __fdiv_rn(y, r);
   }
   R[0] = c; R[1] = -s; R[2] = s; R[3] = c;
 }
