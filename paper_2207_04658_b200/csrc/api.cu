@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "jit.h"
 #include "qmpm.h"
 #include "qmpm_launch.h"
 
@@ -38,7 +39,9 @@ struct qmpm_ctx {
   LayoutDev L{};
   SimDev S{};
   CodecDev C{};  // state codec: vals in scalar order
-  LaunchCfg cfg{};
+  StepJit jit{};
+  std::string jit_src;
+  int jit_regs_p2g = 0, jit_regs_g2p = 0;
   uint64_t cap = 0, n = 0, step = 0;
   uint32_t* rec[2] = {nullptr, nullptr};
   int cur = 0;
@@ -218,8 +221,8 @@ qmpm_status copy_in(qmpm_ctx* ctx, void* dst, const void* src, size_t bytes) {
 qmpm_status rebin(qmpm_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->block_count, 0, sizeof(uint32_t) * ctx->S.nblocks, ctx->stream));
   hook_fn(ctx, KBinCount, 1);
-  CK(launch_bin_count(ctx->dim, ctx->rec[ctx->cur], (uint32_t)ctx->n, ctx->L, ctx->S, ctx->key,
-                      ctx->block_count, ctx->stream));
+  CK(launch_bin_count(ctx->rec[ctx->cur], (uint32_t)ctx->n, ctx->S, ctx->key, ctx->block_count, ctx->jit,
+                      ctx->stream));
   hook_fn(ctx, KBinCount, 0);
   ctx->binned = true;
   return QMPM_OK;
@@ -439,11 +442,42 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   if (!e) e = cudaMemsetAsync(ctx->dc, 0, sizeof(DevCounters), ctx->stream);
   if (!e) e = cudaMemsetAsync(ctx->rec[0], 0, sizeof(uint32_t) * (cap * W + 1), ctx->stream);
   if (!e) e = cudaMemsetAsync(ctx->rec[1], 0, sizeof(uint32_t) * (cap * W + 1), ctx->stream);
-  if (!e) e = setup_kernels(d, ctx->material, ctx->L, ctx->cfg);
   if (!e) e = cudaStreamSynchronize(ctx->stream);
   if (e) {
     qmpm_destroy(ctx);
     return fail(nullptr, QMPM_ECUDA, "qmpm_create: %s", cudaGetErrorString(e));
+  }
+  // specialise the step kernels on this layout (NVRTC, sm_100a)
+  {
+    constexpr int kP2GWarps = 4, kG2PWarps = 4;
+    const int TN = d == 3 ? 216 : 100;
+    ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps);
+    JitModule m;
+    std::string jerr;
+    e = jit_get(ctx->jit_src, m, jerr);
+    if (e) {
+      qmpm_destroy(ctx);
+      return fail(nullptr, QMPM_ECUDA, "kernel specialisation failed: %s", jerr.c_str());
+    }
+    StepJit& J = ctx->jit;
+    J.bin_count = m.bin_count;
+    J.p2g = m.p2g;
+    J.g2p = m.g2p;
+    ctx->jit_regs_p2g = m.regs_p2g;
+    ctx->jit_regs_g2p = m.regs_g2p;
+    cudaDeviceGetAttribute(&J.num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    J.p2g_threads = kP2GWarps * 32;
+    J.g2p_threads = kG2PWarps * 32;
+    J.p2g_smem = sizeof(float4) * kP2GWarps * TN + sizeof(uint32_t) * kP2GWarps * 32 * L.SW;
+    J.g2p_smem = sizeof(float4) * TN + sizeof(uint32_t) * kG2PWarps * 32 * L.SW;
+    e = jit_set_smem(J.p2g, J.p2g_smem);
+    if (!e) e = jit_set_smem(J.g2p, J.g2p_smem);
+    if (e) {
+      qmpm_destroy(ctx);
+      return fail(nullptr, QMPM_ECUDA, "cannot set dynamic shared memory of the step kernels");
+    }
+    J.p2g_ctas = (unsigned)(J.num_sms * jit_occupancy(J.p2g, (int)J.p2g_threads, J.p2g_smem));
+    J.g2p_ctas = (unsigned)(J.num_sms * jit_occupancy(J.g2p, (int)J.g2p_threads, J.g2p_smem));
   }
   *out = ctx;
   return QMPM_OK;
@@ -531,7 +565,7 @@ qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps) {
     B.ntiles = ctx->ntiles;
     const uint64_t t_step = ctx->step + 1;  // steps are numbered 1, 2, ... (Q20)
     const uint32_t salt = step_salt(ctx->L.seed_lo, ctx->L.seed_hi, (uint32_t)t_step);
-    CK(launch_step(ctx->dim, ctx->material, B, ctx->L, ctx->S, salt, ctx->cfg, ctx->stream, hook_fn, ctx));
+    CK(launch_step(ctx->dim, B, ctx->S, salt, ctx->jit, ctx->stream, hook_fn, ctx));
     ctx->cur ^= 1;
     ctx->step = t_step;
     ctx->dbg_valid = ctx->dbg != nullptr;

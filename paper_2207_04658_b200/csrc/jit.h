@@ -1,0 +1,26 @@
+// jit.h -- NVRTC specialisation of the step kernels (internal).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "qmpm_device.cuh"
+
+namespace qmpm {
+
+struct JitModule {
+  CUmodule module;
+  CUfunction bin_count, p2g, g2p;
+  int regs_p2g, regs_g2p;
+  std::string log;
+};
+
+// the generated preamble + #include of step_kernels.cuh for one layout
+std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps, int g2p_warps);
+cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err);
+cudaError_t jit_set_smem(CUfunction f, size_t bytes);
+int jit_occupancy(CUfunction f, int threads, size_t smem);
+cudaError_t jit_launch(CUfunction f, unsigned grid, unsigned block, size_t smem, cudaStream_t st, void** args);
+
+}  // namespace qmpm

@@ -1,0 +1,154 @@
+// mpm_common.cuh -- MLS-MPM device helpers shared by the nvcc-compiled kernels
+// (kernels.cu) and the NVRTC-specialised step kernels (step_kernels.cuh).
+//
+// Grid geometry: the grid is tiled into blocks of 4^3 cells (3D) or 8^2 cells (2D),
+// 64 nodes each; a particle belongs to the block of its base cell
+// base = floor(x/dx - 1/2) (Hu et al. 2018, cited P:561).  Its 3^d stencil lies in
+// the block's (B+2)^d node tile.
+#pragma once
+#include "qmpm_device.cuh"
+
+namespace qmpm {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <int D>
+struct Geo;
+template <>
+struct Geo<3> {
+  static constexpr int B = 4;     // cells per block side
+  static constexpr int LB = 2;    // log2(B)
+  static constexpr int T = 6;     // tile side (nodes): B + 2
+  static constexpr int TN = 216;  // tile nodes
+};
+template <>
+struct Geo<2> {
+  static constexpr int B = 8;
+  static constexpr int LB = 3;
+  static constexpr int T = 10;
+  static constexpr int TN = 100;
+};
+
+template <int D, int MAT>
+struct NS {
+  static constexpr int value = 2 * D + (MAT == 1 ? 1 : D * D) + D * D;
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <int D>
+__device__ __forceinline__ void block_coords(uint32_t b, const SimDev& S, int bc[3]) {
+  if (D == 3) {
+    bc[2] = (int)(b % (uint32_t)S.nb[2]);
+    const uint32_t r = b / (uint32_t)S.nb[2];
+    bc[1] = (int)(r % (uint32_t)S.nb[1]);
+    bc[0] = (int)(r / (uint32_t)S.nb[1]);
+  } else {
+    bc[1] = (int)(b % (uint32_t)S.nb[1]);
+    bc[0] = (int)(b / (uint32_t)S.nb[1]);
+    bc[2] = 0;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t block_id(const int c[3], const SimDev& S) {
+  if (D == 3) return ((uint32_t)c[0] * (uint32_t)S.nb[1] + (uint32_t)c[1]) * (uint32_t)S.nb[2] + (uint32_t)c[2];
+  return (uint32_t)c[0] * (uint32_t)S.nb[1] + (uint32_t)c[1];
+}
+
+// node-in-block linear index (x-major)
+template <int D>
+__device__ __forceinline__ uint32_t local_node(const int l[3]) {
+  if (D == 3) return (uint32_t)((l[0] * 4 + l[1]) * 4 + l[2]);
+  return (uint32_t)(l[0] * 8 + l[1]);
+}
+
+// block key of a particle from its (decoded) position
+template <int D>
+__device__ __forceinline__ uint32_t key_of(const float* x, const SimDev& S) {
+  int c[3] = {0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    float fx;
+    bool o;
+    c[a] = base_fx(x[a], S.inv_dx, S.res[a], fx, o) >> Geo<D>::LB;
+  }
+  return block_id<D>(c, S);
+}
+
+// tile node t -> (global node coordinates) for a block with origin org
+template <int D>
+__device__ __forceinline__ void tile_node(int t, const int org[3], int node[3]) {
+  using G = Geo<D>;
+  if (D == 3) {
+    node[2] = org[2] + t % G::T;
+    node[1] = org[1] + (t / G::T) % G::T;
+    node[0] = org[0] + t / (G::T * G::T);
+  } else {
+    node[1] = org[1] + t % G::T;
+    node[0] = org[0] + t / G::T;
+    node[2] = 0;
+  }
+}
+
+// a harmless particle for the idle lanes of a partial warp (never stored)
+template <int D, int MAT>
+__device__ __forceinline__ void benign_state(float* s, const int org[3], float dx) {
+  constexpr int NSV = NS<D, MAT>::value;
+#pragma unroll
+  for (int i = 0; i < NSV; ++i) s[i] = 0.0f;
+#pragma unroll
+  for (int a = 0; a < D; ++a) s[a] = (org[a] + 1.0f) * dx;
+  if (MAT == 1) {
+    s[2 * D] = 1.0f;
+  } else {
+#pragma unroll
+    for (int a = 0; a < D; ++a) s[2 * D + a * D + a] = 1.0f;
+  }
+}
+
+// affine momentum matrix of one particle (Hu et al. 2018; DESIGN.md §2 Q15):
+//   aff = -dt V_p 4/dx^2 P(F)F^T + m_p C
+//   elastic (fixed corotated): P F^T = 2 mu (F - R) F^T + lambda (J - 1) J I
+//   fluid:                     P F^T = E (J - 1) I
+template <int D, int MAT>
+__device__ __forceinline__ void affine_of(const float* s, const SimDev& S, float aff[D * D]) {
+  constexpr int CO = 2 * D + (MAT == 1 ? 1 : D * D);  // offset of C
+  if (MAT == 1) {
+    const float J = s[2 * D];
+    const float p = S.stress_scale * S.E * (J - 1.0f);
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) aff[i] = S.p_mass * s[CO + i];
+#pragma unroll
+    for (int a = 0; a < D; ++a) aff[a * D + a] += p;
+  } else {
+    const float* F = s + 2 * D;
+    float R[D * D];
+    float J;
+    if (D == 3) {
+      polar3(F, R);
+      J = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
+          F[2] * (F[3] * F[7] - F[4] * F[6]);
+    } else {
+      polar2(F, R);
+      J = F[0] * F[3] - F[1] * F[2];
+    }
+    const float two_mu = 2.0f * S.mu * S.stress_scale;
+    const float diag = S.lambda * (J - 1.0f) * J * S.stress_scale;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc += (F[a * D + k] - R[a * D + k]) * F[b * D + k];
+        aff[a * D + b] = two_mu * acc + S.p_mass * s[CO + a * D + b] + (a == b ? diag : 0.0f);
+      }
+  }
+}
+
+}  // namespace qmpm

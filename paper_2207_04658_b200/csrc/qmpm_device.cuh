@@ -9,8 +9,15 @@
 //             (Q3); RNE (Q6) or u = floor(t) + [y >= 1 - r] (Q6), saturated.
 //   r24       reading Q5 (the paper's generator, is in an unavailable supplement).
 #pragma once
+#ifdef __CUDACC_RTC__
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+#else
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace qmpm {
 

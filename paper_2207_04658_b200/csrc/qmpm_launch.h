@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <cuda.h>
+
 #include "qmpm_device.cuh"
 
 namespace qmpm {
@@ -46,25 +48,21 @@ enum KernelId {
   KNumKernels
 };
 
-struct LaunchCfg {
+// the NVRTC-specialised kernels of one layout and their launch configuration
+struct StepJit {
+  CUfunction bin_count, p2g, g2p;
   int num_sms;
-  int p2g_ctas;
-  int g2p_ctas;
-  size_t p2g_smem;
-  size_t g2p_smem;
+  unsigned p2g_ctas, g2p_ctas, p2g_threads, g2p_threads;
+  size_t p2g_smem, g2p_smem;
 };
-
-cudaError_t setup_kernels(int dim, int material, const LayoutDev& L, LaunchCfg& cfg);
 
 // one hook per kernel so the runtime can bracket launches with events
 typedef void (*KernelHook)(void* user, int kernel_id, int begin);
 
-cudaError_t launch_bin_count(int dim, const uint32_t* rec, uint32_t n, const LayoutDev& L,
-                             const SimDev& S, uint32_t* key, uint32_t* block_count,
-                             cudaStream_t st);
-cudaError_t launch_step(int dim, int material, const StepBuffers& B, const LayoutDev& L,
-                        const SimDev& S, uint32_t salt, const LaunchCfg& cfg, cudaStream_t st,
-                        KernelHook hook, void* user);
+cudaError_t launch_bin_count(const uint32_t* rec, uint32_t n, const SimDev& S, uint32_t* key, uint32_t* block_count,
+                             const StepJit& J, cudaStream_t st);
+cudaError_t launch_step(int dim, const StepBuffers& B, const SimDev& S, uint32_t salt, const StepJit& J,
+                        cudaStream_t st, KernelHook hook, void* user);
 
 cudaError_t launch_encode(const CodecDev& C, uint64_t n, const float* vals, const uint32_t* keys,
                           uint32_t salt, uint32_t* words, unsigned long long* counters,

@@ -1,0 +1,558 @@
+// step_kernels.cuh -- the layout-specialised kernels of one quantized MLS-MPM step.
+//
+// Compiled at qmpm_create by NVRTC for sm_100a, after a generated preamble that
+// defines `struct Spec` (the scheme's bit-pack layout as compile-time constants:
+// per state scalar its word, shift, width, kind, Delta, 1/Delta, offset and packing
+// index).  With the layout constant, every field access is a constant shift/mask on
+// a record held in REGISTERS (bit pack load, Fig. bit_pack_operation), and
+// the re-encode packs into registers (no read-modify-write of shared words).
+//
+//   qmpm_bin_count  a1        block key + histogram (first step after set_state/set_words)
+//   qmpm_p2g        a2+a3     decode, stress, scatter into per-warp shared-memory tiles
+//                             (lanes of one round have distinct base cells, so the
+//                             tile RMW needs no atomics), red.global.add.v4.f32 flush
+//   qmpm_g2p        a2+a5-a7  gather from a shared-memory tile, update, dithered encode,
+//                             coalesced store in sorted order, next step's block key
+#pragma once
+#include "mpm_common.cuh"
+
+namespace qmpm {
+
+// ------------------------------------------------------------------ field access
+// value of state scalar i from a register-resident record w[0..W] (w[W] = 0)
+template <class SP>
+__device__ __forceinline__ float sdec(const uint32_t* w, const int i) {
+  const int wd = SP::word(i), sh = SP::shift(i), wi = SP::width(i);
+  const uint32_t raw = (sh + wi <= 32) ? (w[wd] >> sh) : __funnelshift_r(w[wd], w[wd + 1], sh);
+  if (SP::kind(i) == kKindRaw) return __uint_as_float(raw);
+  const int u = ((int)(raw << (32 - wi))) >> (32 - wi);  // sign-extend b+1 bits (Q2)
+  float x = __fmul_rn(__int2float_rn(u), SP::delta(i));   // Eq. 3: u * Delta
+  if (SP::offset(i) != 0.0f) x = __fadd_rn(x, SP::offset(i));
+  return x;
+}
+
+struct EncFlags {
+  bool up, down, sat, nonfinite;
+};
+
+// Eq. 3 / Eq. 11 encode of state scalar i; returns the field's bits (width-masked).
+template <class SP>
+__device__ __forceinline__ uint32_t senc(const int i, float v, uint32_t r24, EncFlags& fl) {
+  fl.up = fl.down = fl.sat = fl.nonfinite = false;
+  if (SP::kind(i) == kKindRaw) {
+    fl.nonfinite = !isfinite(v);
+    return __float_as_uint(v);
+  }
+  const int wi = SP::width(i);
+  if (!isfinite(v)) {
+    fl.nonfinite = true;
+    return 0u;
+  }
+  const float a = (SP::offset(i) != 0.0f) ? __fsub_rn(v, SP::offset(i)) : v;
+  const float t = __fmul_rn(a, SP::inv_delta(i));  // one fp32 multiply, no FMA (Q3)
+  const uint32_t mask = (wi == 32) ? 0xffffffffu : ((1u << wi) - 1u);
+  if (wi <= 25) {
+    // |codes| <= 2^24: clamping f to [-2^b - 2, 2^b] (exact floats) keeps every
+    // saturation decision of the exact integer rule
+    const float lo_f = -(float)(1 << (wi - 1)) - 2.0f, hi_f = (float)(1 << (wi - 1));
+    const int lo = -(1 << (wi - 1)), hi = (1 << (wi - 1)) - 1;
+    int u;
+    if (SP::DITHER) {
+      const float f = floorf(t);
+      const float y = __fsub_rn(t, f);  // exact
+      const float one_minus_r = __fmul_rn(__uint2float_rn(0x1000000u - r24), 0x1p-24f);  // exact
+      fl.up = y >= one_minus_r;         // u = floor(t + r) (Eq. 11, reading Q6)
+      fl.down = !fl.up && y > 0.0f;
+      u = __float2int_rz(fminf(fmaxf(f, lo_f), hi_f)) + (fl.up ? 1 : 0);
+    } else {
+      const float q = rintf(t);  // round half to even (Q6)
+      fl.up = q > t;
+      fl.down = q < t;
+      u = __float2int_rz(fminf(fmaxf(q, lo_f), hi_f));
+    }
+    if (u > hi) { u = hi; fl.sat = true; }
+    if (u < lo) { u = lo; fl.sat = true; }
+    return (uint32_t)u & mask;
+  } else {
+    long long u;
+    if (SP::DITHER) {
+      const float f = floorf(t);
+      const float y = __fsub_rn(t, f);
+      const float one_minus_r = __fmul_rn(__uint2float_rn(0x1000000u - r24), 0x1p-24f);
+      fl.up = y >= one_minus_r;
+      fl.down = !fl.up && y > 0.0f;
+      u = __float2ll_rz(fminf(fmaxf(f, -1099511627776.0f), 1099511627776.0f)) + (fl.up ? 1 : 0);
+    } else {
+      const float q = rintf(t);
+      fl.up = q > t;
+      fl.down = q < t;
+      u = __float2ll_rz(fminf(fmaxf(q, -1099511627776.0f), 1099511627776.0f));
+    }
+    const long long hi = (1ll << (wi - 1)) - 1, lo = -(1ll << (wi - 1));
+    if (u > hi) { u = hi; fl.sat = true; }
+    if (u < lo) { u = lo; fl.sat = true; }
+    return (uint32_t)u & mask;
+  }
+}
+
+template <class SP>
+__device__ __forceinline__ void sput(uint32_t* w, const int i, uint32_t bits) {
+  const int wd = SP::word(i), sh = SP::shift(i), wi = SP::width(i);
+  w[wd] |= bits << sh;
+  if (sh + wi > 32) w[wd + 1] |= bits >> (32 - sh);
+}
+
+// content key of a record (reading Q5): k = mix(k ^ word) over the words holding x
+template <class SP>
+__device__ __forceinline__ uint32_t content_key(const uint32_t* w) {
+  uint32_t k = 0;
+#pragma unroll
+  for (int q = 0; q < SP::W; ++q)
+    if ((SP::XMASK >> q) & 1u) k = mix32(k ^ w[q]);
+  return k;
+}
+
+// ------------------------------------------------------------------ staging
+// Warp-cooperative load of the warp's cnt records (record index of lane l in r_lane)
+// into registers w[0..W] of their owner lane, through rows of a shared-memory stage.
+// All W loads of a lane are issued before any is consumed.
+template <class SP>
+__device__ __forceinline__ void load_records(const uint32_t* __restrict__ rec, uint32_t r_lane, uint32_t cnt,
+                                             uint32_t* wst, int lane, uint32_t* w) {
+  constexpr int W = SP::W, SW = SP::SW;
+  uint32_t v[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const uint32_t q = (uint32_t)(k * 32 + lane);
+    const uint32_t l = q / W, o = q - l * W;
+    const uint32_t r = __shfl_sync(FULL, r_lane, (int)(l & 31u));
+    v[k] = (l < cnt) ? __ldg(rec + (size_t)r * W + o) : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const uint32_t q = (uint32_t)(k * 32 + lane);
+    const uint32_t l = q / W, o = q - l * W;
+    wst[l * SW + o] = v[k];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < W; ++k) w[k] = wst[lane * SW + k];
+  w[W] = 0u;
+  __syncwarp();
+}
+
+// coalesced store of the warp's cnt records (lane l holds record l in w) to out[0..cnt*W)
+template <class SP>
+__device__ __forceinline__ void store_records(uint32_t* __restrict__ out, uint32_t cnt, uint32_t* wst, int lane,
+                                              const uint32_t* w) {
+  constexpr int W = SP::W, SW = SP::SW;
+#pragma unroll
+  for (int k = 0; k < W; ++k) wst[lane * SW + k] = w[k];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const uint32_t q = (uint32_t)(k * 32 + lane);
+    const uint32_t l = q / W, o = q - l * W;
+    const uint32_t val = wst[l * SW + o];
+    if (l < cnt) out[q] = val;
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------ a1: bin count
+template <class SP>
+__device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec, uint32_t n, const SimDev& S,
+                                               uint32_t* __restrict__ key, uint32_t* __restrict__ block_count) {
+  constexpr int D = SP::D, W = SP::W;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < n;
+  uint32_t k = 0xffffffffu;
+  if (valid) {
+    uint32_t w[W + 1];
+#pragma unroll
+    for (int q = 0; q < W; ++q) w[q] = ((SP::XMASK >> q) & 1u) ? __ldg(rec + (size_t)i * W + q) : 0u;
+    w[W] = 0u;
+    float x[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[a] = sdec<SP>(w, a);
+    k = key_of<D>(x, S);
+    key[i] = k;
+  }
+  const unsigned peers = __match_any_sync(FULL, k);
+  if (valid && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
+}
+
+// ------------------------------------------------------------------ a3: P2G
+template <class SP>
+__device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const uint32_t* __restrict__ perm,
+                                         const uint32_t* __restrict__ block_start,
+                                         const uint32_t* __restrict__ active_list,
+                                         const DevCounters* __restrict__ dc,
+                                         const uint32_t* __restrict__ block_slot, float4* __restrict__ mp,
+                                         const SimDev& S) {
+  constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, WARPS = SP::P2G_WARPS;
+  using G = Geo<D>;
+  extern __shared__ float4 smem4[];
+  float4* tiles = smem4;                                                  // [WARPS][TN]
+  uint32_t* stage = reinterpret_cast<uint32_t*>(tiles + WARPS * G::TN);  // [WARPS][32][SW]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4* tile = tiles + warp * G::TN;
+  uint32_t* wst = stage + warp * 32 * SP::SW;
+  const uint32_t n_active = dc->n_active;
+
+  for (uint32_t ab = blockIdx.x; ab < n_active; ab += gridDim.x) {
+    const uint32_t b = active_list[ab];
+    const uint32_t start = block_start[b], end = block_start[b + 1];
+    int bc[3];
+    block_coords<D>(b, S, bc);
+    const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
+    for (int t = threadIdx.x; t < WARPS * G::TN; t += blockDim.x) tiles[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+
+    for (uint32_t j0 = start + warp * 32; j0 < end; j0 += WARPS * 32) {
+      const uint32_t cnt = min(32u, end - j0);
+      const bool valid = (uint32_t)lane < cnt;
+      const uint32_t r = perm[j0 + (valid ? lane : 0)];
+      uint32_t w[SP::W + 1];
+      load_records<SP>(rec, r, cnt, wst, lane, w);
+      float s[NSV];
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < NSV; ++i) s[i] = sdec<SP>(w, i);
+      } else {
+        benign_state<D, MAT>(s, org, S.dx);
+      }
+      int lb[3] = {0, 0, 0};
+      float fx[3] = {0.f, 0.f, 0.f}, wt[3][3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        bool o;
+        lb[a] = base_fx(s[a], S.inv_dx, S.res[a], fx[a], o) - org[a];
+        bspline_w(fx[a], wt[a]);
+      }
+      float aff[D * D];
+      affine_of<D, MAT>(s, S, aff);
+      // momentum at node o: m v + aff (o - fx) dx = Q + sum_k o_k a_k,  a_k = dx aff[:,k]
+      float ak[3][3], Q[3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        Q[a] = S.p_mass * s[D + a];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          ak[k][a] = S.dx * aff[a * D + k];
+          Q[a] -= fx[k] * ak[k][a];
+        }
+      }
+      const int cell = valid ? (D == 3 ? (lb[0] * 4 + lb[1]) * 4 + lb[2] : lb[0] * 8 + lb[1]) : -1 - lane;
+      const unsigned peers = __match_any_sync(FULL, cell);
+      const int rank = __popc(peers & lanemask_lt());
+      const int rounds = __reduce_max_sync(FULL, (unsigned)__popc(peers));
+      const int base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
+      for (int rr = 0; rr < rounds; ++rr) {
+        const bool mine = valid && rank == rr;
+        const unsigned m = __ballot_sync(FULL, mine);
+        if (mine) {
+#pragma unroll
+          for (int ox = 0; ox < 3; ++ox) {
+#pragma unroll
+            for (int oy = 0; oy < 3; ++oy) {
+              const float wxy = wt[0][ox] * wt[1][oy];
+              float M[3];
+#pragma unroll
+              for (int a = 0; a < 3; ++a) M[a] = Q[a] + ox * ak[0][a] + oy * ak[1][a];
+              if (D == 3) {
+#pragma unroll
+                for (int oz = 0; oz < 3; ++oz) {
+                  const float ww = wxy * wt[2][oz];
+                  const int idx = base_idx + (ox * G::T + oy) * G::T + oz;
+                  float4 t = tile[idx];
+                  t.x = fmaf(ww, S.p_mass, t.x);
+                  t.y = fmaf(ww, M[0], t.y);
+                  t.z = fmaf(ww, M[1], t.z);
+                  t.w = fmaf(ww, M[2], t.w);
+                  tile[idx] = t;
+                  __syncwarp(m);
+#pragma unroll
+                  for (int a = 0; a < 3; ++a) M[a] += ak[2][a];
+                }
+              } else {
+                const int idx = base_idx + ox * G::T + oy;
+                float4 t = tile[idx];
+                t.x = fmaf(wxy, S.p_mass, t.x);
+                t.y = fmaf(wxy, M[0], t.y);
+                t.z = fmaf(wxy, M[1], t.z);
+                tile[idx] = t;
+                __syncwarp(m);
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // flush: sum the warp tiles, one vector reduction per non-empty node
+    for (int t = threadIdx.x; t < G::TN; t += blockDim.x) {
+      float4 acc = tiles[t];
+#pragma unroll
+      for (int wv = 1; wv < WARPS; ++wv) {
+        const float4 o = tiles[wv * G::TN + t];
+        acc.x += o.x;
+        acc.y += o.y;
+        acc.z += o.z;
+        acc.w += o.w;
+      }
+      if (acc.x != 0.0f) {
+        int node[3];
+        tile_node<D>(t, org, node);
+        int nb[3], ln[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          nb[a] = node[a] >> G::LB;
+          ln[a] = node[a] & (G::B - 1);
+        }
+        const uint32_t slot = block_slot[block_id<D>(nb, S)];
+        if (slot != 0xffffffffu) atomicAdd(&mp[(size_t)slot * 64 + local_node<D>(ln)], acc);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ a5-a7: G2P + encode
+template <class SP>
+__device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, uint32_t* __restrict__ rec_out,
+                                         const uint32_t* __restrict__ perm, const uint32_t* __restrict__ ids_in,
+                                         uint32_t* __restrict__ ids_out, float* __restrict__ dbg,
+                                         uint32_t* __restrict__ key_out, uint32_t* __restrict__ block_count,
+                                         const uint32_t* __restrict__ block_start,
+                                         const uint32_t* __restrict__ active_list, DevCounters* __restrict__ dc,
+                                         const uint32_t* __restrict__ block_slot, const float4* __restrict__ gv,
+                                         const SimDev& S, uint32_t salt) {
+  constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, WARPS = SP::G2P_WARPS, W = SP::W;
+  constexpr int CO = 2 * D + (MAT == 1 ? 1 : D * D);
+  using G = Geo<D>;
+  extern __shared__ float4 smem4[];
+  float4* tile = smem4;                                         // [TN]
+  uint32_t* stage = reinterpret_cast<uint32_t*>(tile + G::TN);  // [WARPS][32][SW]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* wst = stage + warp * 32 * SP::SW;
+  // per-lane counters: lane f accumulates field-scalar f's round-ups / downs / saturations
+  unsigned c_up = 0, c_down = 0, c_sat = 0, c_nf = 0, c_oob = 0;
+  const uint32_t n_active = dc->n_active;
+  const float four_inv_dx = 4.0f * S.inv_dx;
+
+  for (uint32_t ab = blockIdx.x; ab < n_active; ab += gridDim.x) {
+    const uint32_t b = active_list[ab];
+    const uint32_t start = block_start[b], end = block_start[b + 1];
+    int bc[3];
+    block_coords<D>(b, S, bc);
+    const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
+    __syncthreads();  // previous tile fully consumed
+    for (int t = threadIdx.x; t < G::TN; t += blockDim.x) {
+      int node[3];
+      tile_node<D>(t, org, node);
+      int nb[3], ln[3];
+      bool inside = true;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (a < D && node[a] >= S.res[a]) inside = false;
+        nb[a] = node[a] >> G::LB;
+        ln[a] = node[a] & (G::B - 1);
+      }
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (inside) {
+        const uint32_t slot = block_slot[block_id<D>(nb, S)];
+        if (slot != 0xffffffffu) v = gv[(size_t)slot * 64 + local_node<D>(ln)];
+      }
+      tile[t] = v;
+    }
+    __syncthreads();
+
+    for (uint32_t j0 = start + warp * 32; j0 < end; j0 += WARPS * 32) {
+      const uint32_t cnt = min(32u, end - j0);
+      const bool valid = (uint32_t)lane < cnt;
+      const uint32_t r = perm[j0 + (valid ? lane : 0)];
+      uint32_t w[W + 1];
+      load_records<SP>(rec_in, r, cnt, wst, lane, w);
+      const uint32_t h = mix32(content_key<SP>(w) ^ salt);
+      float s[NSV];
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < NSV; ++i) s[i] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < D; ++i) s[i] = sdec<SP>(w, i);
+#pragma unroll
+        for (int i = 2 * D; i < CO; ++i) s[i] = sdec<SP>(w, i);
+      } else {
+        benign_state<D, MAT>(s, org, S.dx);
+      }
+      int lb[3] = {0, 0, 0};
+      float fx[3] = {0.f, 0.f, 0.f}, wt[3][3];
+      bool oob_any = false;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        bool o;
+        lb[a] = base_fx(s[a], S.inv_dx, S.res[a], fx[a], o) - org[a];
+        oob_any |= o;
+        bspline_w(fx[a], wt[a]);
+      }
+      // gather: v' = sum w v_i;  C' = 4/dx sum w v_i (x) (i - fx) = 4/dx (T - v' fx^T)
+      float Sv[3] = {0.f, 0.f, 0.f}, T[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+      const int base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
+      if (D == 3) {
+#pragma unroll
+        for (int ox = 0; ox < 3; ++ox)
+#pragma unroll
+          for (int oy = 0; oy < 3; ++oy) {
+            const float wxy = wt[0][ox] * wt[1][oy];
+            const int idx = base_idx + (ox * G::T + oy) * G::T;
+            const float4 g0 = tile[idx], g1 = tile[idx + 1], g2 = tile[idx + 2];
+            const float g[3][3] = {{g0.x, g0.y, g0.z}, {g1.x, g1.y, g1.z}, {g2.x, g2.y, g2.z}};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              const float u0 = wt[2][0] * g[0][a], u1 = wt[2][1] * g[1][a], u2 = wt[2][2] * g[2][a];
+              const float sz = u0 + u1 + u2;
+              const float tz = u1 + 2.0f * u2;
+              Sv[a] = fmaf(wxy, sz, Sv[a]);
+              T[a][2] = fmaf(wxy, tz, T[a][2]);
+              if (ox) T[a][0] = fmaf(wxy * ox, sz, T[a][0]);
+              if (oy) T[a][1] = fmaf(wxy * oy, sz, T[a][1]);
+            }
+          }
+      } else {
+#pragma unroll
+        for (int ox = 0; ox < 3; ++ox) {
+          const int idx = base_idx + ox * G::T;
+          const float4 g0 = tile[idx], g1 = tile[idx + 1], g2 = tile[idx + 2];
+          const float g[3][2] = {{g0.x, g0.y}, {g1.x, g1.y}, {g2.x, g2.y}};
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            const float u0 = wt[1][0] * g[0][a], u1 = wt[1][1] * g[1][a], u2 = wt[1][2] * g[2][a];
+            const float sy = u0 + u1 + u2;
+            const float ty = u1 + 2.0f * u2;
+            Sv[a] = fmaf(wt[0][ox], sy, Sv[a]);
+            T[a][1] = fmaf(wt[0][ox], ty, T[a][1]);
+            if (ox) T[a][0] = fmaf(wt[0][ox] * ox, sy, T[a][0]);
+          }
+        }
+      }
+      float Cn[D * D];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int k = 0; k < D; ++k) Cn[a * D + k] = four_inv_dx * (T[a][k] - Sv[a] * fx[k]);
+      float o[NSV];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        o[a] = s[a] + S.dt * Sv[a];
+        o[D + a] = Sv[a];
+      }
+      if (MAT == 1) {
+        float tr = 0.f;
+#pragma unroll
+        for (int a = 0; a < D; ++a) tr += Cn[a * D + a];
+        o[2 * D] = s[2 * D] * (1.0f + S.dt * tr);
+      } else {
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            float acc = s[2 * D + a * D + k];
+#pragma unroll
+            for (int m = 0; m < D; ++m) acc = fmaf(S.dt * Cn[a * D + m], s[2 * D + m * D + k], acc);
+            o[2 * D + a * D + k] = acc;
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < D * D; ++i) o[CO + i] = Cn[i];
+      const uint32_t j = j0 + lane;
+      if (dbg != nullptr && valid) {
+#pragma unroll
+        for (int i = 0; i < NSV; ++i) dbg[(size_t)j * NSV + i] = o[i];
+      }
+      // dithered encode into registers (Eq. 11; reading Q5, Q6)
+      uint32_t ow[W + 1];
+#pragma unroll
+      for (int q = 0; q <= W; ++q) ow[q] = 0u;
+      bool any_flag = false;
+#pragma unroll
+      for (int i = 0; i < NSV; ++i) {
+        const uint32_t r24 = (SP::DITHER && SP::kind(i) == kKindFixed) ? r24_of(h, SP::idx(i)) : 0u;
+        EncFlags fl;
+        const uint32_t bits = senc<SP>(i, o[i], r24, fl);
+        sput<SP>(ow, i, bits);
+        if (SP::COUNTERS && SP::kind(i) == kKindFixed) {
+          const unsigned bu = __ballot_sync(FULL, valid && fl.up);
+          const unsigned bd = __ballot_sync(FULL, valid && fl.down);
+          if (lane == i) {
+            c_up += __popc(bu);
+            c_down += __popc(bd);
+          }
+        }
+        if (valid && (fl.sat || fl.nonfinite)) any_flag = true;
+      }
+      if (__any_sync(FULL, any_flag)) {  // rare: recount saturations / non-finite
+#pragma unroll
+        for (int i = 0; i < NSV; ++i) {
+          EncFlags fl;
+          const uint32_t r24 = (SP::DITHER && SP::kind(i) == kKindFixed) ? r24_of(h, SP::idx(i)) : 0u;
+          senc<SP>(i, o[i], r24, fl);
+          const unsigned bs = __ballot_sync(FULL, valid && fl.sat);
+          const unsigned bn = __ballot_sync(FULL, valid && fl.nonfinite);
+          if (lane == i) c_sat += __popc(bs);
+          if (lane == 0) c_nf += __popc(bn);
+        }
+      }
+      {
+        const unsigned bo = __ballot_sync(FULL, valid && oob_any);
+        if (lane == 0) c_oob += __popc(bo);
+      }
+      // next step's block key from the re-decoded (quantized) x
+      float xq[3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
+      const uint32_t nk = valid ? key_of<D>(xq, S) : 0xffffffffu;
+      if (valid) key_out[j] = nk;
+      const unsigned kp = __match_any_sync(FULL, nk);
+      if (valid && lane == __ffs(kp) - 1) atomicAdd(&block_count[nk], (unsigned)__popc(kp));
+      if (ids_out != nullptr && valid) ids_out[j] = ids_in[r];
+      store_records<SP>(rec_out + (size_t)j0 * W, cnt, wst, lane, ow);
+    }
+  }
+  // flush this thread's counters (lane i holds scalar i's counts)
+  if (lane < NSV) {
+    int fi = 0;
+#pragma unroll
+    for (int i = 0; i < NSV; ++i)
+      if (lane == i) fi = SP::idx(i);
+    if (c_up) atomicAdd(&dc->up[fi], (unsigned long long)c_up);
+    if (c_down) atomicAdd(&dc->down[fi], (unsigned long long)c_down);
+    if (c_sat) atomicAdd(&dc->sat[fi], (unsigned long long)c_sat);
+  }
+  if (c_nf) atomicAdd(&dc->nonfinite, (unsigned long long)c_nf);
+  if (c_oob) atomicAdd(&dc->oob, (unsigned long long)c_oob);
+}
+
+}  // namespace qmpm
+
+// ------------------------------------------------------------------ entry points
+extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t* rec, uint32_t n, qmpm::SimDev S,
+                                                                 uint32_t* key, uint32_t* block_count) {
+  qmpm::bin_count_body<Spec>(rec, n, S, key, block_count);
+}
+
+extern "C" __global__ void __launch_bounds__(Spec::P2G_WARPS * 32)
+    qmpm_p2g(const uint32_t* rec, const uint32_t* perm, const uint32_t* block_start, const uint32_t* active_list,
+             const qmpm::DevCounters* dc, const uint32_t* block_slot, float4* mp, qmpm::SimDev S) {
+  qmpm::p2g_body<Spec>(rec, perm, block_start, active_list, dc, block_slot, mp, S);
+}
+
+extern "C" __global__ void __launch_bounds__(Spec::G2P_WARPS * 32)
+    qmpm_g2p(const uint32_t* rec_in, uint32_t* rec_out, const uint32_t* perm, const uint32_t* ids_in,
+             uint32_t* ids_out, float* dbg, uint32_t* key_out, uint32_t* block_count, const uint32_t* block_start,
+             const uint32_t* active_list, qmpm::DevCounters* dc, const uint32_t* block_slot, const float4* gv,
+             qmpm::SimDev S, uint32_t salt) {
+  qmpm::g2p_body<Spec>(rec_in, rec_out, perm, ids_in, ids_out, dbg, key_out, block_count, block_start, active_list,
+                       dc, block_slot, gv, S, salt);
+}
