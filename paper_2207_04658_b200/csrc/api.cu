@@ -6,6 +6,7 @@
 // and the device counters.  Everything is enqueued on the ctx stream; qmpm_step
 // allocates nothing.
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -450,8 +451,15 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   // specialise the step kernels on this layout (NVRTC, sm_100a)
   {
     constexpr int kP2GWarps = 4, kG2PWarps = 4;
+    // minimum resident CTAs per SM the kernels are compiled for (register cap);
+    // QMPM_P2G_MINB / QMPM_G2P_MINB override the defaults for tuning runs
+    auto env_int = [](const char* name, int dflt) {
+      const char* v = getenv(name);
+      return (v && *v) ? atoi(v) : dflt;
+    };
+    const int kP2GMinBlocks = env_int("QMPM_P2G_MINB", 3), kG2PMinBlocks = env_int("QMPM_G2P_MINB", 4);
     const int TN = d == 3 ? 216 : 100;
-    ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps);
+    ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps, kP2GMinBlocks, kG2PMinBlocks);
     JitModule m;
     std::string jerr;
     e = jit_get(ctx->jit_src, m, jerr);

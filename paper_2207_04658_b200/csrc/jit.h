@@ -17,7 +17,8 @@ struct JitModule {
 };
 
 // the generated preamble + #include of step_kernels.cuh for one layout
-std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps, int g2p_warps);
+std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps, int g2p_warps, int p2g_minb,
+                        int g2p_minb);
 cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err);
 cudaError_t jit_set_smem(CUfunction f, size_t bytes);
 int jit_occupancy(CUfunction f, int threads, size_t smem);

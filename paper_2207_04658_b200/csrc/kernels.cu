@@ -182,7 +182,7 @@ __global__ void k_bin_scatter(const uint32_t* __restrict__ key, uint32_t n,
                               uint32_t* __restrict__ perm) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < n;
-  const uint32_t k = valid ? key[i] : 0xffffffffu;
+  const uint32_t k = valid ? (key[i] >> 6) : 0xffffffffu;  // block of the sort key
   const unsigned peers = __match_any_sync(FULL, k);
   const int leader = __ffs(peers) - 1;
   const int rank = __popc(peers & lanemask_lt());
@@ -329,8 +329,8 @@ static cudaError_t step_d(const StepBuffers& B, const SimDev& S, uint32_t salt, 
   {
     H(KP2G, 1);
     SimDev Sv = S;
-    void* args[] = {(void*)&B.rec_in, (void*)&B.perm, (void*)&B.block_start, (void*)&B.active_list, (void*)&B.dc,
-                    (void*)&B.block_slot, (void*)&B.mp, (void*)&Sv};
+    void* args[] = {(void*)&B.rec_in, (void*)&B.perm,        (void*)&B.key, (void*)&B.block_start,
+                    (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot, (void*)&B.mp, (void*)&Sv};
     e = jit_launch(J.p2g, J.p2g_ctas, J.p2g_threads, J.p2g_smem, st, args);
     H(KP2G, 0);
     if (e) return e;

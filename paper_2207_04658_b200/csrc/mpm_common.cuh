@@ -67,17 +67,22 @@ __device__ __forceinline__ uint32_t local_node(const int l[3]) {
   return (uint32_t)(l[0] * 8 + l[1]);
 }
 
-// block key of a particle from its (decoded) position
+// sort key of a particle from its (decoded) position: block id * 64 + the base cell's
+// index inside its block (x-major).  Binning sorts by block (key >> 6); P2G orders a
+// block's particles by (rank within cell, cell) so that a warp's lanes have distinct
+// base cells.
 template <int D>
 __device__ __forceinline__ uint32_t key_of(const float* x, const SimDev& S) {
-  int c[3] = {0, 0, 0};
+  int c[3] = {0, 0, 0}, l[3] = {0, 0, 0};
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     float fx;
     bool o;
-    c[a] = base_fx(x[a], S.inv_dx, S.res[a], fx, o) >> Geo<D>::LB;
+    const int b = base_fx(x[a], S.inv_dx, S.res[a], fx, o);
+    c[a] = b >> Geo<D>::LB;
+    l[a] = b & (Geo<D>::B - 1);
   }
-  return block_id<D>(c, S);
+  return (block_id<D>(c, S) << 6) | local_node<D>(l);
 }
 
 // tile node t -> (global node coordinates) for a block with origin org

@@ -175,16 +175,90 @@ __device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec,
     float x[3];
 #pragma unroll
     for (int a = 0; a < D; ++a) x[a] = sdec<SP>(w, a);
-    k = key_of<D>(x, S);
-    key[i] = k;
+    const uint32_t full = key_of<D>(x, S);
+    key[i] = full;
+    k = full >> 6;
   }
   const unsigned peers = __match_any_sync(FULL, k);
   if (valid && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
 }
 
+// ------------------------------------------------------------------ cell ordering
+// Within a block, particles are processed in (rank within base cell, cell) order:
+// position = P[r] + #{cells c' < c holding more than r particles}, P[r] = number of
+// particles of rank < r.  Consecutive lanes then have distinct base cells (except
+// across a level boundary, which the match_any rounds below absorb), so the
+// per-warp tile RMW of one stencil offset never collides.
+constexpr int kOrderCap = 1024;   // particles ordered per batch
+constexpr int kOrderLevels = 128; // ranks with a level mask (higher ranks go last)
+
+struct OrderSmem {
+  uint32_t p[kOrderCap];           // perm entries of the batch
+  uint32_t q[kOrderCap];           // reordered
+  uint16_t rank[kOrderCap];
+  uint8_t cell[kOrderCap];
+  unsigned cnt[64];
+  unsigned long long mask[kOrderLevels];
+  unsigned lvl[kOrderLevels + 1];  // exclusive prefix of level sizes
+  unsigned over;
+  unsigned maxc;
+};
+
+__device__ __forceinline__ void order_batch(uint32_t* __restrict__ perm, const uint32_t* __restrict__ key,
+                                            uint32_t nb, OrderSmem& o) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid < 64) o.cnt[tid] = 0u;
+  if (tid == 0) {
+    o.over = 0u;
+    o.maxc = 0u;
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < nb; i += nt) {
+    const uint32_t p = perm[i];
+    const uint32_t c = __ldg(key + p) & 63u;
+    o.p[i] = p;
+    o.cell[i] = (uint8_t)c;
+    o.rank[i] = (uint16_t)atomicAdd(&o.cnt[c], 1u);
+  }
+  __syncthreads();
+  if (tid < 64) atomicMax(&o.maxc, o.cnt[tid]);
+  __syncthreads();
+  const unsigned levels = min(o.maxc, (unsigned)kOrderLevels);
+  if (tid < 64) {
+    const int lane = tid & 31, half = tid >> 5;
+    const unsigned c = o.cnt[tid];
+    for (unsigned r = 0; r < levels; ++r) {
+      const unsigned b = __ballot_sync(FULL, c > r);
+      if (lane == 0) reinterpret_cast<unsigned*>(&o.mask[r])[half] = b;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned acc = 0;
+    for (unsigned r = 0; r < levels; ++r) {
+      o.lvl[r] = acc;
+      acc += __popcll(o.mask[r]);
+    }
+    o.lvl[levels] = acc;
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < nb; i += nt) {
+    const unsigned r = o.rank[i], c = o.cell[i];
+    uint32_t pos;
+    if (r < levels)
+      pos = o.lvl[r] + (uint32_t)__popcll(o.mask[r] & ((1ull << c) - 1ull));
+    else
+      pos = o.lvl[levels] + atomicAdd(&o.over, 1u);
+    o.q[pos] = o.p[i];
+    perm[pos] = o.p[i];
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------ a3: P2G
 template <class SP>
-__device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const uint32_t* __restrict__ perm,
+__device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint32_t* __restrict__ perm,
+                                         const uint32_t* __restrict__ key,
                                          const uint32_t* __restrict__ block_start,
                                          const uint32_t* __restrict__ active_list,
                                          const DevCounters* __restrict__ dc,
@@ -198,6 +272,7 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float4* tile = tiles + warp * G::TN;
   uint32_t* wst = stage + warp * 32 * SP::SW;
+  __shared__ OrderSmem ord;
   const uint32_t n_active = dc->n_active;
 
   for (uint32_t ab = blockIdx.x; ab < n_active; ab += gridDim.x) {
@@ -207,12 +282,14 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     block_coords<D>(b, S, bc);
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
     for (int t = threadIdx.x; t < WARPS * G::TN; t += blockDim.x) tiles[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncthreads();
 
-    for (uint32_t j0 = start + warp * 32; j0 < end; j0 += WARPS * 32) {
-      const uint32_t cnt = min(32u, end - j0);
+    for (uint32_t bs = start; bs < end; bs += kOrderCap) {
+    const uint32_t nb = min((uint32_t)kOrderCap, end - bs);
+    order_batch(perm + bs, key, nb, ord);  // (rank in cell, cell) order; perm rewritten
+    for (uint32_t j0 = warp * 32; j0 < nb; j0 += WARPS * 32) {
+      const uint32_t cnt = min(32u, nb - j0);
       const bool valid = (uint32_t)lane < cnt;
-      const uint32_t r = perm[j0 + (valid ? lane : 0)];
+      const uint32_t r = ord.q[j0 + (valid ? lane : 0)];
       uint32_t w[SP::W + 1];
       load_records<SP>(rec, r, cnt, wst, lane, w);
       float s[NSV];
@@ -290,7 +367,8 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
         __syncwarp();
       }
     }
-    __syncthreads();
+    __syncthreads();  // the batch's order arrays are reused by the next batch
+    }
     // flush: sum the warp tiles, one vector reduction per non-empty node
     for (int t = threadIdx.x; t < G::TN; t += blockDim.x) {
       float4 acc = tiles[t];
@@ -512,8 +590,9 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       float xq[3];
 #pragma unroll
       for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
-      const uint32_t nk = valid ? key_of<D>(xq, S) : 0xffffffffu;
-      if (valid) key_out[j] = nk;
+      const uint32_t nkey = key_of<D>(xq, S);
+      if (valid) key_out[j] = nkey;
+      const uint32_t nk = valid ? (nkey >> 6) : 0xffffffffu;
       const unsigned kp = __match_any_sync(FULL, nk);
       if (valid && lane == __ffs(kp) - 1) atomicAdd(&block_count[nk], (unsigned)__popc(kp));
       if (ids_out != nullptr && valid) ids_out[j] = ids_in[r];
@@ -542,13 +621,14 @@ extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t*
   qmpm::bin_count_body<Spec>(rec, n, S, key, block_count);
 }
 
-extern "C" __global__ void __launch_bounds__(Spec::P2G_WARPS * 32)
-    qmpm_p2g(const uint32_t* rec, const uint32_t* perm, const uint32_t* block_start, const uint32_t* active_list,
-             const qmpm::DevCounters* dc, const uint32_t* block_slot, float4* mp, qmpm::SimDev S) {
-  qmpm::p2g_body<Spec>(rec, perm, block_start, active_list, dc, block_slot, mp, S);
+extern "C" __global__ void __launch_bounds__(Spec::P2G_WARPS * 32, Spec::P2G_MINB)
+    qmpm_p2g(const uint32_t* rec, uint32_t* perm, const uint32_t* key, const uint32_t* block_start,
+             const uint32_t* active_list, const qmpm::DevCounters* dc, const uint32_t* block_slot, float4* mp,
+             qmpm::SimDev S) {
+  qmpm::p2g_body<Spec>(rec, perm, key, block_start, active_list, dc, block_slot, mp, S);
 }
 
-extern "C" __global__ void __launch_bounds__(Spec::G2P_WARPS * 32)
+extern "C" __global__ void __launch_bounds__(Spec::G2P_WARPS * 32, Spec::G2P_MINB)
     qmpm_g2p(const uint32_t* rec_in, uint32_t* rec_out, const uint32_t* perm, const uint32_t* ids_in,
              uint32_t* ids_out, float* dbg, uint32_t* key_out, uint32_t* block_count, const uint32_t* block_start,
              const uint32_t* active_list, qmpm::DevCounters* dc, const uint32_t* block_slot, const float4* gv,
