@@ -458,7 +458,6 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
       return (v && *v) ? atoi(v) : dflt;
     };
     const int kP2GMinBlocks = env_int("QMPM_P2G_MINB", 3), kG2PMinBlocks = env_int("QMPM_G2P_MINB", 4);
-    const int TN = d == 3 ? 216 : 100;
     ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps, kP2GMinBlocks, kG2PMinBlocks);
     JitModule m;
     std::string jerr;
@@ -476,8 +475,8 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
     cudaDeviceGetAttribute(&J.num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
     J.p2g_threads = kP2GWarps * 32;
     J.g2p_threads = kG2PWarps * 32;
-    J.p2g_smem = sizeof(float4) * kP2GWarps * TN + sizeof(uint32_t) * kP2GWarps * 32 * L.SW;
-    J.g2p_smem = sizeof(float4) * TN + sizeof(uint32_t) * kG2PWarps * 32 * L.SW;
+    J.p2g_smem = (size_t)m.smem_warp_p2g * kP2GWarps;
+    J.g2p_smem = (size_t)m.smem_warp_g2p * kG2PWarps;
     e = jit_set_smem(J.p2g, J.p2g_smem);
     if (!e) e = jit_set_smem(J.g2p, J.g2p_smem);
     if (e) {

@@ -114,26 +114,25 @@ __device__ __forceinline__ uint32_t content_key(const uint32_t* w) {
 
 // ------------------------------------------------------------------ staging
 // Warp-cooperative load of the warp's cnt records (record index of lane l in r_lane)
-// into registers w[0..W] of their owner lane, through rows of a shared-memory stage.
-// All W loads of a lane are issued before any is consumed.
+// into registers w[0..W] of their owner lane.  The words go global -> shared with
+// cp.async (LDGSTS: no registers held while the W loads are in flight), then each
+// lane reads its own conflict-free (odd-stride) row.
 template <class SP>
 __device__ __forceinline__ void load_records(const uint32_t* __restrict__ rec, uint32_t r_lane, uint32_t cnt,
                                              uint32_t* wst, int lane, uint32_t* w) {
   constexpr int W = SP::W, SW = SP::SW;
-  uint32_t v[W];
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(wst);
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     const uint32_t q = (uint32_t)(k * 32 + lane);
     const uint32_t l = q / W, o = q - l * W;
     const uint32_t r = __shfl_sync(FULL, r_lane, (int)(l & 31u));
-    v[k] = (l < cnt) ? __ldg(rec + (size_t)r * W + o) : 0u;
+    if (l < cnt) {
+      const unsigned sa = sbase + 4u * (l * SW + o);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(rec + (size_t)r * W + o) : "memory");
+    }
   }
-#pragma unroll
-  for (int k = 0; k < W; ++k) {
-    const uint32_t q = (uint32_t)(k * 32 + lane);
-    const uint32_t l = q / W, o = q - l * W;
-    wst[l * SW + o] = v[k];
-  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < W; ++k) w[k] = wst[lane * SW + k];
@@ -254,6 +253,17 @@ __device__ __forceinline__ void order_batch(uint32_t* __restrict__ perm, const u
   }
   __syncthreads();
 }
+
+// per-warp shared-memory footprint of the two step kernels (16-byte multiples)
+template <class SP>
+struct Smem {
+  static constexpr int TN = Geo<SP::D>::TN;
+  static constexpr int TILE = 16 * TN;
+  static constexpr int STAGE = ((4 * 32 * SP::SW) + 15) / 16 * 16;
+  static constexpr int PRM = 4 * 16 * 32;
+    static constexpr int P2G_WARP = TILE + STAGE + PRM;  // + the CTA's OrderSmem (static)
+  static constexpr int G2P_WARP = TILE + STAGE + 32;  // + 8 neighbour slots
+};
 
 // ------------------------------------------------------------------ a3: P2G
 template <class SP>
@@ -398,6 +408,8 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
 }
 
 // ------------------------------------------------------------------ a5-a7: G2P + encode
+// One WARP per active block: stage the block's (B+2)^d velocity tile, then gather,
+// update, dither + pack in registers, store in sorted order, emit next step's key.
 template <class SP>
 __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, uint32_t* __restrict__ rec_out,
                                          const uint32_t* __restrict__ perm, const uint32_t* __restrict__ ids_in,
@@ -410,44 +422,50 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
   constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, WARPS = SP::G2P_WARPS, W = SP::W;
   constexpr int CO = 2 * D + (MAT == 1 ? 1 : D * D);
   using G = Geo<D>;
+  using SM = Smem<SP>;
   extern __shared__ float4 smem4[];
-  float4* tile = smem4;                                         // [TN]
-  uint32_t* stage = reinterpret_cast<uint32_t*>(tile + G::TN);  // [WARPS][32][SW]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* wst = stage + warp * 32 * SP::SW;
+  char* wbase = reinterpret_cast<char*>(smem4) + warp * SM::G2P_WARP;
+  float4* tile = reinterpret_cast<float4*>(wbase);
+  uint32_t* wst = reinterpret_cast<uint32_t*>(wbase + SM::TILE);
+  uint32_t* nslot = reinterpret_cast<uint32_t*>(wbase + SM::TILE + SM::STAGE);  // [4] / [8] neighbour slots
   // per-lane counters: lane f accumulates field-scalar f's round-ups / downs / saturations
   unsigned c_up = 0, c_down = 0, c_sat = 0, c_nf = 0, c_oob = 0;
   const uint32_t n_active = dc->n_active;
   const float four_inv_dx = 4.0f * S.inv_dx;
 
-  for (uint32_t ab = blockIdx.x; ab < n_active; ab += gridDim.x) {
+  for (uint32_t ab = blockIdx.x * WARPS + warp; ab < n_active; ab += gridDim.x * WARPS) {
     const uint32_t b = active_list[ab];
     const uint32_t start = block_start[b], end = block_start[b + 1];
     int bc[3];
     block_coords<D>(b, S, bc);
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
-    __syncthreads();  // previous tile fully consumed
-    for (int t = threadIdx.x; t < G::TN; t += blockDim.x) {
+    // slots of the block and its +x/+y(/+z) neighbours, then the velocity tile
+    if (lane < (1 << D)) {
+      int nbk[3] = {bc[0] + (lane & 1), bc[1] + ((lane >> 1) & 1), D == 3 ? bc[2] + ((lane >> 2) & 1) : 0};
+      uint32_t sl = 0xffffffffu;
+      if (nbk[0] < S.nb[0] && nbk[1] < S.nb[1] && nbk[2] < S.nb[2]) sl = block_slot[block_id<D>(nbk, S)];
+      nslot[lane] = sl;
+    }
+    __syncwarp();
+    for (int t = lane; t < G::TN; t += 32) {
       int node[3];
       tile_node<D>(t, org, node);
-      int nb[3], ln[3];
-      bool inside = true;
+      int sel = 0, ln[3] = {0, 0, 0};
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        if (a < D && node[a] >= S.res[a]) inside = false;
-        nb[a] = node[a] >> G::LB;
+      for (int a = 0; a < D; ++a) {
+        const int hi = (node[a] - org[a]) >= G::B;
+        sel |= hi << a;
         ln[a] = node[a] & (G::B - 1);
       }
+      const uint32_t slot = nslot[sel];
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (inside) {
-        const uint32_t slot = block_slot[block_id<D>(nb, S)];
-        if (slot != 0xffffffffu) v = gv[(size_t)slot * 64 + local_node<D>(ln)];
-      }
+      if (slot != 0xffffffffu) v = gv[(size_t)slot * 64 + local_node<D>(ln)];
       tile[t] = v;
     }
-    __syncthreads();
+    __syncwarp();
 
-    for (uint32_t j0 = start + warp * 32; j0 < end; j0 += WARPS * 32) {
+    for (uint32_t j0 = start; j0 < end; j0 += 32) {
       const uint32_t cnt = min(32u, end - j0);
       const bool valid = (uint32_t)lane < cnt;
       const uint32_t r = perm[j0 + (valid ? lane : 0)];
@@ -586,7 +604,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         const unsigned bo = __ballot_sync(FULL, valid && oob_any);
         if (lane == 0) c_oob += __popc(bo);
       }
-      // next step's block key from the re-decoded (quantized) x
+      // next step's sort key from the re-decoded (quantized) x
       float xq[3];
 #pragma unroll
       for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
@@ -598,6 +616,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       if (ids_out != nullptr && valid) ids_out[j] = ids_in[r];
       store_records<SP>(rec_out + (size_t)j0 * W, cnt, wst, lane, ow);
     }
+    __syncwarp();
   }
   // flush this thread's counters (lane i holds scalar i's counts)
   if (lane < NSV) {
@@ -616,6 +635,9 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
 }  // namespace qmpm
 
 // ------------------------------------------------------------------ entry points
+// per-warp shared-memory bytes of P2G and G2P, read by the host after loading the module
+extern "C" __device__ const unsigned qmpm_smem_per_warp[2] = {(unsigned)qmpm::Smem<Spec>::P2G_WARP,
+                                                             (unsigned)qmpm::Smem<Spec>::G2P_WARP};
 extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t* rec, uint32_t n, qmpm::SimDev S,
                                                                  uint32_t* key, uint32_t* block_count) {
   qmpm::bin_count_body<Spec>(rec, n, S, key, block_count);
