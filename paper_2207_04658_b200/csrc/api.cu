@@ -49,6 +49,7 @@ struct qmpm_ctx {
   uint32_t* ids[2] = {nullptr, nullptr};
   uint32_t* key = nullptr;
   uint32_t* perm = nullptr;
+  uint8_t* cells = nullptr;
   uint32_t *block_count = nullptr, *block_start = nullptr, *block_slot = nullptr;
   uint32_t *active_list = nullptr, *touched_list = nullptr;
   uint4 *tile_sums = nullptr, *tile_off = nullptr;
@@ -222,7 +223,7 @@ qmpm_status copy_in(qmpm_ctx* ctx, void* dst, const void* src, size_t bytes) {
 qmpm_status rebin(qmpm_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->block_count, 0, sizeof(uint32_t) * ctx->S.nblocks, ctx->stream));
   hook_fn(ctx, KBinCount, 1);
-  CK(launch_bin_count(ctx->rec[ctx->cur], (uint32_t)ctx->n, ctx->S, ctx->key, ctx->block_count, ctx->jit,
+  CK(launch_bin_count(ctx->rec[ctx->cur], 0u, (uint32_t)ctx->n, ctx->S, ctx->key, ctx->block_count, 1, ctx->jit,
                       ctx->stream));
   hook_fn(ctx, KBinCount, 0);
   ctx->binned = true;
@@ -288,7 +289,7 @@ qmpm_status qmpm_layout(const qmpm_scheme* scheme, uint32_t* words_per_particle,
 qmpm_status qmpm_destroy(qmpm_ctx* ctx) {
   if (!ctx) return QMPM_OK;
   cudaStreamSynchronize(ctx->stream);
-  void* ptrs[] = {ctx->rec[0], ctx->rec[1], ctx->ids[0], ctx->ids[1], ctx->key, ctx->perm,
+  void* ptrs[] = {ctx->rec[0], ctx->rec[1], ctx->ids[0], ctx->ids[1], ctx->key, ctx->perm, ctx->cells,
                   ctx->block_count, ctx->block_start, ctx->block_slot, ctx->active_list, ctx->touched_list,
                   ctx->tile_sums, ctx->tile_off, ctx->mp, ctx->gv, ctx->dc, ctx->dbg};
   for (void* p : ptrs)
@@ -426,6 +427,7 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   }
   ALLOC(ctx->key, sizeof(uint32_t) * cap);
   ALLOC(ctx->perm, sizeof(uint32_t) * cap);
+  ALLOC(ctx->cells, cap);
   ALLOC(ctx->block_count, sizeof(uint32_t) * nblocks);
   ALLOC(ctx->block_start, sizeof(uint32_t) * (nblocks + 1));
   ALLOC(ctx->block_slot, sizeof(uint32_t) * nblocks);
@@ -556,6 +558,7 @@ qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps) {
     B.ids_out = ctx->ids[ctx->cur ^ 1];
     B.key = ctx->key;
     B.perm = ctx->perm;
+    B.cells = ctx->cells;
     B.block_count = ctx->block_count;
     B.block_start = ctx->block_start;
     B.block_slot = ctx->block_slot;

@@ -31,6 +31,8 @@ __device__ __forceinline__ void block_flags(uint32_t b, const uint32_t* __restri
   touched = act;
   int bc[3];
   block_coords<D>(b, S, bc);
+  // a slab's bottom block plane receives the lower neighbour's ghost contributions
+  if (D == 3 && S.slab_lo && bc[2] == S.slab_bz0) touched = 1;
 #pragma unroll
   for (int dl = 1; dl < (1 << D); ++dl) {
     int nc[3] = {bc[0] - (dl & 1), bc[1] - ((dl >> 1) & 1), D == 3 ? bc[2] - ((dl >> 2) & 1) : 0};
@@ -129,6 +131,7 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const uint4* __restrict__ t
     dc->n_active = total.y;
     dc->n_touched = total.z;
     dc->n_touched_eff = total.z < pool ? total.z : pool;
+    dc->n_sorted = total.x;
     if (total.z > pool) dc->overflow += 1ull;
     block_start[nblocks] = total.x;
   }
@@ -179,17 +182,23 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __r
 
 __global__ void k_bin_scatter(const uint32_t* __restrict__ key, uint32_t n,
                               const uint32_t* __restrict__ block_start, uint32_t* __restrict__ block_count,
-                              uint32_t* __restrict__ perm) {
+                              uint32_t* __restrict__ perm, uint8_t* __restrict__ cells) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < n;
-  const uint32_t k = valid ? (key[i] >> 6) : 0xffffffffu;  // block of the sort key
+  const uint32_t full = valid ? key[i] : kDeadKey;
+  const bool live = full != kDeadKey;
+  const uint32_t k = live ? (full >> 6) : 0xffffffffu;  // block of the sort key
   const unsigned peers = __match_any_sync(FULL, k);
   const int leader = __ffs(peers) - 1;
   const int rank = __popc(peers & lanemask_lt());
   uint32_t old = 0;
-  if (valid && (int)(threadIdx.x & 31) == leader) old = atomicSub(&block_count[k], (uint32_t)__popc(peers));
+  if (live && (int)(threadIdx.x & 31) == leader) old = atomicSub(&block_count[k], (uint32_t)__popc(peers));
   old = __shfl_sync(FULL, old, leader);
-  if (valid) perm[block_start[k] + old - 1 - rank] = i;
+  if (live) {
+    const uint32_t pos = block_start[k] + old - 1 - rank;
+    perm[pos] = i;
+    cells[pos] = (uint8_t)(full & 63u);  // base cell in the block, for P2G's ordering
+  }
 }
 
 // ============================================================== a4: grid update
@@ -227,6 +236,90 @@ __global__ void k_grid_update(float4* __restrict__ mp, float4* __restrict__ gv,
     }
     gv[t] = o;
     mp[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// ============================================================== slab exchange (a8)
+// Particles of the sorted ranges [0, lo_end) (below the slab) and [hi_begin, n_sorted)
+// (above it) left this rank: copy their records (and ids) into the send buffers.
+__global__ void k_pack_leavers(const uint32_t* __restrict__ rec, const uint32_t* __restrict__ ids,
+                               const uint32_t* __restrict__ perm, const uint32_t* __restrict__ block_start,
+                               uint32_t lo_block, uint32_t hi_block, uint32_t nblocks, uint32_t W,
+                               uint32_t cap, uint32_t* __restrict__ send_dn, uint32_t* __restrict__ send_up,
+                               uint32_t* __restrict__ ids_dn, uint32_t* __restrict__ ids_up, DevCounters* dc) {
+  const uint32_t lo_end = block_start[lo_block], hi_begin = block_start[hi_block], n = block_start[nblocks];
+  const uint32_t n_up = n - hi_begin;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    dc->mig_dn = lo_end;
+    dc->mig_up = n_up;
+    dc->n_sorted = n;
+    if (lo_end > cap || n_up > cap) dc->mig_overflow += 1u;
+  }
+  const uint32_t total = min(lo_end, cap) + min(n_up, cap);
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total * W; t += gridDim.x * blockDim.x) {
+    const uint32_t q = t / W, w = t - q * W;
+    const bool dn = q < min(lo_end, cap);
+    const uint32_t slot = dn ? q : q - min(lo_end, cap);
+    const uint32_t src = perm[dn ? slot : hi_begin + slot];
+    (dn ? send_dn : send_up)[(size_t)slot * W + w] = rec[(size_t)src * W + w];
+    if (w == 0 && ids) (dn ? ids_dn : ids_up)[slot] = ids[src];
+  }
+}
+
+// Count the particles this rank owns (block inside the slab) for the second sort;
+// keys of the others become kDeadKey so the scatter drops them.
+template <int D>
+__global__ void k_recount(uint32_t* __restrict__ key, uint32_t n, SimDev S, uint32_t* __restrict__ block_count) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t k = 0xffffffffu;
+  if (i < n) {
+    const uint32_t full = key[i];
+    if (full != kDeadKey) {
+      int bc[3];
+      block_coords<D>(full >> 6, S, bc);
+      if (bc[2] >= S.slab_bz0 && bc[2] < S.slab_bz1) {
+        k = full >> 6;
+      } else {
+        key[i] = kDeadKey;
+      }
+    }
+  }
+  const unsigned peers = __match_any_sync(FULL, k);
+  if (k != 0xffffffffu && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
+}
+
+// Dense copy of one z block plane of a float4 node array (all nbx * nby blocks,
+// 64 nodes each; blocks without a pool slot read as zero).
+__global__ void k_plane_pack(const float4* __restrict__ src, const uint32_t* __restrict__ block_slot, SimDev S,
+                             int bz, float4* __restrict__ buf) {
+  const uint32_t P = (uint32_t)S.nb[0] * (uint32_t)S.nb[1];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < P * 64u; t += gridDim.x * blockDim.x) {
+    const uint32_t pb = t >> 6;
+    const int c[3] = {(int)(pb / (uint32_t)S.nb[1]), (int)(pb % (uint32_t)S.nb[1]), bz};
+    const uint32_t slot = block_slot[block_id<3>(c, S)];
+    buf[t] = slot != 0xffffffffu ? src[(size_t)slot * 64 + (t & 63u)] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// add (halo reduce of P2G partial sums) or store (velocity halo) a packed plane
+__global__ void k_plane_unpack(float4* __restrict__ dst, const uint32_t* __restrict__ block_slot, SimDev S, int bz,
+                               const float4* __restrict__ buf, int add) {
+  const uint32_t P = (uint32_t)S.nb[0] * (uint32_t)S.nb[1];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < P * 64u; t += gridDim.x * blockDim.x) {
+    const uint32_t pb = t >> 6;
+    const int c[3] = {(int)(pb / (uint32_t)S.nb[1]), (int)(pb % (uint32_t)S.nb[1]), bz};
+    const uint32_t slot = block_slot[block_id<3>(c, S)];
+    if (slot == 0xffffffffu) continue;
+    const float4 v = buf[t];
+    float4& d = dst[(size_t)slot * 64 + (t & 63u)];
+    if (add) {
+      d.x += v.x;
+      d.y += v.y;
+      d.z += v.z;
+      d.w += v.w;
+    } else {
+      d = v;
+    }
   }
 }
 
@@ -303,12 +396,18 @@ __global__ void k_iota(uint32_t* ids, uint32_t n, uint32_t first) {
 }
 
 // ============================================================== launchers
-template <int D>
-static cudaError_t step_d(const StepBuffers& B, const SimDev& S, uint32_t salt, const StepJit& J, cudaStream_t st,
-                          KernelHook hook, void* user) {
-  auto H = [&](int k, int b) {
+namespace {
+struct Hk {
+  KernelHook hook;
+  void* user;
+  void operator()(int k, int b) const {
     if (hook) hook(user, k, b);
-  };
+  }
+};
+}  // namespace
+
+template <int D>
+static cudaError_t sort_d(const StepBuffers& B, const SimDev& S, cudaStream_t st, Hk H) {
   H(KScanReduce, 1);
   k_scan_reduce<D><<<B.ntiles, kScanThreads, 0, st>>>(B.block_count, S, B.tile_sums);
   H(KScanReduce, 0);
@@ -319,53 +418,98 @@ static cudaError_t step_d(const StepBuffers& B, const SimDev& S, uint32_t salt, 
   k_scan_apply<D><<<B.ntiles, kScanThreads, 0, st>>>(B.block_count, S, B.tile_off, B.block_start, B.block_slot,
                                                      B.active_list, B.touched_list, B.pool);
   H(KScanApply, 0);
-  cudaError_t e = cudaGetLastError();
-  if (e) return e;
   if (B.n) {
     H(KBinScatter, 1);
-    k_bin_scatter<<<(B.n + 255) / 256, 256, 0, st>>>(B.key, B.n, B.block_start, B.block_count, B.perm);
+    k_bin_scatter<<<(B.n + 255) / 256, 256, 0, st>>>(B.key, B.n, B.block_start, B.block_count, B.perm, B.cells);
     H(KBinScatter, 0);
   }
-  {
-    H(KP2G, 1);
-    SimDev Sv = S;
-    void* args[] = {(void*)&B.rec_in, (void*)&B.perm,        (void*)&B.key, (void*)&B.block_start,
-                    (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot, (void*)&B.mp, (void*)&Sv};
-    e = jit_launch(J.p2g, J.p2g_ctas, J.p2g_threads, J.p2g_smem, st, args);
-    H(KP2G, 0);
-    if (e) return e;
-  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sort(int dim, const StepBuffers& B, const SimDev& S, cudaStream_t st, KernelHook hook, void* user) {
+  return dim == 3 ? sort_d<3>(B, S, st, Hk{hook, user}) : sort_d<2>(B, S, st, Hk{hook, user});
+}
+
+cudaError_t launch_p2g(const StepBuffers& B, const SimDev& S, const StepJit& J, cudaStream_t st, KernelHook hook,
+                       void* user) {
+  Hk H{hook, user};
+  H(KP2G, 1);
+  SimDev Sv = S;
+  void* args[] = {(void*)&B.rec_in, (void*)&B.perm,        (void*)&B.cells, (void*)&B.block_start,
+                  (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot, (void*)&B.mp, (void*)&Sv};
+  cudaError_t e = jit_launch(J.p2g, J.p2g_ctas, J.p2g_threads, J.p2g_smem, st, args);
+  H(KP2G, 0);
+  return e;
+}
+
+cudaError_t launch_grid_update(int dim, const StepBuffers& B, const SimDev& S, const StepJit& J, cudaStream_t st,
+                               KernelHook hook, void* user) {
+  Hk H{hook, user};
   H(KGridUpdate, 1);
-  k_grid_update<D><<<J.num_sms * 8, 256, 0, st>>>(B.mp, B.gv, B.touched_list, B.dc, S);
+  if (dim == 3)
+    k_grid_update<3><<<J.num_sms * 8, 256, 0, st>>>(B.mp, B.gv, B.touched_list, B.dc, S);
+  else
+    k_grid_update<2><<<J.num_sms * 8, 256, 0, st>>>(B.mp, B.gv, B.touched_list, B.dc, S);
   H(KGridUpdate, 0);
-  e = cudaGetLastError();
-  if (e) return e;
-  {
-    H(KG2P, 1);
-    SimDev Sv = S;
-    uint32_t saltv = salt;
-    void* args[] = {(void*)&B.rec_in, (void*)&B.rec_out, (void*)&B.perm, (void*)&B.ids_in, (void*)&B.ids_out,
-                    (void*)&B.dbg, (void*)&B.key, (void*)&B.block_count, (void*)&B.block_start,
-                    (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot, (void*)&B.gv, (void*)&Sv,
-                    (void*)&saltv};
-    e = jit_launch(J.g2p, J.g2p_ctas, J.g2p_threads, J.g2p_smem, st, args);
-    H(KG2P, 0);
-    if (e) return e;
-  }
-  return cudaSuccess;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_g2p(const StepBuffers& B, const SimDev& S, uint32_t salt, const StepJit& J, cudaStream_t st,
+                       KernelHook hook, void* user) {
+  Hk H{hook, user};
+  H(KG2P, 1);
+  SimDev Sv = S;
+  uint32_t saltv = salt;
+  void* args[] = {(void*)&B.rec_in, (void*)&B.rec_out, (void*)&B.perm, (void*)&B.ids_in, (void*)&B.ids_out,
+                  (void*)&B.dbg, (void*)&B.key, (void*)&B.block_count, (void*)&B.block_start,
+                  (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot, (void*)&B.gv, (void*)&Sv,
+                  (void*)&saltv};
+  cudaError_t e = jit_launch(J.g2p, J.g2p_ctas, J.g2p_threads, J.g2p_smem, st, args);
+  H(KG2P, 0);
+  return e;
 }
 
 cudaError_t launch_step(int dim, const StepBuffers& B, const SimDev& S, uint32_t salt, const StepJit& J,
                         cudaStream_t st, KernelHook hook, void* user) {
-  return dim == 3 ? step_d<3>(B, S, salt, J, st, hook, user) : step_d<2>(B, S, salt, J, st, hook, user);
+  cudaError_t e = launch_sort(dim, B, S, st, hook, user);
+  if (!e) e = launch_p2g(B, S, J, st, hook, user);
+  if (!e) e = launch_grid_update(dim, B, S, J, st, hook, user);
+  if (!e) e = launch_g2p(B, S, salt, J, st, hook, user);
+  return e;
 }
 
-cudaError_t launch_bin_count(const uint32_t* rec, uint32_t n, const SimDev& S, uint32_t* key, uint32_t* block_count,
-                             const StepJit& J, cudaStream_t st) {
+cudaError_t launch_bin_count(const uint32_t* rec, uint32_t first, uint32_t n, const SimDev& S, uint32_t* key,
+                             uint32_t* block_count, int do_count, const StepJit& J, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   SimDev Sv = S;
-  void* args[] = {(void*)&rec, (void*)&n, (void*)&Sv, (void*)&key, (void*)&block_count};
+  void* args[] = {(void*)&rec, (void*)&first, (void*)&n, (void*)&Sv, (void*)&key, (void*)&block_count,
+                  (void*)&do_count};
   return jit_launch(J.bin_count, (n + 255) / 256, 256, 0, st, args);
+}
+
+cudaError_t launch_pack_leavers(const StepBuffers& B, const SimDev& S, uint32_t W, uint32_t cap, uint32_t* send_dn,
+                                uint32_t* send_up, uint32_t* ids_dn, uint32_t* ids_up, int num_sms,
+                                cudaStream_t st) {
+  const uint32_t P = (uint32_t)S.nb[0] * (uint32_t)S.nb[1];
+  k_pack_leavers<<<num_sms * 4, 256, 0, st>>>(B.rec_in, B.ids_in, B.perm, B.block_start, (uint32_t)S.slab_bz0 * P,
+                                               (uint32_t)S.slab_bz1 * P, S.nblocks, W, cap, send_dn, send_up, ids_dn,
+                                               ids_up, B.dc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_recount(const StepBuffers& B, const SimDev& S, uint32_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_recount<3><<<(n + 255) / 256, 256, 0, st>>>(B.key, n, S, B.block_count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plane(float4* nodes, const uint32_t* block_slot, const SimDev& S, int bz, float4* buf, int mode,
+                         int num_sms, cudaStream_t st) {
+  if (mode == 0)
+    k_plane_pack<<<num_sms * 4, 256, 0, st>>>(nodes, block_slot, S, bz, buf);
+  else
+    k_plane_unpack<<<num_sms * 4, 256, 0, st>>>(nodes, block_slot, S, bz, buf, mode == 1);
+  return cudaGetLastError();
 }
 
 static size_t codec_smem(const CodecDev& C) {

@@ -40,13 +40,17 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// Block ids are z-major in 3D, id = (bz * nbx + bx) * nby + by (y-major in 2D), so a
+// slab of z block planes [bz0, bz1) is the contiguous id range [bz0 P, bz1 P),
+// P = nbx * nby: after the counting sort, particles that left a rank's slab are the
+// sorted ranges below and above it.
 template <int D>
 __device__ __forceinline__ void block_coords(uint32_t b, const SimDev& S, int bc[3]) {
   if (D == 3) {
-    bc[2] = (int)(b % (uint32_t)S.nb[2]);
-    const uint32_t r = b / (uint32_t)S.nb[2];
-    bc[1] = (int)(r % (uint32_t)S.nb[1]);
-    bc[0] = (int)(r / (uint32_t)S.nb[1]);
+    bc[1] = (int)(b % (uint32_t)S.nb[1]);
+    const uint32_t r = b / (uint32_t)S.nb[1];
+    bc[0] = (int)(r % (uint32_t)S.nb[0]);
+    bc[2] = (int)(r / (uint32_t)S.nb[0]);
   } else {
     bc[1] = (int)(b % (uint32_t)S.nb[1]);
     bc[0] = (int)(b / (uint32_t)S.nb[1]);
@@ -56,7 +60,7 @@ __device__ __forceinline__ void block_coords(uint32_t b, const SimDev& S, int bc
 
 template <int D>
 __device__ __forceinline__ uint32_t block_id(const int c[3], const SimDev& S) {
-  if (D == 3) return ((uint32_t)c[0] * (uint32_t)S.nb[1] + (uint32_t)c[1]) * (uint32_t)S.nb[2] + (uint32_t)c[2];
+  if (D == 3) return ((uint32_t)c[2] * (uint32_t)S.nb[0] + (uint32_t)c[0]) * (uint32_t)S.nb[1] + (uint32_t)c[1];
   return (uint32_t)c[0] * (uint32_t)S.nb[1] + (uint32_t)c[1];
 }
 

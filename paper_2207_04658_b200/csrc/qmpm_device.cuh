@@ -67,7 +67,12 @@ struct SimDev {
   float E;            // fluid: P F^T = E (J - 1) I
   int bound;
   uint32_t nblocks;
+  // slab decomposition along z (3D): this rank owns block planes
+  // [slab_bz0, slab_bz1); slab_lo / slab_hi = a neighbour rank exists below / above
+  int slab_bz0, slab_bz1, slab_lo, slab_hi;
 };
+
+constexpr uint32_t kDeadKey = 0xffffffffu;  // sort key of a particle this rank does not own
 
 // Device-side counters (accumulated across steps until set_state).
 struct DevCounters {
@@ -77,6 +82,9 @@ struct DevCounters {
   unsigned long long nonfinite;
   unsigned long long oob;
   unsigned long long overflow;
+  unsigned int mig_dn, mig_up;  // particles that left the slab downwards / upwards (last step)
+  unsigned int mig_overflow;
+  unsigned int n_sorted;      // particles sorted in the last scan
   unsigned int n_active;      // last step
   unsigned int n_touched;     // last step (before clamping to the pool)
   unsigned int n_touched_eff; // min(n_touched, pool)

@@ -17,6 +17,7 @@ struct StepBuffers {
   uint32_t* ids_out;       // nullable
   uint32_t* key;           // [n] block key of each record in rec_in order (in), rec_out order (out)
   uint32_t* perm;          // [n] sorted slot -> rec_in index
+  uint8_t* cells;          // [n] base cell in its block, per sorted slot
   uint32_t* block_count;   // [nblocks]
   uint32_t* block_start;   // [nblocks + 1]
   uint32_t* block_slot;    // [nblocks]
@@ -59,10 +60,27 @@ struct StepJit {
 // one hook per kernel so the runtime can bracket launches with events
 typedef void (*KernelHook)(void* user, int kernel_id, int begin);
 
-cudaError_t launch_bin_count(const uint32_t* rec, uint32_t n, const SimDev& S, uint32_t* key, uint32_t* block_count,
-                             const StepJit& J, cudaStream_t st);
+// whole step (single GPU)
 cudaError_t launch_step(int dim, const StepBuffers& B, const SimDev& S, uint32_t salt, const StepJit& J,
                         cudaStream_t st, KernelHook hook, void* user);
+// the step's phases, for the slab decomposition (exchanges in between)
+cudaError_t launch_sort(int dim, const StepBuffers& B, const SimDev& S, cudaStream_t st, KernelHook hook, void* user);
+cudaError_t launch_p2g(const StepBuffers& B, const SimDev& S, const StepJit& J, cudaStream_t st, KernelHook hook,
+                       void* user);
+cudaError_t launch_grid_update(int dim, const StepBuffers& B, const SimDev& S, const StepJit& J, cudaStream_t st,
+                               KernelHook hook, void* user);
+cudaError_t launch_g2p(const StepBuffers& B, const SimDev& S, uint32_t salt, const StepJit& J, cudaStream_t st,
+                       KernelHook hook, void* user);
+// keys (+ optional histogram) of records [first, first + n)
+cudaError_t launch_bin_count(const uint32_t* rec, uint32_t first, uint32_t n, const SimDev& S, uint32_t* key,
+                             uint32_t* block_count, int do_count, const StepJit& J, cudaStream_t st);
+cudaError_t launch_pack_leavers(const StepBuffers& B, const SimDev& S, uint32_t W, uint32_t cap, uint32_t* send_dn,
+                                uint32_t* send_up, uint32_t* ids_dn, uint32_t* ids_up, int num_sms,
+                                cudaStream_t st);
+cudaError_t launch_recount(const StepBuffers& B, const SimDev& S, uint32_t n, cudaStream_t st);
+// mode 0: pack plane bz of `nodes` into buf; 1: add buf into the plane; 2: store buf into the plane
+cudaError_t launch_plane(float4* nodes, const uint32_t* block_slot, const SimDev& S, int bz, float4* buf, int mode,
+                         int num_sms, cudaStream_t st);
 
 cudaError_t launch_encode(const CodecDev& C, uint64_t n, const float* vals, const uint32_t* keys,
                           uint32_t salt, uint32_t* words, unsigned long long* counters,

@@ -116,10 +116,12 @@ __device__ __forceinline__ uint32_t content_key(const uint32_t* w) {
 // Warp-cooperative load of the warp's cnt records (record index of lane l in r_lane)
 // into registers w[0..W] of their owner lane.  The words go global -> shared with
 // cp.async (LDGSTS: no registers held while the W loads are in flight), then each
-// lane reads its own conflict-free (odd-stride) row.
+// lane reads its own conflict-free (odd-stride) row.  issue_records / take_records
+// split the two halves so the next chunk's records can be in flight while the
+// current chunk computes (double-buffered stage).
 template <class SP>
-__device__ __forceinline__ void load_records(const uint32_t* __restrict__ rec, uint32_t r_lane, uint32_t cnt,
-                                             uint32_t* wst, int lane, uint32_t* w) {
+__device__ __forceinline__ void issue_records(const uint32_t* __restrict__ rec, uint32_t r_lane, uint32_t cnt,
+                                              uint32_t* wst, int lane) {
   constexpr int W = SP::W, SW = SP::SW;
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(wst);
 #pragma unroll
@@ -132,12 +134,25 @@ __device__ __forceinline__ void load_records(const uint32_t* __restrict__ rec, u
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(rec + (size_t)r * W + o) : "memory");
     }
   }
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+template <class SP>
+__device__ __forceinline__ void take_records(const uint32_t* wst, int lane, uint32_t* w) {
+  constexpr int W = SP::W, SW = SP::SW;
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < W; ++k) w[k] = wst[lane * SW + k];
   w[W] = 0u;
   __syncwarp();
+}
+
+template <class SP>
+__device__ __forceinline__ void load_records(const uint32_t* __restrict__ rec, uint32_t r_lane, uint32_t cnt,
+                                             uint32_t* wst, int lane, uint32_t* w) {
+  issue_records<SP>(rec, r_lane, cnt, wst, lane);
+  take_records<SP>(wst, lane, w);
 }
 
 // coalesced store of the warp's cnt records (lane l holds record l in w) to out[0..cnt*W)
@@ -160,11 +175,12 @@ __device__ __forceinline__ void store_records(uint32_t* __restrict__ out, uint32
 
 // ------------------------------------------------------------------ a1: bin count
 template <class SP>
-__device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec, uint32_t n, const SimDev& S,
-                                               uint32_t* __restrict__ key, uint32_t* __restrict__ block_count) {
+__device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec, uint32_t first, uint32_t n,
+                                               const SimDev& S, uint32_t* __restrict__ key,
+                                               uint32_t* __restrict__ block_count, int do_count) {
   constexpr int D = SP::D, W = SP::W;
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = i < n;
+  const uint32_t i = first + blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < first + n;
   uint32_t k = 0xffffffffu;
   if (valid) {
     uint32_t w[W + 1];
@@ -178,6 +194,7 @@ __device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec,
     key[i] = full;
     k = full >> 6;
   }
+  if (!do_count) return;
   const unsigned peers = __match_any_sync(FULL, k);
   if (valid && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
 }
@@ -203,28 +220,37 @@ struct OrderSmem {
   unsigned maxc;
 };
 
-__device__ __forceinline__ void order_batch(uint32_t* __restrict__ perm, const uint32_t* __restrict__ key,
+__device__ __forceinline__ void order_batch(uint32_t* __restrict__ perm, const uint8_t* __restrict__ cells,
                                             uint32_t nb, OrderSmem& o) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
   if (tid < 64) o.cnt[tid] = 0u;
   if (tid == 0) {
     o.over = 0u;
     o.maxc = 0u;
   }
   __syncthreads();
-  for (uint32_t i = tid; i < nb; i += nt) {
-    const uint32_t p = perm[i];
-    const uint32_t c = __ldg(key + p) & 63u;
-    o.p[i] = p;
-    o.cell[i] = (uint8_t)c;
-    o.rank[i] = (uint16_t)atomicAdd(&o.cnt[c], 1u);
+  for (uint32_t i0 = tid - lane; i0 < nb; i0 += nt) {  // warp-uniform trip count
+    const uint32_t i = i0 + lane;
+    const bool v = i < nb;
+    const uint32_t p = v ? perm[i] : 0u;
+    const uint32_t c = v ? (uint32_t)cells[i] : 64u + lane;
+    const unsigned peers = __match_any_sync(FULL, c);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (v && lane == leader) base = atomicAdd(&o.cnt[c], (unsigned)__popc(peers));
+    base = __shfl_sync(FULL, base, leader);
+    if (v) {
+      o.p[i] = p;
+      o.cell[i] = (uint8_t)c;
+      o.rank[i] = (uint16_t)(base + __popc(peers & lanemask_lt()));
+    }
   }
   __syncthreads();
   if (tid < 64) atomicMax(&o.maxc, o.cnt[tid]);
   __syncthreads();
   const unsigned levels = min(o.maxc, (unsigned)kOrderLevels);
   if (tid < 64) {
-    const int lane = tid & 31, half = tid >> 5;
+    const int half = tid >> 5;
     const unsigned c = o.cnt[tid];
     for (unsigned r = 0; r < levels; ++r) {
       const unsigned b = __ballot_sync(FULL, c > r);
@@ -232,13 +258,21 @@ __device__ __forceinline__ void order_batch(uint32_t* __restrict__ perm, const u
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    unsigned acc = 0;
-    for (unsigned r = 0; r < levels; ++r) {
-      o.lvl[r] = acc;
-      acc += __popcll(o.mask[r]);
+  if (tid < 32) {  // level prefix, one warp
+    unsigned run = 0;
+    for (unsigned r0 = 0; r0 < levels; r0 += 32) {
+      const unsigned r = r0 + lane;
+      const unsigned sz = r < levels ? (unsigned)__popcll(o.mask[r]) : 0u;
+      unsigned inc = sz;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned t = __shfl_up_sync(FULL, inc, d);
+        if (lane >= d) inc += t;
+      }
+      if (r < levels) o.lvl[r] = run + inc - sz;
+      run += __shfl_sync(FULL, inc, 31);
     }
-    o.lvl[levels] = acc;
+    if (lane == 0) o.lvl[levels] = run;
   }
   __syncthreads();
   for (uint32_t i = tid; i < nb; i += nt) {
@@ -261,14 +295,14 @@ struct Smem {
   static constexpr int TILE = 16 * TN;
   static constexpr int STAGE = ((4 * 32 * SP::SW) + 15) / 16 * 16;
   static constexpr int PRM = 4 * 16 * 32;
-    static constexpr int P2G_WARP = TILE + STAGE + PRM;  // + the CTA's OrderSmem (static)
-  static constexpr int G2P_WARP = TILE + STAGE + 32;  // + 8 neighbour slots
+    static constexpr int P2G_WARP = TILE + 2 * STAGE;  // double-buffered stage; + the CTA's OrderSmem (static)
+  static constexpr int G2P_WARP = TILE + 2 * STAGE + 32;  // double-buffered stage + 8 neighbour slots
 };
 
 // ------------------------------------------------------------------ a3: P2G
 template <class SP>
 __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint32_t* __restrict__ perm,
-                                         const uint32_t* __restrict__ key,
+                                         const uint8_t* __restrict__ cells,
                                          const uint32_t* __restrict__ block_start,
                                          const uint32_t* __restrict__ active_list,
                                          const DevCounters* __restrict__ dc,
@@ -278,10 +312,10 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
   using G = Geo<D>;
   extern __shared__ float4 smem4[];
   float4* tiles = smem4;                                                  // [WARPS][TN]
-  uint32_t* stage = reinterpret_cast<uint32_t*>(tiles + WARPS * G::TN);  // [WARPS][32][SW]
+  uint32_t* stage = reinterpret_cast<uint32_t*>(tiles + WARPS * G::TN);  // [WARPS][2][32][SW]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float4* tile = tiles + warp * G::TN;
-  uint32_t* wst = stage + warp * 32 * SP::SW;
+  uint32_t* wst = stage + warp * 2 * 32 * SP::SW;
   __shared__ OrderSmem ord;
   const uint32_t n_active = dc->n_active;
 
@@ -295,13 +329,26 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
 
     for (uint32_t bs = start; bs < end; bs += kOrderCap) {
     const uint32_t nb = min((uint32_t)kOrderCap, end - bs);
-    order_batch(perm + bs, key, nb, ord);  // (rank in cell, cell) order; perm rewritten
+    order_batch(perm + bs, cells + bs, nb, ord);  // (rank in cell, cell) order; perm rewritten
+    int buf = 0;
+    if (warp * 32 < (int)nb) {  // prefetch this warp's first chunk
+      const uint32_t c0 = min(32u, nb - warp * 32);
+      issue_records<SP>(rec, ord.q[warp * 32 + ((uint32_t)lane < c0 ? lane : 0)], c0, wst, lane);
+    }
     for (uint32_t j0 = warp * 32; j0 < nb; j0 += WARPS * 32) {
       const uint32_t cnt = min(32u, nb - j0);
       const bool valid = (uint32_t)lane < cnt;
-      const uint32_t r = ord.q[j0 + (valid ? lane : 0)];
       uint32_t w[SP::W + 1];
-      load_records<SP>(rec, r, cnt, wst, lane, w);
+      take_records<SP>(wst + buf * 32 * SP::SW, lane, w);
+      {  // records of the next chunk go in flight while this one computes
+        const uint32_t jn = j0 + WARPS * 32;
+        if (jn < nb) {
+          const uint32_t cn = min(32u, nb - jn);
+          issue_records<SP>(rec, ord.q[jn + ((uint32_t)lane < cn ? lane : 0)], cn, wst + (buf ^ 1) * 32 * SP::SW,
+                            lane);
+        }
+        buf ^= 1;
+      }
       float s[NSV];
       if (valid) {
 #pragma unroll
@@ -428,7 +475,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
   char* wbase = reinterpret_cast<char*>(smem4) + warp * SM::G2P_WARP;
   float4* tile = reinterpret_cast<float4*>(wbase);
   uint32_t* wst = reinterpret_cast<uint32_t*>(wbase + SM::TILE);
-  uint32_t* nslot = reinterpret_cast<uint32_t*>(wbase + SM::TILE + SM::STAGE);  // [4] / [8] neighbour slots
+  uint32_t* nslot = reinterpret_cast<uint32_t*>(wbase + SM::TILE + 2 * SM::STAGE);  // [4] / [8] neighbour slots
   // per-lane counters: lane f accumulates field-scalar f's round-ups / downs / saturations
   unsigned c_up = 0, c_down = 0, c_sat = 0, c_nf = 0, c_oob = 0;
   const uint32_t n_active = dc->n_active;
@@ -465,12 +512,29 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
     }
     __syncwarp();
 
+    int buf = 0;
+    uint32_t r_next = 0;
+    if (start < end) {
+      const uint32_t c0 = min(32u, end - start);
+      r_next = perm[start + ((uint32_t)lane < c0 ? lane : 0)];
+      issue_records<SP>(rec_in, r_next, c0, wst, lane);
+    }
     for (uint32_t j0 = start; j0 < end; j0 += 32) {
       const uint32_t cnt = min(32u, end - j0);
       const bool valid = (uint32_t)lane < cnt;
-      const uint32_t r = perm[j0 + (valid ? lane : 0)];
+      const uint32_t r = r_next;
+      uint32_t* cur = wst + buf * 32 * SP::SW;
       uint32_t w[W + 1];
-      load_records<SP>(rec_in, r, cnt, wst, lane, w);
+      take_records<SP>(cur, lane, w);
+      {  // the next chunk's records go in flight while this one computes
+        const uint32_t jn = j0 + 32;
+        if (jn < end) {
+          const uint32_t cn = min(32u, end - jn);
+          r_next = perm[jn + ((uint32_t)lane < cn ? lane : 0)];
+          issue_records<SP>(rec_in, r_next, cn, wst + (buf ^ 1) * 32 * SP::SW, lane);
+        }
+        buf ^= 1;
+      }
       const uint32_t h = mix32(content_key<SP>(w) ^ salt);
       float s[NSV];
       if (valid) {
@@ -614,7 +678,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       const unsigned kp = __match_any_sync(FULL, nk);
       if (valid && lane == __ffs(kp) - 1) atomicAdd(&block_count[nk], (unsigned)__popc(kp));
       if (ids_out != nullptr && valid) ids_out[j] = ids_in[r];
-      store_records<SP>(rec_out + (size_t)j0 * W, cnt, wst, lane, ow);
+      store_records<SP>(rec_out + (size_t)j0 * W, cnt, cur, lane, ow);
     }
     __syncwarp();
   }
@@ -638,16 +702,17 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
 // per-warp shared-memory bytes of P2G and G2P, read by the host after loading the module
 extern "C" __device__ const unsigned qmpm_smem_per_warp[2] = {(unsigned)qmpm::Smem<Spec>::P2G_WARP,
                                                              (unsigned)qmpm::Smem<Spec>::G2P_WARP};
-extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t* rec, uint32_t n, qmpm::SimDev S,
-                                                                 uint32_t* key, uint32_t* block_count) {
-  qmpm::bin_count_body<Spec>(rec, n, S, key, block_count);
+extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t* rec, uint32_t first, uint32_t n,
+                                                                 qmpm::SimDev S, uint32_t* key, uint32_t* block_count,
+                                                                 int do_count) {
+  qmpm::bin_count_body<Spec>(rec, first, n, S, key, block_count, do_count);
 }
 
 extern "C" __global__ void __launch_bounds__(Spec::P2G_WARPS * 32, Spec::P2G_MINB)
-    qmpm_p2g(const uint32_t* rec, uint32_t* perm, const uint32_t* key, const uint32_t* block_start,
+    qmpm_p2g(const uint32_t* rec, uint32_t* perm, const uint8_t* cells, const uint32_t* block_start,
              const uint32_t* active_list, const qmpm::DevCounters* dc, const uint32_t* block_slot, float4* mp,
              qmpm::SimDev S) {
-  qmpm::p2g_body<Spec>(rec, perm, key, block_start, active_list, dc, block_slot, mp, S);
+  qmpm::p2g_body<Spec>(rec, perm, cells, block_start, active_list, dc, block_slot, mp, S);
 }
 
 extern "C" __global__ void __launch_bounds__(Spec::G2P_WARPS * 32, Spec::G2P_MINB)
