@@ -41,7 +41,7 @@ enum {
     QMPM_ELAYOUT = 2,    /* scheme cannot be laid out (width 0 or > 32; missing scalar) */
     QMPM_ENOMEM = 3,     /* device allocation failed */
     QMPM_ECUDA = 4,      /* CUDA runtime error */
-    QMPM_ENCCL = 5,      /* reserved: multi-GPU exchange */
+    QMPM_ENCCL = 5,      /* NCCL error in the slab exchange */
     QMPM_ENONFINITE = 6, /* reserved: non-finite values are counted in qmpm_stats */
     QMPM_EDOMAIN = 7,    /* reserved: out-of-domain particles are counted in qmpm_stats */
     QMPM_ECAPACITY = 8,  /* n > max_particles, or grid pool overflow during a step */
@@ -153,6 +153,10 @@ qmpm_status qmpm_append_state(qmpm_ctx* ctx, uint64_t n, const float* vals);
  * run is bit-identical, reading Q5). */
 qmpm_status qmpm_set_words(qmpm_ctx* ctx, uint64_t n, const uint32_t* words, uint64_t step);
 
+/* Overwrite the ids of the current n particles (host or device [n] u32; needs
+ * QMPM_TRACK_IDS).  With a slab decomposition, ids must be unique across ranks. */
+qmpm_status qmpm_set_ids(qmpm_ctx* ctx, uint64_t n, const uint32_t* ids);
+
 /* Advance n_steps MLS-MPM steps (decode -> bin -> P2G -> grid update -> G2P ->
  * dithered encode), asynchronously on the ctx stream; allocates nothing. */
 qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps);
@@ -192,6 +196,35 @@ qmpm_status qmpm_kernel_times(qmpm_ctx* ctx, double* ms, uint64_t* launches);
 const char* qmpm_kernel_name(int i);
 /* Total kernels this ctx launched (all entry points), for the bench's claim. */
 uint64_t qmpm_launch_count(const qmpm_ctx* ctx);
+
+/* ---- Slab decomposition --------------------------
+ * The 3D grid is cut into slabs of z cell planes, one per rank.  A rank owns the
+ * particles whose base cell lies in its slab.  Every step: P2G partial sums of the
+ * ghost block plane above the slab are added into the upper neighbour; the upper
+ * neighbour's updated velocities of that plane come back; particles whose base
+ * leaves the slab migrate to the neighbour (CFL keeps migration to one hop). */
+typedef struct {
+    int32_t nranks, rank;
+    int32_t z0, z1;            /* owned cell planes [z0, z1): multiples of 4 (z1 may be grid_res[2]) */
+    uint64_t migrate_capacity; /* particles per direction per step; 0 = max(65536, max_particles/64) */
+} qmpm_slab;
+
+/* Like qmpm_create, for rank `slab->rank` of `slab->nranks` (3D only).  Particles
+ * given to qmpm_set_state must lie in this slab or an adjacent one (they are routed
+ * to their owner during the first step).  QMPM_EINVAL for a bad slab. */
+qmpm_status qmpm_create_slab(const qmpm_params* params, const qmpm_scheme* scheme, void* cuda_stream,
+                             const qmpm_slab* slab, qmpm_ctx** out);
+/* NCCL transport (one process per GPU): rank 0 creates the unique id, the caller
+ * broadcasts it (e.g. torch.distributed), every rank connects; qmpm_step then
+ * exchanges halos and migrants with grouped ncclSend/ncclRecv on the ctx stream
+ * (host-synchronising once per step for the migration counts).  QMPM_ENCCL on
+ * failure (including a missing libnccl.so.2). */
+qmpm_status qmpm_get_unique_id(uint8_t id[128]);
+qmpm_status qmpm_connect_nccl(qmpm_ctx* ctx, const uint8_t id[128]);
+/* In-process transport: advance all slabs of one decomposition that live in this
+ * process (ctxs[r] = rank r of n, one shared stream), exchanging with device copies.
+ * Synchronizes once per step. */
+qmpm_status qmpm_step_group(qmpm_ctx* const* ctxs, int n, uint32_t n_steps);
 
 const char* qmpm_last_error(const qmpm_ctx* ctx);
 int qmpm_abi_version(void);

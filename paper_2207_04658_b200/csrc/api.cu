@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "jit.h"
 #include "qmpm.h"
 #include "qmpm_launch.h"
@@ -67,6 +68,18 @@ struct qmpm_ctx {
   uint64_t launches[KNumKernels] = {0};
   uint64_t launches_total = 0;
   std::string err;
+  // slab decomposition
+  bool slab = false;
+  int nranks = 1, rank = 0;
+  uint64_t mig_cap = 0;
+  uint32_t* mig_send[2] = {nullptr, nullptr};  // [0] down, [1] up: records, W words each
+  uint32_t* mig_send_ids[2] = {nullptr, nullptr};
+  float4* plane_send = nullptr;
+  float4* plane_recv = nullptr;
+  size_t plane_elems = 0;
+  uint32_t* d_cnt_recv = nullptr;  // device [2]: counts announced by the neighbour below / above
+  uint32_t* h_cnt = nullptr;       // pinned [8]: mig_dn, mig_up, mig_overflow, n_sorted, recv_dn, recv_up
+  NcclComm* nccl = nullptr;
 };
 
 namespace {
@@ -294,6 +307,12 @@ qmpm_status qmpm_destroy(qmpm_ctx* ctx) {
                   ctx->tile_sums, ctx->tile_off, ctx->mp, ctx->gv, ctx->dc, ctx->dbg};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  void* sptrs[] = {ctx->mig_send[0], ctx->mig_send[1], ctx->mig_send_ids[0], ctx->mig_send_ids[1],
+                   ctx->plane_send, ctx->plane_recv, ctx->d_cnt_recv};
+  for (void* p : sptrs)
+    if (p) cudaFree(p);
+  if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
+  if (ctx->nccl) nccl_destroy(ctx->nccl);
   for (auto& p : ctx->pending) {
     cudaEventDestroy(p.a);
     if (p.b) cudaEventDestroy(p.b);
@@ -403,6 +422,10 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   S.lambda = (float)((double)P.E * (double)P.nu / ((1.0 + (double)P.nu) * (1.0 - 2.0 * (double)P.nu)));
   S.E = P.E;
   S.bound = P.bound;
+  S.slab_bz0 = 0;
+  S.slab_bz1 = S.nb[2];
+  S.slab_lo = 0;
+  S.slab_hi = 0;
 
   ctx->ntiles = (uint32_t)((nblocks + kScanTile - 1) / kScanTile);
   ctx->pool = P.pool_blocks ? P.pool_blocks : std::min<uint64_t>(nblocks, 4096 + P.max_particles / 256);
@@ -544,42 +567,320 @@ qmpm_status qmpm_set_words(qmpm_ctx* ctx, uint64_t n, const uint32_t* words, uin
   return QMPM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+StepBuffers buffers(qmpm_ctx* ctx, uint64_t n) {
+  StepBuffers B{};
+  B.rec_in = ctx->rec[ctx->cur];
+  B.rec_out = ctx->rec[ctx->cur ^ 1];
+  B.ids_in = ctx->ids[ctx->cur];
+  B.ids_out = ctx->ids[ctx->cur ^ 1];
+  B.key = ctx->key;
+  B.perm = ctx->perm;
+  B.cells = ctx->cells;
+  B.block_count = ctx->block_count;
+  B.block_start = ctx->block_start;
+  B.block_slot = ctx->block_slot;
+  B.active_list = ctx->active_list;
+  B.touched_list = ctx->touched_list;
+  B.tile_sums = ctx->tile_sums;
+  B.tile_off = ctx->tile_off;
+  B.mp = ctx->mp;
+  B.gv = ctx->gv;
+  B.dc = ctx->dc;
+  B.dbg = ctx->dbg;
+  B.n = (uint32_t)n;
+  B.pool = (uint32_t)ctx->pool;
+  B.ntiles = ctx->ntiles;
+  return B;
+}
+
+uint32_t salt_of(qmpm_ctx* ctx) {
+  return step_salt(ctx->L.seed_lo, ctx->L.seed_hi, (uint32_t)(ctx->step + 1));  // steps numbered 1, 2, ... (Q20)
+}
+
+void finish_step(qmpm_ctx* ctx) {
+  ctx->cur ^= 1;
+  ctx->step += 1;
+  ctx->dbg_valid = ctx->dbg != nullptr;
+}
+
+// ---------------------------------------------------------------- slab phases
+// A: sort pass 1 (all particles), pack the ones that left the slab, counts -> host
+qmpm_status slab_a(qmpm_ctx* ctx) {
+  if (!ctx->binned) {
+    qmpm_status rc = rebin(ctx);
+    if (rc) return rc;
+  }
+  StepBuffers B = buffers(ctx, ctx->n);
+  CK(launch_sort(ctx->dim, B, ctx->S, ctx->stream, hook_fn, ctx));
+  CK(launch_pack_leavers(B, ctx->S, ctx->W, (uint32_t)ctx->mig_cap, ctx->mig_send[0], ctx->mig_send[1],
+                         ctx->mig_send_ids[0], ctx->mig_send_ids[1], ctx->jit.num_sms, ctx->stream));
+  ctx->launches_total += 1;
+  CK(cudaMemcpyAsync(ctx->h_cnt, &ctx->dc->mig_dn, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  return QMPM_OK;
+}
+
+// B: arrivals are in place at [n, n + arr): their keys, recount owned particles,
+// sort pass 2, P2G, pack the ghost plane for the rank above
+qmpm_status slab_b(qmpm_ctx* ctx, uint32_t arr) {
+  const uint32_t n_slots = (uint32_t)ctx->n + arr;
+  StepBuffers B = buffers(ctx, n_slots);
+  if (arr) {
+    ctx->launches_total += 1;
+    CK(launch_bin_count(ctx->rec[ctx->cur], (uint32_t)ctx->n, arr, ctx->S, ctx->key, ctx->block_count, 0, ctx->jit,
+                        ctx->stream));
+  }
+  ctx->launches_total += 1;
+  CK(launch_recount(B, ctx->S, n_slots, ctx->stream));
+  CK(launch_sort(ctx->dim, B, ctx->S, ctx->stream, hook_fn, ctx));
+  CK(launch_p2g(B, ctx->S, ctx->jit, ctx->stream, hook_fn, ctx));
+  if (ctx->S.slab_hi) {
+    ctx->launches_total += 1;
+    CK(launch_plane(ctx->mp, ctx->block_slot, ctx->S, ctx->S.slab_bz1, ctx->plane_send, 0, ctx->jit.num_sms,
+                    ctx->stream));
+  }
+  return QMPM_OK;
+}
+
+// C: add the lower rank's ghost plane, grid update, pack the velocity plane for the rank below
+qmpm_status slab_c(qmpm_ctx* ctx) {
+  StepBuffers B = buffers(ctx, ctx->n);
+  if (ctx->S.slab_lo) {
+    ctx->launches_total += 1;
+    CK(launch_plane(ctx->mp, ctx->block_slot, ctx->S, ctx->S.slab_bz0, ctx->plane_recv, 1, ctx->jit.num_sms,
+                    ctx->stream));
+  }
+  CK(launch_grid_update(ctx->dim, B, ctx->S, ctx->jit, ctx->stream, hook_fn, ctx));
+  if (ctx->S.slab_lo) {
+    ctx->launches_total += 1;
+    CK(launch_plane(ctx->gv, ctx->block_slot, ctx->S, ctx->S.slab_bz0, ctx->plane_send, 0, ctx->jit.num_sms,
+                    ctx->stream));
+  }
+  return QMPM_OK;
+}
+
+// D: velocities of the ghost plane from the rank above, G2P + encode
+qmpm_status slab_d(qmpm_ctx* ctx, uint64_t n_live) {
+  StepBuffers B = buffers(ctx, n_live);
+  if (ctx->S.slab_hi) {
+    ctx->launches_total += 1;
+    CK(launch_plane(ctx->gv, ctx->block_slot, ctx->S, ctx->S.slab_bz1, ctx->plane_recv, 2, ctx->jit.num_sms,
+                    ctx->stream));
+  }
+  CK(launch_g2p(B, ctx->S, salt_of(ctx), ctx->jit, ctx->stream, hook_fn, ctx));
+  ctx->n = n_live;
+  finish_step(ctx);
+  return QMPM_OK;
+}
+
+qmpm_status check_migration(qmpm_ctx* ctx) {
+  if (ctx->h_cnt[2]) return fail(ctx, QMPM_ECAPACITY, "slab migration buffer overflow (capacity %llu)",
+                                 (unsigned long long)ctx->mig_cap);
+  return QMPM_OK;
+}
+
+// one slab step with NCCL exchanges (one process per GPU)
+qmpm_status slab_step_nccl(qmpm_ctx* ctx) {
+  std::string err;
+  qmpm_status rc = slab_a(ctx);
+  if (rc) return rc;
+  // counts: each neighbour announces how many particles it sends us
+  P2P c{&ctx->dc->mig_dn, 4, &ctx->dc->mig_up, 4, ctx->d_cnt_recv + 0, 4, ctx->d_cnt_recv + 1, 4};
+  if (!nccl_exchange(ctx->nccl, c, ctx->stream, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+  CK(cudaMemcpyAsync(ctx->h_cnt + 4, ctx->d_cnt_recv, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if ((rc = check_migration(ctx))) return rc;
+  const uint32_t W = ctx->W, dn = ctx->h_cnt[0], up = ctx->h_cnt[1], n_sorted = ctx->h_cnt[3];
+  const uint32_t rdn = ctx->S.slab_lo ? ctx->h_cnt[4] : 0, rup = ctx->S.slab_hi ? ctx->h_cnt[5] : 0;
+  if ((uint64_t)ctx->n + rdn + rup > ctx->cap) return fail(ctx, QMPM_ECAPACITY, "arrivals exceed max_particles");
+  uint32_t* dst = ctx->rec[ctx->cur] + (size_t)ctx->n * W;
+  P2P x{ctx->mig_send[0], (size_t)dn * W * 4, ctx->mig_send[1], (size_t)up * W * 4,
+        dst, (size_t)rdn * W * 4, dst + (size_t)rdn * W, (size_t)rup * W * 4};
+  if (!nccl_exchange(ctx->nccl, x, ctx->stream, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+  if (ctx->ids[ctx->cur]) {
+    uint32_t* idst = ctx->ids[ctx->cur] + ctx->n;
+    P2P xi{ctx->mig_send_ids[0], (size_t)dn * 4, ctx->mig_send_ids[1], (size_t)up * 4,
+           idst, (size_t)rdn * 4, idst + rdn, (size_t)rup * 4};
+    if (!nccl_exchange(ctx->nccl, xi, ctx->stream, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+  }
+  const uint64_t n_live = (uint64_t)n_sorted - dn - up + rdn + rup;
+  if ((rc = slab_b(ctx, rdn + rup))) return rc;
+  const size_t pb = ctx->plane_elems * sizeof(float4);
+  P2P h1{nullptr, 0, ctx->plane_send, ctx->S.slab_hi ? pb : 0, ctx->plane_recv, ctx->S.slab_lo ? pb : 0, nullptr, 0};
+  if (!nccl_exchange(ctx->nccl, h1, ctx->stream, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+  if ((rc = slab_c(ctx))) return rc;
+  P2P h2{ctx->plane_send, ctx->S.slab_lo ? pb : 0, nullptr, 0, nullptr, 0, ctx->plane_recv, ctx->S.slab_hi ? pb : 0};
+  if (!nccl_exchange(ctx->nccl, h2, ctx->stream, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+  return slab_d(ctx, n_live);
+}
+
+}  // namespace
+
+extern "C" {
+
 qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps) {
   if (!ctx) return fail(ctx, QMPM_EINVAL, "NULL ctx");
+  if (ctx->slab && ctx->nranks > 1) {
+    if (!ctx->nccl) return fail(ctx, QMPM_ESTATE, "slab ctx: call qmpm_connect_nccl or use qmpm_step_group");
+    for (uint32_t t = 0; t < n_steps; ++t) {
+      qmpm_status rc = slab_step_nccl(ctx);
+      if (rc) return rc;
+    }
+    return QMPM_OK;
+  }
   for (uint32_t t = 0; t < n_steps; ++t) {
     if (!ctx->binned) {
       qmpm_status rc = rebin(ctx);
       if (rc) return rc;
     }
-    StepBuffers B{};
-    B.rec_in = ctx->rec[ctx->cur];
-    B.rec_out = ctx->rec[ctx->cur ^ 1];
-    B.ids_in = ctx->ids[ctx->cur];
-    B.ids_out = ctx->ids[ctx->cur ^ 1];
-    B.key = ctx->key;
-    B.perm = ctx->perm;
-    B.cells = ctx->cells;
-    B.block_count = ctx->block_count;
-    B.block_start = ctx->block_start;
-    B.block_slot = ctx->block_slot;
-    B.active_list = ctx->active_list;
-    B.touched_list = ctx->touched_list;
-    B.tile_sums = ctx->tile_sums;
-    B.tile_off = ctx->tile_off;
-    B.mp = ctx->mp;
-    B.gv = ctx->gv;
-    B.dc = ctx->dc;
-    B.dbg = ctx->dbg;
-    B.n = (uint32_t)ctx->n;
-    B.pool = (uint32_t)ctx->pool;
-    B.ntiles = ctx->ntiles;
-    const uint64_t t_step = ctx->step + 1;  // steps are numbered 1, 2, ... (Q20)
-    const uint32_t salt = step_salt(ctx->L.seed_lo, ctx->L.seed_hi, (uint32_t)t_step);
-    CK(launch_step(ctx->dim, B, ctx->S, salt, ctx->jit, ctx->stream, hook_fn, ctx));
-    ctx->cur ^= 1;
-    ctx->step = t_step;
-    ctx->dbg_valid = ctx->dbg != nullptr;
+    StepBuffers B = buffers(ctx, ctx->n);
+    CK(launch_step(ctx->dim, B, ctx->S, salt_of(ctx), ctx->jit, ctx->stream, hook_fn, ctx));
+    finish_step(ctx);
   }
+  return QMPM_OK;
+}
+
+qmpm_status qmpm_step_group(qmpm_ctx* const* ctxs, int n, uint32_t n_steps) {
+  qmpm_ctx* ctx = nullptr;
+  if (!ctxs || n < 1) return fail(ctx, QMPM_EINVAL, "empty group");
+  for (int r = 0; r < n; ++r) {
+    if (!ctxs[r] || !ctxs[r]->slab || ctxs[r]->nranks != n || ctxs[r]->rank != r)
+      return fail(ctx, QMPM_EINVAL, "qmpm_step_group: ctxs[%d] must be the slab ctx of rank %d of %d", r, r, n);
+    if (ctxs[r]->stream != ctxs[0]->stream) return fail(ctx, QMPM_EINVAL, "qmpm_step_group: one stream for all ctxs");
+    if ((ctxs[r]->ids[0] != nullptr) != (ctxs[0]->ids[0] != nullptr) || ctxs[r]->W != ctxs[0]->W)
+      return fail(ctx, QMPM_EINVAL, "qmpm_step_group: ctxs differ in scheme or flags");
+  }
+  cudaStream_t st = ctxs[0]->stream;
+  const uint32_t W = ctxs[0]->W;
+  std::vector<uint64_t> n_live(n);
+  std::vector<uint32_t> arr(n);
+  for (uint32_t t = 0; t < n_steps; ++t) {
+    for (int r = 0; r < n; ++r) {
+      qmpm_status rc = slab_a(ctxs[r]);
+      if (rc) return rc;
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(ctx, QMPM_ECUDA, "step_group sync failed");
+    for (int r = 0; r < n; ++r) {
+      qmpm_ctx* c = ctxs[r];
+      qmpm_status rc = check_migration(c);
+      if (rc) return rc;
+      const uint32_t rdn = r > 0 ? ctxs[r - 1]->h_cnt[1] : 0, rup = r + 1 < n ? ctxs[r + 1]->h_cnt[0] : 0;
+      if (c->n + rdn + rup > c->cap) return fail(c, QMPM_ECAPACITY, "arrivals exceed max_particles");
+      uint32_t* dst = c->rec[c->cur] + (size_t)c->n * W;
+      if (rdn) {
+        CK(cudaMemcpyAsync(dst, ctxs[r - 1]->mig_send[1], (size_t)rdn * W * 4, cudaMemcpyDeviceToDevice, st));
+        if (c->ids[c->cur])
+          CK(cudaMemcpyAsync(c->ids[c->cur] + c->n, ctxs[r - 1]->mig_send_ids[1], (size_t)rdn * 4,
+                             cudaMemcpyDeviceToDevice, st));
+      }
+      if (rup) {
+        CK(cudaMemcpyAsync(dst + (size_t)rdn * W, ctxs[r + 1]->mig_send[0], (size_t)rup * W * 4,
+                           cudaMemcpyDeviceToDevice, st));
+        if (c->ids[c->cur])
+          CK(cudaMemcpyAsync(c->ids[c->cur] + c->n + rdn, ctxs[r + 1]->mig_send_ids[0], (size_t)rup * 4,
+                             cudaMemcpyDeviceToDevice, st));
+      }
+      arr[r] = rdn + rup;
+      n_live[r] = (uint64_t)c->h_cnt[3] - c->h_cnt[0] - c->h_cnt[1] + rdn + rup;
+    }
+    for (int r = 0; r < n; ++r) {
+      qmpm_status rc = slab_b(ctxs[r], arr[r]);
+      if (rc) return rc;
+    }
+    for (int r = 0; r + 1 < n; ++r)
+      CK(cudaMemcpyAsync(ctxs[r + 1]->plane_recv, ctxs[r]->plane_send, ctxs[r]->plane_elems * sizeof(float4),
+                         cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < n; ++r) {
+      qmpm_status rc = slab_c(ctxs[r]);
+      if (rc) return rc;
+    }
+    for (int r = 1; r < n; ++r)
+      CK(cudaMemcpyAsync(ctxs[r - 1]->plane_recv, ctxs[r]->plane_send, ctxs[r]->plane_elems * sizeof(float4),
+                         cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < n; ++r) {
+      qmpm_status rc = slab_d(ctxs[r], n_live[r]);
+      if (rc) return rc;
+    }
+  }
+  return QMPM_OK;
+}
+
+qmpm_status qmpm_get_unique_id(uint8_t id[128]) {
+  qmpm_ctx* ctx = nullptr;
+  std::string err;
+  if (!id) return fail(ctx, QMPM_EINVAL, "NULL id");
+  if (!nccl_unique_id(id, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+  return QMPM_OK;
+}
+
+qmpm_status qmpm_connect_nccl(qmpm_ctx* ctx, const uint8_t id[128]) {
+  if (!ctx || !id) return fail(ctx, QMPM_EINVAL, "NULL argument");
+  if (!ctx->slab) return fail(ctx, QMPM_ESTATE, "qmpm_connect_nccl needs a slab ctx (qmpm_create_slab)");
+  std::string err;
+  ctx->nccl = nccl_connect(id, ctx->nranks, ctx->rank, err);
+  if (!ctx->nccl) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+  return QMPM_OK;
+}
+
+qmpm_status qmpm_create_slab(const qmpm_params* params, const qmpm_scheme* scheme, void* cuda_stream,
+                             const qmpm_slab* slab, qmpm_ctx** out) {
+  qmpm_ctx* ctx = nullptr;
+  if (!slab || !out) return fail(ctx, QMPM_EINVAL, "NULL argument to qmpm_create_slab");
+  if (!scheme || scheme->dim != 3) return fail(ctx, QMPM_EINVAL, "slab decomposition is 3D (z slabs)");
+  if (slab->nranks < 1 || slab->rank < 0 || slab->rank >= slab->nranks)
+    return fail(ctx, QMPM_EINVAL, "bad rank %d of %d", slab->rank, slab->nranks);
+  if (!params) return fail(ctx, QMPM_EINVAL, "NULL params");
+  const int nz = params->grid_res[2];
+  if (slab->z0 < 0 || slab->z1 > nz || slab->z0 >= slab->z1 || slab->z0 % 4 != 0 || (slab->z1 % 4 != 0 && slab->z1 != nz))
+    return fail(ctx, QMPM_EINVAL, "slab [%d, %d) must be non-empty, inside [0, %d) and on 4-cell block planes",
+                slab->z0, slab->z1, nz);
+  qmpm_status rc = qmpm_create(params, scheme, cuda_stream, &ctx);
+  if (rc) return rc;
+  ctx->slab = true;
+  ctx->nranks = slab->nranks;
+  ctx->rank = slab->rank;
+  SimDev& S = ctx->S;
+  S.slab_bz0 = slab->z0 / 4;
+  S.slab_bz1 = (slab->z1 + 3) / 4;
+  S.slab_lo = slab->rank > 0;
+  S.slab_hi = slab->rank + 1 < slab->nranks;
+  ctx->mig_cap = slab->migrate_capacity ? slab->migrate_capacity : std::max<uint64_t>(65536, ctx->cap / 64);
+  ctx->plane_elems = (size_t)S.nb[0] * S.nb[1] * 64;
+  const size_t W = ctx->W;
+  cudaError_t e = cudaSuccess;
+  for (int dir = 0; dir < 2 && !e; ++dir) {
+    e = cudaMalloc((void**)&ctx->mig_send[dir], sizeof(uint32_t) * W * ctx->mig_cap);
+    if (!e && ctx->ids[0]) e = cudaMalloc((void**)&ctx->mig_send_ids[dir], sizeof(uint32_t) * ctx->mig_cap);
+  }
+  if (!e) e = cudaMalloc((void**)&ctx->plane_send, sizeof(float4) * ctx->plane_elems);
+  if (!e) e = cudaMalloc((void**)&ctx->plane_recv, sizeof(float4) * ctx->plane_elems);
+  if (!e) e = cudaMalloc((void**)&ctx->d_cnt_recv, 2 * sizeof(uint32_t));
+  if (!e) e = cudaMallocHost((void**)&ctx->h_cnt, 8 * sizeof(uint32_t));
+  if (!e) e = cudaMemsetAsync(ctx->plane_recv, 0, sizeof(float4) * ctx->plane_elems, ctx->stream);
+  if (!e) e = cudaMemsetAsync(ctx->d_cnt_recv, 0, 2 * sizeof(uint32_t), ctx->stream);
+  if (!e) e = cudaStreamSynchronize(ctx->stream);
+  if (e) {
+    cudaGetLastError();
+    qmpm_destroy(ctx);
+    return fail(nullptr, e == cudaErrorMemoryAllocation ? QMPM_ENOMEM : QMPM_ECUDA, "qmpm_create_slab: %s",
+                cudaGetErrorString(e));
+  }
+  memset(ctx->h_cnt, 0, 8 * sizeof(uint32_t));
+  *out = ctx;
+  return QMPM_OK;
+}
+
+qmpm_status qmpm_set_ids(qmpm_ctx* ctx, uint64_t n, const uint32_t* ids) {
+  if (!ctx) return fail(ctx, QMPM_EINVAL, "NULL ctx");
+  if (!ctx->ids[ctx->cur]) return fail(ctx, QMPM_ESTATE, "qmpm_set_ids needs QMPM_TRACK_IDS");
+  if (n != ctx->n) return fail(ctx, QMPM_EINVAL, "n=%llu but the ctx holds %llu particles", (unsigned long long)n,
+                               (unsigned long long)ctx->n);
+  if (n && !ids) return fail(ctx, QMPM_EINVAL, "ids is NULL");
+  if (n) CK(cudaMemcpyAsync(ctx->ids[ctx->cur], ids, sizeof(uint32_t) * n, cudaMemcpyDefault, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   return QMPM_OK;
 }
 

@@ -49,6 +49,11 @@ class Params(ctypes.Structure):
                 ("flags", ctypes.c_uint32), ("max_particles", ctypes.c_uint64), ("pool_blocks", ctypes.c_uint64)]
 
 
+class Slab(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("z0", ctypes.c_int32), ("z1", ctypes.c_int32),
+                ("migrate_capacity", ctypes.c_uint64)]
+
+
 class Stats(ctypes.Structure):
     _fields_ = [("step", ctypes.c_uint64), ("n_particles", ctypes.c_uint64),
                 ("saturations", ctypes.c_uint64 * MAX_FIELDS), ("round_up", ctypes.c_uint64 * MAX_FIELDS),
@@ -61,7 +66,8 @@ _lib = None
 EXPORTS = ["qmpm_abi_version", "qmpm_last_error", "qmpm_layout", "qmpm_create", "qmpm_destroy",
            "qmpm_set_state", "qmpm_append_state", "qmpm_set_words", "qmpm_step", "qmpm_read_state",
            "qmpm_read_debug", "qmpm_stats", "qmpm_encode", "qmpm_decode", "qmpm_set_profiling",
-           "qmpm_kernel_times", "qmpm_kernel_name", "qmpm_launch_count"]
+           "qmpm_kernel_times", "qmpm_kernel_name", "qmpm_launch_count", "qmpm_create_slab",
+           "qmpm_get_unique_id", "qmpm_connect_nccl", "qmpm_step_group", "qmpm_set_ids"]
 
 
 def lib():
@@ -93,6 +99,12 @@ def lib():
         "qmpm_kernel_times": (i32, [P, P, P]),
         "qmpm_kernel_name": (ctypes.c_char_p, [ctypes.c_int]),
         "qmpm_launch_count": (u64, [P]),
+        "qmpm_create_slab": (i32, [ctypes.POINTER(Params), ctypes.POINTER(Scheme), P, ctypes.POINTER(Slab),
+                                   ctypes.POINTER(P)]),
+        "qmpm_get_unique_id": (i32, [P]),
+        "qmpm_connect_nccl": (i32, [P, P]),
+        "qmpm_step_group": (i32, [P, ctypes.c_int, u32]),
+        "qmpm_set_ids": (i32, [P, u64, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -192,11 +204,24 @@ def kernel_names():
     return [lib().qmpm_kernel_name(i).decode() for i in range(NUM_KERNELS)]
 
 
+def get_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().qmpm_get_unique_id(buf))
+    return bytes(buf)
+
+
+def step_group(sims, n_steps=1):
+    """qmpm_step_group: advance the slabs of one decomposition living in this process."""
+    arr = (ctypes.c_void_p * len(sims))(*[s.ctx.value for s in sims])
+    _check(lib().qmpm_step_group(arr, len(sims), n_steps))
+
+
 class Sim:
-    """One qmpm context (qmpm_create .. qmpm_destroy)."""
+    """One qmpm context (qmpm_create .. qmpm_destroy); `slab=(nranks, rank, z0, z1)`
+    creates the context of one slab of a z decomposition (qmpm_create_slab)."""
 
     def __init__(self, sim: dict, scheme: dict, max_particles: int, flags: int = 0, pool_blocks: int = 0,
-                 stream=None):
+                 stream=None, slab=None, migrate_capacity: int = 0):
         self.scheme = CScheme(scheme)
         self.params = make_params(sim, max_particles, flags, pool_blocks)
         self.dim = scheme["dim"]
@@ -206,7 +231,12 @@ class Sim:
         _, self.W, self.bits = layout(scheme)
         self.stream = stream_handle(stream)
         h = ctypes.c_void_p()
-        _check(lib().qmpm_create(ctypes.byref(self.params), self.scheme.ref, self.stream, ctypes.byref(h)))
+        if slab is None:
+            _check(lib().qmpm_create(ctypes.byref(self.params), self.scheme.ref, self.stream, ctypes.byref(h)))
+        else:
+            self.slab = Slab(slab[0], slab[1], slab[2], slab[3], migrate_capacity)
+            _check(lib().qmpm_create_slab(ctypes.byref(self.params), self.scheme.ref, self.stream,
+                                          ctypes.byref(self.slab), ctypes.byref(h)))
         self.ctx = h
 
     def close(self):
@@ -237,6 +267,9 @@ class Sim:
 
     def set_words(self, words, step):
         self._c(lib().qmpm_set_words(self.ctx, words.shape[0], ptr(words), step))
+
+    def set_ids(self, ids):
+        self._c(lib().qmpm_set_ids(self.ctx, ids.shape[0], ptr(ids)))
 
     def step(self, n_steps=1):
         self._c(lib().qmpm_step(self.ctx, n_steps))
@@ -273,3 +306,7 @@ class Sim:
 
     def launch_count(self):
         return lib().qmpm_launch_count(self.ctx)
+
+    def connect_nccl(self, uid: bytes):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        self._c(lib().qmpm_connect_nccl(self.ctx, buf))

@@ -1,0 +1,139 @@
+"""GPU tests of the slab decomposition with the in-process
+transport (qmpm_step_group): k z-slabs on one GPU exchange ghost planes, velocity
+planes and migrating particles exactly as the NCCL transport does between GPUs.
+
+The slab run must meet the SAME parity bar as the single-GPU run: one step from
+oracle-generated words vs the fp64 oracle within 1e-5 on the conditioning-aware
+scales, and the stored words bit-exact to the oracle codec on the GPU's own floats
+(content-keyed dithering makes codes independent of the rank that stores them)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2207_04658_b200 import qmpm, scenes, schemes
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from test_gpu_step import REL, scales  # noqa: E402
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def cuts(nz, k):
+    """k slabs of whole 4-cell block planes"""
+    nb = nz // 4
+    b = [round(i * nb / k) * 4 for i in range(k + 1)]
+    b[-1] = nz
+    return list(zip(b[:-1], b[1:]))
+
+
+def owner(state, sim, slabs):
+    z = np.floor(state[:, 2].astype(np.float64) / sim["dx"] - 0.5).astype(np.int64)
+    z = np.clip(z, 0, sim["grid_res"][2] - 3)
+    o = np.zeros(len(z), np.int64)
+    for r, (z0, z1) in enumerate(slabs):
+        o[(z >= z0) & (z < z1)] = r
+    return o
+
+
+def make_group(sc, sch, words, step0, k, flags):
+    slabs = cuts(sc.sim["grid_res"][2], k)
+    st = oracle.decode_state(sch, words)
+    own = owner(st, sc.sim, slabs)
+    stream = torch.cuda.Stream()
+    sims = []
+    for r, (z0, z1) in enumerate(slabs):
+        idx = np.nonzero(own == r)[0]
+        s = qmpm.Sim(sc.sim, sch, words.shape[0], flags=flags, stream=stream, slab=(k, r, z0, z1))
+        s.set_words(dev(words[idx]), step0)
+        s.set_ids(dev(idx.astype(np.uint32)))
+        sims.append(s)
+    return sims, slabs
+
+
+def gather(sims, ns, W, debug=True):
+    pre, words, ids = [], [], []
+    for s in sims:
+        n = s.stats().n_particles
+        w = np.zeros((n, W), np.uint32)
+        i = np.zeros(n, np.uint32)
+        s.read_state(words=w, ids=i, capacity=n)
+        words.append(w)
+        ids.append(i)
+        if debug:
+            p = np.zeros((n, ns), np.float32)
+            s.read_debug(p)
+            pre.append(p)
+    ids = np.concatenate(ids)
+    order = np.argsort(ids)
+    out_pre = np.concatenate(pre)[order] if debug else None
+    return ids[order], np.concatenate(words)[order], out_pre
+
+
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("case", ["fluid", "elastic"])
+def test_slab_step_matches_oracle(case, k):
+    if case == "fluid":
+        sc, sch = scenes.small_fluid_3d(), schemes.f2()
+    else:
+        sc, sch = scenes.small_elastic_3d(), schemes.e01()
+    w0, _ = oracle.encode_state(sch, sc.state())
+    w_in, _ = oracle.run(sc.sim, sch, w0, 1, 10)
+    o_pre, o_words, _ = oracle.step(sc.sim, sch, w_in, 11)
+    sims, slabs = make_group(sc, sch, w_in, 10, k, qmpm.TRACK_IDS | qmpm.DEBUG_PREENCODE)
+    qmpm.step_group(sims, 1)
+    ids, g_words, g_pre = gather(sims, sims[0].n_scalars, sims[0].W)
+    for s in sims:
+        s.close()
+    n = w_in.shape[0]
+    assert np.array_equal(ids, np.arange(n))  # every particle exactly once
+    s_h = scales(sc.sim, o_pre, oracle.decode_state(sch, w_in))
+    err = np.abs(g_pre.astype(np.float64) - o_pre) / np.maximum(np.abs(o_pre), s_h)
+    assert err.max() <= REL, err.max(axis=0)
+    keys = np.array([oracle.particle_key(sch, w_in[i]) for i in range(n)], np.uint32)
+    assert np.array_equal(g_words, oracle.encode_state(sch, g_pre, step=11, keys=keys)[0])
+
+
+def test_slab_run_conserves_and_matches_single_gpu():
+    """20 steps of a 3-slab group vs one context: particle count conserved, every
+    particle stored by the rank owning its slab, KE/COM within 1e-3 (P3)."""
+    sc, sch = scenes.small_fluid_3d(), schemes.f2()
+    st0 = sc.state()
+    w0, _ = oracle.encode_state(sch, st0)
+    sims, slabs = make_group(sc, sch, w0, 0, 3, qmpm.TRACK_IDS)
+    qmpm.step_group(sims, 20)
+    ids, g_words, _ = gather(sims, sims[0].n_scalars, sims[0].W, debug=False)
+    for r, s in enumerate(sims):
+        n = s.stats().n_particles
+        w = np.zeros((n, s.W), np.uint32)
+        s.read_state(words=w, capacity=n)
+        st = oracle.decode_state(sch, w)
+        assert np.all(owner(st, sc.sim, slabs) == r)
+        s.close()
+    assert np.array_equal(ids, np.arange(st0.shape[0]))
+    one = qmpm.Sim(sc.sim, sch, st0.shape[0])
+    one.set_words(dev(w0), 0)
+    one.step(20)
+    w1 = np.zeros_like(w0)
+    one.read_state(words=w1)
+    one.close()
+    ke_g, com_g = oracle.aggregates(sc.sim, oracle.decode_state(sch, g_words))
+    ke_1, com_1 = oracle.aggregates(sc.sim, oracle.decode_state(sch, w1))
+    assert abs(ke_g - ke_1) <= 1e-3 * abs(ke_1)
+    assert np.all(np.abs(com_g - com_1) <= 1e-3 * np.abs(com_1))
+
+
+def test_slab_validation():
+    sc, sch = scenes.small_fluid_3d(), schemes.f2()
+    with pytest.raises(qmpm.QmpmError):
+        qmpm.Sim(sc.sim, sch, 10, slab=(2, 0, 0, 30))  # not on a block plane
+    with pytest.raises(qmpm.QmpmError):
+        qmpm.Sim(sc.sim, sch, 10, slab=(2, 2, 0, 32))  # bad rank
+    s = qmpm.Sim(sc.sim, sch, 10, slab=(2, 0, 0, 32))
+    with pytest.raises(qmpm.QmpmError) as e:
+        s.step(1)  # no transport
+    assert e.value.code == 9
+    s.close()
