@@ -3,13 +3,16 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--scheme e0.01]
     python bench.py --impl reference ...   (the CPU oracle as it stands, host cores)
 
-Workload at N=1 (BASELINE.json configs[2], the paper's T-large elastic run):
-C3 = 295,280,208 particles of 3D elastic cubes on a 1024^3 block-sparse grid,
-dt 7.5e-5, stand-in scheme E0.01 (351 bits/particle, W = 11 words).  Inputs are
-generated on the device (seeded), encoded by qmpm_set_state, then advanced
-`scene_warmup` untimed steps so F != I and C != 0, then W warm-up steps, then K
-timed steps.  The state (13 GB) is far larger than L2 (126 MB), so no flush is
-needed between steps.
+Default workload (BASELINE.json configs[3], the paper's T-large fluid run, P:946;
+the config its metric is quoted on at 1/2/4/8 GPUs): C4 = 3D fluid dam-break,
+400M particles PER GPU (weak scaling: the domain is extended along z by N and cut
+into z slabs, one per rank, exchanging ghost planes and migrants over NCCL), 256^3
+cells per GPU, dt 1e-4, stand-in scheme F2 (253 bits, W = 8 words).
+`--config c3` runs configs[2] instead (295M elastic particles on 1024^3, E0.01,
+single GPU).  Inputs are generated on the device (seeded), encoded by
+qmpm_set_state, advanced `scene_warmup` untimed steps (so C != 0 and the flow
+develops), then W warm-up steps, then K timed steps.  The state (>12 GB) is far
+larger than L2 (126 MB), so no flush is needed between steps.
 
 One JSON line on rank 0 (see the contract in the task statement); the roofline
 object is for the dominant kernel, with algorithmic bytes per launch defined in
@@ -29,7 +32,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-PAPER_C3_PSTEPS = 295_280_208 * 128 / 63.5  # derived from T-large, RTX 3090: context
+PAPER_PSTEPS = {"c3": 295_280_208 * 128 / 63.5,   # derived from T-large, RTX 3090: context
+                "c4": 400_000_000 * 128 / 139.3}   # derived from T-large, RTX 3090: context
 
 
 def parse():
@@ -38,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="qmpm", choices=["qmpm", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--scheme", default=None, help="x16 | e0.1 | e0.01 | f2 | fp32")
     ap.add_argument("--n", type=int, default=0, help="override particle count (reduced runs)")
     ap.add_argument("--scene-warmup", type=int, default=50)
@@ -47,10 +51,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1_000_000)
     ap.add_argument("--cpu-steps", type=int, default=5)
+    ap.add_argument("--ref-sample", type=int, default=250_000, help="particles per --impl reference step")
     return ap.parse_args()
 
 
-def make_scene(args):
+def make_scene(args, world=1):
     from paper_2207_04658_b200 import scenes, schemes
     if args.config == "c1":
         sc = scenes.c1()
@@ -62,7 +67,7 @@ def make_scene(args):
         sc = scenes.c3(n_target=args.n or scenes.C3_PARTICLES)
         sch = schemes.e001()
     else:
-        sc = scenes.c4(n_target=args.n or 400_000_000)
+        sc = scenes.c4(n_target=(args.n or 400_000_000) * world, z_extent=float(world))
         sch = schemes.f2()
     if args.scheme:
         sch = schemes.fp32(sc.dim, sc.material) if args.scheme == "fp32" else schemes.BY_NAME[args.scheme]()
@@ -149,7 +154,7 @@ def run_reference(args):
     sc, sch = make_scene(args)
     import oracle
     _, W, bits = oracle.layout(sch)
-    n = min(args.cpu_sample, sc.n_particles)
+    n = min(args.ref_sample, sc.n_particles)
     st = sc.state_chunk(0, n)
     w, _ = oracle.encode_state(sch, st)
     for t in range(args.warmup):
@@ -163,7 +168,7 @@ def run_reference(args):
     value = n * args.steps / total
     line = {
         "impl": "reference", "metric": "quantized MPM particle-steps/sec", "value": value,
-        "unit": "particle-steps/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "unit": "particle-steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args, sc, W, bits), "sample_particles": n},
@@ -193,23 +198,37 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    sc, sch = make_scene(args)
+    sc, sch = make_scene(args, world)
     _, W, bits = qmpm.layout(sch)
-    N = sc.n_particles
     flags = qmpm.NO_ROUND_COUNTERS if args.no_counters else 0
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        sim = qmpm.Sim(sc.sim, sch, N, flags=flags, stream=stream)
-        chunk = 1 << 24
-        for s0 in range(0, N, chunk):
-            cnt = min(chunk, N - s0)
-            st = sc.state_chunk(s0, cnt, backend="torch", device="cuda")
-            if s0 == 0:
-                sim.set_state(st)
-            else:
-                sim.append_state(st)
-            stream.synchronize()
-            del st
+        if world == 1:
+            N = sc.n_particles
+            sim = qmpm.Sim(sc.sim, sch, N, flags=flags, stream=stream)
+            chunk = 1 << 24
+            for s0 in range(0, N, chunk):
+                cnt = min(chunk, N - s0)
+                st = sc.state_chunk(s0, cnt, backend="torch", device="cuda")
+                if s0 == 0:
+                    sim.set_state(st)
+                else:
+                    sim.append_state(st)
+                stream.synchronize()
+                del st
+        else:
+            # slab decomposition along z (one slab per rank), NCCL exchanges
+            from paper_2207_04658_b200 import dist as qdist
+            if sc.dim != 3:
+                raise SystemExit("multi-GPU runs need a 3D config")
+            cuts = qdist.slab_cuts(sc.sim["grid_res"][2], world)
+            per = sc.n_particles // world
+            sim = qmpm.Sim(sc.sim, sch, int(per * 1.25) + 65536, flags=flags, stream=stream,
+                           slab=(world, rank, cuts[rank][0], cuts[rank][1]))
+            uid = qdist.share_unique_id(qmpm.get_unique_id)
+            sim.connect_nccl(uid)
+            qdist.load_slab(sim, sc, cuts, rank, track_ids=False)
+            N = sc.n_particles // world  # particles per GPU (weak scaling)
         torch.cuda.empty_cache()
         sim.step(args.scene_warmup + args.warmup)
         stream.synchronize()
@@ -239,7 +258,7 @@ def run_gpu(args):
             t = torch.tensor([ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        value = world * N * args.steps / (ms / 1e3)
+        value = sc.n_particles * args.steps / (ms / 1e3)
 
         # ---------------- end to end through the C ABI with pinned host buffers
         e2e = None
@@ -264,7 +283,7 @@ def run_gpu(args):
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 e2e_s = float(t.item())
             stats_bytes = 8 * (2 + 3 * 64 + 5)
-            e2e = {"value": world * N * k / e2e_s, "unit": "particle-steps/s",
+            e2e = {"value": sc.n_particles * k / e2e_s, "unit": "particle-steps/s",
                    "h2d_bytes_per_step": int(N * W * 4 / k),
                    "d2h_bytes_per_step": int(N * W * 4 / k + stats_bytes),
                    "note": f"timed: set_words(pinned host, {N*W*4/1e9:.2f} GB) + {k} x (qmpm_step + qmpm_stats D2H) "
@@ -319,16 +338,19 @@ def run_gpu(args):
         "metric": "quantized MPM particle-steps/sec", "value": value, "unit": "particle-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
         "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": (value / PAPER_C3_PSTEPS) if (args.config == "c3" and not args.n
-                                                     and scheme_name(args) == "e0.01") else None,
+        "vs_baseline": (value / world / PAPER_PSTEPS[args.config])
+        if (args.config in PAPER_PSTEPS and not args.n and scheme_name(args) == {"c3": "e0.01", "c4": "f2"}[args.config])
+        else None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(args, sc, W, bits), "particles_per_gpu": N,
+                   "particles_total": sc.n_particles,
                    "scheme": scheme_name(args), "record_bytes": S, "rounding": args.rounding,
                    "round_counters": not args.no_counters, "scene_warmup_steps": args.scene_warmup,
                    "l2": f"state {N * S / 1e9:.1f} GB per buffer >> 126 MB L2: no flush needed",
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (slab exchange not built)",
-                   "baseline_ref": "vs_baseline = value / 5.95e8 p-steps/s, the paper's RTX 3090 T-large elastic rate "
-                                   "(derived, P:945): context, not a target"},
+                   "parallelism": "single GPU" if world == 1 else
+                   f"z-slab decomposition over {world} GPUs (ghost-plane + velocity halo + migration over NCCL)",
+                   "baseline_ref": "vs_baseline = per-GPU value / the paper's RTX 3090 T-large rate for this workload "
+                                   "(derived: C3 5.95e8, C4 3.68e8 p-steps/s, P:945-946): context, not a target"},
         "roofline": roofline,
         "hbm_roofline_step": {"bytes_per_particle_step": B_alg,
                               "achieved_GBps": value / world * B_alg / 1e9,

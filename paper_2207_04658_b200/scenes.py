@@ -134,6 +134,64 @@ class Scene:
     def state(self, backend="numpy", device=None):
         return self.state_chunk(0, self.n_particles, backend, device)
 
+    def zrange_runs(self, z_lo, z_hi, margin=0.3):
+        """(start, count) runs of global particle indices whose LATTICE z position lies
+        within [z_lo - margin*s, z_hi + margin*s) -- a superset of the particles whose
+        jittered z lies in [z_lo, z_hi) (jitter is +-0.25 s).  3D boxes only."""
+        runs = []
+        first = 0
+        for b in self.boxes:
+            nb = b.size()
+            nx, ny, nz = b.counts
+            k0 = 0 if z_lo == -math.inf else max(0, int(math.floor((z_lo - b.origin[2]) / b.spacing - 0.5 - margin)))
+            k1 = nz if z_hi == math.inf else min(nz, int(math.ceil((z_hi - b.origin[2]) / b.spacing - 0.5 + margin)) + 1)
+            if k0 < k1:
+                for ij in range(nx * ny):
+                    lo = ij * nz + k0
+                    if lo >= nb:
+                        break
+                    hi = min(ij * nz + k1, nb)
+                    if runs and runs[-1][0] + runs[-1][1] == first + lo:
+                        runs[-1] = (runs[-1][0], runs[-1][1] + hi - lo)
+                    else:
+                        runs.append((first + lo, hi - lo))
+            first += nb
+        return runs
+
+    def state_zrange(self, z_lo, z_hi, backend="numpy", device=None, max_chunk=1 << 24):
+        """Generator of (global_indices, state) chunks of the particles whose z lies in
+        [z_lo, z_hi): exactly the rows of state() with that z, in index order."""
+        runs = self.zrange_runs(z_lo, z_hi)
+        pend = []
+        tot = 0
+
+        def flush(pend):
+            if backend == "numpy":
+                idx = np.concatenate([np.arange(a, a + c, dtype=np.int64) for a, c in pend])
+                st = np.concatenate([self.state_chunk(a, c) for a, c in pend])
+                z = st[:, 2]
+                keep = (z >= np.float32(z_lo)) & (z < np.float32(z_hi))
+                return idx[keep], st[keep]
+            import torch
+            idx = torch.cat([torch.arange(a, a + c, dtype=torch.int64, device=device) for a, c in pend])
+            st = torch.cat([self.state_chunk(a, c, backend, device) for a, c in pend])
+            z = st[:, 2]
+            keep = (z >= float(np.float32(z_lo))) & (z < float(np.float32(z_hi)))
+            return idx[keep], st[keep]
+
+        for a, c in runs:
+            while c > 0:
+                take = min(c, max_chunk - tot)
+                pend.append((a, take))
+                tot += take
+                a += take
+                c -= take
+                if tot >= max_chunk:
+                    yield flush(pend)
+                    pend, tot = [], 0
+        if pend:
+            yield flush(pend)
+
 
 def _box_velocity(seed, box_index, dim, vmax):
     if vmax == 0:

@@ -1,0 +1,73 @@
+"""CPU (gloo, world_size 2) tests of the multi-rank host logic of the slab decomposition:
+slab cuts, per-rank scene generation and the id handshake.  The union of what the
+ranks generate must be exactly the full scene, each particle once."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2207_04658_b200 import dist as qdist
+from paper_2207_04658_b200 import scenes
+
+
+def test_slab_cuts_cover_on_block_planes():
+    for nz, world in [(256, 2), (256, 8), (2048, 8), (66, 3)]:
+        c = qdist.slab_cuts(nz, world)
+        assert c[0][0] == 0 and c[-1][1] == nz and len(c) == world
+        for (a, b), (a2, _) in zip(c[:-1], c[1:]):
+            assert b == a2 and a % 4 == 0 and b % 4 == 0 and b > a
+    w = np.zeros(64)
+    w[40:] = 1.0  # all particles in the upper part: cuts balance them
+    c = qdist.slab_cuts(64, 2, weights=w)
+    assert c[0][1] >= 40
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    sc = scenes.small_fluid_3d()
+    cuts = qdist.slab_cuts(sc.sim["grid_res"][2], world)
+    uid = qdist.share_unique_id(lambda: b"\x07" * 128)
+    assert uid == b"\x07" * 128
+    z_lo, z_hi = qdist.rank_zrange(cuts, rank, sc.sim["dx"])
+    if rank == 0:
+        z_lo = -np.inf
+    if rank == world - 1:
+        z_hi = np.inf
+    idx = np.concatenate([i for i, _ in sc.state_zrange(z_lo, z_hi, max_chunk=7000)])
+    n = torch.tensor([idx.size], dtype=torch.int64)
+    dist.all_reduce(n)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, idx)
+    if rank == 0:
+        allidx = np.sort(np.concatenate(gathered))
+        out.put((int(n.item()), bool(np.array_equal(allidx, np.arange(sc.n_particles))), sc.n_particles))
+    dist.destroy_process_group()
+
+
+def test_two_rank_generation_partitions_the_scene():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    total, exact, n = res
+    assert total == n and exact
