@@ -295,11 +295,157 @@ struct Smem {
   static constexpr int TILE = 16 * TN;
   static constexpr int STAGE = ((4 * 32 * SP::SW) + 15) / 16 * 16;
   static constexpr int PRM = 4 * 16 * 32;
-    static constexpr int P2G_WARP = TILE + 2 * STAGE;  // double-buffered stage; + the CTA's OrderSmem (static)
+  // P2G: two tiles, four chunk stages (two pairs) and two parameter blocks per warp
+  static constexpr int P2G_WARP = 2 * TILE + 4 * STAGE + 2 * PRM;  // + the CTA's OrderSmem (static)
   static constexpr int G2P_WARP = TILE + 2 * STAGE + 32;  // double-buffered stage + 8 neighbour slots
 };
 
 // ------------------------------------------------------------------ a3: P2G
+// phase 1 of the scatter: decode + stress of the lane's particle -> 16 parameters
+// (cell, fx, Q, a_k) parked in shared memory: the momentum at stencil node o is
+// m v + aff (o - fx) dx = Q + sum_k o_k a_k with a_k = dx aff[:,k], Q = m v - sum_k fx_k a_k.
+template <class SP>
+__device__ __forceinline__ void p2g_params(const uint32_t* w, bool valid, const int org[3], const SimDev& S,
+                                           float* prm, int lane) {
+  constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS;
+  float s[NSV];
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NSV; ++i) s[i] = sdec<SP>(w, i);
+  } else {
+    benign_state<D, MAT>(s, org, S.dx);
+  }
+  int lb[3] = {0, 0, 0};
+  float fx[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    bool o;
+    lb[a] = base_fx(s[a], S.inv_dx, S.res[a], fx[a], o) - org[a];
+  }
+  float aff[D * D];
+  affine_of<D, MAT>(s, S, aff);
+  float Q[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    Q[a] = S.p_mass * s[D + a];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const float akv = S.dx * aff[a * D + k];
+      Q[a] -= fx[k] * akv;
+      prm[(7 + k * 3 + a) * 32 + lane] = akv;
+    }
+  }
+  const int cell = valid ? (D == 3 ? (lb[0] * 4 + lb[1]) * 4 + lb[2] : lb[0] * 8 + lb[1]) : -1 - lane;
+  prm[0 * 32 + lane] = __int_as_float(cell);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    prm[(1 + a) * 32 + lane] = fx[a];
+    prm[(4 + a) * 32 + lane] = Q[a];
+  }
+}
+
+// phase 2 operand of one particle, read back from the parked parameters
+struct ScatterOp {
+  float wt[3][3], Q[3], ak[3][3];
+  int base_idx, rank;
+  bool active;
+};
+
+template <int D>
+__device__ __forceinline__ int scatter_setup(const float* prm, int lane, bool valid, ScatterOp& op) {
+  using G = Geo<D>;
+  const volatile float* vp = prm;
+  const int cell = __float_as_int(vp[0 * 32 + lane]);
+  float fx[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    fx[a] = vp[(1 + a) * 32 + lane];
+    op.Q[a] = vp[(4 + a) * 32 + lane];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) op.ak[k][a] = vp[(7 + k * 3 + a) * 32 + lane];
+  }
+  int lb[3];
+  if (D == 3) {
+    lb[0] = (cell >> 4) & 3;
+    lb[1] = (cell >> 2) & 3;
+    lb[2] = cell & 3;
+  } else {
+    lb[0] = (cell >> 3) & 7;
+    lb[1] = cell & 7;
+    lb[2] = 0;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) bspline_w(fx[a], op.wt[a]);
+  const unsigned peers = __match_any_sync(FULL, cell);
+  op.rank = __popc(peers & lanemask_lt());
+  op.active = valid;
+  op.base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
+  return __reduce_max_sync(FULL, (unsigned)__popc(peers));  // conflict rounds
+}
+
+// One WARP scatters two chunks at once, each into its own tile, so the two
+// read-modify-write chains (LDS -> FMA -> STS -> __syncwarp per stencil node) overlap.
+template <int D>
+__device__ __forceinline__ void scatter_pair(float4* tA, float4* tB, const ScatterOp& A, const ScatterOp& B,
+                                             int rounds, float p_mass) {
+  using G = Geo<D>;
+  for (int rr = 0; rr < rounds; ++rr) {
+    const bool ma = A.active && A.rank == rr, mb = B.active && B.rank == rr;
+    const unsigned m = __ballot_sync(FULL, ma || mb);
+    if (ma || mb) {
+#pragma unroll 1
+      for (int ox = 0; ox < 3; ++ox) {
+#pragma unroll
+        for (int oy = 0; oy < 3; ++oy) {
+          const float wa = A.wt[0][ox] * A.wt[1][oy], wb = B.wt[0][ox] * B.wt[1][oy];
+          float Ma[3], Mb[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            Ma[a] = A.Q[a] + ox * A.ak[0][a] + oy * A.ak[1][a];
+            Mb[a] = B.Q[a] + ox * B.ak[0][a] + oy * B.ak[1][a];
+          }
+#pragma unroll
+          for (int oz = 0; oz < (D == 3 ? 3 : 1); ++oz) {
+            const int off = D == 3 ? (ox * G::T + oy) * G::T + oz : ox * G::T + oy;
+            const float wwa = D == 3 ? wa * A.wt[2][oz] : wa, wwb = D == 3 ? wb * B.wt[2][oz] : wb;
+            float4 ta, tb;
+            if (ma) ta = tA[A.base_idx + off];
+            if (mb) tb = tB[B.base_idx + off];
+            if (ma) {
+              ta.x = fmaf(wwa, p_mass, ta.x);
+              ta.y = fmaf(wwa, Ma[0], ta.y);
+              ta.z = fmaf(wwa, Ma[1], ta.z);
+              ta.w = fmaf(wwa, Ma[2], ta.w);
+              tA[A.base_idx + off] = ta;
+            }
+            if (mb) {
+              tb.x = fmaf(wwb, p_mass, tb.x);
+              tb.y = fmaf(wwb, Mb[0], tb.y);
+              tb.z = fmaf(wwb, Mb[1], tb.z);
+              tb.w = fmaf(wwb, Mb[2], tb.w);
+              tB[B.base_idx + off] = tb;
+            }
+            __syncwarp(m);
+            if (D == 3) {
+#pragma unroll
+              for (int a = 0; a < 3; ++a) {
+                Ma[a] += A.ak[2][a];
+                Mb[a] += B.ak[2][a];
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// One CTA (WARPS warps) per active block, grid-stride.  The CTA orders the block's
+// particles by (rank in cell, cell); each warp takes 64 consecutive positions (two
+// chunks A, B), stages their records with cp.async (the next pair in flight while
+// this one computes), parks per-particle parameters, scatters A and B into its two
+// private tiles; the 2*WARPS tiles are summed and flushed with red.global.add.v4.f32.
 template <class SP>
 __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint32_t* __restrict__ perm,
                                          const uint8_t* __restrict__ cells,
@@ -308,16 +454,21 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
                                          const DevCounters* __restrict__ dc,
                                          const uint32_t* __restrict__ block_slot, float4* __restrict__ mp,
                                          const SimDev& S) {
-  constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, WARPS = SP::P2G_WARPS;
+  constexpr int D = SP::D, WARPS = SP::P2G_WARPS;
   using G = Geo<D>;
+  using SM = Smem<SP>;
   extern __shared__ float4 smem4[];
-  float4* tiles = smem4;                                                  // [WARPS][TN]
-  uint32_t* stage = reinterpret_cast<uint32_t*>(tiles + WARPS * G::TN);  // [WARPS][2][32][SW]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float4* tile = tiles + warp * G::TN;
-  uint32_t* wst = stage + warp * 2 * 32 * SP::SW;
+  float4* tiles = smem4;  // [2 * WARPS][TN]
+  char* wbase = reinterpret_cast<char*>(tiles + 2 * WARPS * G::TN) + warp * (4 * SM::STAGE + 2 * SM::PRM);
+  uint32_t* wst = reinterpret_cast<uint32_t*>(wbase);                   // [4][32][SW]: 2 pairs of chunk stages
+  float* prmA = reinterpret_cast<float*>(wbase + 4 * SM::STAGE);       // [16][32]
+  float* prmB = prmA + 16 * 32;
+  float4* tA = tiles + (2 * warp) * G::TN;
+  float4* tB = tiles + (2 * warp + 1) * G::TN;
   __shared__ OrderSmem ord;
   const uint32_t n_active = dc->n_active;
+  constexpr int SWW = 32 * SP::SW;  // words per chunk stage
 
   for (uint32_t ab = blockIdx.x; ab < n_active; ab += gridDim.x) {
     const uint32_t b = active_list[ab];
@@ -325,112 +476,52 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
     int bc[3];
     block_coords<D>(b, S, bc);
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
-    for (int t = threadIdx.x; t < WARPS * G::TN; t += blockDim.x) tiles[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int t = threadIdx.x; t < 2 * WARPS * G::TN; t += blockDim.x) tiles[t] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     for (uint32_t bs = start; bs < end; bs += kOrderCap) {
-    const uint32_t nb = min((uint32_t)kOrderCap, end - bs);
-    order_batch(perm + bs, cells + bs, nb, ord);  // (rank in cell, cell) order; perm rewritten
-    int buf = 0;
-    if (warp * 32 < (int)nb) {  // prefetch this warp's first chunk
-      const uint32_t c0 = min(32u, nb - warp * 32);
-      issue_records<SP>(rec, ord.q[warp * 32 + ((uint32_t)lane < c0 ? lane : 0)], c0, wst, lane);
-    }
-    for (uint32_t j0 = warp * 32; j0 < nb; j0 += WARPS * 32) {
-      const uint32_t cnt = min(32u, nb - j0);
-      const bool valid = (uint32_t)lane < cnt;
-      uint32_t w[SP::W + 1];
-      take_records<SP>(wst + buf * 32 * SP::SW, lane, w);
-      {  // records of the next chunk go in flight while this one computes
-        const uint32_t jn = j0 + WARPS * 32;
-        if (jn < nb) {
-          const uint32_t cn = min(32u, nb - jn);
-          issue_records<SP>(rec, ord.q[jn + ((uint32_t)lane < cn ? lane : 0)], cn, wst + (buf ^ 1) * 32 * SP::SW,
-                            lane);
-        }
-        buf ^= 1;
-      }
-      float s[NSV];
-      if (valid) {
+      const uint32_t nb = min((uint32_t)kOrderCap, end - bs);
+      order_batch(perm + bs, cells + bs, nb, ord);  // (rank in cell, cell) order; perm rewritten
+      auto issue_pair = [&](uint32_t jp, int set) {  // chunks [jp, jp+32) and [jp+32, jp+64)
 #pragma unroll
-        for (int i = 0; i < NSV; ++i) s[i] = sdec<SP>(w, i);
-      } else {
-        benign_state<D, MAT>(s, org, S.dx);
-      }
-      int lb[3] = {0, 0, 0};
-      float fx[3] = {0.f, 0.f, 0.f}, wt[3][3];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        bool o;
-        lb[a] = base_fx(s[a], S.inv_dx, S.res[a], fx[a], o) - org[a];
-        bspline_w(fx[a], wt[a]);
-      }
-      float aff[D * D];
-      affine_of<D, MAT>(s, S, aff);
-      // momentum at node o: m v + aff (o - fx) dx = Q + sum_k o_k a_k,  a_k = dx aff[:,k]
-      float ak[3][3], Q[3];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        Q[a] = S.p_mass * s[D + a];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          ak[k][a] = S.dx * aff[a * D + k];
-          Q[a] -= fx[k] * ak[k][a];
-        }
-      }
-      const int cell = valid ? (D == 3 ? (lb[0] * 4 + lb[1]) * 4 + lb[2] : lb[0] * 8 + lb[1]) : -1 - lane;
-      const unsigned peers = __match_any_sync(FULL, cell);
-      const int rank = __popc(peers & lanemask_lt());
-      const int rounds = __reduce_max_sync(FULL, (unsigned)__popc(peers));
-      const int base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
-      for (int rr = 0; rr < rounds; ++rr) {
-        const bool mine = valid && rank == rr;
-        const unsigned m = __ballot_sync(FULL, mine);
-        if (mine) {
-#pragma unroll
-          for (int ox = 0; ox < 3; ++ox) {
-#pragma unroll
-            for (int oy = 0; oy < 3; ++oy) {
-              const float wxy = wt[0][ox] * wt[1][oy];
-              float M[3];
-#pragma unroll
-              for (int a = 0; a < 3; ++a) M[a] = Q[a] + ox * ak[0][a] + oy * ak[1][a];
-              if (D == 3) {
-#pragma unroll
-                for (int oz = 0; oz < 3; ++oz) {
-                  const float ww = wxy * wt[2][oz];
-                  const int idx = base_idx + (ox * G::T + oy) * G::T + oz;
-                  float4 t = tile[idx];
-                  t.x = fmaf(ww, S.p_mass, t.x);
-                  t.y = fmaf(ww, M[0], t.y);
-                  t.z = fmaf(ww, M[1], t.z);
-                  t.w = fmaf(ww, M[2], t.w);
-                  tile[idx] = t;
-                  __syncwarp(m);
-#pragma unroll
-                  for (int a = 0; a < 3; ++a) M[a] += ak[2][a];
-                }
-              } else {
-                const int idx = base_idx + ox * G::T + oy;
-                float4 t = tile[idx];
-                t.x = fmaf(wxy, S.p_mass, t.x);
-                t.y = fmaf(wxy, M[0], t.y);
-                t.z = fmaf(wxy, M[1], t.z);
-                tile[idx] = t;
-                __syncwarp(m);
-              }
-            }
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t j = jp + 32 * h;
+          if (j < nb) {
+            const uint32_t c = min(32u, nb - j);
+            issue_records<SP>(rec, ord.q[j + ((uint32_t)lane < c ? lane : 0)], c, wst + (2 * set + h) * SWW, lane);
           }
         }
+      };
+      int set = 0;
+      issue_pair(warp * 64, 0);
+      for (uint32_t j0 = warp * 64; j0 < nb; j0 += WARPS * 64) {
+        const uint32_t ca = min(32u, nb - j0);
+        const uint32_t cb = j0 + 32 < nb ? min(32u, nb - j0 - 32) : 0u;
+        const bool va = (uint32_t)lane < ca, vb = (uint32_t)lane < cb;
+        uint32_t wa[SP::W + 1], wb[SP::W + 1];
+        take_records<SP>(wst + (2 * set) * SWW, lane, wa);
+        if (cb) {
+          take_records<SP>(wst + (2 * set + 1) * SWW, lane, wb);
+        } else {
+#pragma unroll
+          for (int q = 0; q <= SP::W; ++q) wb[q] = 0u;
+        }
+        if (j0 + WARPS * 64 < nb) issue_pair(j0 + WARPS * 64, set ^ 1);
+        set ^= 1;
+        p2g_params<SP>(wa, va, org, S, prmA, lane);
+        p2g_params<SP>(wb, vb, org, S, prmB, lane);
         __syncwarp();
+        ScatterOp A, B;
+        const int ra = scatter_setup<D>(prmA, lane, va, A);
+        const int rb = scatter_setup<D>(prmB, lane, vb, B);
+        scatter_pair<D>(tA, tB, A, B, max(ra, rb), S.p_mass);
       }
+      __syncthreads();  // the batch's order arrays are reused by the next batch
     }
-    __syncthreads();  // the batch's order arrays are reused by the next batch
-    }
-    // flush: sum the warp tiles, one vector reduction per non-empty node
+    // flush: sum the 2*WARPS tiles, one vector reduction per non-empty node
     for (int t = threadIdx.x; t < G::TN; t += blockDim.x) {
       float4 acc = tiles[t];
 #pragma unroll
-      for (int wv = 1; wv < WARPS; ++wv) {
+      for (int wv = 1; wv < 2 * WARPS; ++wv) {
         const float4 o = tiles[wv * G::TN + t];
         acc.x += o.x;
         acc.y += o.y;
@@ -440,13 +531,13 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
       if (acc.x != 0.0f) {
         int node[3];
         tile_node<D>(t, org, node);
-        int nb[3], ln[3];
+        int nbk[3], ln[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          nb[a] = node[a] >> G::LB;
+          nbk[a] = node[a] >> G::LB;
           ln[a] = node[a] & (G::B - 1);
         }
-        const uint32_t slot = block_slot[block_id<D>(nb, S)];
+        const uint32_t slot = block_slot[block_id<D>(nbk, S)];
         if (slot != 0xffffffffu) atomicAdd(&mp[(size_t)slot * 64 + local_node<D>(ln)], acc);
       }
     }
