@@ -475,14 +475,14 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   }
   // specialise the step kernels on this layout (NVRTC, sm_100a)
   {
-    constexpr int kP2GWarps = 4, kG2PWarps = 4;
+    constexpr int kP2GWarps = 2, kG2PWarps = 4;  // P2G: 64 lanes = the 64 cells of a block
     // minimum resident CTAs per SM the kernels are compiled for (register cap);
     // QMPM_P2G_MINB / QMPM_G2P_MINB override the defaults for tuning runs
     auto env_int = [](const char* name, int dflt) {
       const char* v = getenv(name);
       return (v && *v) ? atoi(v) : dflt;
     };
-    const int kP2GMinBlocks = env_int("QMPM_P2G_MINB", 3), kG2PMinBlocks = env_int("QMPM_G2P_MINB", 4);
+    const int kP2GMinBlocks = env_int("QMPM_P2G_MINB", 6), kG2PMinBlocks = env_int("QMPM_G2P_MINB", 4);
     ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps, kP2GMinBlocks, kG2PMinBlocks);
     JitModule m;
     std::string jerr;

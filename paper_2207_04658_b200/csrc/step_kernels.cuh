@@ -295,8 +295,9 @@ struct Smem {
   static constexpr int TILE = 16 * TN;
   static constexpr int STAGE = ((4 * 32 * SP::SW) + 15) / 16 * 16;
   static constexpr int PRM = 4 * 16 * 32;
-  // P2G: two tiles, four chunk stages (two pairs) and two parameter blocks per warp
-  static constexpr int P2G_WARP = 2 * TILE + 4 * STAGE + 2 * PRM;  // + the CTA's OrderSmem (static)
+  // P2G (2 warps per CTA): per warp one tile, two chunk stages and half of the
+  // [16][kCellCap] parameter block; + the CTA's CellSmem (static)
+  static constexpr int P2G_WARP = TILE + 2 * STAGE + 16 * 4 * 256 / 2;
   static constexpr int G2P_WARP = TILE + 2 * STAGE + 32;  // double-buffered stage + 8 neighbour slots
 };
 
@@ -306,7 +307,8 @@ struct Smem {
 // m v + aff (o - fx) dx = Q + sum_k o_k a_k with a_k = dx aff[:,k], Q = m v - sum_k fx_k a_k.
 template <class SP>
 __device__ __forceinline__ void p2g_params(const uint32_t* w, bool valid, const int org[3], const SimDev& S,
-                                           float* prm, int lane) {
+                                           float* prm, int stride) {
+  const int lane = threadIdx.x & 31;
   constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS;
   float s[NSV];
   if (valid) {
@@ -332,120 +334,40 @@ __device__ __forceinline__ void p2g_params(const uint32_t* w, bool valid, const 
     for (int k = 0; k < D; ++k) {
       const float akv = S.dx * aff[a * D + k];
       Q[a] -= fx[k] * akv;
-      prm[(7 + k * 3 + a) * 32 + lane] = akv;
+      if (valid) prm[(7 + k * 3 + a) * stride + lane] = akv;
     }
   }
-  const int cell = valid ? (D == 3 ? (lb[0] * 4 + lb[1]) * 4 + lb[2] : lb[0] * 8 + lb[1]) : -1 - lane;
-  prm[0 * 32 + lane] = __int_as_float(cell);
+  if (!valid) return;
+  prm[0 * stride + lane] = __int_as_float(D == 3 ? (lb[0] * 4 + lb[1]) * 4 + lb[2] : lb[0] * 8 + lb[1]);
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    prm[(1 + a) * 32 + lane] = fx[a];
-    prm[(4 + a) * 32 + lane] = Q[a];
+    prm[(1 + a) * stride + lane] = fx[a];
+    prm[(4 + a) * stride + lane] = Q[a];
   }
 }
 
-// phase 2 operand of one particle, read back from the parked parameters
-struct ScatterOp {
-  float wt[3][3], Q[3], ak[3][3];
-  int base_idx, rank;
-  bool active;
+// One CTA of 2 warps (64 lanes = the 64 base cells of a block) per active block,
+// grid-stride.  Per batch of <= kCellCap particles of the block:
+//   1. counting sort by base cell (cells[] from the scatter, warp-aggregated ranks);
+//   2. phase 1: both warps stage records (cp.async, the next chunk in flight) and park
+//      16 parameters per particle in shared memory (structure of arrays);
+//   3. phase 2: lane c OWNS cell c: it loops over its cell's particles accumulating
+//      one stencil layer (fixed ox: 3^(d-1) nodes x 4 channels) in registers, then
+//      read-modify-writes those nodes of its warp's private tile.  Lanes own distinct
+//      cells, so one layer's RMW never collides; __syncwarp orders successive nodes.
+//      The shared-memory RMW count drops from 27 per particle to 27 per cell.
+// The two warp tiles are summed and flushed with red.global.add.v4.f32.
+constexpr int kCellCap = 256;
+
+struct CellSmem {
+  uint32_t p[kCellCap];   // perm entries of the batch
+  uint32_t q[kCellCap];   // sorted by cell
+  uint16_t pos[kCellCap];
+  uint8_t cell[kCellCap];
+  uint32_t cnt[64];
+  uint32_t cstart[65];
 };
 
-template <int D>
-__device__ __forceinline__ int scatter_setup(const float* prm, int lane, bool valid, ScatterOp& op) {
-  using G = Geo<D>;
-  const volatile float* vp = prm;
-  const int cell = __float_as_int(vp[0 * 32 + lane]);
-  float fx[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    fx[a] = vp[(1 + a) * 32 + lane];
-    op.Q[a] = vp[(4 + a) * 32 + lane];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) op.ak[k][a] = vp[(7 + k * 3 + a) * 32 + lane];
-  }
-  int lb[3];
-  if (D == 3) {
-    lb[0] = (cell >> 4) & 3;
-    lb[1] = (cell >> 2) & 3;
-    lb[2] = cell & 3;
-  } else {
-    lb[0] = (cell >> 3) & 7;
-    lb[1] = cell & 7;
-    lb[2] = 0;
-  }
-#pragma unroll
-  for (int a = 0; a < 3; ++a) bspline_w(fx[a], op.wt[a]);
-  const unsigned peers = __match_any_sync(FULL, cell);
-  op.rank = __popc(peers & lanemask_lt());
-  op.active = valid;
-  op.base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
-  return __reduce_max_sync(FULL, (unsigned)__popc(peers));  // conflict rounds
-}
-
-// One WARP scatters two chunks at once, each into its own tile, so the two
-// read-modify-write chains (LDS -> FMA -> STS -> __syncwarp per stencil node) overlap.
-template <int D>
-__device__ __forceinline__ void scatter_pair(float4* tA, float4* tB, const ScatterOp& A, const ScatterOp& B,
-                                             int rounds, float p_mass) {
-  using G = Geo<D>;
-  for (int rr = 0; rr < rounds; ++rr) {
-    const bool ma = A.active && A.rank == rr, mb = B.active && B.rank == rr;
-    const unsigned m = __ballot_sync(FULL, ma || mb);
-    if (ma || mb) {
-#pragma unroll 1
-      for (int ox = 0; ox < 3; ++ox) {
-#pragma unroll
-        for (int oy = 0; oy < 3; ++oy) {
-          const float wa = A.wt[0][ox] * A.wt[1][oy], wb = B.wt[0][ox] * B.wt[1][oy];
-          float Ma[3], Mb[3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            Ma[a] = A.Q[a] + ox * A.ak[0][a] + oy * A.ak[1][a];
-            Mb[a] = B.Q[a] + ox * B.ak[0][a] + oy * B.ak[1][a];
-          }
-#pragma unroll
-          for (int oz = 0; oz < (D == 3 ? 3 : 1); ++oz) {
-            const int off = D == 3 ? (ox * G::T + oy) * G::T + oz : ox * G::T + oy;
-            const float wwa = D == 3 ? wa * A.wt[2][oz] : wa, wwb = D == 3 ? wb * B.wt[2][oz] : wb;
-            float4 ta, tb;
-            if (ma) ta = tA[A.base_idx + off];
-            if (mb) tb = tB[B.base_idx + off];
-            if (ma) {
-              ta.x = fmaf(wwa, p_mass, ta.x);
-              ta.y = fmaf(wwa, Ma[0], ta.y);
-              ta.z = fmaf(wwa, Ma[1], ta.z);
-              ta.w = fmaf(wwa, Ma[2], ta.w);
-              tA[A.base_idx + off] = ta;
-            }
-            if (mb) {
-              tb.x = fmaf(wwb, p_mass, tb.x);
-              tb.y = fmaf(wwb, Mb[0], tb.y);
-              tb.z = fmaf(wwb, Mb[1], tb.z);
-              tb.w = fmaf(wwb, Mb[2], tb.w);
-              tB[B.base_idx + off] = tb;
-            }
-            __syncwarp(m);
-            if (D == 3) {
-#pragma unroll
-              for (int a = 0; a < 3; ++a) {
-                Ma[a] += A.ak[2][a];
-                Mb[a] += B.ak[2][a];
-              }
-            }
-          }
-        }
-      }
-    }
-    __syncwarp();
-  }
-}
-
-// One CTA (WARPS warps) per active block, grid-stride.  The CTA orders the block's
-// particles by (rank in cell, cell); each warp takes 64 consecutive positions (two
-// chunks A, B), stages their records with cp.async (the next pair in flight while
-// this one computes), parks per-particle parameters, scatters A and B into its two
-// private tiles; the 2*WARPS tiles are summed and flushed with red.global.add.v4.f32.
 template <class SP>
 __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint32_t* __restrict__ perm,
                                          const uint8_t* __restrict__ cells,
@@ -454,21 +376,19 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
                                          const DevCounters* __restrict__ dc,
                                          const uint32_t* __restrict__ block_slot, float4* __restrict__ mp,
                                          const SimDev& S) {
-  constexpr int D = SP::D, WARPS = SP::P2G_WARPS;
+  constexpr int D = SP::D;
   using G = Geo<D>;
   using SM = Smem<SP>;
-  extern __shared__ float4 smem4[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float4* tiles = smem4;  // [2 * WARPS][TN]
-  char* wbase = reinterpret_cast<char*>(tiles + 2 * WARPS * G::TN) + warp * (4 * SM::STAGE + 2 * SM::PRM);
-  uint32_t* wst = reinterpret_cast<uint32_t*>(wbase);                   // [4][32][SW]: 2 pairs of chunk stages
-  float* prmA = reinterpret_cast<float*>(wbase + 4 * SM::STAGE);       // [16][32]
-  float* prmB = prmA + 16 * 32;
-  float4* tA = tiles + (2 * warp) * G::TN;
-  float4* tB = tiles + (2 * warp + 1) * G::TN;
-  __shared__ OrderSmem ord;
-  const uint32_t n_active = dc->n_active;
   constexpr int SWW = 32 * SP::SW;  // words per chunk stage
+  extern __shared__ float4 smem4[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float4* tiles = smem4;                                                            // [2][TN]
+  float* prm = reinterpret_cast<float*>(tiles + 2 * G::TN);                         // [16][kCellCap]
+  uint32_t* stage = reinterpret_cast<uint32_t*>(prm + 16 * kCellCap);               // [2 warps][2][SWW]
+  uint32_t* wst = stage + warp * 2 * SWW;
+  float4* tile = tiles + warp * G::TN;
+  __shared__ CellSmem cs;
+  const uint32_t n_active = dc->n_active;
 
   for (uint32_t ab = blockIdx.x; ab < n_active; ab += gridDim.x) {
     const uint32_t b = active_list[ab];
@@ -476,66 +396,170 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
     int bc[3];
     block_coords<D>(b, S, bc);
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
-    for (int t = threadIdx.x; t < 2 * WARPS * G::TN; t += blockDim.x) tiles[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int t = tid; t < 2 * G::TN; t += 64) tiles[t] = make_float4(0.f, 0.f, 0.f, 0.f);
 
-    for (uint32_t bs = start; bs < end; bs += kOrderCap) {
-      const uint32_t nb = min((uint32_t)kOrderCap, end - bs);
-      order_batch(perm + bs, cells + bs, nb, ord);  // (rank in cell, cell) order; perm rewritten
-      auto issue_pair = [&](uint32_t jp, int set) {  // chunks [jp, jp+32) and [jp+32, jp+64)
+    for (uint32_t bs = start; bs < end; bs += kCellCap) {
+      const uint32_t nb = min((uint32_t)kCellCap, end - bs);
+      // ---- 1. counting sort of the batch by base cell
+      cs.cnt[tid] = 0u;
+      __syncthreads();
+      for (uint32_t i0 = warp * 32; i0 < nb; i0 += 64) {
+        const uint32_t i = i0 + lane;
+        const bool v = i < nb;
+        const uint32_t c = v ? (uint32_t)cells[bs + i] : 64u + lane;
+        const unsigned peers = __match_any_sync(FULL, c);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (v && lane == leader) base = atomicAdd(&cs.cnt[c], (unsigned)__popc(peers));
+        base = __shfl_sync(FULL, base, leader);
+        if (v) {
+          cs.p[i] = perm[bs + i];
+          cs.cell[i] = (uint8_t)c;
+          cs.pos[i] = (uint16_t)(base + __popc(peers & lanemask_lt()));
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {  // exclusive scan of the 64 cell counts
+        const uint32_t c0 = cs.cnt[lane], c1 = cs.cnt[lane + 32];
+        uint32_t i0 = c0, i1 = c1;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t j = jp + 32 * h;
-          if (j < nb) {
-            const uint32_t c = min(32u, nb - j);
-            issue_records<SP>(rec, ord.q[j + ((uint32_t)lane < c ? lane : 0)], c, wst + (2 * set + h) * SWW, lane);
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t0 = __shfl_up_sync(FULL, i0, d), t1 = __shfl_up_sync(FULL, i1, d);
+          if (lane >= d) {
+            i0 += t0;
+            i1 += t1;
           }
         }
-      };
-      int set = 0;
-      issue_pair(warp * 64, 0);
-      for (uint32_t j0 = warp * 64; j0 < nb; j0 += WARPS * 64) {
-        const uint32_t ca = min(32u, nb - j0);
-        const uint32_t cb = j0 + 32 < nb ? min(32u, nb - j0 - 32) : 0u;
-        const bool va = (uint32_t)lane < ca, vb = (uint32_t)lane < cb;
-        uint32_t wa[SP::W + 1], wb[SP::W + 1];
-        take_records<SP>(wst + (2 * set) * SWW, lane, wa);
-        if (cb) {
-          take_records<SP>(wst + (2 * set + 1) * SWW, lane, wb);
-        } else {
-#pragma unroll
-          for (int q = 0; q <= SP::W; ++q) wb[q] = 0u;
+        const uint32_t tot0 = __shfl_sync(FULL, i0, 31);
+        cs.cstart[lane] = i0 - c0;
+        cs.cstart[lane + 32] = tot0 + i1 - c1;
+        if (lane == 31) cs.cstart[64] = tot0 + i1;
+      }
+      __syncthreads();
+      for (uint32_t i = tid; i < nb; i += 64) {
+        const uint32_t q = cs.cstart[cs.cell[i]] + cs.pos[i];
+        cs.q[q] = cs.p[i];
+        perm[bs + q] = cs.p[i];  // G2P processes the block in the same order
+      }
+      __syncthreads();
+      // ---- 2. phase 1: parameters of every particle of the batch
+      {
+        int buf = 0;
+        uint32_t j0 = warp * 32;
+        if (j0 < nb) {
+          const uint32_t c0 = min(32u, nb - j0);
+          issue_records<SP>(rec, cs.q[j0 + ((uint32_t)lane < c0 ? lane : 0)], c0, wst, lane);
         }
-        if (j0 + WARPS * 64 < nb) issue_pair(j0 + WARPS * 64, set ^ 1);
-        set ^= 1;
-        p2g_params<SP>(wa, va, org, S, prmA, lane);
-        p2g_params<SP>(wb, vb, org, S, prmB, lane);
-        __syncwarp();
-        ScatterOp A, B;
-        const int ra = scatter_setup<D>(prmA, lane, va, A);
-        const int rb = scatter_setup<D>(prmB, lane, vb, B);
-        scatter_pair<D>(tA, tB, A, B, max(ra, rb), S.p_mass);
+        for (; j0 < nb; j0 += 64) {
+          const uint32_t cnt = min(32u, nb - j0);
+          const bool valid = (uint32_t)lane < cnt;
+          uint32_t w[SP::W + 1];
+          take_records<SP>(wst + buf * SWW, lane, w);
+          const uint32_t jn = j0 + 64;
+          if (jn < nb) {
+            const uint32_t cn = min(32u, nb - jn);
+            issue_records<SP>(rec, cs.q[jn + ((uint32_t)lane < cn ? lane : 0)], cn, wst + (buf ^ 1) * SWW, lane);
+          }
+          buf ^= 1;
+          p2g_params<SP>(w, valid, org, S, prm + j0, kCellCap);
+        }
       }
-      __syncthreads();  // the batch's order arrays are reused by the next batch
-    }
-    // flush: sum the 2*WARPS tiles, one vector reduction per non-empty node
-    for (int t = threadIdx.x; t < G::TN; t += blockDim.x) {
-      float4 acc = tiles[t];
+      __syncthreads();
+      // ---- 3. phase 2: lane `tid` owns base cell `tid`
+      {
+        const int c = tid;
+        const uint32_t k0 = cs.cstart[c], k1 = cs.cstart[c + 1];
+        const unsigned has = __ballot_sync(FULL, k1 > k0);
+        int lb[3];
+        if (D == 3) {
+          lb[0] = (c >> 4) & 3;
+          lb[1] = (c >> 2) & 3;
+          lb[2] = c & 3;
+        } else {
+          lb[0] = (c >> 3) & 7;
+          lb[1] = c & 7;
+          lb[2] = 0;
+        }
+        const int base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
+        const uint32_t kmax = __reduce_max_sync(FULL, k1 - k0);
+        if (has) {
+#pragma unroll 1
+          for (int ox = 0; ox < 3; ++ox) {
+            constexpr int NL = D == 3 ? 9 : 3;  // nodes of one layer
+            float am[NL], ax[NL], ay[NL], az[NL];
 #pragma unroll
-      for (int wv = 1; wv < 2 * WARPS; ++wv) {
-        const float4 o = tiles[wv * G::TN + t];
-        acc.x += o.x;
-        acc.y += o.y;
-        acc.z += o.z;
-        acc.w += o.w;
+            for (int q = 0; q < NL; ++q) am[q] = ax[q] = ay[q] = az[q] = 0.0f;
+            for (uint32_t k = 0; k < kmax; ++k) {
+              if (k0 + k < k1) {
+                const uint32_t pi = k0 + k;
+                const float fx0 = prm[1 * kCellCap + pi], fx1 = prm[2 * kCellCap + pi];
+                float wq[3], wy[3], wz[3] = {1.f, 0.f, 0.f};
+                bspline_w(fx0, wq);
+                bspline_w(fx1, wy);
+                if (D == 3) bspline_w(prm[3 * kCellCap + pi], wz);
+                const float wxo = wq[ox];
+                float M[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) M[a] = prm[(4 + a) * kCellCap + pi] + ox * prm[(7 + a) * kCellCap + pi];
+                float a1[3], a2[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                  a1[a] = prm[(10 + a) * kCellCap + pi];
+                  a2[a] = prm[(13 + a) * kCellCap + pi];
+                }
+#pragma unroll
+                for (int oy = 0; oy < 3; ++oy) {
+                  const float wxy = wxo * wy[oy];
+                  float My[3] = {M[0] + oy * a1[0], M[1] + oy * a1[1], M[2] + oy * a1[2]};
+#pragma unroll
+                  for (int oz = 0; oz < (D == 3 ? 3 : 1); ++oz) {
+                    const int q = D == 3 ? oy * 3 + oz : oy;
+                    const float ww = D == 3 ? wxy * wz[oz] : wxy;
+                    am[q] += ww;
+                    ax[q] = fmaf(ww, My[0], ax[q]);
+                    ay[q] = fmaf(ww, My[1], ay[q]);
+                    az[q] = fmaf(ww, My[2], az[q]);
+                    if (D == 3) {
+                      My[0] += a2[0];
+                      My[1] += a2[1];
+                      My[2] += a2[2];
+                    }
+                  }
+                }
+              }
+            }
+            // one RMW per node of the layer (m = p_mass * sum w)
+#pragma unroll
+            for (int q = 0; q < NL; ++q) {
+              const int oy = D == 3 ? q / 3 : q, oz = D == 3 ? q % 3 : 0;
+              const int idx = base_idx + (D == 3 ? (ox * G::T + oy) * G::T + oz : ox * G::T + oy);
+              if (k1 > k0) {
+                float4 t = tile[idx];
+                t.x = fmaf(am[q], S.p_mass, t.x);
+                t.y += ax[q];
+                t.z += ay[q];
+                t.w += az[q];
+                tile[idx] = t;
+              }
+              __syncwarp();
+            }
+          }
+        }
       }
+      __syncthreads();  // parameters and sort arrays are reused by the next batch
+    }
+    // flush: sum the two warp tiles, one vector reduction per non-empty node
+    for (int t = tid; t < G::TN; t += 64) {
+      const float4 a = tiles[t], o = tiles[G::TN + t];
+      const float4 acc = make_float4(a.x + o.x, a.y + o.y, a.z + o.z, a.w + o.w);
       if (acc.x != 0.0f) {
         int node[3];
         tile_node<D>(t, org, node);
         int nbk[3], ln[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          nbk[a] = node[a] >> G::LB;
-          ln[a] = node[a] & (G::B - 1);
+        for (int a2 = 0; a2 < 3; ++a2) {
+          nbk[a2] = node[a2] >> G::LB;
+          ln[a2] = node[a2] & (G::B - 1);
         }
         const uint32_t slot = block_slot[block_id<D>(nbk, S)];
         if (slot != 0xffffffffu) atomicAdd(&mp[(size_t)slot * 64 + local_node<D>(ln)], acc);
@@ -799,7 +823,7 @@ extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t*
   qmpm::bin_count_body<Spec>(rec, first, n, S, key, block_count, do_count);
 }
 
-extern "C" __global__ void __launch_bounds__(Spec::P2G_WARPS * 32, Spec::P2G_MINB)
+extern "C" __global__ void __launch_bounds__(64, Spec::P2G_MINB)
     qmpm_p2g(const uint32_t* rec, uint32_t* perm, const uint8_t* cells, const uint32_t* block_start,
              const uint32_t* active_list, const qmpm::DevCounters* dc, const uint32_t* block_slot, float4* mp,
              qmpm::SimDev S) {
