@@ -288,6 +288,9 @@ __device__ __forceinline__ void order_batch(uint32_t* __restrict__ perm, const u
   __syncthreads();
 }
 
+#ifndef QMPM_CELL_CAP
+#define QMPM_CELL_CAP 256
+#endif
 // per-warp shared-memory footprint of the two step kernels (16-byte multiples)
 template <class SP>
 struct Smem {
@@ -297,7 +300,7 @@ struct Smem {
   static constexpr int PRM = 4 * 16 * 32;
   // P2G (2 warps per CTA): per warp one tile, two chunk stages and half of the
   // [16][kCellCap] parameter block; + the CTA's CellSmem (static)
-  static constexpr int P2G_WARP = TILE + 2 * STAGE + 16 * 4 * 256 / 2;
+  static constexpr int P2G_WARP = TILE + 2 * STAGE + 16 * 4 * QMPM_CELL_CAP / 2;
   static constexpr int G2P_WARP = TILE + 2 * STAGE + 32;  // double-buffered stage + 8 neighbour slots
 };
 
@@ -357,7 +360,10 @@ __device__ __forceinline__ void p2g_params(const uint32_t* w, bool valid, const 
 //      cells, so one layer's RMW never collides; __syncwarp orders successive nodes.
 //      The shared-memory RMW count drops from 27 per particle to 27 per cell.
 // The two warp tiles are summed and flushed with red.global.add.v4.f32.
-constexpr int kCellCap = 256;
+#ifndef QMPM_CELL_CAP
+#define QMPM_CELL_CAP 256
+#endif
+constexpr int kCellCap = QMPM_CELL_CAP;  // particles per P2G batch
 
 struct CellSmem {
   uint32_t p[kCellCap];   // perm entries of the batch
@@ -398,22 +404,28 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
     for (int t = tid; t < 2 * G::TN; t += 64) tiles[t] = make_float4(0.f, 0.f, 0.f, 0.f);
 
-    for (uint32_t bs = start; bs < end; bs += kCellCap) {
-      const uint32_t nb = min((uint32_t)kCellCap, end - bs);
+    // batches are strided samples of the block (element i of batch bi is block
+    // particle bi + i * nbatch), so every batch spans all cells even when the block's
+    // particles arrive grouped by cell
+    const uint32_t n_blk = end - start;
+    const uint32_t nbatch = (n_blk + kCellCap - 1) / kCellCap;
+    for (uint32_t bi = 0; bi < nbatch; ++bi) {
+      const uint32_t nb = (n_blk - bi + nbatch - 1) / nbatch;
       // ---- 1. counting sort of the batch by base cell
       cs.cnt[tid] = 0u;
       __syncthreads();
       for (uint32_t i0 = warp * 32; i0 < nb; i0 += 64) {
         const uint32_t i = i0 + lane;
         const bool v = i < nb;
-        const uint32_t c = v ? (uint32_t)cells[bs + i] : 64u + lane;
+        const uint32_t gi = start + bi + i * nbatch;
+        const uint32_t c = v ? (uint32_t)cells[gi] : 64u + lane;
         const unsigned peers = __match_any_sync(FULL, c);
         const int leader = __ffs(peers) - 1;
         uint32_t base = 0;
         if (v && lane == leader) base = atomicAdd(&cs.cnt[c], (unsigned)__popc(peers));
         base = __shfl_sync(FULL, base, leader);
         if (v) {
-          cs.p[i] = perm[bs + i];
+          cs.p[i] = perm[gi];
           cs.cell[i] = (uint8_t)c;
           cs.pos[i] = (uint16_t)(base + __popc(peers & lanemask_lt()));
         }
@@ -439,7 +451,6 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
       for (uint32_t i = tid; i < nb; i += 64) {
         const uint32_t q = cs.cstart[cs.cell[i]] + cs.pos[i];
         cs.q[q] = cs.p[i];
-        perm[bs + q] = cs.p[i];  // G2P processes the block in the same order
       }
       __syncthreads();
       // ---- 2. phase 1: parameters of every particle of the batch
