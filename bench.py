@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--scheme", default=None, help="x16 | e0.1 | e0.01 | f2 | fp32")
     ap.add_argument("--n", type=int, default=0, help="override particle count (reduced runs)")
+    ap.add_argument("--z-extent", type=float, default=1.0,
+                    help="C4 only: z extent of the 1-GPU domain (reduced same-density runs for profiling)")
     ap.add_argument("--scene-warmup", type=int, default=50)
     ap.add_argument("--rounding", default="dither", choices=["dither", "rne"])
     ap.add_argument("--no-counters", action="store_true")
@@ -67,7 +69,7 @@ def make_scene(args, world=1):
         sc = scenes.c3(n_target=args.n or scenes.C3_PARTICLES)
         sch = schemes.e001()
     else:
-        sc = scenes.c4(n_target=(args.n or 400_000_000) * world, z_extent=float(world))
+        sc = scenes.c4(n_target=(args.n or 400_000_000) * world, z_extent=float(world) * args.z_extent)
         sch = schemes.f2()
     if args.scheme:
         sch = schemes.fp32(sc.dim, sc.material) if args.scheme == "fp32" else schemes.BY_NAME[args.scheme]()

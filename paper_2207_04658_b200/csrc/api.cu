@@ -51,6 +51,7 @@ struct qmpm_ctx {
   uint32_t* key = nullptr;
   uint32_t* perm = nullptr;
   uint8_t* cells = nullptr;
+  uint32_t* perm_cell = nullptr;
   uint32_t *block_count = nullptr, *block_start = nullptr, *block_slot = nullptr;
   uint32_t *active_list = nullptr, *touched_list = nullptr;
   uint4 *tile_sums = nullptr, *tile_off = nullptr;
@@ -302,7 +303,7 @@ qmpm_status qmpm_layout(const qmpm_scheme* scheme, uint32_t* words_per_particle,
 qmpm_status qmpm_destroy(qmpm_ctx* ctx) {
   if (!ctx) return QMPM_OK;
   cudaStreamSynchronize(ctx->stream);
-  void* ptrs[] = {ctx->rec[0], ctx->rec[1], ctx->ids[0], ctx->ids[1], ctx->key, ctx->perm, ctx->cells,
+  void* ptrs[] = {ctx->rec[0], ctx->rec[1], ctx->ids[0], ctx->ids[1], ctx->key, ctx->perm, ctx->cells, ctx->perm_cell,
                   ctx->block_count, ctx->block_start, ctx->block_slot, ctx->active_list, ctx->touched_list,
                   ctx->tile_sums, ctx->tile_off, ctx->mp, ctx->gv, ctx->dc, ctx->dbg};
   for (void* p : ptrs)
@@ -451,6 +452,7 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   ALLOC(ctx->key, sizeof(uint32_t) * cap);
   ALLOC(ctx->perm, sizeof(uint32_t) * cap);
   ALLOC(ctx->cells, cap);
+  ALLOC(ctx->perm_cell, sizeof(uint32_t) * cap);
   ALLOC(ctx->block_count, sizeof(uint32_t) * nblocks);
   ALLOC(ctx->block_start, sizeof(uint32_t) * (nblocks + 1));
   ALLOC(ctx->block_slot, sizeof(uint32_t) * nblocks);
@@ -580,6 +582,7 @@ StepBuffers buffers(qmpm_ctx* ctx, uint64_t n) {
   B.key = ctx->key;
   B.perm = ctx->perm;
   B.cells = ctx->cells;
+  B.perm_cell = ctx->perm_cell;
   B.block_count = ctx->block_count;
   B.block_start = ctx->block_start;
   B.block_slot = ctx->block_slot;

@@ -435,8 +435,9 @@ cudaError_t launch_p2g(const StepBuffers& B, const SimDev& S, const StepJit& J, 
   Hk H{hook, user};
   H(KP2G, 1);
   SimDev Sv = S;
-  void* args[] = {(void*)&B.rec_in, (void*)&B.perm,        (void*)&B.cells, (void*)&B.block_start,
-                  (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot, (void*)&B.mp, (void*)&Sv};
+  void* args[] = {(void*)&B.rec_in,      (void*)&B.perm, (void*)&B.cells,      (void*)&B.perm_cell,
+                  (void*)&B.block_start, (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot,
+                  (void*)&B.mp,          (void*)&Sv};
   cudaError_t e = jit_launch(J.p2g, J.p2g_ctas, J.p2g_threads, J.p2g_smem, st, args);
   H(KP2G, 0);
   return e;
@@ -460,7 +461,7 @@ cudaError_t launch_g2p(const StepBuffers& B, const SimDev& S, uint32_t salt, con
   H(KG2P, 1);
   SimDev Sv = S;
   uint32_t saltv = salt;
-  void* args[] = {(void*)&B.rec_in, (void*)&B.rec_out, (void*)&B.perm, (void*)&B.ids_in, (void*)&B.ids_out,
+  void* args[] = {(void*)&B.rec_in, (void*)&B.rec_out, (void*)&B.perm_cell, (void*)&B.ids_in, (void*)&B.ids_out,
                   (void*)&B.dbg, (void*)&B.key, (void*)&B.block_count, (void*)&B.block_start,
                   (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot, (void*)&B.gv, (void*)&Sv,
                   (void*)&saltv};

@@ -18,6 +18,7 @@ struct StepBuffers {
   uint32_t* key;           // [n] block key of each record in rec_in order (in), rec_out order (out)
   uint32_t* perm;          // [n] sorted slot -> rec_in index
   uint8_t* cells;          // [n] base cell in its block, per sorted slot
+  uint32_t* perm_cell;     // [n] P2G's re-sort of perm by (block, base cell); G2P's order
   uint32_t* block_count;   // [nblocks]
   uint32_t* block_start;   // [nblocks + 1]
   uint32_t* block_slot;    // [nblocks]

@@ -8,9 +8,9 @@
 // the re-encode packs into registers (no read-modify-write of shared words).
 //
 //   qmpm_bin_count  a1        block key + histogram (first step after set_state/set_words)
-//   qmpm_p2g        a2+a3     decode, stress, scatter into per-warp shared-memory tiles
-//                             (lanes of one round have distinct base cells, so the
-//                             tile RMW needs no atomics), red.global.add.v4.f32 flush
+//   qmpm_p2g        a2+a3     sort the block by base cell; lane = cell accumulates its
+//                             particles' 3^d stencil in registers; one tile RMW per node
+//                             per cell (no atomics), red.global.add.v4.f32 flush
 //   qmpm_g2p        a2+a5-a7  gather from a shared-memory tile, update, dithered encode,
 //                             coalesced store in sorted order, next step's block key
 #pragma once
@@ -199,202 +199,155 @@ __device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec,
   if (valid && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
 }
 
-// ------------------------------------------------------------------ cell ordering
-// Within a block, particles are processed in (rank within base cell, cell) order:
-// position = P[r] + #{cells c' < c holding more than r particles}, P[r] = number of
-// particles of rank < r.  Consecutive lanes then have distinct base cells (except
-// across a level boundary, which the match_any rounds below absorb), so the
-// per-warp tile RMW of one stencil offset never collides.
-constexpr int kOrderCap = 1024;   // particles ordered per batch
-constexpr int kOrderLevels = 128; // ranks with a level mask (higher ranks go last)
-
-struct OrderSmem {
-  uint32_t p[kOrderCap];           // perm entries of the batch
-  uint32_t q[kOrderCap];           // reordered
-  uint16_t rank[kOrderCap];
-  uint8_t cell[kOrderCap];
-  unsigned cnt[64];
-  unsigned long long mask[kOrderLevels];
-  unsigned lvl[kOrderLevels + 1];  // exclusive prefix of level sizes
-  unsigned over;
-  unsigned maxc;
-};
-
-__device__ __forceinline__ void order_batch(uint32_t* __restrict__ perm, const uint8_t* __restrict__ cells,
-                                            uint32_t nb, OrderSmem& o) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
-  if (tid < 64) o.cnt[tid] = 0u;
-  if (tid == 0) {
-    o.over = 0u;
-    o.maxc = 0u;
-  }
-  __syncthreads();
-  for (uint32_t i0 = tid - lane; i0 < nb; i0 += nt) {  // warp-uniform trip count
-    const uint32_t i = i0 + lane;
-    const bool v = i < nb;
-    const uint32_t p = v ? perm[i] : 0u;
-    const uint32_t c = v ? (uint32_t)cells[i] : 64u + lane;
-    const unsigned peers = __match_any_sync(FULL, c);
-    const int leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if (v && lane == leader) base = atomicAdd(&o.cnt[c], (unsigned)__popc(peers));
-    base = __shfl_sync(FULL, base, leader);
-    if (v) {
-      o.p[i] = p;
-      o.cell[i] = (uint8_t)c;
-      o.rank[i] = (uint16_t)(base + __popc(peers & lanemask_lt()));
-    }
-  }
-  __syncthreads();
-  if (tid < 64) atomicMax(&o.maxc, o.cnt[tid]);
-  __syncthreads();
-  const unsigned levels = min(o.maxc, (unsigned)kOrderLevels);
-  if (tid < 64) {
-    const int half = tid >> 5;
-    const unsigned c = o.cnt[tid];
-    for (unsigned r = 0; r < levels; ++r) {
-      const unsigned b = __ballot_sync(FULL, c > r);
-      if (lane == 0) reinterpret_cast<unsigned*>(&o.mask[r])[half] = b;
-    }
-  }
-  __syncthreads();
-  if (tid < 32) {  // level prefix, one warp
-    unsigned run = 0;
-    for (unsigned r0 = 0; r0 < levels; r0 += 32) {
-      const unsigned r = r0 + lane;
-      const unsigned sz = r < levels ? (unsigned)__popcll(o.mask[r]) : 0u;
-      unsigned inc = sz;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const unsigned t = __shfl_up_sync(FULL, inc, d);
-        if (lane >= d) inc += t;
-      }
-      if (r < levels) o.lvl[r] = run + inc - sz;
-      run += __shfl_sync(FULL, inc, 31);
-    }
-    if (lane == 0) o.lvl[levels] = run;
-  }
-  __syncthreads();
-  for (uint32_t i = tid; i < nb; i += nt) {
-    const unsigned r = o.rank[i], c = o.cell[i];
-    uint32_t pos;
-    if (r < levels)
-      pos = o.lvl[r] + (uint32_t)__popcll(o.mask[r] & ((1ull << c) - 1ull));
-    else
-      pos = o.lvl[levels] + atomicAdd(&o.over, 1u);
-    o.q[pos] = o.p[i];
-    perm[pos] = o.p[i];
-  }
-  __syncthreads();
-}
-
-#ifndef QMPM_CELL_CAP
-#define QMPM_CELL_CAP 256
+#ifndef QMPM_P2G_CAP
+#define QMPM_P2G_CAP 5120
 #endif
+constexpr int kP2GCap = QMPM_P2G_CAP;  // block particles whose sorted indices stay in shared memory
+constexpr int kSortU = 4;              // loads in flight per thread in the sort passes
+
 // per-warp shared-memory footprint of the two step kernels (16-byte multiples)
 template <class SP>
 struct Smem {
   static constexpr int TN = Geo<SP::D>::TN;
   static constexpr int TILE = 16 * TN;
   static constexpr int STAGE = ((4 * 32 * SP::SW) + 15) / 16 * 16;
-  static constexpr int PRM = 4 * 16 * 32;
-  // P2G (2 warps per CTA): per warp one tile, two chunk stages and half of the
-  // [16][kCellCap] parameter block; + the CTA's CellSmem (static)
-  static constexpr int P2G_WARP = TILE + 2 * STAGE + 16 * 4 * QMPM_CELL_CAP / 2;
-  static constexpr int G2P_WARP = TILE + 2 * STAGE + 32;  // double-buffered stage + 8 neighbour slots
+  // private node tile + half of s_perm + half of the 3-slot record ring
+  static constexpr int P2G_WARP = TILE + 4 * QMPM_P2G_CAP / 2 + 3 * 32 * 4 * SP::W;
+  // velocity tile + 8 neighbour slots + double-buffered record stage
+  static constexpr int G2P_WARP = TILE + 32 + (2 * 32 * 4 * SP::W + 15) / 16 * 16;
 };
 
-// ------------------------------------------------------------------ a3: P2G
-// phase 1 of the scatter: decode + stress of the lane's particle -> 16 parameters
-// (cell, fx, Q, a_k) parked in shared memory: the momentum at stencil node o is
-// m v + aff (o - fx) dx = Q + sum_k o_k a_k with a_k = dx aff[:,k], Q = m v - sum_k fx_k a_k.
+// Per-lane load of record r (W words) into registers, 128/64-bit vectors when the
+// record size allows (records are 4W-byte aligned).
 template <class SP>
-__device__ __forceinline__ void p2g_params(const uint32_t* w, bool valid, const int org[3], const SimDev& S,
-                                           float* prm, int stride) {
-  const int lane = threadIdx.x & 31;
-  constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS;
-  float s[NSV];
-  if (valid) {
+__device__ __forceinline__ void load_record(const uint32_t* __restrict__ rec, uint32_t r, uint32_t* w) {
+  constexpr int W = SP::W;
+  const uint32_t* p = rec + (size_t)r * W;
+  if (W % 4 == 0) {
 #pragma unroll
-    for (int i = 0; i < NSV; ++i) s[i] = sdec<SP>(w, i);
-  } else {
-    benign_state<D, MAT>(s, org, S.dx);
-  }
-  int lb[3] = {0, 0, 0};
-  float fx[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    bool o;
-    lb[a] = base_fx(s[a], S.inv_dx, S.res[a], fx[a], o) - org[a];
-  }
-  float aff[D * D];
-  affine_of<D, MAT>(s, S, aff);
-  float Q[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    Q[a] = S.p_mass * s[D + a];
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const float akv = S.dx * aff[a * D + k];
-      Q[a] -= fx[k] * akv;
-      if (valid) prm[(7 + k * 3 + a) * stride + lane] = akv;
+    for (int q = 0; q < W / 4; ++q) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + q);
+      w[4 * q] = v.x;
+      w[4 * q + 1] = v.y;
+      w[4 * q + 2] = v.z;
+      w[4 * q + 3] = v.w;
     }
-  }
-  if (!valid) return;
-  prm[0 * stride + lane] = __int_as_float(D == 3 ? (lb[0] * 4 + lb[1]) * 4 + lb[2] : lb[0] * 8 + lb[1]);
+  } else if (W % 2 == 0) {
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    prm[(1 + a) * stride + lane] = fx[a];
-    prm[(4 + a) * stride + lane] = Q[a];
+    for (int q = 0; q < W / 2; ++q) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(p) + q);
+      w[2 * q] = v.x;
+      w[2 * q + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; ++q) w[q] = __ldg(p + q);
   }
 }
 
-// One CTA of 2 warps (64 lanes = the 64 base cells of a block) per active block,
-// grid-stride.  Per batch of <= kCellCap particles of the block:
-//   1. counting sort by base cell (cells[] from the scatter, warp-aggregated ranks);
-//   2. phase 1: both warps stage records (cp.async, the next chunk in flight) and park
-//      16 parameters per particle in shared memory (structure of arrays);
-//   3. phase 2: lane c OWNS cell c: it loops over its cell's particles accumulating
-//      one stencil layer (fixed ox: 3^(d-1) nodes x 4 channels) in registers, then
-//      read-modify-writes those nodes of its warp's private tile.  Lanes own distinct
-//      cells, so one layer's RMW never collides; __syncwarp orders successive nodes.
-//      The shared-memory RMW count drops from 27 per particle to 27 per cell.
-// The two warp tiles are summed and flushed with red.global.add.v4.f32.
-#ifndef QMPM_CELL_CAP
-#define QMPM_CELL_CAP 256
-#endif
-constexpr int kCellCap = QMPM_CELL_CAP;  // particles per P2G batch
-
-struct CellSmem {
-  uint32_t p[kCellCap];   // perm entries of the batch
-  uint32_t q[kCellCap];   // sorted by cell
-  uint16_t pos[kCellCap];
-  uint8_t cell[kCellCap];
-  uint32_t cnt[64];
-  uint32_t cstart[65];
-};
-
+// Per-lane asynchronous copy of record r (W words) into shared memory (cp.async, no
+// registers held while in flight; 16-byte granules when the record size allows).
+// The caller commits the group and waits with cp_async_wait<N>.
 template <class SP>
-__device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint32_t* __restrict__ perm,
-                                         const uint8_t* __restrict__ cells,
+__device__ __forceinline__ void record_async(const uint32_t* __restrict__ rec, uint32_t r, uint32_t* dst) {
+  constexpr int W = SP::W;
+  const uint32_t* src = rec + (size_t)r * W;
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  if (W % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + 16u * q), "l"(src + 4 * q) : "memory");
+  } else if (W % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < W / 2; ++q)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa + 8u * q), "l"(src + 2 * q) : "memory");
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa + 4u * q), "l"(src + q) : "memory");
+  }
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// read a record this thread staged (row of W words, 16/8-byte aligned as staged)
+template <class SP>
+__device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
+  constexpr int W = SP::W;
+  if (W % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q) {
+      const uint4 v = reinterpret_cast<const uint4*>(row)[q];
+      w[4 * q] = v.x;
+      w[4 * q + 1] = v.y;
+      w[4 * q + 2] = v.z;
+      w[4 * q + 3] = v.w;
+    }
+  } else if (W % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < W / 2; ++q) {
+      const uint2 v = reinterpret_cast<const uint2*>(row)[q];
+      w[2 * q] = v.x;
+      w[2 * q + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; ++q) w[q] = row[q];
+  }
+  w[W] = 0u;
+}
+
+// ------------------------------------------------------------------ a3: P2G
+// One CTA of 2 warps per active block, grid-stride; lane `tid` OWNS base cell `tid`
+// of the block (64 cells = 4^3 in 3D, 8^2 in 2D).
+//   1. counting sort of the block's particles by base cell (shared histogram, scan,
+//      warp-aggregated cursors): perm_cell[block range] = the block's records in cell
+//      order (also the order G2P processes, and hence stores, them in);
+//   2. lane c walks its cell's particles: load + decode the record (the next one in
+//      flight), stress and affine momentum, and accumulates all 3^d stencil nodes x
+//      (m, p) in REGISTERS -- no shared-memory traffic per particle;
+//   3. one read-modify-write per stencil node per cell into the warp's private tile:
+//      lanes own distinct cells, so for a fixed stencil offset their nodes are
+//      distinct; __syncwarp orders successive offsets;
+//   4. the two warp tiles are summed and flushed with one red.global.add.v4.f32 per
+//      non-empty node.
+// Momentum at stencil node o of a particle: m v + aff (o - fx) dx = Q + sum_k o_k a_k,
+// a_k = dx aff[:, k], Q = m v - sum_k fx_k a_k (Hu et al. 2018 APIC/MLS form).
+template <class SP>
+__device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const uint32_t* __restrict__ perm,
+                                         const uint8_t* __restrict__ cells, uint32_t* perm_cell,
                                          const uint32_t* __restrict__ block_start,
                                          const uint32_t* __restrict__ active_list,
                                          const DevCounters* __restrict__ dc,
                                          const uint32_t* __restrict__ block_slot, float4* __restrict__ mp,
                                          const SimDev& S) {
-  constexpr int D = SP::D;
+  constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, W = SP::W;
+  constexpr int NN = D == 3 ? 27 : 9;  // stencil nodes
   using G = Geo<D>;
-  using SM = Smem<SP>;
-  constexpr int SWW = 32 * SP::SW;  // words per chunk stage
   extern __shared__ float4 smem4[];
+  __shared__ uint32_t s_cnt[64], s_cur[64], s_start[65];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  float4* tiles = smem4;                                                            // [2][TN]
-  float* prm = reinterpret_cast<float*>(tiles + 2 * G::TN);                         // [16][kCellCap]
-  uint32_t* stage = reinterpret_cast<uint32_t*>(prm + 16 * kCellCap);               // [2 warps][2][SWW]
-  uint32_t* wst = stage + warp * 2 * SWW;
+  float4* tiles = smem4;                                               // [2][TN]
+  uint32_t* s_perm = reinterpret_cast<uint32_t*>(tiles + 2 * G::TN);  // [kP2GCap]
+  uint32_t* s_ring = s_perm + kP2GCap;                                 // [3][64][W] record ring
   float4* tile = tiles + warp * G::TN;
-  __shared__ CellSmem cs;
   const uint32_t n_active = dc->n_active;
+  // this lane's cell and the tile index of its stencil's first node
+  int lc[3];
+  if (D == 3) {
+    lc[0] = (tid >> 4) & 3;
+    lc[1] = (tid >> 2) & 3;
+    lc[2] = tid & 3;
+  } else {
+    lc[0] = (tid >> 3) & 7;
+    lc[1] = tid & 7;
+    lc[2] = 0;
+  }
+  const int base_idx = D == 3 ? (lc[0] * G::T + lc[1]) * G::T + lc[2] : lc[0] * G::T + lc[1];
 
   for (uint32_t ab = blockIdx.x; ab < n_active; ab += gridDim.x) {
     const uint32_t b = active_list[ab];
@@ -403,163 +356,184 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
     block_coords<D>(b, S, bc);
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
     for (int t = tid; t < 2 * G::TN; t += 64) tiles[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-
-    // batches are strided samples of the block (element i of batch bi is block
-    // particle bi + i * nbatch), so every batch spans all cells even when the block's
-    // particles arrive grouped by cell
+    s_cnt[tid] = 0u;
+    __syncthreads();
+    // ---- 1. counting sort of the block by base cell.  Loads are batched (kSortU per
+    // thread in flight) so the histogram and scatter passes are not latency-bound; the
+    // sorted record indices stay in shared memory (s_perm) when the block fits.
     const uint32_t n_blk = end - start;
-    const uint32_t nbatch = (n_blk + kCellCap - 1) / kCellCap;
-    for (uint32_t bi = 0; bi < nbatch; ++bi) {
-      const uint32_t nb = (n_blk - bi + nbatch - 1) / nbatch;
-      // ---- 1. counting sort of the batch by base cell
-      cs.cnt[tid] = 0u;
-      __syncthreads();
-      for (uint32_t i0 = warp * 32; i0 < nb; i0 += 64) {
-        const uint32_t i = i0 + lane;
-        const bool v = i < nb;
-        const uint32_t gi = start + bi + i * nbatch;
-        const uint32_t c = v ? (uint32_t)cells[gi] : 64u + lane;
-        const unsigned peers = __match_any_sync(FULL, c);
+    const bool in_smem = n_blk <= (uint32_t)kP2GCap;
+    for (uint32_t i0 = start + warp * 32; i0 < end; i0 += 64 * kSortU) {
+      uint32_t c[kSortU];
+#pragma unroll
+      for (int u = 0; u < kSortU; ++u) {
+        const uint32_t i = i0 + u * 64 + lane;
+        c[u] = i < end ? (uint32_t)__ldg(cells + i) : 64u + lane;
+      }
+#pragma unroll
+      for (int u = 0; u < kSortU; ++u) {
+        const uint32_t i = i0 + u * 64 + lane;
+        const unsigned peers = __match_any_sync(FULL, c[u]);
+        if (i < end && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[c[u]], (unsigned)__popc(peers));
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 64 cell counts
+      const uint32_t c0 = s_cnt[lane], c1 = s_cnt[lane + 32];
+      uint32_t i0 = c0, i1 = c1;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t0 = __shfl_up_sync(FULL, i0, d), t1 = __shfl_up_sync(FULL, i1, d);
+        if (lane >= d) {
+          i0 += t0;
+          i1 += t1;
+        }
+      }
+      const uint32_t tot0 = __shfl_sync(FULL, i0, 31);
+      s_start[lane] = i0 - c0;
+      s_start[lane + 32] = tot0 + i1 - c1;
+      s_cur[lane] = i0 - c0;
+      s_cur[lane + 32] = tot0 + i1 - c1;
+      if (lane == 31) s_start[64] = tot0 + i1;
+    }
+    __syncthreads();
+    for (uint32_t i0 = start + warp * 32; i0 < end; i0 += 64 * kSortU) {
+      uint32_t c[kSortU], p[kSortU];
+#pragma unroll
+      for (int u = 0; u < kSortU; ++u) {
+        const uint32_t i = i0 + u * 64 + lane;
+        const bool v = i < end;
+        c[u] = v ? (uint32_t)__ldg(cells + i) : 64u + lane;
+        p[u] = v ? __ldg(perm + i) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kSortU; ++u) {
+        const uint32_t i = i0 + u * 64 + lane;
+        const bool v = i < end;
+        const unsigned peers = __match_any_sync(FULL, c[u]);
         const int leader = __ffs(peers) - 1;
         uint32_t base = 0;
-        if (v && lane == leader) base = atomicAdd(&cs.cnt[c], (unsigned)__popc(peers));
+        if (v && lane == leader) base = atomicAdd(&s_cur[c[u]], (unsigned)__popc(peers));
         base = __shfl_sync(FULL, base, leader);
+        const uint32_t pos = base + __popc(peers & lanemask_lt());
         if (v) {
-          cs.p[i] = perm[gi];
-          cs.cell[i] = (uint8_t)c;
-          cs.pos[i] = (uint16_t)(base + __popc(peers & lanemask_lt()));
+          perm_cell[start + pos] = p[u];
+          if (in_smem) s_perm[pos] = p[u];
         }
       }
-      __syncthreads();
-      if (warp == 0) {  // exclusive scan of the 64 cell counts
-        const uint32_t c0 = cs.cnt[lane], c1 = cs.cnt[lane + 32];
-        uint32_t i0 = c0, i1 = c1;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t t0 = __shfl_up_sync(FULL, i0, d), t1 = __shfl_up_sync(FULL, i1, d);
-          if (lane >= d) {
-            i0 += t0;
-            i1 += t1;
-          }
-        }
-        const uint32_t tot0 = __shfl_sync(FULL, i0, 31);
-        cs.cstart[lane] = i0 - c0;
-        cs.cstart[lane + 32] = tot0 + i1 - c1;
-        if (lane == 31) cs.cstart[64] = tot0 + i1;
-      }
-      __syncthreads();
-      for (uint32_t i = tid; i < nb; i += 64) {
-        const uint32_t q = cs.cstart[cs.cell[i]] + cs.pos[i];
-        cs.q[q] = cs.p[i];
-      }
-      __syncthreads();
-      // ---- 2. phase 1: parameters of every particle of the batch
-      {
-        int buf = 0;
-        uint32_t j0 = warp * 32;
-        if (j0 < nb) {
-          const uint32_t c0 = min(32u, nb - j0);
-          issue_records<SP>(rec, cs.q[j0 + ((uint32_t)lane < c0 ? lane : 0)], c0, wst, lane);
-        }
-        for (; j0 < nb; j0 += 64) {
-          const uint32_t cnt = min(32u, nb - j0);
-          const bool valid = (uint32_t)lane < cnt;
-          uint32_t w[SP::W + 1];
-          take_records<SP>(wst + buf * SWW, lane, w);
-          const uint32_t jn = j0 + 64;
-          if (jn < nb) {
-            const uint32_t cn = min(32u, nb - jn);
-            issue_records<SP>(rec, cs.q[jn + ((uint32_t)lane < cn ? lane : 0)], cn, wst + (buf ^ 1) * SWW, lane);
-          }
-          buf ^= 1;
-          p2g_params<SP>(w, valid, org, S, prm + j0, kCellCap);
-        }
-      }
-      __syncthreads();
-      // ---- 3. phase 2: lane `tid` owns base cell `tid`
-      {
-        const int c = tid;
-        const uint32_t k0 = cs.cstart[c], k1 = cs.cstart[c + 1];
-        const unsigned has = __ballot_sync(FULL, k1 > k0);
-        int lb[3];
-        if (D == 3) {
-          lb[0] = (c >> 4) & 3;
-          lb[1] = (c >> 2) & 3;
-          lb[2] = c & 3;
-        } else {
-          lb[0] = (c >> 3) & 7;
-          lb[1] = c & 7;
-          lb[2] = 0;
-        }
-        const int base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
-        const uint32_t kmax = __reduce_max_sync(FULL, k1 - k0);
-        if (has) {
-#pragma unroll 1
-          for (int ox = 0; ox < 3; ++ox) {
-            constexpr int NL = D == 3 ? 9 : 3;  // nodes of one layer
-            float am[NL], ax[NL], ay[NL], az[NL];
-#pragma unroll
-            for (int q = 0; q < NL; ++q) am[q] = ax[q] = ay[q] = az[q] = 0.0f;
-            for (uint32_t k = 0; k < kmax; ++k) {
-              if (k0 + k < k1) {
-                const uint32_t pi = k0 + k;
-                const float fx0 = prm[1 * kCellCap + pi], fx1 = prm[2 * kCellCap + pi];
-                float wq[3], wy[3], wz[3] = {1.f, 0.f, 0.f};
-                bspline_w(fx0, wq);
-                bspline_w(fx1, wy);
-                if (D == 3) bspline_w(prm[3 * kCellCap + pi], wz);
-                const float wxo = wq[ox];
-                float M[3];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) M[a] = prm[(4 + a) * kCellCap + pi] + ox * prm[(7 + a) * kCellCap + pi];
-                float a1[3], a2[3];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                  a1[a] = prm[(10 + a) * kCellCap + pi];
-                  a2[a] = prm[(13 + a) * kCellCap + pi];
-                }
-#pragma unroll
-                for (int oy = 0; oy < 3; ++oy) {
-                  const float wxy = wxo * wy[oy];
-                  float My[3] = {M[0] + oy * a1[0], M[1] + oy * a1[1], M[2] + oy * a1[2]};
-#pragma unroll
-                  for (int oz = 0; oz < (D == 3 ? 3 : 1); ++oz) {
-                    const int q = D == 3 ? oy * 3 + oz : oy;
-                    const float ww = D == 3 ? wxy * wz[oz] : wxy;
-                    am[q] += ww;
-                    ax[q] = fmaf(ww, My[0], ax[q]);
-                    ay[q] = fmaf(ww, My[1], ay[q]);
-                    az[q] = fmaf(ww, My[2], az[q]);
-                    if (D == 3) {
-                      My[0] += a2[0];
-                      My[1] += a2[1];
-                      My[2] += a2[2];
-                    }
-                  }
-                }
-              }
-            }
-            // one RMW per node of the layer (m = p_mass * sum w)
-#pragma unroll
-            for (int q = 0; q < NL; ++q) {
-              const int oy = D == 3 ? q / 3 : q, oz = D == 3 ? q % 3 : 0;
-              const int idx = base_idx + (D == 3 ? (ox * G::T + oy) * G::T + oz : ox * G::T + oy);
-              if (k1 > k0) {
-                float4 t = tile[idx];
-                t.x = fmaf(am[q], S.p_mass, t.x);
-                t.y += ax[q];
-                t.z += ay[q];
-                t.w += az[q];
-                tile[idx] = t;
-              }
-              __syncwarp();
-            }
-          }
-        }
-      }
-      __syncthreads();  // parameters and sort arrays are reused by the next batch
     }
-    // flush: sum the two warp tiles, one vector reduction per non-empty node
+    __syncthreads();  // perm_cell / s_perm of the block are visible to the whole CTA
+    // ---- 2. lane `tid` accumulates its cell's particles
+    const uint32_t* idx_src = in_smem ? s_perm : perm_cell + start;
+    const uint32_t k0 = s_start[tid], k1 = s_start[tid + 1];
+    float am[NN], ax[NN], ay[NN], az[NN];
+#pragma unroll
+    for (int q = 0; q < NN; ++q) am[q] = ax[q] = ay[q] = az[q] = 0.0f;
+    // records stream through a per-lane 3-slot shared ring, two in flight (cp.async)
+    uint32_t* ring = s_ring + tid * W;  // slot q at ring + q * 64 * W
+    if (k0 < k1) record_async<SP>(rec, idx_src[k0], ring);
+    cp_async_commit();
+    if (k0 + 1 < k1) record_async<SP>(rec, idx_src[k0 + 1], ring + 64 * W);
+    cp_async_commit();
+    int slot = 0;
+#pragma unroll 1
+    for (uint32_t k = k0; k < k1; ++k) {
+      {
+        const int s2 = slot == 0 ? 2 : slot - 1;  // (slot + 2) % 3
+        if (k + 2 < k1) record_async<SP>(rec, idx_src[k + 2], ring + s2 * 64 * W);
+        cp_async_commit();
+      }
+      cp_async_wait<2>();
+      uint32_t w[W + 1];
+      read_staged<SP>(ring + slot * 64 * W, w);
+      slot = slot == 2 ? 0 : slot + 1;
+      float s[NSV];
+#pragma unroll
+      for (int i = 0; i < NSV; ++i) s[i] = sdec<SP>(w, i);
+      float fx[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        bool o;
+        base_fx(s[a], S.inv_dx, S.res[a], fx[a], o);
+      }
+      float aff[D * D];
+      affine_of<D, MAT>(s, S, aff);
+      float Q[3] = {0.f, 0.f, 0.f}, A[3][3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        Q[a] = S.p_mass * s[D + a];
+#pragma unroll
+        for (int k2 = 0; k2 < D; ++k2) {
+          A[k2][a] = S.dx * aff[a * D + k2];
+          Q[a] = fmaf(-fx[k2], A[k2][a], Q[a]);
+        }
+      }
+      float wt[3][3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
+      if (D == 3) {
+#pragma unroll
+        for (int ox = 0; ox < 3; ++ox) {
+#pragma unroll
+          for (int oy = 0; oy < 3; ++oy) {
+            const float wxy = wt[0][ox] * wt[1][oy];
+            float M[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) M[a] = Q[a] + (float)ox * A[0][a] + (float)oy * A[1][a];
+#pragma unroll
+            for (int oz = 0; oz < 3; ++oz) {
+              const int q = (ox * 3 + oy) * 3 + oz;
+              const float ww = wxy * wt[2][oz];
+              am[q] += ww;
+              ax[q] = fmaf(ww, M[0], ax[q]);
+              ay[q] = fmaf(ww, M[1], ay[q]);
+              az[q] = fmaf(ww, M[2], az[q]);
+              if (oz < 2) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) M[a] += A[2][a];
+              }
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int ox = 0; ox < 3; ++ox) {
+          float M[2];
+#pragma unroll
+          for (int a = 0; a < 2; ++a) M[a] = Q[a] + (float)ox * A[0][a];
+#pragma unroll
+          for (int oy = 0; oy < 3; ++oy) {
+            const int q = ox * 3 + oy;
+            const float ww = wt[0][ox] * wt[1][oy];
+            am[q] += ww;
+            ax[q] = fmaf(ww, M[0], ax[q]);
+            ay[q] = fmaf(ww, M[1], ay[q]);
+            if (oy < 2) {
+              M[0] += A[1][0];
+              M[1] += A[1][1];
+            }
+          }
+        }
+      }
+    }
+    // ---- 3. one RMW per stencil node of the cell (m = p_mass * sum w)
+    const bool mine = k1 > k0;
+#pragma unroll
+    for (int q = 0; q < NN; ++q) {
+      const int ox = D == 3 ? q / 9 : q / 3, oy = D == 3 ? (q / 3) % 3 : q % 3, oz = D == 3 ? q % 3 : 0;
+      const int idx = base_idx + (D == 3 ? (ox * G::T + oy) * G::T + oz : ox * G::T + oy);
+      if (mine) {
+        float4 t = tile[idx];
+        t.x = fmaf(am[q], S.p_mass, t.x);
+        t.y += ax[q];
+        t.z += ay[q];
+        t.w += az[q];
+        tile[idx] = t;
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- 4. flush: sum the two warp tiles, one vector reduction per non-empty node
     for (int t = tid; t < G::TN; t += 64) {
       const float4 a = tiles[t], o = tiles[G::TN + t];
       const float4 acc = make_float4(a.x + o.x, a.y + o.y, a.z + o.z, a.w + o.w);
@@ -581,8 +555,83 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, uint3
 }
 
 // ------------------------------------------------------------------ a5-a7: G2P + encode
-// One WARP per active block: stage the block's (B+2)^d velocity tile, then gather,
-// update, dither + pack in registers, store in sorted order, emit next step's key.
+// Fast-path encode of state scalar i (Eq. 3 / Eq. 11, readings Q3, Q6): the code's
+// bits WITHOUT the saturation clamp.  `flag` is raised (OR-accumulated) whenever the
+// value might saturate or is not finite -- |t| >= 2^b - 1 or NaN -- and the caller then
+// re-encodes the whole record with the exact senc() (rare).  up: u > t;  nz: the value
+// is not on the grid (dither: down = nz - up) or, for RNE, dn: u < t.
+template <class SP>
+__device__ __forceinline__ uint32_t senc_fast(const int i, float v, uint32_t r24, bool& up, bool& nz, bool& flag) {
+  if (SP::kind(i) == kKindRaw) {
+    up = nz = false;
+    flag |= !(fabsf(v) < __int_as_float(0x7f800000));
+    return __float_as_uint(v);
+  }
+  const int wi = SP::width(i);
+  const float a = (SP::offset(i) != 0.0f) ? __fsub_rn(v, SP::offset(i)) : v;
+  const float t = __fmul_rn(a, SP::inv_delta(i));  // one fp32 multiply, no FMA (Q3)
+  const uint32_t mask = (wi == 32) ? 0xffffffffu : ((1u << wi) - 1u);
+  // |t| below lim => floor/round(t) (+1) lies inside [-2^b, 2^b - 1]
+  constexpr float lim_tab[33] = {0.f, 0.f, 1.f, 3.f, 7.f, 15.f, 31.f, 63.f, 127.f, 255.f, 511.f, 1023.f, 2047.f,
+                                 4095.f, 8191.f, 16383.f, 32767.f, 65535.f, 131071.f, 262143.f, 524287.f,
+                                 1048575.f, 2097151.f, 4194303.f, 8388607.f, 16777215.f, 0x1p24f, 0x1p25f,
+                                 0x1p26f, 0x1p27f, 0x1p28f, 0x1p29f, 0x1p30f};
+  const float lim = lim_tab[wi];
+  flag |= !(fabsf(t) < lim);
+  int u;
+  if (SP::DITHER) {
+    const float f = floorf(t);
+    const float y = __fsub_rn(t, f);  // exact
+    const float one_minus_r = __fmul_rn(__uint2float_rn(0x1000000u - r24), 0x1p-24f);  // exact
+    up = y >= one_minus_r;  // u = floor(t + r) (Eq. 11, reading Q6)
+    nz = y > 0.0f;
+    u = __float2int_rz(f) + (up ? 1 : 0);
+  } else {
+    const float q = rintf(t);  // round half to even (Q6)
+    up = q > t;
+    nz = q < t;
+    u = __float2int_rz(q);
+  }
+  return (uint32_t)u & mask;
+}
+
+// per-lane round counters packed 4 per register (byte i%4 of word i/4 counts state
+// scalar i), flushed into 32-bit per-lane totals (lane i holds scalar i) before a
+// byte can overflow
+template <class SP>
+struct RoundCounters {
+  static constexpr int NP = (SP::NS + 3) / 4;
+  uint32_t pu[NP], pz[NP];
+  uint32_t n_since;  // particles (per lane) since the last flush, warp-uniform
+  unsigned c_up, c_nz;
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) pu[k] = pz[k] = 0u;
+    n_since = 0u;
+    c_up = c_nz = 0u;
+  }
+  __device__ __forceinline__ void flush(int lane) {
+#pragma unroll
+    for (int i = 0; i < SP::NS; ++i) {
+      if (SP::kind(i) != kKindFixed) continue;
+      const unsigned tu = __reduce_add_sync(FULL, (pu[i / 4] >> (8 * (i % 4))) & 255u);
+      const unsigned tz = __reduce_add_sync(FULL, (pz[i / 4] >> (8 * (i % 4))) & 255u);
+      if (lane == i) {
+        c_up += tu;
+        c_nz += tz;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NP; ++k) pu[k] = pz[k] = 0u;
+    n_since = 0u;
+  }
+};
+
+// One WARP per active block: stage the block's (B+2)^d velocity tile, then per chunk of
+// 32 particles (P2G's cell order, so lanes mostly share a cell and the tile reads
+// broadcast): gather, update, dither + pack in registers, store in that order, emit
+// the next step's block key.  Records move with per-lane vector loads/stores; the next
+// chunk's records are in flight while the current one computes.
 template <class SP>
 __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, uint32_t* __restrict__ rec_out,
                                          const uint32_t* __restrict__ perm, const uint32_t* __restrict__ ids_in,
@@ -600,10 +649,11 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   char* wbase = reinterpret_cast<char*>(smem4) + warp * SM::G2P_WARP;
   float4* tile = reinterpret_cast<float4*>(wbase);
-  uint32_t* wst = reinterpret_cast<uint32_t*>(wbase + SM::TILE);
-  uint32_t* nslot = reinterpret_cast<uint32_t*>(wbase + SM::TILE + 2 * SM::STAGE);  // [4] / [8] neighbour slots
-  // per-lane counters: lane f accumulates field-scalar f's round-ups / downs / saturations
-  unsigned c_up = 0, c_down = 0, c_sat = 0, c_nf = 0, c_oob = 0;
+  uint32_t* nslot = reinterpret_cast<uint32_t*>(wbase + SM::TILE);  // [4] / [8] neighbour slots
+  uint32_t* wring = reinterpret_cast<uint32_t*>(wbase + SM::TILE + 32);  // [2][32][W] record stage
+  RoundCounters<SP> rc;
+  rc.init();
+  unsigned c_sat = 0, c_nf = 0, c_oob = 0;
   const uint32_t n_active = dc->n_active;
   const float four_inv_dx = 4.0f * S.inv_dx;
 
@@ -613,6 +663,14 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
     int bc[3];
     block_coords<D>(b, S, bc);
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
+    // first chunk's records in flight while the tile is staged
+    uint32_t r_next = 0;
+    if ((uint32_t)lane < end - start) {
+      r_next = perm[start + lane];
+      record_async<SP>(rec_in, r_next, wring + lane * W);
+    }
+    cp_async_commit();
+    int buf = 0;
     // slots of the block and its +x/+y(/+z) neighbours, then the velocity tile
     if (lane < (1 << D)) {
       int nbk[3] = {bc[0] + (lane & 1), bc[1] + ((lane >> 1) & 1), D == 3 ? bc[2] + ((lane >> 2) & 1) : 0};
@@ -638,29 +696,22 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
     }
     __syncwarp();
 
-    int buf = 0;
-    uint32_t r_next = 0;
-    if (start < end) {
-      const uint32_t c0 = min(32u, end - start);
-      r_next = perm[start + ((uint32_t)lane < c0 ? lane : 0)];
-      issue_records<SP>(rec_in, r_next, c0, wst, lane);
-    }
     for (uint32_t j0 = start; j0 < end; j0 += 32) {
       const uint32_t cnt = min(32u, end - j0);
       const bool valid = (uint32_t)lane < cnt;
       const uint32_t r = r_next;
-      uint32_t* cur = wst + buf * 32 * SP::SW;
-      uint32_t w[W + 1];
-      take_records<SP>(cur, lane, w);
       {  // the next chunk's records go in flight while this one computes
-        const uint32_t jn = j0 + 32;
+        const uint32_t jn = j0 + 32 + lane;
         if (jn < end) {
-          const uint32_t cn = min(32u, end - jn);
-          r_next = perm[jn + ((uint32_t)lane < cn ? lane : 0)];
-          issue_records<SP>(rec_in, r_next, cn, wst + (buf ^ 1) * 32 * SP::SW, lane);
+          r_next = perm[jn];
+          record_async<SP>(rec_in, r_next, wring + ((buf ^ 1) * 32 + lane) * W);
         }
-        buf ^= 1;
+        cp_async_commit();
       }
+      cp_async_wait<1>();
+      uint32_t w[W + 1];
+      read_staged<SP>(wring + (buf * 32 + lane) * W, w);
+      buf ^= 1;
       const uint32_t h = mix32(content_key<SP>(w) ^ salt);
       float s[NSV];
       if (valid) {
@@ -683,29 +734,38 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         oob_any |= o;
         bspline_w(fx[a], wt[a]);
       }
-      // gather: v' = sum w v_i;  C' = 4/dx sum w v_i (x) (i - fx) = 4/dx (T - v' fx^T)
+      // gather: v' = sum w v_i;  C' = 4/dx sum w v_i (x) (i - fx) = 4/dx (T - v' fx^T),
+      // T[a][k] = sum w v_i,a o_k, reduced axis by axis (z, then y, then x)
       float Sv[3] = {0.f, 0.f, 0.f}, T[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
       const int base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
       if (D == 3) {
+        const float wz2x2 = 2.0f * wt[2][2];
 #pragma unroll
-        for (int ox = 0; ox < 3; ++ox)
+        for (int ox = 0; ox < 3; ++ox) {
+          float sy[3] = {0.f, 0.f, 0.f}, ty[3] = {0.f, 0.f, 0.f}, tzy[3] = {0.f, 0.f, 0.f};
 #pragma unroll
           for (int oy = 0; oy < 3; ++oy) {
-            const float wxy = wt[0][ox] * wt[1][oy];
             const int idx = base_idx + (ox * G::T + oy) * G::T;
             const float4 g0 = tile[idx], g1 = tile[idx + 1], g2 = tile[idx + 2];
-            const float g[3][3] = {{g0.x, g0.y, g0.z}, {g1.x, g1.y, g1.z}, {g2.x, g2.y, g2.z}};
+            const float ga[3][3] = {{g0.x, g0.y, g0.z}, {g1.x, g1.y, g1.z}, {g2.x, g2.y, g2.z}};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-              const float u0 = wt[2][0] * g[0][a], u1 = wt[2][1] * g[1][a], u2 = wt[2][2] * g[2][a];
-              const float sz = u0 + u1 + u2;
-              const float tz = u1 + 2.0f * u2;
-              Sv[a] = fmaf(wxy, sz, Sv[a]);
-              T[a][2] = fmaf(wxy, tz, T[a][2]);
-              if (ox) T[a][0] = fmaf(wxy * ox, sz, T[a][0]);
-              if (oy) T[a][1] = fmaf(wxy * oy, sz, T[a][1]);
+              const float p1 = wt[2][1] * ga[1][a];
+              const float tz = fmaf(wz2x2, ga[2][a], p1);                       // sum_oz w oz g
+              const float sz = fmaf(wt[2][0], ga[0][a], fmaf(wt[2][2], ga[2][a], p1));  // sum_oz w g
+              sy[a] = fmaf(wt[1][oy], sz, sy[a]);
+              tzy[a] = fmaf(wt[1][oy], tz, tzy[a]);
+              if (oy) ty[a] = fmaf(wt[1][oy] * oy, sz, ty[a]);
             }
           }
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            Sv[a] = fmaf(wt[0][ox], sy[a], Sv[a]);
+            T[a][1] = fmaf(wt[0][ox], ty[a], T[a][1]);
+            T[a][2] = fmaf(wt[0][ox], tzy[a], T[a][2]);
+            if (ox) T[a][0] = fmaf(wt[0][ox] * ox, sy[a], T[a][0]);
+          }
+        }
       } else {
 #pragma unroll
         for (int ox = 0; ox < 3; ++ox) {
@@ -761,35 +821,32 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       uint32_t ow[W + 1];
 #pragma unroll
       for (int q = 0; q <= W; ++q) ow[q] = 0u;
-      bool any_flag = false;
+      bool flag = false;
 #pragma unroll
       for (int i = 0; i < NSV; ++i) {
         const uint32_t r24 = (SP::DITHER && SP::kind(i) == kKindFixed) ? r24_of(h, SP::idx(i)) : 0u;
-        EncFlags fl;
-        const uint32_t bits = senc<SP>(i, o[i], r24, fl);
-        sput<SP>(ow, i, bits);
+        bool up, nz;
+        sput<SP>(ow, i, senc_fast<SP>(i, o[i], r24, up, nz, flag));
         if (SP::COUNTERS && SP::kind(i) == kKindFixed) {
-          const unsigned bu = __ballot_sync(FULL, valid && fl.up);
-          const unsigned bd = __ballot_sync(FULL, valid && fl.down);
-          if (lane == i) {
-            c_up += __popc(bu);
-            c_down += __popc(bd);
-          }
+          if (up && valid) rc.pu[i / 4] += 1u << (8 * (i % 4));
+          if (nz && valid) rc.pz[i / 4] += 1u << (8 * (i % 4));
         }
-        if (valid && (fl.sat || fl.nonfinite)) any_flag = true;
       }
-      if (__any_sync(FULL, any_flag)) {  // rare: recount saturations / non-finite
+      if (__any_sync(FULL, valid && flag)) {  // rare: exact re-encode with saturation / non-finite
+#pragma unroll
+        for (int q = 0; q <= W; ++q) ow[q] = 0u;
 #pragma unroll
         for (int i = 0; i < NSV; ++i) {
           EncFlags fl;
           const uint32_t r24 = (SP::DITHER && SP::kind(i) == kKindFixed) ? r24_of(h, SP::idx(i)) : 0u;
-          senc<SP>(i, o[i], r24, fl);
+          sput<SP>(ow, i, senc<SP>(i, o[i], r24, fl));
           const unsigned bs = __ballot_sync(FULL, valid && fl.sat);
           const unsigned bn = __ballot_sync(FULL, valid && fl.nonfinite);
           if (lane == i) c_sat += __popc(bs);
           if (lane == 0) c_nf += __popc(bn);
         }
       }
+      if (SP::COUNTERS && ++rc.n_since == 255u) rc.flush(lane);
       {
         const unsigned bo = __ballot_sync(FULL, valid && oob_any);
         if (lane == 0) c_oob += __popc(bo);
@@ -803,19 +860,34 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       const uint32_t nk = valid ? (nkey >> 6) : 0xffffffffu;
       const unsigned kp = __match_any_sync(FULL, nk);
       if (valid && lane == __ffs(kp) - 1) atomicAdd(&block_count[nk], (unsigned)__popc(kp));
-      if (ids_out != nullptr && valid) ids_out[j] = ids_in[r];
-      store_records<SP>(rec_out + (size_t)j0 * W, cnt, cur, lane, ow);
+      if (valid) {
+        if (ids_out != nullptr) ids_out[j] = ids_in[r];
+        uint32_t* op = rec_out + (size_t)j * W;
+        if (W % 4 == 0) {
+#pragma unroll
+          for (int q = 0; q < W / 4; ++q)
+            reinterpret_cast<uint4*>(op)[q] = make_uint4(ow[4 * q], ow[4 * q + 1], ow[4 * q + 2], ow[4 * q + 3]);
+        } else if (W % 2 == 0) {
+#pragma unroll
+          for (int q = 0; q < W / 2; ++q) reinterpret_cast<uint2*>(op)[q] = make_uint2(ow[2 * q], ow[2 * q + 1]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < W; ++q) op[q] = ow[q];
+        }
+      }
     }
     __syncwarp();
   }
+  if (SP::COUNTERS) rc.flush(lane);
   // flush this thread's counters (lane i holds scalar i's counts)
   if (lane < NSV) {
     int fi = 0;
 #pragma unroll
     for (int i = 0; i < NSV; ++i)
       if (lane == i) fi = SP::idx(i);
-    if (c_up) atomicAdd(&dc->up[fi], (unsigned long long)c_up);
-    if (c_down) atomicAdd(&dc->down[fi], (unsigned long long)c_down);
+    const unsigned c_dn = SP::DITHER ? rc.c_nz - rc.c_up : rc.c_nz;
+    if (rc.c_up) atomicAdd(&dc->up[fi], (unsigned long long)rc.c_up);
+    if (c_dn) atomicAdd(&dc->down[fi], (unsigned long long)c_dn);
     if (c_sat) atomicAdd(&dc->sat[fi], (unsigned long long)c_sat);
   }
   if (c_nf) atomicAdd(&dc->nonfinite, (unsigned long long)c_nf);
@@ -835,10 +907,10 @@ extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t*
 }
 
 extern "C" __global__ void __launch_bounds__(64, Spec::P2G_MINB)
-    qmpm_p2g(const uint32_t* rec, uint32_t* perm, const uint8_t* cells, const uint32_t* block_start,
-             const uint32_t* active_list, const qmpm::DevCounters* dc, const uint32_t* block_slot, float4* mp,
-             qmpm::SimDev S) {
-  qmpm::p2g_body<Spec>(rec, perm, cells, block_start, active_list, dc, block_slot, mp, S);
+    qmpm_p2g(const uint32_t* rec, const uint32_t* perm, const uint8_t* cells, uint32_t* perm_cell,
+             const uint32_t* block_start, const uint32_t* active_list, const qmpm::DevCounters* dc,
+             const uint32_t* block_slot, float4* mp, qmpm::SimDev S) {
+  qmpm::p2g_body<Spec>(rec, perm, cells, perm_cell, block_start, active_list, dc, block_slot, mp, S);
 }
 
 extern "C" __global__ void __launch_bounds__(Spec::G2P_WARPS * 32, Spec::G2P_MINB)
