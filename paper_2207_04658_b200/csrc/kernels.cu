@@ -180,24 +180,43 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __r
   }
 }
 
-__global__ void k_bin_scatter(const uint32_t* __restrict__ key, uint32_t n,
-                              const uint32_t* __restrict__ block_start, uint32_t* __restrict__ block_count,
-                              uint32_t* __restrict__ perm, uint8_t* __restrict__ cells) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = i < n;
-  const uint32_t full = valid ? key[i] : kDeadKey;
-  const bool live = full != kDeadKey;
-  const uint32_t k = live ? (full >> 6) : 0xffffffffu;  // block of the sort key
-  const unsigned peers = __match_any_sync(FULL, k);
-  const int leader = __ffs(peers) - 1;
-  const int rank = __popc(peers & lanemask_lt());
-  uint32_t old = 0;
-  if (live && (int)(threadIdx.x & 31) == leader) old = atomicSub(&block_count[k], (uint32_t)__popc(peers));
-  old = __shfl_sync(FULL, old, leader);
-  if (live) {
-    const uint32_t pos = block_start[k] + old - 1 - rank;
-    perm[pos] = i;
-    cells[pos] = (uint8_t)(full & 63u);  // base cell in the block, for P2G's ordering
+// kBinItems particles per thread (strided by the CTA size, so loads stay coalesced):
+// the per-particle chain key -> atomic -> store is latency-bound, so several chains
+// are kept in flight per thread.
+constexpr int kBinItems = 4;
+__global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ key, uint32_t n,
+                                                      const uint32_t* __restrict__ block_start,
+                                                      uint32_t* __restrict__ block_count, uint32_t* __restrict__ perm,
+                                                      uint8_t* __restrict__ cells) {
+  const uint32_t i0 = blockIdx.x * (blockDim.x * kBinItems) + threadIdx.x;
+  uint32_t full[kBinItems], k[kBinItems], old[kBinItems], bs[kBinItems];
+  unsigned peers[kBinItems];
+#pragma unroll
+  for (int u = 0; u < kBinItems; ++u) {
+    const uint32_t i = i0 + u * blockDim.x;
+    full[u] = i < n ? __ldg(key + i) : kDeadKey;
+    k[u] = full[u] != kDeadKey ? (full[u] >> 6) : 0xffffffffu;  // block of the sort key
+  }
+#pragma unroll
+  for (int u = 0; u < kBinItems; ++u) {
+    peers[u] = __match_any_sync(FULL, k[u]);
+    const int leader = __ffs(peers[u]) - 1;
+    old[u] = 0;
+    bs[u] = 0;
+    if (k[u] != 0xffffffffu && (int)(threadIdx.x & 31) == leader) {
+      old[u] = atomicSub(&block_count[k[u]], (uint32_t)__popc(peers[u]));
+      bs[u] = __ldg(block_start + k[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kBinItems; ++u) {
+    const int leader = __ffs(peers[u]) - 1;
+    const uint32_t base = __shfl_sync(FULL, bs[u] + old[u], leader);
+    if (k[u] != 0xffffffffu) {
+      const uint32_t pos = base - 1 - __popc(peers[u] & lanemask_lt());
+      perm[pos] = i0 + u * blockDim.x;
+      cells[pos] = (uint8_t)(full[u] & 63u);  // base cell in the block, for P2G's cell sort
+    }
   }
 }
 
@@ -420,7 +439,8 @@ static cudaError_t sort_d(const StepBuffers& B, const SimDev& S, cudaStream_t st
   H(KScanApply, 0);
   if (B.n) {
     H(KBinScatter, 1);
-    k_bin_scatter<<<(B.n + 255) / 256, 256, 0, st>>>(B.key, B.n, B.block_start, B.block_count, B.perm, B.cells);
+    k_bin_scatter<<<(B.n + 256 * kBinItems - 1) / (256 * kBinItems), 256, 0, st>>>(B.key, B.n, B.block_start,
+                                                                                  B.block_count, B.perm, B.cells);
     H(KBinScatter, 0);
   }
   return cudaGetLastError();

@@ -435,13 +435,15 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     cp_async_commit();
     if (k0 + 1 < k1) record_async<SP>(rec, idx_src[k0 + 1], ring + 64 * W);
     cp_async_commit();
+    uint32_t idx_next = k0 + 2 < k1 ? idx_src[k0 + 2] : 0u;  // index of the record issued next
     int slot = 0;
 #pragma unroll 1
     for (uint32_t k = k0; k < k1; ++k) {
       {
         const int s2 = slot == 0 ? 2 : slot - 1;  // (slot + 2) % 3
-        if (k + 2 < k1) record_async<SP>(rec, idx_src[k + 2], ring + s2 * 64 * W);
+        if (k + 2 < k1) record_async<SP>(rec, idx_next, ring + s2 * 64 * W);
         cp_async_commit();
+        if (k + 3 < k1) idx_next = idx_src[k + 3];
       }
       cp_async_wait<2>();
       uint32_t w[W + 1];
@@ -664,11 +666,12 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
     block_coords<D>(b, S, bc);
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
     // first chunk's records in flight while the tile is staged
-    uint32_t r_next = 0;
+    uint32_t r_next = 0, r_after = 0;  // record indices of the next chunk and the one after
     if ((uint32_t)lane < end - start) {
       r_next = perm[start + lane];
       record_async<SP>(rec_in, r_next, wring + lane * W);
     }
+    if (start + 32 + lane < end) r_after = perm[start + 32 + lane];
     cp_async_commit();
     int buf = 0;
     // slots of the block and its +x/+y(/+z) neighbours, then the velocity tile
@@ -703,10 +706,11 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       {  // the next chunk's records go in flight while this one computes
         const uint32_t jn = j0 + 32 + lane;
         if (jn < end) {
-          r_next = perm[jn];
+          r_next = r_after;
           record_async<SP>(rec_in, r_next, wring + ((buf ^ 1) * 32 + lane) * W);
         }
         cp_async_commit();
+        if (jn + 32 < end) r_after = perm[jn + 32];
       }
       cp_async_wait<1>();
       uint32_t w[W + 1];
