@@ -50,8 +50,7 @@ struct qmpm_ctx {
   uint32_t* ids[2] = {nullptr, nullptr};
   uint32_t* key = nullptr;
   uint32_t* perm = nullptr;
-  uint8_t* cells = nullptr;
-  uint32_t* perm_cell = nullptr;
+  uint32_t* cell_count = nullptr;  // [nblocks * 64]
   uint32_t *block_count = nullptr, *block_start = nullptr, *block_slot = nullptr;
   uint32_t *active_list = nullptr, *touched_list = nullptr;
   uint4 *tile_sums = nullptr, *tile_off = nullptr;
@@ -236,9 +235,10 @@ qmpm_status copy_in(qmpm_ctx* ctx, void* dst, const void* src, size_t bytes) {
 
 qmpm_status rebin(qmpm_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->block_count, 0, sizeof(uint32_t) * ctx->S.nblocks, ctx->stream));
+  CK(cudaMemsetAsync(ctx->cell_count, 0, sizeof(uint32_t) * 64 * (size_t)ctx->S.nblocks, ctx->stream));
   hook_fn(ctx, KBinCount, 1);
-  CK(launch_bin_count(ctx->rec[ctx->cur], 0u, (uint32_t)ctx->n, ctx->S, ctx->key, ctx->block_count, 1, ctx->jit,
-                      ctx->stream));
+  CK(launch_bin_count(ctx->rec[ctx->cur], 0u, (uint32_t)ctx->n, ctx->S, ctx->key, ctx->block_count, ctx->cell_count,
+                      1, ctx->jit, ctx->stream));
   hook_fn(ctx, KBinCount, 0);
   ctx->binned = true;
   return QMPM_OK;
@@ -303,7 +303,7 @@ qmpm_status qmpm_layout(const qmpm_scheme* scheme, uint32_t* words_per_particle,
 qmpm_status qmpm_destroy(qmpm_ctx* ctx) {
   if (!ctx) return QMPM_OK;
   cudaStreamSynchronize(ctx->stream);
-  void* ptrs[] = {ctx->rec[0], ctx->rec[1], ctx->ids[0], ctx->ids[1], ctx->key, ctx->perm, ctx->cells, ctx->perm_cell,
+  void* ptrs[] = {ctx->rec[0], ctx->rec[1], ctx->ids[0], ctx->ids[1], ctx->key, ctx->perm, ctx->cell_count,
                   ctx->block_count, ctx->block_start, ctx->block_slot, ctx->active_list, ctx->touched_list,
                   ctx->tile_sums, ctx->tile_off, ctx->mp, ctx->gv, ctx->dc, ctx->dbg};
   for (void* p : ptrs)
@@ -451,8 +451,7 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   }
   ALLOC(ctx->key, sizeof(uint32_t) * cap);
   ALLOC(ctx->perm, sizeof(uint32_t) * cap);
-  ALLOC(ctx->cells, cap);
-  ALLOC(ctx->perm_cell, sizeof(uint32_t) * cap);
+  ALLOC(ctx->cell_count, sizeof(uint32_t) * 64 * nblocks);
   ALLOC(ctx->block_count, sizeof(uint32_t) * nblocks);
   ALLOC(ctx->block_start, sizeof(uint32_t) * (nblocks + 1));
   ALLOC(ctx->block_slot, sizeof(uint32_t) * nblocks);
@@ -467,6 +466,7 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
 #undef ALLOC
   cudaError_t e = cudaMemsetAsync(ctx->mp, 0, sizeof(float4) * 64 * ctx->pool, ctx->stream);
   if (!e) e = cudaMemsetAsync(ctx->block_count, 0, sizeof(uint32_t) * nblocks, ctx->stream);
+  if (!e) e = cudaMemsetAsync(ctx->cell_count, 0, sizeof(uint32_t) * 64 * nblocks, ctx->stream);
   if (!e) e = cudaMemsetAsync(ctx->dc, 0, sizeof(DevCounters), ctx->stream);
   if (!e) e = cudaMemsetAsync(ctx->rec[0], 0, sizeof(uint32_t) * (cap * W + 1), ctx->stream);
   if (!e) e = cudaMemsetAsync(ctx->rec[1], 0, sizeof(uint32_t) * (cap * W + 1), ctx->stream);
@@ -581,8 +581,8 @@ StepBuffers buffers(qmpm_ctx* ctx, uint64_t n) {
   B.ids_out = ctx->ids[ctx->cur ^ 1];
   B.key = ctx->key;
   B.perm = ctx->perm;
-  B.cells = ctx->cells;
-  B.perm_cell = ctx->perm_cell;
+  B.cell_count = ctx->cell_count;
+  B.num_sms = ctx->jit.num_sms;
   B.block_count = ctx->block_count;
   B.block_start = ctx->block_start;
   B.block_slot = ctx->block_slot;
@@ -633,11 +633,11 @@ qmpm_status slab_b(qmpm_ctx* ctx, uint32_t arr) {
   StepBuffers B = buffers(ctx, n_slots);
   if (arr) {
     ctx->launches_total += 1;
-    CK(launch_bin_count(ctx->rec[ctx->cur], (uint32_t)ctx->n, arr, ctx->S, ctx->key, ctx->block_count, 0, ctx->jit,
-                        ctx->stream));
+    CK(launch_bin_count(ctx->rec[ctx->cur], (uint32_t)ctx->n, arr, ctx->S, ctx->key, ctx->block_count,
+                        ctx->cell_count, 0, ctx->jit, ctx->stream));
   }
-  ctx->launches_total += 1;
-  CK(launch_recount(B, ctx->S, n_slots, ctx->stream));
+  ctx->launches_total += 2;
+  CK(launch_recount(B, ctx->S, n_slots, ctx->jit.num_sms, ctx->stream));
   CK(launch_sort(ctx->dim, B, ctx->S, ctx->stream, hook_fn, ctx));
   CK(launch_p2g(B, ctx->S, ctx->jit, ctx->stream, hook_fn, ctx));
   if (ctx->S.slab_hi) {

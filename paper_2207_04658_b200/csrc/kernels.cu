@@ -4,7 +4,8 @@
 //
 //   k_scan_*       a1  exclusive scan over the dense block table: particle offsets,
 //                      active-block list, touched-block (pool slot) assignment
-//   k_bin_scatter  a1  counting-sort scatter: perm[sorted slot] = record index
+//   k_cell_scan    a1  per active block: cell counts -> cell cursors (end positions)
+//   k_bin_scatter  a1  counting-sort scatter by (block, cell): perm[sorted slot] = record index
 //   k_grid_update  a4  v = p/m + dt g, separating walls; clears (m, p) for next step
 //   k_encode/k_decode  Eq. 3 / Eq. 11 + bit pack for set_state, read_state and the
 //                      standalone qmpm_encode / qmpm_decode
@@ -180,43 +181,74 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __r
   }
 }
 
-// kBinItems particles per thread (strided by the CTA size, so loads stay coalesced):
-// the per-particle chain key -> atomic -> store is latency-bound, so several chains
-// are kept in flight per thread.
+// Cell-level cursors of the counting sort by (block, base cell): one warp per active
+// block turns the 64 cell counts (accumulated by G2P / bin_count) into END positions
+// block_start[b] + inclusive prefix; the scatter's atomicSub leaves each at its cell's
+// START, which P2G reads (and zeroes for the next step's counts).  The block's count
+// has been consumed by the scan: it is zeroed here for the next step's histogram.
+__global__ void k_cell_scan(uint32_t* __restrict__ cell_count, uint32_t* __restrict__ block_count,
+                            const uint32_t* __restrict__ block_start, const uint32_t* __restrict__ active_list,
+                            const DevCounters* __restrict__ dc) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t n_active = dc->n_active;
+  for (uint32_t ab = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ab < n_active; ab += warps) {
+    const uint32_t b = active_list[ab];
+    uint32_t* cc = cell_count + (size_t)b * 64;
+    const uint32_t c0 = cc[lane], c1 = cc[lane + 32];
+    uint32_t i0 = c0, i1 = c1;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t0 = __shfl_up_sync(FULL, i0, d), t1 = __shfl_up_sync(FULL, i1, d);
+      if ((int)lane >= d) {
+        i0 += t0;
+        i1 += t1;
+      }
+    }
+    const uint32_t base = block_start[b];
+    const uint32_t tot0 = __shfl_sync(FULL, i0, 31);
+    cc[lane] = base + i0;
+    cc[lane + 32] = base + tot0 + i1;
+    if (lane == 0) block_count[b] = 0u;
+  }
+}
+
+// zero the cell counters of the active blocks (slab sort pass 1 -> recount)
+__global__ void k_cell_reset(uint32_t* __restrict__ cell_count, const uint32_t* __restrict__ active_list,
+                             const DevCounters* __restrict__ dc) {
+  const uint32_t n = dc->n_active * 64u;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    cell_count[(size_t)active_list[t >> 6] * 64 + (t & 63u)] = 0u;
+}
+
+// Counting-sort scatter by the full key (block, base cell): perm[pos] = record index,
+// pos from a warp-aggregated atomicSub on the key's cell cursor.  kBinItems particles
+// per thread (strided by the CTA size, so loads stay coalesced): the per-particle
+// chain key -> atomic -> store is latency-bound, so several are kept in flight.
 constexpr int kBinItems = 4;
 __global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ key, uint32_t n,
-                                                      const uint32_t* __restrict__ block_start,
-                                                      uint32_t* __restrict__ block_count, uint32_t* __restrict__ perm,
-                                                      uint8_t* __restrict__ cells) {
+                                                      uint32_t* __restrict__ cell_count, uint32_t* __restrict__ perm) {
   const uint32_t i0 = blockIdx.x * (blockDim.x * kBinItems) + threadIdx.x;
-  uint32_t full[kBinItems], k[kBinItems], old[kBinItems], bs[kBinItems];
+  uint32_t k[kBinItems], old[kBinItems];
   unsigned peers[kBinItems];
 #pragma unroll
   for (int u = 0; u < kBinItems; ++u) {
     const uint32_t i = i0 + u * blockDim.x;
-    full[u] = i < n ? __ldg(key + i) : kDeadKey;
-    k[u] = full[u] != kDeadKey ? (full[u] >> 6) : 0xffffffffu;  // block of the sort key
+    k[u] = i < n ? __ldg(key + i) : kDeadKey;
   }
 #pragma unroll
   for (int u = 0; u < kBinItems; ++u) {
     peers[u] = __match_any_sync(FULL, k[u]);
     const int leader = __ffs(peers[u]) - 1;
     old[u] = 0;
-    bs[u] = 0;
-    if (k[u] != 0xffffffffu && (int)(threadIdx.x & 31) == leader) {
-      old[u] = atomicSub(&block_count[k[u]], (uint32_t)__popc(peers[u]));
-      bs[u] = __ldg(block_start + k[u]);
-    }
+    if (k[u] != kDeadKey && (int)(threadIdx.x & 31) == leader)
+      old[u] = atomicSub(&cell_count[k[u]], (uint32_t)__popc(peers[u]));
   }
 #pragma unroll
   for (int u = 0; u < kBinItems; ++u) {
     const int leader = __ffs(peers[u]) - 1;
-    const uint32_t base = __shfl_sync(FULL, bs[u] + old[u], leader);
-    if (k[u] != 0xffffffffu) {
-      const uint32_t pos = base - 1 - __popc(peers[u] & lanemask_lt());
-      perm[pos] = i0 + u * blockDim.x;
-      cells[pos] = (uint8_t)(full[u] & 63u);  // base cell in the block, for P2G's cell sort
-    }
+    const uint32_t top = __shfl_sync(FULL, old[u], leader);
+    if (k[u] != kDeadKey) perm[top - 1 - __popc(peers[u] & lanemask_lt())] = i0 + u * blockDim.x;
   }
 }
 
@@ -288,7 +320,8 @@ __global__ void k_pack_leavers(const uint32_t* __restrict__ rec, const uint32_t*
 // Count the particles this rank owns (block inside the slab) for the second sort;
 // keys of the others become kDeadKey so the scatter drops them.
 template <int D>
-__global__ void k_recount(uint32_t* __restrict__ key, uint32_t n, SimDev S, uint32_t* __restrict__ block_count) {
+__global__ void k_recount(uint32_t* __restrict__ key, uint32_t n, SimDev S, uint32_t* __restrict__ block_count,
+                          uint32_t* __restrict__ cell_count) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t k = 0xffffffffu;
   if (i < n) {
@@ -305,6 +338,9 @@ __global__ void k_recount(uint32_t* __restrict__ key, uint32_t n, SimDev S, uint
   }
   const unsigned peers = __match_any_sync(FULL, k);
   if (k != 0xffffffffu && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
+  const uint32_t full = k != 0xffffffffu ? key[i] : kDeadKey;
+  const unsigned cp = __match_any_sync(FULL, full);
+  if (full != kDeadKey && (threadIdx.x & 31) == (unsigned)(__ffs(cp) - 1)) atomicAdd(&cell_count[full], __popc(cp));
 }
 
 // Dense copy of one z block plane of a float4 node array (all nbx * nby blocks,
@@ -439,8 +475,9 @@ static cudaError_t sort_d(const StepBuffers& B, const SimDev& S, cudaStream_t st
   H(KScanApply, 0);
   if (B.n) {
     H(KBinScatter, 1);
-    k_bin_scatter<<<(B.n + 256 * kBinItems - 1) / (256 * kBinItems), 256, 0, st>>>(B.key, B.n, B.block_start,
-                                                                                  B.block_count, B.perm, B.cells);
+    k_cell_scan<<<B.num_sms * 8, 256, 0, st>>>(B.cell_count, B.block_count, B.block_start, B.active_list, B.dc);
+    k_bin_scatter<<<(B.n + 256 * kBinItems - 1) / (256 * kBinItems), 256, 0, st>>>(B.key, B.n, B.cell_count,
+                                                                                  B.perm);
     H(KBinScatter, 0);
   }
   return cudaGetLastError();
@@ -455,9 +492,9 @@ cudaError_t launch_p2g(const StepBuffers& B, const SimDev& S, const StepJit& J, 
   Hk H{hook, user};
   H(KP2G, 1);
   SimDev Sv = S;
-  void* args[] = {(void*)&B.rec_in,      (void*)&B.perm, (void*)&B.cells,      (void*)&B.perm_cell,
-                  (void*)&B.block_start, (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot,
-                  (void*)&B.mp,          (void*)&Sv};
+  void* args[] = {(void*)&B.rec_in,      (void*)&B.perm, (void*)&B.cell_count, (void*)&B.block_start,
+                  (void*)&B.active_list, (void*)&B.dc,   (void*)&B.block_slot, (void*)&B.mp,
+                  (void*)&Sv};
   cudaError_t e = jit_launch(J.p2g, J.p2g_ctas, J.p2g_threads, J.p2g_smem, st, args);
   H(KP2G, 0);
   return e;
@@ -481,8 +518,8 @@ cudaError_t launch_g2p(const StepBuffers& B, const SimDev& S, uint32_t salt, con
   H(KG2P, 1);
   SimDev Sv = S;
   uint32_t saltv = salt;
-  void* args[] = {(void*)&B.rec_in, (void*)&B.rec_out, (void*)&B.perm_cell, (void*)&B.ids_in, (void*)&B.ids_out,
-                  (void*)&B.dbg, (void*)&B.key, (void*)&B.block_count, (void*)&B.block_start,
+  void* args[] = {(void*)&B.rec_in, (void*)&B.rec_out, (void*)&B.perm, (void*)&B.ids_in, (void*)&B.ids_out,
+                  (void*)&B.dbg, (void*)&B.key, (void*)&B.block_count, (void*)&B.cell_count, (void*)&B.block_start,
                   (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot, (void*)&B.gv, (void*)&Sv,
                   (void*)&saltv};
   cudaError_t e = jit_launch(J.g2p, J.g2p_ctas, J.g2p_threads, J.g2p_smem, st, args);
@@ -500,11 +537,12 @@ cudaError_t launch_step(int dim, const StepBuffers& B, const SimDev& S, uint32_t
 }
 
 cudaError_t launch_bin_count(const uint32_t* rec, uint32_t first, uint32_t n, const SimDev& S, uint32_t* key,
-                             uint32_t* block_count, int do_count, const StepJit& J, cudaStream_t st) {
+                             uint32_t* block_count, uint32_t* cell_count, int do_count, const StepJit& J,
+                             cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   SimDev Sv = S;
-  void* args[] = {(void*)&rec, (void*)&first, (void*)&n, (void*)&Sv, (void*)&key, (void*)&block_count,
-                  (void*)&do_count};
+  void* args[] = {(void*)&rec,         (void*)&first,      (void*)&n,       (void*)&Sv,
+                  (void*)&key,         (void*)&block_count, (void*)&cell_count, (void*)&do_count};
   return jit_launch(J.bin_count, (n + 255) / 256, 256, 0, st, args);
 }
 
@@ -518,9 +556,10 @@ cudaError_t launch_pack_leavers(const StepBuffers& B, const SimDev& S, uint32_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_recount(const StepBuffers& B, const SimDev& S, uint32_t n, cudaStream_t st) {
+cudaError_t launch_recount(const StepBuffers& B, const SimDev& S, uint32_t n, int num_sms, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  k_recount<3><<<(n + 255) / 256, 256, 0, st>>>(B.key, n, S, B.block_count);
+  k_cell_reset<<<num_sms * 4, 256, 0, st>>>(B.cell_count, B.active_list, B.dc);  // pass-1 cursors
+  k_recount<3><<<(n + 255) / 256, 256, 0, st>>>(B.key, n, S, B.block_count, B.cell_count);
   return cudaGetLastError();
 }
 

@@ -16,9 +16,9 @@ struct StepBuffers {
   const uint32_t* ids_in;  // nullable
   uint32_t* ids_out;       // nullable
   uint32_t* key;           // [n] block key of each record in rec_in order (in), rec_out order (out)
-  uint32_t* perm;          // [n] sorted slot -> rec_in index
-  uint8_t* cells;          // [n] base cell in its block, per sorted slot
-  uint32_t* perm_cell;     // [n] P2G's re-sort of perm by (block, base cell); G2P's order
+  uint32_t* perm;          // [n] sorted slot -> rec_in index, sorted by (block, base cell)
+  uint32_t* cell_count;    // [nblocks * 64] per (block, cell): next step's counts (G2P) ->
+                           // cursors (k_cell_scan) -> cell starts (scatter) -> 0 (P2G)
   uint32_t* block_count;   // [nblocks]
   uint32_t* block_start;   // [nblocks + 1]
   uint32_t* block_slot;    // [nblocks]
@@ -33,6 +33,7 @@ struct StepBuffers {
   uint32_t n;
   uint32_t pool;
   uint32_t ntiles;
+  int num_sms;
 };
 
 constexpr int kScanTile = 1024;  // grid blocks per scan tile
@@ -74,11 +75,12 @@ cudaError_t launch_g2p(const StepBuffers& B, const SimDev& S, uint32_t salt, con
                        KernelHook hook, void* user);
 // keys (+ optional histogram) of records [first, first + n)
 cudaError_t launch_bin_count(const uint32_t* rec, uint32_t first, uint32_t n, const SimDev& S, uint32_t* key,
-                             uint32_t* block_count, int do_count, const StepJit& J, cudaStream_t st);
+                             uint32_t* block_count, uint32_t* cell_count, int do_count, const StepJit& J,
+                             cudaStream_t st);
 cudaError_t launch_pack_leavers(const StepBuffers& B, const SimDev& S, uint32_t W, uint32_t cap, uint32_t* send_dn,
                                 uint32_t* send_up, uint32_t* ids_dn, uint32_t* ids_up, int num_sms,
                                 cudaStream_t st);
-cudaError_t launch_recount(const StepBuffers& B, const SimDev& S, uint32_t n, cudaStream_t st);
+cudaError_t launch_recount(const StepBuffers& B, const SimDev& S, uint32_t n, int num_sms, cudaStream_t st);
 // mode 0: pack plane bz of `nodes` into buf; 1: add buf into the plane; 2: store buf into the plane
 cudaError_t launch_plane(float4* nodes, const uint32_t* block_slot, const SimDev& S, int bz, float4* buf, int mode,
                          int num_sms, cudaStream_t st);

@@ -8,9 +8,9 @@
 // the re-encode packs into registers (no read-modify-write of shared words).
 //
 //   qmpm_bin_count  a1        block key + histogram (first step after set_state/set_words)
-//   qmpm_p2g        a2+a3     sort the block by base cell; lane = cell accumulates its
-//                             particles' 3^d stencil in registers; one tile RMW per node
-//                             per cell (no atomics), red.global.add.v4.f32 flush
+//   qmpm_p2g        a2+a3     balanced per-cell segments; a lane accumulates its segment's
+//                             3^d stencil in registers; one tile RMW per node per
+//                             segment (no atomics), red.global.add.v4.f32 flush
 //   qmpm_g2p        a2+a5-a7  gather from a shared-memory tile, update, dithered encode,
 //                             coalesced store in sorted order, next step's block key
 #pragma once
@@ -177,11 +177,12 @@ __device__ __forceinline__ void store_records(uint32_t* __restrict__ out, uint32
 template <class SP>
 __device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec, uint32_t first, uint32_t n,
                                                const SimDev& S, uint32_t* __restrict__ key,
-                                               uint32_t* __restrict__ block_count, int do_count) {
+                                               uint32_t* __restrict__ block_count,
+                                               uint32_t* __restrict__ cell_count, int do_count) {
   constexpr int D = SP::D, W = SP::W;
   const uint32_t i = first + blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < first + n;
-  uint32_t k = 0xffffffffu;
+  uint32_t k = 0xffffffffu, full = kDeadKey;
   if (valid) {
     uint32_t w[W + 1];
 #pragma unroll
@@ -190,20 +191,16 @@ __device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec,
     float x[3];
 #pragma unroll
     for (int a = 0; a < D; ++a) x[a] = sdec<SP>(w, a);
-    const uint32_t full = key_of<D>(x, S);
+    full = key_of<D>(x, S);
     key[i] = full;
     k = full >> 6;
   }
   if (!do_count) return;
   const unsigned peers = __match_any_sync(FULL, k);
   if (valid && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
+  const unsigned cp = __match_any_sync(FULL, full);
+  if (valid && (threadIdx.x & 31) == (unsigned)(__ffs(cp) - 1)) atomicAdd(&cell_count[full], __popc(cp));
 }
-
-#ifndef QMPM_P2G_CAP
-#define QMPM_P2G_CAP 5120
-#endif
-constexpr int kP2GCap = QMPM_P2G_CAP;  // block particles whose sorted indices stay in shared memory
-constexpr int kSortU = 4;              // loads in flight per thread in the sort passes
 
 // per-warp shared-memory footprint of the two step kernels (16-byte multiples)
 template <class SP>
@@ -211,8 +208,8 @@ struct Smem {
   static constexpr int TN = Geo<SP::D>::TN;
   static constexpr int TILE = 16 * TN;
   static constexpr int STAGE = ((4 * 32 * SP::SW) + 15) / 16 * 16;
-  // private node tile + half of s_perm + half of the 3-slot record ring
-  static constexpr int P2G_WARP = TILE + 4 * QMPM_P2G_CAP / 2 + 3 * 32 * 4 * SP::W;
+  // private node tile + half of the 3-slot record ring
+  static constexpr int P2G_WARP = TILE + 3 * 32 * 4 * SP::W;
   // velocity tile + 8 neighbour slots + double-buffered record stage
   static constexpr int G2P_WARP = TILE + 32 + (2 * 32 * 4 * SP::W + 15) / 16 * 16;
 };
@@ -302,24 +299,33 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 }
 
 // ------------------------------------------------------------------ a3: P2G
-// One CTA of 2 warps per active block, grid-stride; lane `tid` OWNS base cell `tid`
-// of the block (64 cells = 4^3 in 3D, 8^2 in 2D).
-//   1. counting sort of the block's particles by base cell (shared histogram, scan,
-//      warp-aggregated cursors): perm_cell[block range] = the block's records in cell
-//      order (also the order G2P processes, and hence stores, them in);
-//   2. lane c walks its cell's particles: load + decode the record (the next one in
-//      flight), stress and affine momentum, and accumulates all 3^d stencil nodes x
-//      (m, p) in REGISTERS -- no shared-memory traffic per particle;
-//   3. one read-modify-write per stencil node per cell into the warp's private tile:
-//      lanes own distinct cells, so for a fixed stencil offset their nodes are
-//      distinct; __syncwarp orders successive offsets;
+// One CTA of 2 warps per active block, grid-stride.  The global counting sort orders
+// particles by (block, base cell), and its cursors leave each cell's start in
+// cell_count, so the block's 64 cell ranges are known without a local sort.
+//   1. segment table: cell c is cut into ceil(n_c / kSegL) segments (at most kSegLev;
+//      the last takes the rest), listed level-major (all first segments in cell
+//      order, then all second segments, ...); group g = entries [32 g, 32 g + 32) is
+//      processed by warp g % 2, one segment per lane: lanes get near-equal work
+//      whatever the cells' occupancy (remainders cluster in the late levels);
+//   2. a lane walks its segment: records stream through a per-lane 3-slot cp.async
+//      ring (two in flight), decode, stress and affine momentum, and accumulates all
+//      3^d stencil nodes x (m, p) in REGISTERS -- no shared-memory traffic per particle;
+//   3. per group, one read-modify-write per stencil node per lane into the warp's
+//      private tile: lanes holding distinct cells touch distinct nodes for a fixed
+//      offset; lanes sharing a cell (a group straddling two levels) take turns;
 //   4. the two warp tiles are summed and flushed with one red.global.add.v4.f32 per
 //      non-empty node.
 // Momentum at stencil node o of a particle: m v + aff (o - fx) dx = Q + sum_k o_k a_k,
 // a_k = dx aff[:, k], Q = m v - sum_k fx_k a_k (Hu et al. 2018 APIC/MLS form).
+#ifndef QMPM_SEG_L
+#define QMPM_SEG_L 16
+#endif
+constexpr int kSegL = QMPM_SEG_L;  // particles per P2G segment (one lane, one group)
+constexpr int kSegLev = 32;        // segments per cell at most (the last one takes the rest)
+
 template <class SP>
 __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const uint32_t* __restrict__ perm,
-                                         const uint8_t* __restrict__ cells, uint32_t* perm_cell,
+                                         uint32_t* __restrict__ cell_count,
                                          const uint32_t* __restrict__ block_start,
                                          const uint32_t* __restrict__ active_list,
                                          const DevCounters* __restrict__ dc,
@@ -329,26 +335,15 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
   constexpr int NN = D == 3 ? 27 : 9;  // stencil nodes
   using G = Geo<D>;
   extern __shared__ float4 smem4[];
-  __shared__ uint32_t s_cnt[64], s_cur[64], s_start[65];
+  __shared__ uint32_t s_start[65], s_nseg, s_lmask[kSegLev][2], s_lstart[kSegLev];
+  __shared__ uint32_t s_seg[64 * kSegLev];
+  __shared__ uint8_t s_ns[64];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  float4* tiles = smem4;                                               // [2][TN]
-  uint32_t* s_perm = reinterpret_cast<uint32_t*>(tiles + 2 * G::TN);  // [kP2GCap]
-  uint32_t* s_ring = s_perm + kP2GCap;                                 // [3][64][W] record ring
+  float4* tiles = smem4;                                          // [2][TN]
+  uint32_t* s_ring = reinterpret_cast<uint32_t*>(tiles + 2 * G::TN);  // [3][64][W] record ring
   float4* tile = tiles + warp * G::TN;
+  uint32_t* ring = s_ring + tid * W;  // this lane's slots: ring + q * 64 * W
   const uint32_t n_active = dc->n_active;
-  // this lane's cell and the tile index of its stencil's first node
-  int lc[3];
-  if (D == 3) {
-    lc[0] = (tid >> 4) & 3;
-    lc[1] = (tid >> 2) & 3;
-    lc[2] = tid & 3;
-  } else {
-    lc[0] = (tid >> 3) & 7;
-    lc[1] = tid & 7;
-    lc[2] = 0;
-  }
-  const int base_idx = D == 3 ? (lc[0] * G::T + lc[1]) * G::T + lc[2] : lc[0] * G::T + lc[1];
-
   for (uint32_t ab = blockIdx.x; ab < n_active; ab += gridDim.x) {
     const uint32_t b = active_list[ab];
     const uint32_t start = block_start[b], end = block_start[b + 1];
@@ -356,184 +351,204 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     block_coords<D>(b, S, bc);
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
     for (int t = tid; t < 2 * G::TN; t += 64) tiles[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    s_cnt[tid] = 0u;
+    {  // cell starts (the scatter left them in cell_count); zero them for the next step
+      uint32_t* cc = cell_count + (size_t)b * 64;
+      s_start[tid] = cc[tid] - start;
+      cc[tid] = 0u;
+      if (tid == 0) s_start[64] = end - start;
+    }
     __syncthreads();
-    // ---- 1. counting sort of the block by base cell.  Loads are batched (kSortU per
-    // thread in flight) so the histogram and scatter passes are not latency-bound; the
-    // sorted record indices stay in shared memory (s_perm) when the block fits.
-    const uint32_t n_blk = end - start;
-    const bool in_smem = n_blk <= (uint32_t)kP2GCap;
-    for (uint32_t i0 = start + warp * 32; i0 < end; i0 += 64 * kSortU) {
-      uint32_t c[kSortU];
-#pragma unroll
-      for (int u = 0; u < kSortU; ++u) {
-        const uint32_t i = i0 + u * 64 + lane;
-        c[u] = i < end ? (uint32_t)__ldg(cells + i) : 64u + lane;
-      }
-#pragma unroll
-      for (int u = 0; u < kSortU; ++u) {
-        const uint32_t i = i0 + u * 64 + lane;
-        const unsigned peers = __match_any_sync(FULL, c[u]);
-        if (i < end && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[c[u]], (unsigned)__popc(peers));
+    // ---- 1. segment table
+    {
+      const uint32_t nc = s_start[tid + 1] - s_start[tid];
+      const uint32_t ns = min((nc + kSegL - 1) / kSegL, (uint32_t)kSegLev);
+      s_ns[tid] = (uint8_t)ns;
+      for (int l = 0; l < kSegLev; ++l) {
+        const unsigned m = __ballot_sync(FULL, ns > (uint32_t)l);
+        if (lane == 0) s_lmask[l][warp] = m;
       }
     }
     __syncthreads();
-    if (warp == 0) {  // exclusive scan of the 64 cell counts
-      const uint32_t c0 = s_cnt[lane], c1 = s_cnt[lane + 32];
-      uint32_t i0 = c0, i1 = c1;
+    if (warp == 0) {  // level starts (exclusive scan of the level sizes)
+      const uint32_t sz = lane < kSegLev ? __popc(s_lmask[lane][0]) + __popc(s_lmask[lane][1]) : 0u;
+      uint32_t inc = sz;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t0 = __shfl_up_sync(FULL, i0, d), t1 = __shfl_up_sync(FULL, i1, d);
-        if (lane >= d) {
-          i0 += t0;
-          i1 += t1;
-        }
+        const uint32_t t = __shfl_up_sync(FULL, inc, d);
+        if (lane >= d) inc += t;
       }
-      const uint32_t tot0 = __shfl_sync(FULL, i0, 31);
-      s_start[lane] = i0 - c0;
-      s_start[lane + 32] = tot0 + i1 - c1;
-      s_cur[lane] = i0 - c0;
-      s_cur[lane + 32] = tot0 + i1 - c1;
-      if (lane == 31) s_start[64] = tot0 + i1;
+      if (lane < kSegLev) s_lstart[lane] = inc - sz;
+      if (lane == 31) s_nseg = inc;
     }
     __syncthreads();
-    for (uint32_t i0 = start + warp * 32; i0 < end; i0 += 64 * kSortU) {
-      uint32_t c[kSortU], p[kSortU];
-#pragma unroll
-      for (int u = 0; u < kSortU; ++u) {
-        const uint32_t i = i0 + u * 64 + lane;
-        const bool v = i < end;
-        c[u] = v ? (uint32_t)__ldg(cells + i) : 64u + lane;
-        p[u] = v ? __ldg(perm + i) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < kSortU; ++u) {
-        const uint32_t i = i0 + u * 64 + lane;
-        const bool v = i < end;
-        const unsigned peers = __match_any_sync(FULL, c[u]);
-        const int leader = __ffs(peers) - 1;
-        uint32_t base = 0;
-        if (v && lane == leader) base = atomicAdd(&s_cur[c[u]], (unsigned)__popc(peers));
-        base = __shfl_sync(FULL, base, leader);
-        const uint32_t pos = base + __popc(peers & lanemask_lt());
-        if (v) {
-          perm_cell[start + pos] = p[u];
-          if (in_smem) s_perm[pos] = p[u];
-        }
+    {
+      const uint32_t ns = s_ns[tid];
+      for (uint32_t l = 0; l < ns; ++l) {
+        const uint32_t e =
+            s_lstart[l] + (warp ? __popc(s_lmask[l][0]) : 0u) + __popc(s_lmask[l][warp] & lanemask_lt());
+        s_seg[e] = (tid << 16) | l;
       }
     }
-    __syncthreads();  // perm_cell / s_perm of the block are visible to the whole CTA
-    // ---- 2. lane `tid` accumulates its cell's particles
-    const uint32_t* idx_src = in_smem ? s_perm : perm_cell + start;
-    const uint32_t k0 = s_start[tid], k1 = s_start[tid + 1];
-    float am[NN], ax[NN], ay[NN], az[NN];
-#pragma unroll
-    for (int q = 0; q < NN; ++q) am[q] = ax[q] = ay[q] = az[q] = 0.0f;
-    // records stream through a per-lane 3-slot shared ring, two in flight (cp.async)
-    uint32_t* ring = s_ring + tid * W;  // slot q at ring + q * 64 * W
-    if (k0 < k1) record_async<SP>(rec, idx_src[k0], ring);
-    cp_async_commit();
-    if (k0 + 1 < k1) record_async<SP>(rec, idx_src[k0 + 1], ring + 64 * W);
-    cp_async_commit();
-    uint32_t idx_next = k0 + 2 < k1 ? idx_src[k0 + 2] : 0u;  // index of the record issued next
-    int slot = 0;
-#pragma unroll 1
-    for (uint32_t k = k0; k < k1; ++k) {
-      {
-        const int s2 = slot == 0 ? 2 : slot - 1;  // (slot + 2) % 3
-        if (k + 2 < k1) record_async<SP>(rec, idx_next, ring + s2 * 64 * W);
-        cp_async_commit();
-        if (k + 3 < k1) idx_next = idx_src[k + 3];
+    __syncthreads();
+    const uint32_t nseg = s_nseg;
+    const uint32_t ngroups = (nseg + 31) / 32;
+    const uint32_t* pidx = perm + start;  // the block's record indices in (cell) order
+    // particle range [k, e) of segment entry i (empty past the table)
+    auto seg_range = [&](uint32_t i, uint32_t& k, uint32_t& e, int& c) {
+      if (i < nseg) {
+        const uint32_t v = s_seg[i];
+        c = (int)(v >> 16);
+        const uint32_t l = v & 0xffffu;
+        k = s_start[c] + l * kSegL;
+        e = (l + 1 == (uint32_t)s_ns[c]) ? s_start[c + 1] : k + kSegL;
+      } else {
+        k = e = 0u;
+        c = 0;
       }
-      cp_async_wait<2>();
-      uint32_t w[W + 1];
-      read_staged<SP>(ring + slot * 64 * W, w);
-      slot = slot == 2 ? 0 : slot + 1;
-      float s[NSV];
-#pragma unroll
-      for (int i = 0; i < NSV; ++i) s[i] = sdec<SP>(w, i);
-      float fx[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        bool o;
-        base_fx(s[a], S.inv_dx, S.res[a], fx[a], o);
-      }
-      float aff[D * D];
-      affine_of<D, MAT>(s, S, aff);
-      float Q[3] = {0.f, 0.f, 0.f}, A[3][3];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        Q[a] = S.p_mass * s[D + a];
-#pragma unroll
-        for (int k2 = 0; k2 < D; ++k2) {
-          A[k2][a] = S.dx * aff[a * D + k2];
-          Q[a] = fmaf(-fx[k2], A[k2][a], Q[a]);
+    };
+    // ---- 2. the fetch cursor walks this lane's segments of all its groups ahead of
+    // the compute; fidx = pidx[fk] is loaded one fetch ahead
+    uint32_t fg = warp, fk, fe, fidx = 0u;
+    int fslot = 0, slot = 0;
+    {
+      int c_;
+      seg_range(fg * 32 + lane, fk, fe, c_);
+      if (fk < fe) fidx = __ldg(pidx + fk);
+    }
+    auto fetch = [&]() {
+      if (fk < fe) {
+        record_async<SP>(rec, fidx, ring + fslot * 64 * W);
+        fslot = fslot == 2 ? 0 : fslot + 1;
+        if (++fk == fe) {
+          fg += 2;
+          int c_;
+          seg_range(fg * 32 + lane, fk, fe, c_);
         }
+        if (fk < fe) fidx = __ldg(pidx + fk);
       }
-      float wt[3][3];
+      cp_async_commit();
+    };
+    fetch();
+    fetch();
+#pragma unroll 1
+    for (uint32_t g = warp; g < ngroups; g += 2) {
+      uint32_t k0, k1;
+      int c;
+      seg_range(g * 32 + lane, k0, k1, c);
+      float am[NN], ax[NN], ay[NN], az[NN];
 #pragma unroll
-      for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
-      if (D == 3) {
-#pragma unroll
-        for (int ox = 0; ox < 3; ++ox) {
-#pragma unroll
-          for (int oy = 0; oy < 3; ++oy) {
-            const float wxy = wt[0][ox] * wt[1][oy];
-            float M[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) M[a] = Q[a] + (float)ox * A[0][a] + (float)oy * A[1][a];
-#pragma unroll
-            for (int oz = 0; oz < 3; ++oz) {
-              const int q = (ox * 3 + oy) * 3 + oz;
-              const float ww = wxy * wt[2][oz];
+      for (int q = 0; q < NN; ++q) am[q] = ax[q] = ay[q] = az[q] = 0.0f;
+#pragma unroll 1
+      for (uint32_t k = k0; k < k1; ++k) {
+        fetch();
+        cp_async_wait<2>();
+        uint32_t w[W + 1];
+        read_staged<SP>(ring + slot * 64 * W, w);
+        slot = slot == 2 ? 0 : slot + 1;
+        float s[NSV];
+  #pragma unroll
+        for (int i = 0; i < NSV; ++i) s[i] = sdec<SP>(w, i);
+        float fx[3] = {0.f, 0.f, 0.f};
+  #pragma unroll
+        for (int a = 0; a < D; ++a) {
+          bool o;
+          base_fx(s[a], S.inv_dx, S.res[a], fx[a], o);
+        }
+        float aff[D * D];
+        affine_of<D, MAT>(s, S, aff);
+        float Q[3] = {0.f, 0.f, 0.f}, A[3][3];
+  #pragma unroll
+        for (int a = 0; a < D; ++a) {
+          Q[a] = S.p_mass * s[D + a];
+  #pragma unroll
+          for (int k2 = 0; k2 < D; ++k2) {
+            A[k2][a] = S.dx * aff[a * D + k2];
+            Q[a] = fmaf(-fx[k2], A[k2][a], Q[a]);
+          }
+        }
+        float wt[3][3];
+  #pragma unroll
+        for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
+        if (D == 3) {
+  #pragma unroll
+          for (int ox = 0; ox < 3; ++ox) {
+  #pragma unroll
+            for (int oy = 0; oy < 3; ++oy) {
+              const float wxy = wt[0][ox] * wt[1][oy];
+              float M[3];
+  #pragma unroll
+              for (int a = 0; a < 3; ++a) M[a] = Q[a] + (float)ox * A[0][a] + (float)oy * A[1][a];
+  #pragma unroll
+              for (int oz = 0; oz < 3; ++oz) {
+                const int q = (ox * 3 + oy) * 3 + oz;
+                const float ww = wxy * wt[2][oz];
+                am[q] += ww;
+                ax[q] = fmaf(ww, M[0], ax[q]);
+                ay[q] = fmaf(ww, M[1], ay[q]);
+                az[q] = fmaf(ww, M[2], az[q]);
+                if (oz < 2) {
+  #pragma unroll
+                  for (int a = 0; a < 3; ++a) M[a] += A[2][a];
+                }
+              }
+            }
+          }
+        } else {
+  #pragma unroll
+          for (int ox = 0; ox < 3; ++ox) {
+            float M[2];
+  #pragma unroll
+            for (int a = 0; a < 2; ++a) M[a] = Q[a] + (float)ox * A[0][a];
+  #pragma unroll
+            for (int oy = 0; oy < 3; ++oy) {
+              const int q = ox * 3 + oy;
+              const float ww = wt[0][ox] * wt[1][oy];
               am[q] += ww;
               ax[q] = fmaf(ww, M[0], ax[q]);
               ay[q] = fmaf(ww, M[1], ay[q]);
-              az[q] = fmaf(ww, M[2], az[q]);
-              if (oz < 2) {
-#pragma unroll
-                for (int a = 0; a < 3; ++a) M[a] += A[2][a];
+              if (oy < 2) {
+                M[0] += A[1][0];
+                M[1] += A[1][1];
               }
             }
           }
         }
+      }
+      // ---- 3. one RMW per stencil node of the segment's cell (m = p_mass * sum w)
+      const bool mine = k1 > k0;
+      int lc[3];
+      if (D == 3) {
+        lc[0] = (c >> 4) & 3;
+        lc[1] = (c >> 2) & 3;
+        lc[2] = c & 3;
       } else {
+        lc[0] = (c >> 3) & 7;
+        lc[1] = c & 7;
+        lc[2] = 0;
+      }
+      const int base_idx = D == 3 ? (lc[0] * G::T + lc[1]) * G::T + lc[2] : lc[0] * G::T + lc[1];
+      const unsigned peers = __match_any_sync(FULL, mine ? (unsigned)c : 64u + lane);
+      const int occ = __popc(peers & lanemask_lt());
+      const int nocc = (int)__reduce_max_sync(FULL, (unsigned)__popc(peers));
+#pragma unroll 1
+      for (int o = 0; o < nocc; ++o) {
 #pragma unroll
-        for (int ox = 0; ox < 3; ++ox) {
-          float M[2];
-#pragma unroll
-          for (int a = 0; a < 2; ++a) M[a] = Q[a] + (float)ox * A[0][a];
-#pragma unroll
-          for (int oy = 0; oy < 3; ++oy) {
-            const int q = ox * 3 + oy;
-            const float ww = wt[0][ox] * wt[1][oy];
-            am[q] += ww;
-            ax[q] = fmaf(ww, M[0], ax[q]);
-            ay[q] = fmaf(ww, M[1], ay[q]);
-            if (oy < 2) {
-              M[0] += A[1][0];
-              M[1] += A[1][1];
-            }
+        for (int q = 0; q < NN; ++q) {
+          const int ox = D == 3 ? q / 9 : q / 3, oy = D == 3 ? (q / 3) % 3 : q % 3, oz = D == 3 ? q % 3 : 0;
+          const int idx = base_idx + (D == 3 ? (ox * G::T + oy) * G::T + oz : ox * G::T + oy);
+          if (mine && occ == o) {
+            float4 t = tile[idx];
+            t.x = fmaf(am[q], S.p_mass, t.x);
+            t.y += ax[q];
+            t.z += ay[q];
+            t.w += az[q];
+            tile[idx] = t;
           }
+          __syncwarp();
         }
       }
     }
-    // ---- 3. one RMW per stencil node of the cell (m = p_mass * sum w)
-    const bool mine = k1 > k0;
-#pragma unroll
-    for (int q = 0; q < NN; ++q) {
-      const int ox = D == 3 ? q / 9 : q / 3, oy = D == 3 ? (q / 3) % 3 : q % 3, oz = D == 3 ? q % 3 : 0;
-      const int idx = base_idx + (D == 3 ? (ox * G::T + oy) * G::T + oz : ox * G::T + oy);
-      if (mine) {
-        float4 t = tile[idx];
-        t.x = fmaf(am[q], S.p_mass, t.x);
-        t.y += ax[q];
-        t.z += ay[q];
-        t.w += az[q];
-        tile[idx] = t;
-      }
-      __syncwarp();
-    }
+    cp_async_wait<0>();
     __syncthreads();
     // ---- 4. flush: sum the two warp tiles, one vector reduction per non-empty node
     for (int t = tid; t < G::TN; t += 64) {
@@ -639,7 +654,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
                                          const uint32_t* __restrict__ perm, const uint32_t* __restrict__ ids_in,
                                          uint32_t* __restrict__ ids_out, float* __restrict__ dbg,
                                          uint32_t* __restrict__ key_out, uint32_t* __restrict__ block_count,
-                                         const uint32_t* __restrict__ block_start,
+                                         uint32_t* __restrict__ cell_count, const uint32_t* __restrict__ block_start,
                                          const uint32_t* __restrict__ active_list, DevCounters* __restrict__ dc,
                                          const uint32_t* __restrict__ block_slot, const float4* __restrict__ gv,
                                          const SimDev& S, uint32_t salt) {
@@ -864,6 +879,8 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       const uint32_t nk = valid ? (nkey >> 6) : 0xffffffffu;
       const unsigned kp = __match_any_sync(FULL, nk);
       if (valid && lane == __ffs(kp) - 1) atomicAdd(&block_count[nk], (unsigned)__popc(kp));
+      const unsigned cp = __match_any_sync(FULL, valid ? nkey : kDeadKey);
+      if (valid && lane == __ffs(cp) - 1) atomicAdd(&cell_count[nkey], (unsigned)__popc(cp));
       if (valid) {
         if (ids_out != nullptr) ids_out[j] = ids_in[r];
         uint32_t* op = rec_out + (size_t)j * W;
@@ -906,22 +923,22 @@ extern "C" __device__ const unsigned qmpm_smem_per_warp[2] = {(unsigned)qmpm::Sm
                                                              (unsigned)qmpm::Smem<Spec>::G2P_WARP};
 extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t* rec, uint32_t first, uint32_t n,
                                                                  qmpm::SimDev S, uint32_t* key, uint32_t* block_count,
-                                                                 int do_count) {
-  qmpm::bin_count_body<Spec>(rec, first, n, S, key, block_count, do_count);
+                                                                 uint32_t* cell_count, int do_count) {
+  qmpm::bin_count_body<Spec>(rec, first, n, S, key, block_count, cell_count, do_count);
 }
 
 extern "C" __global__ void __launch_bounds__(64, Spec::P2G_MINB)
-    qmpm_p2g(const uint32_t* rec, const uint32_t* perm, const uint8_t* cells, uint32_t* perm_cell,
-             const uint32_t* block_start, const uint32_t* active_list, const qmpm::DevCounters* dc,
-             const uint32_t* block_slot, float4* mp, qmpm::SimDev S) {
-  qmpm::p2g_body<Spec>(rec, perm, cells, perm_cell, block_start, active_list, dc, block_slot, mp, S);
+    qmpm_p2g(const uint32_t* rec, const uint32_t* perm, uint32_t* cell_count, const uint32_t* block_start,
+             const uint32_t* active_list, const qmpm::DevCounters* dc, const uint32_t* block_slot, float4* mp,
+             qmpm::SimDev S) {
+  qmpm::p2g_body<Spec>(rec, perm, cell_count, block_start, active_list, dc, block_slot, mp, S);
 }
 
 extern "C" __global__ void __launch_bounds__(Spec::G2P_WARPS * 32, Spec::G2P_MINB)
     qmpm_g2p(const uint32_t* rec_in, uint32_t* rec_out, const uint32_t* perm, const uint32_t* ids_in,
-             uint32_t* ids_out, float* dbg, uint32_t* key_out, uint32_t* block_count, const uint32_t* block_start,
-             const uint32_t* active_list, qmpm::DevCounters* dc, const uint32_t* block_slot, const float4* gv,
-             qmpm::SimDev S, uint32_t salt) {
-  qmpm::g2p_body<Spec>(rec_in, rec_out, perm, ids_in, ids_out, dbg, key_out, block_count, block_start, active_list,
-                       dc, block_slot, gv, S, salt);
+             uint32_t* ids_out, float* dbg, uint32_t* key_out, uint32_t* block_count, uint32_t* cell_count,
+             const uint32_t* block_start, const uint32_t* active_list, qmpm::DevCounters* dc,
+             const uint32_t* block_slot, const float4* gv, qmpm::SimDev S, uint32_t salt) {
+  qmpm::g2p_body<Spec>(rec_in, rec_out, perm, ids_in, ids_out, dbg, key_out, block_count, cell_count, block_start,
+                       active_list, dc, block_slot, gv, S, salt);
 }

@@ -250,3 +250,43 @@ def test_round_counters_match_oracle_on_identical_floats():
     assert list(st.round_up)[:nf] == list(c[64:64 + nf])
     assert list(st.round_down)[:nf] == list(c[128:128 + nf])
     assert list(st.saturations)[:nf] == list(c[:nf])
+
+
+@pytest.mark.parametrize("case", ["s3_3d_e0.01", "s4_3d_fluid_f2", "c1_2d_x16"])
+def test_p2g_short_segments(case, monkeypatch):
+    """Short P2G segments (many groups straddling levels, so lanes sharing a cell take
+    turns in the flush) and the level cap (cells with more than kSegLev segments, whose
+    last segment takes the rest) meet the same P2 bar: the step kernels are
+    re-specialised with a segment length of 2 particles."""
+    monkeypatch.setenv("QMPM_JIT_OPTS", "-DQMPM_SEG_L=2")
+    mk_scene, mk_scheme, warm = CASES[case]
+    sc, sch = mk_scene(), mk_scheme()
+    w0, _ = oracle.encode_state(sch, sc.state())
+    w_in, _ = oracle.run(sc.sim, sch, w0, 1, 3)
+    o_pre, _, _ = oracle.step(sc.sim, sch, w_in, 4, "f64")
+    g_pre, g_words, st = run_gpu_step(sc, sch, w_in, 4)
+    s = scales(sc.sim, o_pre, oracle.decode_state(sch, w_in))
+    err = np.abs(g_pre.astype(np.float64) - o_pre) / np.maximum(np.abs(o_pre), s)
+    assert err.max() <= REL, err.max(axis=0)
+    keys = np.array([oracle.particle_key(sch, w_in[i]) for i in range(w_in.shape[0])], np.uint32)
+    assert np.array_equal(g_words, oracle.encode_state(sch, g_pre, step=4, keys=keys)[0])
+
+
+@pytest.mark.parametrize("rounding", ["dither", "rne"])
+def test_saturating_step_matches_codec(rounding):
+    """A v range far below the velocities forces the G2P re-encode's rare (exact,
+    saturating) path: the stored words and the saturation / round counters still equal
+    the oracle codec's on the GPU's pre-encode floats."""
+    sc = scenes.c1()
+    sch = schemes.with_rounding(schemes.x16(v_range=2.0 ** -6), rounding)
+    w0, _ = oracle.encode_state(sch, sc.state())
+    w_in, _ = oracle.run(sc.sim, sch, w0, 1, 40)
+    g_pre, g_words, st = run_gpu_step(sc, sch, w_in, 41)
+    keys = np.array([oracle.particle_key(sch, w_in[i]) for i in range(w_in.shape[0])], np.uint32)
+    w_ref, c = oracle.encode_state(sch, g_pre, step=41, keys=keys)
+    assert np.array_equal(g_words, w_ref)
+    nf = len(sch["fields"])
+    assert sum(c[:nf]) > 0  # the case really saturates
+    assert list(st.saturations)[:nf] == list(c[:nf])
+    assert list(st.round_up)[:nf] == list(c[64:64 + nf])
+    assert list(st.round_down)[:nf] == list(c[128:128 + nf])
