@@ -1,6 +1,6 @@
 """Capacity probe: the largest particle count one B200 holds for the
 fp32 layout vs a quantized scheme, with the SAME code and every per-particle array
-counted (two record buffers, sort key, permutation, cell byte), at the C3 grid.
+counted (two record buffers, sort key, permutation), at the C3 grid.
 
     python bench_capacity.py [--schemes fp32,e0.01] [--grid 1024]
 

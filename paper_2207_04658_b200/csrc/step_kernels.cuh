@@ -407,24 +407,32 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
       }
     };
     // ---- 2. the fetch cursor walks this lane's segments of all its groups ahead of
-    // the compute; fidx = pidx[fk] is loaded one fetch ahead
-    uint32_t fg = warp, fk, fe, fidx = 0u;
+    // the compute: fidx = pidx[fk] is loaded one fetch ahead, and the next segment's
+    // first index (nidx) a whole segment ahead (it starts a new cache line)
+    uint32_t fk, fe, fidx = 0u, nk, ne, nidx = 0u, fg = warp + 2;
     int fslot = 0, slot = 0;
     {
       int c_;
-      seg_range(fg * 32 + lane, fk, fe, c_);
+      seg_range(warp * 32 + lane, fk, fe, c_);
       if (fk < fe) fidx = __ldg(pidx + fk);
+      seg_range(fg * 32 + lane, nk, ne, c_);
+      if (nk < ne) nidx = __ldg(pidx + nk);
     }
     auto fetch = [&]() {
       if (fk < fe) {
         record_async<SP>(rec, fidx, ring + fslot * 64 * W);
         fslot = fslot == 2 ? 0 : fslot + 1;
         if (++fk == fe) {
+          fk = nk;
+          fe = ne;
+          fidx = nidx;
           fg += 2;
           int c_;
-          seg_range(fg * 32 + lane, fk, fe, c_);
+          seg_range(fg * 32 + lane, nk, ne, c_);
+          if (nk < ne) nidx = __ldg(pidx + nk);
+        } else {
+          fidx = __ldg(pidx + fk);
         }
-        if (fk < fe) fidx = __ldg(pidx + fk);
       }
       cp_async_commit();
     };
@@ -697,20 +705,30 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       nslot[lane] = sl;
     }
     __syncwarp();
-    for (int t = lane; t < G::TN; t += 32) {
-      int node[3];
-      tile_node<D>(t, org, node);
-      int sel = 0, ln[3] = {0, 0, 0};
+    {  // all of the lane's tile loads in flight at once, then the shared stores
+      constexpr int TPL = (G::TN + 31) / 32;
+      float4 v[TPL];
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const int hi = (node[a] - org[a]) >= G::B;
-        sel |= hi << a;
-        ln[a] = node[a] & (G::B - 1);
+      for (int u = 0; u < TPL; ++u) {
+        const int t = lane + 32 * u;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (t < G::TN) {
+          int node[3];
+          tile_node<D>(t, org, node);
+          int sel = 0, ln[3] = {0, 0, 0};
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const int hi = (node[a] - org[a]) >= G::B;
+            sel |= hi << a;
+            ln[a] = node[a] & (G::B - 1);
+          }
+          const uint32_t slot = nslot[sel];
+          if (slot != 0xffffffffu) v[u] = gv[(size_t)slot * 64 + local_node<D>(ln)];
+        }
       }
-      const uint32_t slot = nslot[sel];
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (slot != 0xffffffffu) v = gv[(size_t)slot * 64 + local_node<D>(ln)];
-      tile[t] = v;
+#pragma unroll
+      for (int u = 0; u < TPL; ++u)
+        if (lane + 32 * u < G::TN) tile[lane + 32 * u] = v[u];
     }
     __syncwarp();
 
@@ -876,11 +894,13 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
       const uint32_t nkey = key_of<D>(xq, S);
       if (valid) key_out[j] = nkey;
-      const uint32_t nk = valid ? (nkey >> 6) : 0xffffffffu;
-      const unsigned kp = __match_any_sync(FULL, nk);
-      if (valid && lane == __ffs(kp) - 1) atomicAdd(&block_count[nk], (unsigned)__popc(kp));
-      const unsigned cp = __match_any_sync(FULL, valid ? nkey : kDeadKey);
-      if (valid && lane == __ffs(cp) - 1) atomicAdd(&cell_count[nkey], (unsigned)__popc(cp));
+      {  // next step's histograms, one atomic per distinct key of the warp
+        const uint32_t nk = valid ? (nkey >> 6) : 0xffffffffu;
+        const unsigned kp = __match_any_sync(FULL, nk);
+        if (valid && lane == __ffs(kp) - 1) atomicAdd(&block_count[nk], (unsigned)__popc(kp));
+        const unsigned cp = __match_any_sync(FULL, valid ? nkey : kDeadKey);
+        if (valid && lane == __ffs(cp) - 1) atomicAdd(&cell_count[nkey], (unsigned)__popc(cp));
+      }
       if (valid) {
         if (ids_out != nullptr) ids_out[j] = ids_in[r];
         uint32_t* op = rec_out + (size_t)j * W;

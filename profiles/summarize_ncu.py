@@ -1,7 +1,12 @@
 """Summarise an ncu report: key metrics, stall reasons and the SASS opcode mix per kernel.
 
-    python profiles/summarize_ncu.py gpurun_out/prof.ncu-rep > profiles/<round>_<name>.txt
+    python profiles/summarize_ncu.py gpurun_out/prof.ncu-rep [--traffic-json profiles/ncu_traffic.json]
+        > profiles/<round>_<name>.txt
+
+--traffic-json writes dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes)
+for each kernel ("p2g", "g2p", ...), the `traffic` term bench.py reports.
 """
+import json
 import collections
 import csv
 import io
@@ -18,7 +23,11 @@ def run(args):
     return subprocess.run(["ncu"] + args, capture_output=True, text=True).stdout
 
 
-def main(rep):
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def main(rep, traffic_json=None):
+    traffic = {}
     rows = list(csv.reader(io.StringIO(run(["-i", rep, "--page", "details", "--csv"]))))
     h = rows[0]
     ki, mi, vi, ui, ii = (h.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit", "ID"))
@@ -33,6 +42,14 @@ def main(rep):
             if w in m:
                 print(f"   {w:38s} {m[w][0]} {m[w][1]}")
         d = dict(zip(rh, raw[2 + n])) if len(raw) > 2 + n else {}
+        units = dict(zip(rh, raw[1])) if len(raw) > 1 else {}
+        try:
+            tb = sum(float(d[kk].replace(",", "")) * UNIT.get(units.get(kk, "byte"), 1.0)
+                     for kk in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            traffic[k.replace("qmpm_", "").replace("qmpm::k_", "")] = tb
+            print(f"   {'dram read+write per launch (bytes)':60s} {tb:.4e}")
+        except (KeyError, ValueError):
+            pass
         for key in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__inst_executed.sum",
                     "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum",
                     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
@@ -81,5 +98,10 @@ def main(rep):
                 print(f"      {op:10s} {100 * c / max(tot, 1):5.1f}% of instr  {100 * stl[op] / max(tst, 1):5.1f}% of stall samples")
 
 
+    if traffic_json:
+        json.dump(traffic, open(traffic_json, "w"), indent=1)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1])
+    tj = sys.argv[sys.argv.index("--traffic-json") + 1] if "--traffic-json" in sys.argv else None
+    main(sys.argv[1], tj)
