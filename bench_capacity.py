@@ -62,7 +62,7 @@ def main():
     for name in args.schemes.split(","):
         sch = schemes.fp32(3) if name == "fp32" else schemes.BY_NAME[name]()
         _, W, _ = qmpm.layout(sch)
-        out["bytes_per_particle"][name] = 2 * 4 * W + 4 + 4 + 1  # records x2, key, perm, cell
+        out["bytes_per_particle"][name] = 2 * 4 * W + 4 + 4  # records x2, key, perm
         lo = int(args.lo)
         if not try_n(scene, sch, lo, torch, qmpm):
             out["capacity"][name] = None
