@@ -35,14 +35,19 @@ uint32_t oracle_mix32(uint32_t x) {
 
 /* 24-bit uniform integer for (seed, step, particle key, field index).
  * salt = mix(seed_lo ^ mix(seed_hi ^ mix(step)));  h = mix(key ^ salt);
- * r24 = mix(h + field * 0x9E3779B9) >> 8.   (reading Q5; step taken mod 2^32) */
+ * per field (reading Q5, revision 2): x = (h ^ field * 0x9E3779B9) * 0x7feb352d;
+ * x ^= x >> 15;  r24 = (x * 0x846ca68b) >> 8 -- the second half of lowbias32 applied
+ * to the field-salted particle hash (every step a bijection of h, so r24 is uniform
+ * whenever h is).  (step taken mod 2^32) */
 uint32_t oracle_r24(uint64_t seed, uint64_t step, uint32_t key, uint32_t field) {
     uint32_t seed_lo = (uint32_t)(seed & 0xffffffffu);
     uint32_t seed_hi = (uint32_t)(seed >> 32);
     uint32_t salt = oracle_mix32(seed_lo ^ oracle_mix32(seed_hi ^ oracle_mix32((uint32_t)step)));
     uint32_t h = oracle_mix32(key ^ salt);
-    uint32_t r = oracle_mix32(h + field * 0x9E3779B9u);
-    return r >> 8;
+    uint32_t x = (h ^ (field * 0x9E3779B9u)) * 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    return x >> 8;
 }
 
 static uint32_t field_width(const oracle_scheme* s, uint32_t f) {

@@ -130,6 +130,8 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const uint4* __restrict__ t
   }
   if (threadIdx.x == 0) {
     dc->n_active = total.y;
+    dc->next_p2g = 0u;
+    dc->next_g2p = 0u;
     dc->n_touched = total.z;
     dc->n_touched_eff = total.z < pool ? total.z : pool;
     dc->n_sorted = total.x;

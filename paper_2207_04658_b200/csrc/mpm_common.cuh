@@ -72,9 +72,8 @@ __device__ __forceinline__ uint32_t local_node(const int l[3]) {
 }
 
 // sort key of a particle from its (decoded) position: block id * 64 + the base cell's
-// index inside its block (x-major).  Binning sorts by block (key >> 6); P2G orders a
-// block's particles by (rank within cell, cell) so that a warp's lanes have distinct
-// base cells.
+// index inside its block (x-major).  The counting sort orders particles by this full
+// key, so P2G finds each cell's particles as a contiguous range.
 template <int D>
 __device__ __forceinline__ uint32_t key_of(const float* x, const SimDev& S) {
   int c[3] = {0, 0, 0}, l[3] = {0, 0, 0};
@@ -83,6 +82,21 @@ __device__ __forceinline__ uint32_t key_of(const float* x, const SimDev& S) {
     float fx;
     bool o;
     const int b = base_fx(x[a], S.inv_dx, S.res[a], fx, o);
+    c[a] = b >> Geo<D>::LB;
+    l[a] = b & (Geo<D>::B - 1);
+  }
+  return (block_id<D>(c, S) << 6) | local_node<D>(l);
+}
+
+// key_of without the clamp; `oob` set when any axis is out of the domain (the caller
+// then recomputes with key_of)
+template <int D>
+__device__ __forceinline__ uint32_t key_of_fast(const float* x, const SimDev& S, bool& oob) {
+  int c[3] = {0, 0, 0}, l[3] = {0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    float fx;
+    const int b = base_fx_fast(x[a], S.inv_dx, S.res[a], fx, oob);
     c[a] = b >> Geo<D>::LB;
     l[a] = b & (Geo<D>::B - 1);
   }

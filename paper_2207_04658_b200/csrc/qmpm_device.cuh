@@ -88,6 +88,8 @@ struct DevCounters {
   unsigned int n_active;      // last step
   unsigned int n_touched;     // last step (before clamping to the pool)
   unsigned int n_touched_eff; // min(n_touched, pool)
+  unsigned int next_p2g;      // dynamic work counters of P2G / G2P (active-list position),
+  unsigned int next_g2p;      // reset by the scan every step
   unsigned int pad;
 };
 
@@ -116,9 +118,12 @@ __host__ __device__ __forceinline__ uint32_t step_salt(uint32_t seed_lo, uint32_
   return mix32_hd(seed_lo ^ mix32_hd(seed_hi ^ mix32_hd(step)));
 }
 
-// r24 for (particle hash h = mix(key ^ salt), field index f)
+// r24 for (particle hash h = mix(key ^ salt), field index f): reading Q5 (revision 2),
+// the second half of lowbias32 on the field-salted particle hash
 __device__ __forceinline__ uint32_t r24_of(uint32_t h, uint32_t f) {
-  return mix32(h + f * 0x9E3779B9u) >> 8;
+  uint32_t x = (h ^ (f * 0x9E3779B9u)) * 0x7feb352du;
+  x ^= x >> 15;
+  return (x * 0x846ca68bu) >> 8;
 }
 
 // ---------------------------------------------------------------- decode (Eq. 3)
@@ -205,6 +210,16 @@ __device__ __forceinline__ int base_fx(float x, float inv_dx, int n_axis, float&
   float f = __fsub_rn(X, (float)b);
   if (oob) f = fminf(fmaxf(f, 0.5f), 1.5f);
   fx = f;
+  return b;
+}
+
+// The same without the clamp: `oob` is OR-accumulated and the caller redoes the warp
+// with base_fx() when any lane saw it (identical arithmetic when in the domain).
+__device__ __forceinline__ int base_fx_fast(float x, float inv_dx, int n_axis, float& fx, bool& oob) {
+  const float X = __fmul_rn(x, inv_dx);
+  const int b = (int)floorf(__fsub_rn(X, 0.5f));
+  oob |= (unsigned)b > (unsigned)(n_axis - 3);
+  fx = __fsub_rn(X, (float)b);
   return b;
 }
 

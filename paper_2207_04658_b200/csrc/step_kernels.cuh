@@ -208,8 +208,6 @@ struct Smem {
   static constexpr int TN = Geo<SP::D>::TN;
   static constexpr int TILE = 16 * TN;
   static constexpr int STAGE = ((4 * 32 * SP::SW) + 15) / 16 * 16;
-  // private node tile + half of the 3-slot record ring
-  static constexpr int P2G_WARP = TILE + 3 * 32 * 4 * SP::W;
   // velocity tile + 8 neighbour slots + double-buffered record stage
   static constexpr int G2P_WARP = TILE + 32 + (2 * 32 * 4 * SP::W + 15) / 16 * 16;
 };
@@ -299,22 +297,22 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 }
 
 // ------------------------------------------------------------------ a3: P2G
-// One CTA of 2 warps per active block, grid-stride.  The global counting sort orders
-// particles by (block, base cell), and its cursors leave each cell's start in
+// One WARP per active block (taken dynamically from a work counter; the warps of a CTA
+// are independent, so there is no CTA barrier and no tail).  The global counting sort
+// orders particles by (block, base cell) and its cursors leave each cell's start in
 // cell_count, so the block's 64 cell ranges are known without a local sort.
 //   1. segment table: cell c is cut into ceil(n_c / kSegL) segments (at most kSegLev;
-//      the last takes the rest), listed level-major (all first segments in cell
-//      order, then all second segments, ...); group g = entries [32 g, 32 g + 32) is
-//      processed by warp g % 2, one segment per lane: lanes get near-equal work
-//      whatever the cells' occupancy (remainders cluster in the late levels);
-//   2. a lane walks its segment: records stream through a per-lane 3-slot cp.async
-//      ring (two in flight), decode, stress and affine momentum, and accumulates all
-//      3^d stencil nodes x (m, p) in REGISTERS -- no shared-memory traffic per particle;
+//      the last takes the rest), listed level-major (all first segments in cell order,
+//      then all second segments, ...); group g = entries [32 g, 32 g + 32), one segment
+//      per lane: lanes get near-equal work whatever the cells' occupancy (remainders
+//      cluster in the late levels);
+//   2. a lane walks its segment: records stream through a per-lane 3-slot cp.async ring
+//      (two in flight), decode, stress and affine momentum, and it accumulates all 3^d
+//      stencil nodes x (m, p) in REGISTERS -- no shared-memory traffic per particle;
 //   3. per group, one read-modify-write per stencil node per lane into the warp's
 //      private tile: lanes holding distinct cells touch distinct nodes for a fixed
 //      offset; lanes sharing a cell (a group straddling two levels) take turns;
-//   4. the two warp tiles are summed and flushed with one red.global.add.v4.f32 per
-//      non-empty node.
+//   4. the tile is flushed with one red.global.add.v4.f32 per non-empty node.
 // Momentum at stencil node o of a particle: m v + aff (o - fx) dx = Q + sum_k o_k a_k,
 // a_k = dx aff[:, k], Q = m v - sum_k fx_k a_k (Hu et al. 2018 APIC/MLS form).
 #ifndef QMPM_SEG_L
@@ -323,82 +321,96 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 constexpr int kSegL = QMPM_SEG_L;  // particles per P2G segment (one lane, one group)
 constexpr int kSegLev = 32;        // segments per cell at most (the last one takes the rest)
 
+// per-warp shared-memory layout of P2G (byte offsets; 16-byte aligned parts first)
+template <class SP>
+struct P2GLayout {
+  static constexpr int TN = Geo<SP::D>::TN;
+  static constexpr int TILE = 0;                               // float4[TN]
+  static constexpr int RING = TILE + 16 * TN;                  // u32[3][32][W]
+  static constexpr int START = RING + 3 * 32 * 4 * SP::W;      // u32[65]
+  static constexpr int LSTART = START + 4 * 68;                // u32[kSegLev]
+  static constexpr int SEG = LSTART + 4 * kSegLev;             // u16[64 * kSegLev]
+  static constexpr int NS = SEG + 2 * 64 * kSegLev;            // u8[64]
+  static constexpr int BYTES = (NS + 64 + 15) / 16 * 16;
+};
+
 template <class SP>
 __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const uint32_t* __restrict__ perm,
                                          uint32_t* __restrict__ cell_count,
                                          const uint32_t* __restrict__ block_start,
-                                         const uint32_t* __restrict__ active_list,
-                                         const DevCounters* __restrict__ dc,
+                                         const uint32_t* __restrict__ active_list, DevCounters* __restrict__ dc,
                                          const uint32_t* __restrict__ block_slot, float4* __restrict__ mp,
                                          const SimDev& S) {
   constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, W = SP::W;
   constexpr int NN = D == 3 ? 27 : 9;  // stencil nodes
   using G = Geo<D>;
+  using LY = P2GLayout<SP>;
   extern __shared__ float4 smem4[];
-  __shared__ uint32_t s_start[65], s_nseg, s_lmask[kSegLev][2], s_lstart[kSegLev];
-  __shared__ uint32_t s_seg[64 * kSegLev];
-  __shared__ uint8_t s_ns[64];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  float4* tiles = smem4;                                          // [2][TN]
-  uint32_t* s_ring = reinterpret_cast<uint32_t*>(tiles + 2 * G::TN);  // [3][64][W] record ring
-  float4* tile = tiles + warp * G::TN;
-  uint32_t* ring = s_ring + tid * W;  // this lane's slots: ring + q * 64 * W
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  char* wb = reinterpret_cast<char*>(smem4) + warp * LY::BYTES;
+  float4* tile = reinterpret_cast<float4*>(wb + LY::TILE);
+  uint32_t* ring = reinterpret_cast<uint32_t*>(wb + LY::RING) + lane * W;  // slot q at ring + q * 32 * W
+  uint32_t* s_start = reinterpret_cast<uint32_t*>(wb + LY::START);
+  uint32_t* s_lstart = reinterpret_cast<uint32_t*>(wb + LY::LSTART);
+  uint16_t* s_seg = reinterpret_cast<uint16_t*>(wb + LY::SEG);
+  uint8_t* s_ns = reinterpret_cast<uint8_t*>(wb + LY::NS);
   const uint32_t n_active = dc->n_active;
-  for (uint32_t ab = blockIdx.x; ab < n_active; ab += gridDim.x) {
+  for (;;) {  // blocks are taken dynamically (a work counter): no tail from uneven blocks
+    uint32_t ab = 0;
+    if (lane == 0) ab = atomicAdd(&dc->next_p2g, 1u);
+    ab = __shfl_sync(FULL, ab, 0);
+    if (ab >= n_active) break;
     const uint32_t b = active_list[ab];
     const uint32_t start = block_start[b], end = block_start[b + 1];
     int bc[3];
     block_coords<D>(b, S, bc);
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
-    for (int t = tid; t < 2 * G::TN; t += 64) tiles[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    {  // cell starts (the scatter left them in cell_count); zero them for the next step
-      uint32_t* cc = cell_count + (size_t)b * 64;
-      s_start[tid] = cc[tid] - start;
-      cc[tid] = 0u;
-      if (tid == 0) s_start[64] = end - start;
+    for (int t = lane; t < G::TN; t += 32) tile[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // cell starts (the scatter left them in cell_count); zeroed for the next step
+    uint32_t* cc = cell_count + (size_t)b * 64;
+    const uint32_t st0 = cc[lane] - start, st1 = cc[lane + 32] - start;
+    cc[lane] = 0u;
+    cc[lane + 32] = 0u;
+    s_start[lane] = st0;
+    s_start[lane + 32] = st1;
+    if (lane == 0) s_start[64] = end - start;
+    __syncwarp();
+    // ---- 1. segment table (lane handles cells lane and lane + 32)
+    const uint32_t nc0 = s_start[lane + 1] - st0, nc1 = s_start[lane + 33] - st1;
+    const uint32_t ns0 = min((nc0 + kSegL - 1) / kSegL, (uint32_t)kSegLev);
+    const uint32_t ns1 = min((nc1 + kSegL - 1) / kSegL, (uint32_t)kSegLev);
+    s_ns[lane] = (uint8_t)ns0;
+    s_ns[lane + 32] = (uint8_t)ns1;
+    const uint32_t nlev = __reduce_max_sync(FULL, max(ns0, ns1));
+    uint32_t sz = 0;  // lane l: size of level l
+    for (uint32_t l = 0; l < nlev; ++l) {
+      const unsigned m0 = __ballot_sync(FULL, ns0 > l), m1 = __ballot_sync(FULL, ns1 > l);
+      if ((uint32_t)lane == l) sz = __popc(m0) + __popc(m1);
     }
-    __syncthreads();
-    // ---- 1. segment table
-    {
-      const uint32_t nc = s_start[tid + 1] - s_start[tid];
-      const uint32_t ns = min((nc + kSegL - 1) / kSegL, (uint32_t)kSegLev);
-      s_ns[tid] = (uint8_t)ns;
-      for (int l = 0; l < kSegLev; ++l) {
-        const unsigned m = __ballot_sync(FULL, ns > (uint32_t)l);
-        if (lane == 0) s_lmask[l][warp] = m;
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {  // level starts (exclusive scan of the level sizes)
-      const uint32_t sz = lane < kSegLev ? __popc(s_lmask[lane][0]) + __popc(s_lmask[lane][1]) : 0u;
-      uint32_t inc = sz;
+    uint32_t inc = sz;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(FULL, inc, d);
-        if (lane >= d) inc += t;
-      }
-      if (lane < kSegLev) s_lstart[lane] = inc - sz;
-      if (lane == 31) s_nseg = inc;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL, inc, d);
+      if (lane >= d) inc += t;
     }
-    __syncthreads();
-    {
-      const uint32_t ns = s_ns[tid];
-      for (uint32_t l = 0; l < ns; ++l) {
-        const uint32_t e =
-            s_lstart[l] + (warp ? __popc(s_lmask[l][0]) : 0u) + __popc(s_lmask[l][warp] & lanemask_lt());
-        s_seg[e] = (tid << 16) | l;
-      }
+    s_lstart[lane] = inc - sz;
+    const uint32_t nseg = __shfl_sync(FULL, inc, 31);
+    __syncwarp();
+    for (uint32_t l = 0; l < nlev; ++l) {
+      const unsigned m0 = __ballot_sync(FULL, ns0 > l), m1 = __ballot_sync(FULL, ns1 > l);
+      const uint32_t ls = s_lstart[l];
+      if (ns0 > l) s_seg[ls + __popc(m0 & lanemask_lt())] = (uint16_t)((lane << 8) | l);
+      if (ns1 > l) s_seg[ls + __popc(m0) + __popc(m1 & lanemask_lt())] = (uint16_t)(((lane + 32) << 8) | l);
     }
-    __syncthreads();
-    const uint32_t nseg = s_nseg;
+    __syncwarp();
     const uint32_t ngroups = (nseg + 31) / 32;
     const uint32_t* pidx = perm + start;  // the block's record indices in (cell) order
     // particle range [k, e) of segment entry i (empty past the table)
     auto seg_range = [&](uint32_t i, uint32_t& k, uint32_t& e, int& c) {
       if (i < nseg) {
         const uint32_t v = s_seg[i];
-        c = (int)(v >> 16);
-        const uint32_t l = v & 0xffffu;
+        c = (int)(v >> 8);
+        const uint32_t l = v & 255u;
         k = s_start[c] + l * kSegL;
         e = (l + 1 == (uint32_t)s_ns[c]) ? s_start[c + 1] : k + kSegL;
       } else {
@@ -406,27 +418,27 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
         c = 0;
       }
     };
-    // ---- 2. the fetch cursor walks this lane's segments of all its groups ahead of
-    // the compute: fidx = pidx[fk] is loaded one fetch ahead, and the next segment's
-    // first index (nidx) a whole segment ahead (it starts a new cache line)
-    uint32_t fk, fe, fidx = 0u, nk, ne, nidx = 0u, fg = warp + 2;
+    // ---- 2. the fetch cursor walks this lane's segments of all groups ahead of the
+    // compute: fidx = pidx[fk] is loaded one fetch ahead, and the next segment's first
+    // index (nidx) a whole segment ahead (it starts a new cache line)
+    uint32_t fk, fe, fidx = 0u, nk, ne, nidx = 0u, fg = 1;
     int fslot = 0, slot = 0;
     {
       int c_;
-      seg_range(warp * 32 + lane, fk, fe, c_);
+      seg_range(lane, fk, fe, c_);
       if (fk < fe) fidx = __ldg(pidx + fk);
-      seg_range(fg * 32 + lane, nk, ne, c_);
+      seg_range(32 + lane, nk, ne, c_);
       if (nk < ne) nidx = __ldg(pidx + nk);
     }
     auto fetch = [&]() {
       if (fk < fe) {
-        record_async<SP>(rec, fidx, ring + fslot * 64 * W);
+        record_async<SP>(rec, fidx, ring + fslot * 32 * W);
         fslot = fslot == 2 ? 0 : fslot + 1;
         if (++fk == fe) {
           fk = nk;
           fe = ne;
           fidx = nidx;
-          fg += 2;
+          fg += 1;
           int c_;
           seg_range(fg * 32 + lane, nk, ne, c_);
           if (nk < ne) nidx = __ldg(pidx + nk);
@@ -439,7 +451,7 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     fetch();
     fetch();
 #pragma unroll 1
-    for (uint32_t g = warp; g < ngroups; g += 2) {
+    for (uint32_t g = 0; g < ngroups; ++g) {
       uint32_t k0, k1;
       int c;
       seg_range(g * 32 + lane, k0, k1, c);
@@ -451,42 +463,49 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
         fetch();
         cp_async_wait<2>();
         uint32_t w[W + 1];
-        read_staged<SP>(ring + slot * 64 * W, w);
+        read_staged<SP>(ring + slot * 32 * W, w);
         slot = slot == 2 ? 0 : slot + 1;
         float s[NSV];
-  #pragma unroll
+#pragma unroll
         for (int i = 0; i < NSV; ++i) s[i] = sdec<SP>(w, i);
         float fx[3] = {0.f, 0.f, 0.f};
-  #pragma unroll
-        for (int a = 0; a < D; ++a) {
-          bool o;
-          base_fx(s[a], S.inv_dx, S.res[a], fx[a], o);
+        {
+          bool oob = false;
+#pragma unroll
+          for (int a = 0; a < D; ++a) base_fx_fast(s[a], S.inv_dx, S.res[a], fx[a], oob);
+          if (__any_sync(__activemask(), oob)) {  // rare: the clamped rule of reading Q14
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              bool o;
+              base_fx(s[a], S.inv_dx, S.res[a], fx[a], o);
+            }
+          }
         }
         float aff[D * D];
         affine_of<D, MAT>(s, S, aff);
         float Q[3] = {0.f, 0.f, 0.f}, A[3][3];
-  #pragma unroll
+#pragma unroll
         for (int a = 0; a < D; ++a) {
           Q[a] = S.p_mass * s[D + a];
-  #pragma unroll
+#pragma unroll
           for (int k2 = 0; k2 < D; ++k2) {
             A[k2][a] = S.dx * aff[a * D + k2];
             Q[a] = fmaf(-fx[k2], A[k2][a], Q[a]);
           }
         }
         float wt[3][3];
-  #pragma unroll
+#pragma unroll
         for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
         if (D == 3) {
-  #pragma unroll
+#pragma unroll
           for (int ox = 0; ox < 3; ++ox) {
-  #pragma unroll
+#pragma unroll
             for (int oy = 0; oy < 3; ++oy) {
               const float wxy = wt[0][ox] * wt[1][oy];
               float M[3];
-  #pragma unroll
+#pragma unroll
               for (int a = 0; a < 3; ++a) M[a] = Q[a] + (float)ox * A[0][a] + (float)oy * A[1][a];
-  #pragma unroll
+#pragma unroll
               for (int oz = 0; oz < 3; ++oz) {
                 const int q = (ox * 3 + oy) * 3 + oz;
                 const float ww = wxy * wt[2][oz];
@@ -495,19 +514,19 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
                 ay[q] = fmaf(ww, M[1], ay[q]);
                 az[q] = fmaf(ww, M[2], az[q]);
                 if (oz < 2) {
-  #pragma unroll
+#pragma unroll
                   for (int a = 0; a < 3; ++a) M[a] += A[2][a];
                 }
               }
             }
           }
         } else {
-  #pragma unroll
+#pragma unroll
           for (int ox = 0; ox < 3; ++ox) {
             float M[2];
-  #pragma unroll
+#pragma unroll
             for (int a = 0; a < 2; ++a) M[a] = Q[a] + (float)ox * A[0][a];
-  #pragma unroll
+#pragma unroll
             for (int oy = 0; oy < 3; ++oy) {
               const int q = ox * 3 + oy;
               const float ww = wt[0][ox] * wt[1][oy];
@@ -557,11 +576,10 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
       }
     }
     cp_async_wait<0>();
-    __syncthreads();
-    // ---- 4. flush: sum the two warp tiles, one vector reduction per non-empty node
-    for (int t = tid; t < G::TN; t += 64) {
-      const float4 a = tiles[t], o = tiles[G::TN + t];
-      const float4 acc = make_float4(a.x + o.x, a.y + o.y, a.z + o.z, a.w + o.w);
+    __syncwarp();
+    // ---- 4. flush: one vector reduction per non-empty node
+    for (int t = lane; t < G::TN; t += 32) {
+      const float4 acc = tile[t];
       if (acc.x != 0.0f) {
         int node[3];
         tile_node<D>(t, org, node);
@@ -575,7 +593,7 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
         if (slot != 0xffffffffu) atomicAdd(&mp[(size_t)slot * 64 + local_node<D>(ln)], acc);
       }
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
@@ -682,7 +700,11 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
   const uint32_t n_active = dc->n_active;
   const float four_inv_dx = 4.0f * S.inv_dx;
 
-  for (uint32_t ab = blockIdx.x * WARPS + warp; ab < n_active; ab += gridDim.x * WARPS) {
+  for (;;) {  // blocks are taken dynamically (a work counter): no tail from uneven blocks
+    uint32_t ab = 0;
+    if (lane == 0) ab = atomicAdd(&dc->next_g2p, 1u);
+    ab = __shfl_sync(FULL, ab, 0);
+    if (ab >= n_active) break;
     const uint32_t b = active_list[ab];
     const uint32_t start = block_start[b], end = block_start[b + 1];
     int bc[3];
@@ -765,12 +787,16 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       float fx[3] = {0.f, 0.f, 0.f}, wt[3][3];
       bool oob_any = false;
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        bool o;
-        lb[a] = base_fx(s[a], S.inv_dx, S.res[a], fx[a], o) - org[a];
-        oob_any |= o;
-        bspline_w(fx[a], wt[a]);
+      for (int a = 0; a < D; ++a) lb[a] = base_fx_fast(s[a], S.inv_dx, S.res[a], fx[a], oob_any) - org[a];
+      if (__any_sync(FULL, oob_any)) {  // rare: the clamped rule of reading Q14
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          bool o;
+          lb[a] = base_fx(s[a], S.inv_dx, S.res[a], fx[a], o) - org[a];
+        }
       }
+#pragma unroll
+      for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
       // gather: v' = sum w v_i;  C' = 4/dx sum w v_i (x) (i - fx) = 4/dx (T - v' fx^T),
       // T[a][k] = sum w v_i,a o_k, reduced axis by axis (z, then y, then x)
       float Sv[3] = {0.f, 0.f, 0.f}, T[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
@@ -892,7 +918,9 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       float xq[3];
 #pragma unroll
       for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
-      const uint32_t nkey = key_of<D>(xq, S);
+      bool koob = false;
+      uint32_t nkey = key_of_fast<D>(xq, S, koob);
+      if (__any_sync(FULL, koob)) nkey = key_of<D>(xq, S);  // rare: clamped base (Q14)
       if (valid) key_out[j] = nkey;
       {  // next step's histograms, one atomic per distinct key of the warp
         const uint32_t nk = valid ? (nkey >> 6) : 0xffffffffu;
@@ -939,7 +967,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
 
 // ------------------------------------------------------------------ entry points
 // per-warp shared-memory bytes of P2G and G2P, read by the host after loading the module
-extern "C" __device__ const unsigned qmpm_smem_per_warp[2] = {(unsigned)qmpm::Smem<Spec>::P2G_WARP,
+extern "C" __device__ const unsigned qmpm_smem_per_warp[2] = {(unsigned)qmpm::P2GLayout<Spec>::BYTES,
                                                              (unsigned)qmpm::Smem<Spec>::G2P_WARP};
 extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t* rec, uint32_t first, uint32_t n,
                                                                  qmpm::SimDev S, uint32_t* key, uint32_t* block_count,
@@ -947,9 +975,9 @@ extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t*
   qmpm::bin_count_body<Spec>(rec, first, n, S, key, block_count, cell_count, do_count);
 }
 
-extern "C" __global__ void __launch_bounds__(64, Spec::P2G_MINB)
+extern "C" __global__ void __launch_bounds__(Spec::P2G_WARPS * 32, Spec::P2G_MINB)
     qmpm_p2g(const uint32_t* rec, const uint32_t* perm, uint32_t* cell_count, const uint32_t* block_start,
-             const uint32_t* active_list, const qmpm::DevCounters* dc, const uint32_t* block_slot, float4* mp,
+             const uint32_t* active_list, qmpm::DevCounters* dc, const uint32_t* block_slot, float4* mp,
              qmpm::SimDev S) {
   qmpm::p2g_body<Spec>(rec, perm, cell_count, block_start, active_list, dc, block_slot, mp, S);
 }

@@ -292,6 +292,24 @@ def test_r24_uniform_chi_square_and_field_independence():
     assert abs(np.corrcoef(r0, r2)[0, 1]) < 0.01
 
 
+def test_r24_fields_jointly_uniform():
+    """Fields of one particle draw from one particle hash (reading Q5): every pair of the
+    first 8 fields is jointly uniform (chi^2 over 32x32 bins of the top bits, 2^16
+    particles) and uncorrelated, and each field alone is uniform."""
+    L = oracle.lib()
+    n = 1 << 16
+    r = np.array([[L.oracle_r24(11, 3, k, f) for f in range(8)] for k in range(n)], dtype=np.int64)
+    e = n / 1024
+    lim = 1023 + 5 * np.sqrt(2 * 1023)
+    for f in range(8):
+        hist = np.bincount(r[:, f] >> 14, minlength=1024)
+        assert float(np.sum((hist - e) ** 2 / e)) < lim, f
+        for g in range(f + 1, 8):
+            joint = np.bincount((r[:, f] >> 19) * 32 + (r[:, g] >> 19), minlength=1024)
+            assert float(np.sum((joint - e) ** 2 / e)) < lim, (f, g)
+            assert abs(np.corrcoef(r[:, f], r[:, g])[0, 1]) < 0.02, (f, g)
+
+
 def test_mix32_is_a_bijection_on_a_sample():
     L = oracle.lib()
     xs = np.arange(0, 1 << 16, dtype=np.uint64) * 65537 + 12345
