@@ -473,7 +473,7 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
           bool oob = false;
 #pragma unroll
           for (int a = 0; a < D; ++a) base_fx_fast(s[a], S.inv_dx, S.res[a], fx[a], oob);
-          if (__any_sync(__activemask(), oob)) {  // rare: the clamped rule of reading Q14
+          if (oob) {  // rare (per lane, no warp vote in this divergent loop): reading Q14's clamp
 #pragma unroll
             for (int a = 0; a < D; ++a) {
               bool o;
