@@ -284,6 +284,19 @@ def c4(seed=0, n_target=400_000_000, res=256, dt=1e-4, z_extent=1.0, E=100.0):
     return Scene("C4", 3, "fluid", sim, [box], seed)
 
 
+def dense_elastic(n_target, res=1024, seed=0):
+    """Capacity probe scene: one elastic block at 8 ppc (spacing dx/2) filling x and z
+    (3 cells from the walls) and as many y layers as n_target needs, at rest."""
+    dx = 1.0 / res
+    spacing = dx / 2
+    lo = 3 * dx
+    nxz = int((1.0 - 2 * lo) / spacing)
+    ny = -(-n_target // (nxz * nxz))
+    box = Box((lo, lo, lo), (nxz, ny, nxz), spacing, (0.0, 0.0, 0.0), n_target)
+    sim = _sim(3, "elastic", (res,) * 3, 7.5e-5, 12.0, spacing ** 3)
+    return Scene("DENSE", 3, "elastic", sim, [box], seed)
+
+
 def small_elastic_3d(seed=0, cube=12, res=64, vmax=1.0):
     """Reduced C2-like scene for fast parity tests (several blocks, ragged tails)."""
     dx = 1.0 / res
