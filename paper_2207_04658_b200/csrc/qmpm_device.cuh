@@ -235,6 +235,7 @@ __device__ __forceinline__ void bspline_w(float fx, float w[3]) {
 __device__ __forceinline__ void polar3(const float F[9], float R[9]) {
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = F[i];
+#pragma unroll 1
   for (int it = 0; it < 12; ++it) {
     // cofactor matrix (= det * R^{-T})
     float c[9];
@@ -250,8 +251,22 @@ __device__ __forceinline__ void polar3(const float F[9], float R[9]) {
     const float det = R[0] * c[0] + R[1] * c[1] + R[2] * c[2];
     const float ad = fabsf(det);
     if (!(ad > 1e-30f)) break;
+#ifdef QMPM_POLAR_SLOW
     const float g = (it < 6) ? rcbrtf(ad) : 1.0f;
     const float a = 0.5f * g, b = 0.5f / (g * det);
+#else
+    // the scaling only speeds convergence (the fixed point R = R^{-T} does not depend on
+    // it), so |det|^{-1/3} = 2^(-log2|det| / 3) from the approximate SFU ops serves; the
+    // 1/(g det) of the update is an IEEE-rounded reciprocal
+    float g = 1.0f;
+    if (it < 6) {
+      float lg, e;
+      asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(ad));
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-0.33333334f * lg));
+      g = e;
+    }
+    const float a = 0.5f * g, b = 0.5f * __frcp_rn(g * det);
+#endif
     float delta = 0.0f;
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
