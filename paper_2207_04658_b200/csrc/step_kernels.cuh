@@ -301,7 +301,7 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 // are independent, so there is no CTA barrier and no tail).  The global counting sort
 // orders particles by (block, base cell) and its cursors leave each cell's start in
 // cell_count, so the block's 64 cell ranges are known without a local sort.
-//   1. segment table: cell c is cut into ceil(n_c / kSegL) segments (at most kSegLev;
+//   1. segment table: cell c is cut into ceil(n_c / L) segments (at most kSegLev;
 //      the last takes the rest), listed level-major (all first segments in cell order,
 //      then all second segments, ...); group g = entries [32 g, 32 g + 32), one segment
 //      per lane: lanes get near-equal work whatever the cells' occupancy (remainders
@@ -318,7 +318,14 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 #ifndef QMPM_SEG_L
 #define QMPM_SEG_L 16
 #endif
-constexpr int kSegL = QMPM_SEG_L;  // particles per P2G segment (one lane, one group)
+#ifndef QMPM_SEG_LMIN
+#define QMPM_SEG_LMIN 8
+#endif
+// particles per P2G segment (one lane, one group): n_blk / 128 clamped to [kSegLmin, kSegL],
+// so sparse blocks (few particles per cell) still give every lane work, while dense
+// blocks keep long segments (fewer per-group flushes)
+constexpr int kSegL = QMPM_SEG_L;
+constexpr int kSegLmin = QMPM_SEG_LMIN < QMPM_SEG_L ? QMPM_SEG_LMIN : QMPM_SEG_L;
 constexpr int kSegLev = 32;        // segments per cell at most (the last one takes the rest)
 
 // per-warp shared-memory layout of P2G (byte offsets; 16-byte aligned parts first)
@@ -377,8 +384,9 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     __syncwarp();
     // ---- 1. segment table (lane handles cells lane and lane + 32)
     const uint32_t nc0 = s_start[lane + 1] - st0, nc1 = s_start[lane + 33] - st1;
-    const uint32_t ns0 = min((nc0 + kSegL - 1) / kSegL, (uint32_t)kSegLev);
-    const uint32_t ns1 = min((nc1 + kSegL - 1) / kSegL, (uint32_t)kSegLev);
+    const uint32_t L = min((uint32_t)kSegL, max((uint32_t)kSegLmin, (end - start + 127) / 128));
+    const uint32_t ns0 = min((nc0 + L - 1) / L, (uint32_t)kSegLev);
+    const uint32_t ns1 = min((nc1 + L - 1) / L, (uint32_t)kSegLev);
     s_ns[lane] = (uint8_t)ns0;
     s_ns[lane + 32] = (uint8_t)ns1;
     const uint32_t nlev = __reduce_max_sync(FULL, max(ns0, ns1));
@@ -411,8 +419,8 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
         const uint32_t v = s_seg[i];
         c = (int)(v >> 8);
         const uint32_t l = v & 255u;
-        k = s_start[c] + l * kSegL;
-        e = (l + 1 == (uint32_t)s_ns[c]) ? s_start[c + 1] : k + kSegL;
+        k = s_start[c] + l * L;
+        e = (l + 1 == (uint32_t)s_ns[c]) ? s_start[c + 1] : k + L;
       } else {
         k = e = 0u;
         c = 0;

@@ -258,7 +258,7 @@ def test_p2g_short_segments(case, monkeypatch):
     turns in the flush) and the level cap (cells with more than kSegLev segments, whose
     last segment takes the rest) meet the same P2 bar: the step kernels are
     re-specialised with a segment length of 2 particles."""
-    monkeypatch.setenv("QMPM_JIT_OPTS", "-DQMPM_SEG_L=2")
+    monkeypatch.setenv("QMPM_JIT_OPTS", "-DQMPM_SEG_L=2 -DQMPM_SEG_LMIN=2")
     mk_scene, mk_scheme, warm = CASES[case]
     sc, sch = mk_scene(), mk_scheme()
     w0, _ = oracle.encode_state(sch, sc.state())
