@@ -633,10 +633,12 @@ __device__ __forceinline__ uint32_t senc_fast(const int i, float v, uint32_t r24
   if (SP::DITHER) {
     const float f = floorf(t);
     const float y = __fsub_rn(t, f);  // exact
-    const float one_minus_r = __fmul_rn(__uint2float_rn(0x1000000u - r24), 0x1p-24f);  // exact
+    // 1 - r24 2^-24 = (2^24 - r24) 2^-24 is representable, so the fma is exact
+    const float one_minus_r = __fmaf_rn(-0x1p-24f, __uint2float_rn(r24), 1.0f);
     up = y >= one_minus_r;  // u = floor(t + r) (Eq. 11, reading Q6)
     nz = y > 0.0f;
-    u = __float2int_rz(f) + (up ? 1 : 0);
+    u = __float2int_rz(f);
+    if (up) ++u;
   } else {
     const float q = rintf(t);  // round half to even (Q6)
     up = q > t;
@@ -888,7 +890,13 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
 #pragma unroll
         for (int i = 0; i < NSV; ++i) dbg[(size_t)j * NSV + i] = o[i];
       }
-      // dithered encode into registers (Eq. 11; reading Q5, Q6)
+      // dithered encode into registers (Eq. 11; reading Q5, Q6).  Idle lanes of a partial
+      // chunk encode their fields' offsets (t = 0: on the grid, counted neither up nor
+      // down), so the round counters need no per-field lane predicate.
+      if (cnt < 32u && !valid) {
+#pragma unroll
+        for (int i = 0; i < NSV; ++i) o[i] = SP::kind(i) == kKindFixed ? SP::offset(i) : 0.0f;
+      }
       uint32_t ow[W + 1];
 #pragma unroll
       for (int q = 0; q <= W; ++q) ow[q] = 0u;
@@ -899,8 +907,8 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         bool up, nz;
         sput<SP>(ow, i, senc_fast<SP>(i, o[i], r24, up, nz, flag));
         if (SP::COUNTERS && SP::kind(i) == kKindFixed) {
-          if (up && valid) rc.pu[i / 4] += 1u << (8 * (i % 4));
-          if (nz && valid) rc.pz[i / 4] += 1u << (8 * (i % 4));
+          if (up) rc.pu[i / 4] += 1u << (8 * (i % 4));
+          if (nz) rc.pz[i / 4] += 1u << (8 * (i % 4));
         }
       }
       if (__any_sync(FULL, valid && flag)) {  // rare: exact re-encode with saturation / non-finite
@@ -928,7 +936,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
       bool koob = false;
       uint32_t nkey = key_of_fast<D>(xq, S, koob);
-      if (__any_sync(FULL, koob)) nkey = key_of<D>(xq, S);  // rare: clamped base (Q14)
+      if (__any_sync(FULL, valid && koob)) nkey = key_of<D>(xq, S);  // rare: clamped base (Q14)
       if (valid) key_out[j] = nkey;
       {  // next step's histograms, one atomic per distinct key of the warp
         const uint32_t nk = valid ? (nkey >> 6) : 0xffffffffu;
