@@ -484,7 +484,9 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
       const char* v = getenv(name);
       return (v && *v) ? atoi(v) : dflt;
     };
-    const int kP2GMinBlocks = env_int("QMPM_P2G_MINB", 6), kG2PMinBlocks = env_int("QMPM_G2P_MINB", 4);
+    // (3D elastic G2P holds F and C: 3 CTAs x 168 registers beat 4 x 128 with spills)
+    const int kP2GMinBlocks = env_int("QMPM_P2G_MINB", 6),
+              kG2PMinBlocks = env_int("QMPM_G2P_MINB", (d == 3 && ctx->material == QMPM_ELASTIC_FCR) ? 3 : 4);
     ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps, kP2GMinBlocks, kG2PMinBlocks);
     JitModule m;
     std::string jerr;
