@@ -65,7 +65,8 @@ enum { QMPM_ELASTIC_FCR = 0, QMPM_FLUID_J = 1 };
 enum {
     QMPM_TRACK_IDS = 1u << 0,       /* keep a u32 particle id alongside each record */
     QMPM_DEBUG_PREENCODE = 1u << 1, /* keep the last step's fp32 state before encode */
-    QMPM_NO_ROUND_COUNTERS = 1u << 2 /* skip the per-field round-up/down counters */
+    QMPM_NO_ROUND_COUNTERS = 1u << 2, /* skip the per-field round-up/down counters */
+    QMPM_RECORD_RANGES = 1u << 3      /* fold max |value| per state scalar into qmpm_read_ranges */
 };
 
 /* One quantized quantity h: one scalar component of one attribute.
@@ -225,6 +226,38 @@ qmpm_status qmpm_connect_nccl(qmpm_ctx* ctx, const uint8_t id[128]);
  * process (ctxs[r] = rank r of n, one shared stream), exchanging with device copies.
  * Synchronizes once per step. */
 qmpm_status qmpm_step_group(qmpm_ctx* const* ctxs, int n, uint32_t n_steps);
+
+/* ---- Scheme derivation (Algorithm 1) ------------
+ * Range recording, Alg. 1 line 9 "Update R_1...R_H according to s_{t+1}":
+ * with params.flags |= QMPM_RECORD_RANGES every step's G2P folds max |value| of each
+ * state scalar of s_{t+1} (the fp32 value before its encode) into a device
+ * accumulator.  qmpm_read_ranges copies it to max_abs (host, [n_scalars], scalar
+ * order of qmpm_set_state) and zeroes it when reset != 0.  Synchronizes.  The paper
+ * records on the full-precision run and multiplies by a factor, e.g. 2.
+ * QMPM_ESTATE without the flag. */
+qmpm_status qmpm_read_ranges(qmpm_ctx* ctx, float* max_abs, int reset);
+
+/* Predicted error, Eq. 8: *sigma_out = sqrt(1/12 sum_h delta[h]^2 g[h]).
+ * H quantities; host arrays; g = the accumulated squared gradients (caller-supplied). */
+qmpm_status qmpm_predict_error(uint32_t H, const double* delta, const double* g, double* sigma_out);
+/* Error-bounded scheme (Eq. 6/9; Algorithm 1 lines 13-15):
+ * delta_out[h] = sqrt(12 P_h (eps_err z)^2 / (g_h sum P)), bits_out[h] = frac bits
+ * ceil(-log2(delta/R_h)) clamped to [b_min, b_max] (0 <= b_min <= b_max <= 31).
+ * P_h > 0 (variables of type h), g_h >= 0 (a type with g_h = 0 gets b_min and
+ * delta = inf), R_h > 0 (ranges), z != 0 the reference metric, eps_err > 0.  Host
+ * arrays, no GPU.  QMPM_EINVAL (message in qmpm_last_error(NULL)) on bad input. */
+qmpm_status qmpm_solve_error_bounded(uint32_t H, const double* P, const double* g, const double* R, double z,
+                                     double eps_err, int32_t b_min, int32_t b_max, double* delta_out,
+                                     int32_t* bits_out);
+/* Memory-bounded scheme (Eq. 7): minimise E[dz] subject to
+ * sum_h P_h bits[h] <= budget_bits (FRACTION bits: the stored width is bits + 1, so a
+ * physical budget eps_mem * M is budget_bits = eps_mem * M - sum_h P_h).  Closed form
+ * of SPEC.md:342 (the paper's is in its supplement): delta_h = c sqrt(P_h/g_h),
+ * bits = floor(-log2(delta/R_h)) clamped; types with g_h = 0 take b_min.  QMPM_EINVAL
+ * when the budget cannot hold b_min everywhere. */
+qmpm_status qmpm_solve_memory_bounded(uint32_t H, const double* P, const double* g, const double* R,
+                                      double budget_bits, int32_t b_min, int32_t b_max, double* delta_out,
+                                      int32_t* bits_out);
 
 const char* qmpm_last_error(const qmpm_ctx* ctx);
 int qmpm_abi_version(void);

@@ -82,6 +82,11 @@ struct qmpm_ctx {
   NcclComm* nccl = nullptr;
 };
 
+namespace qmpm {
+// the thread-local message qmpm_last_error(NULL) returns (used by solver.cu too)
+void set_thread_error(const char* msg) { g_err = msg; }
+}  // namespace qmpm
+
 namespace {
 
 qmpm_status fail(qmpm_ctx* ctx, qmpm_status code, const char* fmt, ...) {
@@ -378,6 +383,7 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   L.ns = (uint32_t)ns;
   L.dither = scheme->rounding == QMPM_DITHER;
   L.counters = (P.flags & QMPM_NO_ROUND_COUNTERS) ? 0u : 1u;
+  L.ranges = (P.flags & QMPM_RECORD_RANGES) ? 1u : 0u;
   L.seed_lo = (uint32_t)(scheme->dither_seed & 0xffffffffu);
   L.seed_hi = (uint32_t)(scheme->dither_seed >> 32);
   L.xword_mask = 0;
@@ -930,6 +936,17 @@ qmpm_status qmpm_read_debug(qmpm_ctx* ctx, float* pre, uint64_t capacity, uint64
   if (capacity < n) return fail(ctx, QMPM_ECAPACITY, "capacity < n");
   if (n) CK(cudaMemcpyAsync(pre, ctx->dbg, sizeof(float) * ctx->ns * n, cudaMemcpyDefault, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  return QMPM_OK;
+}
+
+qmpm_status qmpm_read_ranges(qmpm_ctx* ctx, float* max_abs, int reset) {
+  if (!ctx || !max_abs) return fail(ctx, QMPM_EINVAL, "NULL argument to qmpm_read_ranges");
+  if (!ctx->L.ranges) return fail(ctx, QMPM_ESTATE, "qmpm_read_ranges needs params.flags |= QMPM_RECORD_RANGES");
+  uint32_t bits[kMaxScalars];
+  CK(cudaMemcpyAsync(bits, ctx->dc->range_bits, sizeof(bits), cudaMemcpyDeviceToHost, ctx->stream));
+  if (reset) CK(cudaMemsetAsync(ctx->dc->range_bits, 0, sizeof(bits), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < ctx->ns; ++i) memcpy(&max_abs[i], &bits[i], sizeof(float));
   return QMPM_OK;
 }
 

@@ -42,6 +42,7 @@ struct LayoutDev {
   uint32_t xword_mask;  // record words holding any x bit (particle key, Q5)
   uint32_t dither;      // 1 = Eq. 11 dithering, 0 = RNE
   uint32_t counters;    // 1 = count round-ups/downs
+  uint32_t ranges;      // 1 = record max |value| per state scalar (Alg. 1 line 9)
   uint32_t seed_lo, seed_hi;
   FieldDev s[kMaxScalars];
 };
@@ -88,6 +89,7 @@ struct DevCounters {
   unsigned int n_active;      // last step
   unsigned int n_touched;     // last step (before clamping to the pool)
   unsigned int n_touched_eff; // min(n_touched, pool)
+  unsigned int range_bits[kMaxScalars];  // max |value| per state scalar (float bits, >= 0)
   unsigned int next_p2g;      // dynamic work counters of P2G / G2P (active-list position),
   unsigned int next_g2p;      // reset by the scan every step
   unsigned int pad;

@@ -706,6 +706,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
   uint32_t* wring = reinterpret_cast<uint32_t*>(wbase + SM::TILE + 32);  // [2][32][W] record stage
   RoundCounters<SP> rc;
   rc.init();
+  unsigned rmax = 0u;  // range recording (float bits of max |value|, lane i: scalar i)
   unsigned c_sat = 0, c_nf = 0, c_oob = 0;
   const uint32_t n_active = dc->n_active;
   const float four_inv_dx = 4.0f * S.inv_dx;
@@ -926,6 +927,13 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         }
       }
       if (SP::COUNTERS && ++rc.n_since == 255u) rc.flush(lane);
+      if (SP::RANGES) {  // Alg. 1 line 9: max |value| of s_{t+1} per state scalar (lane i keeps scalar i)
+#pragma unroll
+        for (int i = 0; i < NSV; ++i) {
+          const unsigned m = __reduce_max_sync(FULL, valid ? (__float_as_uint(o[i]) & 0x7fffffffu) : 0u);
+          if (lane == i) rmax = max(rmax, m);
+        }
+      }
       {
         const unsigned bo = __ballot_sync(FULL, valid && oob_any);
         if (lane == 0) c_oob += __popc(bo);
@@ -977,6 +985,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
   }
   if (c_nf) atomicAdd(&dc->nonfinite, (unsigned long long)c_nf);
   if (c_oob) atomicAdd(&dc->oob, (unsigned long long)c_oob);
+  if (SP::RANGES && lane < NSV && rmax) atomicMax(&dc->range_bits[lane], rmax);
 }
 
 }  // namespace qmpm

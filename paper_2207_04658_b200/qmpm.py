@@ -10,6 +10,8 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
+
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "libqmpm.so")
 
@@ -19,7 +21,7 @@ ATTR = {"x": 0, "v": 1, "F": 2, "C": 3, "J": 4}
 KIND = {"fixed": 0, "raw": 1, "shared_exp": 2}
 MATERIAL = {"elastic": 0, "fluid": 1}
 ROUNDING = {"rne": 0, "dither": 1}
-TRACK_IDS, DEBUG_PREENCODE, NO_ROUND_COUNTERS = 1, 2, 4
+TRACK_IDS, DEBUG_PREENCODE, NO_ROUND_COUNTERS, RECORD_RANGES = 1, 2, 4, 8
 STATUS = {0: "OK", 1: "EINVAL", 2: "ELAYOUT", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ENONFINITE",
           7: "EDOMAIN", 8: "ECAPACITY", 9: "ESTATE"}
 
@@ -67,7 +69,8 @@ EXPORTS = ["qmpm_abi_version", "qmpm_last_error", "qmpm_layout", "qmpm_create", 
            "qmpm_set_state", "qmpm_append_state", "qmpm_set_words", "qmpm_step", "qmpm_read_state",
            "qmpm_read_debug", "qmpm_stats", "qmpm_encode", "qmpm_decode", "qmpm_set_profiling",
            "qmpm_kernel_times", "qmpm_kernel_name", "qmpm_launch_count", "qmpm_create_slab",
-           "qmpm_get_unique_id", "qmpm_connect_nccl", "qmpm_step_group", "qmpm_set_ids"]
+           "qmpm_get_unique_id", "qmpm_connect_nccl", "qmpm_step_group", "qmpm_set_ids",
+           "qmpm_read_ranges", "qmpm_predict_error", "qmpm_solve_error_bounded", "qmpm_solve_memory_bounded"]
 
 
 def lib():
@@ -105,6 +108,10 @@ def lib():
         "qmpm_connect_nccl": (i32, [P, P]),
         "qmpm_step_group": (i32, [P, ctypes.c_int, u32]),
         "qmpm_set_ids": (i32, [P, u64, P]),
+        "qmpm_read_ranges": (i32, [P, P, ctypes.c_int]),
+        "qmpm_predict_error": (i32, [u32, P, P, P]),
+        "qmpm_solve_error_bounded": (i32, [u32, P, P, P, ctypes.c_double, ctypes.c_double, i32, i32, P, P]),
+        "qmpm_solve_memory_bounded": (i32, [u32, P, P, P, ctypes.c_double, i32, i32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -200,6 +207,38 @@ def decode(scheme: dict, words, vals, stream=None):
     _check(lib().qmpm_decode(cs.ref, words.shape[0], ptr(words), ptr(vals), stream_handle(stream)))
 
 
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def predict_error(delta, g) -> float:
+    """qmpm_predict_error: sigma_pred = sqrt(1/12 sum delta_h^2 g_h) (Eq. 8)."""
+    d, gg = _f64(delta), _f64(g)
+    out = ctypes.c_double()
+    _check(lib().qmpm_predict_error(len(d), d.ctypes.data, gg.ctypes.data, ctypes.byref(out)))
+    return out.value
+
+
+def solve_error_bounded(P, g, R, z, eps, b_min=0, b_max=31):
+    """qmpm_solve_error_bounded (Eq. 9 + Algorithm 1): returns (delta_h, bits_h)."""
+    P, g, R = _f64(P), _f64(g), _f64(R)
+    d = np.zeros(len(P))
+    b = np.zeros(len(P), np.int32)
+    _check(lib().qmpm_solve_error_bounded(len(P), P.ctypes.data, g.ctypes.data, R.ctypes.data, float(z), float(eps),
+                                          int(b_min), int(b_max), d.ctypes.data, b.ctypes.data))
+    return d, b
+
+
+def solve_memory_bounded(P, g, R, budget_bits, b_min=0, b_max=31):
+    """qmpm_solve_memory_bounded (Eq. 7, closed form of SPEC.md:342): (delta_h, bits_h)."""
+    P, g, R = _f64(P), _f64(g), _f64(R)
+    d = np.zeros(len(P))
+    b = np.zeros(len(P), np.int32)
+    _check(lib().qmpm_solve_memory_bounded(len(P), P.ctypes.data, g.ctypes.data, R.ctypes.data, float(budget_bits),
+                                           int(b_min), int(b_max), d.ctypes.data, b.ctypes.data))
+    return d, b
+
+
 def kernel_names():
     return [lib().qmpm_kernel_name(i).decode() for i in range(NUM_KERNELS)]
 
@@ -289,6 +328,13 @@ class Sim:
         n = ctypes.c_uint64()
         self._c(lib().qmpm_read_debug(self.ctx, ptr(pre), pre.shape[0], ctypes.byref(n)))
         return n.value
+
+    def read_ranges(self, reset=False):
+        """qmpm_read_ranges: max |value| per state scalar since set_state / the last reset
+        (needs flags |= RECORD_RANGES)."""
+        out = np.zeros(self.n_scalars, np.float32)
+        self._c(lib().qmpm_read_ranges(self.ctx, out.ctypes.data, 1 if reset else 0))
+        return out
 
     def stats(self) -> Stats:
         st = Stats()

@@ -58,6 +58,39 @@ def f2():
     return dict(dim=3, material="fluid", rounding="dither", seed=DITHER_SEED, fields=f)
 
 
+def ranges_from_record(max_abs, factor=2.0, pow2=True):
+    """R_h from a recorded full-precision run ("record the ranges from the full
+    precision simulation and multiply the ranges by a factor (e.g., 2)"); rounded up
+    to a power of two so Delta = R 2^-b is exact (reading Q1).  Zero ranges become 1."""
+    import math
+    out = []
+    for m in max_abs:
+        r = factor * float(m)
+        if not r > 0.0:
+            r = 1.0
+        if pow2:
+            r = 2.0 ** math.ceil(math.log2(r))
+        out.append(r)
+    return out
+
+
+def scalar_names(dim, material):
+    """(attr, comp) of each state scalar, in the order of qmpm_set_state."""
+    d = dim
+    names = [("x", c) for c in range(d)] + [("v", c) for c in range(d)]
+    names += [("J", 0)] if material == "fluid" else [("F", c) for c in range(d * d)]
+    names += [("C", c) for c in range(d * d)]
+    return names
+
+
+def from_solution(dim, material, ranges, bits, rounding="dither"):
+    """A scheme with every state scalar FIXED, in state-scalar order, from per-scalar
+    ranges R_h and fraction bits b_h (Algorithm 1's output (b_h, R_h))."""
+    f = [dict(attr=a, comp=c, kind="fixed", frac_bits=int(b), range=float(r), offset=0.0)
+         for (a, c), r, b in zip(scalar_names(dim, material), ranges, bits)]
+    return dict(dim=dim, material=material, rounding=rounding, seed=DITHER_SEED, fields=f)
+
+
 def with_rounding(scheme, rounding):
     s = dict(scheme)
     s["rounding"] = rounding
