@@ -186,6 +186,14 @@ qmpm_status qmpm_encode(const qmpm_scheme* scheme, uint64_t n, const float* vals
                         uint64_t* counters, void* cuda_stream);
 qmpm_status qmpm_decode(const qmpm_scheme* scheme, uint64_t n, const uint32_t* words, float* vals,
                         void* cuda_stream);
+/* The paper's "MatMul" codec task: each record holds a 3x3 matrix M (the
+ * scheme's 9 fields, row-major M[r][c] = field 3r+c); it is decoded, multiplied by the
+ * constant a (host, 9 floats, row-major) as out[r][c] = (M[r][0] a[c] + M[r][1] a[3+c])
+ * + M[r][2] a[6+c] in fp32 (no FMA) and re-encoded into words_out (dithered with
+ * keys[i] when keys != NULL and the scheme dithers, else RNE).  Device arrays
+ * [n][W]; words_in and words_out must not overlap.  QMPM_ELAYOUT unless 9 fields. */
+qmpm_status qmpm_codec_matmul3(const qmpm_scheme* scheme, uint64_t n, const uint32_t* words_in, const float* a,
+                               const uint32_t* keys, uint64_t step, uint32_t* words_out, void* cuda_stream);
 
 /* Per-kernel timing for the roofline: when enabled, qmpm_step brackets each
  * kernel with CUDA events on the ctx stream.  qmpm_kernel_times (synchronizes)

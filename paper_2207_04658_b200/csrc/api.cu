@@ -5,6 +5,7 @@
 // of the sorted order), the block table of the counting sort, the grid-block pool
 // and the device counters.  Everything is enqueued on the ctx stream; qmpm_step
 // allocates nothing.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdarg>
@@ -254,6 +255,52 @@ qmpm_status reset_counters(qmpm_ctx* ctx) {
   return QMPM_OK;
 }
 
+// The standalone codec through its NVRTC-specialised kernels (codec_kernels.cuh).
+// op 0: vals -> words (keys: nullable => RNE), op 1: words -> vals, op 2: matmul3.
+qmpm_status codec_run(qmpm_ctx* ctx, const CodecDev& C, int op, uint64_t n, const float* vals_in, float* vals_out,
+                      const uint32_t* keys, uint32_t salt, const uint32_t* words_in, uint32_t* words_out,
+                      unsigned long long* counters, const float* mat, cudaStream_t st) {
+  if (n == 0) return QMPM_OK;
+  auto vec = [](uint32_t count, const void* p) {
+    const uintptr_t a = (uintptr_t)p;
+    if (count % 4 == 0 && a % 16 == 0) return 4;
+    if (count % 2 == 0 && a % 8 == 0) return 2;
+    return 1;
+  };
+  const void* wp = op == 0 ? (const void*)words_out : (const void*)words_in;
+  int wv = vec(C.W, wp);
+  if (op == 2) wv = std::min(wv, vec(C.W, words_out));
+  const void* vp = op == 0 ? (const void*)vals_in : (const void*)vals_out;
+  const int vv = op == 2 ? 1 : vec(C.stride, vp);
+  const bool dither = C.dither && keys != nullptr && op != 1;
+  const bool counters_on = counters != nullptr && op == 0;
+  CodecJit J;
+  std::string err;
+  cudaError_t e = jit_codec(codec_spec_source(C, dither, counters_on, wv, vv), J, err);
+  if (e) return fail(ctx, QMPM_ECUDA, "codec specialisation failed: %s", err.c_str());
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t want = (n + 255) / 256;
+  const unsigned grid = (unsigned)std::min<uint64_t>(want, (uint64_t)sms * 8);
+  if (op == 0) {
+    void* args[] = {(void*)&vals_in, (void*)&keys, (void*)&n, (void*)&salt, (void*)&words_out, (void*)&counters};
+    e = jit_launch(J.encode, grid, 256, 0, st, args);
+  } else if (op == 1) {
+    void* args[] = {(void*)&words_in, (void*)&n, (void*)&vals_out};
+    e = jit_launch(J.decode, grid, 256, 0, st, args);
+  } else {
+    struct {
+      float a[9];
+    } A;
+    for (int i = 0; i < 9; ++i) A.a[i] = mat[i];
+    void* args[] = {(void*)&words_in, (void*)&n, (void*)&A, (void*)&keys, (void*)&salt, (void*)&words_out};
+    e = jit_launch(J.matmul3, grid, 256, 0, st, args);
+  }
+  if (e) return fail(ctx, QMPM_ECUDA, "codec kernel launch failed");
+  return QMPM_OK;
+}
+
 // encode n scalar-order rows (host or device) into records [first, first+n) at step 0
 qmpm_status encode_rows(qmpm_ctx* ctx, uint64_t first, uint64_t n, const float* vals) {
   if (n == 0) return QMPM_OK;
@@ -265,8 +312,9 @@ qmpm_status encode_rows(qmpm_ctx* ctx, uint64_t first, uint64_t n, const float* 
     dv = tmp;
   }
   ctx->launches_total += 1;
-  CK(launch_encode(ctx->C, n, dv, nullptr, 0u, ctx->rec[ctx->cur] + first * ctx->W,
-                   (unsigned long long*)ctx->dc, ctx->stream));
+  qmpm_status rc = codec_run(ctx, ctx->C, 0, n, dv, nullptr, nullptr, 0u, nullptr, ctx->rec[ctx->cur] + first * ctx->W,
+                             (unsigned long long*)ctx->dc, nullptr, ctx->stream);
+  if (rc) return rc;
   if (ctx->ids[ctx->cur]) {
     ctx->launches_total += 1;
     CK(launch_iota(ctx->ids[ctx->cur] + first, (uint32_t)n, (uint32_t)first, ctx->stream));
@@ -911,7 +959,9 @@ qmpm_status qmpm_read_state(qmpm_ctx* ctx, float* vals, uint32_t* words, uint32_
       dv = tmp;
     }
     ctx->launches_total += 1;
-    CK(launch_decode(ctx->C, n, ctx->rec[ctx->cur], dv, ctx->stream));
+    qmpm_status rc = codec_run(ctx, ctx->C, 1, n, nullptr, dv, nullptr, 0u, ctx->rec[ctx->cur], nullptr, nullptr,
+                               nullptr, ctx->stream);
+    if (rc) return rc;
     if (tmp) {
       CK(cudaMemcpyAsync(vals, tmp, sizeof(float) * ctx->ns * n, cudaMemcpyDefault, ctx->stream));
       CK(cudaFreeAsync(tmp, ctx->stream));
@@ -979,8 +1029,21 @@ qmpm_status qmpm_encode(const qmpm_scheme* scheme, uint64_t n, const float* vals
   if (rc) return rc;
   if (n && (!vals || !words)) return fail(ctx, QMPM_EINVAL, "NULL vals/words");
   const uint32_t salt = step_salt(C.seed_lo, C.seed_hi, (uint32_t)step);
-  CK(launch_encode(C, n, vals, keys, salt, words, (unsigned long long*)counters, (cudaStream_t)cuda_stream));
-  return QMPM_OK;
+  return codec_run(ctx, C, 0, n, vals, nullptr, keys, salt, nullptr, words, (unsigned long long*)counters, nullptr,
+                   (cudaStream_t)cuda_stream);
+}
+
+qmpm_status qmpm_codec_matmul3(const qmpm_scheme* scheme, uint64_t n, const uint32_t* words_in, const float* a,
+                               const uint32_t* keys, uint64_t step, uint32_t* words_out, void* cuda_stream) {
+  qmpm_ctx* ctx = nullptr;
+  CodecDev C;
+  qmpm_status rc = codec_of(ctx, scheme, C);
+  if (rc) return rc;
+  if (C.nf != 9) return fail(ctx, QMPM_ELAYOUT, "qmpm_codec_matmul3 needs a scheme of 9 fields (got %u)", C.nf);
+  if (n && (!words_in || !words_out || !a)) return fail(ctx, QMPM_EINVAL, "NULL words/matrix");
+  const uint32_t salt = step_salt(C.seed_lo, C.seed_hi, (uint32_t)step);
+  return codec_run(ctx, C, 2, n, nullptr, nullptr, keys, salt, words_in, words_out, nullptr, a,
+                   (cudaStream_t)cuda_stream);
 }
 
 qmpm_status qmpm_decode(const qmpm_scheme* scheme, uint64_t n, const uint32_t* words, float* vals, void* cuda_stream) {
@@ -989,8 +1052,8 @@ qmpm_status qmpm_decode(const qmpm_scheme* scheme, uint64_t n, const uint32_t* w
   qmpm_status rc = codec_of(ctx, scheme, C);
   if (rc) return rc;
   if (n && (!vals || !words)) return fail(ctx, QMPM_EINVAL, "NULL vals/words");
-  CK(launch_decode(C, n, words, vals, (cudaStream_t)cuda_stream));
-  return QMPM_OK;
+  return codec_run(ctx, C, 1, n, nullptr, vals, nullptr, 0u, words, nullptr, nullptr, nullptr,
+                   (cudaStream_t)cuda_stream);
 }
 
 qmpm_status qmpm_set_profiling(qmpm_ctx* ctx, int enabled) {

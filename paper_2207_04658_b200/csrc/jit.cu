@@ -23,7 +23,7 @@
 
 namespace qmpm {
 
-#include "jit_sources.inc"  // kSrcDevice, kSrcCommon, kSrcStep (generated by build.py)
+#include "jit_sources.inc"  // kSrcDevice, kSrcCommon, kSrcField, kSrcStep, kSrcCodec (build.py)
 
 namespace {
 
@@ -54,7 +54,6 @@ struct Nvrtc {
 std::mutex g_mu;
 Driver g_drv;
 Nvrtc g_rtc;
-std::map<std::string, JitModule> g_cache;
 
 template <class T>
 bool entry(const char* name, T& fn) {
@@ -153,33 +152,39 @@ std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps
   return s;
 }
 
-cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err) {
-  std::lock_guard<std::mutex> lk(g_mu);
+namespace {
+std::map<std::string, CUmodule> g_modules;
+
+// Compile `src` (which #includes the embedded headers) for sm_100a with NVRTC and load
+// it; modules are cached per process by (device, QMPM_JIT_OPTS, source).  g_mu held.
+cudaError_t compile_module(const std::string& src, const char* prog_name, CUmodule& mod, std::string& log,
+                           std::string& err) {
   int dev = 0;
   cudaGetDevice(&dev);
   const char* jopts = getenv("QMPM_JIT_OPTS");
   const std::string key = std::to_string(dev) + "\n" + (jopts ? jopts : "") + "\n" + src;
-  auto it = g_cache.find(key);
-  if (it != g_cache.end()) {
-    out = it->second;
+  auto it = g_modules.find(key);
+  if (it != g_modules.end()) {
+    mod = it->second;
     return cudaSuccess;
   }
   if (!init_driver(err) || !init_nvrtc(err)) return cudaErrorNotSupported;
   cudaFree(nullptr);  // make sure the primary context is current
   nvrtcProgram prog;
-  const char* hdrs[] = {kSrcDevice, kSrcCommon, kSrcStep};
-  const char* names[] = {"qmpm_device.cuh", "mpm_common.cuh", "step_kernels.cuh"};
-  nvrtcResult r = g_rtc.create(&prog, src.c_str(), "qmpm_step_spec.cu", 3, hdrs, names);
+  const char* hdrs[] = {kSrcDevice, kSrcCommon, kSrcField, kSrcStep, kSrcCodec};
+  const char* names[] = {"qmpm_device.cuh", "mpm_common.cuh", "field_codec.cuh", "step_kernels.cuh",
+                         "codec_kernels.cuh"};
+  nvrtcResult r = g_rtc.create(&prog, src.c_str(), prog_name, 5, hdrs, names);
   if (r != NVRTC_SUCCESS) {
     err = std::string("nvrtcCreateProgram: ") + g_rtc.errstr(r);
     return cudaErrorInvalidSource;
   }
   std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true",
                                    "-DQMPM_JIT=1"};
-  // QMPM_JIT_OPTS: extra space-separated NVRTC options (tuning runs only, e.g. -DQMPM_CELL_CAP=512)
+  // QMPM_JIT_OPTS: extra space-separated NVRTC options (tuning runs only, e.g. -DQMPM_SEG_L=24)
   std::vector<std::string> extra;
-  if (const char* env = getenv("QMPM_JIT_OPTS")) {
-    std::string e(env), tok;
+  if (jopts) {
+    std::string e(jopts), tok;
     for (char ch : e + " ") {
       if (ch == ' ') {
         if (!tok.empty()) extra.push_back(tok);
@@ -193,7 +198,7 @@ cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err) {
   r = g_rtc.compile(prog, (int)opts.size(), opts.data());
   size_t ls = 0;
   g_rtc.logSize(prog, &ls);
-  std::string log(ls, '\0');
+  log.assign(ls, '\0');
   if (ls) g_rtc.log(prog, &log[0]);
   if (r != NVRTC_SUCCESS) {
     err = std::string("NVRTC compile failed: ") + g_rtc.errstr(r) + "\n" + log;
@@ -205,13 +210,23 @@ cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err) {
   std::vector<char> cubin(n);
   g_rtc.cubin(prog, cubin.data());
   g_rtc.destroy(&prog);
-  JitModule m{};
-  CUmodule mod;
   CUresult cr = g_drv.moduleLoadData(&mod, cubin.data());
   if (cr != CUDA_SUCCESS) {
     err = "cuModuleLoadData failed (" + std::to_string((int)cr) + ")";
     return cudaErrorInvalidKernelImage;
   }
+  g_modules[key] = mod;
+  return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  JitModule m{};
+  std::string log;
+  CUmodule mod;
+  cudaError_t e = compile_module(src, "qmpm_step_spec.cu", mod, log, err);
+  if (e) return e;
   m.module = mod;
   if (g_drv.moduleGetFunction(&m.bin_count, mod, "qmpm_bin_count") != CUDA_SUCCESS ||
       g_drv.moduleGetFunction(&m.p2g, mod, "qmpm_p2g") != CUDA_SUCCESS ||
@@ -239,8 +254,62 @@ cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err) {
   m.regs_p2g = regs(m.p2g);
   m.regs_g2p = regs(m.g2p);
   m.log = log;
-  g_cache[key] = m;
   out = m;
+  return cudaSuccess;
+}
+
+std::string codec_spec_source(const CodecDev& C, bool dither, bool counters, int wv, int vv) {
+  std::string s;
+  char buf[512];
+  const int nf = (int)C.nf;
+  snprintf(buf, sizeof(buf),
+           "struct Spec {\n  static constexpr int NF = %d, W = %u, STRIDE = %u, WV = %d, VV = %d;\n"
+           "  static constexpr bool DITHER = %s, COUNTERS = %s;\n",
+           nf, C.W, C.stride, wv, vv, dither ? "true" : "false", counters ? "true" : "false");
+  s += buf;
+  auto ints = [&](const char* name, auto get) {
+    s += "  __host__ __device__ static constexpr int ";
+    s += name;
+    s += "(int i) {\n    constexpr int a[" + std::to_string(nf) + "] = {";
+    for (int i = 0; i < nf; ++i) s += std::to_string(get(C.f[i])) + (i + 1 < nf ? ", " : "");
+    s += "};\n    return a[i];\n  }\n";
+  };
+  auto floats = [&](const char* name, auto get) {
+    s += "  __host__ __device__ static constexpr float ";
+    s += name;
+    s += "(int i) {\n    constexpr float a[" + std::to_string(nf) + "] = {";
+    for (int i = 0; i < nf; ++i) {
+      snprintf(buf, sizeof(buf), "%af", (double)get(C.f[i]));
+      s += buf;
+      s += (i + 1 < nf ? ", " : "");
+    }
+    s += "};\n    return a[i];\n  }\n";
+  };
+  ints("word", [](const FieldDev& f) { return (int)f.word; });
+  ints("shift", [](const FieldDev& f) { return (int)f.shift; });
+  ints("width", [](const FieldDev& f) { return (int)f.width; });
+  ints("kind", [](const FieldDev& f) { return (int)f.kind; });
+  ints("idx", [](const FieldDev& f) { return (int)f.idx; });
+  ints("col", [](const FieldDev& f) { return (int)f.col; });
+  floats("delta", [](const FieldDev& f) { return f.delta; });
+  floats("inv_delta", [](const FieldDev& f) { return f.inv_delta; });
+  floats("offset", [](const FieldDev& f) { return f.offset; });
+  s += "};\n#include \"codec_kernels.cuh\"\n";
+  return s;
+}
+
+cudaError_t jit_codec(const std::string& src, CodecJit& out, std::string& err) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  std::string log;
+  CUmodule mod;
+  cudaError_t e = compile_module(src, "qmpm_codec_spec.cu", mod, log, err);
+  if (e) return e;
+  if (g_drv.moduleGetFunction(&out.encode, mod, "qmpm_codec_encode") != CUDA_SUCCESS ||
+      g_drv.moduleGetFunction(&out.decode, mod, "qmpm_codec_decode") != CUDA_SUCCESS ||
+      g_drv.moduleGetFunction(&out.matmul3, mod, "qmpm_codec_matmul3") != CUDA_SUCCESS) {
+    err = "codec JIT module lacks a kernel";
+    return cudaErrorSymbolNotFound;
+  }
   return cudaSuccess;
 }
 

@@ -21,6 +21,14 @@ struct JitModule {
 std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps, int g2p_warps, int p2g_minb,
                         int g2p_minb);
 cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err);
+
+// the standalone codec specialised on one layout (codec_kernels.cuh)
+struct CodecJit {
+  CUfunction encode, decode, matmul3;
+};
+// wv / vv: vector widths (4, 2, 1) usable for the records / the vals rows
+std::string codec_spec_source(const CodecDev& C, bool dither, bool counters, int wv, int vv);
+cudaError_t jit_codec(const std::string& src, CodecJit& out, std::string& err);
 cudaError_t jit_set_smem(CUfunction f, size_t bytes);
 int jit_occupancy(CUfunction f, int threads, size_t smem);
 cudaError_t jit_launch(CUfunction f, unsigned grid, unsigned block, size_t smem, cudaStream_t st, void** args);

@@ -7,8 +7,7 @@
 //   k_cell_scan    a1  per active block: cell counts -> cell cursors (end positions)
 //   k_bin_scatter  a1  counting-sort scatter by (block, cell): perm[sorted slot] = record index
 //   k_grid_update  a4  v = p/m + dt g, separating walls; clears (m, p) for next step
-//   k_encode/k_decode  Eq. 3 / Eq. 11 + bit pack for set_state, read_state and the
-//                      standalone qmpm_encode / qmpm_decode
+// (the standalone codec is NVRTC-specialised too: codec_kernels.cuh)
 #include <cuda_runtime.h>
 
 #include "jit.h"
@@ -380,73 +379,6 @@ __global__ void k_plane_unpack(float4* __restrict__ dst, const uint32_t* __restr
   }
 }
 
-// ============================================================== standalone codec
-constexpr int kCodecThreads = 128;
-
-__global__ void __launch_bounds__(kCodecThreads) k_encode(const float* __restrict__ vals,
-                                                          const uint32_t* __restrict__ keys, uint64_t n,
-                                                          CodecDev C, uint32_t salt,
-                                                          uint32_t* __restrict__ words,
-                                                          unsigned long long* __restrict__ counters) {
-  extern __shared__ uint32_t sm[];
-  float* vst = reinterpret_cast<float*>(sm);         // [128][stride]
-  uint32_t* wst = sm + kCodecThreads * C.stride;     // [128][SW]
-  __shared__ unsigned s_cnt[3][kMaxFields];
-  for (int i = threadIdx.x; i < 3 * kMaxFields; i += blockDim.x) (&s_cnt[0][0])[i] = 0u;
-  const uint64_t row0 = (uint64_t)blockIdx.x * kCodecThreads;
-  const uint32_t cnt = (uint32_t)min((uint64_t)kCodecThreads, n - row0);
-  for (uint32_t q = threadIdx.x; q < cnt * C.stride; q += blockDim.x) vst[q] = vals[row0 * C.stride + q];
-  __syncthreads();
-  const uint32_t tid = threadIdx.x;
-  if (tid < cnt) {
-    uint32_t* row = wst + tid * C.SW;
-    for (uint32_t q = 0; q <= C.W; ++q) row[q] = 0u;
-    const bool dither = keys != nullptr && C.dither;
-    const uint32_t h = dither ? mix32(keys[row0 + tid] ^ salt) : 0u;
-    for (uint32_t fi = 0; fi < C.nf; ++fi) {
-      const FieldDev& f = C.f[fi];
-      EncStat st;
-      const uint32_t r24 = (dither && f.kind == kKindFixed) ? r24_of(h, fi) : 0u;
-      const uint32_t bits = encode_field(vst[tid * C.stride + f.col], f, dither, r24, st);
-      put_field(row, f, bits);
-      if (counters) {
-        if (st.sat) atomicAdd(&s_cnt[0][fi], 1u);
-        if (st.up) atomicAdd(&s_cnt[1][fi], 1u);
-        if (st.down) atomicAdd(&s_cnt[2][fi], 1u);
-      }
-    }
-  }
-  __syncthreads();
-  for (uint32_t q = threadIdx.x; q < cnt * C.W; q += blockDim.x)
-    words[row0 * C.W + q] = wst[(q / C.W) * C.SW + q % C.W];
-  if (counters) {
-    for (uint32_t i = threadIdx.x; i < 3 * C.nf; i += blockDim.x) {
-      const uint32_t k = i / C.nf, fi = i % C.nf;
-      if (s_cnt[k][fi]) atomicAdd(&counters[k * kMaxFields + fi], (unsigned long long)s_cnt[k][fi]);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kCodecThreads) k_decode(const uint32_t* __restrict__ words, uint64_t n,
-                                                          CodecDev C, float* __restrict__ vals) {
-  extern __shared__ uint32_t sm[];
-  float* vst = reinterpret_cast<float*>(sm);
-  uint32_t* wst = sm + kCodecThreads * C.stride;
-  const uint64_t row0 = (uint64_t)blockIdx.x * kCodecThreads;
-  const uint32_t cnt = (uint32_t)min((uint64_t)kCodecThreads, n - row0);
-  for (uint32_t q = threadIdx.x; q < cnt * C.W; q += blockDim.x)
-    wst[(q / C.W) * C.SW + q % C.W] = words[row0 * C.W + q];
-  __syncthreads();
-  const uint32_t tid = threadIdx.x;
-  if (tid < cnt) {
-    uint32_t* row = wst + tid * C.SW;
-    row[C.W] = 0u;
-    for (uint32_t fi = 0; fi < C.nf; ++fi) vst[tid * C.stride + C.f[fi].col] = decode_field(row, C.f[fi]);
-  }
-  __syncthreads();
-  for (uint32_t q = threadIdx.x; q < cnt * C.stride; q += blockDim.x) vals[row0 * C.stride + q] = vst[q];
-}
-
 __global__ void k_iota(uint32_t* ids, uint32_t n, uint32_t first) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) ids[i] = first + i;
@@ -571,31 +503,6 @@ cudaError_t launch_plane(float4* nodes, const uint32_t* block_slot, const SimDev
     k_plane_pack<<<num_sms * 4, 256, 0, st>>>(nodes, block_slot, S, bz, buf);
   else
     k_plane_unpack<<<num_sms * 4, 256, 0, st>>>(nodes, block_slot, S, bz, buf, mode == 1);
-  return cudaGetLastError();
-}
-
-static size_t codec_smem(const CodecDev& C) {
-  return sizeof(uint32_t) * kCodecThreads * (C.stride + C.SW);
-}
-
-cudaError_t launch_encode(const CodecDev& C, uint64_t n, const float* vals, const uint32_t* keys, uint32_t salt,
-                          uint32_t* words, unsigned long long* counters, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  const size_t sm = codec_smem(C);
-  cudaError_t e = cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e) return e;
-  const uint64_t blocks = (n + kCodecThreads - 1) / kCodecThreads;
-  k_encode<<<(unsigned)blocks, kCodecThreads, sm, st>>>(vals, keys, n, C, salt, words, counters);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_decode(const CodecDev& C, uint64_t n, const uint32_t* words, float* vals, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  const size_t sm = codec_smem(C);
-  cudaError_t e = cudaFuncSetAttribute(k_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e) return e;
-  const uint64_t blocks = (n + kCodecThreads - 1) / kCodecThreads;
-  k_decode<<<(unsigned)blocks, kCodecThreads, sm, st>>>(words, n, C, vals);
   return cudaGetLastError();
 }
 

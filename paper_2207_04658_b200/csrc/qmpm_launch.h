@@ -85,11 +85,6 @@ cudaError_t launch_recount(const StepBuffers& B, const SimDev& S, uint32_t n, in
 cudaError_t launch_plane(float4* nodes, const uint32_t* block_slot, const SimDev& S, int bz, float4* buf, int mode,
                          int num_sms, cudaStream_t st);
 
-cudaError_t launch_encode(const CodecDev& C, uint64_t n, const float* vals, const uint32_t* keys,
-                          uint32_t salt, uint32_t* words, unsigned long long* counters,
-                          cudaStream_t st);
-cudaError_t launch_decode(const CodecDev& C, uint64_t n, const uint32_t* words, float* vals,
-                          cudaStream_t st);
 cudaError_t launch_iota(uint32_t* ids, uint32_t n, uint32_t first, cudaStream_t st);
 
 }  // namespace qmpm

@@ -14,164 +14,10 @@
 //   qmpm_g2p        a2+a5-a7  gather from a shared-memory tile, update, dithered encode,
 //                             coalesced store in sorted order, next step's block key
 #pragma once
+#include "field_codec.cuh"
 #include "mpm_common.cuh"
 
 namespace qmpm {
-
-// ------------------------------------------------------------------ field access
-// value of state scalar i from a register-resident record w[0..W] (w[W] = 0)
-template <class SP>
-__device__ __forceinline__ float sdec(const uint32_t* w, const int i) {
-  const int wd = SP::word(i), sh = SP::shift(i), wi = SP::width(i);
-  const uint32_t raw = (sh + wi <= 32) ? (w[wd] >> sh) : __funnelshift_r(w[wd], w[wd + 1], sh);
-  if (SP::kind(i) == kKindRaw) return __uint_as_float(raw);
-  const int u = ((int)(raw << (32 - wi))) >> (32 - wi);  // sign-extend b+1 bits (Q2)
-  float x = __fmul_rn(__int2float_rn(u), SP::delta(i));   // Eq. 3: u * Delta
-  if (SP::offset(i) != 0.0f) x = __fadd_rn(x, SP::offset(i));
-  return x;
-}
-
-struct EncFlags {
-  bool up, down, sat, nonfinite;
-};
-
-// Eq. 3 / Eq. 11 encode of state scalar i; returns the field's bits (width-masked).
-template <class SP>
-__device__ __forceinline__ uint32_t senc(const int i, float v, uint32_t r24, EncFlags& fl) {
-  fl.up = fl.down = fl.sat = fl.nonfinite = false;
-  if (SP::kind(i) == kKindRaw) {
-    fl.nonfinite = !isfinite(v);
-    return __float_as_uint(v);
-  }
-  const int wi = SP::width(i);
-  if (!isfinite(v)) {
-    fl.nonfinite = true;
-    return 0u;
-  }
-  const float a = (SP::offset(i) != 0.0f) ? __fsub_rn(v, SP::offset(i)) : v;
-  const float t = __fmul_rn(a, SP::inv_delta(i));  // one fp32 multiply, no FMA (Q3)
-  const uint32_t mask = (wi == 32) ? 0xffffffffu : ((1u << wi) - 1u);
-  if (wi <= 25) {
-    // |codes| <= 2^24: clamping f to [-2^b - 2, 2^b] (exact floats) keeps every
-    // saturation decision of the exact integer rule
-    const float lo_f = -(float)(1 << (wi - 1)) - 2.0f, hi_f = (float)(1 << (wi - 1));
-    const int lo = -(1 << (wi - 1)), hi = (1 << (wi - 1)) - 1;
-    int u;
-    if (SP::DITHER) {
-      const float f = floorf(t);
-      const float y = __fsub_rn(t, f);  // exact
-      const float one_minus_r = __fmul_rn(__uint2float_rn(0x1000000u - r24), 0x1p-24f);  // exact
-      fl.up = y >= one_minus_r;         // u = floor(t + r) (Eq. 11, reading Q6)
-      fl.down = !fl.up && y > 0.0f;
-      u = __float2int_rz(fminf(fmaxf(f, lo_f), hi_f)) + (fl.up ? 1 : 0);
-    } else {
-      const float q = rintf(t);  // round half to even (Q6)
-      fl.up = q > t;
-      fl.down = q < t;
-      u = __float2int_rz(fminf(fmaxf(q, lo_f), hi_f));
-    }
-    if (u > hi) { u = hi; fl.sat = true; }
-    if (u < lo) { u = lo; fl.sat = true; }
-    return (uint32_t)u & mask;
-  } else {
-    long long u;
-    if (SP::DITHER) {
-      const float f = floorf(t);
-      const float y = __fsub_rn(t, f);
-      const float one_minus_r = __fmul_rn(__uint2float_rn(0x1000000u - r24), 0x1p-24f);
-      fl.up = y >= one_minus_r;
-      fl.down = !fl.up && y > 0.0f;
-      u = __float2ll_rz(fminf(fmaxf(f, -1099511627776.0f), 1099511627776.0f)) + (fl.up ? 1 : 0);
-    } else {
-      const float q = rintf(t);
-      fl.up = q > t;
-      fl.down = q < t;
-      u = __float2ll_rz(fminf(fmaxf(q, -1099511627776.0f), 1099511627776.0f));
-    }
-    const long long hi = (1ll << (wi - 1)) - 1, lo = -(1ll << (wi - 1));
-    if (u > hi) { u = hi; fl.sat = true; }
-    if (u < lo) { u = lo; fl.sat = true; }
-    return (uint32_t)u & mask;
-  }
-}
-
-template <class SP>
-__device__ __forceinline__ void sput(uint32_t* w, const int i, uint32_t bits) {
-  const int wd = SP::word(i), sh = SP::shift(i), wi = SP::width(i);
-  w[wd] |= bits << sh;
-  if (sh + wi > 32) w[wd + 1] |= bits >> (32 - sh);
-}
-
-// content key of a record (reading Q5): k = mix(k ^ word) over the words holding x
-template <class SP>
-__device__ __forceinline__ uint32_t content_key(const uint32_t* w) {
-  uint32_t k = 0;
-#pragma unroll
-  for (int q = 0; q < SP::W; ++q)
-    if ((SP::XMASK >> q) & 1u) k = mix32(k ^ w[q]);
-  return k;
-}
-
-// ------------------------------------------------------------------ staging
-// Warp-cooperative load of the warp's cnt records (record index of lane l in r_lane)
-// into registers w[0..W] of their owner lane.  The words go global -> shared with
-// cp.async (LDGSTS: no registers held while the W loads are in flight), then each
-// lane reads its own conflict-free (odd-stride) row.  issue_records / take_records
-// split the two halves so the next chunk's records can be in flight while the
-// current chunk computes (double-buffered stage).
-template <class SP>
-__device__ __forceinline__ void issue_records(const uint32_t* __restrict__ rec, uint32_t r_lane, uint32_t cnt,
-                                              uint32_t* wst, int lane) {
-  constexpr int W = SP::W, SW = SP::SW;
-  const unsigned sbase = (unsigned)__cvta_generic_to_shared(wst);
-#pragma unroll
-  for (int k = 0; k < W; ++k) {
-    const uint32_t q = (uint32_t)(k * 32 + lane);
-    const uint32_t l = q / W, o = q - l * W;
-    const uint32_t r = __shfl_sync(FULL, r_lane, (int)(l & 31u));
-    if (l < cnt) {
-      const unsigned sa = sbase + 4u * (l * SW + o);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(rec + (size_t)r * W + o) : "memory");
-    }
-  }
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-
-template <class SP>
-__device__ __forceinline__ void take_records(const uint32_t* wst, int lane, uint32_t* w) {
-  constexpr int W = SP::W, SW = SP::SW;
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < W; ++k) w[k] = wst[lane * SW + k];
-  w[W] = 0u;
-  __syncwarp();
-}
-
-template <class SP>
-__device__ __forceinline__ void load_records(const uint32_t* __restrict__ rec, uint32_t r_lane, uint32_t cnt,
-                                             uint32_t* wst, int lane, uint32_t* w) {
-  issue_records<SP>(rec, r_lane, cnt, wst, lane);
-  take_records<SP>(wst, lane, w);
-}
-
-// coalesced store of the warp's cnt records (lane l holds record l in w) to out[0..cnt*W)
-template <class SP>
-__device__ __forceinline__ void store_records(uint32_t* __restrict__ out, uint32_t cnt, uint32_t* wst, int lane,
-                                              const uint32_t* w) {
-  constexpr int W = SP::W, SW = SP::SW;
-#pragma unroll
-  for (int k = 0; k < W; ++k) wst[lane * SW + k] = w[k];
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < W; ++k) {
-    const uint32_t q = (uint32_t)(k * 32 + lane);
-    const uint32_t l = q / W, o = q - l * W;
-    const uint32_t val = wst[l * SW + o];
-    if (l < cnt) out[q] = val;
-  }
-  __syncwarp();
-}
 
 // ------------------------------------------------------------------ a1: bin count
 template <class SP>
@@ -211,34 +57,6 @@ struct Smem {
   // velocity tile + 8 neighbour slots + double-buffered record stage
   static constexpr int G2P_WARP = TILE + 32 + (2 * 32 * 4 * SP::W + 15) / 16 * 16;
 };
-
-// Per-lane load of record r (W words) into registers, 128/64-bit vectors when the
-// record size allows (records are 4W-byte aligned).
-template <class SP>
-__device__ __forceinline__ void load_record(const uint32_t* __restrict__ rec, uint32_t r, uint32_t* w) {
-  constexpr int W = SP::W;
-  const uint32_t* p = rec + (size_t)r * W;
-  if (W % 4 == 0) {
-#pragma unroll
-    for (int q = 0; q < W / 4; ++q) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + q);
-      w[4 * q] = v.x;
-      w[4 * q + 1] = v.y;
-      w[4 * q + 2] = v.z;
-      w[4 * q + 3] = v.w;
-    }
-  } else if (W % 2 == 0) {
-#pragma unroll
-    for (int q = 0; q < W / 2; ++q) {
-      const uint2 v = __ldg(reinterpret_cast<const uint2*>(p) + q);
-      w[2 * q] = v.x;
-      w[2 * q + 1] = v.y;
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < W; ++q) w[q] = __ldg(p + q);
-  }
-}
 
 // Per-lane asynchronous copy of record r (W words) into shared memory (cp.async, no
 // registers held while in flight; 16-byte granules when the record size allows).
@@ -606,48 +424,6 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
 }
 
 // ------------------------------------------------------------------ a5-a7: G2P + encode
-// Fast-path encode of state scalar i (Eq. 3 / Eq. 11, readings Q3, Q6): the code's
-// bits WITHOUT the saturation clamp.  `flag` is raised (OR-accumulated) whenever the
-// value might saturate or is not finite -- |t| >= 2^b - 1 or NaN -- and the caller then
-// re-encodes the whole record with the exact senc() (rare).  up: u > t;  nz: the value
-// is not on the grid (dither: down = nz - up) or, for RNE, dn: u < t.
-template <class SP>
-__device__ __forceinline__ uint32_t senc_fast(const int i, float v, uint32_t r24, bool& up, bool& nz, bool& flag) {
-  if (SP::kind(i) == kKindRaw) {
-    up = nz = false;
-    flag |= !(fabsf(v) < __int_as_float(0x7f800000));
-    return __float_as_uint(v);
-  }
-  const int wi = SP::width(i);
-  const float a = (SP::offset(i) != 0.0f) ? __fsub_rn(v, SP::offset(i)) : v;
-  const float t = __fmul_rn(a, SP::inv_delta(i));  // one fp32 multiply, no FMA (Q3)
-  const uint32_t mask = (wi == 32) ? 0xffffffffu : ((1u << wi) - 1u);
-  // |t| below lim => floor/round(t) (+1) lies inside [-2^b, 2^b - 1]
-  constexpr float lim_tab[33] = {0.f, 0.f, 1.f, 3.f, 7.f, 15.f, 31.f, 63.f, 127.f, 255.f, 511.f, 1023.f, 2047.f,
-                                 4095.f, 8191.f, 16383.f, 32767.f, 65535.f, 131071.f, 262143.f, 524287.f,
-                                 1048575.f, 2097151.f, 4194303.f, 8388607.f, 16777215.f, 0x1p24f, 0x1p25f,
-                                 0x1p26f, 0x1p27f, 0x1p28f, 0x1p29f, 0x1p30f};
-  const float lim = lim_tab[wi];
-  flag |= !(fabsf(t) < lim);
-  int u;
-  if (SP::DITHER) {
-    const float f = floorf(t);
-    const float y = __fsub_rn(t, f);  // exact
-    // 1 - r24 2^-24 = (2^24 - r24) 2^-24 is representable, so the fma is exact
-    const float one_minus_r = __fmaf_rn(-0x1p-24f, __uint2float_rn(r24), 1.0f);
-    up = y >= one_minus_r;  // u = floor(t + r) (Eq. 11, reading Q6)
-    nz = y > 0.0f;
-    u = __float2int_rz(f);
-    if (up) ++u;
-  } else {
-    const float q = rintf(t);  // round half to even (Q6)
-    up = q > t;
-    nz = q < t;
-    u = __float2int_rz(q);
-  }
-  return (uint32_t)u & mask;
-}
-
 // per-lane round counters packed 4 per register (byte i%4 of word i/4 counts state
 // scalar i), flushed into 32-bit per-lane totals (lane i holds scalar i) before a
 // byte can overflow

@@ -70,7 +70,8 @@ EXPORTS = ["qmpm_abi_version", "qmpm_last_error", "qmpm_layout", "qmpm_create", 
            "qmpm_read_debug", "qmpm_stats", "qmpm_encode", "qmpm_decode", "qmpm_set_profiling",
            "qmpm_kernel_times", "qmpm_kernel_name", "qmpm_launch_count", "qmpm_create_slab",
            "qmpm_get_unique_id", "qmpm_connect_nccl", "qmpm_step_group", "qmpm_set_ids",
-           "qmpm_read_ranges", "qmpm_predict_error", "qmpm_solve_error_bounded", "qmpm_solve_memory_bounded"]
+           "qmpm_read_ranges", "qmpm_predict_error", "qmpm_solve_error_bounded", "qmpm_solve_memory_bounded",
+           "qmpm_codec_matmul3"]
 
 
 def lib():
@@ -109,6 +110,7 @@ def lib():
         "qmpm_step_group": (i32, [P, ctypes.c_int, u32]),
         "qmpm_set_ids": (i32, [P, u64, P]),
         "qmpm_read_ranges": (i32, [P, P, ctypes.c_int]),
+        "qmpm_codec_matmul3": (i32, [ctypes.POINTER(Scheme), u64, P, P, P, u64, P, P]),
         "qmpm_predict_error": (i32, [u32, P, P, P]),
         "qmpm_solve_error_bounded": (i32, [u32, P, P, P, ctypes.c_double, ctypes.c_double, i32, i32, P, P]),
         "qmpm_solve_memory_bounded": (i32, [u32, P, P, P, ctypes.c_double, i32, i32, P, P]),
@@ -200,6 +202,16 @@ def encode(scheme: dict, vals, words, keys=None, step=0, counters=None, stream=N
     n = vals.shape[0]
     _check(lib().qmpm_encode(cs.ref, n, ptr(vals), ptr(keys), step, ptr(words), ptr(counters),
                              stream_handle(stream)))
+
+
+def codec_matmul3(scheme: dict, words_in, a, words_out, keys=None, step=0, stream=None):
+    """qmpm_codec_matmul3: records of a 3x3 matrix -> decode, times the constant a (3x3,
+    host), re-encode (the paper's MatMul task)."""
+    cs = CScheme(scheme)
+    n = words_in.shape[0]
+    am = np.ascontiguousarray(np.asarray(a, dtype=np.float32).reshape(9))
+    _check(lib().qmpm_codec_matmul3(cs.ref, n, ptr(words_in), am.ctypes.data, ptr(keys), step, ptr(words_out),
+                                    stream_handle(stream)))
 
 
 def decode(scheme: dict, words, vals, stream=None):

@@ -128,3 +128,54 @@ def test_set_state_read_state_bit_exact(name):
     sim.read_state(words=words2)
     assert np.array_equal(words2, w_ref)
     sim.close()
+
+
+def _matmul3_oracle(sch, words, a, keys, step):
+    """Oracle of qmpm_codec_matmul3 (P:797 MatMul task): oracle decode -> fp32 product
+    summed left to right without FMA (numpy float32 elementwise ops) -> oracle encode."""
+    m = oracle.decode(sch, words).astype(np.float32).reshape(-1, 3, 3)
+    A = np.asarray(a, np.float32).reshape(3, 3)
+    out = np.zeros_like(m)
+    for r in range(3):
+        for c in range(3):
+            out[:, r, c] = (m[:, r, 0] * A[0, c] + m[:, r, 1] * A[1, c]) + m[:, r, 2] * A[2, c]
+    return oracle.encode(sch, out.reshape(-1, 9), keys=keys, step=step)[0]
+
+
+@pytest.mark.parametrize("dithered", [False, True])
+@pytest.mark.parametrize("bits", [15, 11])
+def test_codec_matmul3_bit_exact(dithered, bits):
+    rng = np.random.default_rng(bits)
+    sch = dict(dim=3, material="elastic", rounding="dither" if dithered else "rne", seed=99,
+               fields=[dict(kind="fixed", frac_bits=bits, range=2.0, offset=0.0) for _ in range(9)])
+    n = 5000
+    v = rng.uniform(-0.9, 0.9, (n, 9)).astype(np.float32)
+    w_in, _ = oracle.encode(sch, v)
+    a = rng.uniform(-1.2, 1.2, 9).astype(np.float32)
+    keys = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32) if dithered else None
+    out = torch.zeros((n, w_in.shape[1]), dtype=torch.int32, device="cuda")
+    qmpm.codec_matmul3(sch, dev(w_in), a, out, keys=None if keys is None else dev(keys), step=7)
+    torch.cuda.synchronize()
+    ref = _matmul3_oracle(sch, w_in, a, keys, 7)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref)
+
+
+def test_codec_vector_paths_and_unaligned_pointers():
+    """The specialised codec picks 16/8/4-byte vector accesses from the row sizes and the
+    pointers' alignment: an offset (unaligned) view must give the same bits."""
+    rng = np.random.default_rng(5)
+    sch = dict(dim=3, material="elastic", rounding="dither", seed=3,
+               fields=[dict(kind="fixed", frac_bits=15, range=1.0, offset=0.0) for _ in range(8)])
+    n = 1000
+    v = rng.uniform(-0.99, 0.99, (n + 1, 8)).astype(np.float32)
+    keys = rng.integers(0, 2 ** 32, n + 1, dtype=np.uint64).astype(np.uint32)
+    ref, _ = oracle.encode(sch, v[1:], keys=keys[1:], step=2)
+    vt, kt = dev(v), dev(keys)
+    out = torch.zeros((n + 1) * 4 + 1, dtype=torch.int32, device="cuda")  # W = 4
+    qmpm.encode(sch, vt[1:], out[1:1 + n * 4].view(n, 4), keys=kt[1:], step=2)  # unaligned vals and words
+    torch.cuda.synchronize()
+    assert np.array_equal(out[1:1 + n * 4].cpu().numpy().view(np.uint32).reshape(n, 4), ref)
+    back = torch.zeros((n, 8), dtype=torch.float32, device="cuda")
+    qmpm.decode(sch, out[1:1 + n * 4].view(n, 4), back)
+    torch.cuda.synchronize()
+    assert np.array_equal(back.cpu().numpy(), oracle.decode(sch, ref))
