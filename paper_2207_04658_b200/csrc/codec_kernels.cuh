@@ -151,41 +151,68 @@ __device__ __forceinline__ void encode_record(const float* v, uint32_t h, bool v
 }  // namespace qmpm
 
 // ------------------------------------------------------------------ entry points
+// Each thread handles kU records per grid-stride iteration (record u*256 + tid of the
+// CTA's chunk), issuing all kU loads before any compute so enough bytes are in flight
+// to cover the HBM latency.
+constexpr int kU = 4;
+
 extern "C" __global__ void __launch_bounds__(256) qmpm_codec_encode(const float* __restrict__ vals,
                                                                     const uint32_t* __restrict__ keys, uint64_t n,
                                                                     uint32_t salt, uint32_t* __restrict__ words,
                                                                     unsigned long long* __restrict__ counters) {
   constexpr int NF = Spec::NF, W = Spec::W, ST = Spec::STRIDE;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n; i0 += stride) {
-    const uint64_t i = i0 + (threadIdx.x & 31u);
-    const bool valid = i < n;
-    float row[ST], v[NF];
+  const uint64_t chunk = 256ull * kU;
+  for (uint64_t c0 = (uint64_t)blockIdx.x * chunk; c0 < n; c0 += (uint64_t)gridDim.x * chunk) {
+    float row[kU][ST];
+    uint32_t key[kU];
 #pragma unroll
-    for (int q = 0; q < ST; ++q) row[q] = 0.0f;
-    if (valid) qmpm::load_row<ST, Spec::VV>(vals + i * ST, row);
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = c0 + u * 256 + threadIdx.x;
 #pragma unroll
-    for (int f = 0; f < NF; ++f) v[f] = valid ? row[Spec::col(f)] : Spec::offset(f);
-    const uint32_t h = Spec::DITHER ? qmpm::mix32((valid ? __ldg(keys + i) : 0u) ^ salt) : 0u;
-    uint32_t w[W + 1];
-    qmpm::encode_record<Spec>(v, h, valid, w, counters);
-    if (valid) qmpm::store_words<Spec>(words + i * W, w);
+      for (int q = 0; q < ST; ++q) row[u][q] = 0.0f;
+      key[u] = 0u;
+      if (i < n) {
+        qmpm::load_row<ST, Spec::VV>(vals + i * ST, row[u]);
+        if (Spec::DITHER) key[u] = __ldg(keys + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = c0 + u * 256 + threadIdx.x;
+      const bool valid = i < n;
+      float v[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) v[f] = valid ? row[u][Spec::col(f)] : Spec::offset(f);
+      const uint32_t h = Spec::DITHER ? qmpm::mix32(key[u] ^ salt) : 0u;
+      uint32_t w[W + 1];
+      qmpm::encode_record<Spec>(v, h, valid, w, counters);
+      if (valid) qmpm::store_words<Spec>(words + i * W, w);
+    }
   }
 }
 
 extern "C" __global__ void __launch_bounds__(256) qmpm_codec_decode(const uint32_t* __restrict__ words, uint64_t n,
                                                                     float* __restrict__ vals) {
   constexpr int NF = Spec::NF, W = Spec::W, ST = Spec::STRIDE;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    uint32_t w[W + 1];
-    qmpm::load_words<Spec>(words + i * W, w);
-    float row[ST];
+  const uint64_t chunk = 256ull * kU;
+  for (uint64_t c0 = (uint64_t)blockIdx.x * chunk; c0 < n; c0 += (uint64_t)gridDim.x * chunk) {
+    uint32_t w[kU][W + 1];
 #pragma unroll
-    for (int q = 0; q < ST; ++q) row[q] = 0.0f;
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = c0 + u * 256 + threadIdx.x;
+      if (i < n) qmpm::load_words<Spec>(words + i * W, w[u]);
+    }
 #pragma unroll
-    for (int f = 0; f < NF; ++f) row[Spec::col(f)] = qmpm::sdec<Spec>(w, f);
-    qmpm::store_row<ST, Spec::VV>(vals + i * ST, row);
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = c0 + u * 256 + threadIdx.x;
+      if (i >= n) continue;
+      float row[ST];
+#pragma unroll
+      for (int q = 0; q < ST; ++q) row[q] = 0.0f;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) row[Spec::col(f)] = qmpm::sdec<Spec>(w[u], f);
+      qmpm::store_row<ST, Spec::VV>(vals + i * ST, row);
+    }
   }
 }
 
@@ -200,26 +227,37 @@ extern "C" __global__ void __launch_bounds__(256) qmpm_codec_matmul3(const uint3
                                                                      uint32_t salt, uint32_t* __restrict__ out) {
   constexpr int W = Spec::W;
   if constexpr (Spec::NF != 9) return;  // records must hold a 3x3 matrix (the host checks)
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n; i0 += stride) {
-    const uint64_t i = i0 + (threadIdx.x & 31u);
-    const bool valid = i < n;
-    uint32_t w[W + 1];
+  const uint64_t chunk = 256ull * kU;
+  for (uint64_t c0 = (uint64_t)blockIdx.x * chunk; c0 < n; c0 += (uint64_t)gridDim.x * chunk) {
+    uint32_t wi[kU][W + 1], key[kU];
 #pragma unroll
-    for (int q = 0; q <= W; ++q) w[q] = 0u;
-    if (valid) qmpm::load_words<Spec>(in + i * W, w);
-    float m[9], v[9];
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = c0 + u * 256 + threadIdx.x;
 #pragma unroll
-    for (int f = 0; f < 9; ++f) m[f] = qmpm::sdec<Spec>(w, f < Spec::NF ? f : 0);
+      for (int q = 0; q <= W; ++q) wi[u][q] = 0u;
+      key[u] = 0u;
+      if (i < n) {
+        qmpm::load_words<Spec>(in + i * W, wi[u]);
+        if (Spec::DITHER) key[u] = __ldg(keys + i);
+      }
+    }
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = c0 + u * 256 + threadIdx.x;
+      const bool valid = i < n;
+      float m[9], v[9];
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        v[3 * r + c] = __fadd_rn(__fadd_rn(__fmul_rn(m[3 * r], A.a[c]), __fmul_rn(m[3 * r + 1], A.a[3 + c])),
-                                 __fmul_rn(m[3 * r + 2], A.a[6 + c]));
-    const uint32_t h = Spec::DITHER ? qmpm::mix32((valid ? __ldg(keys + i) : 0u) ^ salt) : 0u;
-    uint32_t o[W + 1];
-    qmpm::encode_record<Spec>(v, h, valid, o, nullptr);
-    if (valid) qmpm::store_words<Spec>(out + i * W, o);
+      for (int f = 0; f < 9; ++f) m[f] = qmpm::sdec<Spec>(wi[u], f < Spec::NF ? f : 0);
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          v[3 * r + c] = __fadd_rn(__fadd_rn(__fmul_rn(m[3 * r], A.a[c]), __fmul_rn(m[3 * r + 1], A.a[3 + c])),
+                                   __fmul_rn(m[3 * r + 2], A.a[6 + c]));
+      const uint32_t h = Spec::DITHER ? qmpm::mix32(key[u] ^ salt) : 0u;
+      uint32_t o[W + 1];
+      qmpm::encode_record<Spec>(v, h, valid, o, nullptr);
+      if (valid) qmpm::store_words<Spec>(out + i * W, o);
+    }
   }
 }
