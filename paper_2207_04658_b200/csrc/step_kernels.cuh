@@ -281,9 +281,11 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
       uint32_t k0, k1;
       int c;
       seg_range(g * 32 + lane, k0, k1, c);
-      float am[NN], ax[NN], ay[NN], az[NN];
+      // node accumulators as fp32 pairs for the packed FFMA2/FADD2 (sm_100): axy = (p_x,
+      // p_y), azm = (p_z, sum w); each lane of a pair is the same IEEE op as scalar code
+      float2 axy[NN], azm[NN];
 #pragma unroll
-      for (int q = 0; q < NN; ++q) am[q] = ax[q] = ay[q] = az[q] = 0.0f;
+      for (int q = 0; q < NN; ++q) axy[q] = azm[q] = make_float2(0.0f, 0.0f);
 #pragma unroll 1
       for (uint32_t k = k0; k < k1; ++k) {
         fetch();
@@ -323,46 +325,43 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
 #pragma unroll
         for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
         if (D == 3) {
+          const float2 a2xy = make_float2(A[2][0], A[2][1]), a2z0 = make_float2(A[2][2], 0.0f);
 #pragma unroll
           for (int ox = 0; ox < 3; ++ox) {
 #pragma unroll
             for (int oy = 0; oy < 3; ++oy) {
               const float wxy = wt[0][ox] * wt[1][oy];
-              float M[3];
-#pragma unroll
-              for (int a = 0; a < 3; ++a) M[a] = Q[a] + (float)ox * A[0][a] + (float)oy * A[1][a];
+              // (M_x, M_y), (M_z, 1): momentum per unit weight at node (ox, oy, 0)
+              float2 mxy = make_float2(Q[0] + (float)ox * A[0][0] + (float)oy * A[1][0],
+                                       Q[1] + (float)ox * A[0][1] + (float)oy * A[1][1]);
+              float2 mz1 = make_float2(Q[2] + (float)ox * A[0][2] + (float)oy * A[1][2], 1.0f);
 #pragma unroll
               for (int oz = 0; oz < 3; ++oz) {
                 const int q = (ox * 3 + oy) * 3 + oz;
                 const float ww = wxy * wt[2][oz];
-                am[q] += ww;
-                ax[q] = fmaf(ww, M[0], ax[q]);
-                ay[q] = fmaf(ww, M[1], ay[q]);
-                az[q] = fmaf(ww, M[2], az[q]);
+                const float2 w2 = make_float2(ww, ww);
+                axy[q] = __ffma2_rn(w2, mxy, axy[q]);
+                azm[q] = __ffma2_rn(w2, mz1, azm[q]);  // .y: sum w + ww * 1 (exact product)
                 if (oz < 2) {
-#pragma unroll
-                  for (int a = 0; a < 3; ++a) M[a] += A[2][a];
+                  mxy = __fadd2_rn(mxy, a2xy);
+                  mz1 = __fadd2_rn(mz1, a2z0);
                 }
               }
             }
           }
         } else {
+          const float2 a1xy = make_float2(A[1][0], A[1][1]);
 #pragma unroll
           for (int ox = 0; ox < 3; ++ox) {
-            float M[2];
-#pragma unroll
-            for (int a = 0; a < 2; ++a) M[a] = Q[a] + (float)ox * A[0][a];
+            float2 mxy = make_float2(Q[0] + (float)ox * A[0][0], Q[1] + (float)ox * A[0][1]);
 #pragma unroll
             for (int oy = 0; oy < 3; ++oy) {
               const int q = ox * 3 + oy;
               const float ww = wt[0][ox] * wt[1][oy];
-              am[q] += ww;
-              ax[q] = fmaf(ww, M[0], ax[q]);
-              ay[q] = fmaf(ww, M[1], ay[q]);
-              if (oy < 2) {
-                M[0] += A[1][0];
-                M[1] += A[1][1];
-              }
+              const float2 w2 = make_float2(ww, ww);
+              axy[q] = __ffma2_rn(w2, mxy, axy[q]);
+              azm[q].y += ww;
+              if (oy < 2) mxy = __fadd2_rn(mxy, a1xy);
             }
           }
         }
@@ -391,10 +390,10 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
           const int idx = base_idx + (D == 3 ? (ox * G::T + oy) * G::T + oz : ox * G::T + oy);
           if (mine && occ == o) {
             float4 t = tile[idx];
-            t.x = fmaf(am[q], S.p_mass, t.x);
-            t.y += ax[q];
-            t.z += ay[q];
-            t.w += az[q];
+            t.x = fmaf(azm[q].y, S.p_mass, t.x);
+            t.y += axy[q].x;
+            t.z += axy[q].y;
+            t.w += azm[q].x;
             tile[idx] = t;
           }
           __syncwarp();
