@@ -588,33 +588,55 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       float Sv[3] = {0.f, 0.f, 0.f}, T[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
       const int base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
       if (D == 3) {
-        const float wz2x2 = 2.0f * wt[2][2];
+        // packed FP32x2 (sm_100 FFMA2 / FMUL2): pair 0 = (v_x, v_y), pair 1 = (v_z, 0) of a
+        // node; each lane is the same IEEE op the scalar form does
+        const float wz0 = wt[2][0], wz1 = wt[2][1], wz2 = wt[2][2], wz2x2 = 2.0f * wt[2][2];
+        float2 sv[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float2 tx[2] = {sv[0], sv[0]}, tyy[2] = {sv[0], sv[0]}, tzz[2] = {sv[0], sv[0]};
 #pragma unroll
         for (int ox = 0; ox < 3; ++ox) {
-          float sy[3] = {0.f, 0.f, 0.f}, ty[3] = {0.f, 0.f, 0.f}, tzy[3] = {0.f, 0.f, 0.f};
+          float2 sy[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, ty[2] = {sy[0], sy[0]},
+                 tzy[2] = {sy[0], sy[0]};
 #pragma unroll
           for (int oy = 0; oy < 3; ++oy) {
             const int idx = base_idx + (ox * G::T + oy) * G::T;
             const float4 g0 = tile[idx], g1 = tile[idx + 1], g2 = tile[idx + 2];
-            const float ga[3][3] = {{g0.x, g0.y, g0.z}, {g1.x, g1.y, g1.z}, {g2.x, g2.y, g2.z}};
+            const float2 ga[3][2] = {{make_float2(g0.x, g0.y), make_float2(g0.z, g0.w)},
+                                     {make_float2(g1.x, g1.y), make_float2(g1.z, g1.w)},
+                                     {make_float2(g2.x, g2.y), make_float2(g2.z, g2.w)}};
+            const float wy = wt[1][oy], wyo = wt[1][oy] * oy;
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              const float p1 = wt[2][1] * ga[1][a];
-              const float tz = fmaf(wz2x2, ga[2][a], p1);                       // sum_oz w oz g
-              const float sz = fmaf(wt[2][0], ga[0][a], fmaf(wt[2][2], ga[2][a], p1));  // sum_oz w g
-              sy[a] = fmaf(wt[1][oy], sz, sy[a]);
-              tzy[a] = fmaf(wt[1][oy], tz, tzy[a]);
-              if (oy) ty[a] = fmaf(wt[1][oy] * oy, sz, ty[a]);
+            for (int pp = 0; pp < 2; ++pp) {
+              const float2 p1 = __fmul2_rn(make_float2(wz1, wz1), ga[1][pp]);
+              const float2 tz = __ffma2_rn(make_float2(wz2x2, wz2x2), ga[2][pp], p1);  // sum_oz w oz g
+              const float2 sz = __ffma2_rn(make_float2(wz0, wz0), ga[0][pp],
+                                           __ffma2_rn(make_float2(wz2, wz2), ga[2][pp], p1));  // sum_oz w g
+              sy[pp] = __ffma2_rn(make_float2(wy, wy), sz, sy[pp]);
+              tzy[pp] = __ffma2_rn(make_float2(wy, wy), tz, tzy[pp]);
+              if (oy) ty[pp] = __ffma2_rn(make_float2(wyo, wyo), sz, ty[pp]);
             }
           }
+          const float wx = wt[0][ox], wxo = wt[0][ox] * ox;
 #pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            Sv[a] = fmaf(wt[0][ox], sy[a], Sv[a]);
-            T[a][1] = fmaf(wt[0][ox], ty[a], T[a][1]);
-            T[a][2] = fmaf(wt[0][ox], tzy[a], T[a][2]);
-            if (ox) T[a][0] = fmaf(wt[0][ox] * ox, sy[a], T[a][0]);
+          for (int pp = 0; pp < 2; ++pp) {
+            sv[pp] = __ffma2_rn(make_float2(wx, wx), sy[pp], sv[pp]);
+            tyy[pp] = __ffma2_rn(make_float2(wx, wx), ty[pp], tyy[pp]);
+            tzz[pp] = __ffma2_rn(make_float2(wx, wx), tzy[pp], tzz[pp]);
+            if (ox) tx[pp] = __ffma2_rn(make_float2(wxo, wxo), sy[pp], tx[pp]);
           }
         }
+        Sv[0] = sv[0].x;
+        Sv[1] = sv[0].y;
+        Sv[2] = sv[1].x;
+        T[0][0] = tx[0].x;
+        T[1][0] = tx[0].y;
+        T[2][0] = tx[1].x;
+        T[0][1] = tyy[0].x;
+        T[1][1] = tyy[0].y;
+        T[2][1] = tyy[1].x;
+        T[0][2] = tzz[0].x;
+        T[1][2] = tzz[0].y;
+        T[2][2] = tzz[1].x;
       } else {
 #pragma unroll
         for (int ox = 0; ox < 3; ++ox) {
