@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--scheme", default=None, help="x16 | e0.1 | e0.01 | f2 | fp32")
     ap.add_argument("--n", type=int, default=0, help="override particle count (reduced runs)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="C4 with N > 1 GPUs: weak = 400M per GPU on a z-extended domain (default); "
+                         "strong = 400M in total on the 256^3 domain, cut into N z slabs")
     ap.add_argument("--z-extent", type=float, default=1.0,
                     help="C4 only: z extent of the 1-GPU domain (reduced same-density runs for profiling)")
     ap.add_argument("--scene-warmup", type=int, default=50)
@@ -69,7 +72,8 @@ def make_scene(args, world=1):
         sc = scenes.c3(n_target=args.n or scenes.C3_PARTICLES)
         sch = schemes.e001()
     else:
-        sc = scenes.c4(n_target=(args.n or 400_000_000) * world, z_extent=float(world) * args.z_extent)
+        wx = world if args.scaling == "weak" else 1
+        sc = scenes.c4(n_target=(args.n or 400_000_000) * wx, z_extent=float(wx) * args.z_extent)
         sch = schemes.f2()
     if args.scheme:
         sch = schemes.fp32(sc.dim, sc.material) if args.scheme == "fp32" else schemes.BY_NAME[args.scheme]()
@@ -171,7 +175,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "quantized MPM particle-steps/sec", "value": value,
         "unit": "particle-steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args, sc, W, bits), "sample_particles": n},
         "cpu_baseline": {"value": value, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
@@ -230,7 +234,7 @@ def run_gpu(args):
             uid = qdist.share_unique_id(qmpm.get_unique_id)
             sim.connect_nccl(uid)
             qdist.load_slab(sim, sc, cuts, rank, track_ids=False)
-            N = sc.n_particles // world  # particles per GPU (weak scaling)
+            N = sc.n_particles // world  # particles per GPU
         torch.cuda.empty_cache()
         sim.step(args.scene_warmup + args.warmup)
         stream.synchronize()
@@ -339,8 +343,8 @@ def run_gpu(args):
     line = {
         "metric": "quantized MPM particle-steps/sec", "value": value, "unit": "particle-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-        "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": (value / world / PAPER_PSTEPS[args.config])
+        "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": (value / (world if args.scaling == "weak" else 1) / PAPER_PSTEPS[args.config])
         if (args.config in PAPER_PSTEPS and not args.n and scheme_name(args) == {"c3": "e0.01", "c4": "f2"}[args.config])
         else None,
         "dtype": "f32", "data": "synthetic",
