@@ -51,7 +51,9 @@ class OracleScheme(ctypes.Structure):
                 ("scalar", ctypes.c_uint32 * MAX_FIELDS),
                 ("rounding", ctypes.c_uint32),
                 ("pad", ctypes.c_uint32),
-                ("dither_seed", ctypes.c_uint64)]
+                ("dither_seed", ctypes.c_uint64),
+                ("exp_bits", ctypes.c_uint32 * MAX_FIELDS),
+                ("group", ctypes.c_uint32 * MAX_FIELDS)]
 
 
 class OracleSim(ctypes.Structure):
@@ -131,7 +133,9 @@ def make_scheme(scheme) -> OracleScheme:
     fields = scheme["fields"]
     s.n_fields = len(fields)
     for i, f in enumerate(fields):
-        s.kind[i] = 0 if f["kind"] == "fixed" else 1
+        s.kind[i] = {"fixed": 0, "raw": 1, "shared_exp": 2}[f["kind"]]
+        s.exp_bits[i] = f.get("exp_bits", 0)
+        s.group[i] = f.get("group", 0)
         s.frac_bits[i] = f.get("frac_bits", 0)
         s.range[i] = f.get("range", 1.0)
         s.offset[i] = f.get("offset", 0.0)

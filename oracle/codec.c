@@ -50,9 +50,31 @@ uint32_t oracle_r24(uint64_t seed, uint64_t step, uint32_t key, uint32_t field) 
     return x >> 8;
 }
 
+/* SHARED_EXP groups (reading Q4): a maximal run of consecutive SHARED_EXP fields with
+ * equal group ids.  The first member stores the group exponent in front of its
+ * mantissa. */
+static int group_first(const oracle_scheme* s, uint32_t f) {
+    return s->kind[f] == ORACLE_SHARED_EXP &&
+           (f == 0 || s->kind[f - 1] != ORACLE_SHARED_EXP || s->group[f - 1] != s->group[f]);
+}
+static uint32_t group_start(const oracle_scheme* s, uint32_t f) {
+    while (!group_first(s, f)) --f;
+    return f;
+}
+static uint32_t group_last(const oracle_scheme* s, uint32_t f) {
+    while (f + 1 < s->n_fields && s->kind[f + 1] == ORACLE_SHARED_EXP && !group_first(s, f + 1)) ++f;
+    return f;
+}
+
 static uint32_t field_width(const oracle_scheme* s, uint32_t f) {
     if (s->kind[f] == ORACLE_RAW_F32) return 32;
+    if (s->kind[f] == ORACLE_SHARED_EXP) return s->frac_bits[f] + 1 + (group_first(s, f) ? s->exp_bits[f] : 0);
     return s->frac_bits[f] + 1;
+}
+
+static int is_pow2(float r) {
+    int e;
+    return r > 0.0f && isfinite(r) && frexpf(r, &e) == 0.5f;
 }
 
 /* Layout: offset_k = sum_{j<k} width_j; W = ceil(total/32).
@@ -61,7 +83,14 @@ int oracle_layout(const oracle_scheme* s, uint32_t* offsets, uint32_t* words, ui
     if (s->n_fields == 0 || s->n_fields > ORACLE_MAX_FIELDS) return -1;
     uint32_t total = 0;
     for (uint32_t f = 0; f < s->n_fields; ++f) {
-        if (s->kind[f] != ORACLE_FIXED && s->kind[f] != ORACLE_RAW_F32) return -1;
+        if (s->kind[f] != ORACLE_FIXED && s->kind[f] != ORACLE_RAW_F32 && s->kind[f] != ORACLE_SHARED_EXP) return -1;
+        if (s->kind[f] == ORACLE_SHARED_EXP) { /* members share b, e and R_min; e in 1..8 */
+            uint32_t g0 = group_start(s, f);
+            if (s->exp_bits[f] < 1 || s->exp_bits[f] > 8 || s->frac_bits[f] != s->frac_bits[g0] ||
+                s->exp_bits[f] != s->exp_bits[g0] || s->range[f] != s->range[g0] || !is_pow2(s->range[f]) ||
+                s->offset[f] != 0.0f)
+                return -1;
+        }
         uint32_t w = field_width(s, f);
         if (w == 0 || w > 32) return -1;
         if (offsets) offsets[f] = total;
@@ -156,12 +185,52 @@ static int32_t sign_extend(uint32_t raw, uint32_t width) {
     return (int32_t)raw;
 }
 
+/* One SHARED_EXP group [f0, f1] of a record (reading Q4).  M = max |v| over the finite
+ * members; E = the smallest exponent in [0, 2^e - 1] with M < R_min 2^E; the members
+ * are encoded by the FIXED rule with range R_min 2^E (Delta_E = R_min 2^(E - b), exact);
+ * if a member's code would saturate and E < 2^e - 1, E is raised by one and the group
+ * re-encoded.  At E = 2^e - 1 codes saturate (counted). */
+static void encode_group(const oracle_scheme* s, const uint32_t* offsets, uint32_t f0, uint32_t f1,
+                         const float* vals, int dithered, uint32_t key, uint64_t step, uint32_t* rec,
+                         uint64_t* counters) {
+    uint32_t b = s->frac_bits[f0], e = s->exp_bits[f0], emax = (1u << e) - 1u;
+    float R = s->range[f0];
+    float M = 0.0f;
+    for (uint32_t f = f0; f <= f1; ++f)
+        if (isfinite(vals[f]) && fabsf(vals[f]) > M) M = fabsf(vals[f]);
+    uint32_t E = 0;
+    while (E < emax && !(M < ldexpf(R, (int)E))) ++E;
+    for (;;) {
+        uint64_t sat = 0;
+        for (uint32_t f = f0; f <= f1; ++f) {
+            uint32_t r24 = dithered ? oracle_r24(s->dither_seed, step, key, f) : 0;
+            oracle_encode_value(vals[f], b, ldexpf(R, (int)E), 0.0f, dithered, r24, &sat, 0, 0, 0);
+        }
+        if (sat == 0 || E == emax) break;
+        ++E;
+    }
+    oracle_put_bits(rec, offsets[f0], e, E);
+    for (uint32_t f = f0; f <= f1; ++f) {
+        uint32_t r24 = dithered ? oracle_r24(s->dither_seed, step, key, f) : 0;
+        int64_t u = oracle_encode_value(vals[f], b, ldexpf(R, (int)E), 0.0f, dithered, r24,
+                                        counters ? &counters[f] : 0, counters ? &counters[64 + f] : 0,
+                                        counters ? &counters[128 + f] : 0, counters ? &counters[192] : 0);
+        uint32_t width = b + 1, mask = (width == 32) ? 0xffffffffu : ((1u << width) - 1u);
+        oracle_put_bits(rec, offsets[f] + (f == f0 ? e : 0), width, (uint32_t)u & mask);
+    }
+}
+
 static void encode_record(const oracle_scheme* s, const uint32_t* offsets, uint32_t W,
                           const float* vals /* packing order */, int dithered, uint32_t key,
                           uint64_t step, uint32_t* rec, uint64_t* counters) {
     for (uint32_t w = 0; w < W; ++w) rec[w] = 0;
     for (uint32_t f = 0; f < s->n_fields; ++f) {
         float v = vals[f];
+        if (s->kind[f] == ORACLE_SHARED_EXP) {
+            if (group_first(s, f)) encode_group(s, offsets, f, group_last(s, f), vals, dithered, key, step, rec,
+                                                counters);
+            continue;
+        }
         if (s->kind[f] == ORACLE_RAW_F32) {
             if (!isfinite(v) && counters) counters[192]++;
             uint32_t bits;
@@ -194,6 +263,12 @@ int oracle_encode(const oracle_scheme* s, uint64_t n, const float* vals, const u
 
 static float decode_field(const oracle_scheme* s, const uint32_t* offsets, const uint32_t* rec,
                           uint32_t f) {
+    if (s->kind[f] == ORACLE_SHARED_EXP) { /* reading Q4: u * R_min 2^(E - b) */
+        uint32_t g0 = group_start(s, f), e = s->exp_bits[f], width = s->frac_bits[f] + 1;
+        uint32_t E = oracle_get_bits(rec, offsets[g0], e);
+        int32_t u = sign_extend(oracle_get_bits(rec, offsets[f] + (f == g0 ? e : 0), width), width);
+        return oracle_decode_value(u, s->frac_bits[f], ldexpf(s->range[f], (int)E), 0.0f);
+    }
     if (s->kind[f] == ORACLE_RAW_F32) {
         uint32_t bits = oracle_get_bits(rec, offsets[f], 32);
         float v;

@@ -22,6 +22,7 @@
 #define ORACLE_MAX_FIELDS 64
 #define ORACLE_FIXED 0u
 #define ORACLE_RAW_F32 1u
+#define ORACLE_SHARED_EXP 2u
 #define ORACLE_RNE 0u
 #define ORACLE_DITHER 1u
 #define ORACLE_ELASTIC 0u
@@ -43,6 +44,11 @@ typedef struct {
     uint32_t rounding;                     /* ORACLE_RNE or ORACLE_DITHER */
     uint32_t pad;
     uint64_t dither_seed;
+    /* SHARED_EXP (reading Q4): consecutive fields with the same group id share one
+     * exp_bits-bit exponent E stored in front of the group's first mantissa; member
+     * values are u * Delta_E, Delta_E = range * 2^(E - b) (range = R_min, a power of 2). */
+    uint32_t exp_bits[ORACLE_MAX_FIELDS];
+    uint32_t group[ORACLE_MAX_FIELDS];
 } oracle_scheme;
 
 /* MLS-MPM scene parameters (reading SURVEY §8(c) C-mpm). */

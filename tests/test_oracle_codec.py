@@ -316,3 +316,80 @@ def test_mix32_is_a_bijection_on_a_sample():
     hs = {L.oracle_mix32(int(x) & 0xFFFFFFFF) for x in xs}
     assert len(hs) == len(xs)
     assert L.oracle_mix32(0) == 0
+
+
+# --------------------------------------------------------------- SHARED_EXP (reading Q4)
+def shared_scheme(n, b, e, R, rounding="rne", groups=None):
+    groups = groups or [0] * n
+    return dict(dim=0, material="elastic", rounding=rounding, seed=11,
+                fields=[dict(kind="shared_exp", frac_bits=b, exp_bits=e, range=R, offset=0.0, group=g)
+                        for g in groups])
+
+
+def test_shared_exp_worked_example():
+    """Reading Q4 by hand: b = 3, e = 3, R_min = 1/4, v = (0.6, -0.1, 0.05): M = 0.6 ->
+    smallest E with 0.6 < 2^E / 4 is E = 2 (range 1, Delta = 1/8); codes rne(4.8) = 5,
+    rne(-0.8) = -1, rne(0.4) = 0 -> (0.625, -0.125, 0).  Layout: 3 + 4 + 4 + 4 bits."""
+    s = shared_scheme(3, 3, 3, 0.25)
+    offs, W, bits = oracle.layout(s)
+    assert list(offs) == [0, 7, 11] and bits == 15
+    w, cnt = oracle.encode(s, np.array([[0.6, -0.1, 0.05]], np.float32))
+    L = oracle.lib()
+    assert L.oracle_get_bits(w[0].ctypes.data, 0, 3) == 2
+    assert L.oracle_get_bits(w[0].ctypes.data, 3, 4) == 5
+    assert L.oracle_get_bits(w[0].ctypes.data, 7, 4) == 0b1111
+    assert L.oracle_get_bits(w[0].ctypes.data, 11, 4) == 0
+    assert list(oracle.decode(s, w)[0]) == [0.625, -0.125, 0.0]
+
+
+def test_shared_exp_rounding_overflow_raises_the_exponent():
+    """b = 3, R_min = 1: M = 0.97 < 1 gives E = 0, but rne(0.97 * 8) = 8 > 2^3 - 1, so
+    E = 1 (Delta = 1/4) and the code is rne(3.88) = 4 -> 1.0, no saturation counted."""
+    s = shared_scheme(2, 3, 2, 1.0)
+    w, cnt = oracle.encode(s, np.array([[0.97, 0.1]], np.float32))
+    assert oracle.lib().oracle_get_bits(w[0].ctypes.data, 0, 2) == 1
+    assert list(oracle.decode(s, w)[0]) == [1.0, 0.0]
+    assert cnt[0] == 0 and cnt[1] == 0
+
+
+def test_shared_exp_zero_group_and_saturation():
+    s = shared_scheme(3, 5, 2, 0.5)
+    w, _ = oracle.encode(s, np.zeros((1, 3), np.float32))
+    assert np.all(w == 0)
+    # E_max = 3: range 0.5 * 8 = 4; 100 saturates at the largest code, counted
+    w, cnt = oracle.encode(s, np.array([[100.0, -100.0, 1.0]], np.float32))
+    d = oracle.decode(s, w)[0]
+    assert oracle.lib().oracle_get_bits(w[0].ctypes.data, 0, 2) == 3
+    assert d[0] == 4.0 * (31 / 32) and d[1] == -4.0 and d[2] == 1.0
+    assert cnt[0] == 1 and cnt[1] == 1 and cnt[2] == 0
+
+
+@pytest.mark.parametrize("rounding", ["rne", "dither"])
+def test_shared_exp_error_bound_and_minimal_exponent(rounding):
+    """Per group the stored E is the smallest that holds max |v| (or one more after a
+    rounding overflow), and every member is within 1/2 Delta_E (RNE) or below Delta_E
+    (dithered) of its value (Eq. 3 / Eq. 11 with the group's resolution)."""
+    rng = np.random.default_rng(3)
+    b, e, R = 9, 4, 2.0 ** -6
+    s = shared_scheme(6, b, e, R, rounding=rounding, groups=[0, 0, 0, 1, 1, 1])
+    n = 20000
+    mag = 2.0 ** rng.uniform(-8, 7, (n, 2))
+    v = (rng.uniform(-1, 1, (n, 6)) * np.repeat(mag, 3, axis=1)).astype(np.float32)
+    keys = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32) if rounding == "dither" else None
+    w, _ = oracle.encode(s, v, keys=keys, step=3)
+    d = oracle.decode(s, w)
+    offs, _, _ = oracle.layout(s)
+    L = oracle.lib()
+    for g, f0 in enumerate((0, 3)):
+        E = np.array([L.oracle_get_bits(w[i].ctypes.data, int(offs[f0]), e) for i in range(n)])
+        M = np.abs(v[:, f0:f0 + 3]).max(axis=1).astype(np.float64)
+        delta = R * 2.0 ** (E - b)
+        err = np.abs(d[:, f0:f0 + 3] - v[:, f0:f0 + 3]).max(axis=1)
+        ok = E < 2 ** e - 1
+        if rounding == "rne":
+            assert np.all(err[ok] <= 0.5 * delta[ok] * (1 + 1e-7))
+        else:
+            assert np.all(err[ok] < delta[ok])
+        minimal = (E == 0) | (M >= R * 2.0 ** (E - 1)) | (M >= R * 2.0 ** (E - 1) * (1 - 2.0 ** -b))
+        assert np.all(minimal)
+        assert np.all(M[ok] < R * 2.0 ** E[ok])
