@@ -123,7 +123,22 @@ int scalar_of(int attr, int comp, int d, int material) {
   }
 }
 
+// SHARED_EXP groups (reading Q4): maximal runs of consecutive SHARED_EXP fields with equal
+// group ids; the first (the leader) stores the exponent in front of its mantissa.
+bool group_first(const qmpm_scheme* s, uint32_t i) {
+  const qmpm_field* f = s->fields;
+  return f[i].kind == QMPM_SHARED_EXP &&
+         (i == 0 || f[i - 1].kind != QMPM_SHARED_EXP || f[i - 1].group != f[i].group);
+}
+uint32_t group_start(const qmpm_scheme* s, uint32_t i) {
+  while (!group_first(s, i)) --i;
+  return i;
+}
+
 uint32_t field_width(const qmpm_field& f) { return f.kind == QMPM_RAW_F32 ? 32u : (uint32_t)f.frac_bits + 1u; }
+uint32_t field_width_in(const qmpm_scheme* s, uint32_t i) {
+  return field_width(s->fields[i]) + (group_first(s, i) ? s->fields[i].exp_bits : 0u);
+}
 
 // bit-pack layout: contiguous, LSB-first, in declaration order
 qmpm_status layout_of(qmpm_ctx* ctx, const qmpm_scheme* s, std::vector<uint32_t>& offs, uint32_t& W,
@@ -136,28 +151,50 @@ qmpm_status layout_of(qmpm_ctx* ctx, const qmpm_scheme* s, std::vector<uint32_t>
   uint32_t total = 0;
   for (uint32_t i = 0; i < s->n_fields; ++i) {
     const qmpm_field& f = s->fields[i];
-    if (f.kind == QMPM_SHARED_EXP) return fail(ctx, QMPM_ELAYOUT, "field %u: SHARED_EXP is not supported", i);
-    if (f.kind != QMPM_FIXED && f.kind != QMPM_RAW_F32) return fail(ctx, QMPM_ELAYOUT, "field %u: bad kind %u", i, f.kind);
+    if (f.kind != QMPM_FIXED && f.kind != QMPM_RAW_F32 && f.kind != QMPM_SHARED_EXP)
+      return fail(ctx, QMPM_ELAYOUT, "field %u: bad kind %u", i, f.kind);
+    if (f.kind == QMPM_SHARED_EXP) {  // members share b, e and R_min (a power of two); no offset
+      const qmpm_field& g = s->fields[group_start(s, i)];
+      int ex = 0;
+      const bool pow2 = f.range > 0.0f && std::isfinite(f.range) && std::frexp(f.range, &ex) == 0.5f;
+      if (f.exp_bits < 1 || f.exp_bits > 8 || f.frac_bits != g.frac_bits || f.exp_bits != g.exp_bits ||
+          f.range != g.range || !pow2 || f.offset != 0.0f || (uint32_t)f.frac_bits + 1u > 24u)
+        return fail(ctx, QMPM_ELAYOUT,
+                    "field %u: SHARED_EXP members need equal frac_bits (<= 23), exp_bits (1..8) and a power-of-two "
+                    "range, and no offset", i);
+      // Delta_0 2^E must stay a normal float for E in [0, 2^e - 1]
+      const int lo = (ex - 1) - (int)f.frac_bits, hi = lo + (1 << f.exp_bits) - 1;
+      if (lo < -120 || hi > 120) return fail(ctx, QMPM_ELAYOUT, "field %u: SHARED_EXP range out of bounds", i);
+    }
     if (f.kind == QMPM_FIXED) {
       if ((uint32_t)f.frac_bits + 1u > 32u) return fail(ctx, QMPM_ELAYOUT, "field %u: width %u > 32", i, f.frac_bits + 1u);
       if (!(f.range > 0.0f) || !std::isfinite(f.range)) return fail(ctx, QMPM_ELAYOUT, "field %u: range must be > 0", i);
       if (!std::isfinite(f.offset)) return fail(ctx, QMPM_ELAYOUT, "field %u: offset not finite", i);
     }
     offs[i] = total;
-    total += field_width(f);
+    total += field_width_in(s, i);
   }
   bits = total;
   W = (total + 31) / 32;
   return QMPM_OK;
 }
 
-FieldDev field_dev(const qmpm_field& f, uint32_t off, uint16_t idx, uint16_t col) {
+// `off` = the field's first bit; `lead_off` = its group leader's first bit (SHARED_EXP)
+FieldDev field_dev(const qmpm_field& f, uint32_t off, uint16_t idx, uint16_t col, bool lead = false,
+                   uint32_t lead_off = 0, uint16_t lead_idx = 0) {
   FieldDev d{};
+  if (f.kind == QMPM_SHARED_EXP) off += lead ? f.exp_bits : 0u;  // the mantissa follows the exponent
   d.word = (uint8_t)(off / 32);
   d.shift = (uint8_t)(off % 32);
   d.width = (uint8_t)field_width(f);
-  d.kind = f.kind == QMPM_RAW_F32 ? kKindRaw : kKindFixed;
-  if (f.kind == QMPM_FIXED) {
+  d.kind = f.kind == QMPM_RAW_F32 ? kKindRaw : (f.kind == QMPM_SHARED_EXP ? kKindShared : kKindFixed);
+  if (f.kind == QMPM_SHARED_EXP) {
+    d.ebits = f.exp_bits;
+    d.gword = (uint8_t)(lead_off / 32);
+    d.gshift = (uint8_t)(lead_off % 32);
+    d.glead = lead_idx;
+  }
+  if (f.kind == QMPM_FIXED || f.kind == QMPM_SHARED_EXP) {
     d.delta = (float)std::ldexp((double)f.range, -(int)f.frac_bits);             // exact
     d.inv_delta = (float)(std::ldexp(1.0, (int)f.frac_bits) / (double)f.range);  // one rounding (Q3)
     d.offset = f.offset;
@@ -186,7 +223,10 @@ qmpm_status codec_of(qmpm_ctx* ctx, const qmpm_scheme* s, CodecDev& C) {
   C.dither = s->rounding == QMPM_DITHER;
   C.seed_lo = (uint32_t)(s->dither_seed & 0xffffffffu);
   C.seed_hi = (uint32_t)(s->dither_seed >> 32);
-  for (uint32_t i = 0; i < s->n_fields; ++i) C.f[i] = field_dev(s->fields[i], offs[i], (uint16_t)i, (uint16_t)i);
+  for (uint32_t i = 0; i < s->n_fields; ++i) {
+    const uint32_t g = s->fields[i].kind == QMPM_SHARED_EXP ? group_start(s, i) : i;
+    C.f[i] = field_dev(s->fields[i], offs[i], (uint16_t)i, (uint16_t)i, g == i, offs[g], (uint16_t)g);
+  }
   return QMPM_OK;
 }
 
@@ -445,10 +485,14 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   for (uint32_t i = 0; i < scheme->n_fields; ++i) {
     const qmpm_field& f = scheme->fields[i];
     const int s = scalar_of(f.attr, f.comp, d, (int)scheme->material);
-    L.s[s] = field_dev(f, offs[i], (uint16_t)i, (uint16_t)s);
-    C.f[i] = field_dev(f, offs[i], (uint16_t)i, (uint16_t)s);
+    const uint32_t g = f.kind == QMPM_SHARED_EXP ? group_start(scheme, i) : i;
+    const qmpm_field& fg = scheme->fields[g];
+    const int sg = scalar_of(fg.attr, fg.comp, d, (int)scheme->material);
+    // the MPM layout indexes by state scalar: its group leader is the leader's scalar
+    L.s[s] = field_dev(f, offs[i], (uint16_t)i, (uint16_t)s, g == i, offs[g], (uint16_t)sg);
+    C.f[i] = field_dev(f, offs[i], (uint16_t)i, (uint16_t)s, g == i, offs[g], (uint16_t)g);
     if (f.attr == QMPM_X) {
-      const uint32_t w0 = offs[i] / 32, w1 = (offs[i] + field_width(f) - 1) / 32;
+      const uint32_t w0 = offs[i] / 32, w1 = (offs[i] + field_width_in(scheme, i) - 1) / 32;
       for (uint32_t w = w0; w <= w1; ++w) L.xword_mask |= 1u << w;
     }
   }

@@ -113,14 +113,21 @@ __device__ __forceinline__ void encode_record(const float* v, uint32_t h, bool v
   for (int q = 0; q <= W; ++q) w[q] = 0u;
   if (SP::COUNTERS) {
     const int lane = threadIdx.x & 31;
+    EncFlags fl[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-      EncFlags fl;
+      if (SP::kind(f) == kKindShared) {  // reading Q4: the whole group at its leader
+        if (SP::glead(f) == f) senc_group<SP>(f, v, h, w, fl);
+        continue;
+      }
       const uint32_t r24 = (SP::DITHER && SP::kind(f) == kKindFixed) ? r24_of(h, SP::idx(f)) : 0u;
-      sput<SP>(w, f, senc<SP>(f, v[f], r24, fl));
-      const unsigned bs = __ballot_sync(kCFull, valid && fl.sat);
-      const unsigned bu = __ballot_sync(kCFull, valid && fl.up);
-      const unsigned bd = __ballot_sync(kCFull, valid && fl.down);
+      sput<SP>(w, f, senc<SP>(f, v[f], r24, fl[f]));
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const unsigned bs = __ballot_sync(kCFull, valid && fl[f].sat);
+      const unsigned bu = __ballot_sync(kCFull, valid && fl[f].up);
+      const unsigned bd = __ballot_sync(kCFull, valid && fl[f].down);
       if (lane == 0) {
         if (bs) atomicAdd(&counters[SP::idx(f)], (unsigned long long)__popc(bs));
         if (bu) atomicAdd(&counters[64 + SP::idx(f)], (unsigned long long)__popc(bu));
@@ -132,6 +139,16 @@ __device__ __forceinline__ void encode_record(const float* v, uint32_t h, bool v
   bool flag = false;
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
+    if (SP::kind(f) == kKindShared) {
+      if (SP::glead(f) == f) {
+        EncFlags gfl[NF];
+        senc_group<SP>(f, v, h, w, gfl);
+#pragma unroll
+        for (int j = 0; j < NF; ++j)
+          if (SP::kind(j) == kKindShared && SP::glead(j) == f) flag |= gfl[j].sat || gfl[j].nonfinite;
+      }
+      continue;
+    }
     const uint32_t r24 = (SP::DITHER && SP::kind(f) == kKindFixed) ? r24_of(h, SP::idx(f)) : 0u;
     bool up, nz;
     sput<SP>(w, f, senc_fast<SP>(f, v[f], r24, up, nz, flag));
@@ -139,11 +156,15 @@ __device__ __forceinline__ void encode_record(const float* v, uint32_t h, bool v
   if (__any_sync(kCFull, valid && flag)) {  // rare: the exact saturating rule
 #pragma unroll
     for (int q = 0; q <= W; ++q) w[q] = 0u;
+    EncFlags fl[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-      EncFlags fl;
+      if (SP::kind(f) == kKindShared) {
+        if (SP::glead(f) == f) senc_group<SP>(f, v, h, w, fl);
+        continue;
+      }
       const uint32_t r24 = (SP::DITHER && SP::kind(f) == kKindFixed) ? r24_of(h, SP::idx(f)) : 0u;
-      sput<SP>(w, f, senc<SP>(f, v[f], r24, fl));
+      sput<SP>(w, f, senc<SP>(f, v[f], r24, fl[f]));
     }
   }
 }

@@ -145,10 +145,14 @@ std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps
   ints("width", [](const FieldDev& f) { return (int)f.width; });
   ints("kind", [](const FieldDev& f) { return (int)f.kind; });
   ints("idx", [](const FieldDev& f) { return (int)f.idx; });
+  ints("ebits", [](const FieldDev& f) { return (int)f.ebits; });
+  ints("gword", [](const FieldDev& f) { return (int)f.gword; });
+  ints("gshift", [](const FieldDev& f) { return (int)f.gshift; });
+  ints("glead", [](const FieldDev& f) { return f.kind == kKindShared ? (int)f.glead : -1; });
   floats("delta", [](const FieldDev& f) { return f.delta; });
   floats("inv_delta", [](const FieldDev& f) { return f.inv_delta; });
   floats("offset", [](const FieldDev& f) { return f.offset; });
-  s += "};\n#include \"step_kernels.cuh\"\n";
+  s += "  static constexpr int NSPEC = NS;\n};\n#include \"step_kernels.cuh\"\n";
   return s;
 }
 
@@ -291,10 +295,14 @@ std::string codec_spec_source(const CodecDev& C, bool dither, bool counters, int
   ints("kind", [](const FieldDev& f) { return (int)f.kind; });
   ints("idx", [](const FieldDev& f) { return (int)f.idx; });
   ints("col", [](const FieldDev& f) { return (int)f.col; });
+  ints("ebits", [](const FieldDev& f) { return (int)f.ebits; });
+  ints("gword", [](const FieldDev& f) { return (int)f.gword; });
+  ints("gshift", [](const FieldDev& f) { return (int)f.gshift; });
+  ints("glead", [](const FieldDev& f) { return f.kind == kKindShared ? (int)f.glead : -1; });
   floats("delta", [](const FieldDev& f) { return f.delta; });
   floats("inv_delta", [](const FieldDev& f) { return f.inv_delta; });
   floats("offset", [](const FieldDev& f) { return f.offset; });
-  s += "};\n#include \"codec_kernels.cuh\"\n";
+  s += "  static constexpr int NSPEC = NF;\n};\n#include \"codec_kernels.cuh\"\n";
   return s;
 }
 

@@ -25,13 +25,17 @@ constexpr int kMaxScalars = 24;   // 3D elastic: x3 v3 F9 C9
 constexpr int kMaxFields = 64;
 constexpr int kKindFixed = 0;
 constexpr int kKindRaw = 1;
+constexpr int kKindShared = 2;  // SHARED_EXP member (reading Q4)
 
 // One field as the kernels see it.  `idx` is the packing index (RNG stream and
 // counters); `col` is the column of the field's value in a vals row.
 struct FieldDev {
-  uint8_t word, shift, width, kind;
-  float delta, inv_delta, offset;
+  uint8_t word, shift, width, kind;   // SHARED_EXP: word/shift/width of the mantissa
+  float delta, inv_delta, offset;     // SHARED_EXP: Delta_0 = R_min 2^-b and its inverse
   uint16_t idx, col;
+  uint8_t ebits, gword, gshift, pad;  // SHARED_EXP: exponent width and position
+  uint16_t glead, pad2;               // SHARED_EXP: the group leader (packing index; the MPM
+                                      // layout re-maps it to the leader's state scalar)
 };
 
 // Layout for the MPM kernels: fields indexed by STATE SCALAR (x.., v.., F../J, C..).

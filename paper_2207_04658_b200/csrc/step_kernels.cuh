@@ -469,7 +469,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
                                          const uint32_t* __restrict__ active_list, DevCounters* __restrict__ dc,
                                          const uint32_t* __restrict__ block_slot, const float4* __restrict__ gv,
                                          const SimDev& S, uint32_t salt) {
-  constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, WARPS = SP::G2P_WARPS, W = SP::W;
+  constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, W = SP::W;
   constexpr int CO = 2 * D + (MAT == 1 ? 1 : D * D);
   using G = Geo<D>;
   using SM = Smem<SP>;
@@ -693,7 +693,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       // down), so the round counters need no per-field lane predicate.
       if (cnt < 32u && !valid) {
 #pragma unroll
-        for (int i = 0; i < NSV; ++i) o[i] = SP::kind(i) == kKindFixed ? SP::offset(i) : 0.0f;
+        for (int i = 0; i < NSV; ++i) o[i] = SP::kind(i) == kKindFixed ? SP::offset(i) : 0.0f;  // (shared: 0)
       }
       uint32_t ow[W + 1];
 #pragma unroll
@@ -701,6 +701,22 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       bool flag = false;
 #pragma unroll
       for (int i = 0; i < NSV; ++i) {
+        if (SP::kind(i) == kKindShared) {  // reading Q4: the whole group at its leader
+          if (SP::glead(i) == i) {
+            EncFlags gfl[NSV];
+            senc_group<SP>(i, o, h, ow, gfl);
+#pragma unroll
+            for (int j = 0; j < NSV; ++j) {
+              if (SP::kind(j) != kKindShared || SP::glead(j) != i) continue;
+              flag |= gfl[j].sat || gfl[j].nonfinite;
+              if (SP::COUNTERS) {
+                if (gfl[j].up) rc.pu[j / 4] += 1u << (8 * (j % 4));
+                if (SP::DITHER ? (gfl[j].up || gfl[j].down) : gfl[j].down) rc.pz[j / 4] += 1u << (8 * (j % 4));
+              }
+            }
+          }
+          continue;
+        }
         const uint32_t r24 = (SP::DITHER && SP::kind(i) == kKindFixed) ? r24_of(h, SP::idx(i)) : 0u;
         bool up, nz;
         sput<SP>(ow, i, senc_fast<SP>(i, o[i], r24, up, nz, flag));
@@ -712,13 +728,20 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       if (__any_sync(FULL, valid && flag)) {  // rare: exact re-encode with saturation / non-finite
 #pragma unroll
         for (int q = 0; q <= W; ++q) ow[q] = 0u;
+        EncFlags fl[NSV];
 #pragma unroll
         for (int i = 0; i < NSV; ++i) {
-          EncFlags fl;
+          if (SP::kind(i) == kKindShared) {
+            if (SP::glead(i) == i) senc_group<SP>(i, o, h, ow, fl);
+            continue;
+          }
           const uint32_t r24 = (SP::DITHER && SP::kind(i) == kKindFixed) ? r24_of(h, SP::idx(i)) : 0u;
-          sput<SP>(ow, i, senc<SP>(i, o[i], r24, fl));
-          const unsigned bs = __ballot_sync(FULL, valid && fl.sat);
-          const unsigned bn = __ballot_sync(FULL, valid && fl.nonfinite);
+          sput<SP>(ow, i, senc<SP>(i, o[i], r24, fl[i]));
+        }
+#pragma unroll
+        for (int i = 0; i < NSV; ++i) {
+          const unsigned bs = __ballot_sync(FULL, valid && fl[i].sat);
+          const unsigned bn = __ballot_sync(FULL, valid && fl[i].nonfinite);
           if (lane == i) c_sat += __popc(bs);
           if (lane == 0) c_nf += __popc(bn);
         }

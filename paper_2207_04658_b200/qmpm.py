@@ -159,6 +159,8 @@ class CScheme:
             F.frac_bits = f.get("frac_bits", 0)
             F.range = f.get("range", 1.0)
             F.offset = f.get("offset", 0.0)
+            F.exp_bits = f.get("exp_bits", 0)
+            F.group = f.get("group", 0)
         self.s = Scheme()
         self.s.dim = scheme.get("dim", 3) or 3
         self.s.material = MATERIAL[scheme.get("material", "elastic")]

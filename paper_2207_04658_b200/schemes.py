@@ -91,10 +91,24 @@ def from_solution(dim, material, ranges, bits, rounding="dither"):
     return dict(dim=dim, material=material, rounding=rounding, seed=DITHER_SEED, fields=f)
 
 
+def se2():
+    """A SHARED_EXP stand-in (reading Q4) for the 3D fluid: x 3x19 fixed; v one group of
+    3 mantissas (b = 11) sharing a 4-bit exponent from R_min = 2^-4; J 1x16 fixed
+    (offset 1); C one group of 9 mantissas (b = 11) sharing a 5-bit exponent from
+    R_min = 2^-3 -> 57 + 4 + 36 + 16 + 5 + 108 = 226 bits, W = 8."""
+    f = _fields("x", 3, "fixed", 18, 1.0)
+    f += [dict(attr="v", comp=c, kind="shared_exp", frac_bits=11, exp_bits=4, range=2.0 ** -4, offset=0.0,
+               group=1) for c in range(3)]
+    f += _fields("J", 1, "fixed", 15, 0.25, 1.0)
+    f += [dict(attr="C", comp=c, kind="shared_exp", frac_bits=11, exp_bits=5, range=2.0 ** -3, offset=0.0,
+               group=2) for c in range(9)]
+    return dict(dim=3, material="fluid", rounding="dither", seed=DITHER_SEED, fields=f)
+
+
 def with_rounding(scheme, rounding):
     s = dict(scheme)
     s["rounding"] = rounding
     return s
 
 
-BY_NAME = {"x16": x16, "e0.1": e01, "e0.01": e001, "f2": f2}
+BY_NAME = {"x16": x16, "e0.1": e01, "e0.01": e001, "f2": f2, "se2": se2}

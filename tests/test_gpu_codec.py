@@ -27,6 +27,8 @@ def random_vals(scheme, n, rng, oversat=0.02):
         v[m] *= 3.0  # saturating values
         if f["kind"] == "raw":
             v = rng.normal(0, 10, n)
+        if f["kind"] == "shared_exp":  # magnitudes across the group's exponent range (and beyond)
+            v = rng.uniform(-1, 1, n) * R * 2.0 ** rng.uniform(-3, 2 ** f["exp_bits"] + 1, n)
         cols.append(v)
     return np.stack(cols, 1).astype(np.float32)
 
@@ -44,15 +46,41 @@ def mixed_scheme(rng, nf=23):
     return dict(dim=3, material="elastic", rounding="dither", seed=int(rng.integers(0, 2 ** 63)), fields=fields)
 
 
+def mixed_shared_scheme(rng, nf=24):
+    """Fixed / raw fields interleaved with SHARED_EXP groups of 1..9 members (reading Q4),
+    random mantissa widths and exponent widths, groups adjacent to each other too."""
+    fields, g = [], 0
+    while len(fields) < nf:
+        r = rng.random()
+        if r < 0.5:
+            k, b, e = int(rng.integers(1, 10)), int(rng.integers(1, 20)), int(rng.integers(1, 7))
+            R = float(2.0 ** rng.integers(-8, 4))
+            g += 1
+            fields += [dict(kind="shared_exp", frac_bits=b, exp_bits=e, range=R, offset=0.0, group=g)
+                       for _ in range(k)]
+        elif r < 0.6:
+            fields.append(dict(kind="raw"))
+        else:
+            fields.append(dict(kind="fixed", frac_bits=int(rng.integers(0, 24)), range=float(2.0 ** rng.integers(-3, 9)),
+                               offset=0.0))
+    fields = fields[:nf]
+    return dict(dim=3, material="elastic", rounding="dither", seed=int(rng.integers(0, 2 ** 63)), fields=fields)
+
+
 SCHEMES = {"x16": schemes.x16(), "e0.1": schemes.e01(), "e0.01": schemes.e001(), "f2": schemes.f2(),
-           "fp32": schemes.fp32(3)}
+           "fp32": schemes.fp32(3), "se2": schemes.se2()}
 
 
-@pytest.mark.parametrize("name", list(SCHEMES) + ["mixed0", "mixed1", "mixed2"])
+@pytest.mark.parametrize("name", list(SCHEMES) + ["mixed0", "mixed1", "mixed2", "mixed_se0", "mixed_se1", "mixed_se2"])
 @pytest.mark.parametrize("dithered", [False, True])
 def test_encode_decode_bit_exact(name, dithered):
-    rng = np.random.default_rng(hash(name) % 1000 + dithered)
-    sch = SCHEMES[name] if name in SCHEMES else mixed_scheme(rng)
+    rng = np.random.default_rng(sum(map(ord, name)) + dithered)
+    if name in SCHEMES:
+        sch = SCHEMES[name]
+    elif name.startswith("mixed_se"):
+        sch = mixed_shared_scheme(rng)
+    else:
+        sch = mixed_scheme(rng)
     n = 100_003  # ragged tail
     vals = random_vals(sch, n, rng)
     vals[rng.integers(0, n, 20), rng.integers(0, vals.shape[1], 20)] = np.nan
@@ -103,7 +131,7 @@ def test_exhaustive_codes(b):
     assert np.array_equal(w2.cpu().numpy().view(np.uint32), words)
 
 
-@pytest.mark.parametrize("name", ["x16", "e0.1", "f2"])
+@pytest.mark.parametrize("name", ["x16", "e0.1", "f2", "se2"])
 def test_set_state_read_state_bit_exact(name):
     """qmpm_set_state encodes with RNE at step 0 (reading Q20), bit-exact to the oracle;
     qmpm_read_state returns the oracle's decode."""

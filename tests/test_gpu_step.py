@@ -86,6 +86,7 @@ CASES = {
     "s3_3d_e0.01": (scenes.small_elastic_3d, schemes.e001, 20),
     "s3_3d_fp32": (scenes.small_elastic_3d, lambda: schemes.fp32(3), 20),
     "s4_3d_fluid_f2": (scenes.small_fluid_3d, schemes.f2, 20),
+    "s4_3d_fluid_se2": (scenes.small_fluid_3d, schemes.se2, 20),
 }
 
 
@@ -149,7 +150,8 @@ def aggregates(sim, st):
     return oracle.aggregates(sim, st)
 
 
-@pytest.mark.parametrize("case,steps", [("c1_2d_x16", 100), ("s3_3d_e0.1", 100), ("s4_3d_fluid_f2", 100)])
+@pytest.mark.parametrize("case,steps", [("c1_2d_x16", 100), ("s3_3d_e0.1", 100), ("s4_3d_fluid_f2", 100),
+                                        ("s4_3d_fluid_se2", 100)])
 def test_100_step_aggregates(case, steps):
     """P3: KE and COM after 100 steps within 1e-3 relative (GPU vs fp64 oracle)."""
     mk_scene, mk_scheme, _ = CASES[case]
