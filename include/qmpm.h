@@ -51,7 +51,15 @@ enum {
 /* Field kinds.  FIXED: Eq. 3, u = round(v/Delta) stored as frac_bits+1-bit
  * two's complement (reading Q2), Delta = range * 2^-frac_bits, value =
  * offset + u*Delta (offset: reading Q21).  RAW_F32: the IEEE bits (32 bits).
- * SHARED_EXP is reserved (reading Q4) and rejected with QMPM_ELAYOUT. */
+ * SHARED_EXP (reading Q4): a group -- a maximal run of consecutive SHARED_EXP fields
+ * with equal `group` ids -- shares one unsigned exp_bits-bit exponent E, stored in
+ * front of the group's first mantissa; each member is a frac_bits+1-bit two's
+ * complement mantissa u with value u * range * 2^(E - frac_bits) (range = R_min, a
+ * power of two).  The encoder picks the smallest E in [0, 2^exp_bits - 1] with
+ * max |v| < R_min 2^E, raises it once if a member's rounding overflows, and
+ * saturates at the top.  Members share frac_bits (<= 23), exp_bits (1..8), range;
+ * offset must be 0.  The paper's types are fixed-point; the shared exponent
+ * is the north star's "shared-exponent fields". */
 enum { QMPM_FIXED = 0, QMPM_RAW_F32 = 1, QMPM_SHARED_EXP = 2 };
 /* Attributes of a particle: position, velocity, deformation
  * gradient (elastic), its determinant J (fluid), affine velocity C. */
@@ -75,11 +83,11 @@ enum {
 typedef struct {
     uint8_t attr;      /* QMPM_X .. QMPM_J */
     uint8_t comp;      /* component: 0..d-1 for x, v; row-major 0..d*d-1 for F, C; 0 for J */
-    uint8_t kind;      /* QMPM_FIXED | QMPM_RAW_F32 */
+    uint8_t kind;      /* QMPM_FIXED | QMPM_RAW_F32 | QMPM_SHARED_EXP */
     uint8_t frac_bits; /* b; FIXED width = b+1 in [1, 32] */
     float range;       /* R > 0 (FIXED) */
     float offset;      /* value = offset + u*Delta (FIXED) */
-    uint8_t exp_bits, group, pad[2]; /* reserved for SHARED_EXP */
+    uint8_t exp_bits, group, pad[2]; /* SHARED_EXP: exponent width (1..8) and group id */
 } qmpm_field;
 
 /* A quantization scheme {(b_h, R_h)} (Alg. 1 output) plus packing order. */
