@@ -119,11 +119,11 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 // are independent, so there is no CTA barrier and no tail).  The global counting sort
 // orders particles by (block, base cell) and its cursors leave each cell's start in
 // cell_count, so the block's 64 cell ranges are known without a local sort.
-//   1. segment table: cell c is cut into ceil(n_c / L) segments (at most kSegLev;
-//      the last takes the rest), listed level-major (all first segments in cell order,
-//      then all second segments, ...); group g = entries [32 g, 32 g + 32), one segment
-//      per lane: lanes get near-equal work whatever the cells' occupancy (remainders
-//      cluster in the late levels);
+//   1. segment table: cell c is cut into full segments of L particles (listed
+//      level-major: all first segments in cell order, then all second segments, ...)
+//      and one tail segment (the tails sorted by length); group g = entries
+//      [32 g, 32 g + 32), one segment per lane: lanes get near-equal work whatever the
+//      cells' occupancy;
 //   2. a lane walks its segment: records stream through a per-lane 3-slot cp.async ring
 //      (two in flight), decode, stress and affine momentum, and it accumulates all 3^d
 //      stencil nodes x (m, p) in REGISTERS -- no shared-memory traffic per particle;
@@ -200,17 +200,24 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     s_start[lane + 32] = st1;
     if (lane == 0) s_start[64] = end - start;
     __syncwarp();
-    // ---- 1. segment table (lane handles cells lane and lane + 32)
+    // ---- 1. segment table (lane handles cells lane and lane + 32).  Cell c has
+    // nf_c = min(n_c / L, kSegLev - 1) FULL segments of L particles and, if anything is
+    // left, one TAIL segment.  Full segments come first, level-major (all first
+    // segments in cell order, then all second segments, ...): those groups run exactly
+    // L iterations.  Tails follow, sorted by length (longest first, then cell order),
+    // so each tail group's lanes have similar lengths.  A cell appears at most once per
+    // level and once among the tails, so only the group straddling two sections can
+    // hold a cell twice (the flush serialises those lanes).
     const uint32_t nc0 = s_start[lane + 1] - st0, nc1 = s_start[lane + 33] - st1;
     const uint32_t L = min((uint32_t)kSegL, max((uint32_t)kSegLmin, (end - start + 127) / 128));
-    const uint32_t ns0 = min((nc0 + L - 1) / L, (uint32_t)kSegLev);
-    const uint32_t ns1 = min((nc1 + L - 1) / L, (uint32_t)kSegLev);
-    s_ns[lane] = (uint8_t)ns0;
-    s_ns[lane + 32] = (uint8_t)ns1;
-    const uint32_t nlev = __reduce_max_sync(FULL, max(ns0, ns1));
+    const uint32_t nf0 = min(nc0 / L, (uint32_t)kSegLev - 1u), nf1 = min(nc1 / L, (uint32_t)kSegLev - 1u);
+    const uint32_t tl0 = nc0 - nf0 * L, tl1 = nc1 - nf1 * L;  // tail lengths (0: none)
+    s_ns[lane] = (uint8_t)nf0;
+    s_ns[lane + 32] = (uint8_t)nf1;
+    const uint32_t nlev = __reduce_max_sync(FULL, max(nf0, nf1));
     uint32_t sz = 0;  // lane l: size of level l
     for (uint32_t l = 0; l < nlev; ++l) {
-      const unsigned m0 = __ballot_sync(FULL, ns0 > l), m1 = __ballot_sync(FULL, ns1 > l);
+      const unsigned m0 = __ballot_sync(FULL, nf0 > l), m1 = __ballot_sync(FULL, nf1 > l);
       if ((uint32_t)lane == l) sz = __popc(m0) + __popc(m1);
     }
     uint32_t inc = sz;
@@ -220,25 +227,39 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
       if (lane >= d) inc += t;
     }
     s_lstart[lane] = inc - sz;
-    const uint32_t nseg = __shfl_sync(FULL, inc, 31);
+    const uint32_t nfull = __shfl_sync(FULL, inc, 31);
     __syncwarp();
     for (uint32_t l = 0; l < nlev; ++l) {
-      const unsigned m0 = __ballot_sync(FULL, ns0 > l), m1 = __ballot_sync(FULL, ns1 > l);
+      const unsigned m0 = __ballot_sync(FULL, nf0 > l), m1 = __ballot_sync(FULL, nf1 > l);
       const uint32_t ls = s_lstart[l];
-      if (ns0 > l) s_seg[ls + __popc(m0 & lanemask_lt())] = (uint16_t)((lane << 8) | l);
-      if (ns1 > l) s_seg[ls + __popc(m0) + __popc(m1 & lanemask_lt())] = (uint16_t)(((lane + 32) << 8) | l);
+      if (nf0 > l) s_seg[ls + __popc(m0 & lanemask_lt())] = (uint16_t)((lane << 8) | l);
+      if (nf1 > l) s_seg[ls + __popc(m0) + __popc(m1 & lanemask_lt())] = (uint16_t)(((lane + 32) << 8) | l);
+    }
+    uint32_t nseg = nfull;
+    {  // tails, by key = min(length, L) descending, ties in cell order
+      const uint32_t k0 = min(tl0, L), k1 = min(tl1, L);
+      uint32_t above = 0;
+      for (uint32_t v = L; v >= 1u; --v) {
+        const unsigned b0 = __ballot_sync(FULL, k0 == v), b1 = __ballot_sync(FULL, k1 == v);
+        if (k0 == v) s_seg[nfull + above + __popc(b0 & lanemask_lt())] = (uint16_t)((lane << 8) | nf0);
+        if (k1 == v)
+          s_seg[nfull + above + __popc(b0) + __popc(b1 & lanemask_lt())] = (uint16_t)(((lane + 32) << 8) | nf1);
+        above += __popc(b0) + __popc(b1);
+      }
+      nseg += above;
     }
     __syncwarp();
     const uint32_t ngroups = (nseg + 31) / 32;
     const uint32_t* pidx = perm + start;  // the block's record indices in (cell) order
-    // particle range [k, e) of segment entry i (empty past the table)
+    // particle range [k, e) of segment entry i (empty past the table): level l < nf_c is
+    // a full segment, l == nf_c the tail
     auto seg_range = [&](uint32_t i, uint32_t& k, uint32_t& e, int& c) {
       if (i < nseg) {
         const uint32_t v = s_seg[i];
         c = (int)(v >> 8);
         const uint32_t l = v & 255u;
         k = s_start[c] + l * L;
-        e = (l + 1 == (uint32_t)s_ns[c]) ? s_start[c + 1] : k + L;
+        e = (l == (uint32_t)s_ns[c]) ? s_start[c + 1] : k + L;
       } else {
         k = e = 0u;
         c = 0;
