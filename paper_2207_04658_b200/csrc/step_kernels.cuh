@@ -53,7 +53,6 @@ template <class SP>
 struct Smem {
   static constexpr int TN = Geo<SP::D>::TN;
   static constexpr int TILE = 16 * TN;
-  static constexpr int STAGE = ((4 * 32 * SP::SW) + 15) / 16 * 16;
   // velocity tile + 8 neighbour slots + double-buffered record stage
   static constexpr int G2P_WARP = TILE + 32 + (2 * 32 * 4 * SP::W + 15) / 16 * 16;
 };
