@@ -1,0 +1,75 @@
+"""Per-step overhead of the slab decomposition, measured on ONE GPU with the in-process
+group transport (qmpm_step_group): the C4 scene (n particles) as one context vs k z slabs
+stepping together.  The slab path adds a second sort pass, the migration packing and
+recount, the ghost/velocity plane packs and two host synchronisations per step; with k
+slabs on one GPU their kernels run back to back, so (t_k - t_1) / k estimates the
+per-rank overhead of an N-GPU weak-scaling step.
+
+    python tools/slab_overhead.py [--n 200000000] [--k 2] [--steps 10]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=200_000_000)
+    ap.add_argument("--k", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warm", type=int, default=20)
+    args = ap.parse_args()
+    import torch
+    from paper_2207_04658_b200 import dist as qdist
+    from paper_2207_04658_b200 import qmpm, scenes, schemes
+    torch.cuda.set_device(0)
+    sc, sch = scenes.c4(n_target=args.n), schemes.f2()
+    stream = torch.cuda.Stream()
+    out = {"n": sc.n_particles, "k": args.k}
+    with torch.cuda.stream(stream):
+        sim = qmpm.Sim(sc.sim, sch, sc.n_particles, stream=stream)
+        chunk = 1 << 24
+        for s0 in range(0, sc.n_particles, chunk):
+            st = sc.state_chunk(s0, min(chunk, sc.n_particles - s0), backend="torch", device="cuda")
+            (sim.set_state if s0 == 0 else sim.append_state)(st)
+            stream.synchronize()
+        sim.step(args.warm)
+        stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sim.step(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+        out["single_ms"] = e0.elapsed_time(e1) / args.steps
+        sim.close()
+        torch.cuda.empty_cache()
+        cuts = qdist.slab_cuts(sc.sim["grid_res"][2], args.k)
+        per = sc.n_particles // args.k
+        sims = []
+        for r in range(args.k):
+            s = qmpm.Sim(sc.sim, sch, int(per * 1.25) + 65536, stream=stream, slab=(args.k, r, cuts[r][0], cuts[r][1]))
+            qdist.load_slab(s, sc, cuts, r, track_ids=False)
+            sims.append(s)
+        qmpm.step_group(sims, args.warm)
+        stream.synchronize()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        qmpm.step_group(sims, args.steps)
+        e1.record(stream)
+        e1.synchronize()
+        out["group_ms"] = e0.elapsed_time(e1) / args.steps
+        out["group_wall_ms"] = (time.perf_counter() - t0) * 1e3 / args.steps
+        out["overhead_per_slab_ms"] = (out["group_ms"] - out["single_ms"]) / args.k
+        out["n_per_slab"] = [s.stats().n_particles for s in sims]
+        for s in sims:
+            s.close()
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
