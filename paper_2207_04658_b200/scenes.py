@@ -315,3 +315,51 @@ def small_fluid_3d(seed=0, res=64, n_target=60_000):
 
 
 BY_NAME = {"c1": c1, "c2": c2, "c3": c3, "c4": c4}
+
+
+# ---------------------------------------------------------------- smoke (f4)
+SMOKE_VOXELS = 228_982_784  # the paper's large smoke run (T-large)
+
+
+def smoke(res=(64, 64, 64), seed=0, dt=0.01, buoyancy=1.0, amp=0.5, modes=4, rho_blobs=4, p_amp=0.0,
+          jacobi_iters=64):
+    """A seeded smoke scene on a collocated grid (DESIGN.md §12 input recipe): dx = 1/ny
+    (unit-height box), a smooth random velocity field (sum of `modes` random Fourier modes
+    per component, max |u| <= amp), density blobs in [0, 1], pressure p_amp-scaled modes
+    (0: the usual zero warm start), a source box at the bottom centre.  dt 0.01.
+    Returns (params dict, u [nx,ny,nz,3] f32, p [nx,ny,nz] f32, rho [nx,ny,nz] f32)."""
+    nx, ny, nz = res
+    rng = np.random.default_rng(seed)
+    x = [np.arange(n, dtype=np.float64) / n for n in res]
+    X, Y, Z = np.meshgrid(*x, indexing="ij")
+
+    def field(a):
+        f = np.zeros(res)
+        for _ in range(modes):
+            k = rng.integers(1, 4, size=3)
+            ph = rng.uniform(0, 2 * np.pi, size=3)
+            f += rng.uniform(-1, 1) * np.sin(2 * np.pi * k[0] * X + ph[0]) * np.sin(2 * np.pi * k[1] * Y + ph[1]) \
+                * np.sin(2 * np.pi * k[2] * Z + ph[2])
+        m = np.abs(f).max()
+        return (a * f / m if m > 0 else f).astype(np.float32)
+
+    u = np.stack([field(amp) for _ in range(3)], -1) if amp > 0 else np.zeros(res + (3,), np.float32)
+    p = field(p_amp) if p_amp > 0 else np.zeros(res, np.float32)
+    rho = np.zeros(res)
+    for _ in range(rho_blobs):
+        c = rng.uniform(0.2, 0.8, size=3)
+        r = rng.uniform(0.05, 0.2)
+        rho += np.exp(-((X - c[0]) ** 2 + (Y - c[1]) ** 2 + (Z - c[2]) ** 2) / (r * r))
+    rho = np.clip(rho, 0, 1).astype(np.float32)
+    lo = (nx * 3 // 8, 1, nz * 3 // 8)
+    hi = (max(lo[0] + 1, nx * 5 // 8), max(2, ny // 16 + 1), max(lo[2] + 1, nz * 5 // 8))
+    params = dict(res=tuple(res), dx=1.0 / ny, dt=dt, buoyancy=buoyancy, source_lo=lo, source_hi=hi,
+                  jacobi_iters=jacobi_iters)
+    return params, u.astype(np.float32), p, rho
+
+
+def smoke_plume(res, dt=0.01, buoyancy=1.0, jacobi_iters=64):
+    """The large-scale bench scene: everything at rest, zero density, the source box at the
+    bottom centre (the plume rises by buoyancy)."""
+    params, u, p, rho = smoke(res=res, amp=0.0, rho_blobs=0, dt=dt, buoyancy=buoyancy, jacobi_iters=jacobi_iters)
+    return params
