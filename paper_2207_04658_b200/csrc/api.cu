@@ -365,6 +365,11 @@ qmpm_status encode_rows(qmpm_ctx* ctx, uint64_t first, uint64_t n, const float* 
 
 }  // namespace
 
+namespace qmpm {
+// the scheme -> CodecDev translation of the standalone codec, for smoke.cu
+qmpm_status codec_dev_of(const qmpm_scheme* s, CodecDev& C) { return codec_of(nullptr, s, C); }
+}  // namespace qmpm
+
 extern "C" {
 
 int qmpm_abi_version(void) { return QMPM_ABI_VERSION; }

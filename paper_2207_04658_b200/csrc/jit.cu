@@ -23,7 +23,7 @@
 
 namespace qmpm {
 
-#include "jit_sources.inc"  // kSrcDevice, kSrcCommon, kSrcField, kSrcStep, kSrcCodec (build.py)
+#include "jit_sources.inc"  // kSrc* (build.py JIT_HEADERS)
 
 namespace {
 
@@ -175,10 +175,10 @@ cudaError_t compile_module(const std::string& src, const char* prog_name, CUmodu
   if (!init_driver(err) || !init_nvrtc(err)) return cudaErrorNotSupported;
   cudaFree(nullptr);  // make sure the primary context is current
   nvrtcProgram prog;
-  const char* hdrs[] = {kSrcDevice, kSrcCommon, kSrcField, kSrcStep, kSrcCodec};
-  const char* names[] = {"qmpm_device.cuh", "mpm_common.cuh", "field_codec.cuh", "step_kernels.cuh",
-                         "codec_kernels.cuh"};
-  nvrtcResult r = g_rtc.create(&prog, src.c_str(), prog_name, 5, hdrs, names);
+  const char* hdrs[] = {kSrcDevice, kSrcCommon, kSrcField, kSrcStep, kSrcRecord, kSrcCodec, kSrcSmoke};
+  const char* names[] = {"qmpm_device.cuh",  "mpm_common.cuh",    "field_codec.cuh",  "step_kernels.cuh",
+                         "codec_record.cuh", "codec_kernels.cuh", "smoke_kernels.cuh"};
+  nvrtcResult r = g_rtc.create(&prog, src.c_str(), prog_name, 7, hdrs, names);
   if (r != NVRTC_SUCCESS) {
     err = std::string("nvrtcCreateProgram: ") + g_rtc.errstr(r);
     return cudaErrorInvalidSource;
@@ -262,14 +262,14 @@ cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err) {
   return cudaSuccess;
 }
 
-std::string codec_spec_source(const CodecDev& C, bool dither, bool counters, int wv, int vv) {
+std::string codec_spec_struct(const char* name, const CodecDev& C, bool dither, bool counters, int wv, int vv) {
   std::string s;
   char buf[512];
   const int nf = (int)C.nf;
   snprintf(buf, sizeof(buf),
-           "struct Spec {\n  static constexpr int NF = %d, W = %u, STRIDE = %u, WV = %d, VV = %d;\n"
+           "struct %s {\n  static constexpr int NF = %d, W = %u, STRIDE = %u, WV = %d, VV = %d;\n"
            "  static constexpr bool DITHER = %s, COUNTERS = %s;\n",
-           nf, C.W, C.stride, wv, vv, dither ? "true" : "false", counters ? "true" : "false");
+           name, nf, C.W, C.stride, wv, vv, dither ? "true" : "false", counters ? "true" : "false");
   s += buf;
   auto ints = [&](const char* name, auto get) {
     s += "  __host__ __device__ static constexpr int ";
@@ -302,8 +302,34 @@ std::string codec_spec_source(const CodecDev& C, bool dither, bool counters, int
   floats("delta", [](const FieldDev& f) { return f.delta; });
   floats("inv_delta", [](const FieldDev& f) { return f.inv_delta; });
   floats("offset", [](const FieldDev& f) { return f.offset; });
-  s += "  static constexpr int NSPEC = NF;\n};\n#include \"codec_kernels.cuh\"\n";
+  s += "  static constexpr int NSPEC = NF;\n};\n";
   return s;
+}
+
+std::string codec_spec_source(const CodecDev& C, bool dither, bool counters, int wv, int vv) {
+  return codec_spec_struct("Spec", C, dither, counters, wv, vv) + "#include \"codec_kernels.cuh\"\n";
+}
+
+std::string smoke_spec_source(const CodecDev& U, const CodecDev& P, int wvu, int wvp) {
+  return codec_spec_struct("SpecU", U, U.dither != 0, false, wvu, 1) +
+         codec_spec_struct("SpecP", P, P.dither != 0, false, wvp, 1) + "#include \"smoke_kernels.cuh\"\n";
+}
+
+cudaError_t jit_smoke(const std::string& src, SmokeJit& out, std::string& err) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  std::string log;
+  CUmodule mod;
+  cudaError_t e = compile_module(src, "qsmoke_spec.cu", mod, log, err);
+  if (e) return e;
+  if (g_drv.moduleGetFunction(&out.advect_u, mod, "qsmoke_advect_u") != CUDA_SUCCESS ||
+      g_drv.moduleGetFunction(&out.div, mod, "qsmoke_div") != CUDA_SUCCESS ||
+      g_drv.moduleGetFunction(&out.jacobi, mod, "qsmoke_jacobi") != CUDA_SUCCESS ||
+      g_drv.moduleGetFunction(&out.project, mod, "qsmoke_project") != CUDA_SUCCESS ||
+      g_drv.moduleGetFunction(&out.advect_rho, mod, "qsmoke_advect_rho") != CUDA_SUCCESS) {
+    err = "smoke JIT module lacks a kernel";
+    return cudaErrorSymbolNotFound;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t jit_codec(const std::string& src, CodecJit& out, std::string& err) {

@@ -29,6 +29,13 @@ struct CodecJit {
 // wv / vv: vector widths (4, 2, 1) usable for the records / the vals rows
 std::string codec_spec_source(const CodecDev& C, bool dither, bool counters, int wv, int vv);
 cudaError_t jit_codec(const std::string& src, CodecJit& out, std::string& err);
+
+// the quantized smoke step (smoke_kernels.cuh) on a velocity and a pressure layout
+struct SmokeJit {
+  CUfunction advect_u, div, jacobi, project, advect_rho;
+};
+std::string smoke_spec_source(const CodecDev& U, const CodecDev& P, int wvu, int wvp);
+cudaError_t jit_smoke(const std::string& src, SmokeJit& out, std::string& err);
 cudaError_t jit_set_smem(CUfunction f, size_t bytes);
 int jit_occupancy(CUfunction f, int threads, size_t smem);
 cudaError_t jit_launch(CUfunction f, unsigned grid, unsigned block, size_t smem, cudaStream_t st, void** args);

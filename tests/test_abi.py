@@ -12,10 +12,10 @@ from paper_2207_04658_b200 import qmpm, schemes
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    src = open(os.path.join(ROOT, "include", "qmpm.h")).read()
+def declared_symbols(header="qmpm.h", prefix="qmpm_"):
+    src = open(os.path.join(ROOT, "include", header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(qmpm_[a-z0-9_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(" + prefix + r"[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -35,6 +35,36 @@ def test_library_exports_every_declared_symbol():
 
 def test_binding_names_match_header():
     assert sorted(qmpm.EXPORTS) == declared_symbols()
+
+
+def test_smoke_header_symbols_exported_and_bound():
+    from paper_2207_04658_b200 import qsmoke
+    decl = declared_symbols("qsmoke.h", "qsmoke_")
+    assert len(decl) == 12
+    out = subprocess.check_output(["nm", "-D", "--defined-only", qmpm.LIB_PATH], text=True)
+    exported = set(l.split()[-1] for l in out.splitlines() if l.strip())
+    assert not [s for s in decl if s not in exported]
+    assert sorted(qsmoke.EXPORTS) == decl
+    L = qsmoke.lib()
+    for s in decl:
+        assert hasattr(L, s)
+
+
+def test_smoke_create_rejects_bad_params_without_gpu():
+    """Argument validation happens before any device work, so it runs here."""
+    import ctypes
+    from paper_2207_04658_b200 import qsmoke, scenes
+    params, _, _, _ = scenes.smoke(res=(8, 8, 8))
+
+    def create(p, su, sp):
+        cu, cp, pp, ctx = qmpm.CScheme(su), qmpm.CScheme(sp), qsmoke.make_params(p), ctypes.c_void_p()
+        return qsmoke.lib().qsmoke_create(ctypes.byref(pp), cu.ref, cp.ref, None, ctypes.byref(ctx))
+
+    assert create(dict(params, res=(7, 8, 8)), schemes.smoke_u(), schemes.smoke_p()) == 1
+    assert create(dict(params, jacobi_iters=99), schemes.smoke_u(), schemes.smoke_p()) == 1
+    assert create(params, schemes.smoke_p(), schemes.smoke_p()) == 2
+    assert create(params, schemes.smoke_u(), schemes.smoke_u()) == 2
+    assert b"6 fields" in qmpm.lib().qmpm_last_error(None) or b"2 fields" in qmpm.lib().qmpm_last_error(None)
 
 
 @pytest.mark.parametrize("name", ["x16", "e0.1", "e0.01", "f2"])
