@@ -359,6 +359,12 @@ int jit_occupancy(CUfunction f, int threads, size_t smem) {
   return n > 0 ? n : 1;
 }
 
+cudaError_t jit_launch3(CUfunction f, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void** args) {
+  CUresult r = g_drv.launchKernel(f, grid.x, grid.y, grid.z, block.x, block.y, block.z, (unsigned)smem, (CUstream)st,
+                                  args, nullptr);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
+}
+
 cudaError_t jit_launch(CUfunction f, unsigned grid, unsigned block, size_t smem, cudaStream_t st, void** args) {
   CUresult r = g_drv.launchKernel(f, grid, 1, 1, block, 1, 1, (unsigned)smem, (CUstream)st, args, nullptr);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;

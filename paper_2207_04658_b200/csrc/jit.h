@@ -39,5 +39,6 @@ cudaError_t jit_smoke(const std::string& src, SmokeJit& out, std::string& err);
 cudaError_t jit_set_smem(CUfunction f, size_t bytes);
 int jit_occupancy(CUfunction f, int threads, size_t smem);
 cudaError_t jit_launch(CUfunction f, unsigned grid, unsigned block, size_t smem, cudaStream_t st, void** args);
+cudaError_t jit_launch3(CUfunction f, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void** args);
 
 }  // namespace qmpm

@@ -41,7 +41,6 @@ struct qsmoke_ctx {
   SmokeJit k{};
   SmokeDev g{};
   cudaStream_t stream = nullptr, cap = nullptr;
-  int grid = 0;
   uint64_t n_rec = 0, n_cells = 0, launches = 0, step = 0;
   uint32_t *u = nullptr, *ut = nullptr, *uh = nullptr, *up = nullptr, *p[2] = {nullptr, nullptr};
   float *div = nullptr, *rho[2] = {nullptr, nullptr};
@@ -87,36 +86,40 @@ SaltSrc dev_salt(const qsmoke_ctx* c, const CodecDev& C, uint32_t sub) {
   return s;
 }
 
-qmpm_status launch(qsmoke_ctx* c, CUfunction f, cudaStream_t st, void** args, uint64_t items) {
-  const unsigned grid = (unsigned)std::min<uint64_t>((items + 255) / 256, (uint64_t)c->grid);
+// (32 z, 8 y) tiles; blockIdx.z = the x plane of a record (per-record kernels), of a cell
+// (density) or of a march of kXM = 8 record planes (stencil kernels) -- smoke_kernels.cuh
+enum Span { kRecords, kCells, kMarch };
+qmpm_status launch(qsmoke_ctx* c, CUfunction f, cudaStream_t st, void** args, Span span) {
+  const unsigned gz = span == kCells ? c->g.nx : span == kRecords ? c->g.nxr : (c->g.nxr + 7) / 8;
+  const dim3 grid((c->g.nz + 31) / 32, (c->g.ny + 7) / 8, gz);
   c->launches += 1;
-  SCK(jit_launch(f, grid ? grid : 1, 256, 0, st, args));
+  SCK(jit_launch3(f, grid, dim3(32, 8, 1), 0, st, args));
   return QMPM_OK;
 }
 
 qmpm_status advect_u(qsmoke_ctx* c, cudaStream_t st, const uint32_t* uv, const uint32_t* ur, const float* rho,
                      float dt, float bdt, SaltSrc ss, uint32_t* out, float* dbg) {
   void* a[] = {&uv, &ur, &rho, &c->g, &dt, &bdt, &ss, &out, &dbg};
-  return launch(c, c->k.advect_u, st, a, c->n_rec);
+  return launch(c, c->k.advect_u, st, a, kRecords);
 }
 qmpm_status divergence(qsmoke_ctx* c, cudaStream_t st, const uint32_t* u, float* div) {
   void* a[] = {&u, &c->g, &div};
-  return launch(c, c->k.div, st, a, c->n_rec);
+  return launch(c, c->k.div, st, a, kMarch);
 }
 qmpm_status jacobi(qsmoke_ctx* c, cudaStream_t st, const uint32_t* pin, const float* div, SaltSrc ss, uint32_t* pout,
                    float* dbg) {
   void* a[] = {&pin, &div, &c->g, &ss, &pout, &dbg};
-  return launch(c, c->k.jacobi, st, a, c->n_rec);
+  return launch(c, c->k.jacobi, st, a, kMarch);
 }
 qmpm_status project(qsmoke_ctx* c, cudaStream_t st, const uint32_t* u, const uint32_t* p, SaltSrc ss, uint32_t* out,
                     float* dbg) {
   void* a[] = {&u, &p, &c->g, &ss, &out, &dbg};
-  return launch(c, c->k.project, st, a, c->n_rec);
+  return launch(c, c->k.project, st, a, kMarch);
 }
 qmpm_status advect_rho(qsmoke_ctx* c, cudaStream_t st, const float* rin, const uint32_t* u, float dt, float* rout,
                        unsigned long long* tick) {
   void* a[] = {&rin, &u, &c->g, &dt, &rout, &tick};
-  return launch(c, c->k.advect_rho, st, a, c->n_cells);
+  return launch(c, c->k.advect_rho, st, a, kCells);
 }
 
 // one projection (S6-S7) of u_in into u_out; subs: sub0 = the velocity store,
@@ -195,6 +198,7 @@ qmpm_status qsmoke_create(const qsmoke_params* params, const qmpm_scheme* u_sche
     return sfail(QMPM_EINVAL, "res must be nx even >= 2, ny, nz >= 2 (got %d %d %d)", P.res[0], P.res[1], P.res[2]);
   if (!(P.dx > 0.0f) || !(P.dt >= 0.0f)) return sfail(QMPM_EINVAL, "dx must be > 0 and dt >= 0");
   if (P.jacobi_iters < 0 || P.jacobi_iters > 98) return sfail(QMPM_EINVAL, "jacobi_iters must be in 0..98");
+  if (P.res[0] > 65535 || P.res[1] > 65535 * 8) return sfail(QMPM_EINVAL, "res too large for the launch grid");
   if (u_scheme->n_fields != 6) return sfail(QMPM_ELAYOUT, "velocity scheme needs 6 fields (got %u)", u_scheme->n_fields);
   if (p_scheme->n_fields != 2) return sfail(QMPM_ELAYOUT, "pressure scheme needs 2 fields (got %u)", p_scheme->n_fields);
   qsmoke_ctx* c = new qsmoke_ctx();
@@ -228,10 +232,6 @@ qmpm_status qsmoke_create(const qsmoke_params* params, const qmpm_scheme* u_sche
     g.hi[a] = P.source_hi[a];
   }
   g.n_rec = c->n_rec;
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  c->grid = std::max(1, sms) * 8;  // 8 resident 256-thread CTAs per SM
   const size_t bu = sizeof(uint32_t) * c->U.W * c->n_rec, bp = sizeof(uint32_t) * c->Pc.W * c->n_rec,
                bf = sizeof(float) * c->n_cells;
   cudaError_t e = cudaSuccess;

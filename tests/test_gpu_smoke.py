@@ -54,7 +54,7 @@ def make(res, seed=0, su=None, sp=None, iters=4, p_amp=0.05, **kw):
     return params, su, sp, uw, uq, pw, pq[..., 0], rho
 
 
-RES = [(16, 12, 10), (18, 7, 11), (2, 2, 2)]
+RES = [(16, 12, 10), (18, 7, 11), (2, 2, 2), (20, 10, 40)]  # several y and z tiles, ragged x marches
 
 
 @pytest.mark.parametrize("res", RES)
