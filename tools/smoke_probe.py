@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--res", type=int, nargs=3, default=[612, 612, 612])
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--ncu", action="store_true", help="after 4 plume steps (540 launches) run each sub-step kernel once")
     a = ap.parse_args()
     import torch
     from paper_2207_04658_b200 import qsmoke, scenes, schemes
@@ -42,6 +43,21 @@ def main():
         e1.synchronize()
         return e0.elapsed_time(e1) / reps
 
+    if a.ncu:
+        sm.get_state(u, p, rho)
+        u2, p2 = torch.empty_like(u), torch.empty_like(p)
+        div = torch.zeros(tuple(a.res), dtype=torch.float32, device="cuda")
+        rho2 = torch.empty_like(rho)
+        dt = params["dt"]
+        sm.advect_velocity(u, u2, 0.5 * dt, rho=rho, bdt=0.005, dstep=1)
+        sm.advect_velocity(u, u2, 0.5 * dt, u_refl=u, dstep=1)
+        sm.divergence(u, div)
+        sm.jacobi(p, div, p2, dstep=2)
+        sm.project(u, p, u2, dstep=3)
+        sm.advect_density(rho, u, rho2, dt)
+        torch.cuda.synchronize()
+        print("ncu pass done", flush=True)
+        return
     out = {"res": a.res, "records": n, "Wu": sm.Wu, "Wp": sm.Wp}
     out["step_ms"] = timed(lambda: sm.step(1), a.steps)
     sm.get_state(u, p, rho)
