@@ -322,6 +322,7 @@ cudaError_t jit_smoke(const std::string& src, SmokeJit& out, std::string& err) {
   cudaError_t e = compile_module(src, "qsmoke_spec.cu", mod, log, err);
   if (e) return e;
   if (g_drv.moduleGetFunction(&out.advect_u, mod, "qsmoke_advect_u") != CUDA_SUCCESS ||
+      g_drv.moduleGetFunction(&out.advect_refl, mod, "qsmoke_advect_refl") != CUDA_SUCCESS ||
       g_drv.moduleGetFunction(&out.div, mod, "qsmoke_div") != CUDA_SUCCESS ||
       g_drv.moduleGetFunction(&out.jacobi, mod, "qsmoke_jacobi") != CUDA_SUCCESS ||
       g_drv.moduleGetFunction(&out.project, mod, "qsmoke_project") != CUDA_SUCCESS ||

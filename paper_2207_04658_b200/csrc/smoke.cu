@@ -86,40 +86,43 @@ SaltSrc dev_salt(const qsmoke_ctx* c, const CodecDev& C, uint32_t sub) {
   return s;
 }
 
-// (32 z, 8 y) tiles; blockIdx.z = the x plane of a record (per-record kernels), of a cell
-// (density) or of a march of kXM = 8 record planes (stencil kernels) -- smoke_kernels.cuh
-enum Span { kRecords, kCells, kMarch };
-qmpm_status launch(qsmoke_ctx* c, CUfunction f, cudaStream_t st, void** args, Span span) {
-  const unsigned gz = span == kCells ? c->g.nx : span == kRecords ? c->g.nxr : (c->g.nxr + 7) / 8;
-  const dim3 grid((c->g.nz + 31) / 32, (c->g.ny + 7) / 8, gz);
+// every kernel: (32 z, 8 y) record tiles, blockIdx.z = a march of kXM = 8 record planes
+// (smoke_kernels.cuh); the advections take dynamic shared memory for their rings of
+// 3 planes x (8 + 2 kH) x (32 + 2 kH) records x 2 cells (kH = 2): float4 velocity,
+// float4 reflected field, float density
+constexpr size_t kRingCells = 3 * (8 + 4) * (32 + 4) * 2;
+constexpr size_t kSmemAdvect = kRingCells * 16, kSmemReflect = 2 * kRingCells * 16,
+                 kSmemDensity = kRingCells * 16 + kRingCells * 4;
+qmpm_status launch(qsmoke_ctx* c, CUfunction f, cudaStream_t st, void** args, size_t smem = 0) {
+  const dim3 grid((c->g.nz + 31) / 32, (c->g.ny + 7) / 8, (c->g.nxr + 7) / 8);
   c->launches += 1;
-  SCK(jit_launch3(f, grid, dim3(32, 8, 1), 0, st, args));
+  SCK(jit_launch3(f, grid, dim3(32, 8, 1), smem, st, args));
   return QMPM_OK;
 }
 
 qmpm_status advect_u(qsmoke_ctx* c, cudaStream_t st, const uint32_t* uv, const uint32_t* ur, const float* rho,
                      float dt, float bdt, SaltSrc ss, uint32_t* out, float* dbg) {
   void* a[] = {&uv, &ur, &rho, &c->g, &dt, &bdt, &ss, &out, &dbg};
-  return launch(c, c->k.advect_u, st, a, kRecords);
+  return ur ? launch(c, c->k.advect_refl, st, a, kSmemReflect) : launch(c, c->k.advect_u, st, a, kSmemAdvect);
 }
 qmpm_status divergence(qsmoke_ctx* c, cudaStream_t st, const uint32_t* u, float* div) {
   void* a[] = {&u, &c->g, &div};
-  return launch(c, c->k.div, st, a, kMarch);
+  return launch(c, c->k.div, st, a);
 }
 qmpm_status jacobi(qsmoke_ctx* c, cudaStream_t st, const uint32_t* pin, const float* div, SaltSrc ss, uint32_t* pout,
                    float* dbg) {
   void* a[] = {&pin, &div, &c->g, &ss, &pout, &dbg};
-  return launch(c, c->k.jacobi, st, a, kMarch);
+  return launch(c, c->k.jacobi, st, a);
 }
 qmpm_status project(qsmoke_ctx* c, cudaStream_t st, const uint32_t* u, const uint32_t* p, SaltSrc ss, uint32_t* out,
                     float* dbg) {
   void* a[] = {&u, &p, &c->g, &ss, &out, &dbg};
-  return launch(c, c->k.project, st, a, kMarch);
+  return launch(c, c->k.project, st, a);
 }
 qmpm_status advect_rho(qsmoke_ctx* c, cudaStream_t st, const float* rin, const uint32_t* u, float dt, float* rout,
                        unsigned long long* tick) {
   void* a[] = {&rin, &u, &c->g, &dt, &rout, &tick};
-  return launch(c, c->k.advect_rho, st, a, kCells);
+  return launch(c, c->k.advect_rho, st, a, kSmemDensity);
 }
 
 // one projection (S6-S7) of u_in into u_out; subs: sub0 = the velocity store,
@@ -214,6 +217,12 @@ qmpm_status qsmoke_create(const qsmoke_params* params, const qmpm_scheme* u_sche
   if (jit_smoke(src, c->k, err) != cudaSuccess) {
     delete c;
     return sfail(QMPM_ECUDA, "%s", err.c_str());
+  }
+  if (jit_set_smem(c->k.advect_u, kSmemAdvect) != cudaSuccess ||
+      jit_set_smem(c->k.advect_refl, kSmemReflect) != cudaSuccess ||
+      jit_set_smem(c->k.advect_rho, kSmemDensity) != cudaSuccess) {
+    delete c;
+    return sfail(QMPM_ECUDA, "cannot enable %zu bytes of shared memory for the advection kernels", kSmemReflect);
   }
   c->stream = (cudaStream_t)cuda_stream;
   c->n_rec = (uint64_t)(P.res[0] / 2) * P.res[1] * P.res[2];

@@ -17,9 +17,16 @@
 //   qsmoke_project    u -= grad p (S7), wall-normal components zeroed, u re-encoded
 //   qsmoke_advect_rho fp32 density advected by u, then the source box set to 1 (S8);
 //                     optionally advances the device step counter (graph replay)
+// All kernels march a CTA's (32 z x 8 y) record column along x (kXM planes per CTA):
+// the stencils through a shared tile with a one-record halo, the advections through
+// rings of decoded planes with a kH-cell halo (see below).
 // Encodes are dithered with h = mix(record ^ salt) (reading Q5); salt comes from the host.
 #pragma once
 #include "codec_record.cuh"
+
+#ifndef QSMOKE_ADV_MINB  // min resident CTAs per SM for the advection kernels (tuning)
+#define QSMOKE_ADV_MINB 2
+#endif
 
 struct SmokeDev {
   int nx, ny, nz, nxr;     // cells per axis; records along x (nx / 2)
@@ -91,21 +98,18 @@ __device__ __forceinline__ void corner(float p, int n, int& i0, float& t) {
   t = p - (float)i0;
 }
 
-// trilinear sample of the velocity field at p (cell units)
-__device__ __forceinline__ void sample_u(const uint32_t* __restrict__ U, const SmokeDev& g, const float* p, float* out) {
-  int i, j, k;
-  float tx, ty, tz;
-  corner(p[0], g.nx, i, tx);
-  corner(p[1], g.ny, j, ty);
-  corner(p[2], g.nz, k, tz);
+// trilinear blend of the 8 corner values v[(dj * 2 + dk) * 2 + di][3] with weights t
+// (S3); every sampling path uses this one arithmetic, so the shared-window and the
+// global paths give identical results
+__device__ __forceinline__ void trilerp(const float (*v)[3], float tx, float ty, float tz, float* out) {
 #pragma unroll
   for (int c = 0; c < 3; ++c) out[c] = 0.0f;
 #pragma unroll
   for (int dj = 0; dj < 2; ++dj) {
 #pragma unroll
     for (int dk = 0; dk < 2; ++dk) {
-      float a[3], b[3];
-      u_pair(U, g, i, j + dj, k + dk, a, b);
+      const float* a = v[(dj * 2 + dk) * 2];
+      const float* b = v[(dj * 2 + dk) * 2 + 1];
       const float wyz = (dj ? ty : 1.0f - ty) * (dk ? tz : 1.0f - tz);
       const float wa = (1.0f - tx) * wyz, wb = tx * wyz;
 #pragma unroll
@@ -114,36 +118,51 @@ __device__ __forceinline__ void sample_u(const uint32_t* __restrict__ U, const S
   }
 }
 
-__device__ __forceinline__ float sample_s(const float* __restrict__ f, const SmokeDev& g, const float* p) {
-  int i, j, k;
-  float tx, ty, tz;
-  corner(p[0], g.nx, i, tx);
-  corner(p[1], g.ny, j, ty);
-  corner(p[2], g.nz, k, tz);
-  float out = 0.0f;
+// the 8 corners of the cell block at (i, j, k) from the records in global memory
+__device__ __forceinline__ void cube_global(const uint32_t* __restrict__ U, const SmokeDev& g, int i, int j, int k,
+                                            float (*v)[3]) {
 #pragma unroll
-  for (int di = 0; di < 2; ++di)
+  for (int dj = 0; dj < 2; ++dj)
 #pragma unroll
-    for (int dj = 0; dj < 2; ++dj)
-#pragma unroll
-      for (int dk = 0; dk < 2; ++dk) {
-        const float w = (di ? tx : 1.0f - tx) * (dj ? ty : 1.0f - ty) * (dk ? tz : 1.0f - tz);
-        out = fmaf(w, __ldg(f + ((unsigned long long)(i + di) * g.ny + (j + dj)) * g.nz + (k + dk)), out);
-      }
-  return out;
+    for (int dk = 0; dk < 2; ++dk) u_pair(U, g, i, j + dj, k + dk, v[(dj * 2 + dk) * 2], v[(dj * 2 + dk) * 2 + 1]);
 }
 
-// S4: RK-3 (Ralston) departure point of cell centre x, velocity in world units / dx
-__device__ __forceinline__ void backtrace(const uint32_t* __restrict__ U, const SmokeDev& g, const float* x,
-                                          const float* u0, float dt, float* xb) {
+// sample of u (UR == NULL) or of 2 u - u_R (the reflection, S8) at p from global memory:
+// the out-of-window path, not inlined so it costs the window path nothing
+__device__ __noinline__ float3 sample_global(const uint32_t* __restrict__ U, const uint32_t* __restrict__ UR,
+                                             const SmokeDev& g, float px, float py, float pz) {
+  int i, j, k;
+  float tx, ty, tz;
+  corner(px, g.nx, i, tx);
+  corner(py, g.ny, j, ty);
+  corner(pz, g.nz, k, tz);
+  float v[8][3], out[3];
+  cube_global(U, g, i, j, k, v);
+  if (UR) {
+    float d[8][3];
+    cube_global(UR, g, i, j, k, d);
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[e][c] = 2.0f * v[e][c] - d[e][c];
+  }
+  trilerp(v, tx, ty, tz, out);
+  return make_float3(out[0], out[1], out[2]);
+}
+
+// S4: RK-3 (Ralston) departure point of cell centre x, velocity in world units / dx;
+// samp(p, out) samples the velocity
+template <class Samp>
+__device__ __forceinline__ void backtrace3(const SmokeDev& g, const float* x, const float* u0, float dt, Samp&& samp,
+                                           float* xb) {
   const float s = dt * g.inv_dx;
   float k2[3], k3[3], p[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) p[c] = x[c] - 0.5f * s * u0[c];
-  sample_u(U, g, p, k2);
+  samp(p, k2);
 #pragma unroll
   for (int c = 0; c < 3; ++c) p[c] = x[c] - 0.75f * s * k2[c];
-  sample_u(U, g, p, k3);
+  samp(p, k3);
 #pragma unroll
   for (int c = 0; c < 3; ++c)
     xb[c] = x[c] - s * ((2.0f / 9.0f) * u0[c] + (1.0f / 3.0f) * k2[c] + (4.0f / 9.0f) * k3[c]);
@@ -345,45 +364,224 @@ __device__ __forceinline__ void p_march(const uint32_t* __restrict__ P, const fl
     cell += 2 * m.plane;
   }
 }
+
+// ---- advection windows ---------------------------------------------------------------
+// An advection CTA marches its (32 z x 8 y) record column along x like the stencils,
+// keeping a ring of 3 record planes (xr - 1, xr, xr + 1 = cells 2xr - 2 .. 2xr + 3) of
+// DECODED velocity with a kH-cell y/z halo in shared memory (float4 per cell), so the
+// backtrace and the final sample read corners with LDS instead of re-decoding records
+// (a corner pair outside the window -- a departure point more than ~2 cells away -- is
+// decoded from global memory, with identical arithmetic).  The reflection's q = 2 u_h -
+// u~ and the density get rings of their own.
+constexpr int kH = 2;
+constexpr int kWY = kTY + 2 * kH, kWZ = kTZ + 2 * kH;  // window tile (records)
+constexpr int kRing = 3 * kWY * kWZ * 2;                // float4 cells per ring
+
+struct Win {
+  int xr, y0, z0;
+  __device__ __forceinline__ bool has(int i, int j, int k) const {
+    return i >= 2 * xr - 2 && i <= 2 * xr + 2 && j >= y0 - kH && j < y0 + kTY + kH - 1 && k >= z0 - kH &&
+           k < z0 + kTZ + kH - 1;
+  }
+  // index of cell (i, j, k) in a ring (float4 units): [slot][cell parity][y][z], so a
+  // warp's lanes (consecutive z) read consecutive 16-byte slots (no bank conflicts)
+  __device__ __forceinline__ int at(int i, int j, int k) const {
+    const int slot = ((i >> 1) + 3) % 3;
+    return ((slot * 2 + (i & 1)) * kWY + (j - y0 + kH)) * kWZ + (k - z0 + kH);
+  }
+  // sample of ring R at p; out of the window: sample_global(U, UR) (identical arithmetic)
+  __device__ __forceinline__ void sample(const SmokeDev& g, const float4* R, const uint32_t* U, const uint32_t* UR,
+                                         const float* p, float* out) const {
+    int i, j, k;
+    float tx, ty, tz;
+    corner(p[0], g.nx, i, tx);
+    corner(p[1], g.ny, j, ty);
+    corner(p[2], g.nz, k, tz);
+    if (has(i, j, k)) {
+      float v[8][3];
+      cube(R, i, j, k, v);
+      trilerp(v, tx, ty, tz, out);
+    } else {
+      const float3 r = sample_global(U, UR, g, p[0], p[1], p[2]);
+      out[0] = r.x, out[1] = r.y, out[2] = r.z;
+    }
+  }
+  // the 8 corners of the block at (i, j, k) from ring R (has(i, j, k) must hold)
+  __device__ __forceinline__ void cube(const float4* R, int i, int j, int k, float (*v)[3]) const {
+    const int a = at(i, j, k), b = at(i + 1, j, k);
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+      for (int dk = 0; dk < 2; ++dk) {
+        const int o = dj * kWZ + dk;
+        const float4 A = R[a + o], B = R[b + o];
+        float* va = v[(dj * 2 + dk) * 2];
+        float* vb = v[(dj * 2 + dk) * 2 + 1];
+        va[0] = A.x, va[1] = A.y, va[2] = A.z, vb[0] = B.x, vb[1] = B.y, vb[2] = B.z;
+      }
+  }
+};
+
+// Ring fills are software-pipelined: the raw words of plane q are loaded into registers
+// (each thread owns tile records t and t + 256 of the 12 x 36 window tile) one plane
+// before they are decoded into the ring, so the loads overlap the previous plane's work.
+constexpr int kFillPer = (kWY * kWZ + kTY * kTZ - 1) / (kTY * kTZ);  // 2
+
+template <bool REFL, bool RHO>
+struct Fill {
+  uint32_t u[kFillPer][SpecU::W];
+  uint32_t ur[REFL ? kFillPer : 1][SpecU::W];
+  float d[RHO ? kFillPer : 1][2];
+  bool ok[kFillPer];
+};
+
+template <bool REFL, bool RHO>
+__device__ __forceinline__ void fill_load(const uint32_t* __restrict__ U, const uint32_t* __restrict__ UR,
+                                          const float* __restrict__ D, const SmokeDev& g, const Win& w, int q,
+                                          Fill<REFL, RHO>& F) {
+  const unsigned long long plane = (unsigned long long)g.ny * g.nz;
+#pragma unroll
+  for (int e = 0; e < kFillPer; ++e) {
+    const int t = threadIdx.y * kTZ + threadIdx.x + e * kTY * kTZ;
+    const int jy = t / kWZ, kz = t - jy * kWZ;
+    const int j = w.y0 - kH + jy, k = w.z0 - kH + kz;
+    F.ok[e] = t < kWY * kWZ && q < g.nxr && j >= 0 && j < g.ny && k >= 0 && k < g.nz;
+    if (!F.ok[e]) continue;
+    const unsigned long long r = (unsigned long long)q * plane + (unsigned long long)j * g.nz + k;
+#pragma unroll
+    for (int c = 0; c < SpecU::W; ++c) F.u[e][c] = __ldg(U + r * SpecU::W + c);
+    if (REFL) {
+#pragma unroll
+      for (int c = 0; c < SpecU::W; ++c) F.ur[e][c] = __ldg(UR + r * SpecU::W + c);
+    }
+    if (RHO) {
+      const unsigned long long c = 2ull * q * plane + (unsigned long long)j * g.nz + k;
+      F.d[e][0] = __ldg(D + c);
+      F.d[e][1] = __ldg(D + c + plane);
+    }
+  }
+}
+
+template <bool REFL, bool RHO>
+__device__ __forceinline__ void fill_store(const Fill<REFL, RHO>& F, int q, float4* ru, float4* rr, float* rd) {
+  const int slot = (q + 3) % 3;
+#pragma unroll
+  for (int e = 0; e < kFillPer; ++e) {
+    if (!F.ok[e]) continue;
+    const int t = threadIdx.y * kTZ + threadIdx.x + e * kTY * kTZ;
+    const int o = slot * 2 * kWY * kWZ + t;  // t = jy * kWZ + kz; cell 1 one plane further
+    uint32_t wv[SpecU::W + 1];
+#pragma unroll
+    for (int c = 0; c < SpecU::W; ++c) wv[c] = F.u[e][c];
+    wv[SpecU::W] = 0u;
+    float u[6];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) u[f] = sdec<SpecU>(wv, f);
+    ru[o] = make_float4(u[0], u[1], u[2], 0.f);
+    ru[o + kWY * kWZ] = make_float4(u[3], u[4], u[5], 0.f);
+    if (REFL) {
+#pragma unroll
+      for (int c = 0; c < SpecU::W; ++c) wv[c] = F.ur[e][c];
+      float a[6];
+#pragma unroll
+      for (int f = 0; f < 6; ++f) a[f] = 2.0f * u[f] - sdec<SpecU>(wv, f);
+      rr[o] = make_float4(a[0], a[1], a[2], 0.f);
+      rr[o + kWY * kWZ] = make_float4(a[3], a[4], a[5], 0.f);
+    }
+    if (RHO) {
+      rd[o] = F.d[e][0];
+      rd[o + kWY * kWZ] = F.d[e][1];
+    }
+  }
+}
+
+// march skeleton of the advection kernels: f(xr, y, z, r, valid, win) per record plane,
+// once the ring holds planes xr - 1 .. xr + 1
+template <bool REFL, bool RHO, class F>
+__device__ __forceinline__ void adv_march(const uint32_t* __restrict__ U, const uint32_t* __restrict__ UR,
+                                          const float* __restrict__ D, const SmokeDev& g, float4* ru, float4* rr,
+                                          float* rd, F&& f) {
+  Win w;
+  w.y0 = blockIdx.y * kTY;
+  w.z0 = blockIdx.x * kTZ;
+  const int xs = blockIdx.z * kXM, xe = min(xs + kXM, g.nxr);
+  const int y = w.y0 + threadIdx.y, z = w.z0 + threadIdx.x;
+  const bool valid = y < g.ny && z < g.nz;
+  Fill<REFL, RHO> fl;
+  if (xs > 0) {
+    fill_load(U, UR, D, g, w, xs - 1, fl);
+    fill_store(fl, xs - 1, ru, rr, rd);
+  }
+  fill_load(U, UR, D, g, w, xs, fl);
+  fill_store(fl, xs, ru, rr, rd);
+  fill_load(U, UR, D, g, w, xs + 1, fl);  // q >= nxr loads nothing
+  for (int xr = xs; xr < xe; ++xr) {
+    w.xr = xr;
+    fill_store(fl, xr + 1, ru, rr, rd);
+    __syncthreads();
+    if (xr + 1 < xe) fill_load(U, UR, D, g, w, xr + 2, fl);
+    const unsigned long long r = valid ? ((unsigned long long)xr * g.ny + y) * g.nz + z : 0ull;
+    f(xr, y, z, r, valid, w);
+    __syncthreads();
+  }
+}
 }  // namespace smoke
 
 // ------------------------------------------------------------------ entry points
-extern "C" __global__ void __launch_bounds__(256)
+template <bool REFL>
+__device__ __forceinline__ void advect_u_body(const uint32_t* __restrict__ uv, const uint32_t* __restrict__ ur,
+                                              const float* __restrict__ rho, const SmokeDev& g, float dt, float bdt,
+                                              const SaltSrc& ss, uint32_t* __restrict__ out, float* __restrict__ dbg) {
+  constexpr int W = SpecU::W;
+  extern __shared__ float4 smem_adv[];
+  float4* ru = smem_adv;
+  float4* rr = REFL ? smem_adv + smoke::kRing : nullptr;
+  const uint32_t salt = smoke::salt_of(ss);
+  smoke::adv_march<REFL, false>(uv, ur, nullptr, g, ru, rr, nullptr, [&](int xr, int y, int z, unsigned long long r,
+                                                                       bool valid, const smoke::Win& w) {
+    auto samp_u = [&](const float* p, float* o) { w.sample(g, ru, uv, nullptr, p, o); };
+    float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (valid) {
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        const int x = 2 * xr + c2;
+        const float xp[3] = {(float)x, (float)y, (float)z};
+        const float4 U0 = ru[w.at(x, y, z)];
+        const float u0[3] = {U0.x, U0.y, U0.z};
+        float xb[3], q[3];
+        smoke::backtrace3(g, xp, u0, dt, samp_u, xb);
+        if (REFL)
+          w.sample(g, rr, uv, ur, xb, q);
+        else
+          samp_u(xb, q);
+        if (!REFL && rho) q[1] += bdt * __ldg(rho + ((unsigned long long)x * g.ny + y) * g.nz + z);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[3 * c2 + c] = q[c];
+      }
+      if (dbg) {
+#pragma unroll
+        for (int f = 0; f < 6; ++f) dbg[r * 6 + f] = v[f];
+      }
+    }
+    const uint32_t hh = SpecU::DITHER ? qmpm::mix32((uint32_t)r ^ salt) : 0u;
+    uint32_t o[W + 1];
+    qmpm::encode_record<SpecU>(v, hh, valid, o, nullptr);
+    if (valid) qmpm::store_words<SpecU>(out + r * W, o);
+  });
+}
+
+extern "C" __global__ void __launch_bounds__(256, QSMOKE_ADV_MINB)
     qsmoke_advect_u(const uint32_t* __restrict__ uv, const uint32_t* __restrict__ ur, const float* __restrict__ rho,
                     SmokeDev g, float dt, float bdt, SaltSrc ss, uint32_t* __restrict__ out, float* __restrict__ dbg) {
-  constexpr int W = SpecU::W;
-  const smoke::Here h = smoke::here(g);
-  float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  if (h.valid) {
-    uint32_t w[W + 1];
-    smoke::ldrec<SpecU>(uv, h.r, w);
-#pragma unroll
-    for (int c2 = 0; c2 < 2; ++c2) {
-      const float x[3] = {(float)(2 * h.xr + c2), (float)h.y, (float)h.z};
-      float u0[3], xb[3], q[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) u0[c] = qmpm::sdec<SpecU>(w, 3 * c2 + c);
-      smoke::backtrace(uv, g, x, u0, dt, xb);
-      smoke::sample_u(uv, g, xb, q);
-      if (ur) {  // reflection: sample 2 u_vel - u_refl (S8; trilinear sampling is linear)
-        float qr[3];
-        smoke::sample_u(ur, g, xb, qr);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) q[c] = 2.0f * q[c] - qr[c];
-      }
-      if (rho) q[1] += bdt * __ldg(rho + ((unsigned long long)(2 * h.xr + c2) * g.ny + h.y) * g.nz + h.z);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) v[3 * c2 + c] = q[c];
-    }
-    if (dbg) {
-#pragma unroll
-      for (int f = 0; f < 6; ++f) dbg[h.r * 6 + f] = v[f];
-    }
-  }
-  const uint32_t hh = SpecU::DITHER ? qmpm::mix32((uint32_t)h.r ^ smoke::salt_of(ss)) : 0u;
-  uint32_t o[W + 1];
-  qmpm::encode_record<SpecU>(v, hh, h.valid, o, nullptr);
-  if (h.valid) qmpm::store_words<SpecU>(out + h.r * W, o);
+  advect_u_body<false>(uv, nullptr, rho, g, dt, bdt, ss, out, dbg);
+}
+
+// the reflection's advection (S8): q = 2 u_vel - u_refl sampled at the departure point
+extern "C" __global__ void __launch_bounds__(256, QSMOKE_ADV_MINB)
+    qsmoke_advect_refl(const uint32_t* __restrict__ uv, const uint32_t* __restrict__ ur, const float* __restrict__ rho,
+                       SmokeDev g, float dt, float bdt, SaltSrc ss, uint32_t* __restrict__ out,
+                       float* __restrict__ dbg) {
+  advect_u_body<true>(uv, ur, nullptr, g, dt, 0.0f, ss, out, dbg);
 }
 
 // S5 on the x march: neighbours outside the domain are 0 (halo / x loads masked)
@@ -489,25 +687,70 @@ extern "C" __global__ void __launch_bounds__(256)
   });
 }
 
-// one thread per CELL: blockIdx.z = the cell plane x
-extern "C" __global__ void __launch_bounds__(256)
+// density (S8): per record, backtrace on the velocity window, sample the density window
+extern "C" __global__ void __launch_bounds__(256, QSMOKE_ADV_MINB)
     qsmoke_advect_rho(const float* __restrict__ rho, const uint32_t* __restrict__ U, SmokeDev g, float dt,
                       float* __restrict__ out, unsigned long long* __restrict__ tick) {
+  extern __shared__ float4 smem_adv[];
+  float4* ru = smem_adv;
+  float* rd = reinterpret_cast<float*>(smem_adv + smoke::kRing);
   // the last kernel of a step advances the device step counter (nothing here reads it)
   if (tick && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && threadIdx.y == 0)
     *tick += 1ull;
-  const int z = blockIdx.x * smoke::kTZ + threadIdx.x, y = blockIdx.y * smoke::kTY + threadIdx.y, x = blockIdx.z;
-  if (z >= g.nz || y >= g.ny) return;
-  const unsigned long long c = ((unsigned long long)x * g.ny + y) * g.nz + z;
-  float val;
-  if (x >= g.lo[0] && x < g.hi[0] && y >= g.lo[1] && y < g.hi[1] && z >= g.lo[2] && z < g.hi[2]) {
-    val = 1.0f;  // S8: the source box
-  } else {
-    const float p[3] = {(float)x, (float)y, (float)z};
-    float u0[3], xb[3];
-    smoke::u_cell(U, g, x, y, z, u0);
-    smoke::backtrace(U, g, p, u0, dt, xb);
-    val = smoke::sample_s(rho, g, xb);
-  }
-  out[c] = val;
+  smoke::adv_march<false, true>(U, nullptr, rho, g, ru, nullptr, rd, [&](int xr, int y, int z, unsigned long long r,
+                                                                          bool valid, const smoke::Win& w) {
+    if (!valid) return;
+    auto samp_u = [&](const float* p, float* o) { w.sample(g, ru, U, nullptr, p, o); };
+    const unsigned long long plane = (unsigned long long)g.ny * g.nz;
+#pragma unroll
+    for (int c2 = 0; c2 < 2; ++c2) {
+      const int x = 2 * xr + c2;
+      const unsigned long long c = (unsigned long long)x * plane + (unsigned long long)y * g.nz + z;
+      float val;
+      if (x >= g.lo[0] && x < g.hi[0] && y >= g.lo[1] && y < g.hi[1] && z >= g.lo[2] && z < g.hi[2]) {
+        val = 1.0f;  // S8: the source box
+      } else {
+        const float xp[3] = {(float)x, (float)y, (float)z};
+        const float4 U0 = ru[w.at(x, y, z)];
+        const float u0[3] = {U0.x, U0.y, U0.z};
+        float xb[3];
+        smoke::backtrace3(g, xp, u0, dt, samp_u, xb);
+        int i, j, k;
+        float tx, ty, tz;
+        smoke::corner(xb[0], g.nx, i, tx);
+        smoke::corner(xb[1], g.ny, j, ty);
+        smoke::corner(xb[2], g.nz, k, tz);
+        float f8[8];
+        if (w.has(i, j, k)) {
+          const int a = w.at(i, j, k), b = w.at(i + 1, j, k);
+#pragma unroll
+          for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+            for (int dk = 0; dk < 2; ++dk) {
+              f8[dj * 2 + dk] = rd[a + dj * smoke::kWZ + dk];
+              f8[4 + dj * 2 + dk] = rd[b + dj * smoke::kWZ + dk];
+            }
+        } else {
+#pragma unroll
+          for (int di = 0; di < 2; ++di)
+#pragma unroll
+            for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+              for (int dk = 0; dk < 2; ++dk)
+                f8[di * 4 + dj * 2 + dk] = __ldg(rho + ((unsigned long long)(i + di) * g.ny + (j + dj)) * g.nz + (k + dk));
+        }
+        val = 0.0f;
+#pragma unroll
+        for (int di = 0; di < 2; ++di)
+#pragma unroll
+          for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+            for (int dk = 0; dk < 2; ++dk) {
+              const float wt = (di ? tx : 1.0f - tx) * (dj ? ty : 1.0f - ty) * (dk ? tz : 1.0f - tz);
+              val = fmaf(wt, f8[di * 4 + dj * 2 + dk], val);
+            }
+      }
+      out[c] = val;
+    }
+  });
 }
