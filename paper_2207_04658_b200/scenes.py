@@ -363,3 +363,22 @@ def smoke_plume(res, dt=0.01, buoyancy=1.0, jacobi_iters=64):
     bottom centre (the plume rises by buoyancy)."""
     params, u, p, rho = smoke(res=res, amp=0.0, rho_blobs=0, dt=dt, buoyancy=buoyancy, jacobi_iters=jacobi_iters)
     return params
+
+
+# ---------------------------------------------------------------- adjoint (f3)
+def adjoint_fluid(dim=2, side=8, res=32, seed=0, dt=2e-4, E=50.0, vmax=1.0, jitter=0.25, dJ=0.02, cmax=2.0,
+                  ppc=2, origin=0.35, gravity=None):
+    """A seeded J-fluid block for the gradient-tally path (DESIGN.md §13 input recipe):
+    side^dim particles on a jittered lattice of spacing dx/ppc starting at `origin`
+    (fraction of the box), random velocity |v_a| <= vmax, J = 1 + U(-dJ, dJ), C with
+    entries U(-cmax, cmax).  Returns (sim, state [n][ns] float32)."""
+    rng = np.random.default_rng(seed)
+    sim = _sim(dim, "fluid", (res,) * dim, dt, E, p_vol=(1.0 / res / ppc) ** dim, gravity=gravity)
+    h = sim["dx"] / ppc
+    grid = np.stack(np.meshgrid(*[np.arange(side)] * dim, indexing="ij"), -1).reshape(-1, dim)
+    x = origin + (grid + 0.5 + rng.uniform(-jitter, jitter, grid.shape)) * h
+    n = x.shape[0]
+    v = rng.uniform(-vmax, vmax, (n, dim))
+    J = 1.0 + rng.uniform(-dJ, dJ, (n, 1))
+    C = rng.uniform(-cmax, cmax, (n, dim * dim))
+    return sim, np.concatenate([x, v, J, C], 1).astype(np.float32)
