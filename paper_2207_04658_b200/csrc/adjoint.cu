@@ -1,0 +1,694 @@
+// adjoint.cu -- gradient tallies g_h of Algorithm 1 line 12 (Eq. 8,
+// P:337; "Gradient Computation") on the GPU: the full-precision (fp32) J-fluid
+// MLS-MPM step on a dense grid, its adjoint, and the paper's bisection checkpointing.
+// C ABI: include/qadjoint.h.  DESIGN.md §13.
+//
+// Forward (the same rules as the quantized step's, with fp32 state rows
+// [n][ns] = x, v, J, C instead of records): P2G into a dense float4 grid (m, P) with
+// atomics, grid update (v = P/m + dt g, separating walls), G2P.
+// Adjoint of one step, lambda_t = (ds_{t+1}/ds_t)^T lambda_{t+1}, in three kernels:
+//   g2p_bwd  gathers v_i, scatters the node adjoints W (lv' + 4/dx lC' (o - fx)) with
+//            atomics, keeps the particle's partial (lx, lJ, d/dfx)
+//   grid_bwd per node: lP = lv / m, lm = -lv . u / m (zero on wall-clamped components
+//            and empty nodes)
+//   p2g_bwd  gathers (lm, lP), finishes lambda_t (lv, lC, lJ from the stress, lx through
+//            fx) and folds sum_p lambda^2 per scalar into the tallies (double atomics)
+// Every derivative is the forward's as written: floor() is constant, clamps have zero
+// derivative.  The elastic material (the polar decomposition's derivative) is not built.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "qadjoint.h"
+
+namespace qmpm {
+void set_thread_error(const char* msg);  // api.cu
+}
+
+struct AdjSim {
+  int res[3];
+  float dx, inv_dx, dt;
+  float g[3];
+  float m, k;  // particle mass; stress factor -dt V_p 4/dx^2 E
+  int bound;
+};
+
+namespace {
+
+qmpm_status afail(qmpm_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  qmpm::set_thread_error(buf);
+  return code;
+}
+
+#define ACK(x)                                                                                   \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess) return afail(QMPM_ECUDA, "%s: %s", #x, cudaGetErrorString(e_));        \
+  } while (0)
+
+template <int D>
+struct Stencil {
+  int base[3];
+  float fx[3], dfx[3];  // fx and d fx / d x (0 where the out-of-domain clamp holds)
+  float w[3][3], dw[3][3];
+};
+
+// base / fx with the out-of-domain clamp (reading Q14) and the B-spline weights
+template <int D>
+__device__ __forceinline__ Stencil<D> stencil(const float* x, const AdjSim& S) {
+  Stencil<D> st;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const float X = x[a] * S.inv_dx;
+    int b = (int)floorf(X - 0.5f);
+    bool oob = false;
+    if (b < 0) b = 0, oob = true;
+    if (b > S.res[a] - 3) b = S.res[a] - 3, oob = true;
+    float f = X - (float)b;
+    float df = S.inv_dx;
+    if (oob && f < 0.5f) f = 0.5f, df = 0.0f;
+    if (oob && f > 1.5f) f = 1.5f, df = 0.0f;
+    st.base[a] = b;
+    st.fx[a] = f;
+    st.dfx[a] = df;
+    st.w[a][0] = 0.5f * (1.5f - f) * (1.5f - f);
+    st.w[a][1] = 0.75f - (f - 1.0f) * (f - 1.0f);
+    st.w[a][2] = 0.5f * (f - 0.5f) * (f - 0.5f);
+    st.dw[a][0] = -(1.5f - f);
+    st.dw[a][1] = -2.0f * (f - 1.0f);
+    st.dw[a][2] = f - 0.5f;
+  }
+  return st;
+}
+
+template <int D>
+constexpr int kNS = 2 * D + 1 + D * D;
+template <int D>
+constexpr int kNO = D == 3 ? 27 : 9;
+
+template <int D>
+__device__ __forceinline__ void offset_of(int q, int* o) {
+  if (D == 3) {
+    o[0] = q / 9, o[1] = (q / 3) % 3, o[2] = q % 3;
+  } else {
+    o[0] = q / 3, o[1] = q % 3, o[2] = 0;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ long long node_of(const Stencil<D>& st, const int* o, const AdjSim& S) {
+  const int i = st.base[0] + o[0], j = st.base[1] + o[1], k = D == 3 ? st.base[2] + o[2] : 0;
+  return ((long long)i * S.res[1] + j) * (D == 3 ? S.res[2] : 1) + k;
+}
+
+template <int D>
+__device__ __forceinline__ void weight(const Stencil<D>& st, const int* o, float& W, float* dW) {
+  W = 1.0f;
+#pragma unroll
+  for (int a = 0; a < D; ++a) W *= st.w[a][o[a]];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    float p = st.dw[a][o[a]];
+#pragma unroll
+    for (int b = 0; b < D; ++b)
+      if (b != a) p *= st.w[b][o[b]];
+    dW[a] = p;
+  }
+}
+
+// ---------------------------------------------------------------- forward
+template <int D>
+__global__ void k_p2g_fwd(const float* __restrict__ s, uint64_t n, AdjSim S, float4* __restrict__ grid) {
+  constexpr int NS = kNS<D>;
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float* st = s + p * NS;
+  const Stencil<D> sc = stencil<D>(st, S);
+  float A[D][D];
+  const float sJ = S.k * (st[2 * D] - 1.0f);
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) A[a][b] = S.m * st[2 * D + 1 + a * D + b] + (a == b ? sJ : 0.0f);
+  for (int q = 0; q < kNO<D>; ++q) {
+    int o[3];
+    offset_of<D>(q, o);
+    float W, dW[3];
+    weight<D>(sc, o, W, dW);
+    float dpos[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) dpos[a] = ((float)o[a] - sc.fx[a]) * S.dx;
+    float4* nd = grid + node_of<D>(sc, o, S);
+    atomicAdd(&nd->x, W * S.m);
+    float P[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float Ad = 0.0f;
+#pragma unroll
+      for (int b = 0; b < D; ++b) Ad += A[a][b] * dpos[b];
+      P[a] = W * (S.m * st[D + a] + Ad);
+    }
+    atomicAdd(&nd->y, P[0]);
+    atomicAdd(&nd->z, P[1]);
+    if (D == 3) atomicAdd(&nd->w, P[2]);
+  }
+}
+
+__device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? v.y : (a == 1 ? v.z : v.w); }
+
+// v = P/m + dt g, separating walls (reading Q13): gv = (m, vx, vy, vz)
+template <int D>
+__global__ void k_grid_fwd(const float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ gv) {
+  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nn) return;
+  const float4 nd = grid[c];
+  float4 out = make_float4(nd.x, 0.f, 0.f, 0.f);
+  if (nd.x > 0.0f) {
+    const int nz = D == 3 ? S.res[2] : 1;
+    const int ijk[3] = {(int)(c / ((uint64_t)S.res[1] * nz)), (int)((c / nz) % S.res[1]), (int)(c % nz)};
+    float v[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float va = comp(nd, a) / nd.x + S.dt * S.g[a];
+      if (ijk[a] < S.bound && va < 0.0f) va = 0.0f;
+      if (ijk[a] > S.res[a] - S.bound && va > 0.0f) va = 0.0f;
+      v[a] = va;
+    }
+    out = make_float4(nd.x, v[0], v[1], v[2]);
+  }
+  gv[c] = out;
+}
+
+template <int D>
+__global__ void k_g2p_fwd(const float* __restrict__ s, uint64_t n, const float4* __restrict__ gv, AdjSim S,
+                          float* __restrict__ out) {
+  constexpr int NS = kNS<D>;
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float* st = s + p * NS;
+  const Stencil<D> sc = stencil<D>(st, S);
+  float v[D], C[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    v[a] = 0.0f;
+#pragma unroll
+    for (int b = 0; b < D; ++b) C[a][b] = 0.0f;
+  }
+  for (int q = 0; q < kNO<D>; ++q) {
+    int o[3];
+    offset_of<D>(q, o);
+    float W, dW[3];
+    weight<D>(sc, o, W, dW);
+    const float4 nd = gv[node_of<D>(sc, o, S)];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const float vi = comp(nd, a);
+      v[a] += W * vi;
+#pragma unroll
+      for (int b = 0; b < D; ++b) C[a][b] += 4.0f * S.inv_dx * W * vi * ((float)o[b] - sc.fx[b]);
+    }
+  }
+  float* o = out + p * NS;
+  float tr = 0.0f;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    o[a] = st[a] + S.dt * v[a];
+    o[D + a] = v[a];
+    tr += C[a][a];
+  }
+  o[2 * D] = st[2 * D] * (1.0f + S.dt * tr);
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) o[2 * D + 1 + a * D + b] = C[a][b];
+}
+
+// ---------------------------------------------------------------- adjoint
+// lambda_T = (0, m v_T, 0, 0), the kinetic energy z and the tally of lambda_T
+template <int D>
+__device__ __forceinline__ void tally(const float* lam, bool valid, double* g) {
+  constexpr int NS = kNS<D>;
+  const unsigned full = 0xffffffffu;
+#pragma unroll
+  for (int h = 0; h < NS; ++h) {
+    float q = valid ? lam[h] * lam[h] : 0.0f;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(full, q, off);
+    if ((threadIdx.x & 31) == 0 && q != 0.0f) atomicAdd(g + h, (double)q);
+  }
+}
+
+template <int D>
+__global__ void k_lambda_T(const float* __restrict__ s, uint64_t n, AdjSim S, float* __restrict__ lam, double* g,
+                           double* z) {
+  constexpr int NS = kNS<D>;
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = p < n;
+  float l[NS];
+#pragma unroll
+  for (int h = 0; h < NS; ++h) l[h] = 0.0f;
+  float ke = 0.0f;
+  if (valid) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const float va = s[p * NS + D + a];
+      l[D + a] = S.m * va;
+      ke += 0.5f * S.m * va * va;
+    }
+#pragma unroll
+    for (int h = 0; h < NS; ++h) lam[p * NS + h] = l[h];
+  }
+  tally<D>(l, valid, g);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, off);
+  if ((threadIdx.x & 31) == 0 && ke != 0.0f) atomicAdd(z, (double)ke);
+}
+
+// G2P reverse: node adjoints lgrid.yzw += W (lv' + 4/dx lC' (o - fx)); particle partials:
+// lam_t = (lx', 0, lJ' (1 + dt tr C'), 0) and lfx = d/dfx through G2P
+template <int D>
+__global__ void k_g2p_bwd(const float* __restrict__ s, const float* __restrict__ lam1, uint64_t n,
+                          const float4* __restrict__ gv, AdjSim S, float4* __restrict__ lgrid,
+                          float* __restrict__ lam, float* __restrict__ lfx_out) {
+  constexpr int NS = kNS<D>;
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float* st = s + p * NS;
+  const float* l1 = lam1 + p * NS;
+  const Stencil<D> sc = stencil<D>(st, S);
+  // tr C' (forward recompute)
+  float tr = 0.0f;
+  for (int q = 0; q < kNO<D>; ++q) {
+    int o[3];
+    offset_of<D>(q, o);
+    float W, dW[3];
+    weight<D>(sc, o, W, dW);
+    const float4 nd = gv[node_of<D>(sc, o, S)];
+#pragma unroll
+    for (int a = 0; a < D; ++a) tr += 4.0f * S.inv_dx * W * comp(nd, a) * ((float)o[a] - sc.fx[a]);
+  }
+  const float J = st[2 * D], lJ1 = l1[2 * D];
+  float lv[D], lC[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    lv[a] = l1[D + a] + S.dt * l1[a];
+#pragma unroll
+    for (int b = 0; b < D; ++b) lC[a][b] = l1[2 * D + 1 + a * D + b] + (a == b ? lJ1 * J * S.dt : 0.0f);
+  }
+  float lfx[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) lfx[a] = 0.0f;
+  for (int q = 0; q < kNO<D>; ++q) {
+    int o[3];
+    offset_of<D>(q, o);
+    float W, dW[3];
+    weight<D>(sc, o, W, dW);
+    const long long ni = node_of<D>(sc, o, S);
+    const float4 nd = gv[ni];
+    float dpc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) dpc[a] = (float)o[a] - sc.fx[a];
+    float lW = 0.0f, add[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const float vi = comp(nd, a);
+      float Cd = 0.0f;
+#pragma unroll
+      for (int b = 0; b < D; ++b) Cd += lC[a][b] * dpc[b];
+      add[a] = W * (lv[a] + 4.0f * S.inv_dx * Cd);
+      lW += lv[a] * vi + 4.0f * S.inv_dx * vi * Cd;
+    }
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      float s2 = 0.0f;
+#pragma unroll
+      for (int a = 0; a < D; ++a) s2 += lC[a][b] * comp(nd, a);
+      lfx[b] += -4.0f * S.inv_dx * W * s2 + lW * dW[b];
+    }
+    atomicAdd(&lgrid[ni].y, add[0]);
+    atomicAdd(&lgrid[ni].z, add[1]);
+    if (D == 3) atomicAdd(&lgrid[ni].w, add[2]);
+  }
+  float* lo = lam + p * NS;
+#pragma unroll
+  for (int h = 0; h < NS; ++h) lo[h] = 0.0f;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    lo[a] = l1[a];
+    lfx_out[p * 3 + a] = lfx[a];
+  }
+  lo[2 * D] = lJ1 * (1.0f + S.dt * tr);
+}
+
+// grid reverse: (0, lv) -> (lm, lP); lP = lv / m, lm = -lv . u / m, u = P / m; zero on
+// wall-clamped components and on empty nodes
+template <int D>
+__global__ void k_grid_bwd(const float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ lgrid) {
+  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nn) return;
+  const float4 nd = grid[c];
+  const float4 lvn = lgrid[c];
+  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (nd.x > 0.0f) {
+    const int nz = D == 3 ? S.res[2] : 1;
+    const int ijk[3] = {(int)(c / ((uint64_t)S.res[1] * nz)), (int)((c / nz) % S.res[1]), (int)(c % nz)};
+    float lP[3] = {0.f, 0.f, 0.f}, lm = 0.0f;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const float u = comp(nd, a) / nd.x;
+      const float va = u + S.dt * S.g[a];
+      const bool clamp = (ijk[a] < S.bound && va < 0.0f) || (ijk[a] > S.res[a] - S.bound && va > 0.0f);
+      const float l = clamp ? 0.0f : comp(lvn, a);
+      lP[a] = l / nd.x;
+      lm -= l * u / nd.x;
+    }
+    out = make_float4(lm, lP[0], lP[1], lP[2]);
+  }
+  lgrid[c] = out;
+}
+
+// P2G reverse: finishes lambda_t and tallies it
+template <int D>
+__global__ void k_p2g_bwd(const float* __restrict__ s, uint64_t n, const float4* __restrict__ lgrid, AdjSim S,
+                          const float* __restrict__ lfx_in, float* __restrict__ lam, double* __restrict__ g) {
+  constexpr int NS = kNS<D>;
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = p < n;
+  float l[NS];
+#pragma unroll
+  for (int h = 0; h < NS; ++h) l[h] = 0.0f;
+  if (valid) {
+    const float* st = s + p * NS;
+    const Stencil<D> sc = stencil<D>(st, S);
+    const float sJ = S.k * (st[2 * D] - 1.0f);
+    float A[D][D], lA[D][D], lv[D], lfx[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      lv[a] = 0.0f;
+      lfx[a] = lfx_in[p * 3 + a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        A[a][b] = S.m * st[2 * D + 1 + a * D + b] + (a == b ? sJ : 0.0f);
+        lA[a][b] = 0.0f;
+      }
+    }
+    for (int q = 0; q < kNO<D>; ++q) {
+      int o[3];
+      offset_of<D>(q, o);
+      float W, dW[3];
+      weight<D>(sc, o, W, dW);
+      const float4 ln = lgrid[node_of<D>(sc, o, S)];
+      float dpos[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) dpos[a] = ((float)o[a] - sc.fx[a]) * S.dx;
+      float lW = ln.x * S.m;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const float lPa = comp(ln, a);
+        float Ad = 0.0f;
+#pragma unroll
+        for (int b = 0; b < D; ++b) Ad += A[a][b] * dpos[b];
+        lW += lPa * (S.m * st[D + a] + Ad);
+        lv[a] += W * S.m * lPa;
+#pragma unroll
+        for (int b = 0; b < D; ++b) lA[a][b] += W * lPa * dpos[b];
+      }
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float ld = 0.0f;
+#pragma unroll
+        for (int a = 0; a < D; ++a) ld += A[a][b] * comp(ln, a);
+        lfx[b] += -S.dx * W * ld + lW * dW[b];
+      }
+    }
+    const float* lo = lam + p * NS;
+    float trA = 0.0f;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      l[a] = lo[a] + sc.dfx[a] * lfx[a];
+      l[D + a] = lv[a];
+      trA += lA[a][a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) l[2 * D + 1 + a * D + b] = S.m * lA[a][b];
+    }
+    l[2 * D] = lo[2 * D] + S.k * trA;
+    float* lw = lam + p * NS;
+#pragma unroll
+    for (int h = 0; h < NS; ++h) lw[h] = l[h];
+  }
+  if (g) tally<D>(l, valid, g);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- runtime
+struct qadj_ctx {
+  int dim = 3;
+  uint64_t n = 0, nn = 0;
+  int ns = 0;
+  AdjSim S{};
+  cudaStream_t stream = nullptr;
+  float4 *grid = nullptr, *gv = nullptr, *lgrid = nullptr;
+  float* lfx = nullptr;
+  double* dacc = nullptr;  // [ns] tallies + [1] z
+  std::vector<float*> pool;  // state / adjoint buffers [n][ns]
+  uint64_t launches = 0;
+};
+
+namespace {
+
+unsigned blocks(uint64_t n) { return (unsigned)((n + 255) / 256); }
+
+qmpm_status forward_dev(qadj_ctx* c, const float* in, float* out) {
+  ACK(cudaMemsetAsync(c->grid, 0, sizeof(float4) * c->nn, c->stream));
+  if (c->dim == 3) {
+    k_p2g_fwd<3><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->S, c->grid);
+    k_grid_fwd<3><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
+    k_g2p_fwd<3><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->gv, c->S, out);
+  } else {
+    k_p2g_fwd<2><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->S, c->grid);
+    k_grid_fwd<2><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
+    k_g2p_fwd<2><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->gv, c->S, out);
+  }
+  c->launches += 3;
+  ACK(cudaGetLastError());
+  return QMPM_OK;
+}
+
+// lambda_t from s_t and lambda_{t+1} (g nullable: device tallies to accumulate)
+qmpm_status adjoint_dev(qadj_ctx* c, const float* s, const float* lam1, float* lam, double* g) {
+  ACK(cudaMemsetAsync(c->grid, 0, sizeof(float4) * c->nn, c->stream));
+  ACK(cudaMemsetAsync(c->lgrid, 0, sizeof(float4) * c->nn, c->stream));
+  if (c->dim == 3) {
+    k_p2g_fwd<3><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->S, c->grid);
+    k_grid_fwd<3><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
+    k_g2p_bwd<3><<<blocks(c->n), 256, 0, c->stream>>>(s, lam1, c->n, c->gv, c->S, c->lgrid, lam, c->lfx);
+    k_grid_bwd<3><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->lgrid);
+    k_p2g_bwd<3><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->lgrid, c->S, c->lfx, lam, g);
+  } else {
+    k_p2g_fwd<2><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->S, c->grid);
+    k_grid_fwd<2><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
+    k_g2p_bwd<2><<<blocks(c->n), 256, 0, c->stream>>>(s, lam1, c->n, c->gv, c->S, c->lgrid, lam, c->lfx);
+    k_grid_bwd<2><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->lgrid);
+    k_p2g_bwd<2><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->lgrid, c->S, c->lfx, lam, g);
+  }
+  c->launches += 5;
+  ACK(cudaGetLastError());
+  return QMPM_OK;
+}
+
+qmpm_status get_buf(qadj_ctx* c, std::vector<float*>& freel, float** out) {
+  if (!freel.empty()) {
+    *out = freel.back();
+    freel.pop_back();
+    return QMPM_OK;
+  }
+  float* b = nullptr;
+  if (cudaMalloc(&b, sizeof(float) * c->n * c->ns) != cudaSuccess) {
+    cudaGetLastError();
+    return afail(QMPM_ENOMEM, "qadj: cannot allocate a checkpoint (%zu bytes)", sizeof(float) * c->n * c->ns);
+  }
+  c->pool.push_back(b);
+  *out = b;
+  return QMPM_OK;
+}
+
+struct Bisect {
+  qadj_ctx* c;
+  std::vector<float*> freel;
+  uint32_t resident = 0, max_resident = 0;
+  uint64_t fwd = 0, adj = 0;
+
+  // state at `to` from the state at `from` (k >= 1 steps) into a fresh buffer
+  qmpm_status advance(const float* s, uint32_t k, float** out) {
+    float *a = nullptr, *b = nullptr;
+    qmpm_status rc = get_buf(c, freel, &a);
+    if (!rc) rc = get_buf(c, freel, &b);
+    if (rc) return rc;
+    const float* cur = s;
+    for (uint32_t i = 0; i < k; ++i) {
+      float* dst = (i % 2 == 0) ? a : b;
+      rc = forward_dev(c, cur, dst);
+      if (rc) return rc;
+      cur = dst;
+      ++fwd;
+    }
+    *out = (float*)cur;
+    freel.push_back(cur == a ? b : a);
+    return QMPM_OK;
+  }
+
+  // lambda_lo (into lam_out) from the state at lo and lambda_hi
+  qmpm_status back(uint32_t lo, uint32_t hi, const float* s_lo, const float* lam_hi, float* lam_out, double* g) {
+    if (hi - lo == 1) {
+      ++adj;
+      return adjoint_dev(c, s_lo, lam_hi, lam_out, g);
+    }
+    const uint32_t mid = lo + (hi - lo) / 2;
+    float* s_mid = nullptr;
+    qmpm_status rc = advance(s_lo, mid - lo, &s_mid);
+    if (rc) return rc;
+    max_resident = std::max(max_resident, ++resident + 1);  // + s0
+    float* lam_mid = nullptr;
+    rc = get_buf(c, freel, &lam_mid);
+    if (!rc) rc = back(mid, hi, s_mid, lam_hi, lam_mid, g);
+    freel.push_back(s_mid);
+    --resident;
+    if (!rc) rc = back(lo, mid, s_lo, lam_mid, lam_out, g);
+    freel.push_back(lam_mid);
+    return rc;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+qmpm_status qadj_create(const qmpm_params* params, int32_t dim, int32_t material, uint64_t n, void* cuda_stream,
+                        qadj_ctx** out) {
+  if (!params || !out) return afail(QMPM_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (dim != 2 && dim != 3) return afail(QMPM_EINVAL, "dim must be 2 or 3");
+  if (material != QMPM_FLUID_J)
+    return afail(QMPM_EINVAL, "qadj: only the J-fluid adjoint is built (the fixed-corotated one is not)");
+  if (n == 0) return afail(QMPM_EINVAL, "n must be > 0");
+  for (int a = 0; a < dim; ++a)
+    if (params->grid_res[a] < 3) return afail(QMPM_EINVAL, "grid_res must be >= 3 per axis");
+  qadj_ctx* c = new qadj_ctx();
+  c->dim = dim;
+  c->n = n;
+  c->ns = 2 * dim + 1 + dim * dim;
+  c->stream = (cudaStream_t)cuda_stream;
+  AdjSim& S = c->S;
+  for (int a = 0; a < 3; ++a) {
+    S.res[a] = a < dim ? params->grid_res[a] : 1;
+    S.g[a] = params->gravity[a];
+  }
+  S.dx = params->dx;
+  S.inv_dx = 1.0f / params->dx;
+  S.dt = params->dt;
+  S.m = params->p_rho * params->p_vol;
+  S.k = -params->dt * params->p_vol * 4.0f * S.inv_dx * S.inv_dx * params->E;
+  S.bound = params->bound;
+  c->nn = (uint64_t)S.res[0] * S.res[1] * S.res[2];
+  cudaError_t e = cudaMalloc(&c->grid, sizeof(float4) * c->nn);
+  if (!e) e = cudaMalloc(&c->gv, sizeof(float4) * c->nn);
+  if (!e) e = cudaMalloc(&c->lgrid, sizeof(float4) * c->nn);
+  if (!e) e = cudaMalloc(&c->lfx, sizeof(float) * 3 * n);
+  if (!e) e = cudaMalloc(&c->dacc, sizeof(double) * (c->ns + 1));
+  if (e) {
+    cudaGetLastError();
+    qadj_destroy(c);
+    return afail(QMPM_ENOMEM, "qadj_create: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return QMPM_OK;
+}
+
+qmpm_status qadj_destroy(qadj_ctx* c) {
+  if (!c) return QMPM_OK;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : {(void*)c->grid, (void*)c->gv, (void*)c->lgrid, (void*)c->lfx, (void*)c->dacc})
+    if (p) cudaFree(p);
+  for (float* p : c->pool) cudaFree(p);
+  delete c;
+  return QMPM_OK;
+}
+
+qmpm_status qadj_forward(qadj_ctx* c, const float* s_in, float* s_out) {
+  if (!c || !s_in || !s_out) return afail(QMPM_EINVAL, "NULL argument");
+  return forward_dev(c, s_in, s_out);
+}
+
+qmpm_status qadj_adjoint_step(qadj_ctx* c, const float* s_t, const float* lam_next, float* lam_t, double* g) {
+  if (!c || !s_t || !lam_next || !lam_t) return afail(QMPM_EINVAL, "NULL argument");
+  if (lam_t == lam_next) return afail(QMPM_EINVAL, "lam_t must not alias lam_next");
+  return adjoint_dev(c, s_t, lam_next, lam_t, g);
+}
+
+qmpm_status qadj_gradient_tally(qadj_ctx* c, const float* s0, uint32_t T, double* g, double* z, float* lam0,
+                                qadj_stats* stats) {
+  if (!c || !s0 || !g) return afail(QMPM_EINVAL, "NULL argument");
+  const size_t bytes = sizeof(float) * c->n * c->ns;
+  Bisect B{c};
+  float *s_first = nullptr, *lamT = nullptr, *lam_out = nullptr;
+  qmpm_status rc = get_buf(c, B.freel, &s_first);
+  if (rc) return rc;
+  ACK(cudaMemcpyAsync(s_first, s0, bytes, cudaMemcpyDefault, c->stream));
+  ACK(cudaMemsetAsync(c->dacc, 0, sizeof(double) * (c->ns + 1), c->stream));
+  B.max_resident = 1;
+  // s_T, lambda_T (and z, the tally of lambda_T)
+  float* sT = s_first;
+  if (T > 0) {
+    rc = B.advance(s_first, T, &sT);
+    if (rc) return rc;
+    B.max_resident = 2;
+  }
+  rc = get_buf(c, B.freel, &lamT);
+  if (rc) return rc;
+  if (c->dim == 3)
+    k_lambda_T<3><<<blocks(c->n), 256, 0, c->stream>>>(sT, c->n, c->S, lamT, c->dacc, c->dacc + c->ns);
+  else
+    k_lambda_T<2><<<blocks(c->n), 256, 0, c->stream>>>(sT, c->n, c->S, lamT, c->dacc, c->dacc + c->ns);
+  c->launches += 1;
+  ACK(cudaGetLastError());
+  if (T > 0) B.freel.push_back(sT);
+  float* lam_final = lamT;
+  if (T > 0) {
+    rc = get_buf(c, B.freel, &lam_out);
+    if (rc) return rc;
+    rc = B.back(0, T, s_first, lamT, lam_out, c->dacc);
+    if (rc) return rc;
+    lam_final = lam_out;
+  }
+  std::vector<double> h(c->ns + 1);
+  ACK(cudaMemcpyAsync(h.data(), c->dacc, sizeof(double) * (c->ns + 1), cudaMemcpyDeviceToHost, c->stream));
+  if (lam0) ACK(cudaMemcpyAsync(lam0, lam_final, bytes, cudaMemcpyDefault, c->stream));
+  ACK(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < c->ns; ++i) g[i] = h[i];
+  if (z) *z = h[c->ns];
+  if (stats) {
+    stats->max_resident = B.max_resident;
+    stats->forward_steps = B.fwd;
+    stats->adjoint_steps = B.adj;
+  }
+  return QMPM_OK;
+}
+
+qmpm_status qadj_launch_count(const qadj_ctx* c, uint64_t* launches) {
+  if (!c || !launches) return afail(QMPM_EINVAL, "NULL argument");
+  *launches = c->launches;
+  return QMPM_OK;
+}
+
+}  // extern "C"

@@ -103,3 +103,28 @@ def test_create_without_gpu_fails_loudly_or_validates():
     h = ctypes.c_void_p()
     rc = qmpm.lib().qmpm_create(ctypes.byref(p), cs.ref, None, ctypes.byref(h))
     assert rc == 2
+
+
+def test_adjoint_header_symbols_exported_and_bound():
+    from paper_2207_04658_b200 import qadjoint
+    decl = declared_symbols("qadjoint.h", "qadj_")
+    assert len(decl) == 6
+    out = subprocess.check_output(["nm", "-D", "--defined-only", qmpm.LIB_PATH], text=True)
+    exported = set(l.split()[-1] for l in out.splitlines() if l.strip())
+    assert not [s for s in decl if s not in exported]
+    assert sorted(qadjoint.EXPORTS) == decl
+    L = qadjoint.lib()
+    for s in decl:
+        assert hasattr(L, s)
+
+
+def test_adjoint_create_rejects_bad_arguments_without_gpu():
+    import ctypes
+    from paper_2207_04658_b200 import qadjoint, scenes
+    sim, s0 = scenes.adjoint_fluid(dim=2, side=4)
+    p = qmpm.make_params(sim, s0.shape[0])
+    ctx = ctypes.c_void_p()
+    L = qadjoint.lib()
+    assert L.qadj_create(ctypes.byref(p), 2, 0, s0.shape[0], None, ctypes.byref(ctx)) == 1  # elastic
+    assert L.qadj_create(ctypes.byref(p), 4, 1, s0.shape[0], None, ctypes.byref(ctx)) == 1  # dim
+    assert L.qadj_create(ctypes.byref(p), 2, 1, 0, None, ctypes.byref(ctx)) == 1            # n = 0

@@ -1,0 +1,119 @@
+"""GPU parity of the gradient tallies (include/qadjoint.h) against the
+oracle (oracle/adjoint.py), through the C-ABI: the fp32 forward step and one adjoint step
+on identical inputs (fp32 vs fp64: within FWD_TOL / ADJ_TOL of each scalar's scale), the
+whole Algorithm 1 line 12 with bisection checkpointing against the oracle's store-all
+run, the GPU bisection against a GPU store-all loop, and the checkpoint counts."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import adjoint as adj
+from paper_2207_04658_b200 import qadjoint, qmpm, scenes
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+FWD_TOL = 2e-5  # one fp32 step vs fp64, relative to the column's max |value|
+ADJ_TOL = 2e-4  # adjoint: divisions by node masses amplify the fp32 rounding of u = P/m
+
+
+def col_err(g, o):
+    scale = np.maximum(np.abs(o).max(0), 1e-30)
+    return (np.abs(g.astype(np.float64) - o).max(0) / scale).max()
+
+
+CASES = [dict(dim=2, side=12, seed=1), dict(dim=3, side=8, seed=2),
+         dict(dim=2, side=10, seed=3, origin=0.02), dict(dim=3, side=6, seed=4, origin=0.05)]  # last two: walls
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_forward_matches_oracle(case):
+    sim, s0 = scenes.adjoint_fluid(**case)
+    A = qadjoint.Adjoint(sim, s0.shape[0])
+    si = torch.from_numpy(s0).cuda()
+    so = torch.empty_like(si)
+    A.forward(si, so)
+    o = adj.forward(sim, s0.astype(np.float64))
+    assert col_err(so.cpu().numpy(), o) <= FWD_TOL
+    A.close()
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_adjoint_step_matches_oracle(case):
+    sim, s0 = scenes.adjoint_fluid(**case)
+    n, ns = s0.shape
+    rng = np.random.default_rng(5)
+    lam1 = rng.normal(size=(n, ns)).astype(np.float32)
+    A = qadjoint.Adjoint(sim, n)
+    lam = torch.empty((n, ns), dtype=torch.float32, device="cuda")
+    g = torch.zeros(ns, dtype=torch.float64, device="cuda")
+    A.adjoint_step(torch.from_numpy(s0).cuda(), torch.from_numpy(lam1).cuda(), lam, g)
+    o = adj.adjoint_step(sim, s0.astype(np.float64), lam1.astype(np.float64))
+    gl = lam.cpu().numpy()
+    assert col_err(gl, o) <= ADJ_TOL, col_err(gl, o)
+    assert np.allclose(g.cpu().numpy(), np.sum(gl.astype(np.float64) ** 2, 0), rtol=1e-5)
+    A.close()
+
+
+@pytest.mark.parametrize("dim,T", [(2, 1), (2, 6), (3, 4), (3, 9)])
+def test_gradient_tally_matches_oracle(dim, T):
+    sim, s0 = scenes.adjoint_fluid(dim=dim, side=10 if dim == 2 else 6, seed=10 + T)
+    A = qadjoint.Adjoint(sim, s0.shape[0])
+    lam0 = np.zeros_like(s0)
+    g, z, st = A.gradient_tally(s0, T, lam0=lam0)
+    oz, og, ol = adj.backward_all(sim, s0, T)
+    assert abs(z - oz) <= 1e-5 * oz
+    assert np.all(np.abs(g - og) <= 1e-3 * np.maximum(og, og.max() * 1e-6)), (g, og)
+    assert col_err(lam0, ol) <= 10 * ADJ_TOL
+    assert st["adjoint_steps"] == T
+    assert st["forward_steps"] <= T + T * math.ceil(math.log2(max(T, 1)))
+    assert st["max_resident"] <= math.ceil(math.log2(max(T, 1))) + 2
+    assert A.launch_count() > 0
+    A.close()
+
+
+def test_bisection_equals_store_all_on_gpu():
+    sim, s0 = scenes.adjoint_fluid(dim=3, side=6, seed=21)
+    T = 7
+    n, ns = s0.shape
+    A = qadjoint.Adjoint(sim, n)
+    g_b, z_b, _ = A.gradient_tally(s0, T)
+    states = [torch.from_numpy(s0).cuda()]
+    for _ in range(T):
+        nxt = torch.empty_like(states[0])
+        A.forward(states[-1], nxt)
+        states.append(nxt)
+    m = sim["p_rho"] * sim["p_vol"]
+    lam = torch.zeros_like(states[0])
+    lam[:, 3:6] = m * states[T][:, 3:6]
+    g = (lam.double() ** 2).sum(0)
+    for t in range(T - 1, -1, -1):
+        nl = torch.empty_like(lam)
+        A.adjoint_step(states[t], lam, nl, g)
+        lam = nl
+    assert np.allclose(g.cpu().numpy(), g_b, rtol=1e-4)
+    A.close()
+
+
+def test_elastic_is_rejected():
+    sim, s0 = scenes.adjoint_fluid(dim=2, side=4)
+    with pytest.raises(qmpm.QmpmError) as e:
+        qadjoint.Adjoint(dict(sim, material="elastic"), s0.shape[0])
+    assert e.value.code == 1
+
+
+def test_tallies_drive_the_error_bounded_solver():
+    """Algorithm 1 end to end on the GPU pieces: ranges -> tallies -> Delta_h, b_h."""
+    sim, s0 = scenes.adjoint_fluid(dim=2, side=12, seed=30)
+    T = 8
+    A = qadjoint.Adjoint(sim, s0.shape[0])
+    g, z, _ = A.gradient_tally(s0, T)
+    A.close()
+    n, ns = s0.shape
+    R = np.maximum(np.abs(s0).max(0).astype(np.float64) * 2, 1e-3)
+    P = np.full(ns, float(n * (T + 1)))
+    delta, bits = qmpm.solve_error_bounded(P, np.maximum(g, 1e-30), R, z, 0.01)
+    assert np.all(bits >= 0) and np.all(bits <= 31)
+    sigma = qmpm.predict_error(delta, g)
+    assert sigma <= 0.01 * z * (1 + 1e-9)
