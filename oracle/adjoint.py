@@ -5,9 +5,11 @@ TEST INFRASTRUCTURE ONLY (same rule as the rest of oracle/).  Shares no code wit
 paper_2207_04658_b200/csrc/adjoint.cu.  The forward step is the C oracle's fp64
 p2g -> grid_update -> g2p (oracle/mpm_impl.h); this file adds its adjoint.
 
-Scope: the J-fluid material (reading Q15: stress = E (J-1) I),
-2D and 3D.  The adjoint of the fixed-corotated elastic (the polar decomposition's
-derivative) is not built.
+Scope: both materials, 2D and 3D -- the J-fluid (reading Q15:
+P F^T = E (J-1) I) and the fixed-corotated elastic (P F^T = 2 mu (F - R) F^T +
+lambda (J-1) J I) with the polar decomposition's derivative: from F = R S,
+skew(R^T dF) = (Omega S + S Omega)/2 with Omega = R^T dR, so (3D) the axial vector of
+Omega is (tr(S) I - S)^{-1} axial(R^T dF - dF^T R) and (2D) Omega = (R^T dF - dF^T R)/tr S.
 
   z = KE(s_T) = 1/2 m_p sum_p |v_{T,p}|^2                     (final kinetic energy)
   lambda_T = dz/ds_T = (0, m_p v_T, 0, 0)
@@ -34,8 +36,11 @@ import oracle
 def _consts(sim):
     d = sim["dim"]
     dx = float(sim["dx"])
+    E, nu = float(sim["E"]), float(sim["nu"])
     return dict(d=d, dx=dx, inv_dx=1.0 / dx, dt=float(sim["dt"]), m=float(sim["p_rho"] * sim["p_vol"]),
-                k=-float(sim["dt"]) * float(sim["p_vol"]) * 4.0 / (dx * dx) * float(sim["E"]),
+                k=-float(sim["dt"]) * float(sim["p_vol"]) * 4.0 / (dx * dx) * E,
+                scale=-float(sim["dt"]) * float(sim["p_vol"]) * 4.0 / (dx * dx),
+                mu=E / (2.0 * (1.0 + nu)), la=E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)),
                 g=np.asarray(sim["gravity"][:d], dtype=np.float64), bound=int(sim["bound"]),
                 res=np.asarray(sim["grid_res"][:d]))
 
@@ -80,18 +85,64 @@ def _offsets(d):
     return [(i, j, k) for i in range(3) for j in range(3) for k in range(3)]
 
 
+def _polar(F):
+    """R, S of F = R S (batched, det F > 0) by SVD."""
+    U, sig, Vt = np.linalg.svd(F)
+    R = U @ Vt
+    S = np.einsum("pji,pj,pjk->pik", Vt, sig, Vt)
+    return R, S
+
+
+def _stress_F_adjoint(c, F, lP):
+    """dL/dF for P F^T = 2 mu (F - R) F^T + lambda (J - 1) J I given dL/d(P F^T) = lP."""
+    d = F.shape[1]
+    mu, la = c["mu"], c["la"]
+    R, S = _polar(F)
+    J = np.linalg.det(F)
+    lF = 2.0 * mu * (np.einsum("pab,pbc->pac", lP, F) + np.einsum("pba,pbc->pac", lP, F - R))
+    lR = -2.0 * mu * np.einsum("pab,pbc->pac", lP, F)
+    G = np.einsum("pba,pbc->pac", R, lR)  # R^T lR
+    sk = 0.5 * (G - np.transpose(G, (0, 2, 1)))
+    if d == 3:
+        a = np.stack([sk[:, 2, 1], sk[:, 0, 2], sk[:, 1, 0]], -1)
+        K = np.trace(S, axis1=1, axis2=2)[:, None, None] * np.eye(3)[None] - S
+        cc = np.linalg.solve(K, a[..., None])[..., 0]
+        X = np.zeros_like(F)
+        X[:, 0, 1], X[:, 0, 2], X[:, 1, 2] = -cc[:, 2], cc[:, 1], -cc[:, 0]
+        X[:, 1, 0], X[:, 2, 0], X[:, 2, 1] = cc[:, 2], -cc[:, 1], cc[:, 0]
+        lF += 2.0 * np.einsum("pab,pbc->pac", R, X)
+    else:
+        lF += 2.0 * np.einsum("pab,pbc->pac", R, sk) / np.trace(S, axis1=1, axis2=2)[:, None, None]
+    lJ = la * (2.0 * J - 1.0) * np.trace(lP, axis1=1, axis2=2)
+    lF += (lJ * J)[:, None, None] * np.transpose(np.linalg.inv(F), (0, 2, 1))
+    return lF
+
+
+def _stress(c, F):
+    R, _ = _polar(F)
+    J = np.linalg.det(F)
+    d = F.shape[1]
+    PFt = 2.0 * c["mu"] * np.einsum("pab,pcb->pac", F - R, F) + (c["la"] * (J - 1.0) * J)[:, None, None] * np.eye(d)
+    return c["scale"] * PFt
+
+
 def adjoint_step(sim, s, lam_next):
-    """lambda_t = (d s_{t+1} / d s_t)^T lambda_{t+1} for the J-fluid (fp64)."""
-    assert sim["material"] == "fluid"
+    """lambda_t = (d s_{t+1} / d s_t)^T lambda_{t+1} (fp64), J-fluid or fixed-corotated."""
+    fluid = sim["material"] == "fluid"
     c = _consts(sim)
     d, dx, inv_dx, dt, m, k = c["d"], c["dx"], c["inv_dx"], c["dt"], c["m"], c["k"]
     s = np.asarray(s, dtype=np.float64)
     lam1 = np.asarray(lam_next, dtype=np.float64)
     n = s.shape[0]
-    x, v, J = s[:, :d], s[:, d:2 * d], s[:, 2 * d]
-    C = s[:, 2 * d + 1:].reshape(n, d, d)
-    lx1, lv1, lJ1 = lam1[:, :d], lam1[:, d:2 * d], lam1[:, 2 * d]
-    lC1 = lam1[:, 2 * d + 1:].reshape(n, d, d)
+    nF = 1 if fluid else d * d
+    x, v = s[:, :d], s[:, d:2 * d]
+    C = s[:, 2 * d + nF:].reshape(n, d, d)
+    lx1, lv1 = lam1[:, :d], lam1[:, d:2 * d]
+    lC1 = lam1[:, 2 * d + nF:].reshape(n, d, d)
+    if fluid:
+        J, lJ1 = s[:, 2 * d], lam1[:, 2 * d]
+    else:
+        F, lF1 = s[:, 2 * d:2 * d + nF].reshape(n, d, d), lam1[:, 2 * d:2 * d + nF].reshape(n, d, d)
 
     # forward recompute: grid of step t
     grid, origin, gsize, _ = oracle.p2g(sim, s)
@@ -125,12 +176,17 @@ def adjoint_step(sim, s, lam_next):
         vi = gv[node(o)][:, 1:1 + d]
         dpc = np.asarray(o, dtype=np.float64)[None, :] - fx
         newC += 4.0 * inv_dx * W[:, None, None] * vi[:, :, None] * dpc[:, None, :]
-    trC = np.trace(newC, axis1=1, axis2=2)
     lam = np.zeros_like(s)
     lx = lx1.copy()
-    lJ = lJ1 * (1.0 + dt * trC)
     lv_tot = lv1 + dt * lx1
-    lC_tot = lC1 + (lJ1 * J * dt)[:, None, None] * np.eye(d)[None]
+    if fluid:  # J' = J (1 + dt tr C')
+        trC = np.trace(newC, axis1=1, axis2=2)
+        lJ = lJ1 * (1.0 + dt * trC)
+        lC_tot = lC1 + (lJ1 * J * dt)[:, None, None] * np.eye(d)[None]
+    else:  # F' = (I + dt C') F
+        Gm = np.eye(d)[None] + dt * newC
+        lF = np.einsum("pba,pbc->pac", Gm, lF1)
+        lC_tot = lC1 + dt * np.einsum("pab,pcb->pac", lF1, F)
     lfx = np.zeros((n, d))
     lgrid_v = np.zeros(gv.shape[:3] + (d,))
     for o in offs:
@@ -157,8 +213,11 @@ def adjoint_step(sim, s, lam_next):
     lP = lvt / safe_m[..., None]
     lm = -np.sum(lvt * u, -1) / safe_m
 
-    # ---- P2G reverse: m_i += W m, P_i += W (m v + A dpos), A = k (J - 1) I + m C
-    A = (k * (J - 1.0))[:, None, None] * np.eye(d)[None] + m * C
+    # ---- P2G reverse: m_i += W m, P_i += W (m v + A dpos), A = stress + m C
+    if fluid:
+        A = (k * (J - 1.0))[:, None, None] * np.eye(d)[None] + m * C
+    else:
+        A = _stress(c, F) + m * C
     lv = np.zeros((n, d))
     lA = np.zeros((n, d, d))
     for o in offs:
@@ -174,12 +233,14 @@ def adjoint_step(sim, s, lam_next):
         ldpos = W[:, None] * np.einsum("pab,pa->pb", A, lPi)
         lfx += -dx * ldpos + lW[:, None] * dW
     lC = m * lA
-    lJ = lJ + k * np.trace(lA, axis1=1, axis2=2)
     lx = lx + dfx * lfx
     lam[:, :d] = lx
     lam[:, d:2 * d] = lv
-    lam[:, 2 * d] = lJ
-    lam[:, 2 * d + 1:] = lC.reshape(n, d * d)
+    if fluid:
+        lam[:, 2 * d] = lJ + k * np.trace(lA, axis1=1, axis2=2)
+    else:
+        lam[:, 2 * d:2 * d + nF] = (lF + _stress_F_adjoint(c, F, c["scale"] * lA)).reshape(n, nF)
+    lam[:, 2 * d + nF:] = lC.reshape(n, d * d)
     return lam
 
 

@@ -382,3 +382,19 @@ def adjoint_fluid(dim=2, side=8, res=32, seed=0, dt=2e-4, E=50.0, vmax=1.0, jitt
     J = 1.0 + rng.uniform(-dJ, dJ, (n, 1))
     C = rng.uniform(-cmax, cmax, (n, dim * dim))
     return sim, np.concatenate([x, v, J, C], 1).astype(np.float32)
+
+
+def adjoint_elastic(dim=2, side=8, res=32, seed=0, dt=2e-4, E=500.0, nu=0.2, vmax=1.0, jitter=0.25, dF=0.05,
+                    cmax=2.0, ppc=2, origin=0.35, gravity=None):
+    """A seeded fixed-corotated block for the gradient-tally path: as adjoint_fluid, with
+    F = I + U(-dF, dF) per entry (det F > 0) instead of J.  Returns (sim, state float32)."""
+    rng = np.random.default_rng(seed)
+    sim = _sim(dim, "elastic", (res,) * dim, dt, E, p_vol=(1.0 / res / ppc) ** dim, nu=nu, gravity=gravity)
+    h = sim["dx"] / ppc
+    grid = np.stack(np.meshgrid(*[np.arange(side)] * dim, indexing="ij"), -1).reshape(-1, dim)
+    x = origin + (grid + 0.5 + rng.uniform(-jitter, jitter, grid.shape)) * h
+    n = x.shape[0]
+    v = rng.uniform(-vmax, vmax, (n, dim))
+    F = np.eye(dim).reshape(1, -1) + rng.uniform(-dF, dF, (n, dim * dim))
+    C = rng.uniform(-cmax, cmax, (n, dim * dim))
+    return sim, np.concatenate([x, v, F, C], 1).astype(np.float32)

@@ -30,14 +30,21 @@ def lam0(sim, s0, T):
     return lam
 
 
+def make(material, **kw):
+    return (scenes.adjoint_fluid if material == "fluid" else scenes.adjoint_elastic)(**kw)
+
+
+@pytest.mark.parametrize("material", ["fluid", "elastic"])
 @pytest.mark.parametrize("dim,T", [(2, 1), (2, 3), (3, 2)])
-def test_adjoint_matches_finite_differences(dim, T):
-    sim, s0 = scenes.adjoint_fluid(dim=dim, side=6 if dim == 2 else 4, seed=dim + T)
+def test_adjoint_matches_finite_differences(material, dim, T):
+    sim, s0 = make(material, dim=dim, side=6 if dim == 2 else 4, seed=dim + T)
     s0 = s0.astype(np.float64)
     lam = lam0(sim, s0, T)
     rng = np.random.default_rng(7)
     scale = np.ones(s0.shape[1])
     scale[:dim] = sim["dx"] * 1e-2  # positions: stay well inside a cell
+    if material == "elastic":
+        scale[2 * dim:2 * dim + dim * dim] = 1e-2  # the stiff F directions: small steps
     for trial in range(3):
         e = rng.normal(size=s0.shape) * scale
         eps = 1e-4
@@ -46,17 +53,18 @@ def test_adjoint_matches_finite_differences(dim, T):
         assert abs(fd - an) <= 1e-6 * max(abs(fd), 1e-12) + 1e-9 * np.abs(lam * e).sum(), (trial, fd, an)
 
 
-def test_adjoint_single_coordinates_of_every_kind():
-    """One coordinate of each kind (x, v, J, C) of one particle: a dropped term in any
-    branch of the adjoint fails here."""
-    dim, T = 2, 2
-    sim, s0 = scenes.adjoint_fluid(dim=dim, side=5, seed=3)
+@pytest.mark.parametrize("material,dim", [("fluid", 2), ("elastic", 2), ("elastic", 3)])
+def test_adjoint_single_coordinates_of_every_kind(material, dim):
+    """One coordinate of each kind (x, v, J or F, C) of one particle: a dropped term in
+    any branch of the adjoint fails here."""
+    T = 2
+    sim, s0 = make(material, dim=dim, side=5 if dim == 2 else 4, seed=3)
     s0 = s0.astype(np.float64)
     lam = lam0(sim, s0, T)
     p = 7
     for h in range(s0.shape[1]):
         e = np.zeros_like(s0)
-        e[p, h] = sim["dx"] * 1e-2 if h < dim else 1.0
+        e[p, h] = sim["dx"] * 1e-2 if h < dim else (1e-2 if material == "elastic" and h < 2 * dim + dim * dim else 1.0)
         eps = 1e-4
         fd = (z_of(sim, s0 + eps * e, T) - z_of(sim, s0 - eps * e, T)) / (2 * eps)
         an = float(np.sum(lam * e))
