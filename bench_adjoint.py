@@ -2,12 +2,12 @@
 include/qadjoint.h): T forward fp32 steps, KE(s_T), back-propagation with the paper's
 bisection checkpointing, g_h per state scalar.
 
-Default workload: the paper's error-bounded MPM experiment size (80,000
-particles, 128^2 grid, 8192 steps, dt 2e-4) with the J-fluid material (the elastic
-adjoint is not built): 2D, 283^2 = 80,089 particles at 16 per cell.  --config 3d: 1M
-particles (100^3, 8 per cell) on 128^3, T = 64.
+Default workload: the paper's error-bounded MPM experiment (an elastic body,
+80,000 particles, 128^2 grid, 8192 steps, dt 2e-4): 2D fixed-corotated, 283^2 = 80,089
+particles at 16 per cell.  --config 3d: 1M elastic particles (100^3, 8 per cell) on
+128^3, T = 64; 2d-fluid / 3d-fluid: the same with the J-fluid.
 
-    python bench_adjoint.py [--config 2d|3d] [--steps T]
+    python bench_adjoint.py [--config 2d|3d|2d-fluid|3d-fluid] [--steps T]
     python bench_adjoint.py --impl reference     # the numpy oracle on a bounded sample
 
 One JSON line: metric = particle-steps of the whole tally (n T) per second.
@@ -24,8 +24,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIGS = {"2d": dict(dim=2, side=283, res=128, ppc=4, T=8192, origin=0.2),
-           "3d": dict(dim=3, side=100, res=128, ppc=2, T=64, origin=0.2)}
+CONFIGS = {"2d": dict(material="elastic", dim=2, side=283, res=128, ppc=4, T=8192, origin=0.2),
+           "3d": dict(material="elastic", dim=3, side=100, res=128, ppc=2, T=64, origin=0.2),
+           "2d-fluid": dict(material="fluid", dim=2, side=283, res=128, ppc=4, T=8192, origin=0.2),
+           "3d-fluid": dict(material="fluid", dim=3, side=100, res=128, ppc=2, T=64, origin=0.2)}
 
 
 def parse():
@@ -42,12 +44,16 @@ def parse():
 
 def scene(cfg):
     from paper_2207_04658_b200 import scenes
-    return scenes.adjoint_fluid(dim=cfg["dim"], side=cfg["side"], res=cfg["res"], ppc=cfg["ppc"], seed=0,
-                                vmax=0.5, cmax=0.5, dJ=0.01, origin=cfg["origin"])
+    kw = dict(dim=cfg["dim"], side=cfg["side"], res=cfg["res"], ppc=cfg["ppc"], seed=0, vmax=0.5, cmax=0.5,
+              origin=cfg["origin"])
+    if cfg["material"] == "fluid":
+        return scenes.adjoint_fluid(dJ=0.01, **kw)
+    return scenes.adjoint_elastic(dF=0.01, **kw)
 
 
 def workload(cfg, n, T):
-    return (f"gradient tallies, {cfg['dim']}D J-fluid, {n:,} particles, {cfg['res']}^{cfg['dim']} grid, T = {T} "
+    mat = "J-fluid" if cfg["material"] == "fluid" else "fixed-corotated elastic"
+    return (f"gradient tallies, {cfg['dim']}D {mat}, {n:,} particles, {cfg['res']}^{cfg['dim']} grid, T = {T} "
             f"steps, KE(s_T), bisection checkpointing")
 
 

@@ -6,13 +6,14 @@
  *
  *   z   = KE(s_T) = 1/2 m_p sum_p |v_{T,p}|^2             (the evaluation function)
  *   g_h = sum_{t=0..T} sum_p (dz / ds_{t,p,h})^2           (Eq. 8)
- * with one type h per state scalar (x_a, v_a, J, C_ab: the order of qmpm.h's state rows).
+ * with one type h per state scalar (x_a, v_a, J | F_ab, C_ab: the order of qmpm.h's state rows).
  * The g_h feed qmpm_solve_error_bounded / qmpm_solve_memory_bounded (qmpm.h).
  *
- * Scope: the J-fluid material (reading Q15), 2D and 3D; the step is the MLS-MPM step of
- * qmpm.h in fp32 on a dense grid of grid_res nodes (16 B per node, 3 grids), state rows
- * fp32 [n][ns], ns = 2d + 1 + d^2.  The fixed-corotated elastic adjoint is not built
- * (QMPM_EINVAL).  DESIGN.md §13.
+ * Scope: both materials (QMPM_FLUID_J, reading Q15; QMPM_ELASTIC_FCR, whose
+ * adjoint differentiates the polar decomposition), 2D and 3D; the step is the MLS-MPM
+ * step of qmpm.h in fp32 on a dense grid of grid_res nodes (16 B per node, 3 grids),
+ * state rows fp32 [n][ns] in qmpm.h's scalar order, ns = 2d + 1 + d^2 (fluid) or
+ * 2d + 2d^2 (elastic).  DESIGN.md §13.
  *
  * Conventions as qmpm.h.  Device pointers unless marked "host or device"; work goes to
  * the ctx stream; qadj_gradient_tally synchronizes.
@@ -34,9 +35,10 @@ typedef struct {
     uint64_t adjoint_steps; /* T */
 } qadj_stats;
 
-/* A ctx for n particles of dimension dim (2 | 3) and material QMPM_FLUID_J; params as
- * qmpm_create's (grid_res, dx, dt, gravity, p_rho, p_vol, E, bound; flags and
- * capacities ignored).  QMPM_EINVAL for another material or bad sizes, QMPM_ENOMEM. */
+/* A ctx for n particles of dimension dim (2 | 3) and material (QMPM_ELASTIC_FCR |
+ * QMPM_FLUID_J); params as qmpm_create's (grid_res, dx, dt, gravity, p_rho, p_vol, E,
+ * nu, bound; flags and capacities ignored).  QMPM_EINVAL for bad sizes or an unknown
+ * material, QMPM_ENOMEM. */
 qmpm_status qadj_create(const qmpm_params* params, int32_t dim, int32_t material, uint64_t n, void* cuda_stream,
                         qadj_ctx** out);
 qmpm_status qadj_destroy(qadj_ctx* ctx); /* synchronizes; NULL is a no-op */

@@ -1,10 +1,11 @@
 // adjoint.cu -- gradient tallies g_h of Algorithm 1 line 12 (Eq. 8,
-// P:337; "Gradient Computation") on the GPU: the full-precision (fp32) J-fluid
-// MLS-MPM step on a dense grid, its adjoint, and the paper's bisection checkpointing.
+// P:337; "Gradient Computation") on the GPU: the full-precision (fp32)
+// MLS-MPM step (J-fluid or fixed-corotated elastic) on a dense grid, its adjoint, and
+// the paper's bisection checkpointing.
 // C ABI: include/qadjoint.h.  DESIGN.md §13.
 //
 // Forward (the same rules as the quantized step's, with fp32 state rows
-// [n][ns] = x, v, J, C instead of records): P2G into a dense float4 grid (m, P) with
+// [n][ns] = x, v, J | F, C instead of records): P2G into a dense float4 grid (m, P) with
 // atomics, grid update (v = P/m + dt g, separating walls), G2P.
 // Adjoint of one step, lambda_t = (ds_{t+1}/ds_t)^T lambda_{t+1}, in three kernels:
 //   g2p_bwd  gathers v_i, scatters the node adjoints W (lv' + 4/dx lC' (o - fx)) with
@@ -14,7 +15,9 @@
 //   p2g_bwd  gathers (lm, lP), finishes lambda_t (lv, lC, lJ from the stress, lx through
 //            fx) and folds sum_p lambda^2 per scalar into the tallies (double atomics)
 // Every derivative is the forward's as written: floor() is constant, clamps have zero
-// derivative.  The elastic material (the polar decomposition's derivative) is not built.
+// derivative.  Both materials: the J-fluid (reading Q15) and the fixed-corotated
+// elastic, whose stress adjoint differentiates the polar decomposition F = R S through
+// skew(R^T dF) = (Omega S + S Omega)/2, Omega = R^T dR (oracle/adjoint.py states it).
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -25,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include "qadjoint.h"
+#include "qmpm_device.cuh"  // polar2 / polar3 (Newton-Higham), as the quantized step
 
 namespace qmpm {
 void set_thread_error(const char* msg);  // api.cu
@@ -34,7 +38,8 @@ struct AdjSim {
   int res[3];
   float dx, inv_dx, dt;
   float g[3];
-  float m, k;  // particle mass; stress factor -dt V_p 4/dx^2 E
+  float m, k;  // particle mass; fluid stress factor -dt V_p 4/dx^2 E
+  float scale, mu, la;  // elastic: -dt V_p 4/dx^2, Lame parameters
   int bound;
 };
 
@@ -91,8 +96,10 @@ __device__ __forceinline__ Stencil<D> stencil(const float* x, const AdjSim& S) {
   return st;
 }
 
-template <int D>
-constexpr int kNS = 2 * D + 1 + D * D;
+template <int D, bool EL>
+constexpr int kNS = 2 * D + (EL ? D * D : 1) + D * D;
+template <int D, bool EL>
+constexpr int kCO = 2 * D + (EL ? D * D : 1);  // offset of C in a state row
 template <int D>
 constexpr int kNO = D == 3 ? 27 : 9;
 
@@ -126,20 +133,164 @@ __device__ __forceinline__ void weight(const Stencil<D>& st, const int* o, float
   }
 }
 
-// ---------------------------------------------------------------- forward
+// ---- fixed-corotated stress and its adjoint
 template <int D>
+__device__ __forceinline__ void cof(const float* F, float* c) {  // cofactor matrix = J F^{-T}
+  if (D == 3) {
+    c[0] = F[4] * F[8] - F[5] * F[7];
+    c[1] = F[5] * F[6] - F[3] * F[8];
+    c[2] = F[3] * F[7] - F[4] * F[6];
+    c[3] = F[2] * F[7] - F[1] * F[8];
+    c[4] = F[0] * F[8] - F[2] * F[6];
+    c[5] = F[1] * F[6] - F[0] * F[7];
+    c[6] = F[1] * F[5] - F[2] * F[4];
+    c[7] = F[2] * F[3] - F[0] * F[5];
+    c[8] = F[0] * F[4] - F[1] * F[3];
+  } else {
+    c[0] = F[3], c[1] = -F[2], c[2] = -F[1], c[3] = F[0];
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void polarD(const float* F, float* R) {
+  if constexpr (D == 3)
+    qmpm::polar3(F, R);
+  else
+    qmpm::polar2(F, R);
+}
+
+// A_stress = scale (2 mu (F - R) F^T + la (J - 1) J I)
+template <int D>
+__device__ __forceinline__ void stress_el(const float* F, const AdjSim& S, float (*A)[D]) {
+  float R[D * D], c[D * D];
+  polarD<D>(F, R);
+  cof<D>(F, c);
+  float J = 0.0f;
+#pragma unroll
+  for (int b = 0; b < D; ++b) J += F[b] * c[b];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int e = 0; e < D; ++e) acc += (F[a * D + e] - R[a * D + e]) * F[b * D + e];
+      A[a][b] = S.scale * (2.0f * S.mu * acc + (a == b ? S.la * (J - 1.0f) * J : 0.0f));
+    }
+}
+
+// lF += d/dF of <lP, P F^T> (lP = dL/d(P F^T))
+template <int D>
+__device__ __forceinline__ void stress_el_adj(const float* F, const float (*lP)[D], const AdjSim& S, float* lF) {
+  float R[D * D], c[D * D];
+  polarD<D>(F, R);
+  cof<D>(F, c);
+  float J = 0.0f, trP = 0.0f;
+#pragma unroll
+  for (int b = 0; b < D; ++b) J += F[b] * c[b];
+#pragma unroll
+  for (int a = 0; a < D; ++a) trP += lP[a][a];
+  float lR[D][D], Sm[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      float pf = 0.0f, pt = 0.0f, rs = 0.0f;
+#pragma unroll
+      for (int e = 0; e < D; ++e) {
+        pf += lP[a][e] * F[e * D + b];                          // (lP F)_ab
+        pt += lP[e][a] * (F[e * D + b] - R[e * D + b]);         // (lP^T (F - R))_ab
+        rs += R[e * D + a] * F[e * D + b];                      // (R^T F)_ab = S
+      }
+      lF[a * D + b] += 2.0f * S.mu * (pf + pt) + S.la * (2.0f * J - 1.0f) * trP * c[a * D + b];
+      lR[a][b] = -2.0f * S.mu * pf;
+      Sm[a][b] = rs;
+    }
+  // G = R^T lR, sk = skew(G)
+  float sk[D][D];
+  {
+    float G[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int e = 0; e < D; ++e) acc += R[e * D + a] * lR[e][b];
+        G[a][b] = acc;
+      }
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) sk[a][b] = 0.5f * (G[a][b] - G[b][a]);
+  }
+  float X[D][D];
+  if constexpr (D == 3) {
+    // c = (tr S I - S)^{-1} axial(sk), X = [c]x; S symmetrised
+    const float a0 = sk[2][1], a1 = sk[0][2], a2 = sk[1][0];
+    const float tr = Sm[0][0] + Sm[1][1] + Sm[2][2];
+    float K[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) K[a * 3 + b] = (a == b ? tr : 0.0f) - 0.5f * (Sm[a][b] + Sm[b][a]);
+    float kc[9];
+    cof<3>(K, kc);
+    const float kd = K[0] * kc[0] + K[1] * kc[1] + K[2] * kc[2];
+    // K^{-1} = cof(K)^T / det K (K symmetric: cof(K) symmetric)
+    const float c0 = (kc[0] * a0 + kc[3] * a1 + kc[6] * a2) / kd;
+    const float c1 = (kc[1] * a0 + kc[4] * a1 + kc[7] * a2) / kd;
+    const float c2 = (kc[2] * a0 + kc[5] * a1 + kc[8] * a2) / kd;
+    X[0][0] = 0.f, X[0][1] = -c2, X[0][2] = c1;
+    X[1][0] = c2, X[1][1] = 0.f, X[1][2] = -c0;
+    X[2][0] = -c1, X[2][1] = c0, X[2][2] = 0.f;
+  } else {
+    const float tr = Sm[0][0] + Sm[1][1];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) X[a][b] = sk[a][b] / tr;
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int e = 0; e < D; ++e) acc += R[a * D + e] * X[e][b];
+      lF[a * D + b] += 2.0f * acc;
+    }
+}
+
+// ---------------------------------------------------------------- forward
+// the affine matrix A = stress + m C of a state row (fluid: k (J - 1) I)
+template <int D, bool EL>
+__device__ __forceinline__ void affine(const float* st, const AdjSim& S, float (*A)[D]) {
+  constexpr int CO = kCO<D, EL>;
+  if constexpr (EL) {
+    stress_el<D>(st + 2 * D, S, A);
+  } else {
+    const float sJ = S.k * (st[2 * D] - 1.0f);
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) A[a][b] = a == b ? sJ : 0.0f;
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) A[a][b] += S.m * st[CO + a * D + b];
+}
+
+template <int D, bool EL>
 __global__ void k_p2g_fwd(const float* __restrict__ s, uint64_t n, AdjSim S, float4* __restrict__ grid) {
-  constexpr int NS = kNS<D>;
+  constexpr int NS = kNS<D, EL>;
   const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const float* st = s + p * NS;
   const Stencil<D> sc = stencil<D>(st, S);
   float A[D][D];
-  const float sJ = S.k * (st[2 * D] - 1.0f);
-#pragma unroll
-  for (int a = 0; a < D; ++a)
-#pragma unroll
-    for (int b = 0; b < D; ++b) A[a][b] = S.m * st[2 * D + 1 + a * D + b] + (a == b ? sJ : 0.0f);
+  affine<D, EL>(st, S, A);
   for (int q = 0; q < kNO<D>; ++q) {
     int o[3];
     offset_of<D>(q, o);
@@ -189,15 +340,10 @@ __global__ void k_grid_fwd(const float4* __restrict__ grid, uint64_t nn, AdjSim 
   gv[c] = out;
 }
 
+// v' and C' of a particle from the updated grid
 template <int D>
-__global__ void k_g2p_fwd(const float* __restrict__ s, uint64_t n, const float4* __restrict__ gv, AdjSim S,
-                          float* __restrict__ out) {
-  constexpr int NS = kNS<D>;
-  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const float* st = s + p * NS;
-  const Stencil<D> sc = stencil<D>(st, S);
-  float v[D], C[D][D];
+__device__ __forceinline__ void gather(const Stencil<D>& sc, const float4* __restrict__ gv, const AdjSim& S, float* v,
+                                       float (*C)[D]) {
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     v[a] = 0.0f;
@@ -218,26 +364,49 @@ __global__ void k_g2p_fwd(const float* __restrict__ s, uint64_t n, const float4*
       for (int b = 0; b < D; ++b) C[a][b] += 4.0f * S.inv_dx * W * vi * ((float)o[b] - sc.fx[b]);
     }
   }
+}
+
+template <int D, bool EL>
+__global__ void k_g2p_fwd(const float* __restrict__ s, uint64_t n, const float4* __restrict__ gv, AdjSim S,
+                          float* __restrict__ out) {
+  constexpr int NS = kNS<D, EL>, CO = kCO<D, EL>;
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float* st = s + p * NS;
+  const Stencil<D> sc = stencil<D>(st, S);
+  float v[D], C[D][D];
+  gather<D>(sc, gv, S, v, C);
   float* o = out + p * NS;
-  float tr = 0.0f;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     o[a] = st[a] + S.dt * v[a];
     o[D + a] = v[a];
-    tr += C[a][a];
   }
-  o[2 * D] = st[2 * D] * (1.0f + S.dt * tr);
+  if constexpr (EL) {  // F' = (I + dt C') F
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int e = 0; e < D; ++e) acc += ((a == e ? 1.0f : 0.0f) + S.dt * C[a][e]) * st[2 * D + e * D + b];
+        o[2 * D + a * D + b] = acc;
+      }
+  } else {  // J' = J (1 + dt tr C')
+    float tr = 0.0f;
+#pragma unroll
+    for (int a = 0; a < D; ++a) tr += C[a][a];
+    o[2 * D] = st[2 * D] * (1.0f + S.dt * tr);
+  }
 #pragma unroll
   for (int a = 0; a < D; ++a)
 #pragma unroll
-    for (int b = 0; b < D; ++b) o[2 * D + 1 + a * D + b] = C[a][b];
+    for (int b = 0; b < D; ++b) o[CO + a * D + b] = C[a][b];
 }
 
 // ---------------------------------------------------------------- adjoint
-// lambda_T = (0, m v_T, 0, 0), the kinetic energy z and the tally of lambda_T
-template <int D>
+template <int NS>
 __device__ __forceinline__ void tally(const float* lam, bool valid, double* g) {
-  constexpr int NS = kNS<D>;
   const unsigned full = 0xffffffffu;
 #pragma unroll
   for (int h = 0; h < NS; ++h) {
@@ -248,10 +417,11 @@ __device__ __forceinline__ void tally(const float* lam, bool valid, double* g) {
   }
 }
 
-template <int D>
+// lambda_T = (0, m v_T, 0, 0), the kinetic energy z and the tally of lambda_T
+template <int D, bool EL>
 __global__ void k_lambda_T(const float* __restrict__ s, uint64_t n, AdjSim S, float* __restrict__ lam, double* g,
                            double* z) {
-  constexpr int NS = kNS<D>;
+  constexpr int NS = kNS<D, EL>;
   const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = p < n;
   float l[NS];
@@ -268,42 +438,60 @@ __global__ void k_lambda_T(const float* __restrict__ s, uint64_t n, AdjSim S, fl
 #pragma unroll
     for (int h = 0; h < NS; ++h) lam[p * NS + h] = l[h];
   }
-  tally<D>(l, valid, g);
+  tally<NS>(l, valid, g);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, off);
   if ((threadIdx.x & 31) == 0 && ke != 0.0f) atomicAdd(z, (double)ke);
 }
 
 // G2P reverse: node adjoints lgrid.yzw += W (lv' + 4/dx lC' (o - fx)); particle partials:
-// lam_t = (lx', 0, lJ' (1 + dt tr C'), 0) and lfx = d/dfx through G2P
-template <int D>
+// lam_t = (lx', 0, lJ' (1 + dt tr C') | (I + dt C')^T lF', 0) and lfx through G2P
+template <int D, bool EL>
 __global__ void k_g2p_bwd(const float* __restrict__ s, const float* __restrict__ lam1, uint64_t n,
                           const float4* __restrict__ gv, AdjSim S, float4* __restrict__ lgrid,
                           float* __restrict__ lam, float* __restrict__ lfx_out) {
-  constexpr int NS = kNS<D>;
+  constexpr int NS = kNS<D, EL>, CO = kCO<D, EL>;
   const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const float* st = s + p * NS;
   const float* l1 = lam1 + p * NS;
   const Stencil<D> sc = stencil<D>(st, S);
-  // tr C' (forward recompute)
-  float tr = 0.0f;
-  for (int q = 0; q < kNO<D>; ++q) {
-    int o[3];
-    offset_of<D>(q, o);
-    float W, dW[3];
-    weight<D>(sc, o, W, dW);
-    const float4 nd = gv[node_of<D>(sc, o, S)];
-#pragma unroll
-    for (int a = 0; a < D; ++a) tr += 4.0f * S.inv_dx * W * comp(nd, a) * ((float)o[a] - sc.fx[a]);
-  }
-  const float J = st[2 * D], lJ1 = l1[2 * D];
+  float vnew[D], Cn[D][D];
+  gather<D>(sc, gv, S, vnew, Cn);  // forward recompute of C'
   float lv[D], lC[D][D];
+  float* lo = lam + p * NS;
+#pragma unroll
+  for (int h = 0; h < NS; ++h) lo[h] = 0.0f;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     lv[a] = l1[D + a] + S.dt * l1[a];
+    lo[a] = l1[a];
 #pragma unroll
-    for (int b = 0; b < D; ++b) lC[a][b] = l1[2 * D + 1 + a * D + b] + (a == b ? lJ1 * J * S.dt : 0.0f);
+    for (int b = 0; b < D; ++b) lC[a][b] = l1[CO + a * D + b];
+  }
+  if constexpr (EL) {
+    // lF = (I + dt C')^T lF',  lC' += dt lF' F^T
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float acc = 0.0f, acc2 = 0.0f;
+#pragma unroll
+        for (int e = 0; e < D; ++e) {
+          acc += ((e == a ? 1.0f : 0.0f) + S.dt * Cn[e][a]) * l1[2 * D + e * D + b];
+          acc2 += l1[2 * D + a * D + e] * st[2 * D + b * D + e];
+        }
+        lo[2 * D + a * D + b] = acc;
+        lC[a][b] += S.dt * acc2;
+      }
+  } else {
+    float tr = 0.0f;
+#pragma unroll
+    for (int a = 0; a < D; ++a) tr += Cn[a][a];
+    const float lJ1 = l1[2 * D];
+    lo[2 * D] = lJ1 * (1.0f + S.dt * tr);
+#pragma unroll
+    for (int a = 0; a < D; ++a) lC[a][a] += lJ1 * st[2 * D] * S.dt;
   }
   float lfx[D];
 #pragma unroll
@@ -339,15 +527,8 @@ __global__ void k_g2p_bwd(const float* __restrict__ s, const float* __restrict__
     atomicAdd(&lgrid[ni].z, add[1]);
     if (D == 3) atomicAdd(&lgrid[ni].w, add[2]);
   }
-  float* lo = lam + p * NS;
 #pragma unroll
-  for (int h = 0; h < NS; ++h) lo[h] = 0.0f;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    lo[a] = l1[a];
-    lfx_out[p * 3 + a] = lfx[a];
-  }
-  lo[2 * D] = lJ1 * (1.0f + S.dt * tr);
+  for (int a = 0; a < D; ++a) lfx_out[p * 3 + a] = lfx[a];
 }
 
 // grid reverse: (0, lv) -> (lm, lP); lP = lv / m, lm = -lv . u / m, u = P / m; zero on
@@ -378,10 +559,10 @@ __global__ void k_grid_bwd(const float4* __restrict__ grid, uint64_t nn, AdjSim 
 }
 
 // P2G reverse: finishes lambda_t and tallies it
-template <int D>
+template <int D, bool EL>
 __global__ void k_p2g_bwd(const float* __restrict__ s, uint64_t n, const float4* __restrict__ lgrid, AdjSim S,
                           const float* __restrict__ lfx_in, float* __restrict__ lam, double* __restrict__ g) {
-  constexpr int NS = kNS<D>;
+  constexpr int NS = kNS<D, EL>, CO = kCO<D, EL>;
   const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = p < n;
   float l[NS];
@@ -390,17 +571,14 @@ __global__ void k_p2g_bwd(const float* __restrict__ s, uint64_t n, const float4*
   if (valid) {
     const float* st = s + p * NS;
     const Stencil<D> sc = stencil<D>(st, S);
-    const float sJ = S.k * (st[2 * D] - 1.0f);
     float A[D][D], lA[D][D], lv[D], lfx[D];
+    affine<D, EL>(st, S, A);
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       lv[a] = 0.0f;
       lfx[a] = lfx_in[p * 3 + a];
 #pragma unroll
-      for (int b = 0; b < D; ++b) {
-        A[a][b] = S.m * st[2 * D + 1 + a * D + b] + (a == b ? sJ : 0.0f);
-        lA[a][b] = 0.0f;
-      }
+      for (int b = 0; b < D; ++b) lA[a][b] = 0.0f;
     }
     for (int q = 0; q < kNO<D>; ++q) {
       int o[3];
@@ -432,21 +610,33 @@ __global__ void k_p2g_bwd(const float* __restrict__ s, uint64_t n, const float4*
       }
     }
     const float* lo = lam + p * NS;
-    float trA = 0.0f;
+#pragma unroll
+    for (int h = 0; h < NS; ++h) l[h] = lo[h];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      l[a] = lo[a] + sc.dfx[a] * lfx[a];
+      l[a] += sc.dfx[a] * lfx[a];
       l[D + a] = lv[a];
-      trA += lA[a][a];
 #pragma unroll
-      for (int b = 0; b < D; ++b) l[2 * D + 1 + a * D + b] = S.m * lA[a][b];
+      for (int b = 0; b < D; ++b) l[CO + a * D + b] = S.m * lA[a][b];
     }
-    l[2 * D] = lo[2 * D] + S.k * trA;
+    if constexpr (EL) {
+      float lP[D][D];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) lP[a][b] = S.scale * lA[a][b];
+      stress_el_adj<D>(st + 2 * D, lP, S, l + 2 * D);
+    } else {
+      float trA = 0.0f;
+#pragma unroll
+      for (int a = 0; a < D; ++a) trA += lA[a][a];
+      l[2 * D] += S.k * trA;
+    }
     float* lw = lam + p * NS;
 #pragma unroll
     for (int h = 0; h < NS; ++h) lw[h] = l[h];
   }
-  if (g) tally<D>(l, valid, g);
+  if (g) tally<NS>(l, valid, g);
 }
 
 }  // namespace
@@ -454,6 +644,7 @@ __global__ void k_p2g_bwd(const float* __restrict__ s, uint64_t n, const float4*
 // ---------------------------------------------------------------- runtime
 struct qadj_ctx {
   int dim = 3;
+  bool el = false;  // fixed-corotated elastic (else J-fluid)
   uint64_t n = 0, nn = 0;
   int ns = 0;
   AdjSim S{};
@@ -469,17 +660,28 @@ namespace {
 
 unsigned blocks(uint64_t n) { return (unsigned)((n + 255) / 256); }
 
+template <int D, bool EL>
+void forward_k(qadj_ctx* c, const float* in, float* out) {
+  k_p2g_fwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->S, c->grid);
+  k_grid_fwd<D><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
+  k_g2p_fwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->gv, c->S, out);
+}
+
+template <int D, bool EL>
+void adjoint_k(qadj_ctx* c, const float* s, const float* lam1, float* lam, double* g) {
+  k_p2g_fwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->S, c->grid);
+  k_grid_fwd<D><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
+  k_g2p_bwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(s, lam1, c->n, c->gv, c->S, c->lgrid, lam, c->lfx);
+  k_grid_bwd<D><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->lgrid);
+  k_p2g_bwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->lgrid, c->S, c->lfx, lam, g);
+}
+
 qmpm_status forward_dev(qadj_ctx* c, const float* in, float* out) {
   ACK(cudaMemsetAsync(c->grid, 0, sizeof(float4) * c->nn, c->stream));
-  if (c->dim == 3) {
-    k_p2g_fwd<3><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->S, c->grid);
-    k_grid_fwd<3><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
-    k_g2p_fwd<3><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->gv, c->S, out);
-  } else {
-    k_p2g_fwd<2><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->S, c->grid);
-    k_grid_fwd<2><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
-    k_g2p_fwd<2><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->gv, c->S, out);
-  }
+  if (c->dim == 3)
+    c->el ? forward_k<3, true>(c, in, out) : forward_k<3, false>(c, in, out);
+  else
+    c->el ? forward_k<2, true>(c, in, out) : forward_k<2, false>(c, in, out);
   c->launches += 3;
   ACK(cudaGetLastError());
   return QMPM_OK;
@@ -489,19 +691,10 @@ qmpm_status forward_dev(qadj_ctx* c, const float* in, float* out) {
 qmpm_status adjoint_dev(qadj_ctx* c, const float* s, const float* lam1, float* lam, double* g) {
   ACK(cudaMemsetAsync(c->grid, 0, sizeof(float4) * c->nn, c->stream));
   ACK(cudaMemsetAsync(c->lgrid, 0, sizeof(float4) * c->nn, c->stream));
-  if (c->dim == 3) {
-    k_p2g_fwd<3><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->S, c->grid);
-    k_grid_fwd<3><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
-    k_g2p_bwd<3><<<blocks(c->n), 256, 0, c->stream>>>(s, lam1, c->n, c->gv, c->S, c->lgrid, lam, c->lfx);
-    k_grid_bwd<3><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->lgrid);
-    k_p2g_bwd<3><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->lgrid, c->S, c->lfx, lam, g);
-  } else {
-    k_p2g_fwd<2><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->S, c->grid);
-    k_grid_fwd<2><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
-    k_g2p_bwd<2><<<blocks(c->n), 256, 0, c->stream>>>(s, lam1, c->n, c->gv, c->S, c->lgrid, lam, c->lfx);
-    k_grid_bwd<2><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->lgrid);
-    k_p2g_bwd<2><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->lgrid, c->S, c->lfx, lam, g);
-  }
+  if (c->dim == 3)
+    c->el ? adjoint_k<3, true>(c, s, lam1, lam, g) : adjoint_k<3, false>(c, s, lam1, lam, g);
+  else
+    c->el ? adjoint_k<2, true>(c, s, lam1, lam, g) : adjoint_k<2, false>(c, s, lam1, lam, g);
   c->launches += 5;
   ACK(cudaGetLastError());
   return QMPM_OK;
@@ -579,15 +772,15 @@ qmpm_status qadj_create(const qmpm_params* params, int32_t dim, int32_t material
   if (!params || !out) return afail(QMPM_EINVAL, "NULL argument");
   *out = nullptr;
   if (dim != 2 && dim != 3) return afail(QMPM_EINVAL, "dim must be 2 or 3");
-  if (material != QMPM_FLUID_J)
-    return afail(QMPM_EINVAL, "qadj: only the J-fluid adjoint is built (the fixed-corotated one is not)");
+  if (material != QMPM_FLUID_J && material != QMPM_ELASTIC_FCR) return afail(QMPM_EINVAL, "qadj: unknown material");
   if (n == 0) return afail(QMPM_EINVAL, "n must be > 0");
   for (int a = 0; a < dim; ++a)
     if (params->grid_res[a] < 3) return afail(QMPM_EINVAL, "grid_res must be >= 3 per axis");
   qadj_ctx* c = new qadj_ctx();
   c->dim = dim;
+  c->el = material == QMPM_ELASTIC_FCR;
   c->n = n;
-  c->ns = 2 * dim + 1 + dim * dim;
+  c->ns = 2 * dim + (c->el ? dim * dim : 1) + dim * dim;
   c->stream = (cudaStream_t)cuda_stream;
   AdjSim& S = c->S;
   for (int a = 0; a < 3; ++a) {
@@ -599,6 +792,9 @@ qmpm_status qadj_create(const qmpm_params* params, int32_t dim, int32_t material
   S.dt = params->dt;
   S.m = params->p_rho * params->p_vol;
   S.k = -params->dt * params->p_vol * 4.0f * S.inv_dx * S.inv_dx * params->E;
+  S.scale = -params->dt * params->p_vol * 4.0f * S.inv_dx * S.inv_dx;
+  S.mu = params->E / (2.0f * (1.0f + params->nu));
+  S.la = params->E * params->nu / ((1.0f + params->nu) * (1.0f - 2.0f * params->nu));
   S.bound = params->bound;
   c->nn = (uint64_t)S.res[0] * S.res[1] * S.res[2];
   cudaError_t e = cudaMalloc(&c->grid, sizeof(float4) * c->nn);
@@ -656,10 +852,14 @@ qmpm_status qadj_gradient_tally(qadj_ctx* c, const float* s0, uint32_t T, double
   }
   rc = get_buf(c, B.freel, &lamT);
   if (rc) return rc;
-  if (c->dim == 3)
-    k_lambda_T<3><<<blocks(c->n), 256, 0, c->stream>>>(sT, c->n, c->S, lamT, c->dacc, c->dacc + c->ns);
+  if (c->dim == 3 && c->el)
+    k_lambda_T<3, true><<<blocks(c->n), 256, 0, c->stream>>>(sT, c->n, c->S, lamT, c->dacc, c->dacc + c->ns);
+  else if (c->dim == 3)
+    k_lambda_T<3, false><<<blocks(c->n), 256, 0, c->stream>>>(sT, c->n, c->S, lamT, c->dacc, c->dacc + c->ns);
+  else if (c->el)
+    k_lambda_T<2, true><<<blocks(c->n), 256, 0, c->stream>>>(sT, c->n, c->S, lamT, c->dacc, c->dacc + c->ns);
   else
-    k_lambda_T<2><<<blocks(c->n), 256, 0, c->stream>>>(sT, c->n, c->S, lamT, c->dacc, c->dacc + c->ns);
+    k_lambda_T<2, false><<<blocks(c->n), 256, 0, c->stream>>>(sT, c->n, c->S, lamT, c->dacc, c->dacc + c->ns);
   c->launches += 1;
   ACK(cudaGetLastError());
   if (T > 0) B.freel.push_back(sT);

@@ -41,13 +41,13 @@ def lib():
 
 
 class Adjoint:
-    """One qadj_ctx for n particles of a J-fluid scene (sim dict as scenes.*)."""
+    """One qadj_ctx for n particles of a scene (sim dict as scenes.*; fluid or elastic)."""
 
     def __init__(self, sim: dict, n: int, stream=None):
         self._p = make_params(sim, n)
         self.dim = sim["dim"]
         self.n = n
-        self.ns = 2 * self.dim + 1 + self.dim * self.dim
+        self.ns = 2 * self.dim + (1 if sim["material"] == "fluid" else self.dim ** 2) + self.dim ** 2
         self.ctx = ctypes.c_void_p()
         _check(lib().qadj_create(ctypes.byref(self._p), self.dim, MATERIAL[sim["material"]], n,
                                  stream_handle(stream), ctypes.byref(self.ctx)))

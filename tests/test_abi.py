@@ -125,6 +125,6 @@ def test_adjoint_create_rejects_bad_arguments_without_gpu():
     p = qmpm.make_params(sim, s0.shape[0])
     ctx = ctypes.c_void_p()
     L = qadjoint.lib()
-    assert L.qadj_create(ctypes.byref(p), 2, 0, s0.shape[0], None, ctypes.byref(ctx)) == 1  # elastic
+    assert L.qadj_create(ctypes.byref(p), 2, 7, s0.shape[0], None, ctypes.byref(ctx)) == 1  # material
     assert L.qadj_create(ctypes.byref(p), 4, 1, s0.shape[0], None, ctypes.byref(ctx)) == 1  # dim
     assert L.qadj_create(ctypes.byref(p), 2, 1, 0, None, ctypes.byref(ctx)) == 1            # n = 0
