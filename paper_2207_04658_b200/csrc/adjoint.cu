@@ -317,12 +317,18 @@ __global__ void k_p2g_fwd(const float* __restrict__ s, uint64_t n, AdjSim S, flo
 
 __device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? v.y : (a == 1 ? v.z : v.w); }
 
-// v = P/m + dt g, separating walls (reading Q13): gv = (m, vx, vy, vz)
+// v = P/m + dt g, separating walls (reading Q13): gv = (m, vx, vy, vz).  The grids are
+// zero at the start of every step (no memsets): the forward clears `grid` here once
+// read (clear_grid), the adjoint step clears `lgrid` here (before g2p_bwd accumulates
+// into it) and `grid` in k_grid_bwd, its last reader.
 template <int D>
-__global__ void k_grid_fwd(const float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ gv) {
+__global__ void k_grid_fwd(float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ gv,
+                           bool clear_grid, float4* __restrict__ clear_lgrid) {
   const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nn) return;
   const float4 nd = grid[c];
+  if (clear_grid) grid[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (clear_lgrid) clear_lgrid[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   float4 out = make_float4(nd.x, 0.f, 0.f, 0.f);
   if (nd.x > 0.0f) {
     const int nz = D == 3 ? S.res[2] : 1;
@@ -534,10 +540,11 @@ __global__ void k_g2p_bwd(const float* __restrict__ s, const float* __restrict__
 // grid reverse: (0, lv) -> (lm, lP); lP = lv / m, lm = -lv . u / m, u = P / m; zero on
 // wall-clamped components and on empty nodes
 template <int D>
-__global__ void k_grid_bwd(const float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ lgrid) {
+__global__ void k_grid_bwd(float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ lgrid) {
   const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nn) return;
   const float4 nd = grid[c];
+  grid[c] = make_float4(0.f, 0.f, 0.f, 0.f);  // last reader of the step's grid
   const float4 lvn = lgrid[c];
   float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
   if (nd.x > 0.0f) {
@@ -663,21 +670,20 @@ unsigned blocks(uint64_t n) { return (unsigned)((n + 255) / 256); }
 template <int D, bool EL>
 void forward_k(qadj_ctx* c, const float* in, float* out) {
   k_p2g_fwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->S, c->grid);
-  k_grid_fwd<D><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
+  k_grid_fwd<D><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv, true, nullptr);
   k_g2p_fwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(in, c->n, c->gv, c->S, out);
 }
 
 template <int D, bool EL>
 void adjoint_k(qadj_ctx* c, const float* s, const float* lam1, float* lam, double* g) {
   k_p2g_fwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->S, c->grid);
-  k_grid_fwd<D><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv);
+  k_grid_fwd<D><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->gv, false, c->lgrid);
   k_g2p_bwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(s, lam1, c->n, c->gv, c->S, c->lgrid, lam, c->lfx);
   k_grid_bwd<D><<<blocks(c->nn), 256, 0, c->stream>>>(c->grid, c->nn, c->S, c->lgrid);
   k_p2g_bwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->lgrid, c->S, c->lfx, lam, g);
 }
 
 qmpm_status forward_dev(qadj_ctx* c, const float* in, float* out) {
-  ACK(cudaMemsetAsync(c->grid, 0, sizeof(float4) * c->nn, c->stream));
   if (c->dim == 3)
     c->el ? forward_k<3, true>(c, in, out) : forward_k<3, false>(c, in, out);
   else
@@ -689,8 +695,6 @@ qmpm_status forward_dev(qadj_ctx* c, const float* in, float* out) {
 
 // lambda_t from s_t and lambda_{t+1} (g nullable: device tallies to accumulate)
 qmpm_status adjoint_dev(qadj_ctx* c, const float* s, const float* lam1, float* lam, double* g) {
-  ACK(cudaMemsetAsync(c->grid, 0, sizeof(float4) * c->nn, c->stream));
-  ACK(cudaMemsetAsync(c->lgrid, 0, sizeof(float4) * c->nn, c->stream));
   if (c->dim == 3)
     c->el ? adjoint_k<3, true>(c, s, lam1, lam, g) : adjoint_k<3, false>(c, s, lam1, lam, g);
   else
@@ -802,6 +806,8 @@ qmpm_status qadj_create(const qmpm_params* params, int32_t dim, int32_t material
   if (!e) e = cudaMalloc(&c->lgrid, sizeof(float4) * c->nn);
   if (!e) e = cudaMalloc(&c->lfx, sizeof(float) * 3 * n);
   if (!e) e = cudaMalloc(&c->dacc, sizeof(double) * (c->ns + 1));
+  if (!e) e = cudaMemsetAsync(c->grid, 0, sizeof(float4) * c->nn, c->stream);  // zero between steps from here on
+  if (!e) e = cudaStreamSynchronize(c->stream);
   if (e) {
     cudaGetLastError();
     qadj_destroy(c);
