@@ -93,8 +93,8 @@ SaltSrc dev_salt(const qsmoke_ctx* c, const CodecDev& C, uint32_t sub) {
 constexpr size_t kRingCells = 3 * (8 + 4) * (32 + 4) * 2;
 constexpr size_t kSmemAdvect = kRingCells * 16, kSmemReflect = 2 * kRingCells * 16,
                  kSmemDensity = kRingCells * 16 + kRingCells * 4;
-qmpm_status launch(qsmoke_ctx* c, CUfunction f, cudaStream_t st, void** args, size_t smem = 0) {
-  const dim3 grid((c->g.nz + 31) / 32, (c->g.ny + 7) / 8, (c->g.nxr + 7) / 8);
+qmpm_status launch(qsmoke_ctx* c, CUfunction f, cudaStream_t st, void** args, size_t smem = 0, int rows = 8) {
+  const dim3 grid((c->g.nz + 31) / 32, (c->g.ny + rows - 1) / rows, (c->g.nxr + 7) / 8);
   c->launches += 1;
   SCK(jit_launch3(f, grid, dim3(32, 8, 1), smem, st, args));
   return QMPM_OK;
@@ -112,12 +112,12 @@ qmpm_status divergence(qsmoke_ctx* c, cudaStream_t st, const uint32_t* u, float*
 qmpm_status jacobi(qsmoke_ctx* c, cudaStream_t st, const uint32_t* pin, const float* div, SaltSrc ss, uint32_t* pout,
                    float* dbg) {
   void* a[] = {&pin, &div, &c->g, &ss, &pout, &dbg};
-  return launch(c, c->k.jacobi, st, a);
+  return launch(c, c->k.jacobi, st, a, 0, 16);  // two rows per thread (p_march2)
 }
 qmpm_status project(qsmoke_ctx* c, cudaStream_t st, const uint32_t* u, const uint32_t* p, SaltSrc ss, uint32_t* out,
                     float* dbg) {
   void* a[] = {&u, &p, &c->g, &ss, &out, &dbg};
-  return launch(c, c->k.project, st, a);
+  return launch(c, c->k.project, st, a, 0, 16);
 }
 qmpm_status advect_rho(qsmoke_ctx* c, cudaStream_t st, const float* rin, const uint32_t* u, float dt, float* rout,
                        unsigned long long* tick) {

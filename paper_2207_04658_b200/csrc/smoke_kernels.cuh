@@ -525,6 +525,126 @@ __device__ __forceinline__ void adv_march(const uint32_t* __restrict__ U, const 
     __syncthreads();
   }
 }
+
+// p_march with two records per thread (rows ty and ty + 8 of a 16-row tile): the loop,
+// barrier, halo and address overheads are paid once per two records.  Same contract
+// as p_march; f is called for the upper row, then the lower row.  blockDim = (32, 8),
+// gridDim.y = ceil(ny / 16).
+constexpr int kTY2 = 2 * kTY;
+
+template <class F>
+__device__ __forceinline__ void p_march2(const uint32_t* __restrict__ P, const float* __restrict__ DIV,
+                                         const uint32_t* __restrict__ U, const SmokeDev& g, F&& f) {
+  constexpr int W = SpecP::W, WU = SpecU::W;
+  __shared__ float2 tile[kTY2 + 2][kTZ + 2];
+  const int tz = threadIdx.x, ty = threadIdx.y;
+  const int y0 = blockIdx.y * kTY2, z0 = blockIdx.x * kTZ;
+  const int z = z0 + tz;
+  const int xs = blockIdx.z * kXM, xe = min(xs + kXM, g.nxr);
+  const unsigned long long plane = (unsigned long long)g.ny * g.nz, pw = plane * W;
+  March m[2];  // per row: the fields the callbacks read (y, z, valid, r0, plane)
+  unsigned long long r[2], cell[2];
+  const uint32_t* own[2];
+  float2 prev[2], cur[2];
+  uint32_t wn[2][W + 1], wnn[2][W + 1];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    m[k].tz = tz;
+    m[k].ty = ty + k * kTY;
+    m[k].z = z;
+    m[k].y = y0 + ty + k * kTY;
+    m[k].xs = xs;
+    m[k].xe = xe;
+    m[k].valid = z < g.nz && m[k].y < g.ny;
+    m[k].plane = plane;
+    m[k].r0 = (unsigned long long)min(m[k].y, g.ny - 1) * g.nz + min(z, g.nz - 1);
+    m[k].has_halo = false;
+    r[k] = (unsigned long long)xs * plane + m[k].r0;
+    cell[k] = 2ull * xs * plane + m[k].r0;
+    own[k] = P + r[k] * W;
+    prev[k] = xs > 0 ? dec2p<SpecP>(own[k] - pw) : make_float2(0.f, 0.f);
+    cur[k] = dec2p<SpecP>(own[k]);
+    wn[k][W] = wnn[k][W] = 0u;
+#pragma unroll
+    for (int q = 0; q < W; ++q) wn[k][q] = xs + 1 < g.nxr ? __ldg(own[k] + pw + q) : 0u;
+  }
+  // halo: warp 0 -> row y0 - 1, warp 1 -> row y0 + 16, warp 2 lanes 0-15 -> column z0 - 1,
+  // warp 3 lanes 0-15 -> column z0 + 32 (rows y0 .. y0 + 15); clamped = Neumann (S6)
+  bool has_halo = false;
+  int hy = 0, hz = 0, hyg = 0, hzg = 0;
+  if (ty == 0 || ty == 1) {
+    has_halo = true;
+    hyg = ty == 0 ? y0 - 1 : y0 + kTY2;
+    hzg = z;
+    hy = ty == 0 ? 0 : kTY2 + 1;
+    hz = tz + 1;
+  } else if ((ty == 2 || ty == 3) && tz < kTY2) {
+    has_halo = true;
+    hyg = y0 + tz;
+    hzg = ty == 2 ? z0 - 1 : z0 + kTZ;
+    hy = tz + 1;
+    hz = ty == 2 ? 0 : kTZ + 1;
+  }
+  const unsigned long long hoff =
+      (unsigned long long)min(max(hyg, 0), g.ny - 1) * g.nz + min(max(hzg, 0), g.nz - 1);
+  const uint32_t* halo = P + ((unsigned long long)xs * plane + hoff) * W;
+  for (int xr = xs; xr < xe; ++xr) {
+    const bool has_next = xr + 1 < g.nxr;
+    float d[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+    uint32_t wu[2][WU + 1];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) wnn[k][q] = xr + 2 < g.nxr ? __ldg(own[k] + 2 * pw + q) : 0u;
+      if (DIV && m[k].valid) {
+        d[k][0] = __ldg(DIV + cell[k]);
+        d[k][1] = __ldg(DIV + cell[k] + plane);
+      }
+      wu[k][WU] = 0u;
+      if (U && m[k].valid) {
+#pragma unroll
+        for (int q = 0; q < WU; ++q) wu[k][q] = __ldg(U + r[k] * WU + q);
+      }
+    }
+    float2 hv = make_float2(0.f, 0.f);
+    if (has_halo) hv = dec2p<SpecP>(halo);
+    __syncthreads();
+    tile[ty + 1][tz + 1] = cur[0];
+    tile[ty + kTY + 1][tz + 1] = cur[1];
+    if (has_halo) tile[hy][hz] = hv;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int row = ty + k * kTY + 1;
+      const float2 nxt = has_next ? make_float2(sdec<SpecP>(wn[k], 0), sdec<SpecP>(wn[k], 1)) : cur[k];
+      const float2 ym = tile[row - 1][tz + 1], yp = tile[row + 1][tz + 1];
+      const float2 zm = tile[row][tz], zp = tile[row][tz + 2];
+      float nb[2][6];
+      nb[0][0] = xr > 0 ? prev[k].y : cur[k].x;
+      nb[0][1] = cur[k].y;
+      nb[1][0] = cur[k].x;
+      nb[1][1] = has_next ? nxt.x : cur[k].y;
+      nb[0][2] = ym.x;
+      nb[1][2] = ym.y;
+      nb[0][3] = yp.x;
+      nb[1][3] = yp.y;
+      nb[0][4] = zm.x;
+      nb[1][4] = zm.y;
+      nb[0][5] = zp.x;
+      nb[1][5] = zp.y;
+      const float pc[2] = {cur[k].x, cur[k].y};
+      f(m[k], xr, r[k], m[k].valid, pc, nb, d[k], wu[k]);
+      prev[k] = cur[k];
+      cur[k] = nxt;
+#pragma unroll
+      for (int q = 0; q < W; ++q) wn[k][q] = wnn[k][q];
+      own[k] += pw;
+      r[k] += plane;
+      cell[k] += 2 * plane;
+    }
+    halo += pw;
+  }
+}
 }  // namespace smoke
 
 // ------------------------------------------------------------------ entry points
@@ -635,7 +755,7 @@ extern "C" __global__ void __launch_bounds__(256)
                   uint32_t* __restrict__ out, float* __restrict__ dbg) {
   constexpr int W = SpecP::W;
   const uint32_t salt = smoke::salt_of(ss);
-  smoke::p_march(P, div, nullptr, g, [&](const smoke::March& m, int xr, unsigned long long r, bool valid,
+  smoke::p_march2(P, div, nullptr, g, [&](const smoke::March& m, int xr, unsigned long long r, bool valid,
                                           const float* pc, const float (*nb)[6], const float* d, const uint32_t* wu) {
     float v[2] = {0.f, 0.f};
     if (valid) {
@@ -661,7 +781,7 @@ extern "C" __global__ void __launch_bounds__(256)
                    uint32_t* __restrict__ out, float* __restrict__ dbg) {
   constexpr int W = SpecU::W;
   const uint32_t salt = smoke::salt_of(ss);
-  smoke::p_march(P, nullptr, U, g, [&](const smoke::March& m, int xr, unsigned long long r, bool valid,
+  smoke::p_march2(P, nullptr, U, g, [&](const smoke::March& m, int xr, unsigned long long r, bool valid,
                                         const float* pc, const float (*nb)[6], const float* d, const uint32_t* wu) {
     float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (valid) {

@@ -234,3 +234,38 @@ def test_errors_are_reported():
     with pytest.raises(qsmoke.qmpm.QmpmError) as e:
         qsmoke.Smoke(params, schemes.smoke_p(), schemes.smoke_p())
     assert e.value.code == 2
+
+
+def test_far_departure_points_take_the_global_path():
+    """Velocities of several cells per step: most departure points leave the kernels'
+    shared-memory window (2 cells), so the global-memory sampling path is the one checked
+    against the oracle here (same arithmetic as the window path)."""
+    res = (20, 10, 40)
+    params, su, sp, uw, uq, pw, pq, rho = make(res, seed=9, su=schemes.smoke_u(rng=16.0), amp=8.0, dt=0.1)
+    sm = qsmoke.Smoke(params, su, sp)
+    n, dx, dt = sm.n_records, params["dx"], params["dt"]
+    assert 8.0 * 0.5 * dt / dx > 2.0  # departures beyond the window
+    bdt = 0.5 * dt * params["buoyancy"]
+    for refl in (False, True):
+        out = torch.zeros((n, sm.Wu), dtype=torch.int32, device="cuda")
+        dbg = torch.zeros((n, 6), dtype=torch.float32, device="cuda")
+        if refl:
+            _, _, _, uw2, uq2, _, _, _ = make(res, seed=10, su=su, amp=8.0, dt=0.1)
+            sm.advect_velocity(dev(uw), out, 0.5 * dt, u_refl=dev(uw2), dstep=5 * 256 + 100, dbg=dbg)
+            o = osm.sample(2.0 * uq - uq2, osm.backtrace(uq, 0.5 * dt, dx))
+            ds = 5 * 256 + 100
+        else:
+            sm.advect_velocity(dev(uw), out, 0.5 * dt, rho=dev(rho), bdt=bdt, dstep=5 * 256, dbg=dbg)
+            o = osm.advect(uq, uq, 0.5 * dt, dx)
+            o[..., 1] += bdt * rho.astype(np.float64)
+            ds = 5 * 256
+        g_pre = dbg.cpu().numpy()
+        check_close(g_pre, osm.to_records(o, 3), ("far advect", refl))
+        check_words(host_u32(out), g_pre, su, ds, ("far advect", refl))
+    outr = torch.zeros(res, dtype=torch.float32, device="cuda")
+    sm.advect_density(dev(rho), dev(uw), outr, dt)
+    o = osm.advect(rho.astype(np.float64), uq, dt, dx)
+    lo, hi = params["source_lo"], params["source_hi"]
+    o[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]] = 1.0
+    check_close(outr.cpu().numpy(), o, "far rho")
+    sm.close()
