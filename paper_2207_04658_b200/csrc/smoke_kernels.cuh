@@ -759,11 +759,15 @@ extern "C" __global__ void __launch_bounds__(256)
                                           const float* pc, const float (*nb)[6], const float* d, const uint32_t* wu) {
     float v[2] = {0.f, 0.f};
     if (valid) {
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const float s = ((nb[k][0] + nb[k][1]) + (nb[k][2] + nb[k][3])) + (nb[k][4] + nb[k][5]);
-        v[k] = (s - g.dx2 * d[k]) * (1.0f / 6.0f);
-      }
+      // both cells at once in packed FP32x2 (FADD2 / FFMA2 / FMUL2)
+      const float2 sx = __fadd2_rn(make_float2(nb[0][0], nb[1][0]), make_float2(nb[0][1], nb[1][1]));
+      const float2 sy = __fadd2_rn(make_float2(nb[0][2], nb[1][2]), make_float2(nb[0][3], nb[1][3]));
+      const float2 sz = __fadd2_rn(make_float2(nb[0][4], nb[1][4]), make_float2(nb[0][5], nb[1][5]));
+      const float2 s2 = __fadd2_rn(__fadd2_rn(sx, sy), sz);
+      const float2 r2 = __fmul2_rn(__ffma2_rn(make_float2(-g.dx2, -g.dx2), make_float2(d[0], d[1]), s2),
+                                   make_float2(1.0f / 6.0f, 1.0f / 6.0f));
+      v[0] = r2.x;
+      v[1] = r2.y;
       if (dbg) {
         dbg[2 * r] = v[0];
         dbg[2 * r + 1] = v[1];
