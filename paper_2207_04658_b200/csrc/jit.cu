@@ -325,6 +325,7 @@ cudaError_t jit_smoke(const std::string& src, SmokeJit& out, std::string& err) {
       g_drv.moduleGetFunction(&out.advect_refl, mod, "qsmoke_advect_refl") != CUDA_SUCCESS ||
       g_drv.moduleGetFunction(&out.div, mod, "qsmoke_div") != CUDA_SUCCESS ||
       g_drv.moduleGetFunction(&out.jacobi, mod, "qsmoke_jacobi") != CUDA_SUCCESS ||
+      g_drv.moduleGetFunction(&out.jacobi2, mod, "qsmoke_jacobi2") != CUDA_SUCCESS ||
       g_drv.moduleGetFunction(&out.project, mod, "qsmoke_project") != CUDA_SUCCESS ||
       g_drv.moduleGetFunction(&out.advect_rho, mod, "qsmoke_advect_rho") != CUDA_SUCCESS) {
     err = "smoke JIT module lacks a kernel";

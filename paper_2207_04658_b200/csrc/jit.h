@@ -32,7 +32,7 @@ cudaError_t jit_codec(const std::string& src, CodecJit& out, std::string& err);
 
 // the quantized smoke step (smoke_kernels.cuh) on a velocity and a pressure layout
 struct SmokeJit {
-  CUfunction advect_u, advect_refl, div, jacobi, project, advect_rho;
+  CUfunction advect_u, advect_refl, div, jacobi, jacobi2, project, advect_rho;
 };
 std::string smoke_spec_source(const CodecDev& U, const CodecDev& P, int wvu, int wvp);
 cudaError_t jit_smoke(const std::string& src, SmokeJit& out, std::string& err);

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -45,6 +46,11 @@ struct qsmoke_ctx {
   uint32_t *u = nullptr, *ut = nullptr, *uh = nullptr, *up = nullptr, *p[2] = {nullptr, nullptr};
   float *div = nullptr, *rho[2] = {nullptr, nullptr};
   int rcur = 0;  // which density buffer holds the state
+  // two Jacobi sweeps per launch (qsmoke_jacobi2, temporal blocking): bit-identical but
+  // measured SLOWER (1.93 ms per two sweeps at 612^3 vs 2 x 0.54 ms: the halo-extended
+  // first sweep and three barriers per plane cost more issue slots than the halved DRAM
+  // traffic saves -- the single sweep is issue-bound); QSMOKE_FUSE=1 enables
+  bool fuse2 = false;
   unsigned long long* dstep = nullptr;
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
 };
@@ -93,8 +99,9 @@ SaltSrc dev_salt(const qsmoke_ctx* c, const CodecDev& C, uint32_t sub) {
 constexpr size_t kRingCells = 3 * (8 + 4) * (32 + 4) * 2;
 constexpr size_t kSmemAdvect = kRingCells * 16, kSmemReflect = 2 * kRingCells * 16,
                  kSmemDensity = kRingCells * 16 + kRingCells * 4;
-qmpm_status launch(qsmoke_ctx* c, CUfunction f, cudaStream_t st, void** args, size_t smem = 0, int rows = 8) {
-  const dim3 grid((c->g.nz + 31) / 32, (c->g.ny + rows - 1) / rows, (c->g.nxr + 7) / 8);
+qmpm_status launch(qsmoke_ctx* c, CUfunction f, cudaStream_t st, void** args, size_t smem = 0, int rows = 8,
+                   int planes = 8) {
+  const dim3 grid((c->g.nz + 31) / 32, (c->g.ny + rows - 1) / rows, (c->g.nxr + planes - 1) / planes);
   c->launches += 1;
   SCK(jit_launch3(f, grid, dim3(32, 8, 1), smem, st, args));
   return QMPM_OK;
@@ -114,6 +121,12 @@ qmpm_status jacobi(qsmoke_ctx* c, cudaStream_t st, const uint32_t* pin, const fl
   void* a[] = {&pin, &div, &c->g, &ss, &pout, &dbg};
   return launch(c, c->k.jacobi, st, a, 0, 16);  // two rows per thread (p_march2)
 }
+// two sweeps in one launch (qsmoke_jacobi2: 16 planes per CTA, 16-row tiles)
+qmpm_status jacobi2(qsmoke_ctx* c, cudaStream_t st, const uint32_t* pin, const float* div, SaltSrc s1, SaltSrc s2,
+                    uint32_t* pout) {
+  void* a[] = {&pin, &div, &c->g, &s1, &s2, &pout};
+  return launch(c, c->k.jacobi2, st, a, 0, 16, 16);
+}
 qmpm_status project(qsmoke_ctx* c, cudaStream_t st, const uint32_t* u, const uint32_t* p, SaltSrc ss, uint32_t* out,
                     float* dbg) {
   void* a[] = {&u, &p, &c->g, &ss, &out, &dbg};
@@ -131,8 +144,15 @@ qmpm_status projection(qsmoke_ctx* c, cudaStream_t st, const uint32_t* u_in, uin
   qmpm_status rc = divergence(c, st, u_in, c->div);
   if (rc) return rc;
   int cur = 0;
-  for (int k = 0; k < c->P.jacobi_iters; ++k) {
-    rc = jacobi(c, st, c->p[cur], c->div, dev_salt(c, c->Pc, sub0 + 1 + k), c->p[cur ^ 1], nullptr);
+  for (int k = 0; k < c->P.jacobi_iters;) {
+    if (k + 1 < c->P.jacobi_iters && c->fuse2) {  // sweeps k, k + 1 in one launch
+      rc = jacobi2(c, st, c->p[cur], c->div, dev_salt(c, c->Pc, sub0 + 1 + k), dev_salt(c, c->Pc, sub0 + 2 + k),
+                   c->p[cur ^ 1]);
+      k += 2;
+    } else {
+      rc = jacobi(c, st, c->p[cur], c->div, dev_salt(c, c->Pc, sub0 + 1 + k), c->p[cur ^ 1], nullptr);
+      k += 1;
+    }
     if (rc) return rc;
     cur ^= 1;
   }
@@ -212,6 +232,9 @@ qmpm_status qsmoke_create(const qsmoke_params* params, const qmpm_scheme* u_sche
     delete c;
     return rc;
   }
+  if (getenv("QSMOKE_FUSE") && atoi(getenv("QSMOKE_FUSE")) != 0) c->fuse2 = true;
+  for (uint32_t i = 0; i < p_scheme->n_fields; ++i)
+    if (p_scheme->fields[i].kind == QMPM_SHARED_EXP) c->fuse2 = false;
   std::string err;
   const std::string src = smoke_spec_source(c->U, c->Pc, vec_width(c->U.W), vec_width(c->Pc.W));
   if (jit_smoke(src, c->k, err) != cudaSuccess) {
@@ -349,7 +372,9 @@ qmpm_status qsmoke_get_state(qsmoke_ctx* ctx, uint32_t* u_words, uint32_t* p_wor
 
 qmpm_status qsmoke_step(qsmoke_ctx* ctx, uint64_t n_steps) {
   if (!ctx) return sfail(QMPM_EINVAL, "NULL ctx");
-  const uint64_t per_step = 2ull * ctx->P.jacobi_iters + 7;
+  const uint64_t sweeps = ctx->fuse2 ? (uint64_t)(ctx->P.jacobi_iters / 2 + ctx->P.jacobi_iters % 2)
+                                     : (uint64_t)ctx->P.jacobi_iters;
+  const uint64_t per_step = 2ull * sweeps + 7;
   for (uint64_t s = 0; s < n_steps; ++s) {
     SCK(cudaGraphLaunch(ctx->graph[ctx->rcur], ctx->stream));
     ctx->rcur ^= 1;

@@ -645,6 +645,210 @@ __device__ __forceinline__ void p_march2(const uint32_t* __restrict__ P, const f
     halo += pw;
   }
 }
+// ---- two Jacobi sweeps per launch (temporal blocking, S6) -----------------------------
+// A CTA marches a (32 z x 16 y) record column along x (kXM2 planes) keeping three planes
+// of the input pressure L0 (2-record y/z halo) and of the first sweep's pressure L1
+// (1-record halo) decoded in shared memory.  Per plane: the next L0 plane is filled
+// (raw words fetched a plane ahead), L1 is computed on the halo-extended plane and
+// quantized exactly as the single sweep stores it (encode_record, then decode: the
+// same dithered code, never written to memory), then the second sweep of the interior
+// is encoded and stored.  Domain walls: every neighbour index is clamped into the
+// domain (Neumann, S6), so halo slots outside it are never read.  The result is bit-
+// identical to two qsmoke_jacobi launches (tests/test_gpu_smoke.py: graph vs chain).
+constexpr int kXM2 = 16;
+constexpr int kJY = 2 * kTY, kJZ = kTZ;             // interior tile (records)
+constexpr int kL0Y = kJY + 4, kL0Z = kJZ + 4;       // L0 tile: 2-record halo
+constexpr int kL1Y = kJY + 2, kL1Z = kJZ + 2;       // L1 tile: 1-record halo
+constexpr int kL0N = kL0Y * kL0Z, kL1N = kL1Y * kL1Z;
+constexpr int kL0Per = (kL0N + 255) / 256, kL1Per = (kL1N + 255) / 256;
+
+struct Jac2 {
+  int y0, z0;
+  __device__ __forceinline__ int i0(int slot, int y, int z) const {
+    return (slot * kL0Y + (y - y0 + 2)) * kL0Z + (z - z0 + 2);
+  }
+  __device__ __forceinline__ int i1(int slot, int y, int z) const {
+    return (slot * kL1Y + (y - y0 + 1)) * kL1Z + (z - z0 + 1);
+  }
+};
+
+// the single sweep's arithmetic (qsmoke_jacobi), both cells of a record at once
+__device__ __forceinline__ float2 jacobi_pair(float xm0, float xp0, float xm1, float xp1, float2 ym, float2 yp,
+                                              float2 zm, float2 zp, float d0, float d1, float dx2) {
+  const float2 sx = __fadd2_rn(make_float2(xm0, xm1), make_float2(xp0, xp1));
+  const float2 sy = __fadd2_rn(ym, yp);
+  const float2 sz = __fadd2_rn(zm, zp);
+  const float2 s2 = __fadd2_rn(__fadd2_rn(sx, sy), sz);
+  return __fmul2_rn(__ffma2_rn(make_float2(-dx2, -dx2), make_float2(d0, d1), s2),
+                    make_float2(1.0f / 6.0f, 1.0f / 6.0f));
+}
+
+}  // namespace smoke
+
+extern "C" __global__ void __launch_bounds__(256)
+    qsmoke_jacobi2(const uint32_t* __restrict__ P, const float* __restrict__ div, SmokeDev g, SaltSrc ss1,
+                   SaltSrc ss2, uint32_t* __restrict__ out) {
+  using namespace smoke;
+  constexpr int W = SpecP::W;
+  __shared__ float2 L0[3 * kL0N];
+  __shared__ float2 L1[3 * kL1N];
+  const int tid = threadIdx.y * kTZ + threadIdx.x;
+  const int y0 = blockIdx.y * kJY, z0 = blockIdx.x * kJZ;
+  const int xs = blockIdx.z * kXM2, xe = min(xs + kXM2, g.nxr);
+  const unsigned long long plane = (unsigned long long)g.ny * g.nz;
+  const uint32_t salt1 = salt_of(ss1), salt2 = salt_of(ss2);
+  // per-thread constants (the (y, z) of each owned slot does not change along x)
+  unsigned goff0[kL0Per];  // in-plane record offset of fill slot e (valid when in0 bit e)
+  unsigned in0 = 0u;
+#pragma unroll
+  for (int e = 0; e < kL0Per; ++e) {
+    const int t = tid + 256 * e;
+    const int y = y0 - 2 + t / kL0Z, z = z0 - 2 + t % kL0Z;
+    const bool ok = t < kL0N && y >= 0 && y < g.ny && z >= 0 && z < g.nz;
+    in0 |= ok ? (1u << e) : 0u;
+    goff0[e] = ok ? (unsigned)(y * g.nz + z) : 0u;
+  }
+  // sweep-1 slots: in-plane offset, L0 centre index and the clamped neighbour deltas
+  unsigned goff1[kL1Per];
+  int c1[kL1Per], dym[kL1Per], dyp[kL1Per], dzm[kL1Per], dzp[kL1Per];
+  unsigned in1 = 0u;
+#pragma unroll
+  for (int e = 0; e < kL1Per; ++e) {
+    const int t = tid + 256 * e;
+    const int y = y0 - 1 + t / kL1Z, z = z0 - 1 + t % kL1Z;
+    const bool ok = t < kL1N && y >= 0 && y < g.ny && z >= 0 && z < g.nz;
+    in1 |= ok ? (1u << e) : 0u;
+    goff1[e] = ok ? (unsigned)(y * g.nz + z) : 0u;
+    c1[e] = (y - y0 + 2) * kL0Z + (z - z0 + 2);
+    dym[e] = y > 0 ? -kL0Z : 0;
+    dyp[e] = y + 1 < g.ny ? kL0Z : 0;
+    dzm[e] = z > 0 ? -1 : 0;
+    dzp[e] = z + 1 < g.nz ? 1 : 0;
+  }
+  // sweep-2 rows
+  int c2[2], eym[2], eyp[2], ezm[2], ezp[2];
+  unsigned goff2[2];
+  bool in2[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int y = y0 + threadIdx.y + k * kTY, z = z0 + threadIdx.x;
+    in2[k] = y < g.ny && z < g.nz;
+    goff2[k] = in2[k] ? (unsigned)(y * g.nz + z) : 0u;
+    c2[k] = (y - y0 + 1) * kL1Z + (z - z0 + 1);
+    eym[k] = y > 0 ? -kL1Z : 0;
+    eyp[k] = y + 1 < g.ny ? kL1Z : 0;
+    ezm[k] = z > 0 ? -1 : 0;
+    ezp[k] = z + 1 < g.nz ? 1 : 0;
+  }
+  uint32_t raw[kL0Per][W];
+  auto fetch = [&](int q) {
+    if (q < 0 || q >= g.nxr) return;
+    const uint32_t* base = P + (unsigned long long)q * plane * W;
+#pragma unroll
+    for (int e = 0; e < kL0Per; ++e)
+      if ((in0 >> e) & 1u) {
+#pragma unroll
+        for (int k = 0; k < W; ++k) raw[e][k] = __ldg(base + (unsigned long long)goff0[e] * W + k);
+      }
+  };
+  auto store0 = [&](int q, int slot) {
+    if (q < 0 || q >= g.nxr) return;
+#pragma unroll
+    for (int e = 0; e < kL0Per; ++e)
+      if ((in0 >> e) & 1u) {
+        uint32_t w[W + 1];
+#pragma unroll
+        for (int k = 0; k < W; ++k) w[k] = raw[e][k];
+        w[W] = 0u;
+        L0[slot * kL0N + tid + 256 * e] = make_float2(sdec<SpecP>(w, 0), sdec<SpecP>(w, 1));
+      }
+  };
+  // first sweep on plane q: L0 slots (sm, s0, sp) = planes q - 1, q, q + 1; L1 slot t1
+  auto sweep1 = [&](int q, int sm, int s0, int sp, int t1) {
+    const bool qok = q >= 0 && q < g.nxr;
+    const float* dq = div + 2ull * q * plane;
+    const unsigned long long rq = (unsigned long long)q * plane;
+#pragma unroll
+    for (int e = 0; e < kL1Per; ++e) {
+      const bool valid = qok && ((in1 >> e) & 1u);
+      float v[2] = {0.f, 0.f};
+      const unsigned long long r = rq + goff1[e];
+      if (valid) {
+        const float2* S0 = L0 + s0 * kL0N + c1[e];
+        const float2 c = S0[0];
+        const float xm0 = q > 0 ? L0[sm * kL0N + c1[e]].y : c.x;
+        const float xp1 = q + 1 < g.nxr ? L0[sp * kL0N + c1[e]].x : c.y;
+        const float2 rr = jacobi_pair(xm0, c.y, c.x, xp1, S0[dym[e]], S0[dyp[e]], S0[dzm[e]], S0[dzp[e]],
+                                      __ldg(dq + goff1[e]), __ldg(dq + plane + goff1[e]), g.dx2);
+        v[0] = rr.x;
+        v[1] = rr.y;
+      }
+      const uint32_t hh = SpecP::DITHER ? qmpm::mix32((uint32_t)r ^ salt1) : 0u;
+      uint32_t w[W + 1];
+      qmpm::encode_record<SpecP>(v, hh, valid, w, nullptr);
+      if (valid) L1[t1 * kL1N + tid + 256 * e] = make_float2(sdec<SpecP>(w, 0), sdec<SpecP>(w, 1));
+    }
+  };
+  // ring slots rotate: plane q lives in slot (q - xs + 2) % 3 (no modulo in the loop)
+  int a0 = 0, a1 = 1, a2 = 2;  // L0 slots of planes xs - 2, xs - 1, xs
+  fetch(xs - 2);
+  store0(xs - 2, a0);
+  fetch(xs - 1);
+  store0(xs - 1, a1);
+  fetch(xs);
+  store0(xs, a2);
+  __syncthreads();
+  int b0 = 0, b1 = 1, b2 = 2;  // L1 slots of planes xs - 1, xs, xs + 1
+  sweep1(xs - 1, a0, a1, a2, b0);
+  __syncthreads();
+  fetch(xs + 1);
+  store0(xs + 1, a0);  // plane xs - 2's slot: L0 slots now xs - 1 (a1), xs (a2), xs + 1 (a0)
+  {
+    const int t = a0;
+    a0 = a1, a1 = a2, a2 = t;  // a0, a1, a2 = planes xs - 1, xs, xs + 1
+  }
+  __syncthreads();
+  sweep1(xs, a0, a1, a2, b1);
+  fetch(xs + 2);
+  for (int xr = xs; xr < xe; ++xr) {
+    // here: L0 slots a0, a1, a2 = planes xr - 1, xr, xr + 1; L1 slots b0, b1 = xr - 1, xr
+    __syncthreads();
+    store0(xr + 2, a0);  // plane xr - 1's slot
+    {
+      const int t = a0;
+      a0 = a1, a1 = a2, a2 = t;  // planes xr, xr + 1, xr + 2
+    }
+    __syncthreads();
+    fetch(xr + 3);
+    sweep1(xr + 1, a0, a1, a2, b2);
+    __syncthreads();
+    const unsigned long long rq = (unsigned long long)xr * plane;
+    const float* dq = div + 2ull * xr * plane;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      float v[2] = {0.f, 0.f};
+      const unsigned long long r = rq + goff2[k];
+      if (in2[k]) {
+        const float2* S1 = L1 + b1 * kL1N + c2[k];
+        const float2 c = S1[0];
+        const float xm0 = xr > 0 ? L1[b0 * kL1N + c2[k]].y : c.x;
+        const float xp1 = xr + 1 < g.nxr ? L1[b2 * kL1N + c2[k]].x : c.y;
+        const float2 rr = jacobi_pair(xm0, c.y, c.x, xp1, S1[eym[k]], S1[eyp[k]], S1[ezm[k]], S1[ezp[k]],
+                                      __ldg(dq + goff2[k]), __ldg(dq + plane + goff2[k]), g.dx2);
+        v[0] = rr.x;
+        v[1] = rr.y;
+      }
+      const uint32_t hh = SpecP::DITHER ? qmpm::mix32((uint32_t)r ^ salt2) : 0u;
+      uint32_t o[W + 1];
+      qmpm::encode_record<SpecP>(v, hh, in2[k], o, nullptr);
+      if (in2[k]) qmpm::store_words<SpecP>(out + r * W, o);
+    }
+    const int t = b0;
+    b0 = b1, b1 = b2, b2 = t;
+  }
+}
+
+namespace smoke {
 }  // namespace smoke
 
 // ------------------------------------------------------------------ entry points
@@ -760,12 +964,9 @@ extern "C" __global__ void __launch_bounds__(256)
     float v[2] = {0.f, 0.f};
     if (valid) {
       // both cells at once in packed FP32x2 (FADD2 / FFMA2 / FMUL2)
-      const float2 sx = __fadd2_rn(make_float2(nb[0][0], nb[1][0]), make_float2(nb[0][1], nb[1][1]));
-      const float2 sy = __fadd2_rn(make_float2(nb[0][2], nb[1][2]), make_float2(nb[0][3], nb[1][3]));
-      const float2 sz = __fadd2_rn(make_float2(nb[0][4], nb[1][4]), make_float2(nb[0][5], nb[1][5]));
-      const float2 s2 = __fadd2_rn(__fadd2_rn(sx, sy), sz);
-      const float2 r2 = __fmul2_rn(__ffma2_rn(make_float2(-g.dx2, -g.dx2), make_float2(d[0], d[1]), s2),
-                                   make_float2(1.0f / 6.0f, 1.0f / 6.0f));
+      const float2 r2 = smoke::jacobi_pair(nb[0][0], nb[0][1], nb[1][0], nb[1][1], make_float2(nb[0][2], nb[1][2]),
+                                           make_float2(nb[0][3], nb[1][3]), make_float2(nb[0][4], nb[1][4]),
+                                           make_float2(nb[0][5], nb[1][5]), d[0], d[1], g.dx2);
       v[0] = r2.x;
       v[1] = r2.y;
       if (dbg) {

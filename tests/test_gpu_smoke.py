@@ -269,3 +269,20 @@ def test_far_departure_points_take_the_global_path():
     o[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]] = 1.0
     check_close(outr.cpu().numpy(), o, "far rho")
     sm.close()
+
+
+@pytest.mark.parametrize("iters", [4, 5])
+def test_fused_two_sweep_jacobi_is_bit_identical(iters, monkeypatch):
+    """qsmoke_jacobi2 (two sweeps per launch, QSMOKE_FUSE=1; off by default because it is
+    slower) against the chain of single sweeps: identical words."""
+    monkeypatch.setenv("QSMOKE_FUSE", "1")
+    res = (20, 18, 40)  # several y and z tiles of the fused kernel
+    params, su, sp, uw, uq, pw, pq, rho = make(res, seed=12, iters=iters)
+    sm = qsmoke.Smoke(params, su, sp)
+    sm.set_state(dev(uw), dev(pw), dev(rho), step=2)
+    sm.step(1)
+    g_u, g_p, g_rho = sm.get_state_numpy()
+    cu, cp, crho = chained_step(sm, params, su, sp, dev(uw), dev(pw), dev(rho), 2, iters)
+    assert np.array_equal(g_u, host_u32(cu)) and np.array_equal(g_p, host_u32(cp))
+    assert np.array_equal(g_rho, crho.cpu().numpy())
+    sm.close()
