@@ -24,6 +24,9 @@
 #pragma once
 #include "codec_record.cuh"
 
+#ifndef QSMOKE_JACOBI_MINB  // min resident CTAs per SM for the Jacobi sweep (tuning)
+#define QSMOKE_JACOBI_MINB 6  // measured: 6 -> 0.542 ms, 1 -> 0.580, 7-8 -> 0.63 (612^3)
+#endif
 #ifndef QSMOKE_ADV_MINB  // min resident CTAs per SM for the advection kernels (tuning)
 #define QSMOKE_ADV_MINB 2
 #endif
@@ -954,7 +957,7 @@ extern "C" __global__ void __launch_bounds__(256)
   }
 }
 
-extern "C" __global__ void __launch_bounds__(256)
+extern "C" __global__ void __launch_bounds__(256, QSMOKE_JACOBI_MINB)
     qsmoke_jacobi(const uint32_t* __restrict__ P, const float* __restrict__ div, SmokeDev g, SaltSrc ss,
                   uint32_t* __restrict__ out, float* __restrict__ dbg) {
   constexpr int W = SpecP::W;
