@@ -500,10 +500,12 @@ __device__ __forceinline__ void fill_store(const Fill<REFL, RHO>& F, int q, floa
 
 // march skeleton of the advection kernels: f(xr, y, z, r, valid, win) per record plane,
 // once the ring holds planes xr - 1 .. xr + 1
+// B (nullable): the buoyancy density, fetched for the thread's two cells one plane ahead
+// and passed to f as bq
 template <bool REFL, bool RHO, class F>
 __device__ __forceinline__ void adv_march(const uint32_t* __restrict__ U, const uint32_t* __restrict__ UR,
-                                          const float* __restrict__ D, const SmokeDev& g, float4* ru, float4* rr,
-                                          float* rd, F&& f) {
+                                          const float* __restrict__ D, const float* __restrict__ B, const SmokeDev& g,
+                                          float4* ru, float4* rr, float* rd, F&& f) {
   Win w;
   w.y0 = blockIdx.y * kTY;
   w.z0 = blockIdx.x * kTZ;
@@ -518,13 +520,21 @@ __device__ __forceinline__ void adv_march(const uint32_t* __restrict__ U, const 
   fill_load(U, UR, D, g, w, xs, fl);
   fill_store(fl, xs, ru, rr, rd);
   fill_load(U, UR, D, g, w, xs + 1, fl);  // q >= nxr loads nothing
+  const unsigned long long cplane = (unsigned long long)g.ny * g.nz;
+  const unsigned long long c0 = (unsigned long long)y * g.nz + z;
+  float2 bq = make_float2(0.f, 0.f);
+  if (B && valid) bq = make_float2(__ldg(B + 2ull * xs * cplane + c0), __ldg(B + (2ull * xs + 1) * cplane + c0));
   for (int xr = xs; xr < xe; ++xr) {
     w.xr = xr;
     fill_store(fl, xr + 1, ru, rr, rd);
     __syncthreads();
     if (xr + 1 < xe) fill_load(U, UR, D, g, w, xr + 2, fl);
+    float2 bn = make_float2(0.f, 0.f);
+    if (B && valid && xr + 1 < xe)
+      bn = make_float2(__ldg(B + 2ull * (xr + 1) * cplane + c0), __ldg(B + (2ull * xr + 3) * cplane + c0));
     const unsigned long long r = valid ? ((unsigned long long)xr * g.ny + y) * g.nz + z : 0ull;
-    f(xr, y, z, r, valid, w);
+    f(xr, y, z, r, valid, w, bq);
+    bq = bn;
     __syncthreads();
   }
 }
@@ -864,8 +874,9 @@ __device__ __forceinline__ void advect_u_body(const uint32_t* __restrict__ uv, c
   float4* ru = smem_adv;
   float4* rr = REFL ? smem_adv + smoke::kRing : nullptr;
   const uint32_t salt = smoke::salt_of(ss);
-  smoke::adv_march<REFL, false>(uv, ur, nullptr, g, ru, rr, nullptr, [&](int xr, int y, int z, unsigned long long r,
-                                                                       bool valid, const smoke::Win& w) {
+  smoke::adv_march<REFL, false>(uv, ur, nullptr, REFL ? nullptr : rho, g, ru, rr, nullptr,
+                                [&](int xr, int y, int z, unsigned long long r, bool valid, const smoke::Win& w,
+                                    float2 bq) {
     auto samp_u = [&](const float* p, float* o) { w.sample(g, ru, uv, nullptr, p, o); };
     float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (valid) {
@@ -881,7 +892,7 @@ __device__ __forceinline__ void advect_u_body(const uint32_t* __restrict__ uv, c
           w.sample(g, rr, uv, ur, xb, q);
         else
           samp_u(xb, q);
-        if (!REFL && rho) q[1] += bdt * __ldg(rho + ((unsigned long long)x * g.ny + y) * g.nz + z);
+        if (!REFL && rho) q[1] += bdt * (c2 == 0 ? bq.x : bq.y);
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[3 * c2 + c] = q[c];
       }
@@ -1025,8 +1036,9 @@ extern "C" __global__ void __launch_bounds__(256, QSMOKE_ADV_MINB)
   // the last kernel of a step advances the device step counter (nothing here reads it)
   if (tick && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0 && threadIdx.y == 0)
     *tick += 1ull;
-  smoke::adv_march<false, true>(U, nullptr, rho, g, ru, nullptr, rd, [&](int xr, int y, int z, unsigned long long r,
-                                                                          bool valid, const smoke::Win& w) {
+  smoke::adv_march<false, true>(U, nullptr, rho, nullptr, g, ru, nullptr, rd,
+                                [&](int xr, int y, int z, unsigned long long r, bool valid, const smoke::Win& w,
+                                    float2) {
     if (!valid) return;
     auto samp_u = [&](const float* p, float* o) { w.sample(g, ru, U, nullptr, p, o); };
     const unsigned long long plane = (unsigned long long)g.ny * g.nz;
