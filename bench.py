@@ -52,6 +52,8 @@ def parse():
                     help="C4 only: z extent of the 1-GPU domain (reduced same-density runs for profiling)")
     ap.add_argument("--scene-warmup", type=int, default=50)
     ap.add_argument("--rounding", default="dither", choices=["dither", "rne"])
+    ap.add_argument("--layout", default="pack", choices=["pack", "nostraddle"],
+                    help="bit pack (P:542-549) or no field straddling a word (the bit struct's rule, P:540)")
     ap.add_argument("--no-counters", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1_000_000)
@@ -77,7 +79,7 @@ def make_scene(args, world=1):
         sch = schemes.f2()
     if args.scheme:
         sch = schemes.fp32(sc.dim, sc.material) if args.scheme == "fp32" else schemes.BY_NAME[args.scheme]()
-    sch = schemes.with_rounding(sch, args.rounding)
+    sch = schemes.with_layout(schemes.with_rounding(sch, args.rounding), args.layout)
     return sc, sch
 
 
@@ -88,7 +90,8 @@ def scheme_name(args):
 def workload_name(args, sc, W, bits):
     return (f"{sc.name}: {sc.dim}D {sc.material}, {sc.n_particles:,} particles, "
             f"{'x'.join(str(r) for r in sc.sim['grid_res'][:sc.dim])} block-sparse grid, "
-            f"dt {sc.sim['dt']:g}, scheme {scheme_name(args)} ({bits} bits, W={W})")
+            f"dt {sc.sim['dt']:g}, scheme {scheme_name(args)} ({bits} bits, W={W}"
+            + (", no-straddle layout" if args.layout == "nostraddle" else "") + ")")
 
 
 # --------------------------------------------------------------------------- clocks
@@ -345,7 +348,8 @@ def run_gpu(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
         "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": (value / (world if args.scaling == "weak" else 1) / PAPER_PSTEPS[args.config])
-        if (args.config in PAPER_PSTEPS and not args.n and scheme_name(args) == {"c3": "e0.01", "c4": "f2"}[args.config])
+        if (args.config in PAPER_PSTEPS and not args.n and args.layout == "pack"
+            and scheme_name(args) == {"c3": "e0.01", "c4": "f2"}[args.config])
         else None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(args, sc, W, bits), "particles_per_gpu": N,

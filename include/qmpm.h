@@ -98,7 +98,9 @@ typedef struct {
     uint32_t rounding; /* QMPM_DITHER | QMPM_RNE */
     const qmpm_field* fields; /* host pointer, n_fields entries, packing order */
     uint64_t dither_seed;     /* seed of the content-keyed dither hash (reading Q5) */
-    uint32_t layout_policy;   /* 0 = bit pack (fields may straddle words) */
+    uint32_t layout_policy;   /* 0 = bit pack (fields may straddle words); 1 = no field
+                                 straddles a word (the bit struct's rule): a field that would
+                                 cross a word boundary starts at the next word */
     uint32_t pad;
 } qmpm_scheme;
 

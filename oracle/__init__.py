@@ -50,7 +50,7 @@ class OracleScheme(ctypes.Structure):
                 ("offset", ctypes.c_float * MAX_FIELDS),
                 ("scalar", ctypes.c_uint32 * MAX_FIELDS),
                 ("rounding", ctypes.c_uint32),
-                ("pad", ctypes.c_uint32),
+                ("layout_policy", ctypes.c_uint32),
                 ("dither_seed", ctypes.c_uint64),
                 ("exp_bits", ctypes.c_uint32 * MAX_FIELDS),
                 ("group", ctypes.c_uint32 * MAX_FIELDS)]
@@ -144,6 +144,7 @@ def make_scheme(scheme) -> OracleScheme:
         else:
             s.scalar[i] = i
     s.rounding = 1 if scheme.get("rounding", "dither") == "dither" else 0
+    s.layout_policy = {"pack": 0, "nostraddle": 1}[scheme.get("layout", "pack")]
     s.dither_seed = scheme.get("seed", 0)
     return s
 

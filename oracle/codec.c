@@ -93,6 +93,11 @@ int oracle_layout(const oracle_scheme* s, uint32_t* offsets, uint32_t* words, ui
         }
         uint32_t w = field_width(s, f);
         if (w == 0 || w > 32) return -1;
+        /* layout policy 1, the bit struct's rule ("it does not allow custom data
+         * types to span across two physical words"): a field that would straddle starts
+         * at the next word (Fig. bit_struct: three 17-bit fields take 3 words) */
+        if (s->layout_policy == 1 && (total % 32) + w > 32) total = (total + 31) / 32 * 32;
+        if (s->layout_policy > 1) return -1;
         if (offsets) offsets[f] = total;
         total += w;
     }

@@ -42,7 +42,7 @@ typedef struct {
     float offset[ORACLE_MAX_FIELDS];       /* value = offset + u*Delta (reading Q21) */
     uint32_t scalar[ORACLE_MAX_FIELDS];    /* which state scalar the field stores */
     uint32_t rounding;                     /* ORACLE_RNE or ORACLE_DITHER */
-    uint32_t pad;
+    uint32_t layout_policy;                /* 0 bit pack; 1 no field straddles a word (bit struct) */
     uint64_t dither_seed;
     /* SHARED_EXP (reading Q4): consecutive fields with the same group id share one
      * exp_bits-bit exponent E stored in front of the group's first mantissa; member

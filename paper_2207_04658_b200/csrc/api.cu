@@ -140,13 +140,14 @@ uint32_t field_width_in(const qmpm_scheme* s, uint32_t i) {
   return field_width(s->fields[i]) + (group_first(s, i) ? s->fields[i].exp_bits : 0u);
 }
 
-// bit-pack layout: contiguous, LSB-first, in declaration order
+// bit-pack layout: contiguous, LSB-first, in declaration order; layout_policy 1
+// keeps every field inside one word (the bit struct's rule)
 qmpm_status layout_of(qmpm_ctx* ctx, const qmpm_scheme* s, std::vector<uint32_t>& offs, uint32_t& W,
                       uint32_t& bits) {
   if (!s || !s->fields) return fail(ctx, QMPM_EINVAL, "scheme or scheme->fields is NULL");
   if (s->n_fields == 0 || s->n_fields > QMPM_MAX_FIELDS)
     return fail(ctx, QMPM_ELAYOUT, "n_fields=%u out of [1, %d]", s->n_fields, QMPM_MAX_FIELDS);
-  if (s->layout_policy != 0) return fail(ctx, QMPM_ELAYOUT, "layout_policy %u not supported", s->layout_policy);
+  if (s->layout_policy > 1) return fail(ctx, QMPM_ELAYOUT, "layout_policy %u not supported", s->layout_policy);
   offs.resize(s->n_fields);
   uint32_t total = 0;
   for (uint32_t i = 0; i < s->n_fields; ++i) {
@@ -171,8 +172,11 @@ qmpm_status layout_of(qmpm_ctx* ctx, const qmpm_scheme* s, std::vector<uint32_t>
       if (!(f.range > 0.0f) || !std::isfinite(f.range)) return fail(ctx, QMPM_ELAYOUT, "field %u: range must be > 0", i);
       if (!std::isfinite(f.offset)) return fail(ctx, QMPM_ELAYOUT, "field %u: offset not finite", i);
     }
+    const uint32_t w = field_width_in(s, i);
+    // policy 1 (bit struct): a field that would straddle starts at the next word
+    if (s->layout_policy == 1 && (total % 32) + w > 32) total = (total + 31) / 32 * 32;
     offs[i] = total;
-    total += field_width_in(s, i);
+    total += w;
   }
   bits = total;
   W = (total + 31) / 32;

@@ -168,7 +168,7 @@ class CScheme:
         self.s.rounding = ROUNDING[scheme.get("rounding", "dither")]
         self.s.fields = ctypes.cast(self.fields, ctypes.POINTER(Field))
         self.s.dither_seed = scheme.get("seed", 0)
-        self.s.layout_policy = 0
+        self.s.layout_policy = {"pack": 0, "nostraddle": 1}[scheme.get("layout", "pack")]
 
     @property
     def ref(self):

@@ -135,6 +135,14 @@ def smoke_raw(n):
                 fields=[dict(kind="raw") for _ in range(n)])
 
 
+def with_layout(scheme, layout):
+    """layout: "pack" (bit pack) or "nostraddle" (no field crosses a word: the
+    bit struct's rule, P:540 -- the T-bitpack-perf analogue)."""
+    s = dict(scheme)
+    s["layout"] = layout
+    return s
+
+
 def with_rounding(scheme, rounding):
     s = dict(scheme)
     s["rounding"] = rounding

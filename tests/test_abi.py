@@ -82,6 +82,8 @@ def test_layout_fig_bit_struct_and_errors():
              fields=[dict(kind="fixed", frac_bits=16, range=1.0) for _ in range(3)])
     offs, W, bits = qmpm.layout(s)
     assert offs == [0, 17, 34] and W == 2  # three 17-bit values in two words
+    offs, W, bits = qmpm.layout(schemes.with_layout(s, "nostraddle"))
+    assert offs == [0, 32, 64] and W == 3  # "the three 17-bit elements consume three bit structs"
     bad = dict(s, fields=[dict(kind="fixed", frac_bits=32, range=1.0)])
     with pytest.raises(qmpm.QmpmError) as e:
         qmpm.layout(bad)
@@ -128,3 +130,28 @@ def test_adjoint_create_rejects_bad_arguments_without_gpu():
     assert L.qadj_create(ctypes.byref(p), 2, 7, s0.shape[0], None, ctypes.byref(ctx)) == 1  # material
     assert L.qadj_create(ctypes.byref(p), 4, 1, s0.shape[0], None, ctypes.byref(ctx)) == 1  # dim
     assert L.qadj_create(ctypes.byref(p), 2, 1, 0, None, ctypes.byref(ctx)) == 1            # n = 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_nostraddle_layout_matches_oracle_and_never_straddles(seed):
+    """Layout policy 1 (the bit struct's rule): library == oracle offsets, no
+    field crosses a word, bit pack never needs more words, fields keep their order."""
+    import oracle
+    from test_gpu_codec import mixed_scheme, mixed_shared_scheme
+    rng = np.random.default_rng(seed)
+    sch = (mixed_shared_scheme if seed % 2 else mixed_scheme)(rng)
+    ns = schemes.with_layout(sch, "nostraddle")
+    offs, W, bits = qmpm.layout(ns)
+    o_offs, o_W, o_bits = oracle.layout(ns)
+    assert offs == list(o_offs) and W == o_W and bits == o_bits
+    _, W_pack, _ = qmpm.layout(sch)
+    assert W >= W_pack
+    widths = []
+    for i, f in enumerate(ns["fields"]):
+        w = 32 if f["kind"] == "raw" else f["frac_bits"] + 1
+        lead = f["kind"] == "shared_exp" and (i == 0 or ns["fields"][i - 1]["kind"] != "shared_exp"
+                                              or ns["fields"][i - 1].get("group", 0) != f.get("group", 0))
+        widths.append(w + (f["exp_bits"] if lead else 0))
+    for o, w in zip(offs, widths):
+        assert o % 32 + w <= 32
+    assert all(a < b for a, b in zip(offs, offs[1:]))

@@ -68,7 +68,9 @@ def mixed_shared_scheme(rng, nf=24):
 
 
 SCHEMES = {"x16": schemes.x16(), "e0.1": schemes.e01(), "e0.01": schemes.e001(), "f2": schemes.f2(),
-           "fp32": schemes.fp32(3), "se2": schemes.se2()}
+           "fp32": schemes.fp32(3), "se2": schemes.se2(),
+           "e0.01_nostraddle": schemes.with_layout(schemes.e001(), "nostraddle"),
+           "se2_nostraddle": schemes.with_layout(schemes.se2(), "nostraddle")}
 
 
 @pytest.mark.parametrize("name", list(SCHEMES) + ["mixed0", "mixed1", "mixed2", "mixed_se0", "mixed_se1", "mixed_se2"])

@@ -87,6 +87,9 @@ CASES = {
     "s3_3d_fp32": (scenes.small_elastic_3d, lambda: schemes.fp32(3), 20),
     "s4_3d_fluid_f2": (scenes.small_fluid_3d, schemes.f2, 20),
     "s4_3d_fluid_se2": (scenes.small_fluid_3d, schemes.se2, 20),
+    # no field straddles a word (the bit struct's rule; T-bitpack-perf analogue)
+    "s3_3d_e0.01_nostraddle": (scenes.small_elastic_3d, lambda: schemes.with_layout(schemes.e001(), "nostraddle"), 20),
+    "s4_3d_fluid_f2_nostraddle": (scenes.small_fluid_3d, lambda: schemes.with_layout(schemes.f2(), "nostraddle"), 20),
 }
 
 
