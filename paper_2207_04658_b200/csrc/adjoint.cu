@@ -22,9 +22,11 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "qadjoint.h"
@@ -283,9 +285,8 @@ __device__ __forceinline__ void affine(const float* st, const AdjSim& S, float (
 }
 
 template <int D, bool EL>
-__global__ void k_p2g_fwd(const float* __restrict__ s, uint64_t n, AdjSim S, float4* __restrict__ grid) {
+__device__ __forceinline__ void p2g_fwd_body(uint64_t p, const float* __restrict__ s, uint64_t n, AdjSim S, float4* __restrict__ grid) {
   constexpr int NS = kNS<D, EL>;
-  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const float* st = s + p * NS;
   const Stencil<D> sc = stencil<D>(st, S);
@@ -315,6 +316,11 @@ __global__ void k_p2g_fwd(const float* __restrict__ s, uint64_t n, AdjSim S, flo
   }
 }
 
+template <int D, bool EL>
+__global__ void k_p2g_fwd(const float* __restrict__ s, uint64_t n, AdjSim S, float4* __restrict__ grid) {
+  p2g_fwd_body<D, EL>((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, s, n, S, grid);
+}
+
 __device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? v.y : (a == 1 ? v.z : v.w); }
 
 // v = P/m + dt g, separating walls (reading Q13): gv = (m, vx, vy, vz).  The grids are
@@ -322,9 +328,8 @@ __device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? 
 // read (clear_grid), the adjoint step clears `lgrid` here (before g2p_bwd accumulates
 // into it) and `grid` in k_grid_bwd, its last reader.
 template <int D>
-__global__ void k_grid_fwd(float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ gv,
+__device__ __forceinline__ void grid_fwd_body(uint64_t c, float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ gv,
                            bool clear_grid, float4* __restrict__ clear_lgrid) {
-  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nn) return;
   const float4 nd = grid[c];
   if (clear_grid) grid[c] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -344,6 +349,12 @@ __global__ void k_grid_fwd(float4* __restrict__ grid, uint64_t nn, AdjSim S, flo
     out = make_float4(nd.x, v[0], v[1], v[2]);
   }
   gv[c] = out;
+}
+
+template <int D>
+__global__ void k_grid_fwd(float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ gv,
+                           bool clear_grid, float4* __restrict__ clear_lgrid) {
+  grid_fwd_body<D>((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, grid, nn, S, gv, clear_grid, clear_lgrid);
 }
 
 // v' and C' of a particle from the updated grid
@@ -373,10 +384,9 @@ __device__ __forceinline__ void gather(const Stencil<D>& sc, const float4* __res
 }
 
 template <int D, bool EL>
-__global__ void k_g2p_fwd(const float* __restrict__ s, uint64_t n, const float4* __restrict__ gv, AdjSim S,
+__device__ __forceinline__ void g2p_fwd_body(uint64_t p, const float* __restrict__ s, uint64_t n, const float4* __restrict__ gv, AdjSim S,
                           float* __restrict__ out) {
   constexpr int NS = kNS<D, EL>, CO = kCO<D, EL>;
-  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const float* st = s + p * NS;
   const Stencil<D> sc = stencil<D>(st, S);
@@ -410,6 +420,12 @@ __global__ void k_g2p_fwd(const float* __restrict__ s, uint64_t n, const float4*
     for (int b = 0; b < D; ++b) o[CO + a * D + b] = C[a][b];
 }
 
+template <int D, bool EL>
+__global__ void k_g2p_fwd(const float* __restrict__ s, uint64_t n, const float4* __restrict__ gv, AdjSim S,
+                          float* __restrict__ out) {
+  g2p_fwd_body<D, EL>((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, s, n, gv, S, out);
+}
+
 // ---------------------------------------------------------------- adjoint
 // sum_p lambda^2 per scalar into g: warp shuffles, then the 8 warps of the CTA through
 // shared memory (double), then ONE double atomic per scalar per CTA (per-warp atomics on
@@ -437,10 +453,9 @@ __device__ __forceinline__ void tally(const float* lam, bool valid, double* g) {
 
 // lambda_T = (0, m v_T, 0, 0), the kinetic energy z and the tally of lambda_T
 template <int D, bool EL>
-__global__ void k_lambda_T(const float* __restrict__ s, uint64_t n, AdjSim S, float* __restrict__ lam, double* g,
+__device__ __forceinline__ void lambda_T_body(uint64_t p, const float* __restrict__ s, uint64_t n, AdjSim S, float* __restrict__ lam, double* g,
                            double* z) {
   constexpr int NS = kNS<D, EL>;
-  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = p < n;
   float l[NS];
 #pragma unroll
@@ -462,14 +477,19 @@ __global__ void k_lambda_T(const float* __restrict__ s, uint64_t n, AdjSim S, fl
   if ((threadIdx.x & 31) == 0 && ke != 0.0f) atomicAdd(z, (double)ke);
 }
 
+template <int D, bool EL>
+__global__ void k_lambda_T(const float* __restrict__ s, uint64_t n, AdjSim S, float* __restrict__ lam, double* g,
+                           double* z) {
+  lambda_T_body<D, EL>((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, s, n, S, lam, g, z);
+}
+
 // G2P reverse: node adjoints lgrid.yzw += W (lv' + 4/dx lC' (o - fx)); particle partials:
 // lam_t = (lx', 0, lJ' (1 + dt tr C') | (I + dt C')^T lF', 0) and lfx through G2P
 template <int D, bool EL>
-__global__ void k_g2p_bwd(const float* __restrict__ s, const float* __restrict__ lam1, uint64_t n,
+__device__ __forceinline__ void g2p_bwd_body(uint64_t p, const float* __restrict__ s, const float* __restrict__ lam1, uint64_t n,
                           const float4* __restrict__ gv, AdjSim S, float4* __restrict__ lgrid,
                           float* __restrict__ lam, float* __restrict__ lfx_out) {
   constexpr int NS = kNS<D, EL>, CO = kCO<D, EL>;
-  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const float* st = s + p * NS;
   const float* l1 = lam1 + p * NS;
@@ -549,11 +569,17 @@ __global__ void k_g2p_bwd(const float* __restrict__ s, const float* __restrict__
   for (int a = 0; a < D; ++a) lfx_out[p * 3 + a] = lfx[a];
 }
 
+template <int D, bool EL>
+__global__ void k_g2p_bwd(const float* __restrict__ s, const float* __restrict__ lam1, uint64_t n,
+                          const float4* __restrict__ gv, AdjSim S, float4* __restrict__ lgrid,
+                          float* __restrict__ lam, float* __restrict__ lfx_out) {
+  g2p_bwd_body<D, EL>((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, s, lam1, n, gv, S, lgrid, lam, lfx_out);
+}
+
 // grid reverse: (0, lv) -> (lm, lP); lP = lv / m, lm = -lv . u / m, u = P / m; zero on
 // wall-clamped components and on empty nodes
 template <int D>
-__global__ void k_grid_bwd(float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ lgrid) {
-  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void grid_bwd_body(uint64_t c, float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ lgrid) {
   if (c >= nn) return;
   const float4 nd = grid[c];
   grid[c] = make_float4(0.f, 0.f, 0.f, 0.f);  // last reader of the step's grid
@@ -577,12 +603,16 @@ __global__ void k_grid_bwd(float4* __restrict__ grid, uint64_t nn, AdjSim S, flo
   lgrid[c] = out;
 }
 
+template <int D>
+__global__ void k_grid_bwd(float4* __restrict__ grid, uint64_t nn, AdjSim S, float4* __restrict__ lgrid) {
+  grid_bwd_body<D>((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, grid, nn, S, lgrid);
+}
+
 // P2G reverse: finishes lambda_t and tallies it
 template <int D, bool EL>
-__global__ void k_p2g_bwd(const float* __restrict__ s, uint64_t n, const float4* __restrict__ lgrid, AdjSim S,
+__device__ __forceinline__ void p2g_bwd_body(uint64_t p, const float* __restrict__ s, uint64_t n, const float4* __restrict__ lgrid, AdjSim S,
                           const float* __restrict__ lfx_in, float* __restrict__ lam, double* __restrict__ g) {
   constexpr int NS = kNS<D, EL>, CO = kCO<D, EL>;
-  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = p < n;
   float l[NS];
 #pragma unroll
@@ -658,12 +688,65 @@ __global__ void k_p2g_bwd(const float* __restrict__ s, uint64_t n, const float4*
   if (g) tally<NS>(l, valid, g);
 }
 
+template <int D, bool EL>
+__global__ void k_p2g_bwd(const float* __restrict__ s, uint64_t n, const float4* __restrict__ lgrid, AdjSim S,
+                          const float* __restrict__ lfx_in, float* __restrict__ lam, double* __restrict__ g) {
+  p2g_bwd_body<D, EL>((uint64_t)blockIdx.x * blockDim.x + threadIdx.x, s, n, lgrid, S, lfx_in, lam, g);
+}
+
+// ---- cooperative (single-launch) step chains (QADJ_COOP=1) ------------------------------
+// k forward steps, or one adjoint step, in ONE cooperative launch with grid-wide barriers
+// between the phases (the same device bodies as the separate kernels, so the same
+// arithmetic).  Kept as an option: measured no faster (see qadj_create).
+template <int D, bool EL>
+__global__ void __launch_bounds__(256) k_forward_chain(const float* __restrict__ s0, float* __restrict__ a,
+                                                       float* __restrict__ b, uint32_t k, uint64_t n, uint64_t nn,
+                                                       AdjSim S, float4* __restrict__ grid, float4* __restrict__ gv) {
+  cooperative_groups::grid_group G = cooperative_groups::this_grid();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const float* in = s0;
+  for (uint32_t i = 0; i < k; ++i) {
+    float* out = (i % 2 == 0) ? a : b;
+    for (uint64_t p = t0; p < n; p += stride) p2g_fwd_body<D, EL>(p, in, n, S, grid);
+    G.sync();
+    for (uint64_t c = t0; c < nn; c += stride) grid_fwd_body<D>(c, grid, nn, S, gv, true, nullptr);
+    G.sync();
+    for (uint64_t p = t0; p < n; p += stride) g2p_fwd_body<D, EL>(p, in, n, gv, S, out);
+    G.sync();
+    in = out;
+  }
+}
+
+template <int D, bool EL>
+__global__ void __launch_bounds__(256) k_adjoint_coop(const float* __restrict__ s, const float* __restrict__ lam1,
+                                                      float* __restrict__ lam, double* __restrict__ g, uint64_t n,
+                                                      uint64_t nn, AdjSim S, float4* __restrict__ grid,
+                                                      float4* __restrict__ gv, float4* __restrict__ lgrid,
+                                                      float* __restrict__ lfx) {
+  cooperative_groups::grid_group G = cooperative_groups::this_grid();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t p = t0; p < n; p += stride) p2g_fwd_body<D, EL>(p, s, n, S, grid);
+  G.sync();
+  for (uint64_t c = t0; c < nn; c += stride) grid_fwd_body<D>(c, grid, nn, S, gv, false, lgrid);
+  G.sync();
+  for (uint64_t p = t0; p < n; p += stride) g2p_bwd_body<D, EL>(p, s, lam1, n, gv, S, lgrid, lam, lfx);
+  G.sync();
+  for (uint64_t c = t0; c < nn; c += stride) grid_bwd_body<D>(c, grid, nn, S, lgrid);
+  G.sync();
+  // block-uniform trip count: the tally's CTA barrier needs every thread
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride)
+    p2g_bwd_body<D, EL>(base + threadIdx.x, s, n, lgrid, S, lfx, lam, g);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- runtime
 struct qadj_ctx {
   int dim = 3;
   bool el = false;  // fixed-corotated elastic (else J-fluid)
+  unsigned coop_fwd = 0, coop_adj = 0;  // co-resident grid sizes of the cooperative kernels (0: not used)
   uint64_t n = 0, nn = 0;
   int ns = 0;
   AdjSim S{};
@@ -695,6 +778,45 @@ void adjoint_k(qadj_ctx* c, const float* s, const float* lam1, float* lam, doubl
   k_p2g_bwd<D, EL><<<blocks(c->n), 256, 0, c->stream>>>(s, c->n, c->lgrid, c->S, c->lfx, lam, g);
 }
 
+qmpm_status forward_dev(qadj_ctx* c, const float* in, float* out);
+
+template <int D, bool EL>
+cudaError_t chain_k(qadj_ctx* c, const float* s0, float* a, float* b, uint32_t k) {
+  void* args[] = {&s0, &a, &b, &k, &c->n, &c->nn, &c->S, &c->grid, &c->gv};
+  return cudaLaunchCooperativeKernel((const void*)k_forward_chain<D, EL>, dim3(c->coop_fwd), dim3(256), args, 0,
+                                     c->stream);
+}
+
+template <int D, bool EL>
+cudaError_t adjoint_coop_k(qadj_ctx* c, const float* s, const float* lam1, float* lam, double* g) {
+  void* args[] = {&s, &lam1, &lam, &g, &c->n, &c->nn, &c->S, &c->grid, &c->gv, &c->lgrid, &c->lfx};
+  return cudaLaunchCooperativeKernel((const void*)k_adjoint_coop<D, EL>, dim3(c->coop_adj), dim3(256), args, 0,
+                                     c->stream);
+}
+
+// k forward steps from s0 alternating into a, b (the last step lands in (k - 1) % 2 ? b : a)
+qmpm_status forward_chain_dev(qadj_ctx* c, const float* s0, float* a, float* b, uint32_t k) {
+  if (k == 0) return QMPM_OK;
+  if (c->coop_fwd) {
+    cudaError_t e;
+    if (c->dim == 3)
+      e = c->el ? chain_k<3, true>(c, s0, a, b, k) : chain_k<3, false>(c, s0, a, b, k);
+    else
+      e = c->el ? chain_k<2, true>(c, s0, a, b, k) : chain_k<2, false>(c, s0, a, b, k);
+    c->launches += 1;
+    ACK(e);
+    return QMPM_OK;
+  }
+  const float* cur = s0;
+  for (uint32_t i = 0; i < k; ++i) {
+    float* dst = (i % 2 == 0) ? a : b;
+    qmpm_status rc = forward_dev(c, cur, dst);
+    if (rc) return rc;
+    cur = dst;
+  }
+  return QMPM_OK;
+}
+
 qmpm_status forward_dev(qadj_ctx* c, const float* in, float* out) {
   if (c->dim == 3)
     c->el ? forward_k<3, true>(c, in, out) : forward_k<3, false>(c, in, out);
@@ -707,6 +829,16 @@ qmpm_status forward_dev(qadj_ctx* c, const float* in, float* out) {
 
 // lambda_t from s_t and lambda_{t+1} (g nullable: device tallies to accumulate)
 qmpm_status adjoint_dev(qadj_ctx* c, const float* s, const float* lam1, float* lam, double* g) {
+  if (c->coop_adj) {
+    cudaError_t e;
+    if (c->dim == 3)
+      e = c->el ? adjoint_coop_k<3, true>(c, s, lam1, lam, g) : adjoint_coop_k<3, false>(c, s, lam1, lam, g);
+    else
+      e = c->el ? adjoint_coop_k<2, true>(c, s, lam1, lam, g) : adjoint_coop_k<2, false>(c, s, lam1, lam, g);
+    c->launches += 1;
+    ACK(e);
+    return QMPM_OK;
+  }
   if (c->dim == 3)
     c->el ? adjoint_k<3, true>(c, s, lam1, lam, g) : adjoint_k<3, false>(c, s, lam1, lam, g);
   else
@@ -714,6 +846,17 @@ qmpm_status adjoint_dev(qadj_ctx* c, const float* s, const float* lam1, float* l
   c->launches += 5;
   ACK(cudaGetLastError());
   return QMPM_OK;
+}
+
+template <int D, bool EL>
+void coop_sizes(qadj_ctx* c, int sms) {
+  int bf = 0, ba = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_forward_chain<D, EL>, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ba, k_adjoint_coop<D, EL>, 256, 0);
+  cudaGetLastError();
+  const uint64_t need = (std::max(c->n, c->nn) + 255) / 256;  // more CTAs than work only idles
+  c->coop_fwd = (unsigned)std::min<uint64_t>((uint64_t)bf * sms, need);
+  c->coop_adj = (unsigned)std::min<uint64_t>((uint64_t)ba * sms, need);
 }
 
 qmpm_status get_buf(qadj_ctx* c, std::vector<float*>& freel, float** out) {
@@ -744,16 +887,12 @@ struct Bisect {
     qmpm_status rc = get_buf(c, freel, &a);
     if (!rc) rc = get_buf(c, freel, &b);
     if (rc) return rc;
-    const float* cur = s;
-    for (uint32_t i = 0; i < k; ++i) {
-      float* dst = (i % 2 == 0) ? a : b;
-      rc = forward_dev(c, cur, dst);
-      if (rc) return rc;
-      cur = dst;
-      ++fwd;
-    }
-    *out = (float*)cur;
-    freel.push_back(cur == a ? b : a);
+    rc = forward_chain_dev(c, s, a, b, k);
+    if (rc) return rc;
+    fwd += k;
+    float* last = ((k - 1) % 2 == 0) ? a : b;
+    *out = last;
+    freel.push_back(last == a ? b : a);
     return QMPM_OK;
   }
 
@@ -819,6 +958,24 @@ qmpm_status qadj_create(const qmpm_params* params, int32_t dim, int32_t material
   if (!e) e = cudaMalloc(&c->lfx, sizeof(float) * 3 * n);
   if (!e) e = cudaMalloc(&c->dacc, sizeof(double) * (c->ns + 1));
   if (!e) e = cudaMemsetAsync(c->grid, 0, sizeof(float4) * c->nn, c->stream);  // zero between steps from here on
+  // QADJ_COOP=1: one cooperative launch per forward chain / adjoint step.  Measured, not
+  // the default: at 80K particles (2D) a cooperative step costs what the separate
+  // launches cost (29 us: the step is bound by its P2G atomics, not by launches), and at
+  // 1M (3D) the grid-stride phases are 13 % slower than full-width launches.
+  if (!e) {
+    int dev = 0, coop = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const char* env = getenv("QADJ_COOP");
+    const bool use = coop && env && atoi(env) != 0;
+    if (use) {
+      if (dim == 3)
+        c->el ? coop_sizes<3, true>(c, sms) : coop_sizes<3, false>(c, sms);
+      else
+        c->el ? coop_sizes<2, true>(c, sms) : coop_sizes<2, false>(c, sms);
+    }
+  }
   if (!e) e = cudaStreamSynchronize(c->stream);
   if (e) {
     cudaGetLastError();
