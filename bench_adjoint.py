@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=None, help="T (default: the config's)")
     ap.add_argument("--warmup", type=int, default=3, help="warm-up tallies with T = 4")
     ap.add_argument("--cpu-steps", type=int, default=8)
+    ap.add_argument("--repeats", type=int, default=3, help="timed tallies (the median is reported)")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -103,14 +104,17 @@ def run_gpu(args):
     clocks = ClockSampler(0)
     clocks.start()
     time.sleep(0.3)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    g, z, st = A.gradient_tally(s0d, T)  # synchronizes
-    e1.record(stream)
-    e1.synchronize()
+    times = []
+    for _ in range(args.repeats):  # the median of `repeats` whole tallies
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g, z, st = A.gradient_tally(s0d, T)  # synchronizes
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    launches = A.launch_count() - l0
+    ms = sorted(times)[len(times) // 2]
+    launches = (A.launch_count() - l0) // args.repeats
     # e2e: the initial state from pinned host memory, tallies back to the host
     hs = torch.from_numpy(s0).pin_memory()
     t0 = time.perf_counter()
@@ -148,6 +152,7 @@ def run_gpu(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload(cfg, n, T), "particles": n, "state_bytes": n * ns * 4,
                    "parallelism": "single GPU"},
+        "timed_tallies_ms": times,
         "checkpointing": {"max_resident_states": st["max_resident"], "forward_steps": st["forward_steps"],
                           "adjoint_steps": st["adjoint_steps"], "log2_T": math.log2(max(T, 1))},
         "kernels": {"forward_step_ms": f_ms, "adjoint_step_ms": a_ms,

@@ -264,6 +264,39 @@ __device__ __forceinline__ void stress_el_adj(const float* F, const float (*lP)[
     }
 }
 
+// ---- warp-aggregated scatter -----------------------------------------------------------
+// Lanes whose particles share a base cell add into the same stencil nodes.  When every
+// such group is a contiguous run of lanes (particles stored in spatial order, as the
+// scenes' lattices are), the group's sums are formed with a segmented shuffle tree and
+// only its first lane issues the atomics; otherwise every lane adds its own.  All 32
+// lanes must call seg_of / seg_sum (invalid lanes pass a unique key and zeros).
+struct Seg {
+  bool ok;   // every group of the warp is contiguous
+  bool head; // this lane issues the group's atomics
+  int end;   // one past the group's last lane
+};
+
+__device__ __forceinline__ Seg seg_of(int key) {
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int lane = threadIdx.x & 31, s0 = __ffs(peers) - 1, g = __popc(peers);
+  const unsigned run = g == 32 ? 0xffffffffu : (((1u << g) - 1u) << s0);
+  Seg r;
+  r.ok = __all_sync(0xffffffffu, peers == run);
+  r.head = lane == s0;
+  r.end = s0 + g;
+  return r;
+}
+
+__device__ __forceinline__ float seg_sum(float v, const Seg& sg) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float o = __shfl_down_sync(0xffffffffu, v, off);
+    if (lane + off < sg.end) v += o;
+  }
+  return v;
+}
+
 // ---------------------------------------------------------------- forward
 // the affine matrix A = stress + m C of a state row (fluid: k (J - 1) I)
 template <int D, bool EL>
@@ -286,12 +319,15 @@ __device__ __forceinline__ void affine(const float* st, const AdjSim& S, float (
 
 template <int D, bool EL>
 __device__ __forceinline__ void p2g_fwd_body(uint64_t p, const float* __restrict__ s, uint64_t n, AdjSim S, float4* __restrict__ grid) {
+  // every lane of the warp must call (warp-aggregated atomics); lanes past n add nothing
   constexpr int NS = kNS<D, EL>;
-  if (p >= n) return;
-  const float* st = s + p * NS;
+  const bool valid = p < n;
+  const float* st = s + (valid ? p : 0) * NS;
   const Stencil<D> sc = stencil<D>(st, S);
   float A[D][D];
   affine<D, EL>(st, S, A);
+  const int o0[3] = {0, 0, 0};
+  const Seg sg = seg_of(valid ? (int)node_of<D>(sc, o0, S) : -1 - (int)(threadIdx.x & 31));
   for (int q = 0; q < kNO<D>; ++q) {
     int o[3];
     offset_of<D>(q, o);
@@ -300,19 +336,25 @@ __device__ __forceinline__ void p2g_fwd_body(uint64_t p, const float* __restrict
     float dpos[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) dpos[a] = ((float)o[a] - sc.fx[a]) * S.dx;
-    float4* nd = grid + node_of<D>(sc, o, S);
-    atomicAdd(&nd->x, W * S.m);
-    float P[3] = {0.f, 0.f, 0.f};
+    float vals[4] = {valid ? W * S.m : 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       float Ad = 0.0f;
 #pragma unroll
       for (int b = 0; b < D; ++b) Ad += A[a][b] * dpos[b];
-      P[a] = W * (S.m * st[D + a] + Ad);
+      vals[1 + a] = valid ? W * (S.m * st[D + a] + Ad) : 0.f;
     }
-    atomicAdd(&nd->y, P[0]);
-    atomicAdd(&nd->z, P[1]);
-    if (D == 3) atomicAdd(&nd->w, P[2]);
+    float4* nd = grid + node_of<D>(sc, o, S);
+    if (sg.ok) {
+#pragma unroll
+      for (int c = 0; c < D + 1; ++c) vals[c] = seg_sum(vals[c], sg);
+    }
+    if (valid && (!sg.ok || sg.head)) {
+      atomicAdd(&nd->x, vals[0]);
+      atomicAdd(&nd->y, vals[1]);
+      atomicAdd(&nd->z, vals[2]);
+      if (D == 3) atomicAdd(&nd->w, vals[3]);
+    }
   }
 }
 
@@ -490,7 +532,9 @@ __device__ __forceinline__ void g2p_bwd_body(uint64_t p, const float* __restrict
                           const float4* __restrict__ gv, AdjSim S, float4* __restrict__ lgrid,
                           float* __restrict__ lam, float* __restrict__ lfx_out) {
   constexpr int NS = kNS<D, EL>, CO = kCO<D, EL>;
-  if (p >= n) return;
+  // every lane of the warp must call (warp-aggregated atomics); lanes past n write nothing
+  const bool valid = p < n;
+  if (!valid) p = 0;
   const float* st = s + p * NS;
   const float* l1 = lam1 + p * NS;
   const Stencil<D> sc = stencil<D>(st, S);
@@ -498,12 +542,13 @@ __device__ __forceinline__ void g2p_bwd_body(uint64_t p, const float* __restrict
   gather<D>(sc, gv, S, vnew, Cn);  // forward recompute of C'
   float lv[D], lC[D][D];
   float* lo = lam + p * NS;
+  float lw[NS];
 #pragma unroll
-  for (int h = 0; h < NS; ++h) lo[h] = 0.0f;
+  for (int h = 0; h < NS; ++h) lw[h] = 0.0f;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     lv[a] = l1[D + a] + S.dt * l1[a];
-    lo[a] = l1[a];
+    lw[a] = l1[a];
 #pragma unroll
     for (int b = 0; b < D; ++b) lC[a][b] = l1[CO + a * D + b];
   }
@@ -519,7 +564,7 @@ __device__ __forceinline__ void g2p_bwd_body(uint64_t p, const float* __restrict
           acc += ((e == a ? 1.0f : 0.0f) + S.dt * Cn[e][a]) * l1[2 * D + e * D + b];
           acc2 += l1[2 * D + a * D + e] * st[2 * D + b * D + e];
         }
-        lo[2 * D + a * D + b] = acc;
+        lw[2 * D + a * D + b] = acc;
         lC[a][b] += S.dt * acc2;
       }
   } else {
@@ -527,13 +572,15 @@ __device__ __forceinline__ void g2p_bwd_body(uint64_t p, const float* __restrict
 #pragma unroll
     for (int a = 0; a < D; ++a) tr += Cn[a][a];
     const float lJ1 = l1[2 * D];
-    lo[2 * D] = lJ1 * (1.0f + S.dt * tr);
+    lw[2 * D] = lJ1 * (1.0f + S.dt * tr);
 #pragma unroll
     for (int a = 0; a < D; ++a) lC[a][a] += lJ1 * st[2 * D] * S.dt;
   }
   float lfx[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) lfx[a] = 0.0f;
+  const int o0[3] = {0, 0, 0};
+  const Seg sg = seg_of(valid ? (int)node_of<D>(sc, o0, S) : -1 - (int)(threadIdx.x & 31));
   for (int q = 0; q < kNO<D>; ++q) {
     int o[3];
     offset_of<D>(q, o);
@@ -561,12 +608,23 @@ __device__ __forceinline__ void g2p_bwd_body(uint64_t p, const float* __restrict
       for (int a = 0; a < D; ++a) s2 += lC[a][b] * comp(nd, a);
       lfx[b] += -4.0f * S.inv_dx * W * s2 + lW * dW[b];
     }
-    atomicAdd(&lgrid[ni].y, add[0]);
-    atomicAdd(&lgrid[ni].z, add[1]);
-    if (D == 3) atomicAdd(&lgrid[ni].w, add[2]);
-  }
+    if (!valid) add[0] = add[1] = add[2] = 0.0f;
+    if (sg.ok) {
 #pragma unroll
-  for (int a = 0; a < D; ++a) lfx_out[p * 3 + a] = lfx[a];
+      for (int c = 0; c < D; ++c) add[c] = seg_sum(add[c], sg);
+    }
+    if (valid && (!sg.ok || sg.head)) {
+      atomicAdd(&lgrid[ni].y, add[0]);
+      atomicAdd(&lgrid[ni].z, add[1]);
+      if (D == 3) atomicAdd(&lgrid[ni].w, add[2]);
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int h = 0; h < NS; ++h) lo[h] = lw[h];
+#pragma unroll
+    for (int a = 0; a < D; ++a) lfx_out[p * 3 + a] = lfx[a];
+  }
 }
 
 template <int D, bool EL>
@@ -708,7 +766,8 @@ __global__ void __launch_bounds__(256) k_forward_chain(const float* __restrict__
   const float* in = s0;
   for (uint32_t i = 0; i < k; ++i) {
     float* out = (i % 2 == 0) ? a : b;
-    for (uint64_t p = t0; p < n; p += stride) p2g_fwd_body<D, EL>(p, in, n, S, grid);
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride)
+      p2g_fwd_body<D, EL>(base + threadIdx.x, in, n, S, grid);
     G.sync();
     for (uint64_t c = t0; c < nn; c += stride) grid_fwd_body<D>(c, grid, nn, S, gv, true, nullptr);
     G.sync();
@@ -727,11 +786,13 @@ __global__ void __launch_bounds__(256) k_adjoint_coop(const float* __restrict__ 
   cooperative_groups::grid_group G = cooperative_groups::this_grid();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (uint64_t p = t0; p < n; p += stride) p2g_fwd_body<D, EL>(p, s, n, S, grid);
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride)
+    p2g_fwd_body<D, EL>(base + threadIdx.x, s, n, S, grid);
   G.sync();
   for (uint64_t c = t0; c < nn; c += stride) grid_fwd_body<D>(c, grid, nn, S, gv, false, lgrid);
   G.sync();
-  for (uint64_t p = t0; p < n; p += stride) g2p_bwd_body<D, EL>(p, s, lam1, n, gv, S, lgrid, lam, lfx);
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride)
+    g2p_bwd_body<D, EL>(base + threadIdx.x, s, lam1, n, gv, S, lgrid, lam, lfx);
   G.sync();
   for (uint64_t c = t0; c < nn; c += stride) grid_bwd_body<D>(c, grid, nn, S, lgrid);
   G.sync();
