@@ -23,3 +23,25 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert "workload" in d["config"]
+
+
+def _ref_line(script, *args):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, script), "--impl", "reference", *args],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["e2e"]["value"] == d["value"] and "workload" in d["config"]
+    return d
+
+
+def test_smoke_bench_reference_arm():
+    d = _ref_line("bench_smoke.py", "--steps", "1", "--cpu-res", "16", "12", "10", "--iters", "4")
+    assert d["unit"] == "voxel-steps/s"
+
+
+def test_adjoint_bench_reference_arm():
+    d = _ref_line("bench_adjoint.py", "--config", "2d-fluid", "--cpu-steps", "1")
+    assert d["unit"] == "particle-steps/s"
