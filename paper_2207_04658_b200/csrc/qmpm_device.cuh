@@ -280,7 +280,11 @@ __device__ __forceinline__ void polar3(const float F[9], float R[9]) {
       delta = fmaxf(delta, fabsf(nr - R[i]));
       R[i] = nr;
     }
-    if (delta < 1e-7f) break;
+    // Newton's iteration converges quadratically: with delta = |R_{k+1} - R_k| ~ the
+    // error of R_k, the iterate just formed is within ~delta^2 / (2 sigma_min) of the
+    // polar factor, so delta < 1e-4 leaves it at fp32 rounding (~1e-8 for sigma_min >=
+    // 0.5) without the extra confirming iteration a 1e-7 test costs (~90 instructions)
+    if (delta < 1e-4f) break;
   }
 }
 
