@@ -273,12 +273,22 @@ __device__ __forceinline__ void polar3(const float F[9], float R[9]) {
     }
     const float a = 0.5f * g, b = 0.5f * __frcp_rn(g * det);
 #endif
+    // R <- a R + b c in packed FP32x2 (4 pairs + 1), delta = max |change|
     float delta = 0.0f;
+    const float2 a2 = make_float2(a, a), b2 = make_float2(b, b);
 #pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      const float nr = a * R[i] + b * c[i];
-      delta = fmaxf(delta, fabsf(nr - R[i]));
-      R[i] = nr;
+    for (int i = 0; i < 8; i += 2) {
+      const float2 r2 = make_float2(R[i], R[i + 1]);
+      const float2 nr = __ffma2_rn(b2, make_float2(c[i], c[i + 1]), __fmul2_rn(a2, r2));
+      const float2 d2 = __fadd2_rn(nr, make_float2(-r2.x, -r2.y));
+      delta = fmaxf(delta, fmaxf(fabsf(d2.x), fabsf(d2.y)));
+      R[i] = nr.x;
+      R[i + 1] = nr.y;
+    }
+    {
+      const float nr = __fmaf_rn(b, c[8], a * R[8]);
+      delta = fmaxf(delta, fabsf(nr - R[8]));
+      R[8] = nr;
     }
     // Newton's iteration converges quadratically: with delta = |R_{k+1} - R_k| ~ the
     // error of R_k, the iterate just formed is within ~delta^2 / (2 sigma_min) of the
