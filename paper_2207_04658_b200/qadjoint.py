@@ -57,7 +57,17 @@ class Adjoint:
             lib().qadj_destroy(self.ctx)
             self.ctx = ctypes.c_void_p()
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
     def forward(self, s_in, s_out):
         _check(lib().qadj_forward(self.ctx, ptr(s_in), ptr(s_out)))

@@ -86,7 +86,17 @@ class Smoke:
             lib().qsmoke_destroy(self.ctx)
             self.ctx = ctypes.c_void_p()
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
     # sub-steps (device tensors)
     def advect_velocity(self, u_vel, u_out, dt, u_refl=None, rho=None, bdt=0.0, dstep=0, dbg=None):
