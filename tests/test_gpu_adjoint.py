@@ -144,3 +144,19 @@ def test_cooperative_and_separate_launch_paths_agree(material, monkeypatch):
     assert abs(z0 - z1) <= 1e-5 * z0
     assert np.allclose(g0, g1, rtol=1e-3, atol=0)
     assert st0 == st1
+
+
+@pytest.mark.slow
+def test_algorithm1_end_to_end_error_bounded():
+    """Algorithm 1 on the GPU pieces (C1, T = 2048): ranges from the fp32 run, tallies
+    from the adjoint, the error-bounded bits for eps = 0.05, and the quantized run meets
+    |z_q - z| <= eps z with a >2x smaller state; the adjoint engine's own forward
+    reproduces the block-sparse run's z."""
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from alg1_error_bounded import run
+    d = run(2048, [0.05], 2)
+    assert abs(d["z_adjoint_engine"] - d["z_fp32"]) <= 1e-3 * d["z_fp32"]
+    for r in d["runs"]:
+        assert r["success"] and r["saturations"] == 0, r
+        assert r["compression"] > 2.5
