@@ -66,6 +66,20 @@ def run(T, eps_list, seeds, mem_ratios=()):
                              success=abs(zq - z) <= eps * z, sigma_pred=sigma, bits=[int(b) for b in bits],
                              record_bits=nbits, compression=32.0 * len(bits) / nbits,
                              saturations=int(sum(stq.saturations))))
+    # the same schemes rounded to nearest instead of dithered (the paper's dithering
+    # comparison: without dithering the errors correlate and bias z)
+    rne_rows = []
+    for eps in eps_list:
+        delta, bits = qmpm.solve_error_bounded(P, np.maximum(g, 1e-300), R, z, eps, b_min=1, b_max=31)
+        sch = schemes.with_rounding(schemes.from_solution(d, "elastic", R, bits), "rne")
+        q = qmpm.Sim(sc.sim, sch, n)
+        q.set_state(torch.from_numpy(st).cuda())
+        q.step(T)
+        sq = np.zeros(st.shape, np.float32)
+        q.read_state(vals=sq)
+        q.close()
+        zq = ke(sq)
+        rne_rows.append(dict(eps=eps, z_quant=zq, rel_err=abs(zq - z) / z, success=abs(zq - z) <= eps * z))
     # memory-bounded (Eq. 7): stored bits <= ratio x fp32 (32 bits per scalar)
     mem_rows = []
     for ratio in mem_ratios:
@@ -89,7 +103,7 @@ def run(T, eps_list, seeds, mem_ratios=()):
                                  compression=32.0 * len(bits) / nbits, saturations=int(sum(stq.saturations))))
     return dict(scene="C1 (2D elastic, 8192 particles, 128^2, dt 2e-4)", steps=T, z_fp32=z, z_adjoint_engine=z_adj,
                 g=[float(x) for x in g], ranges=[float(r) for r in R], checkpointing=stats, runs=rows,
-                memory_bounded=mem_rows)
+                rne=rne_rows, memory_bounded=mem_rows)
 
 
 def main():
