@@ -129,6 +129,14 @@ def smoke_u_shared(frac_bits=13, exp_bits=4, r_min=2.0 ** -3):
     return dict(dim=3, material="fluid", rounding="dither", seed=DITHER_SEED ^ 0x7, fields=f)
 
 
+def smoke_p_shared(frac_bits=11, exp_bits=4, r_min=2.0 ** -6):
+    """Pressure as SHARED_EXP (reading Q4): the two cells of a record share an exponent:
+    4 + 2 x 12 = 28 bits, W = 1."""
+    f = [dict(kind="shared_exp", frac_bits=frac_bits, exp_bits=exp_bits, range=r_min, offset=0.0, group=1)
+         for _ in range(2)]
+    return dict(dim=3, material="fluid", rounding="dither", seed=DITHER_SEED ^ 0x8, fields=f)
+
+
 def smoke_raw(n):
     """fp32 baseline records (n = 6 velocity or 2 pressure fields)."""
     return dict(dim=3, material="fluid", rounding="dither", seed=DITHER_SEED,

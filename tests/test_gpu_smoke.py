@@ -190,9 +190,13 @@ def chained_step(sm, params, su, sp, uw, pw, rho, step, iters):
     ((10, 6, 8), 2, schemes.smoke_u_shared(), 1),       # SHARED_EXP velocity (reading Q4)
     ((12, 8, 6), 2, schemes.smoke_u(rounding="rne"), 1),
     ((8, 6, 6), 0, schemes.smoke_raw(6), 1),             # no sweeps, fp32 records
+    ((12, 10, 8), 3, "p_shared", 1),                     # SHARED_EXP pressure (reading Q4)
 ])
 def test_graph_step_equals_checked_chain(res, iters, su, steps):
-    params, su, sp, uw, uq, pw, pq, rho = make(res, seed=5, su=su, iters=iters)
+    sp = None
+    if su == "p_shared":
+        su, sp = None, schemes.smoke_p_shared()
+    params, su, sp, uw, uq, pw, pq, rho = make(res, seed=5, su=su, sp=sp, iters=iters)
     sm = qsmoke.Smoke(params, su, sp)
     sm.set_state(dev(uw), dev(pw), dev(rho), step=3)
     sm.step(steps)
