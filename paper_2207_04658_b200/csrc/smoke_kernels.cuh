@@ -27,6 +27,10 @@
 #ifndef QSMOKE_JACOBI_MINB  // min resident CTAs per SM for the Jacobi sweep (tuning)
 #define QSMOKE_JACOBI_MINB 6  // measured: 6 -> 0.542 ms, 1 -> 0.580, 7-8 -> 0.63 (612^3)
 #endif
+#ifndef QSMOKE_ADV_UNROLL  // 2: the two cells of a record interleaved; 1: one after the other
+#define QSMOKE_ADV_UNROLL 2
+#endif
+constexpr int kAdvUnroll = QSMOKE_ADV_UNROLL;
 #ifndef QSMOKE_ADV_MINB  // min resident CTAs per SM for the advection kernels (tuning)
 #define QSMOKE_ADV_MINB 2
 #endif
@@ -880,7 +884,7 @@ __device__ __forceinline__ void advect_u_body(const uint32_t* __restrict__ uv, c
     auto samp_u = [&](const float* p, float* o) { w.sample(g, ru, uv, nullptr, p, o); };
     float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (valid) {
-#pragma unroll
+#pragma unroll(kAdvUnroll)
       for (int c2 = 0; c2 < 2; ++c2) {
         const int x = 2 * xr + c2;
         const float xp[3] = {(float)x, (float)y, (float)z};
@@ -1042,7 +1046,7 @@ extern "C" __global__ void __launch_bounds__(256, QSMOKE_ADV_MINB)
     if (!valid) return;
     auto samp_u = [&](const float* p, float* o) { w.sample(g, ru, U, nullptr, p, o); };
     const unsigned long long plane = (unsigned long long)g.ny * g.nz;
-#pragma unroll
+#pragma unroll(kAdvUnroll)
     for (int c2 = 0; c2 < 2; ++c2) {
       const int x = 2 * xr + c2;
       const unsigned long long c = (unsigned long long)x * plane + (unsigned long long)y * g.nz + z;
