@@ -240,6 +240,13 @@ qmpm_status qmpm_create_slab(const qmpm_params* params, const qmpm_scheme* schem
  * failure (including a missing libnccl.so.2). */
 qmpm_status qmpm_get_unique_id(uint8_t id[128]);
 qmpm_status qmpm_connect_nccl(qmpm_ctx* ctx, const uint8_t id[128]);
+/* The one-call form: qmpm_create_slab for rank `rank` of `nranks` with
+ * the cell planes [slab_cuts[rank], slab_cuts[rank + 1]) (host array of nranks + 1
+ * increasing block-plane cuts from 0 to grid_res[2]), then qmpm_connect_nccl with the
+ * broadcast id.  QMPM_EINVAL for bad cuts / rank, QMPM_ENCCL if the connect fails (the
+ * ctx is destroyed). */
+qmpm_status qmpm_create_dist(const qmpm_params* params, const qmpm_scheme* scheme, void* cuda_stream, int nranks,
+                             int rank, const uint8_t id[128], const int32_t* slab_cuts, qmpm_ctx** out);
 /* In-process transport: advance all slabs of one decomposition that live in this
  * process (ctxs[r] = rank r of n, one shared stream), exchanging with device copies.
  * Synchronizes once per step. */

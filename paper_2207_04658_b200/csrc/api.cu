@@ -938,6 +938,31 @@ qmpm_status qmpm_connect_nccl(qmpm_ctx* ctx, const uint8_t id[128]) {
   return QMPM_OK;
 }
 
+qmpm_status qmpm_create_dist(const qmpm_params* params, const qmpm_scheme* scheme, void* cuda_stream, int nranks,
+                             int rank, const uint8_t id[128], const int32_t* slab_cuts, qmpm_ctx** out) {
+  if (!slab_cuts || !id || !out) return fail(nullptr, QMPM_EINVAL, "NULL argument to qmpm_create_dist");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(nullptr, QMPM_EINVAL, "bad rank %d of %d", rank, nranks);
+  for (int r = 0; r < nranks; ++r)
+    if (slab_cuts[r] >= slab_cuts[r + 1]) return fail(nullptr, QMPM_EINVAL, "slab_cuts must increase");
+  if (!params || slab_cuts[0] != 0 || slab_cuts[nranks] != params->grid_res[2])
+    return fail(nullptr, QMPM_EINVAL, "slab_cuts must span [0, grid_res[2]]");
+  qmpm_slab slab{};
+  slab.nranks = nranks;
+  slab.rank = rank;
+  slab.z0 = slab_cuts[rank];
+  slab.z1 = slab_cuts[rank + 1];
+  qmpm_ctx* ctx = nullptr;
+  qmpm_status rc = qmpm_create_slab(params, scheme, cuda_stream, &slab, &ctx);
+  if (rc) return rc;
+  rc = qmpm_connect_nccl(ctx, id);
+  if (rc) {
+    qmpm_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return QMPM_OK;
+}
+
 qmpm_status qmpm_create_slab(const qmpm_params* params, const qmpm_scheme* scheme, void* cuda_stream,
                              const qmpm_slab* slab, qmpm_ctx** out) {
   qmpm_ctx* ctx = nullptr;

@@ -71,7 +71,7 @@ EXPORTS = ["qmpm_abi_version", "qmpm_last_error", "qmpm_layout", "qmpm_create", 
            "qmpm_kernel_times", "qmpm_kernel_name", "qmpm_launch_count", "qmpm_create_slab",
            "qmpm_get_unique_id", "qmpm_connect_nccl", "qmpm_step_group", "qmpm_set_ids",
            "qmpm_read_ranges", "qmpm_predict_error", "qmpm_solve_error_bounded", "qmpm_solve_memory_bounded",
-           "qmpm_codec_matmul3"]
+           "qmpm_codec_matmul3", "qmpm_create_dist"]
 
 
 def lib():
@@ -105,6 +105,8 @@ def lib():
         "qmpm_launch_count": (u64, [P]),
         "qmpm_create_slab": (i32, [ctypes.POINTER(Params), ctypes.POINTER(Scheme), P, ctypes.POINTER(Slab),
                                    ctypes.POINTER(P)]),
+        "qmpm_create_dist": (i32, [ctypes.POINTER(Params), ctypes.POINTER(Scheme), P, ctypes.c_int, ctypes.c_int, P, P,
+                                   ctypes.POINTER(ctypes.c_void_p)]),
         "qmpm_get_unique_id": (i32, [P]),
         "qmpm_connect_nccl": (i32, [P, P]),
         "qmpm_step_group": (i32, [P, ctypes.c_int, u32]),

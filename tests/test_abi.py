@@ -155,3 +155,20 @@ def test_nostraddle_layout_matches_oracle_and_never_straddles(seed):
     for o, w in zip(offs, widths):
         assert o % 32 + w <= 32
     assert all(a < b for a, b in zip(offs, offs[1:]))
+
+
+def test_create_dist_validates_cuts_without_gpu():
+    import ctypes
+    from paper_2207_04658_b200 import scenes
+    sc = scenes.c4(n_target=1000, res=64)
+    p = qmpm.make_params(sc.sim, 1000)
+    cs = qmpm.CScheme(schemes.f2())
+    ctx = ctypes.c_void_p()
+    uid = (ctypes.c_uint8 * 128)()
+    L = qmpm.lib()
+    bad = (ctypes.c_int32 * 3)(0, 40, 32)      # not increasing
+    assert L.qmpm_create_dist(ctypes.byref(p), cs.ref, None, 2, 0, uid, bad, ctypes.byref(ctx)) == 1
+    short = (ctypes.c_int32 * 3)(0, 32, 60)    # does not reach grid_res[2] = 64
+    assert L.qmpm_create_dist(ctypes.byref(p), cs.ref, None, 2, 0, uid, short, ctypes.byref(ctx)) == 1
+    ok = (ctypes.c_int32 * 3)(0, 32, 64)
+    assert L.qmpm_create_dist(ctypes.byref(p), cs.ref, None, 2, 2, uid, ok, ctypes.byref(ctx)) == 1  # rank
