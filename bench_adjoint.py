@@ -138,7 +138,24 @@ def run_gpu(args):
 
     f_ms = timed(lambda: A.forward(s0d, so))
     a_ms = timed(lambda: A.adjoint_step(s0d, lam, lam2))
+    nn = 1
+    for a in range(cfg["dim"]):
+        nn *= cfg["res"]
     A.close()
+    # roofline of the adjoint step (5 kernels): algorithmic bytes = the state rows it must
+    # read / write (s twice, lambda_{t+1}, lambda_t written and re-read, the fx partials)
+    # plus each dense-grid pass (16 B per node: P2G write, grid read + gv write + lgrid
+    # clear, node-adjoint scatter, grid-adjoint read 2 + write 1 + clear 1, P2G-adjoint
+    # gather)
+    row = 4 * ns
+    alg = n * (2 * row + row + 2 * row + 2 * 12) + nn * 16 * 10
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm_peak = float(json.load(open(peaks_path))["hbm_gbs"]) if os.path.exists(peaks_path) else 6650.0
+    achieved = alg / (a_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "adjoint step (5 kernels)", "achieved": achieved, "peak": hbm_peak,
+                "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                "algorithmic_bytes_per_launch": alg, "avg_launch_ms": a_ms,
+                "note": "small scenes are bound by P2G / node-adjoint atomics, not bytes (DESIGN.md §13)"}
     value = n * T / (ms / 1e3)
     cpu = None
     if not args.no_cpu:
@@ -155,6 +172,7 @@ def run_gpu(args):
         "timed_tallies_ms": times,
         "checkpointing": {"max_resident_states": st["max_resident"], "forward_steps": st["forward_steps"],
                           "adjoint_steps": st["adjoint_steps"], "log2_T": math.log2(max(T, 1))},
+        "roofline": roofline,
         "kernels": {"forward_step_ms": f_ms, "adjoint_step_ms": a_ms,
                     "model_ms": st["forward_steps"] * f_ms + st["adjoint_steps"] * a_ms},
         "z": z, "g": g.tolist(),
