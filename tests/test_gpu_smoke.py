@@ -191,6 +191,7 @@ def chained_step(sm, params, su, sp, uw, pw, rho, step, iters):
     ((12, 8, 6), 2, schemes.smoke_u(rounding="rne"), 1),
     ((8, 6, 6), 0, schemes.smoke_raw(6), 1),             # no sweeps, fp32 records
     ((12, 10, 8), 3, "p_shared", 1),                     # SHARED_EXP pressure (reading Q4)
+    ((4, 4, 4), 98, None, 1),                            # the largest sweep count (dither subs up to 199)
 ])
 def test_graph_step_equals_checked_chain(res, iters, su, steps):
     sp = None
