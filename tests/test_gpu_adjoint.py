@@ -163,3 +163,18 @@ def test_algorithm1_end_to_end_error_bounded():
     assert np.mean(errs) <= 0.05 and max(errs) <= 0.1, errs
     for r in d["runs"]:
         assert r["saturations"] == 0 and r["compression"] > 2.5, r
+
+
+@pytest.mark.parametrize("material", ["fluid", "elastic"])
+def test_gradient_tally_matches_oracle_medium(material):
+    """A 3D block of 13,824 particles (many warps, aggregated scatters, several CTAs per
+    node neighbourhood) over T = 3 against the oracle's store-all tallies."""
+    sim, s0 = make(material, dim=3, side=24, res=64, ppc=2, origin=0.3, seed=77)
+    A = qadjoint.Adjoint(sim, s0.shape[0])
+    lam0 = np.zeros_like(s0)
+    g, z, _ = A.gradient_tally(s0, 3, lam0=lam0)
+    A.close()
+    oz, og, ol = adj.backward_all(sim, s0, 3)
+    assert abs(z - oz) <= 1e-5 * oz
+    assert np.all(np.abs(g - og) <= 1e-3 * np.maximum(og, og.max() * 1e-6)), (g, og)
+    assert col_err(lam0, ol) <= 10 * ADJ_TOL
