@@ -1,6 +1,7 @@
 """CPU checks of the C-ABI library: it loads, exports every symbol include/qmpm.h
 declares, and its host-side layout function follows the bit-pack layout."""
 import re
+import sys
 import subprocess
 import os
 
@@ -172,3 +173,21 @@ def test_create_dist_validates_cuts_without_gpu():
     assert L.qmpm_create_dist(ctypes.byref(p), cs.ref, None, 2, 0, uid, short, ctypes.byref(ctx)) == 1
     ok = (ctypes.c_int32 * 3)(0, 32, 64)
     assert L.qmpm_create_dist(ctypes.byref(p), cs.ref, None, 2, 2, uid, ok, ctypes.byref(ctx)) == 1  # rank
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: with the library absent, every binding raises instead of
+    computing (run in a subprocess with LIB_PATH pointed at a missing file)."""
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "from paper_2207_04658_b200 import qmpm, qsmoke, qadjoint\n"
+        "qmpm.LIB_PATH = %r\n"
+        "qmpm._lib = None\n"
+        "for f in (qmpm.lib, qsmoke.lib, qadjoint.lib):\n"
+        "    try:\n"
+        "        f(); print('LOADED'); sys.exit(1)\n"
+        "    except ImportError:\n"
+        "        pass\n"
+        "print('OK')\n" % (ROOT, str(tmp_path / "missing.so")))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
