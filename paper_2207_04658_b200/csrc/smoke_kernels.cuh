@@ -27,6 +27,12 @@
 #ifndef QSMOKE_JACOBI_MINB  // min resident CTAs per SM for the Jacobi sweep (tuning)
 #define QSMOKE_JACOBI_MINB 6  // measured: 6 -> 0.542 ms, 1 -> 0.580, 7-8 -> 0.63 (612^3)
 #endif
+#ifndef QSMOKE_PROJECT_MINB  // min resident CTAs per SM for the projection (tuning)
+#define QSMOKE_PROJECT_MINB 4  // measured at 612^3: 4 -> 0.92 ms, 1 -> 1.01, 5 -> 1.10
+#endif
+#ifndef QSMOKE_DIV_MINB  // min resident CTAs per SM for the divergence (tuning)
+#define QSMOKE_DIV_MINB 8  // measured: 8 -> 0.63 ms, 1 or 6 -> 0.77
+#endif
 #ifndef QSMOKE_ADV_UNROLL  // 2: the two cells of a record interleaved; 1: one after the other
 #define QSMOKE_ADV_UNROLL 2
 #endif
@@ -927,7 +933,7 @@ extern "C" __global__ void __launch_bounds__(256, QSMOKE_ADV_MINB)
 }
 
 // S5 on the x march: neighbours outside the domain are 0 (halo / x loads masked)
-extern "C" __global__ void __launch_bounds__(256)
+extern "C" __global__ void __launch_bounds__(256, QSMOKE_DIV_MINB)
     qsmoke_div(const uint32_t* __restrict__ U, SmokeDev g, float* __restrict__ div) {
   __shared__ float4 tile[smoke::kTY + 2][smoke::kTZ + 2];  // (uy0, uy1, uz0, uz1)
   const smoke::March m = smoke::march_setup(g);
@@ -999,7 +1005,7 @@ extern "C" __global__ void __launch_bounds__(256, QSMOKE_JACOBI_MINB)
   });
 }
 
-extern "C" __global__ void __launch_bounds__(256)
+extern "C" __global__ void __launch_bounds__(256, QSMOKE_PROJECT_MINB)
     qsmoke_project(const uint32_t* __restrict__ U, const uint32_t* __restrict__ P, SmokeDev g, SaltSrc ss,
                    uint32_t* __restrict__ out, float* __restrict__ dbg) {
   constexpr int W = SpecU::W;
