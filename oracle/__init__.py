@@ -77,7 +77,9 @@ def lib():
         u32, u64, i32 = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
         sig = {
             "oracle_mix32": (u32, [u32]),
-            "oracle_r24": (u32, [u64, u64, u32, u32]),
+            "oracle_pair_hash": (u32, [u64, u64, u32, u32]),
+            "oracle_r16": (u32, [u64, u64, u32, u32]),
+            "oracle_r16_batch": (None, [u64, u64, u64, P, u32, P]),
             "oracle_layout": (i32, [P, P, P, P]),
             "oracle_get_bits": (u32, [P, u32, u32]),
             "oracle_put_bits": (None, [P, u32, u32, u32]),
@@ -171,8 +173,16 @@ def mix32(x):
     return lib().oracle_mix32(x)
 
 
-def r24(seed, step, key, field):
-    return lib().oracle_r24(seed, step, key, field)
+def r16(seed, step, key, field):
+    """The 16-bit dither draw of reading Q5 (revision 3)."""
+    return lib().oracle_r16(seed, step, key, field)
+
+
+def r16_batch(seed, step, keys, field):
+    keys = np.ascontiguousarray(keys, dtype=np.uint32)
+    out = np.empty(keys.shape[0], dtype=np.uint32)
+    lib().oracle_r16_batch(seed, step, keys.shape[0], _p(keys), field, _p(out))
+    return out
 
 
 def layout(scheme):

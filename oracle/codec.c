@@ -11,8 +11,9 @@
  *     t = v/Delta is computed as ONE fp32 multiply by a host-rounded 1/Delta,
  *     no FMA (reading Q3).  Undithered ties round half to even (reading Q6).
  *   - Eq. 11: u = floor(v/Delta + xi) rounded, xi ~ U(-1/2,1/2); evaluated
- *     exactly as u = f + [y >= 1 - r], f = floor(t), y = t - f, r = r24 * 2^-24,
- *     which is floor(t + r) in real arithmetic (reading Q6), so P(up) = y.
+ *     exactly as u = f + [y >= 1 - r], f = floor(t), y = t - f, r = r16 * 2^-16,
+ *     which is floor(t + r) in real arithmetic (reading Q6), so P(up) = y to within
+ *     2^-16.
  *   - Bit pack (Fig. bit_pack_operation): fields placed
  *     contiguously in declaration order, LSB-first, records word-aligned
  *     (reading Q10); a field may straddle two words.
@@ -33,21 +34,38 @@ uint32_t oracle_mix32(uint32_t x) {
     return x;
 }
 
-/* 24-bit uniform integer for (seed, step, particle key, field index).
- * salt = mix(seed_lo ^ mix(seed_hi ^ mix(step)));  h = mix(key ^ salt);
- * per field (reading Q5, revision 2): x = (h ^ field * 0x9E3779B9) * 0x7feb352d;
- * x ^= x >> 15;  r24 = (x * 0x846ca68b) >> 8 -- the second half of lowbias32 applied
- * to the field-salted particle hash (every step a bijection of h, so r24 is uniform
- * whenever h is).  (step taken mod 2^32) */
-uint32_t oracle_r24(uint64_t seed, uint64_t step, uint32_t key, uint32_t field) {
+/* 16-bit uniform integer for (seed, step, particle key, field index): reading Q5,
+ * revision 3 (one 32-bit hash per PAIR of fields, f = 2p and f = 2p + 1):
+ *   salt = mix(seed_lo ^ mix(seed_hi ^ mix(step)))   (step taken mod 2^32)
+ *   h    = mix(key ^ salt)
+ *   z    = x ^ (x >> 16),  x = ((h ^ p * 0x9E3779B9) * 0x7feb352d ^ ...) -- written out
+ *          below: the lowbias32 rounds on the pair-salted particle hash
+ *   even field: r16 = bits 7..22 of z;  odd field: r16 = bits 7..22 of z rotated right
+ *   by 16 (= bits 23..31 and 0..6 of z).
+ * Each step is a bijection of h and the two fields of a pair take disjoint bits of z, so
+ * for a uniform h every r16 is exactly uniform and the pair is exactly jointly uniform. */
+uint32_t oracle_pair_hash(uint64_t seed, uint64_t step, uint32_t key, uint32_t pair) {
     uint32_t seed_lo = (uint32_t)(seed & 0xffffffffu);
     uint32_t seed_hi = (uint32_t)(seed >> 32);
     uint32_t salt = oracle_mix32(seed_lo ^ oracle_mix32(seed_hi ^ oracle_mix32((uint32_t)step)));
     uint32_t h = oracle_mix32(key ^ salt);
-    uint32_t x = (h ^ (field * 0x9E3779B9u)) * 0x7feb352du;
+    uint32_t x = h ^ (pair * 0x9E3779B9u);
+    x *= 0x7feb352du;
     x ^= x >> 15;
     x *= 0x846ca68bu;
-    return x >> 8;
+    x ^= x >> 16;
+    return x;
+}
+
+uint32_t oracle_r16(uint64_t seed, uint64_t step, uint32_t key, uint32_t field) {
+    uint32_t z = oracle_pair_hash(seed, step, key, field >> 1);
+    if (field & 1u) z = (z >> 16) | (z << 16); /* rotate right by 16 */
+    return (z >> 7) & 0xffffu;
+}
+
+void oracle_r16_batch(uint64_t seed, uint64_t step, uint64_t n, const uint32_t* keys, uint32_t field,
+                      uint32_t* out) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = oracle_r16(seed, step, keys[i], field);
 }
 
 /* SHARED_EXP groups (reading Q4): a maximal run of consecutive SHARED_EXP fields with
@@ -136,7 +154,7 @@ static float inv_delta_of(uint32_t b, float range) {
  * Counters: sat when clamped; up when u > t, down when u < t (T-dither-eff,
  * P:735-738; values exactly on the grid count as neither); nonfinite => u = 0. */
 int64_t oracle_encode_value(float v, uint32_t frac_bits, float range, float offset, int dithered,
-                            uint32_t r24, uint64_t* sat, uint64_t* up, uint64_t* down,
+                            uint32_t r16, uint64_t* sat, uint64_t* up, uint64_t* down,
                             uint64_t* nonfinite) {
     if (!isfinite(v)) {
         if (nonfinite) (*nonfinite)++;
@@ -149,7 +167,7 @@ int64_t oracle_encode_value(float v, uint32_t frac_bits, float range, float offs
     if (dithered) {
         float f = floorf(t);
         float y = t - f;                                       /* exact */
-        float one_minus_r = (float)(16777216u - r24) * 0x1p-24f; /* exact */
+        float one_minus_r = (float)(65536u - r16) * 0x1p-16f; /* exact */
         int is_up = (y >= one_minus_r);
         ud = (double)f + (double)is_up;
         if (is_up) {
@@ -208,16 +226,16 @@ static void encode_group(const oracle_scheme* s, const uint32_t* offsets, uint32
     for (;;) {
         uint64_t sat = 0;
         for (uint32_t f = f0; f <= f1; ++f) {
-            uint32_t r24 = dithered ? oracle_r24(s->dither_seed, step, key, f) : 0;
-            oracle_encode_value(vals[f], b, ldexpf(R, (int)E), 0.0f, dithered, r24, &sat, 0, 0, 0);
+            uint32_t r16 = dithered ? oracle_r16(s->dither_seed, step, key, f) : 0;
+            oracle_encode_value(vals[f], b, ldexpf(R, (int)E), 0.0f, dithered, r16, &sat, 0, 0, 0);
         }
         if (sat == 0 || E == emax) break;
         ++E;
     }
     oracle_put_bits(rec, offsets[f0], e, E);
     for (uint32_t f = f0; f <= f1; ++f) {
-        uint32_t r24 = dithered ? oracle_r24(s->dither_seed, step, key, f) : 0;
-        int64_t u = oracle_encode_value(vals[f], b, ldexpf(R, (int)E), 0.0f, dithered, r24,
+        uint32_t r16 = dithered ? oracle_r16(s->dither_seed, step, key, f) : 0;
+        int64_t u = oracle_encode_value(vals[f], b, ldexpf(R, (int)E), 0.0f, dithered, r16,
                                         counters ? &counters[f] : 0, counters ? &counters[64 + f] : 0,
                                         counters ? &counters[128 + f] : 0, counters ? &counters[192] : 0);
         uint32_t width = b + 1, mask = (width == 32) ? 0xffffffffu : ((1u << width) - 1u);
@@ -243,9 +261,9 @@ static void encode_record(const oracle_scheme* s, const uint32_t* offsets, uint3
             oracle_put_bits(rec, offsets[f], 32, bits);
             continue;
         }
-        uint32_t r24 = dithered ? oracle_r24(s->dither_seed, step, key, f) : 0;
+        uint32_t r16 = dithered ? oracle_r16(s->dither_seed, step, key, f) : 0;
         int64_t u = oracle_encode_value(v, s->frac_bits[f], s->range[f], s->offset[f], dithered,
-                                        r24, counters ? &counters[f] : 0,
+                                        r16, counters ? &counters[f] : 0,
                                         counters ? &counters[64 + f] : 0,
                                         counters ? &counters[128 + f] : 0,
                                         counters ? &counters[192] : 0);

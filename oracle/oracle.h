@@ -63,12 +63,15 @@ typedef struct {
 
 /* ---- codec (Eq. 3, Eq. 11, bit pack P:542-549) ---- */
 uint32_t oracle_mix32(uint32_t x);
-uint32_t oracle_r24(uint64_t seed, uint64_t step, uint32_t key, uint32_t field);
+uint32_t oracle_pair_hash(uint64_t seed, uint64_t step, uint32_t key, uint32_t pair);
+uint32_t oracle_r16(uint64_t seed, uint64_t step, uint32_t key, uint32_t field);
+void oracle_r16_batch(uint64_t seed, uint64_t step, uint64_t n, const uint32_t* keys, uint32_t field,
+                      uint32_t* out);
 int oracle_layout(const oracle_scheme* s, uint32_t* offsets, uint32_t* words, uint32_t* bits);
 uint32_t oracle_get_bits(const uint32_t* rec, uint32_t offset, uint32_t width);
 void oracle_put_bits(uint32_t* rec, uint32_t offset, uint32_t width, uint32_t value);
 int64_t oracle_encode_value(float v, uint32_t frac_bits, float range, float offset, int dithered,
-                            uint32_t r24, uint64_t* sat, uint64_t* up, uint64_t* down,
+                            uint32_t r16, uint64_t* sat, uint64_t* up, uint64_t* down,
                             uint64_t* nonfinite);
 float oracle_decode_value(int32_t u, uint32_t frac_bits, float range, float offset);
 /* vals[n][n_fields] in packing order; keys nullable => RNE regardless of s->rounding */

@@ -595,7 +595,8 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
     // P2G measured: fluid C4 7.21 ms at 5 vs 7.32 at 6, elastic C3 12.6 ms at 6 vs 13.0 at 5)
     const int kP2GMinBlocks = env_int("QMPM_P2G_MINB", ctx->material == QMPM_FLUID_J ? 5 : 6),
               kG2PMinBlocks = env_int("QMPM_G2P_MINB", (d == 3 && ctx->material == QMPM_ELASTIC_FCR) ? 3 : 4);
-    ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps, kP2GMinBlocks, kG2PMinBlocks);
+    const int xk = env_int("QMPM_FLOAT_KEY", 0) ? 0 : integer_key_shift(d, ctx->L, S.inv_dx);
+    ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps, kP2GMinBlocks, kG2PMinBlocks, xk);
     JitModule m;
     std::string jerr;
     e = jit_get(ctx->jit_src, m, jerr);

@@ -111,8 +111,8 @@ __device__ __forceinline__ void encode_record(const float* v, uint32_t h, bool v
         if (SP::glead(f) == f) senc_group<SP>(f, v, h, w, fl);
         continue;
       }
-      const uint32_t r24 = (SP::DITHER && SP::kind(f) == kKindFixed) ? r24_of(h, SP::idx(f)) : 0u;
-      sput<SP>(w, f, senc<SP>(f, v[f], r24, fl[f]));
+      const float omr = (SP::DITHER && SP::kind(f) == kKindFixed) ? dither_omr(h, SP::idx(f)) : 1.0f;
+      sput<SP>(w, f, senc<SP>(f, v[f], omr, fl[f]));
     }
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
@@ -140,9 +140,9 @@ __device__ __forceinline__ void encode_record(const float* v, uint32_t h, bool v
       }
       continue;
     }
-    const uint32_t r24 = (SP::DITHER && SP::kind(f) == kKindFixed) ? r24_of(h, SP::idx(f)) : 0u;
+    const float omr = (SP::DITHER && SP::kind(f) == kKindFixed) ? dither_omr(h, SP::idx(f)) : 1.0f;
     bool up, nz;
-    sput<SP>(w, f, senc_fast<SP>(f, v[f], r24, up, nz, flag));
+    sput<SP>(w, f, senc_fast<SP>(f, v[f], omr, up, nz, flag));
   }
   if (__any_sync(kCFull, valid && flag)) {  // rare: the exact saturating rule
 #pragma unroll
@@ -154,8 +154,8 @@ __device__ __forceinline__ void encode_record(const float* v, uint32_t h, bool v
         if (SP::glead(f) == f) senc_group<SP>(f, v, h, w, fl);
         continue;
       }
-      const uint32_t r24 = (SP::DITHER && SP::kind(f) == kKindFixed) ? r24_of(h, SP::idx(f)) : 0u;
-      sput<SP>(w, f, senc<SP>(f, v[f], r24, fl[f]));
+      const float omr = (SP::DITHER && SP::kind(f) == kKindFixed) ? dither_omr(h, SP::idx(f)) : 1.0f;
+      sput<SP>(w, f, senc<SP>(f, v[f], omr, fl[f]));
     }
   }
 }

@@ -45,7 +45,7 @@ struct EncFlags {
 // Eq. 3 / Eq. 11 encode of a fixed-point value of width wi with 1/Delta = inv and the
 // given offset; returns the field's bits (width-masked).
 template <bool DITHER>
-__device__ __forceinline__ uint32_t senc_core(const int wi, const float offset, const float inv, float v, uint32_t r24,
+__device__ __forceinline__ uint32_t senc_core(const int wi, const float offset, const float inv, float v, float omr,
                                               EncFlags& fl) {
   fl.up = fl.down = fl.sat = fl.nonfinite = false;
   if (!isfinite(v)) {
@@ -64,8 +64,7 @@ __device__ __forceinline__ uint32_t senc_core(const int wi, const float offset, 
     if (DITHER) {
       const float f = floorf(t);
       const float y = __fsub_rn(t, f);  // exact
-      const float one_minus_r = __fmul_rn(__uint2float_rn(0x1000000u - r24), 0x1p-24f);  // exact
-      fl.up = y >= one_minus_r;         // u = floor(t + r) (Eq. 11, reading Q6)
+      fl.up = y >= omr;                 // u = floor(t + r), omr = 1 - r (Eq. 11, reading Q6)
       fl.down = !fl.up && y > 0.0f;
       u = __float2int_rz(fminf(fmaxf(f, lo_f), hi_f)) + (fl.up ? 1 : 0);
     } else {
@@ -82,8 +81,7 @@ __device__ __forceinline__ uint32_t senc_core(const int wi, const float offset, 
     if (DITHER) {
       const float f = floorf(t);
       const float y = __fsub_rn(t, f);
-      const float one_minus_r = __fmul_rn(__uint2float_rn(0x1000000u - r24), 0x1p-24f);
-      fl.up = y >= one_minus_r;
+      fl.up = y >= omr;
       fl.down = !fl.up && y > 0.0f;
       u = __float2ll_rz(fminf(fmaxf(f, -1099511627776.0f), 1099511627776.0f)) + (fl.up ? 1 : 0);
     } else {
@@ -101,13 +99,13 @@ __device__ __forceinline__ uint32_t senc_core(const int wi, const float offset, 
 
 // Eq. 3 / Eq. 11 encode of FIXED or RAW entry i (SHARED_EXP entries: senc_group)
 template <class SP>
-__device__ __forceinline__ uint32_t senc(const int i, float v, uint32_t r24, EncFlags& fl) {
+__device__ __forceinline__ uint32_t senc(const int i, float v, float omr, EncFlags& fl) {
   if (SP::kind(i) == kKindRaw) {
     fl.up = fl.down = fl.sat = false;
     fl.nonfinite = !isfinite(v);
     return __float_as_uint(v);
   }
-  return senc_core<SP::DITHER>(SP::width(i), SP::offset(i), SP::inv_delta(i), v, r24, fl);
+  return senc_core<SP::DITHER>(SP::width(i), SP::offset(i), SP::inv_delta(i), v, omr, fl);
 }
 
 template <class SP>
@@ -145,8 +143,8 @@ __device__ __forceinline__ void senc_group(const int lead, const float* v, uint3
     for (int j = 0; j < N; ++j) {
       if (SP::kind(j) == kKindShared && SP::glead(j) == lead) {
         const float inv = __int_as_float(__float_as_int(SP::inv_delta(j)) - (int)(E << 23));
-        const uint32_t r24 = SP::DITHER ? r24_of(h, SP::idx(j)) : 0u;
-        code[j] = senc_core<SP::DITHER>(SP::width(j), 0.0f, inv, v[j], r24, fl[j]);
+        const float omr = SP::DITHER ? dither_omr(h, SP::idx(j)) : 1.0f;
+        code[j] = senc_core<SP::DITHER>(SP::width(j), 0.0f, inv, v[j], omr, fl[j]);
         sat |= fl[j].sat;
       }
     }
@@ -161,6 +159,11 @@ __device__ __forceinline__ void senc_group(const int lead, const float* v, uint3
 #pragma unroll
   for (int j = 0; j < N; ++j)
     if (SP::kind(j) == kKindShared && SP::glead(j) == lead) sput<SP>(w, j, code[j]);
+}
+
+// |t| below enc_lim(width) => floor/round(t) (+1) lies inside [-2^b, 2^b - 1]
+__host__ __device__ constexpr float enc_lim(int wi) {
+  return wi <= 1 ? 0.0f : (wi <= 25 ? (float)((1 << (wi - 1)) - 1) : (float)(1 << 24) * (float)(1 << (wi - 26)));
 }
 
 // content key of a record (reading Q5): k = mix(k ^ word) over the words holding x
@@ -179,7 +182,7 @@ __device__ __forceinline__ uint32_t content_key(const uint32_t* w) {
 // re-encodes the whole record with the exact senc() (rare).  up: u > t;  nz: the value
 // is not on the grid (dither: down = nz - up) or, for RNE, dn: u < t.
 template <class SP>
-__device__ __forceinline__ uint32_t senc_fast(const int i, float v, uint32_t r24, bool& up, bool& nz, bool& flag) {
+__device__ __forceinline__ uint32_t senc_fast(const int i, float v, float omr, bool& up, bool& nz, bool& flag) {
   if (SP::kind(i) == kKindRaw) {
     up = nz = false;
     flag |= !(fabsf(v) < __int_as_float(0x7f800000));
@@ -189,20 +192,13 @@ __device__ __forceinline__ uint32_t senc_fast(const int i, float v, uint32_t r24
   const float a = (SP::offset(i) != 0.0f) ? __fsub_rn(v, SP::offset(i)) : v;
   const float t = __fmul_rn(a, SP::inv_delta(i));  // one fp32 multiply, no FMA (Q3)
   const uint32_t mask = (wi == 32) ? 0xffffffffu : ((1u << wi) - 1u);
-  // |t| below lim => floor/round(t) (+1) lies inside [-2^b, 2^b - 1]
-  constexpr float lim_tab[33] = {0.f, 0.f, 1.f, 3.f, 7.f, 15.f, 31.f, 63.f, 127.f, 255.f, 511.f, 1023.f, 2047.f,
-                                 4095.f, 8191.f, 16383.f, 32767.f, 65535.f, 131071.f, 262143.f, 524287.f,
-                                 1048575.f, 2097151.f, 4194303.f, 8388607.f, 16777215.f, 0x1p24f, 0x1p25f,
-                                 0x1p26f, 0x1p27f, 0x1p28f, 0x1p29f, 0x1p30f};
-  const float lim = lim_tab[wi];
+  const float lim = enc_lim(wi);
   flag |= !(fabsf(t) < lim);
   int u;
   if (SP::DITHER) {
     const float f = floorf(t);
     const float y = __fsub_rn(t, f);  // exact
-    // 1 - r24 2^-24 = (2^24 - r24) 2^-24 is representable, so the fma is exact
-    const float one_minus_r = __fmaf_rn(-0x1p-24f, __uint2float_rn(r24), 1.0f);
-    up = y >= one_minus_r;  // u = floor(t + r) (Eq. 11, reading Q6)
+    up = y >= omr;  // u = floor(t + r) (Eq. 11, reading Q6)
     nz = y > 0.0f;
     u = __float2int_rz(f);
     if (up) ++u;
@@ -213,6 +209,91 @@ __device__ __forceinline__ uint32_t senc_fast(const int i, float v, uint32_t r24
     u = __float2int_rz(q);
   }
   return (uint32_t)u & mask;
+}
+
+// ---------------------------------------------------------------- dithered fast path
+// Eq. 11 with readings Q3, Q5 rev. 3 and Q6 in packed FP32x2 (sm_100 FMUL2 /
+// FADD2 / FFMA2: each lane is the IEEE-rounded scalar op), for FIXED entries of width
+// <= 23 (|t| < 2^22 whenever the value cannot saturate):
+//   t = fl(fl(v - offset) * 1/Delta)                (one multiply, no FMA: Q3)
+//   s = fl_down(t + M) = M + floor(t), M = 1.5 2^23  (exact for |t| < 2^22; no F2I/FRND)
+//   y = t - (s - M)                                  (exact)
+//   d = y + (s_r - 2), s_r = 1 + r16 2^-16           (s_r - 2 = -(1 - r) exactly)
+//   u = floor(t) + [y >= 1 - r] = bits(s) - bits(M) + 1 + (bits(d) >> 31)
+// sign(d) is exact under round-to-nearest (d = +0 iff y = 1 - r: rounds up, Q6).
+// `flag` as senc_fast (|t| >= 2^b - 1 or NaN: the caller re-encodes exactly); `zero` is
+// raised when some y == 0 (an on-grid value: counted as neither up nor down).
+constexpr float kFloorMagic = 12582912.0f;  // 1.5 2^23
+constexpr int kFloorMagicBits = 0x4b400000;
+
+template <class SP>
+__host__ __device__ constexpr bool fast_ok(int i) {
+  return SP::DITHER && SP::kind(i) == kKindFixed && SP::width(i) <= 23;
+}
+
+// 1: entry i opens a packed pair (i, i + 1) (i even); 2: i closes one; 0: i is encoded alone
+template <class SP>
+__host__ __device__ constexpr int pair_role(int i) {
+  return (i % 2 == 0 && i + 1 < SP::NSPEC && fast_ok<SP>(i) && fast_ok<SP>(i + 1)) ? 1
+         : (i % 2 == 1 && fast_ok<SP>(i - 1) && fast_ok<SP>(i)) ? 2
+                                                                 : 0;
+}
+
+template <class SP>
+__device__ __forceinline__ void senc_pair_fast(const int i, const int j, const float vi, const float vj,
+                                               const float si, const float sj, int& ui, int& uj, int& sbi, int& sbj,
+                                               bool& flag, bool& zero) {
+  float2 a = make_float2(vi, vj);
+  if (SP::offset(i) != 0.0f || SP::offset(j) != 0.0f)  // v - offset; adding -0 is the identity
+    a = __fadd2_rn(a, make_float2(-SP::offset(i), -SP::offset(j)));
+  const float2 t = __fmul2_rn(a, make_float2(SP::inv_delta(i), SP::inv_delta(j)));
+  const float2 s = __fadd2_rd(t, make_float2(kFloorMagic, kFloorMagic));
+  const float2 f = __fadd2_rn(s, make_float2(-kFloorMagic, -kFloorMagic));
+  const float2 y = __ffma2_rn(f, make_float2(-1.0f, -1.0f), t);
+  const float2 d = __fadd2_rn(y, __fadd2_rn(make_float2(si, sj), make_float2(-2.0f, -2.0f)));
+  sbi = __float_as_int(d.x) >> 31;
+  sbj = __float_as_int(d.y) >> 31;
+  ui = __float_as_int(s.x) - (kFloorMagicBits - 1) + sbi;
+  uj = __float_as_int(s.y) - (kFloorMagicBits - 1) + sbj;
+  flag |= !(fabsf(t.x) < enc_lim(SP::width(i))) || !(fabsf(t.y) < enc_lim(SP::width(j)));
+  zero |= (y.x == 0.0f) || (y.y == 0.0f);
+}
+
+template <class SP>
+__device__ __forceinline__ int senc1_fast(const int i, const float v, const float si, int& sb, bool& flag,
+                                          bool& zero) {
+  const float a = (SP::offset(i) != 0.0f) ? __fsub_rn(v, SP::offset(i)) : v;
+  const float t = __fmul_rn(a, SP::inv_delta(i));
+  const float s = __fadd_rd(t, kFloorMagic);
+  const float y = __fsub_rn(t, __fsub_rn(s, kFloorMagic));
+  const float d = __fadd_rn(y, __fsub_rn(si, 2.0f));
+  sb = __float_as_int(d) >> 31;
+  flag |= !(fabsf(t) < enc_lim(SP::width(i)));
+  zero |= y == 0.0f;
+  return __float_as_int(s) - (kFloorMagicBits - 1) + sb;
+}
+
+// y == 0 of the fast path (the rare recount of on-grid values)
+template <class SP>
+__device__ __forceinline__ bool on_grid_fast(const int i, const float v) {
+  const float a = (SP::offset(i) != 0.0f) ? __fsub_rn(v, SP::offset(i)) : v;
+  const float t = __fmul_rn(a, SP::inv_delta(i));
+  const float s = __fadd_rd(t, kFloorMagic);
+  return __fsub_rn(t, __fsub_rn(s, kFloorMagic)) == 0.0f;
+}
+
+// the integer code of FIXED entry i (sign-extended b+1 bits, reading Q2)
+template <class SP>
+__device__ __forceinline__ int scode(const uint32_t* w, const int i) {
+  const int wd = SP::word(i), sh = SP::shift(i), wi = SP::width(i);
+  const uint32_t raw = (sh + wi <= 32) ? (w[wd] >> sh) : __funnelshift_r(w[wd], w[wd + 1], sh);
+  return ((int)(raw << (32 - wi))) >> (32 - wi);
+}
+
+template <class SP>
+__device__ __forceinline__ void sput_code(uint32_t* w, const int i, const int u) {
+  const int wi = SP::width(i);
+  sput<SP>(w, i, (uint32_t)u & ((wi == 32) ? 0xffffffffu : ((1u << wi) - 1u)));
 }
 
 }  // namespace qmpm

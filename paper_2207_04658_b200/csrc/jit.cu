@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <string>
@@ -110,16 +111,42 @@ bool init_nvrtc(std::string& err) {
 
 }  // namespace
 
+// The next step's sort key needs base = floor(fl(fl(u Delta) inv_dx) - 1/2) of every x code
+// u.  When Delta and inv_dx are powers of two, the FIXED x fields have no offset and take
+// the packed fast encode (width <= 23, so |u| < 2^22), every step is exact and base =
+// (u - 2^(k-1)) >> k with 2^-k = Delta inv_dx: the same integer, from the code.
+int integer_key_shift(int dim, const LayoutDev& L, float inv_dx) {
+  auto log2_exact = [](double v, int& e) {
+    int ex = 0;
+    if (!(v > 0.0) || std::frexp(v, &ex) != 0.5) return false;
+    e = ex - 1;
+    return true;
+  };
+  int k = -1;
+  for (int a = 0; a < dim; ++a) {
+    const FieldDev& f = L.s[a];
+    int ed = 0, ei = 0;
+    if (!L.dither || f.kind != kKindFixed || f.width > 23 || f.offset != 0.0f) return 0;
+    if (!log2_exact((double)f.delta, ed) || !log2_exact((double)inv_dx, ei)) return 0;
+    const int ka = -(ed + ei);
+    if (ka < 1 || ka > 24 || (k >= 0 && ka != k)) return 0;
+    k = ka;
+  }
+  return k < 0 ? 0 : k;
+}
+
 std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps, int g2p_warps, int p2g_minb,
-                        int g2p_minb) {
+                        int g2p_minb, int xk) {
   std::string s;
   char buf[1024];
   const int ns = (int)L.ns;
   snprintf(buf, sizeof(buf),
            "struct Spec {\n  static constexpr int D = %d, MAT = %d, NS = %d, W = %u, SW = %u;\n"
            "  static constexpr int P2G_WARPS = %d, G2P_WARPS = %d, P2G_MINB = %d, G2P_MINB = %d;\n"
-           "  static constexpr unsigned XMASK = %uu;\n  static constexpr bool DITHER = %s, COUNTERS = %s, RANGES = %s;\n",
-           dim, material, ns, L.W, L.SW, p2g_warps, g2p_warps, p2g_minb, g2p_minb, L.xword_mask, L.dither ? "true" : "false",
+           "  static constexpr unsigned XMASK = %uu;\n  static constexpr int XK = %d;\n"
+           "  static constexpr bool DITHER = %s, COUNTERS = %s, RANGES = %s;\n",
+           dim, material, ns, L.W, L.SW, p2g_warps, g2p_warps, p2g_minb, g2p_minb, L.xword_mask, xk,
+           L.dither ? "true" : "false",
            L.counters ? "true" : "false", L.ranges ? "true" : "false");
   s += buf;
   auto ints = [&](const char* name, auto get) {

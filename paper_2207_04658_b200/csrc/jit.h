@@ -17,9 +17,12 @@ struct JitModule {
   std::string log;
 };
 
-// the generated preamble + #include of step_kernels.cuh for one layout
+// the generated preamble + #include of step_kernels.cuh for one layout; xk = log2(dx / Delta_x)
+// when the next-step key can come from the integer x codes (0: from the decoded floats)
 std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps, int g2p_warps, int p2g_minb,
-                        int g2p_minb);
+                        int g2p_minb, int xk);
+// xk of spec_source for a layout and a cell size (api.cu)
+int integer_key_shift(int dim, const LayoutDev& L, float inv_dx);
 cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err);
 
 // the standalone codec specialised on one layout (codec_kernels.cuh)

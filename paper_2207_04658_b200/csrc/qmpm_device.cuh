@@ -7,7 +7,8 @@
 //             from b+1 bits (Q2); a field may straddle two words (bit pack).
 //   encode    Eq. 3 / Eq. 11: t = fl32(fl32(v - offset) * inv_Delta), no FMA
 //             (Q3); RNE (Q6) or u = floor(t) + [y >= 1 - r] (Q6), saturated.
-//   r24       reading Q5 (the paper's generator, is in an unavailable supplement).
+//   pair_hash / dither_omr  reading Q5 rev. 3 (the paper's generator, is in an
+//             unavailable supplement).
 #pragma once
 #ifdef __CUDACC_RTC__
 typedef unsigned char uint8_t;
@@ -124,85 +125,27 @@ __host__ __device__ __forceinline__ uint32_t step_salt(uint32_t seed_lo, uint32_
   return mix32_hd(seed_lo ^ mix32_hd(seed_hi ^ mix32_hd(step)));
 }
 
-// r24 for (particle hash h = mix(key ^ salt), field index f): reading Q5 (revision 2),
-// the second half of lowbias32 on the field-salted particle hash
-__device__ __forceinline__ uint32_t r24_of(uint32_t h, uint32_t f) {
-  uint32_t x = (h ^ (f * 0x9E3779B9u)) * 0x7feb352du;
+// Reading Q5, revision 3: one 32-bit hash z per PAIR p of fields (packing indices 2p and
+// 2p + 1), the lowbias32 rounds on the pair-salted particle hash h = mix(key ^ salt).
+__device__ __forceinline__ uint32_t pair_hash(uint32_t h, uint32_t p) {
+  uint32_t x = h ^ (p * 0x9E3779B9u);
+  x *= 0x7feb352du;
   x ^= x >> 15;
-  return (x * 0x846ca68bu) >> 8;
-}
-
-// ---------------------------------------------------------------- decode (Eq. 3)
-// `row` points at a record whose word W (one past the end) is readable.
-__device__ __forceinline__ float decode_field(const uint32_t* row, const FieldDev& f) {
-  const uint32_t lo = row[f.word];
-  const uint32_t hi = row[f.word + 1];
-  const uint32_t raw = __funnelshift_r(lo, hi, f.shift);
-  if (f.kind == kKindRaw) return __uint_as_float(raw);
-  const uint32_t sh = 32u - f.width;
-  const int u = ((int)(raw << sh)) >> sh;  // sign-extend b+1 bits (Q2)
-  float x = __fmul_rn(__int2float_rn(u), f.delta);
-  if (f.offset != 0.0f) x = __fadd_rn(x, f.offset);
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
   return x;
 }
 
-// ---------------------------------------------------------------- encode (Eq. 3 / 11)
-struct EncStat {
-  int up, down, sat, nonfinite;
-};
-
-// Returns the field's raw bits (masked to its width).
-__device__ __forceinline__ uint32_t encode_field(float v, const FieldDev& f, bool dither,
-                                                 uint32_t r24, EncStat& st) {
-  st.up = st.down = st.sat = st.nonfinite = 0;
-  if (f.kind == kKindRaw) {
-    st.nonfinite = !isfinite(v);
-    return __float_as_uint(v);
-  }
-  if (!isfinite(v)) {
-    st.nonfinite = 1;
-    return 0u;
-  }
-  const float a = (f.offset != 0.0f) ? __fsub_rn(v, f.offset) : v;
-  const float t = __fmul_rn(a, f.inv_delta);  // no FMA (Q3)
-  float q;
-  if (dither) {
-    const float fl = floorf(t);
-    const float y = __fsub_rn(t, fl);  // exact
-    const float one_minus_r = __fmul_rn(__uint2float_rn(0x1000000u - r24), 0x1p-24f);  // exact
-    const bool up = y >= one_minus_r;
-    st.up = up;
-    st.down = (!up) && (y > 0.0f);
-    q = fl;
-    // q + up below, in integers (exact for any magnitude)
-    const float qc = fminf(fmaxf(q, -1099511627776.0f), 1099511627776.0f);  // +-2^40
-    long long u = __float2ll_rz(qc) + (up ? 1 : 0);
-    const long long hi = (1ll << (f.width - 1)) - 1, lo = -(1ll << (f.width - 1));
-    if (u > hi) { u = hi; st.sat = 1; }
-    if (u < lo) { u = lo; st.sat = 1; }
-    const uint32_t mask = (f.width == 32) ? 0xffffffffu : ((1u << f.width) - 1u);
-    return (uint32_t)u & mask;
-  }
-  q = rintf(t);  // round half to even (Q6)
-  st.up = q > t;
-  st.down = q < t;
-  const float qc = fminf(fmaxf(q, -1099511627776.0f), 1099511627776.0f);
-  long long u = __float2ll_rz(qc);
-  const long long hi = (1ll << (f.width - 1)) - 1, lo = -(1ll << (f.width - 1));
-  if (u > hi) { u = hi; st.sat = 1; }
-  if (u < lo) { u = lo; st.sat = 1; }
-  const uint32_t mask = (f.width == 32) ? 0xffffffffu : ((1u << f.width) - 1u);
-  return (uint32_t)u & mask;
+// s = 1 + r16 2^-16 for field f as a float assembled from bits: r16 = bits 7..22 of z (even
+// f) or of z rotated right by 16 (odd f), placed in mantissa bits 7..22.
+__device__ __forceinline__ float dither_s(uint32_t h, uint32_t f) {
+  uint32_t z = pair_hash(h, f >> 1);
+  if (f & 1u) z = __funnelshift_r(z, z, 16);
+  return __uint_as_float(0x3f800000u | (z & 0x007fff80u));
 }
 
-// OR a field's bits into a record row (row owned by the calling thread; row has a
-// spare word at W so word + 1 is always writable).
-__device__ __forceinline__ void put_field(uint32_t* row, const FieldDev& f, uint32_t bits) {
-  const unsigned long long wide = (unsigned long long)bits << f.shift;
-  row[f.word] |= (uint32_t)wide;
-  const uint32_t hi = (uint32_t)(wide >> 32);
-  if (hi) row[f.word + 1] |= hi;
-}
+// the dither threshold 1 - r16 2^-16 = 2 - s (exact: Sterbenz), u = floor(t) + [y >= it]
+__device__ __forceinline__ float dither_omr(uint32_t h, uint32_t f) { return __fsub_rn(2.0f, dither_s(h, f)); }
 
 // ---------------------------------------------------------------- MLS-MPM helpers
 // base / fx of one axis with the out-of-domain clamp of Q14.  Identical arithmetic

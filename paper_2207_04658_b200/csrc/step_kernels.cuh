@@ -445,34 +445,54 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
 
 // ------------------------------------------------------------------ a5-a7: G2P + encode
 // per-lane round counters packed 4 per register (byte i%4 of word i/4 counts state
-// scalar i), flushed into 32-bit per-lane totals (lane i holds scalar i) before a
-// byte can overflow
+// scalar i), flushed into 32-bit per-lane totals (lane i holds scalar i) before a byte can
+// overflow.  Dithered: pu counts round-ups and pz on-grid values (down = all - up - on
+// grid, with the idle lanes of partial chunks counted as on-grid); RNE: pu ups, pz downs.
 template <class SP>
 struct RoundCounters {
   static constexpr int NP = (SP::NS + 3) / 4;
   uint32_t pu[NP], pz[NP];
-  uint32_t n_since;  // particles (per lane) since the last flush, warp-uniform
-  unsigned c_up, c_nz;
+  uint32_t n_since;  // chunks (per lane) since the last flush, warp-uniform
+  unsigned c_up, c_z;
+  unsigned long long c_n;  // lane-particles counted (dithered: the "all" of down)
+  // + 1 in the byte of every packed-fast-path entry of register k
+  __host__ __device__ static constexpr uint32_t one(int i) {
+    return (i < SP::NS && fast_ok<SP>(i)) ? 1u << (8 * (i % 4)) : 0u;
+  }
+  __host__ __device__ static constexpr uint32_t fast_one(int k) {
+    return one(4 * k) + one(4 * k + 1) + one(4 * k + 2) + one(4 * k + 3);
+  }
   __device__ __forceinline__ void init() {
 #pragma unroll
     for (int k = 0; k < NP; ++k) pu[k] = pz[k] = 0u;
     n_since = 0u;
-    c_up = c_nz = 0u;
+    c_up = c_z = 0u;
+    c_n = 0ull;
+  }
+  // exact flags of scalar i: dithered counts on-grid (neither), RNE counts downs
+  __device__ __forceinline__ void count(int i, bool up, bool down) {
+    if (up) pu[i / 4] += 1u << (8 * (i % 4));
+    if (SP::DITHER ? (!up && !down) : down) pz[i / 4] += 1u << (8 * (i % 4));
   }
   __device__ __forceinline__ void flush(int lane) {
 #pragma unroll
     for (int i = 0; i < SP::NS; ++i) {
-      if (SP::kind(i) != kKindFixed) continue;
+      if (SP::kind(i) == kKindRaw) continue;
       const unsigned tu = __reduce_add_sync(FULL, (pu[i / 4] >> (8 * (i % 4))) & 255u);
       const unsigned tz = __reduce_add_sync(FULL, (pz[i / 4] >> (8 * (i % 4))) & 255u);
       if (lane == i) {
         c_up += tu;
-        c_nz += tz;
+        c_z += tz;
       }
     }
+    c_n += 32ull * n_since;
 #pragma unroll
     for (int k = 0; k < NP; ++k) pu[k] = pz[k] = 0u;
     n_since = 0u;
+  }
+  // (up, down) of this lane's scalar after the last flush
+  __device__ __forceinline__ unsigned long long downs() const {
+    return SP::DITHER ? c_n - c_up - c_z : (unsigned long long)c_z;
   }
 };
 
@@ -719,9 +739,43 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       uint32_t ow[W + 1];
 #pragma unroll
       for (int q = 0; q <= W; ++q) ow[q] = 0u;
-      bool flag = false;
+      bool flag = false, zero = false;
+      int xc[3] = {0, 0, 0};  // x codes (next step's key)
+      uint32_t pu_save[RoundCounters<SP>::NP], pz_save[RoundCounters<SP>::NP];
+      if (SP::COUNTERS) {
+#pragma unroll
+        for (int k = 0; k < RoundCounters<SP>::NP; ++k) {
+          pu_save[k] = rc.pu[k];
+          pz_save[k] = rc.pz[k];
+          rc.pu[k] += RoundCounters<SP>::fast_one(k);  // + 1 per fast entry; - 1 below when rounded down
+        }
+      }
 #pragma unroll
       for (int i = 0; i < NSV; ++i) {
+        const int role = pair_role<SP>(i);
+        if (role == 2) continue;
+        if (role == 1) {  // packed pair (i, i + 1), one pair hash when they share one (Q5 rev. 3)
+          int ui, uj, sbi, sbj;
+          senc_pair_fast<SP>(i, i + 1, o[i], o[i + 1], dither_s(h, SP::idx(i)), dither_s(h, SP::idx(i + 1)), ui, uj,
+                             sbi, sbj, flag, zero);
+          sput_code<SP>(ow, i, ui);
+          sput_code<SP>(ow, i + 1, uj);
+          if (i < D) xc[i] = ui;
+          if (i + 1 < D) xc[i + 1] = uj;
+          if (SP::COUNTERS) {
+            rc.pu[i / 4] += (uint32_t)sbi << (8 * (i % 4));
+            rc.pu[(i + 1) / 4] += (uint32_t)sbj << (8 * ((i + 1) % 4));
+          }
+          continue;
+        }
+        if (fast_ok<SP>(i)) {
+          int sb;
+          const int u = senc1_fast<SP>(i, o[i], dither_s(h, SP::idx(i)), sb, flag, zero);
+          sput_code<SP>(ow, i, u);
+          if (i < D) xc[i] = u;
+          if (SP::COUNTERS) rc.pu[i / 4] += (uint32_t)sb << (8 * (i % 4));
+          continue;
+        }
         if (SP::kind(i) == kKindShared) {  // reading Q4: the whole group at its leader
           if (SP::glead(i) == i) {
             EncFlags gfl[NSV];
@@ -730,21 +784,16 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
             for (int j = 0; j < NSV; ++j) {
               if (SP::kind(j) != kKindShared || SP::glead(j) != i) continue;
               flag |= gfl[j].sat || gfl[j].nonfinite;
-              if (SP::COUNTERS) {
-                if (gfl[j].up) rc.pu[j / 4] += 1u << (8 * (j % 4));
-                if (SP::DITHER ? (gfl[j].up || gfl[j].down) : gfl[j].down) rc.pz[j / 4] += 1u << (8 * (j % 4));
-              }
+              if (SP::COUNTERS) rc.count(j, gfl[j].up, gfl[j].down);
             }
           }
           continue;
         }
-        const uint32_t r24 = (SP::DITHER && SP::kind(i) == kKindFixed) ? r24_of(h, SP::idx(i)) : 0u;
+        const float omr = (SP::DITHER && SP::kind(i) == kKindFixed) ? dither_omr(h, SP::idx(i)) : 1.0f;
         bool up, nz;
-        sput<SP>(ow, i, senc_fast<SP>(i, o[i], r24, up, nz, flag));
-        if (SP::COUNTERS && SP::kind(i) == kKindFixed) {
-          if (up) rc.pu[i / 4] += 1u << (8 * (i % 4));
-          if (nz) rc.pz[i / 4] += 1u << (8 * (i % 4));
-        }
+        sput<SP>(ow, i, senc_fast<SP>(i, o[i], omr, up, nz, flag));
+        if (i < D && SP::kind(i) == kKindFixed) xc[i] = scode<SP>(ow, i);
+        if (SP::COUNTERS && SP::kind(i) == kKindFixed) rc.count(i, up, SP::DITHER ? (nz && !up) : nz);
       }
       if (__any_sync(FULL, valid && flag)) {  // rare: exact re-encode with saturation / non-finite
 #pragma unroll
@@ -756,9 +805,22 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
             if (SP::glead(i) == i) senc_group<SP>(i, o, h, ow, fl);
             continue;
           }
-          const uint32_t r24 = (SP::DITHER && SP::kind(i) == kKindFixed) ? r24_of(h, SP::idx(i)) : 0u;
-          sput<SP>(ow, i, senc<SP>(i, o[i], r24, fl[i]));
+          const float omr = (SP::DITHER && SP::kind(i) == kKindFixed) ? dither_omr(h, SP::idx(i)) : 1.0f;
+          sput<SP>(ow, i, senc<SP>(i, o[i], omr, fl[i]));
         }
+        if (SP::COUNTERS) {  // the exact rule's counts replace the fast pass's
+#pragma unroll
+          for (int k = 0; k < RoundCounters<SP>::NP; ++k) {
+            rc.pu[k] = pu_save[k];
+            rc.pz[k] = pz_save[k];
+          }
+#pragma unroll
+          for (int i = 0; i < NSV; ++i)
+            if (SP::kind(i) != kKindRaw) rc.count(i, fl[i].up, fl[i].down);
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          if (SP::kind(i) == kKindFixed) xc[i] = scode<SP>(ow, i);
 #pragma unroll
         for (int i = 0; i < NSV; ++i) {
           const unsigned bs = __ballot_sync(FULL, valid && fl[i].sat);
@@ -766,6 +828,12 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
           if (lane == i) c_sat += __popc(bs);
           if (lane == 0) c_nf += __popc(bn);
         }
+      } else if (SP::COUNTERS && SP::DITHER && __any_sync(FULL, zero)) {
+        // rare (after the first steps): on-grid values of the packed fast path, counted as
+        // neither up nor down (a value on the grid never rounds up: 1 - r > 0)
+#pragma unroll
+        for (int i = 0; i < NSV; ++i)
+          if (fast_ok<SP>(i) && on_grid_fast<SP>(i, o[i])) rc.pz[i / 4] += 1u << (8 * (i % 4));
       }
       if (SP::COUNTERS && ++rc.n_since == 255u) rc.flush(lane);
       if (SP::RANGES) {  // Alg. 1 line 9: max |value| of s_{t+1} per state scalar (lane i keeps scalar i)
@@ -779,13 +847,35 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         const unsigned bo = __ballot_sync(FULL, valid && oob_any);
         if (lane == 0) c_oob += __popc(bo);
       }
-      // next step's sort key from the re-decoded (quantized) x
-      float xq[3];
+      // next step's sort key: from the integer x codes when x = u Delta and x / dx are exact
+      // powers-of-two scalings (Spec::XK = log2(dx / Delta) > 0: base = floor(u 2^-XK - 1/2),
+      // bit-identical to floor(fl(fl(u Delta) / dx) - 1/2)), else from the re-decoded x
+      uint32_t nkey;
+      {
+        bool koob = false;
+        if (SP::XK > 0) {
+          int c[3] = {0, 0, 0}, l[3] = {0, 0, 0};
 #pragma unroll
-      for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
-      bool koob = false;
-      uint32_t nkey = key_of_fast<D>(xq, S, koob);
-      if (__any_sync(FULL, valid && koob)) nkey = key_of<D>(xq, S);  // rare: clamped base (Q14)
+          for (int a = 0; a < D; ++a) {
+            const int bs = (xc[a] - (1 << (SP::XK - 1))) >> SP::XK;
+            koob |= (unsigned)bs > (unsigned)(S.res[a] - 3);
+            c[a] = bs >> G::LB;
+            l[a] = bs & (G::B - 1);
+          }
+          nkey = (block_id<D>(c, S) << 6) | local_node<D>(l);
+        } else {
+          float xq[3];
+#pragma unroll
+          for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
+          nkey = key_of_fast<D>(xq, S, koob);
+        }
+        if (__any_sync(FULL, valid && koob)) {  // rare: clamped base (Q14)
+          float xq[3];
+#pragma unroll
+          for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
+          nkey = key_of<D>(xq, S);
+        }
+      }
       if (valid) key_out[j] = nkey;
       {  // next step's histograms, one atomic per distinct key of the warp
         const uint32_t nk = valid ? (nkey >> 6) : 0xffffffffu;
@@ -816,12 +906,16 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
   // flush this thread's counters (lane i holds scalar i's counts)
   if (lane < NSV) {
     int fi = 0;
+    bool raw = false;
 #pragma unroll
     for (int i = 0; i < NSV; ++i)
-      if (lane == i) fi = SP::idx(i);
-    const unsigned c_dn = SP::DITHER ? rc.c_nz - rc.c_up : rc.c_nz;
+      if (lane == i) {
+        fi = SP::idx(i);
+        raw = SP::kind(i) == kKindRaw;
+      }
+    const unsigned long long c_dn = (SP::COUNTERS && !raw) ? rc.downs() : 0ull;
     if (rc.c_up) atomicAdd(&dc->up[fi], (unsigned long long)rc.c_up);
-    if (c_dn) atomicAdd(&dc->down[fi], (unsigned long long)c_dn);
+    if (c_dn) atomicAdd(&dc->down[fi], c_dn);
     if (c_sat) atomicAdd(&dc->sat[fi], (unsigned long long)c_sat);
   }
   if (c_nf) atomicAdd(&dc->nonfinite, (unsigned long long)c_nf);

@@ -320,8 +320,9 @@ def test_free_fall_and_rest():
     assert np.array_equal(w1, w2)
 
 
-def test_fluid_uniform_compression():
-    """Fluid (reading Q15): J' = J (1 + dt tr C'); at rest with J = 1 nothing moves."""
+def test_fluid_at_rest_is_a_fixed_point():
+    """Fluid (reading Q15) at rest with J = 1, C = 0 and no gravity: nothing moves (the
+    J = 1 special case of the closed forms below)."""
     s = sim3d(res=32, E=50.0, material="fluid")
     rng = np.random.default_rng(80)
     n = 100
@@ -330,6 +331,75 @@ def test_fluid_uniform_compression():
     w = _state_words(sch, st)
     pre, w2, _ = oracle.step(s, sch, w, 1)
     np.testing.assert_array_equal(w, w2)
+
+
+def fluid_particle(x, v=(0, 0, 0), J=1.0, C=None):
+    C = np.zeros((3, 3)) if C is None else np.asarray(C, float)
+    return np.concatenate([np.asarray(x, float), np.asarray(v, float), [J], C.reshape(-1)])
+
+
+@pytest.mark.parametrize("J", [0.9, 0.97, 1.06])
+def test_fluid_stress_first_moment_closed_form(J):
+    """P2G of the J-fluid stress (reading Q15: P F^T = E (J - 1) I, affine
+    A = -dt V_p 4/dx^2 P F^T): with v = 0 and C = 0 the node momenta are p_i = w_i A (x_i -
+    x_p), so sum_i p_i = 0 and sum_i p_i (x) (x_i - x_p) = A dx^2/4 = -dt V_p E (J - 1) I
+    (B-spline second moment 1/4 per axis).  A sign or scale error in E (J - 1), or an extra
+    J factor, changes the moment."""
+    E, dt = 40.0, 2e-4
+    s = sim3d(res=32, E=E, dt=dt, material="fluid")
+    xp = np.array([0.4731, 0.5212, 0.4968])
+    grid, origin, gsize, _ = oracle.p2g(s, fluid_particle(xp, J=J)[None])
+    X = node_positions(s, origin, gsize) - xp
+    p = grid[..., 1:4]
+    mom = np.einsum("xyza,xyzb->ab", p, X)
+    expect = -dt * s["p_vol"] * E * (J - 1.0) * np.eye(3)
+    np.testing.assert_allclose(mom, expect, rtol=1e-12, atol=1e-12 * abs(expect[0, 0]))
+    np.testing.assert_allclose(p.sum(axis=(0, 1, 2)), 0.0, atol=1e-12 * abs(expect[0, 0]) / s["dx"])
+    assert np.isclose(grid[..., 0].sum(), s["p_rho"] * s["p_vol"], rtol=1e-14)
+
+
+@pytest.mark.parametrize("J", [0.95, 1.02])
+def test_fluid_J_update_affine_field(J):
+    """G2P of the J-fluid (reading Q11/Q15): an affine grid velocity v(x) = G x + b
+    gives C' = G (affine reproduction) and J' = J (1 + dt tr C') = J (1 + dt tr G); a
+    dropped J, a flipped sign or tr over the wrong entries fails."""
+    s = sim3d(res=32, dt=1e-3, material="fluid")
+    rng = np.random.default_rng(81)
+    G = rng.normal(0, 3.0, (3, 3))
+    b = rng.normal(0, 1.0, 3)
+    st = fluid_particle([0.4812, 0.5377, 0.5091], J=J)[None]
+    origin, gsize = oracle.stencil_box(s, st)
+    Xn = node_positions(s, origin, gsize)
+    grid = np.zeros(tuple(int(g) for g in gsize[:3]) + (4,))
+    grid[..., 0] = 1.0
+    grid[..., 1:4] = Xn @ G.T + b
+    out = oracle.g2p(s, st, grid, origin, gsize)[0]
+    np.testing.assert_allclose(out[7:16].reshape(3, 3), G, rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(out[3:6], G @ st[0, :3] + b, rtol=1e-12, atol=1e-12)
+    assert np.isclose(out[6], J * (1.0 + s["dt"] * np.trace(G)), rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("J", [0.9, 1.05])
+def test_fluid_single_particle_step_closed_form(J):
+    """One whole fluid step of a lone particle (no gravity, away from walls): P2G gives
+    p_i = w_i A (x_i - x_p), m_i = w_i m_p, so the grid velocity is the affine field
+    (A / m_p)(x_i - x_p) and G2P returns v' = 0, C' = A / m_p and
+    J' = J (1 + dt tr A / m_p) = J (1 - 12 dt^2 E (J - 1) / (rho dx^2)):
+    a compressed particle (J < 1) expands.  Exercises the stress and the J update together."""
+    E, dt = 30.0, 1e-4
+    s = sim3d(res=32, E=E, dt=dt, material="fluid")
+    st = fluid_particle([0.4903, 0.5066, 0.5127], J=J)[None]
+    sch = schemes.fp32(3, "fluid")
+    w = _state_words(sch, st)
+    pre, _, _ = oracle.step(s, sch, w, 1)
+    Jf = float(np.float32(J))
+    A = -dt * s["p_vol"] * 4.0 / s["dx"] ** 2 * E * (Jf - 1.0)
+    mp = s["p_rho"] * s["p_vol"]
+    np.testing.assert_allclose(pre[0, 3:6], 0.0, atol=1e-12)
+    np.testing.assert_allclose(pre[0, 7:16].reshape(3, 3), A / mp * np.eye(3), rtol=1e-9, atol=1e-9 * abs(A / mp))
+    Jexp = Jf * (1.0 - 12.0 * dt * dt * E * (Jf - 1.0) / (s["p_rho"] * s["dx"] ** 2))
+    assert np.isclose(pre[0, 6], Jexp, rtol=1e-12, atol=0)
+    assert (pre[0, 6] > Jf) == (Jf < 1.0)
 
 
 # --------------------------------------------------------------- consistency
