@@ -31,6 +31,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the OpenMP oracle (cpu_baseline, --impl reference) shares torch's libgomp: passive
+# waiting keeps the two thread pools from spinning against each other (read at init)
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 
 PAPER_PSTEPS = {"c3": 295_280_208 * 128 / 63.5,   # derived from T-large, RTX 3090: context
                 "c4": 400_000_000 * 128 / 139.3}   # derived from T-large, RTX 3090: context
@@ -143,20 +146,34 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- CPU oracle
-def cpu_oracle_rate(sc, sch, n_sample, steps):
-    """The oracle as it stands (single-threaded plain C, fp64), on the first n_sample
-    particles of the same workload; returns particle-steps/s."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_oracle_rate(sc, sch, n_sample, steps, threads=1):
+    """The oracle (plain C, fp64) on the first n_sample particles of the same workload:
+    threads = 1 the single-threaded oracle_step, else its OpenMP particle loops
+    (SURVEY §8(d) M7 ii; 0 = all host cores).  Returns (p-steps/s, n, steps, s, threads)."""
     import oracle
     n = min(n_sample, sc.n_particles)
     st = sc.state_chunk(0, n)
     w, _ = oracle.encode_state(sch, st)
+    used = 1 if threads == 1 else (oracle.num_threads() if threads <= 0 else threads)
     t0 = time.perf_counter()
-    oracle.run(sc.sim, sch, w, 1, steps)
+    oracle.run(sc.sim, sch, w, 1, steps, threads=threads)
     dt = time.perf_counter() - t0
-    return n * steps / dt, n, steps, dt
+    return n * steps / dt, n, steps, dt, used
 
 
 def run_reference(args):
+    """The oracle as it stands on the box's host cores (its OpenMP particle loops on all
+    cores), on a bounded sample of the same workload per step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -166,12 +183,13 @@ def run_reference(args):
     n = min(args.ref_sample, sc.n_particles)
     st = sc.state_chunk(0, n)
     w, _ = oracle.encode_state(sch, st)
+    cores = oracle.num_threads()
     for t in range(args.warmup):
-        w = oracle.step(sc.sim, sch, w, t + 1)[1]
+        w = oracle.step(sc.sim, sch, w, t + 1, threads=0)[1]
     times = []
     for t in range(args.steps):
         t0 = time.perf_counter()
-        w = oracle.step(sc.sim, sch, w, args.warmup + t + 1)[1]
+        w = oracle.step(sc.sim, sch, w, args.warmup + t + 1, threads=0)[1]
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = n * args.steps / total
@@ -181,8 +199,10 @@ def run_reference(args):
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args, sc, W, bits), "sample_particles": n},
-        "cpu_baseline": {"value": value, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
-                         "sample": f"first {n:,} particles of the workload, {args.steps} steps (fp64 plain C, 1 thread)"},
+        "cpu_baseline": {"value": value, "unit": "particle-steps/s", "cores": cores, "kind": "oracle",
+                         "sample": f"first {n:,} particles of the workload, {args.steps} steps "
+                                   f"(fp64 plain C, OpenMP particle loops on {cores} threads)",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -231,16 +251,16 @@ def run_gpu(args):
             if sc.dim != 3:
                 raise SystemExit("multi-GPU runs need a 3D config")
             cuts = qdist.slab_cuts(sc.sim["grid_res"][2], world)
-            per = sc.n_particles // world
-            sim = qmpm.Sim(sc.sim, sch, int(per * 1.25) + 65536, flags=flags, stream=stream,
+            cap = qdist.slab_capacity(sc, cuts, rank)
+            sim = qmpm.Sim(sc.sim, sch, cap, flags=flags, stream=stream,
                            slab=(world, rank, cuts[rank][0], cuts[rank][1]))
             uid = qdist.share_unique_id(qmpm.get_unique_id)
             sim.connect_nccl(uid)
             qdist.load_slab(sim, sc, cuts, rank, track_ids=False)
-            N = sc.n_particles // world  # particles per GPU
         torch.cuda.empty_cache()
         sim.step(args.scene_warmup + args.warmup)
         stream.synchronize()
+        cap = sim.params.max_particles  # this rank's context capacity (host buffers below)
 
         # ---------------- timed region (device): K steps, per-kernel events on the ctx stream
         sim.set_profiling(True)
@@ -263,40 +283,50 @@ def run_gpu(args):
         ktimes = sim.kernel_times()
         st = sim.stats()
         sim.set_profiling(False)
+        N = int(st.n_particles)  # this rank's particles (slabs: after migration)
+        n_total = N
         if world > 1:
             t = torch.tensor([ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        value = sc.n_particles * args.steps / (ms / 1e3)
+            c = torch.tensor([N], device="cuda", dtype=torch.int64)
+            dist.all_reduce(c)
+            n_total = int(c.item())
+        value = n_total * args.steps / (ms / 1e3)
 
         # ---------------- end to end through the C ABI with pinned host buffers
         e2e = None
         if not args.no_e2e:
-            host = torch.empty((N, W), dtype=torch.int32, pin_memory=True)
-            sim.read_state(words=host)  # the current state, as a user would hold it on the host
+            # sized at the context capacity: a slab's count changes with migration
+            host = torch.empty((cap, W), dtype=torch.int32, pin_memory=True)
+            n0 = sim.read_state(words=host)  # the current state, as a user would hold it on the host
             step0 = st.step
             k = args.steps
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            sim.set_words(host, step0)           # H2D of the inputs (pinned)
+            sim.set_words(host[:n0], step0)      # H2D of the inputs (pinned)
             for _ in range(k):
                 sim.step(1)
                 sim.stats()                      # D2H of the step's metric (counters)
-            sim.read_state(words=host)           # D2H of the result
+            n1 = sim.read_state(words=host)      # D2H of the result
             t1 = time.perf_counter()
             e2e_s = t1 - t0
+            nt = n0
             if world > 1:
                 t = torch.tensor([e2e_s], device="cuda")
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 e2e_s = float(t.item())
+                c = torch.tensor([n0], device="cuda", dtype=torch.int64)
+                dist.all_reduce(c)
+                nt = int(c.item())
             stats_bytes = 8 * (2 + 3 * 64 + 5)
-            e2e = {"value": sc.n_particles * k / e2e_s, "unit": "particle-steps/s",
-                   "h2d_bytes_per_step": int(N * W * 4 / k),
-                   "d2h_bytes_per_step": int(N * W * 4 / k + stats_bytes),
-                   "note": f"timed: set_words(pinned host, {N*W*4/1e9:.2f} GB) + {k} x (qmpm_step + qmpm_stats D2H) "
-                           "+ read_state(words -> pinned host)"}
+            e2e = {"value": nt * k / e2e_s, "unit": "particle-steps/s",
+                   "h2d_bytes_per_step": int(n0 * W * 4 / k),
+                   "d2h_bytes_per_step": int(n1 * W * 4 / k + stats_bytes),
+                   "note": f"timed: set_words(pinned host, {n0*W*4/1e9:.2f} GB) + {k} x (qmpm_step + qmpm_stats D2H) "
+                           "+ read_state(words -> pinned host); rank 0's bytes"}
             del host
         sim.close()
 
@@ -338,10 +368,14 @@ def run_gpu(args):
     # ---------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None
     if world == 1:
-        rate, n_s, s_s, secs = cpu_oracle_rate(sc, sch, args.cpu_sample, args.cpu_steps)
-        cpu = {"value": rate, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {n_s:,} particles of the workload, {s_s} steps from the initial state "
-                         f"(fp64 plain C, single thread, {secs:.1f} s)", "cpu": os.cpu_count()}
+        rate1, n_s, s_s, secs1, _ = cpu_oracle_rate(sc, sch, args.cpu_sample, args.cpu_steps, threads=1)
+        rate, n_m, s_m, secs, used = cpu_oracle_rate(sc, sch, args.cpu_sample, 4 * args.cpu_steps, threads=0)
+        cpu = {"value": rate, "unit": "particle-steps/s", "cores": used, "kind": "oracle",
+               "sample": f"first {n_m:,} particles of the workload, {s_m} steps from the initial state "
+                         f"(fp64 plain C, OpenMP particle loops on {used} threads, {secs:.1f} s)",
+               "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
+               "single_thread": {"value": rate1, "cores": 1,
+                                 "sample": f"first {n_s:,} particles, {s_s} steps ({secs1:.1f} s)"}}
 
     line = {
         "metric": "quantized MPM particle-steps/sec", "value": value, "unit": "particle-steps/s",

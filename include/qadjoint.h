@@ -29,8 +29,9 @@ extern "C" {
 typedef struct qadj_ctx qadj_ctx; /* opaque: dense grids + the checkpoint pool */
 
 typedef struct {
-    uint32_t max_resident;  /* states held at once by the bisection (s0 included): O(log T) */
-    uint32_t pad;
+    uint32_t max_resident;  /* forward checkpoints held at once by the bisection (s0 included): O(log T) */
+    uint32_t peak_buffers;  /* state-sized device buffers in use at once: checkpoints + the
+                               adjoints of each recursion level + 2 scratch, ~2 log2 T + 4 */
     uint64_t forward_steps; /* forward steps run (T the first time, then the re-runs): O(T log T) */
     uint64_t adjoint_steps; /* T */
 } qadj_stats;

@@ -270,7 +270,9 @@ qmpm_status qmpm_predict_error(uint32_t H, const double* delta, const double* g,
  * ceil(-log2(delta/R_h)) clamped to [b_min, b_max] (0 <= b_min <= b_max <= 31).
  * P_h > 0 (variables of type h), g_h >= 0 (a type with g_h = 0 gets b_min and
  * delta = inf), R_h > 0 (ranges), z != 0 the reference metric, eps_err > 0.  Host
- * arrays, no GPU.  QMPM_EINVAL (message in qmpm_last_error(NULL)) on bad input. */
+ * arrays, no GPU.  QMPM_EINVAL (message in qmpm_last_error(NULL)) on bad input;
+ * QMPM_EDOMAIN when the b_max clamp leaves sigma_pred (Eq. 8, with the clamped widths)
+ * above eps_err |z| -- the outputs are still filled with the clamped scheme. */
 qmpm_status qmpm_solve_error_bounded(uint32_t H, const double* P, const double* g, const double* R, double z,
                                      double eps_err, int32_t b_min, int32_t b_max, double* delta_out,
                                      int32_t* bits_out);
@@ -278,8 +280,10 @@ qmpm_status qmpm_solve_error_bounded(uint32_t H, const double* P, const double* 
  * sum_h P_h bits[h] <= budget_bits (FRACTION bits: the stored width is bits + 1, so a
  * physical budget eps_mem * M is budget_bits = eps_mem * M - sum_h P_h).  Closed form
  * of SPEC.md:342 (the paper's is in its supplement): delta_h = c sqrt(P_h/g_h),
- * bits = floor(-log2(delta/R_h)) clamped; types with g_h = 0 take b_min.  QMPM_EINVAL
- * when the budget cannot hold b_min everywhere. */
+ * bits = floor(-log2(delta/R_h)) over the box [b_min, b_max] by an active set (a width
+ * the closed form puts outside the box is fixed at the bound and the others re-solved
+ * with the budget left); types with g_h = 0 take b_min.  QMPM_EINVAL when the budget
+ * cannot hold b_min everywhere. */
 qmpm_status qmpm_solve_memory_bounded(uint32_t H, const double* P, const double* g, const double* R,
                                       double budget_bits, int32_t b_min, int32_t b_max, double* delta_out,
                                       int32_t* bits_out);

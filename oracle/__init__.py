@@ -13,6 +13,8 @@ the 100-step aggregates beyond the invariants, and the dither RNG's exact bits
 """
 from __future__ import annotations
 
+import os as _os
+_os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")  # see tests/conftest.py
 import ctypes
 import os
 import subprocess
@@ -36,7 +38,7 @@ def build(force=False):
         t = os.path.getmtime(_LIB_PATH)
         if all(os.path.getmtime(d) <= t for d in deps):
             return _LIB_PATH
-    cmd = ["gcc", "-O2", "-std=c11", "-Wall", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+    cmd = ["gcc", "-O2", "-std=c11", "-Wall", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-fopenmp",
            "-shared", "-o", _LIB_PATH] + srcs + ["-lm"]
     subprocess.check_call(cmd, cwd=_HERE)
     return _LIB_PATH
@@ -96,6 +98,9 @@ def lib():
             "oracle_step_f32": (i32, [P, P, u64, P, u64, P, P, P]),
             "oracle_step_sampled_f64": (i32, [P, P, u64, P, u64, u64, P, P, P]),
             "oracle_run_f64": (i32, [P, P, u64, P, u64, u32, P]),
+            "oracle_step_omp_f64": (i32, [P, P, u64, P, u64, P, P, P, i32]),
+            "oracle_run_omp_f64": (i32, [P, P, u64, P, u64, u32, P, i32]),
+            "oracle_num_threads": (i32, []),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -307,8 +312,14 @@ def polar(F):
     return R.reshape(d, d)
 
 
-def step(sim, scheme, words, step_index, precision="f64"):
-    """One quantized step from packed words -> (pre_encode [n][ns], words_out, counters)."""
+def num_threads():
+    """OpenMP threads the parallel oracle uses by default (all host cores)."""
+    return lib().oracle_num_threads()
+
+
+def step(sim, scheme, words, step_index, precision="f64", threads=1):
+    """One quantized step from packed words -> (pre_encode [n][ns], words_out, counters).
+    threads != 1 (fp64 only): the OpenMP oracle (0 = all cores)."""
     s = make_scheme(scheme)
     so = make_sim(sim)
     words = np.ascontiguousarray(words, dtype=np.uint32)
@@ -318,6 +329,12 @@ def step(sim, scheme, words, step_index, precision="f64"):
     pre = np.zeros((n, ns), dtype=dt)
     out = np.zeros_like(words)
     cnt = np.zeros(NCOUNTERS, dtype=np.uint64)
+    if threads != 1:
+        assert precision == "f64"
+        rc = lib().oracle_step_omp_f64(ctypes.byref(so), ctypes.byref(s), n, _p(words), step_index, _p(pre), _p(out),
+                                       _p(cnt), int(threads))
+        assert rc == 0, rc
+        return pre, out, cnt
     fn = lib().oracle_step_f64 if precision == "f64" else lib().oracle_step_f32
     rc = fn(ctypes.byref(so), ctypes.byref(s), n, _p(words), step_index, _p(pre), _p(out), _p(cnt))
     assert rc == 0, rc
@@ -338,11 +355,17 @@ def step_sampled(sim, scheme, words, step_index, sample):
     return pre, out
 
 
-def run(sim, scheme, words, first_step, n_steps):
+def run(sim, scheme, words, first_step, n_steps, threads=1):
+    """n_steps fp64 steps; threads != 1: the OpenMP oracle (0 = all cores)."""
     s = make_scheme(scheme)
     so = make_sim(sim)
     w = np.ascontiguousarray(words, dtype=np.uint32).copy()
     cnt = np.zeros(NCOUNTERS, dtype=np.uint64)
+    if threads != 1:
+        rc = lib().oracle_run_omp_f64(ctypes.byref(so), ctypes.byref(s), w.shape[0], _p(w), first_step, n_steps,
+                                      _p(cnt), int(threads))
+        assert rc == 0, rc
+        return w, cnt
     rc = lib().oracle_run_f64(ctypes.byref(so), ctypes.byref(s), w.shape[0], _p(w), first_step,
                               n_steps, _p(cnt))
     assert rc == 0, rc

@@ -261,3 +261,142 @@ int oracle_step_sampled_f64(const oracle_sim* sim, const oracle_scheme* s, uint6
     hfree(&nodes);
     return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* The same step as oracle_step_f64 with its particle and node loops spread over
+ * OpenMP threads (the oracle on all host cores).  Nothing of the
+ * arithmetic changes; only the order of the P2G sums: particles are bucketed by the
+ * 4-cell x slab of their base cell, even slabs are scattered in parallel (their
+ * stencils, 6 node planes wide, never overlap), then odd slabs; inside a slab in
+ * particle order.  The order does not depend on the thread count, so the result is
+ * deterministic.  Counters are summed over per-thread copies (integers).            */
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+int oracle_step_omp_f64(const oracle_sim* sim, const oracle_scheme* s, uint64_t n, const uint32_t* words_in,
+                        uint64_t step, double* pre_encode, uint32_t* words_out, uint64_t* counters,
+                        int n_threads) {
+    int d = sim->dim, ns = oracle_n_scalars(d, sim->material);
+    uint32_t W, bits;
+    if (oracle_layout(s, 0, &W, &bits)) return -1;
+#ifdef _OPENMP
+    if (n_threads <= 0) n_threads = omp_get_max_threads();
+#else
+    n_threads = 1;
+#endif
+    uint64_t nn = n ? n : 1;
+    float* dec = (float*)malloc(sizeof(float) * ns * nn);
+    double* st = (double*)malloc(sizeof(double) * ns * nn);
+    double* out = (double*)malloc(sizeof(double) * ns * nn);
+    uint32_t* keys = (uint32_t*)malloc(sizeof(uint32_t) * nn);
+    int32_t* bx = (int32_t*)malloc(sizeof(int32_t) * nn);
+    if (!dec || !st || !out || !keys || !bx) return -2;
+    int err = 0;
+    double inv_dx = 1.0 / sim->dx;
+#pragma omp parallel num_threads(n_threads) reduction(| : err)
+    {
+#ifdef _OPENMP
+        int t = omp_get_thread_num(), nt = omp_get_num_threads();
+#else
+        int t = 0, nt = 1;
+#endif
+        uint64_t lo = n * (uint64_t)t / (uint64_t)nt, hi = n * (uint64_t)(t + 1) / (uint64_t)nt;
+        if (hi > lo) err |= oracle_decode_state(s, d, sim->material, hi - lo, words_in + lo * W, dec + lo * ns) != 0;
+        for (uint64_t p = lo; p < hi; ++p) {
+            for (int a = 0; a < ns; ++a) st[p * ns + a] = (double)dec[p * ns + a];
+            keys[p] = oracle_particle_key(s, d, words_in + p * W);
+            int b;
+            double f;
+            base_fx_f64(st[p * ns], inv_dx, sim->grid_res[0], &b, &f);
+            bx[p] = b;
+        }
+    }
+    if (err) return -1;
+    int32_t origin[3], gsize[3];
+    stencil_box_f64(sim, n, st, origin, gsize);
+    long cells = (long)gsize[0] * gsize[1] * gsize[2];
+    double* grid = (double*)calloc((size_t)cells * 4, sizeof(double));
+    if (!grid) return -2;
+    /* bucket particles by 4-cell x slab (counting sort, particle order kept) */
+    int nslab = (gsize[0] + 3) / 4 + 1;
+    uint64_t* start = (uint64_t*)calloc((size_t)nslab + 1, sizeof(uint64_t));
+    uint64_t* order = (uint64_t*)malloc(sizeof(uint64_t) * nn);
+    if (!start || !order) return -2;
+    for (uint64_t p = 0; p < n; ++p) start[(bx[p] - origin[0]) / 4 + 1]++;
+    for (int q = 0; q < nslab; ++q) start[q + 1] += start[q];
+    {
+        uint64_t* cur = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)nslab);
+        memcpy(cur, start, sizeof(uint64_t) * (size_t)nslab);
+        for (uint64_t p = 0; p < n; ++p) order[cur[(bx[p] - origin[0]) / 4]++] = p;
+        free(cur);
+    }
+    uint64_t oob = 0;
+    for (int parity = 0; parity < 2; ++parity) {
+#pragma omp parallel for num_threads(n_threads) schedule(dynamic, 1) reduction(+ : oob)
+        for (int q = parity; q < nslab; q += 2)
+            for (uint64_t k = start[q]; k < start[q + 1]; ++k)
+                oob += (uint64_t)p2g_one_f64(sim, st + order[k] * ns, origin, gsize, grid);
+    }
+#pragma omp parallel for num_threads(n_threads) schedule(static)
+    for (long c = 0; c < cells; ++c) {
+        long li = c / ((long)gsize[1] * gsize[2]), lj = (c / gsize[2]) % gsize[1], lk = c % gsize[2];
+        int ijk[3] = {origin[0] + (int)li, origin[1] + (int)lj, origin[2] + (int)lk};
+        update_node_f64(sim, ijk, grid + 4 * c);
+    }
+#pragma omp parallel for num_threads(n_threads) schedule(static)
+    for (int64_t p = 0; p < (int64_t)n; ++p) g2p_one_f64(sim, st + p * ns, origin, gsize, grid, out + p * ns);
+    if (counters) counters[193] += oob;
+    if (pre_encode) memcpy(pre_encode, out, sizeof(double) * ns * n);
+    uint64_t* tc = (uint64_t*)calloc((size_t)n_threads * ORACLE_NCOUNTERS, sizeof(uint64_t));
+    if (!tc) return -2;
+#pragma omp parallel num_threads(n_threads) reduction(| : err)
+    {
+#ifdef _OPENMP
+        int t = omp_get_thread_num(), nt = omp_get_num_threads();
+#else
+        int t = 0, nt = 1;
+#endif
+        uint64_t lo = n * (uint64_t)t / (uint64_t)nt, hi = n * (uint64_t)(t + 1) / (uint64_t)nt;
+        for (uint64_t i = lo * ns; i < hi * ns; ++i) dec[i] = (float)out[i];
+        if (hi > lo)
+            err |= oracle_encode_state(s, d, sim->material, hi - lo, dec + lo * ns, step, keys + lo,
+                                       words_out + lo * W, counters ? tc + (size_t)t * ORACLE_NCOUNTERS : 0) != 0;
+    }
+    if (counters)
+        for (int t = 0; t < n_threads; ++t)
+            for (int c = 0; c < ORACLE_NCOUNTERS; ++c) counters[c] += tc[(size_t)t * ORACLE_NCOUNTERS + c];
+    free(tc);
+    free(grid);
+    free(start);
+    free(order);
+    free(dec);
+    free(st);
+    free(out);
+    free(keys);
+    free(bx);
+    return err ? -1 : 0;
+}
+
+int oracle_run_omp_f64(const oracle_sim* sim, const oracle_scheme* s, uint64_t n, uint32_t* words,
+                       uint64_t first_step, uint32_t n_steps, uint64_t* counters, int n_threads) {
+    uint32_t W, bits;
+    if (oracle_layout(s, 0, &W, &bits)) return -1;
+    uint32_t* tmp = (uint32_t*)malloc(sizeof(uint32_t) * W * (n ? n : 1));
+    if (!tmp) return -2;
+    for (uint32_t t = 0; t < n_steps; ++t) {
+        int rc = oracle_step_omp_f64(sim, s, n, words, first_step + t, 0, tmp, counters, n_threads);
+        if (rc) { free(tmp); return rc; }
+        memcpy(words, tmp, sizeof(uint32_t) * W * n);
+    }
+    free(tmp);
+    return 0;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -116,5 +116,13 @@ int oracle_step_sampled_f64(const oracle_sim* sim, const oracle_scheme* s, uint6
 /* run n_steps full steps (fp64), words in/out may alias */
 int oracle_run_f64(const oracle_sim* sim, const oracle_scheme* s, uint64_t n, uint32_t* words,
                    uint64_t first_step, uint32_t n_steps, uint64_t* counters);
+/* the same step / run with the particle and node loops on n_threads OpenMP threads
+ * (<= 0: all); P2G sums ordered by 4-cell x slab (deterministic, thread-count free) */
+int oracle_step_omp_f64(const oracle_sim* sim, const oracle_scheme* s, uint64_t n, const uint32_t* words_in,
+                        uint64_t step, double* pre_encode, uint32_t* words_out, uint64_t* counters,
+                        int n_threads);
+int oracle_run_omp_f64(const oracle_sim* sim, const oracle_scheme* s, uint64_t n, uint32_t* words,
+                       uint64_t first_step, uint32_t n_steps, uint64_t* counters, int n_threads);
+int oracle_num_threads(void);
 
 #endif

@@ -57,27 +57,40 @@ def solve_error_bounded(P, g, R, z, eps, b_min=0, b_max=31):
 
 
 def solve_memory_bounded(P, g, R, budget_bits, b_min=0, b_max=31):
-    """Eq. 7 with the stationarity solution of S:342.  Quantities with g_h = 0 take
-    b_min and leave the rest of the budget to the others.  Returns (Delta_h, b_h);
-    raises ValueError when even b_min everywhere exceeds the budget."""
+    """Eq. 7 with the stationarity solution of S:342 over the box [b_min, b_max]:
+    quantities with g_h = 0 take b_min; the closed form is solved over the free
+    quantities with the budget the fixed ones leave, and a free quantity whose floored
+    width leaves the box is fixed at the bound and the rest re-solved (active set).
+    Returns (Delta_h, b_h); raises ValueError when no scheme in the box fits."""
     P = np.asarray(P, np.float64)
     g = np.asarray(g, np.float64)
     R = np.asarray(R, np.float64)
     H = len(P)
     if np.sum(P * b_min) > budget_bits:
         raise ValueError("budget below b_min everywhere")
-    act = g > 0.0
-    B = budget_bits - np.sum(P[~act] * b_min)
     delta = np.full(H, np.inf)
     bits = np.full(H, b_min, np.int64)
-    if act.any():
-        Pa, ga, Ra = P[act], g[act], R[act]
+    fixed = ~(g > 0.0)
+    for _ in range(H + 1):
+        free = ~fixed
+        if not free.any():
+            break
+        B = budget_bits - np.sum(P[fixed] * bits[fixed])
+        Pa, ga, Ra = P[free], g[free], R[free]
         log2c = (np.sum(Pa * (np.log2(Ra) - 0.5 * np.log2(Pa / ga))) - B) / np.sum(Pa)
-        da = 2.0 ** log2c * np.sqrt(Pa / ga)
-        delta[act] = da
-        bits[act] = [min(max(int(np.floor(-np.log2(d / r))), b_min), b_max) for d, r in zip(da, Ra)]
-    if np.sum(P * bits) > budget_bits:
-        raise ValueError("b_min clamps exceed the budget")
+        changed = False
+        for h in np.nonzero(free)[0]:
+            d = 2.0 ** log2c * np.sqrt(P[h] / g[h])
+            b = np.floor(-np.log2(d / R[h]))
+            delta[h] = d
+            bits[h] = min(max(int(b), b_min), b_max)
+            if b < b_min or b > b_max:
+                fixed[h] = True
+                changed = True
+        if not changed:
+            break
+    if np.sum(P * bits) > budget_bits * (1.0 + 1e-12):
+        raise ValueError("no scheme within [b_min, b_max] fits the budget")
     return delta, bits
 
 

@@ -920,7 +920,14 @@ void coop_sizes(qadj_ctx* c, int sms) {
   c->coop_adj = (unsigned)std::min<uint64_t>((uint64_t)ba * sms, need);
 }
 
-qmpm_status get_buf(qadj_ctx* c, std::vector<float*>& freel, float** out) {
+// a state-sized device buffer: from the free list, else a new pool buffer (kept by the ctx
+// and handed to the next call's free list); `inuse` / `peak` count the call's buffers
+qmpm_status get_buf(qadj_ctx* c, std::vector<float*>& freel, float** out, uint32_t* inuse = nullptr,
+                    uint32_t* peak = nullptr) {
+  if (inuse) {
+    ++*inuse;
+    if (peak && *inuse > *peak) *peak = *inuse;
+  }
   if (!freel.empty()) {
     *out = freel.back();
     freel.pop_back();
@@ -940,20 +947,27 @@ struct Bisect {
   qadj_ctx* c;
   std::vector<float*> freel;
   uint32_t resident = 0, max_resident = 0;
+  uint32_t inuse = 0, peak = 0;  // state-sized buffers in use (checkpoints, adjoints, scratch)
   uint64_t fwd = 0, adj = 0;
+
+  qmpm_status get(float** out) { return get_buf(c, freel, out, &inuse, &peak); }
+  void put(float* b) {
+    freel.push_back(b);
+    --inuse;
+  }
 
   // state at `to` from the state at `from` (k >= 1 steps) into a fresh buffer
   qmpm_status advance(const float* s, uint32_t k, float** out) {
     float *a = nullptr, *b = nullptr;
-    qmpm_status rc = get_buf(c, freel, &a);
-    if (!rc) rc = get_buf(c, freel, &b);
+    qmpm_status rc = get(&a);
+    if (!rc) rc = get(&b);
     if (rc) return rc;
     rc = forward_chain_dev(c, s, a, b, k);
     if (rc) return rc;
     fwd += k;
     float* last = ((k - 1) % 2 == 0) ? a : b;
     *out = last;
-    freel.push_back(last == a ? b : a);
+    put(last == a ? b : a);
     return QMPM_OK;
   }
 
@@ -969,12 +983,12 @@ struct Bisect {
     if (rc) return rc;
     max_resident = std::max(max_resident, ++resident + 1);  // + s0
     float* lam_mid = nullptr;
-    rc = get_buf(c, freel, &lam_mid);
+    rc = get(&lam_mid);
     if (!rc) rc = back(mid, hi, s_mid, lam_hi, lam_mid, g);
-    freel.push_back(s_mid);
+    put(s_mid);
     --resident;
     if (!rc) rc = back(lo, mid, s_lo, lam_mid, lam_out, g);
-    freel.push_back(lam_mid);
+    put(lam_mid);
     return rc;
   }
 };
@@ -1073,8 +1087,9 @@ qmpm_status qadj_gradient_tally(qadj_ctx* c, const float* s0, uint32_t T, double
   if (!c || !s0 || !g) return afail(QMPM_EINVAL, "NULL argument");
   const size_t bytes = sizeof(float) * c->n * c->ns;
   Bisect B{c};
+  B.freel = c->pool;  // every pool buffer is free between calls: reuse them
   float *s_first = nullptr, *lamT = nullptr, *lam_out = nullptr;
-  qmpm_status rc = get_buf(c, B.freel, &s_first);
+  qmpm_status rc = B.get(&s_first);
   if (rc) return rc;
   ACK(cudaMemcpyAsync(s_first, s0, bytes, cudaMemcpyDefault, c->stream));
   ACK(cudaMemsetAsync(c->dacc, 0, sizeof(double) * (c->ns + 1), c->stream));
@@ -1086,7 +1101,7 @@ qmpm_status qadj_gradient_tally(qadj_ctx* c, const float* s0, uint32_t T, double
     if (rc) return rc;
     B.max_resident = 2;
   }
-  rc = get_buf(c, B.freel, &lamT);
+  rc = B.get(&lamT);
   if (rc) return rc;
   if (c->dim == 3 && c->el)
     k_lambda_T<3, true><<<blocks(c->n), 256, 0, c->stream>>>(sT, c->n, c->S, lamT, c->dacc, c->dacc + c->ns);
@@ -1098,10 +1113,10 @@ qmpm_status qadj_gradient_tally(qadj_ctx* c, const float* s0, uint32_t T, double
     k_lambda_T<2, false><<<blocks(c->n), 256, 0, c->stream>>>(sT, c->n, c->S, lamT, c->dacc, c->dacc + c->ns);
   c->launches += 1;
   ACK(cudaGetLastError());
-  if (T > 0) B.freel.push_back(sT);
+  if (T > 0) B.put(sT);
   float* lam_final = lamT;
   if (T > 0) {
-    rc = get_buf(c, B.freel, &lam_out);
+    rc = B.get(&lam_out);
     if (rc) return rc;
     rc = B.back(0, T, s_first, lamT, lam_out, c->dacc);
     if (rc) return rc;
@@ -1115,6 +1130,7 @@ qmpm_status qadj_gradient_tally(qadj_ctx* c, const float* s0, uint32_t T, double
   if (z) *z = h[c->ns];
   if (stats) {
     stats->max_resident = B.max_resident;
+    stats->peak_buffers = B.peak;
     stats->forward_steps = B.fwd;
     stats->adjoint_steps = B.adj;
   }

@@ -381,7 +381,7 @@ int qmpm_abi_version(void) { return QMPM_ABI_VERSION; }
 const char* qmpm_last_error(const qmpm_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
 
 const char* qmpm_kernel_name(int i) {
-  static const char* names[KNumKernels] = {"bin_count", "scan_reduce", "scan_tiles", "scan_apply",
+  static const char* names[KNumKernels] = {"bin_count", "scan_reduce", "scan_tiles",  "scan_apply", "cell_scan",
                                            "bin_scatter", "p2g",       "grid_update", "g2p"};
   return (i >= 0 && i < KNumKernels) ? names[i] : "";
 }

@@ -226,6 +226,16 @@ __device__ __forceinline__ uint32_t senc_fast(const int i, float v, float omr, b
 constexpr float kFloorMagic = 12582912.0f;  // 1.5 2^23
 constexpr int kFloorMagicBits = 0x4b400000;
 
+// -1 when the sign bit of d is set, else 0.  Kept as an opaque shr.s32: ptxas 12.9 fuses
+// `(bits(d) >> 31) + bits(s)` with the later mask-and-shift of the bit pack into a LEA.HI
+// sequence that drops the mask on the first lane of a pair (wrong words; reproduced by
+// tools/pair_probe.py, measured on B200)
+__device__ __forceinline__ int sign_mask(float d) {
+  int r;
+  asm("shr.s32 %0, %1, 31;" : "=r"(r) : "r"(__float_as_int(d)));
+  return r;
+}
+
 template <class SP>
 __host__ __device__ constexpr bool fast_ok(int i) {
   return SP::DITHER && SP::kind(i) == kKindFixed && SP::width(i) <= 23;
@@ -251,8 +261,8 @@ __device__ __forceinline__ void senc_pair_fast(const int i, const int j, const f
   const float2 f = __fadd2_rn(s, make_float2(-kFloorMagic, -kFloorMagic));
   const float2 y = __ffma2_rn(f, make_float2(-1.0f, -1.0f), t);
   const float2 d = __fadd2_rn(y, __fadd2_rn(make_float2(si, sj), make_float2(-2.0f, -2.0f)));
-  sbi = __float_as_int(d.x) >> 31;
-  sbj = __float_as_int(d.y) >> 31;
+  sbi = sign_mask(d.x);
+  sbj = sign_mask(d.y);
   ui = __float_as_int(s.x) - (kFloorMagicBits - 1) + sbi;
   uj = __float_as_int(s.y) - (kFloorMagicBits - 1) + sbj;
   flag |= !(fabsf(t.x) < enc_lim(SP::width(i))) || !(fabsf(t.y) < enc_lim(SP::width(j)));
@@ -267,7 +277,7 @@ __device__ __forceinline__ int senc1_fast(const int i, const float v, const floa
   const float s = __fadd_rd(t, kFloorMagic);
   const float y = __fsub_rn(t, __fsub_rn(s, kFloorMagic));
   const float d = __fadd_rn(y, __fsub_rn(si, 2.0f));
-  sb = __float_as_int(d) >> 31;
+  sb = sign_mask(d);
   flag |= !(fabsf(t) < enc_lim(SP::width(i)));
   zero |= y == 0.0f;
   return __float_as_int(s) - (kFloorMagicBits - 1) + sb;

@@ -408,8 +408,10 @@ static cudaError_t sort_d(const StepBuffers& B, const SimDev& S, cudaStream_t st
                                                      B.active_list, B.touched_list, B.pool);
   H(KScanApply, 0);
   if (B.n) {
-    H(KBinScatter, 1);
+    H(KCellScan, 1);
     k_cell_scan<<<B.num_sms * 8, 256, 0, st>>>(B.cell_count, B.block_count, B.block_start, B.active_list, B.dc);
+    H(KCellScan, 0);
+    H(KBinScatter, 1);
     k_bin_scatter<<<(B.n + 256 * kBinItems - 1) / (256 * kBinItems), 256, 0, st>>>(B.key, B.n, B.cell_count,
                                                                                   B.perm);
     H(KBinScatter, 0);

@@ -44,6 +44,7 @@ enum KernelId {
   KScanReduce,
   KScanTiles,
   KScanApply,
+  KCellScan,
   KBinScatter,
   KP2G,
   KGridUpdate,

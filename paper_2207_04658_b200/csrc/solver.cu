@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <vector>
 
 #include "qmpm.h"
 
@@ -72,6 +73,16 @@ qmpm_status qmpm_solve_error_bounded(uint32_t H, const double* P, const double* 
     delta_out[h] = d;
     bits_out[h] = clampi(std::ceil(-std::log2(d / R[h])), b_min, b_max);
   }
+  // the b_max clamp can leave sigma_pred above eps |z|: report it (outputs stay filled)
+  double e = 0.0;
+  for (uint32_t h = 0; h < H; ++h) {
+    const double dq = std::ldexp(R[h], -bits_out[h]);
+    e += dq * dq * g[h];
+  }
+  if (std::sqrt(e / 12.0) > std::fabs(eps_err * z) * (1.0 + 1e-12)) {
+    qmpm::set_thread_error("solve_error_bounded: the error bound cannot be met with b <= b_max");
+    return QMPM_EDOMAIN;
+  }
   return QMPM_OK;
 }
 
@@ -81,32 +92,48 @@ qmpm_status qmpm_solve_memory_bounded(uint32_t H, const double* P, const double*
   qmpm_status rc = check(H, P, g, R, b_min, b_max);
   if (rc) return rc;
   if (!delta_out || !bits_out) return bad("solve_memory_bounded: NULL output");
-  double floor_bits = 0.0, sum_pa = 0.0, acc = 0.0;
+  double floor_bits = 0.0;
   for (uint32_t h = 0; h < H; ++h) floor_bits += P[h] * b_min;
   if (floor_bits > budget_bits) return bad("solve_memory_bounded: budget below b_min for every quantity");
-  double B = budget_bits;
+  // Active set over the box [b_min, b_max]: quantities with g_h = 0 take b_min; the
+  // stationarity solution is computed over the free quantities with the budget
+  // the fixed ones leave; a free quantity whose floored width leaves the box is fixed at
+  // the bound and the rest re-solved, until no width leaves the box.
+  std::vector<int> state(H, 0);  // 0 free, 1 fixed at its bits_out
   for (uint32_t h = 0; h < H; ++h) {
-    if (g[h] == 0.0) {
-      B -= P[h] * b_min;  // leaves the rest of the budget to the others
-    } else {
-      sum_pa += P[h];
-      acc += P[h] * (std::log2(R[h]) - 0.5 * std::log2(P[h] / g[h]));
-    }
+    delta_out[h] = INFINITY;
+    bits_out[h] = b_min;
+    if (g[h] == 0.0) state[h] = 1;
   }
-  const double log2c = sum_pa > 0.0 ? (acc - B) / sum_pa : 0.0;
-  double used = 0.0;
-  for (uint32_t h = 0; h < H; ++h) {
-    if (g[h] == 0.0) {
-      delta_out[h] = INFINITY;
-      bits_out[h] = b_min;
-    } else {
+  for (uint32_t iter = 0; iter <= H; ++iter) {
+    double B = budget_bits, sum_pa = 0.0, acc = 0.0;
+    for (uint32_t h = 0; h < H; ++h) {
+      if (state[h]) {
+        B -= P[h] * bits_out[h];
+      } else {
+        sum_pa += P[h];
+        acc += P[h] * (std::log2(R[h]) - 0.5 * std::log2(P[h] / g[h]));
+      }
+    }
+    if (sum_pa == 0.0) break;
+    const double log2c = (acc - B) / sum_pa;
+    bool changed = false;
+    for (uint32_t h = 0; h < H; ++h) {
+      if (state[h]) continue;
       const double d = std::exp2(log2c) * std::sqrt(P[h] / g[h]);
+      const double b = std::floor(-std::log2(d / R[h]));
       delta_out[h] = d;
-      bits_out[h] = clampi(std::floor(-std::log2(d / R[h])), b_min, b_max);
+      bits_out[h] = clampi(b, b_min, b_max);
+      if (!(b >= b_min) || b > b_max) {
+        state[h] = 1;
+        changed = true;
+      }
     }
-    used += P[h] * bits_out[h];
+    if (!changed) break;
   }
-  if (used > budget_bits) return bad("solve_memory_bounded: b_min clamps exceed the budget");
+  double used = 0.0;
+  for (uint32_t h = 0; h < H; ++h) used += P[h] * bits_out[h];
+  if (used > budget_bits * (1.0 + 1e-12)) return bad("solve_memory_bounded: no scheme within [b_min, b_max] fits");
   return QMPM_OK;
 }
 

@@ -38,6 +38,26 @@ def rank_zrange(cuts, rank, dx):
     return z0 * dx, z1 * dx
 
 
+def rank_count_bound(scene, cuts, rank):
+    """Upper bound on the particles rank `rank` receives from load_slab (the lattice
+    planes within 0.3 spacings of its z range: Scene.zrange_runs, a superset of the
+    jittered positions) -- host arithmetic on the lattice only, no particle is generated."""
+    z_lo, z_hi = rank_zrange(cuts, rank, scene.sim["dx"])
+    if rank == len(cuts) - 1:
+        z_hi = float("inf")
+    if rank == 0:
+        z_lo = float("-inf")
+    return sum(c for _, c in scene.zrange_runs(z_lo, z_hi))
+
+
+def slab_capacity(scene, cuts, rank, headroom=0.25, extra=65536):
+    """max_particles of a rank's slab context: its initial count bound plus room for the
+    particles that migrate in (the bench's sizing; tests/test_dist_host.py checks it
+    against the per-rank bounds of C4 at 2, 4 and 8 ranks)."""
+    per = scene.n_particles / len(cuts)
+    return int(max(per, rank_count_bound(scene, cuts, rank)) * (1.0 + headroom)) + extra
+
+
 def share_unique_id(uid_fn, group=None):
     """Rank 0 creates an id with uid_fn(); every rank returns it (torch.distributed)."""
     import torch.distributed as dist

@@ -14,7 +14,7 @@ EXPORTS = ["qadj_create", "qadj_destroy", "qadj_forward", "qadj_adjoint_step", "
 
 
 class Stats(ctypes.Structure):
-    _fields_ = [("max_resident", ctypes.c_uint32), ("pad", ctypes.c_uint32), ("forward_steps", ctypes.c_uint64),
+    _fields_ = [("max_resident", ctypes.c_uint32), ("peak_buffers", ctypes.c_uint32), ("forward_steps", ctypes.c_uint64),
                 ("adjoint_steps", ctypes.c_uint64)]
 
 
@@ -82,7 +82,8 @@ class Adjoint:
         st = Stats()
         _check(lib().qadj_gradient_tally(self.ctx, ptr(s0), T, g.ctypes.data, ctypes.byref(z), ptr(lam0),
                                          ctypes.byref(st)))
-        return g, z.value, {"max_resident": st.max_resident, "forward_steps": st.forward_steps,
+        return g, z.value, {"max_resident": st.max_resident, "peak_buffers": st.peak_buffers,
+                            "forward_steps": st.forward_steps,
                             "adjoint_steps": st.adjoint_steps}
 
     def launch_count(self):

@@ -16,12 +16,13 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "libqmpm.so")
 
 MAX_FIELDS = 64
-NUM_KERNELS = 8
+NUM_KERNELS = 9
 ATTR = {"x": 0, "v": 1, "F": 2, "C": 3, "J": 4}
 KIND = {"fixed": 0, "raw": 1, "shared_exp": 2}
 MATERIAL = {"elastic": 0, "fluid": 1}
 ROUNDING = {"rne": 0, "dither": 1}
 TRACK_IDS, DEBUG_PREENCODE, NO_ROUND_COUNTERS, RECORD_RANGES = 1, 2, 4, 8
+EDOMAIN = 7
 STATUS = {0: "OK", 1: "EINVAL", 2: "ELAYOUT", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ENONFINITE",
           7: "EDOMAIN", 8: "ECAPACITY", 9: "ESTATE"}
 
@@ -235,13 +236,17 @@ def predict_error(delta, g) -> float:
     return out.value
 
 
-def solve_error_bounded(P, g, R, z, eps, b_min=0, b_max=31):
-    """qmpm_solve_error_bounded (Eq. 9 + Algorithm 1): returns (delta_h, bits_h)."""
+def solve_error_bounded(P, g, R, z, eps, b_min=0, b_max=31, strict=True):
+    """qmpm_solve_error_bounded (Eq. 9 + Algorithm 1): returns (delta_h, bits_h).  When the
+    b_max clamp cannot meet the bound (QMPM_EDOMAIN) it raises, or with strict=False
+    returns the clamped scheme."""
     P, g, R = _f64(P), _f64(g), _f64(R)
     d = np.zeros(len(P))
     b = np.zeros(len(P), np.int32)
-    _check(lib().qmpm_solve_error_bounded(len(P), P.ctypes.data, g.ctypes.data, R.ctypes.data, float(z), float(eps),
-                                          int(b_min), int(b_max), d.ctypes.data, b.ctypes.data))
+    rc = lib().qmpm_solve_error_bounded(len(P), P.ctypes.data, g.ctypes.data, R.ctypes.data, float(z), float(eps),
+                                        int(b_min), int(b_max), d.ctypes.data, b.ctypes.data)
+    if not (rc == EDOMAIN and not strict):
+        _check(rc)
     return d, b
 
 

@@ -52,6 +52,10 @@ class Box:
     spacing: float
     velocity: tuple
     n: int = -1  # particles taken in lattice order (-1 = all)
+    # a smooth per-particle flow added to `velocity` (developed-state parity scenes):
+    # swirl * sin(2 pi (x_{a+1} - o_{a+1}) / L_{a+1}) on axis a, minus conv * (x_a - centre_a)
+    swirl: float = 0.0
+    conv: float = 0.0
 
     def size(self):
         full = int(np.prod(self.counts))
@@ -111,7 +115,17 @@ class Scene:
                         pos = b.origin[a] + (idx[a].to(xp.float64) + 0.5 + jit) * b.spacing
                     xs.append(pos)
                 out_x.append(xs)
-                out_v.append((hi - lo, b.velocity))
+                if b.swirl or b.conv:
+                    L = [b.counts[a] * b.spacing for a in range(d)]
+                    vel = []
+                    for a in range(d):
+                        nb_ = (a + 1) % d
+                        ph = (xs[nb_] - b.origin[nb_]) * (2.0 * math.pi / L[nb_])
+                        sw = np.sin(ph) if xp is np else xp.sin(ph)
+                        vel.append(b.velocity[a] + b.swirl * sw - b.conv * (xs[a] - (b.origin[a] + 0.5 * L[a])))
+                    out_v.append((hi - lo, vel))
+                else:
+                    out_v.append((hi - lo, b.velocity))
             first += nb
         ns = self.n_scalars
         if xp is np:
@@ -122,7 +136,10 @@ class Scene:
         for xs, (m, vel) in zip(out_x, out_v):
             for a in range(d):
                 st[row:row + m, a] = xs[a].astype(np.float32) if xp is np else xs[a].to(xp.float32)
-                st[row:row + m, d + a] = float(np.float32(vel[a]))
+                if isinstance(vel[a], float):
+                    st[row:row + m, d + a] = float(np.float32(vel[a]))
+                else:
+                    st[row:row + m, d + a] = vel[a].astype(np.float32) if xp is np else vel[a].to(xp.float32)
             row += m
         if self.material == "fluid":
             st[:, 2 * d] = 1.0
@@ -312,6 +329,34 @@ def small_fluid_3d(seed=0, res=64, n_target=60_000):
     sc = c4(seed, n_target=n_target, res=res, dt=2e-4, E=50.0)
     sc.name = "S4"
     return sc
+
+
+def developed_fluid(seed=0, res=64, cells=(14, 12, 14), ppc_axis=4.1, swirl=1.5, conv=6.0, dt=2e-4, E=100.0):
+    """High-density fluid block for developed-state parity (SURVEY §8(c) P2 at C4 density):
+    `ppc_axis`^3 particles per cell (C4 has ~4.2^3 = 72 ppc), a smooth swirling and
+    converging initial flow (|v| ~ 1-2 m/s) so that after ~100 steps the block holds
+    compression (J != 1), pressure and shear (C != 0) -- the P2G's full per-cell segments
+    (16 particles) then carry non-trivial momentum and stress."""
+    dx = 1.0 / res
+    spacing = dx / ppc_axis
+    counts = tuple(int(round(c * ppc_axis)) for c in cells)
+    origin = (0.25, 0.12, 0.25)
+    box = Box(origin, counts, spacing, (0.3, -0.2, 0.1), -1, swirl, conv)
+    sim = _sim(3, "fluid", (res,) * 3, dt, E, spacing ** 3)
+    return Scene("DF", 3, "fluid", sim, [box], seed)
+
+
+def colliding_elastic(seed=0, res=64, cube=14, v=1.5, dt=2e-4, E=25.0):
+    """Two elastic cubes at 8 ppc (C3's density) driven into each other at +-v with a
+    swirl, for developed-state parity: after ~100 steps they are in contact with F far
+    from I."""
+    dx = 1.0 / res
+    spacing = dx / 2
+    c = (cube,) * 3
+    boxes = [Box((0.26, 0.30, 0.30), c, spacing, (v, 0.0, 0.2), -1, 0.5, 0.0),
+             Box((0.26 + cube * spacing + 2.5 * dx, 0.31, 0.305), c, spacing, (-v, 0.1, -0.2), -1, 0.5, 0.0)]
+    sim = _sim(3, "elastic", (res,) * 3, dt, E, spacing ** 3)
+    return Scene("CE", 3, "elastic", sim, boxes, seed)
 
 
 BY_NAME = {"c1": c1, "c2": c2, "c3": c3, "c4": c4}

@@ -1,7 +1,12 @@
 import os
 import sys
 
-import pytest
+# the OpenMP oracle shares torch's libgomp in these processes; with libgomp's default
+# active wait its threads contend with torch's pool (10x slower).  Read at libgomp init,
+# so it is set before anything imports torch.
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
+
+import pytest  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:

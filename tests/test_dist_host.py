@@ -71,3 +71,22 @@ def test_two_rank_generation_partitions_the_scene():
         assert p.exitcode == 0
     total, exact, n = res
     assert total == n and exact
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c4_slab_capacities_hold_every_rank(world):
+    """bench.py sizes each rank's context (and its e2e host buffer) with
+    dist.slab_capacity: for the weak-scaling C4 scene at 2/4/8 ranks the capacity must
+    hold the rank's initial particles (upper bound from the lattice planes) with room for
+    migration, although interior ranks hold MORE than n / world (the water block starts
+    3 cells above the floor and ends 3 cells below the top of the z range)."""
+    sc = scenes.c4(n_target=400_000_000 * world, z_extent=float(world))
+    cuts = qdist.slab_cuts(sc.sim["grid_res"][2], world)
+    bounds = [qdist.rank_count_bound(sc, cuts, r) for r in range(world)]
+    assert sum(bounds) >= sc.n_particles
+    per = sc.n_particles / world
+    assert max(bounds) > per  # the round-1 sizing (n / world) was too small
+    for r in range(world):
+        cap = qdist.slab_capacity(sc, cuts, r)
+        assert cap >= 1.2 * bounds[r], (r, cap, bounds[r])
+        assert cap < 2 ** 32 - 1

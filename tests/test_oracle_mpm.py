@@ -436,3 +436,25 @@ def test_dither_keys_are_content_keyed():
     assert np.array_equal(a[perm], b)
     # (the up/down counters may differ: a value ~1e-17 either side of a grid point
     #  rounds to the same code via "down" or "up" depending on fp64 sum order)
+
+
+@pytest.mark.parametrize("mk", [scenes.small_elastic_3d, scenes.small_fluid_3d])
+def test_openmp_oracle_equals_serial(mk):
+    """The OpenMP oracle (SURVEY §8(d) M7 ii) runs the same arithmetic with a different
+    P2G summation order (4-cell x slabs): fp64 results agree to round-off, the words are
+    identical but for rounding-boundary ties, and the result does not depend on the
+    thread count."""
+    sc = mk()
+    sch = schemes.f2() if sc.material == "fluid" else schemes.e01()
+    w, _ = oracle.encode_state(sch, sc.state())
+    w, _ = oracle.run(sc.sim, sch, w, 1, 3)
+    p1, w1, c1 = oracle.step(sc.sim, sch, w, 4)
+    p8, w8, c8 = oracle.step(sc.sim, sch, w, 4, threads=8)
+    p2, w2, c2 = oracle.step(sc.sim, sch, w, 4, threads=2)
+    scale = np.maximum(np.abs(p1).max(axis=0), 1e-12)
+    assert np.max(np.abs(p8 - p1) / scale) < 1e-8  # (C is a cancelling sum: round-off ~ 4/dx |v| eps)
+    assert np.mean(np.any(w8 != w1, axis=1)) < 1e-3
+    assert np.array_equal(p8, p2) and np.array_equal(w8, w2) and np.array_equal(c8, c2)
+    wr, _ = oracle.run(sc.sim, sch, w, 4, 3, threads=4)
+    wr2, _ = oracle.run(sc.sim, sch, w, 4, 3, threads=3)
+    assert np.array_equal(wr, wr2)

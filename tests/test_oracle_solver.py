@@ -122,3 +122,30 @@ def test_memory_bounded_meets_budget_and_is_near_optimal(seed):
 def test_memory_bounded_infeasible_budget():
     with pytest.raises(ValueError):
         solver.solve_memory_bounded([10.0, 10.0], [1.0, 1.0], [1.0, 1.0], 30.0, b_min=2)
+
+
+def test_memory_bounded_active_set_refits_clamped_widths():
+    """A type the closed form puts below b_min is fixed there and the others re-solved with
+    the budget it leaves: P = (1, 1), g = (1e-12, 1), R = 1, B = 10, b_min = 3
+    -> the first type takes 3, the second the remaining 7 (the one-shot form gave the
+    second 16 bits and broke the budget)."""
+    d, b = solver.solve_memory_bounded([1.0, 1.0], [1e-12, 1.0], [1.0, 1.0], 10.0, b_min=3)
+    assert list(b) == [3, 7] and np.dot([1.0, 1.0], b) <= 10.0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_memory_bounded_with_clamps_near_optimal(seed):
+    """Gradients over 11 orders of magnitude force widths onto both box bounds; the
+    active-set scheme meets the budget and stays within 4x of the exhaustive optimum's
+    predicted error."""
+    rng = np.random.default_rng(300 + seed)
+    H = 3
+    P = rng.integers(1, 8, H).astype(np.float64)
+    g = 10.0 ** rng.uniform(-8, 3, H)
+    R = 2.0 ** rng.integers(-1, 4, H)
+    B = float(rng.integers(10, 40)) * P.mean()
+    d, b = solver.solve_memory_bounded(P, g, R, B, b_min=0, b_max=12)
+    assert np.dot(P, b) <= B and b.min() >= 0 and b.max() <= 12
+    err = solver.predict_error(solver.bits_to_delta(b, R), g)
+    best, _ = solver.brute_force_memory_bounded(P, g, R, B, b_max=12)
+    assert err <= 4.0 * best * (1 + 1e-12)

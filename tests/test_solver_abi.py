@@ -50,3 +50,20 @@ def test_solver_rejects_bad_input():
         qmpm.solve_memory_bounded([10.0, 10.0], [1.0, 1.0], [1.0, 1.0], 30.0, b_min=2)  # infeasible
     with pytest.raises(qmpm.QmpmError):
         qmpm.solve_error_bounded([1.0], [-1.0], [1.0], 1.0, 0.1)  # g < 0
+
+
+def test_error_bounded_reports_an_unmet_bound():
+    """With b_max too small for eps the library returns QMPM_EDOMAIN (the clamped scheme
+    still filled: strict=False) instead of silently missing the bound."""
+    P, g, R = [100.0, 100.0], [50.0, 2.0], [4.0, 4.0]
+    with pytest.raises(qmpm.QmpmError):
+        qmpm.solve_error_bounded(P, g, R, 1.0, 1e-4, b_min=0, b_max=6)
+    d, b = qmpm.solve_error_bounded(P, g, R, 1.0, 1e-4, b_min=0, b_max=6, strict=False)
+    assert list(b) == [6, 6]
+    d, b = qmpm.solve_error_bounded(P, g, R, 1.0, 1e-4, b_min=0, b_max=30)
+    assert qmpm.predict_error(osol.bits_to_delta(b, R), g) <= 1e-4
+
+
+def test_memory_bounded_refits_clamped_widths():
+    d, b = qmpm.solve_memory_bounded([1.0, 1.0], [1e-12, 1.0], [1.0, 1.0], 10.0, b_min=3)
+    assert list(b) == [3, 7]
