@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="qmpm", choices=["qmpm", "reference"])
-    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c4_8ppc"],
+                    help="c4_8ppc: C4's 400M particles on 512^3 cells per GPU (~8 ppc, dt 5e-5; SURVEY Q16)")
     ap.add_argument("--scheme", default=None, help="x16 | e0.1 | e0.01 | f2 | fp32")
     ap.add_argument("--n", type=int, default=0, help="override particle count (reduced runs)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
@@ -53,7 +54,9 @@ def parse():
                          "strong = 400M in total on the 256^3 domain, cut into N z slabs")
     ap.add_argument("--z-extent", type=float, default=1.0,
                     help="C4 only: z extent of the 1-GPU domain (reduced same-density runs for profiling)")
-    ap.add_argument("--scene-warmup", type=int, default=50)
+    ap.add_argument("--scene-warmup", type=int, default=None,
+                    help="untimed steps before the warm-up so the flow is developed (default: C4 2000 -- the dam "
+                         "has started to collapse -- C3 1000 -- the cubes collide --, C1/C2 100)")
     ap.add_argument("--rounding", default="dither", choices=["dither", "rne"])
     ap.add_argument("--layout", default="pack", choices=["pack", "nostraddle"],
                     help="bit pack (P:542-549) or no field straddling a word (the bit struct's rule, P:540)")
@@ -78,7 +81,11 @@ def make_scene(args, world=1):
         sch = schemes.e001()
     else:
         wx = world if args.scaling == "weak" else 1
-        sc = scenes.c4(n_target=(args.n or 400_000_000) * wx, z_extent=float(wx) * args.z_extent)
+        if args.config == "c4_8ppc":
+            sc = scenes.c4(n_target=(args.n or 400_000_000) * wx, res=512, dt=5e-5, z_extent=float(wx) * args.z_extent)
+            sc.name = "C4-8ppc"
+        else:
+            sc = scenes.c4(n_target=(args.n or 400_000_000) * wx, z_extent=float(wx) * args.z_extent)
         sch = schemes.f2()
     if args.scheme:
         sch = schemes.fp32(sc.dim, sc.material) if args.scheme == "fp32" else schemes.BY_NAME[args.scheme]()
@@ -87,7 +94,10 @@ def make_scene(args, world=1):
 
 
 def scheme_name(args):
-    return args.scheme or {"c1": "x16", "c2": "e0.1", "c3": "e0.01", "c4": "f2"}[args.config]
+    return args.scheme or {"c1": "x16", "c2": "e0.1", "c3": "e0.01", "c4": "f2", "c4_8ppc": "f2"}[args.config]
+
+
+DEFAULT_SCENE_WARMUP = {"c1": 100, "c2": 100, "c3": 1000, "c4": 2000, "c4_8ppc": 2000}
 
 
 def workload_name(args, sc, W, bits):
@@ -263,7 +273,8 @@ def run_gpu(args):
         cap = sim.params.max_particles  # this rank's context capacity (host buffers below)
 
         # ---------------- timed region (device): K steps, per-kernel events on the ctx stream
-        sim.set_profiling(True)
+        # (the step as the library runs it: one CUDA graph per step on a single GPU; the
+        # per-kernel event brackets of the roofline are taken in a second pass below)
         launches0 = sim.launch_count()
         if world > 1:
             dist.barrier()
@@ -280,9 +291,12 @@ def run_gpu(args):
         clk = clocks.stop()
         launches = sim.launch_count() - launches0
         ms = e0.elapsed_time(e1)
+        # ---------------- per-kernel device times (CUDA events around each launch, same stream)
+        sim.set_profiling(True)
+        sim.step(args.steps)
         ktimes = sim.kernel_times()
-        st = sim.stats()
         sim.set_profiling(False)
+        st = sim.stats()
         N = int(st.n_particles)  # this rank's particles (slabs: after migration)
         n_total = N
         if world > 1:
@@ -350,18 +364,32 @@ def run_gpu(args):
     kms, kcnt = ktimes[dom]
     avg_ms = kms / max(kcnt, 1)
     achieved = ab[dom](N) / (avg_ms / 1e3) / 1e9
-    traffic = None
+    # ncu `--set full` capture of this config's kernels (profiles/ncu_traffic.json, written
+    # by profiles/summarize_ncu.py --config): DRAM bytes and warp instructions per launch
+    traffic, winst = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and not args.n and args.scaling == "weak" and args.z_extent == 1.0:
         try:
-            traffic = _json.load(open(tpath)).get(dom)
+            rec = _json.load(open(tpath)).get(args.config, {}).get(dom, {})
+            traffic, winst = rec.get("traffic"), rec.get("warp_inst")
         except Exception:
-            traffic = None
+            traffic, winst = None, None
+    # issue-rate roofline: the step kernels are bound by the warp
+    # schedulers, not by bytes -- warp instructions per launch / (launch time x SMs x 4
+    # schedulers x SM clock under load)
+    issue_frac = None
+    if winst and clk and clk.get("sm_mhz"):
+        n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+        issue_frac = winst / (avg_ms * 1e-3 * n_sm * 4 * clk["sm_mhz"] * 1e6)
     step_ms = ms / args.steps
     B_alg = 2 * S + 56.0 * nodes / N  # SURVEY §8(d) M3 per particle-step
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": ab[dom](N), "avg_launch_ms": avg_ms}
+                "algorithmic_bytes_per_launch": ab[dom](N), "avg_launch_ms": avg_ms,
+                "issue_frac": issue_frac,
+                "issue_note": "warp instructions per launch (ncu, profiles/ncu_traffic.json, this config) / "
+                              "(avg launch time x SMs x 4 schedulers x median SM clock): the binding roofline "
+                              "of the issue-bound step kernels (SURVEY §8(d) M4)"}
     kshare = {k: {"ms_per_step": v[0] / max(v[1], 1) * (v[1] / args.steps), "launches": v[1]}
               for k, v in ktimes.items()}
 
@@ -415,6 +443,8 @@ def run_gpu(args):
 
 def main():
     args = parse()
+    if args.scene_warmup is None:
+        args.scene_warmup = DEFAULT_SCENE_WARMUP[args.config]
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -6,6 +6,7 @@
 // and the device counters.  Everything is enqueued on the ctx stream; qmpm_step
 // allocates nothing.
 #include <algorithm>
+#include <cstddef>
 #include <cmath>
 #include <cstdlib>
 #include <cstdarg>
@@ -73,15 +74,24 @@ struct qmpm_ctx {
   bool slab = false;
   int nranks = 1, rank = 0;
   uint64_t mig_cap = 0;
-  uint32_t* mig_send[2] = {nullptr, nullptr};  // [0] down, [1] up: records, W words each
-  uint32_t* mig_send_ids[2] = {nullptr, nullptr};
+  unsigned char* mig_buf[4] = {nullptr, nullptr, nullptr, nullptr};  // send down, send up, recv down, recv up
+  size_t mig_bytes = 0;      // one migration buffer: header + records (+ ids), exchanged whole
+  uint32_t* dead_list = nullptr;
+  uint32_t dead_cap = 0;
   float4* plane_send = nullptr;
   float4* plane_recv = nullptr;
   size_t plane_elems = 0;
-  uint32_t* d_cnt_recv = nullptr;  // device [2]: counts announced by the neighbour below / above
-  uint32_t* h_cnt = nullptr;       // pinned [8]: mig_dn, mig_up, mig_overflow, n_sorted, recv_dn, recv_up
+  cudaStream_t comm = nullptr;       // NCCL exchanges overlapping the interior P2G / G2P
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint32_t sticky = 0;               // device status seen by the last synchronising call
   NcclComm* nccl = nullptr;
+  // single GPU: the step as a CUDA graph per ping-pong parity (QMPM_NO_GRAPH=1: launches)
+  bool use_graphs = true;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
 };
+
+// kernels one single-GPU step launches (sort: 5, P2G, grid update, G2P)
+constexpr uint64_t kStepLaunches = 8;
 
 namespace qmpm {
 // the thread-local message qmpm_last_error(NULL) returns (used by solver.cu too)
@@ -283,12 +293,49 @@ qmpm_status copy_in(qmpm_ctx* ctx, void* dst, const void* src, size_t bytes) {
   return QMPM_OK;
 }
 
+MigDev mig_of(const qmpm_ctx* ctx) {
+  MigDev M{};
+  M.send[0] = ctx->mig_buf[0];
+  M.send[1] = ctx->mig_buf[1];
+  M.recv[0] = ctx->mig_buf[2];
+  M.recv[1] = ctx->mig_buf[3];
+  M.dead_list = ctx->dead_list;
+  M.cap = (uint32_t)ctx->mig_cap;
+  M.dead_cap = ctx->dead_cap;
+  M.W = ctx->W;
+  M.ids = ctx->ids[0] != nullptr;
+  M.dbg_ns = ctx->dbg ? (uint32_t)ctx->ns : 0u;
+  return M;
+}
+
+// the record slot counters of a freshly set state: n_rec = n_slots = n, nothing dead
+qmpm_status set_slot_counts(qmpm_ctx* ctx) {
+  // n_rec, n_slots, n_leave, status, gstep (the scan advances gstep to this step's number)
+  const uint32_t v[5] = {(uint32_t)ctx->n, (uint32_t)ctx->n, 0u, 0u, (uint32_t)ctx->step};
+  static_assert(offsetof(DevCounters, n_slots) == offsetof(DevCounters, n_rec) + 4, "layout");
+  static_assert(offsetof(DevCounters, n_leave) == offsetof(DevCounters, n_rec) + 8, "layout");
+  static_assert(offsetof(DevCounters, gstep) == offsetof(DevCounters, n_rec) + 16, "layout");
+  CK(cudaMemcpyAsync(&ctx->dc->n_rec, v, sizeof(v), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // (v is on the stack)
+  return QMPM_OK;
+}
+
+qmpm_status clear_send_headers(qmpm_ctx* ctx) {
+  for (int d = 0; d < 2; ++d) CK(cudaMemsetAsync(ctx->mig_buf[d], 0, sizeof(MigHeader), ctx->stream));
+  return QMPM_OK;
+}
+
+// keys and histograms of a freshly set state; a slab rank routes the records whose base
+// lies in a neighbour's slab into the send buffers (exchanged before the first sort)
 qmpm_status rebin(qmpm_ctx* ctx) {
+  qmpm_status rc = set_slot_counts(ctx);
+  if (rc) return rc;
   CK(cudaMemsetAsync(ctx->block_count, 0, sizeof(uint32_t) * ctx->S.nblocks, ctx->stream));
   CK(cudaMemsetAsync(ctx->cell_count, 0, sizeof(uint32_t) * 64 * (size_t)ctx->S.nblocks, ctx->stream));
+  if (ctx->slab && (rc = clear_send_headers(ctx))) return rc;
   hook_fn(ctx, KBinCount, 1);
-  CK(launch_bin_count(ctx->rec[ctx->cur], 0u, (uint32_t)ctx->n, ctx->S, ctx->key, ctx->block_count, ctx->cell_count,
-                      1, ctx->jit, ctx->stream));
+  CK(launch_bin_count(ctx->rec[ctx->cur], ctx->ids[ctx->cur], 0u, (uint32_t)ctx->n, ctx->S, ctx->key,
+                      ctx->block_count, ctx->cell_count, 1, mig_of(ctx), ctx->dc, ctx->jit, ctx->stream));
   hook_fn(ctx, KBinCount, 0);
   ctx->binned = true;
   return QMPM_OK;
@@ -296,6 +343,7 @@ qmpm_status rebin(qmpm_ctx* ctx) {
 
 qmpm_status reset_counters(qmpm_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->dc, 0, sizeof(DevCounters), ctx->stream));
+  ctx->sticky = 0;
   return QMPM_OK;
 }
 
@@ -410,11 +458,15 @@ qmpm_status qmpm_destroy(qmpm_ctx* ctx) {
                   ctx->tile_sums, ctx->tile_off, ctx->mp, ctx->gv, ctx->dc, ctx->dbg};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  void* sptrs[] = {ctx->mig_send[0], ctx->mig_send[1], ctx->mig_send_ids[0], ctx->mig_send_ids[1],
-                   ctx->plane_send, ctx->plane_recv, ctx->d_cnt_recv};
+  void* sptrs[] = {ctx->mig_buf[0], ctx->mig_buf[1], ctx->mig_buf[2], ctx->mig_buf[3], ctx->dead_list,
+                   ctx->plane_send, ctx->plane_recv};
   for (void* p : sptrs)
     if (p) cudaFree(p);
-  if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
+  for (auto e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto g : ctx->graph)
+    if (g) cudaGraphExecDestroy(g);
+  if (ctx->comm) cudaStreamDestroy(ctx->comm);
   if (ctx->nccl) nccl_destroy(ctx->nccl);
   for (auto& p : ctx->pending) {
     cudaEventDestroy(p.a);
@@ -425,7 +477,13 @@ qmpm_status qmpm_destroy(qmpm_ctx* ctx) {
   return QMPM_OK;
 }
 
-qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, void* cuda_stream, qmpm_ctx** out) {
+}  // extern "C"
+
+namespace {
+// qmpm_create, and qmpm_create_slab with `slab` set: the block table then covers the
+// rank's own block planes plus the ghost plane above (table-local block ids)
+qmpm_status create_impl(const qmpm_params* params, const qmpm_scheme* scheme, void* cuda_stream,
+                        const qmpm_slab* slab, qmpm_ctx** out) {
   qmpm_ctx* ctx = nullptr;
   if (!params || !scheme || !out) return fail(ctx, QMPM_EINVAL, "NULL argument to qmpm_create");
   *out = nullptr;
@@ -472,6 +530,10 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   ctx->seed = scheme->dither_seed;
   ctx->cap = P.max_particles;
   cudaGetDevice(&ctx->device);
+  {
+    const char* ng = getenv("QMPM_NO_GRAPH");
+    ctx->use_graphs = !(ng && *ng && *ng != '0');
+  }
 
   // MPM layout (fields by state scalar) and the state codec (vals in scalar order)
   LayoutDev& L = ctx->L;
@@ -513,9 +575,21 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   for (int a = 0; a < 3; ++a) {
     S.res[a] = a < d ? P.grid_res[a] : 1;
     S.nb[a] = a < d ? (P.grid_res[a] + B - 1) / B : 1;
-    nblocks *= (uint64_t)S.nb[a];
     S.g[a] = a < d ? P.gravity[a] : 0.0f;
   }
+  S.slab_bz0 = 0;
+  S.slab_bz1 = S.nb[2];
+  S.slab_lo = 0;
+  S.slab_hi = 0;
+  if (slab) {
+    S.slab_bz0 = slab->z0 / 4;
+    S.slab_bz1 = (slab->z1 + 3) / 4;
+    S.slab_lo = slab->rank > 0;
+    S.slab_hi = slab->rank + 1 < slab->nranks;
+  }
+  S.tab_bz0 = S.slab_bz0;
+  S.tab_bz1 = std::min(S.slab_bz1 + (S.slab_hi ? 1 : 0), S.nb[2]);
+  nblocks = (uint64_t)S.nb[0] * S.nb[1] * (uint64_t)(d == 3 ? S.tab_bz1 - S.tab_bz0 : 1);
   if (nblocks >= 0xffffffffull) {
     qmpm_destroy(ctx);
     return fail(nullptr, QMPM_EINVAL, "grid has too many blocks");
@@ -530,10 +604,8 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
   S.lambda = (float)((double)P.E * (double)P.nu / ((1.0 + (double)P.nu) * (1.0 - 2.0 * (double)P.nu)));
   S.E = P.E;
   S.bound = P.bound;
-  S.slab_bz0 = 0;
-  S.slab_bz1 = S.nb[2];
-  S.slab_lo = 0;
-  S.slab_hi = 0;
+  S.seed_lo = L.seed_lo;
+  S.seed_hi = L.seed_hi;
 
   ctx->ntiles = (uint32_t)((nblocks + kScanTile - 1) / kScanTile);
   ctx->pool = P.pool_blocks ? P.pool_blocks : std::min<uint64_t>(nblocks, 4096 + P.max_particles / 256);
@@ -608,6 +680,7 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
     J.bin_count = m.bin_count;
     J.p2g = m.p2g;
     J.g2p = m.g2p;
+    J.append = m.append;
     ctx->jit_regs_p2g = m.regs_p2g;
     ctx->jit_regs_g2p = m.regs_g2p;
     cudaDeviceGetAttribute(&J.num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
@@ -624,8 +697,43 @@ qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, vo
     J.p2g_ctas = (unsigned)(J.num_sms * jit_occupancy(J.p2g, (int)J.p2g_threads, J.p2g_smem));
     J.g2p_ctas = (unsigned)(J.num_sms * jit_occupancy(J.g2p, (int)J.g2p_threads, J.g2p_smem));
   }
+  if (slab) {
+    ctx->slab = true;
+    ctx->nranks = slab->nranks;
+    ctx->rank = slab->rank;
+    // steady state at C4: ~1.5M particles per cell plane, a few % cross a slab face per
+    // step; the first step may route up to half a plane (particles loaded by position)
+    ctx->mig_cap = slab->migrate_capacity ? slab->migrate_capacity
+                                          : std::max<uint64_t>(65536, std::min<uint64_t>(ctx->cap / 256, 1u << 22));
+    ctx->dead_cap = (uint32_t)std::min<uint64_t>(2 * ctx->mig_cap, 0xffffffffull);
+    ctx->mig_bytes = mig_bytes_of(mig_of(ctx));
+    ctx->plane_elems = (size_t)S.nb[0] * S.nb[1] * 64;
+    cudaError_t e2 = cudaSuccess;
+    for (int b = 0; b < 4 && !e2; ++b) e2 = cudaMalloc((void**)&ctx->mig_buf[b], ctx->mig_bytes);
+    if (!e2) e2 = cudaMalloc((void**)&ctx->dead_list, sizeof(uint32_t) * ctx->dead_cap);
+    if (!e2) e2 = cudaMalloc((void**)&ctx->plane_send, sizeof(float4) * ctx->plane_elems);
+    if (!e2) e2 = cudaMalloc((void**)&ctx->plane_recv, sizeof(float4) * ctx->plane_elems);
+    for (int b = 0; b < 4 && !e2; ++b) e2 = cudaMemsetAsync(ctx->mig_buf[b], 0, sizeof(MigHeader), ctx->stream);
+    if (!e2) e2 = cudaMemsetAsync(ctx->plane_recv, 0, sizeof(float4) * ctx->plane_elems, ctx->stream);
+    if (!e2) e2 = cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking);
+    for (int b = 0; b < 4 && !e2; ++b) e2 = cudaEventCreateWithFlags(&ctx->ev[b], cudaEventDisableTiming);
+    if (!e2) e2 = cudaStreamSynchronize(ctx->stream);
+    if (e2) {
+      cudaGetLastError();
+      qmpm_destroy(ctx);
+      return fail(nullptr, e2 == cudaErrorMemoryAllocation ? QMPM_ENOMEM : QMPM_ECUDA, "qmpm_create_slab: %s",
+                  cudaGetErrorString(e2));
+    }
+  }
   *out = ctx;
   return QMPM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+qmpm_status qmpm_create(const qmpm_params* params, const qmpm_scheme* scheme, void* cuda_stream, qmpm_ctx** out) {
+  return create_impl(params, scheme, cuda_stream, nullptr, out);
 }
 
 qmpm_status qmpm_set_state(qmpm_ctx* ctx, uint64_t n, const float* vals) {
@@ -643,7 +751,7 @@ qmpm_status qmpm_set_state(qmpm_ctx* ctx, uint64_t n, const float* vals) {
   if (rc) return rc;
   ctx->n = n;
   ctx->binned = false;
-  return QMPM_OK;
+  return set_slot_counts(ctx);
 }
 
 qmpm_status qmpm_append_state(qmpm_ctx* ctx, uint64_t n, const float* vals) {
@@ -655,7 +763,7 @@ qmpm_status qmpm_append_state(qmpm_ctx* ctx, uint64_t n, const float* vals) {
   ctx->n += n;
   ctx->binned = false;
   ctx->dbg_valid = false;
-  return QMPM_OK;
+  return set_slot_counts(ctx);
 }
 
 qmpm_status qmpm_set_words(qmpm_ctx* ctx, uint64_t n, const uint32_t* words, uint64_t step) {
@@ -677,7 +785,7 @@ qmpm_status qmpm_set_words(qmpm_ctx* ctx, uint64_t n, const uint32_t* words, uin
   ctx->step = step;
   ctx->binned = false;
   ctx->dbg_valid = false;
-  return QMPM_OK;
+  return set_slot_counts(ctx);
 }
 
 }  // extern "C"
@@ -711,10 +819,6 @@ StepBuffers buffers(qmpm_ctx* ctx, uint64_t n) {
   return B;
 }
 
-uint32_t salt_of(qmpm_ctx* ctx) {
-  return step_salt(ctx->L.seed_lo, ctx->L.seed_hi, (uint32_t)(ctx->step + 1));  // steps numbered 1, 2, ... (Q20)
-}
-
 void finish_step(qmpm_ctx* ctx) {
   ctx->cur ^= 1;
   ctx->step += 1;
@@ -722,113 +826,158 @@ void finish_step(qmpm_ctx* ctx) {
 }
 
 // ---------------------------------------------------------------- slab phases
-// A: sort pass 1 (all particles), pack the ones that left the slab, counts -> host
-qmpm_status slab_a(qmpm_ctx* ctx) {
-  if (!ctx->binned) {
-    qmpm_status rc = rebin(ctx);
-    if (rc) return rc;
-  }
-  StepBuffers B = buffers(ctx, ctx->n);
-  CK(launch_sort(ctx->dim, B, ctx->S, ctx->stream, hook_fn, ctx));
-  CK(launch_pack_leavers(B, ctx->S, ctx->W, (uint32_t)ctx->mig_cap, ctx->mig_send[0], ctx->mig_send[1],
-                         ctx->mig_send_ids[0], ctx->mig_send_ids[1], ctx->jit.num_sms, ctx->stream));
-  ctx->launches_total += 1;
-  CK(cudaMemcpyAsync(ctx->h_cnt, &ctx->dc->mig_dn, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
-  return QMPM_OK;
-}
+// One slab step, every size fixed so the exchange schedule never depends
+// on data and the host never waits for the device:
+//   sort                                   (slots [0, n_slots): owned + arrived particles)
+//   P2G top block plane -> pack ghost plane -> [ghost exchange, comm stream]
+//   P2G interior (overlaps the exchange) -> add the lower rank's ghost plane
+//   grid update -> pack bottom plane velocities -> [velocity exchange, comm stream]
+//   G2P interior (overlaps the exchange) -> store the upper rank's velocities -> G2P top
+//     (particles whose new base lies in a neighbour's slab are copied to a send buffer)
+//   [migration exchange + status all-reduce] -> append the arrivals (keys, histograms)
+// The first step after set_state / set_words routes the records loaded outside the slab
+// the same way (bin_count + migration) before its sort.
 
-// B: arrivals are in place at [n, n + arr): their keys, recount owned particles,
-// sort pass 2, P2G, pack the ghost plane for the rank above
-qmpm_status slab_b(qmpm_ctx* ctx, uint32_t arr) {
-  const uint32_t n_slots = (uint32_t)ctx->n + arr;
-  StepBuffers B = buffers(ctx, n_slots);
-  if (arr) {
-    ctx->launches_total += 1;
-    CK(launch_bin_count(ctx->rec[ctx->cur], (uint32_t)ctx->n, arr, ctx->S, ctx->key, ctx->block_count,
-                        ctx->cell_count, 0, ctx->jit, ctx->stream));
-  }
-  ctx->launches_total += 2;
-  CK(launch_recount(B, ctx->S, n_slots, ctx->jit.num_sms, ctx->stream));
-  CK(launch_sort(ctx->dim, B, ctx->S, ctx->stream, hook_fn, ctx));
-  CK(launch_p2g(B, ctx->S, ctx->jit, ctx->stream, hook_fn, ctx));
-  if (ctx->S.slab_hi) {
-    ctx->launches_total += 1;
-    CK(launch_plane(ctx->mp, ctx->block_slot, ctx->S, ctx->S.slab_bz1, ctx->plane_send, 0, ctx->jit.num_sms,
-                    ctx->stream));
-  }
-  return QMPM_OK;
-}
+// transport of one exchange kind between the z-neighbours
+enum XKind { XGhost = 0, XVel = 1, XMig = 2 };
 
-// C: add the lower rank's ghost plane, grid update, pack the velocity plane for the rank below
-qmpm_status slab_c(qmpm_ctx* ctx) {
-  StepBuffers B = buffers(ctx, ctx->n);
-  if (ctx->S.slab_lo) {
-    ctx->launches_total += 1;
-    CK(launch_plane(ctx->mp, ctx->block_slot, ctx->S, ctx->S.slab_bz0, ctx->plane_recv, 1, ctx->jit.num_sms,
-                    ctx->stream));
-  }
-  CK(launch_grid_update(ctx->dim, B, ctx->S, ctx->jit, ctx->stream, hook_fn, ctx));
-  if (ctx->S.slab_lo) {
-    ctx->launches_total += 1;
-    CK(launch_plane(ctx->gv, ctx->block_slot, ctx->S, ctx->S.slab_bz0, ctx->plane_send, 0, ctx->jit.num_sms,
-                    ctx->stream));
-  }
-  return QMPM_OK;
-}
-
-// D: velocities of the ghost plane from the rank above, G2P + encode
-qmpm_status slab_d(qmpm_ctx* ctx, uint64_t n_live) {
-  StepBuffers B = buffers(ctx, n_live);
-  if (ctx->S.slab_hi) {
-    ctx->launches_total += 1;
-    CK(launch_plane(ctx->gv, ctx->block_slot, ctx->S, ctx->S.slab_bz1, ctx->plane_recv, 2, ctx->jit.num_sms,
-                    ctx->stream));
-  }
-  CK(launch_g2p(B, ctx->S, salt_of(ctx), ctx->jit, ctx->stream, hook_fn, ctx));
-  ctx->n = n_live;
-  finish_step(ctx);
-  return QMPM_OK;
-}
-
-qmpm_status check_migration(qmpm_ctx* ctx) {
-  if (ctx->h_cnt[2]) return fail(ctx, QMPM_ECAPACITY, "slab migration buffer overflow (capacity %llu)",
-                                 (unsigned long long)ctx->mig_cap);
-  return QMPM_OK;
-}
-
-// one slab step with NCCL exchanges (one process per GPU)
-qmpm_status slab_step_nccl(qmpm_ctx* ctx) {
+qmpm_status nccl_x(qmpm_ctx* ctx, XKind k, cudaStream_t st) {
   std::string err;
-  qmpm_status rc = slab_a(ctx);
-  if (rc) return rc;
-  // counts: each neighbour announces how many particles it sends us
-  P2P c{&ctx->dc->mig_dn, 4, &ctx->dc->mig_up, 4, ctx->d_cnt_recv + 0, 4, ctx->d_cnt_recv + 1, 4};
-  if (!nccl_exchange(ctx->nccl, c, ctx->stream, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
-  CK(cudaMemcpyAsync(ctx->h_cnt + 4, ctx->d_cnt_recv, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  if ((rc = check_migration(ctx))) return rc;
-  const uint32_t W = ctx->W, dn = ctx->h_cnt[0], up = ctx->h_cnt[1], n_sorted = ctx->h_cnt[3];
-  const uint32_t rdn = ctx->S.slab_lo ? ctx->h_cnt[4] : 0, rup = ctx->S.slab_hi ? ctx->h_cnt[5] : 0;
-  if ((uint64_t)ctx->n + rdn + rup > ctx->cap) return fail(ctx, QMPM_ECAPACITY, "arrivals exceed max_particles");
-  uint32_t* dst = ctx->rec[ctx->cur] + (size_t)ctx->n * W;
-  P2P x{ctx->mig_send[0], (size_t)dn * W * 4, ctx->mig_send[1], (size_t)up * W * 4,
-        dst, (size_t)rdn * W * 4, dst + (size_t)rdn * W, (size_t)rup * W * 4};
-  if (!nccl_exchange(ctx->nccl, x, ctx->stream, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
-  if (ctx->ids[ctx->cur]) {
-    uint32_t* idst = ctx->ids[ctx->cur] + ctx->n;
-    P2P xi{ctx->mig_send_ids[0], (size_t)dn * 4, ctx->mig_send_ids[1], (size_t)up * 4,
-           idst, (size_t)rdn * 4, idst + rdn, (size_t)rup * 4};
-    if (!nccl_exchange(ctx->nccl, xi, ctx->stream, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
-  }
-  const uint64_t n_live = (uint64_t)n_sorted - dn - up + rdn + rup;
-  if ((rc = slab_b(ctx, rdn + rup))) return rc;
   const size_t pb = ctx->plane_elems * sizeof(float4);
-  P2P h1{nullptr, 0, ctx->plane_send, ctx->S.slab_hi ? pb : 0, ctx->plane_recv, ctx->S.slab_lo ? pb : 0, nullptr, 0};
-  if (!nccl_exchange(ctx->nccl, h1, ctx->stream, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
-  if ((rc = slab_c(ctx))) return rc;
-  P2P h2{ctx->plane_send, ctx->S.slab_lo ? pb : 0, nullptr, 0, nullptr, 0, ctx->plane_recv, ctx->S.slab_hi ? pb : 0};
-  if (!nccl_exchange(ctx->nccl, h2, ctx->stream, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
-  return slab_d(ctx, n_live);
+  P2P x{};
+  if (k == XGhost) {  // partial sums of the ghost plane go up
+    x = P2P{nullptr, 0, ctx->plane_send, ctx->S.slab_hi ? pb : 0, ctx->plane_recv, ctx->S.slab_lo ? pb : 0, nullptr, 0};
+  } else if (k == XVel) {  // bottom plane velocities go down
+    x = P2P{ctx->plane_send, ctx->S.slab_lo ? pb : 0, nullptr, 0, nullptr, 0, ctx->plane_recv, ctx->S.slab_hi ? pb : 0};
+  } else {
+    const size_t mb = ctx->mig_bytes;
+    x = P2P{ctx->mig_buf[0], ctx->S.slab_lo ? mb : 0, ctx->mig_buf[1], ctx->S.slab_hi ? mb : 0,
+            ctx->mig_buf[2], ctx->S.slab_lo ? mb : 0, ctx->mig_buf[3], ctx->S.slab_hi ? mb : 0};
+  }
+  if (!nccl_exchange(ctx->nccl, x, st, err)) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+  if (k == XMig && !nccl_allreduce_max_u32(ctx->nccl, &ctx->dc->status, st, err))
+    return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+  return QMPM_OK;
+}
+
+qmpm_status append_arrivals(qmpm_ctx* ctx) {
+  if (!ctx->S.slab_lo) CK(cudaMemsetAsync(ctx->mig_buf[2], 0, sizeof(MigHeader), ctx->stream));
+  if (!ctx->S.slab_hi) CK(cudaMemsetAsync(ctx->mig_buf[3], 0, sizeof(MigHeader), ctx->stream));
+  ctx->launches_total += 1;
+  CK(launch_append(ctx->rec[ctx->cur], ctx->ids[ctx->cur], ctx->dbg, ctx->cap, ctx->S, ctx->key, ctx->block_count,
+                   ctx->cell_count, mig_of(ctx), ctx->dc, ctx->jit, ctx->stream));
+  return QMPM_OK;
+}
+
+// the per-rank phases of one step; `x(kind, stream)` performs one exchange for this rank
+// (NCCL), or is null for the in-process group (its driver copies between the phases)
+struct SlabPhases {
+  qmpm_ctx* ctx;
+  // (first step) keys, routing of out-of-slab records
+  qmpm_status pre() {
+    if (ctx->binned) return QMPM_OK;
+    return rebin(ctx);
+  }
+  qmpm_status sort() {
+    StepBuffers B = buffers(ctx, ctx->n);
+    CK(launch_sort(ctx->dim, B, ctx->S, ctx->stream, hook_fn, ctx));
+    return QMPM_OK;
+  }
+  // P2G; with `overlap` the top plane first, its ghost plane handed to the exchange
+  qmpm_status p2g(bool overlap) {
+    StepBuffers B = buffers(ctx, ctx->n);
+    if (!overlap) {
+      CK(launch_p2g(B, ctx->S, ctx->jit, 0, ctx->stream, hook_fn, ctx));
+      if (ctx->S.slab_hi) {
+        ctx->launches_total += 1;
+        CK(launch_plane(ctx->mp, ctx->block_slot, ctx->S, ctx->S.slab_bz1, ctx->plane_send, 0, ctx->jit.num_sms, ctx->stream));
+      }
+      return QMPM_OK;
+    }
+    CK(launch_p2g(B, ctx->S, ctx->jit, 2, ctx->stream, hook_fn, ctx));
+    if (ctx->S.slab_hi) {
+      ctx->launches_total += 1;
+      CK(launch_plane(ctx->mp, ctx->block_slot, ctx->S, ctx->S.slab_bz1, ctx->plane_send, 0, ctx->jit.num_sms, ctx->stream));
+    }
+    CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->comm, ctx->ev[0], 0));
+    qmpm_status rc = nccl_x(ctx, XGhost, ctx->comm);
+    if (rc) return rc;
+    CK(cudaEventRecord(ctx->ev[1], ctx->comm));
+    CK(launch_p2g(B, ctx->S, ctx->jit, 1, ctx->stream, hook_fn, ctx));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev[1], 0));
+    return QMPM_OK;
+  }
+  qmpm_status grid() {
+    StepBuffers B = buffers(ctx, ctx->n);
+    if (ctx->S.slab_lo) {
+      ctx->launches_total += 1;
+      CK(launch_plane(ctx->mp, ctx->block_slot, ctx->S, ctx->S.slab_bz0, ctx->plane_recv, 1, ctx->jit.num_sms, ctx->stream));
+    }
+    CK(launch_grid_update(ctx->dim, B, ctx->S, ctx->jit, ctx->stream, hook_fn, ctx));
+    if (ctx->S.slab_lo) {
+      ctx->launches_total += 1;
+      CK(launch_plane(ctx->gv, ctx->block_slot, ctx->S, ctx->S.slab_bz0, ctx->plane_send, 0, ctx->jit.num_sms, ctx->stream));
+    }
+    return QMPM_OK;
+  }
+  qmpm_status g2p(bool overlap) {
+    StepBuffers B = buffers(ctx, ctx->n);
+    qmpm_status rc = clear_send_headers(ctx);
+    if (rc) return rc;
+    auto store_ghost = [&]() -> qmpm_status {
+      if (ctx->S.slab_hi) {
+        ctx->launches_total += 1;
+        CK(launch_plane(ctx->gv, ctx->block_slot, ctx->S, ctx->S.slab_bz1, ctx->plane_recv, 2, ctx->jit.num_sms, ctx->stream));
+      }
+      return QMPM_OK;
+    };
+    if (!overlap) {
+      if ((rc = store_ghost())) return rc;
+      CK(launch_g2p(B, ctx->S, mig_of(ctx), ctx->jit, 0, ctx->stream, hook_fn, ctx));
+      return QMPM_OK;
+    }
+    CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->comm, ctx->ev[2], 0));
+    if ((rc = nccl_x(ctx, XVel, ctx->comm))) return rc;
+    CK(cudaEventRecord(ctx->ev[3], ctx->comm));
+    CK(launch_g2p(B, ctx->S, mig_of(ctx), ctx->jit, 1, ctx->stream, hook_fn, ctx));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev[3], 0));
+    if ((rc = store_ghost())) return rc;
+    CK(launch_g2p(B, ctx->S, mig_of(ctx), ctx->jit, 2, ctx->stream, hook_fn, ctx));
+    return QMPM_OK;
+  }
+};
+
+// one slab step with NCCL exchanges (one process per GPU), no host synchronisation
+qmpm_status slab_step_nccl(qmpm_ctx* ctx) {
+  SlabPhases ph{ctx};
+  qmpm_status rc;
+  if (!ctx->binned) {
+    if ((rc = ph.pre())) return rc;
+    if ((rc = nccl_x(ctx, XMig, ctx->stream))) return rc;
+    if ((rc = append_arrivals(ctx))) return rc;
+  }
+  if ((rc = ph.sort())) return rc;
+  if ((rc = ph.p2g(true))) return rc;
+  if ((rc = ph.grid())) return rc;
+  if ((rc = ph.g2p(true))) return rc;
+  finish_step(ctx);
+  if ((rc = nccl_x(ctx, XMig, ctx->stream))) return rc;
+  return append_arrivals(ctx);
+}
+
+// sticky device status -> error code (the ctx stays in error until set_state / set_words)
+qmpm_status status_error(qmpm_ctx* ctx, uint32_t st) {
+  if (st & kStatusTwoHop)
+    return fail(ctx, QMPM_EDOMAIN, "a particle moved more than one slab in one step (CFL violated)");
+  if (st & kStatusMigOverflow)
+    return fail(ctx, QMPM_ECAPACITY, "slab migration buffer overflow (capacity %llu per direction)",
+                (unsigned long long)ctx->mig_cap);
+  if (st & kStatusCapacity) return fail(ctx, QMPM_ECAPACITY, "arrivals exceed max_particles");
+  if (st & kStatusNonfinite)
+    return fail(ctx, QMPM_ENONFINITE, "non-finite values were encoded (as code 0; S:42): see qmpm_stats.nonfinite");
+  return QMPM_OK;
 }
 
 }  // namespace
@@ -837,6 +986,7 @@ extern "C" {
 
 qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps) {
   if (!ctx) return fail(ctx, QMPM_EINVAL, "NULL ctx");
+  if (ctx->sticky) return fail(ctx, QMPM_ESTATE, "the ctx is in error (%u): set_state or set_words first", ctx->sticky);
   if (ctx->slab && ctx->nranks > 1) {
     if (!ctx->nccl) return fail(ctx, QMPM_ESTATE, "slab ctx: call qmpm_connect_nccl or use qmpm_step_group");
     for (uint32_t t = 0; t < n_steps; ++t) {
@@ -850,13 +1000,37 @@ qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps) {
       qmpm_status rc = rebin(ctx);
       if (rc) return rc;
     }
-    StepBuffers B = buffers(ctx, ctx->n);
-    CK(launch_step(ctx->dim, B, ctx->S, salt_of(ctx), ctx->jit, ctx->stream, hook_fn, ctx));
+    if (!ctx->prof && ctx->use_graphs) {
+      // one CUDA-graph launch per step: the step's launches take no per-step argument
+      // (the dither salt comes from the device step counter), so one graph per ping-pong
+      // parity replays for the ctx's lifetime
+      cudaGraphExec_t& g = ctx->graph[ctx->cur];
+      if (!g) {
+        StepBuffers B = buffers(ctx, ctx->n);
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = launch_step(ctx->dim, B, ctx->S, mig_of(ctx), ctx->jit, ctx->stream, nullptr, nullptr);
+        cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &graph);
+        if (!e) e = e2;
+        if (!e) e = cudaGraphInstantiate(&g, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        if (e) {
+          g = nullptr;
+          return fail(ctx, QMPM_ECUDA, "step graph capture: %s", cudaGetErrorString(e));
+        }
+      }
+      CK(cudaGraphLaunch(g, ctx->stream));
+      ctx->launches_total += kStepLaunches;
+    } else {
+      StepBuffers B = buffers(ctx, ctx->n);
+      CK(launch_step(ctx->dim, B, ctx->S, mig_of(ctx), ctx->jit, ctx->stream, hook_fn, ctx));
+    }
     finish_step(ctx);
   }
   return QMPM_OK;
 }
 
+// in-process transport: the same phases, the exchanges as device copies between the ctxs
 qmpm_status qmpm_step_group(qmpm_ctx* const* ctxs, int n, uint32_t n_steps) {
   qmpm_ctx* ctx = nullptr;
   if (!ctxs || n < 1) return fail(ctx, QMPM_EINVAL, "empty group");
@@ -864,60 +1038,50 @@ qmpm_status qmpm_step_group(qmpm_ctx* const* ctxs, int n, uint32_t n_steps) {
     if (!ctxs[r] || !ctxs[r]->slab || ctxs[r]->nranks != n || ctxs[r]->rank != r)
       return fail(ctx, QMPM_EINVAL, "qmpm_step_group: ctxs[%d] must be the slab ctx of rank %d of %d", r, r, n);
     if (ctxs[r]->stream != ctxs[0]->stream) return fail(ctx, QMPM_EINVAL, "qmpm_step_group: one stream for all ctxs");
-    if ((ctxs[r]->ids[0] != nullptr) != (ctxs[0]->ids[0] != nullptr) || ctxs[r]->W != ctxs[0]->W)
-      return fail(ctx, QMPM_EINVAL, "qmpm_step_group: ctxs differ in scheme or flags");
+    if ((ctxs[r]->ids[0] != nullptr) != (ctxs[0]->ids[0] != nullptr) || ctxs[r]->W != ctxs[0]->W ||
+        ctxs[r]->mig_cap != ctxs[0]->mig_cap)
+      return fail(ctx, QMPM_EINVAL, "qmpm_step_group: ctxs differ in scheme, flags or migration capacity");
+    if (ctxs[r]->sticky) return fail(ctxs[r], QMPM_ESTATE, "ctx %d is in error", r);
   }
   cudaStream_t st = ctxs[0]->stream;
-  const uint32_t W = ctxs[0]->W;
-  std::vector<uint64_t> n_live(n);
-  std::vector<uint32_t> arr(n);
+  auto copy = [&](void* dst, const void* src, size_t bytes) -> qmpm_status {
+    if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return fail(ctx, QMPM_ECUDA, "step_group copy failed");
+    return QMPM_OK;
+  };
+  auto migrate = [&]() -> qmpm_status {
+    qmpm_status rc;
+    for (int r = 0; r < n; ++r) {
+      if (r > 0 && (rc = copy(ctxs[r]->mig_buf[2], ctxs[r - 1]->mig_buf[1], ctxs[r]->mig_bytes))) return rc;
+      if (r + 1 < n && (rc = copy(ctxs[r]->mig_buf[3], ctxs[r + 1]->mig_buf[0], ctxs[r]->mig_bytes))) return rc;
+    }
+    for (int r = 0; r < n; ++r)
+      if ((rc = append_arrivals(ctxs[r]))) return rc;
+    return QMPM_OK;
+  };
   for (uint32_t t = 0; t < n_steps; ++t) {
+    qmpm_status rc;
+    bool pre = false;
     for (int r = 0; r < n; ++r) {
-      qmpm_status rc = slab_a(ctxs[r]);
-      if (rc) return rc;
+      pre |= !ctxs[r]->binned;
+      if ((rc = SlabPhases{ctxs[r]}.pre())) return rc;
     }
-    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(ctx, QMPM_ECUDA, "step_group sync failed");
+    if (pre && (rc = migrate())) return rc;
     for (int r = 0; r < n; ++r) {
-      qmpm_ctx* c = ctxs[r];
-      qmpm_status rc = check_migration(c);
-      if (rc) return rc;
-      const uint32_t rdn = r > 0 ? ctxs[r - 1]->h_cnt[1] : 0, rup = r + 1 < n ? ctxs[r + 1]->h_cnt[0] : 0;
-      if (c->n + rdn + rup > c->cap) return fail(c, QMPM_ECAPACITY, "arrivals exceed max_particles");
-      uint32_t* dst = c->rec[c->cur] + (size_t)c->n * W;
-      if (rdn) {
-        CK(cudaMemcpyAsync(dst, ctxs[r - 1]->mig_send[1], (size_t)rdn * W * 4, cudaMemcpyDeviceToDevice, st));
-        if (c->ids[c->cur])
-          CK(cudaMemcpyAsync(c->ids[c->cur] + c->n, ctxs[r - 1]->mig_send_ids[1], (size_t)rdn * 4,
-                             cudaMemcpyDeviceToDevice, st));
-      }
-      if (rup) {
-        CK(cudaMemcpyAsync(dst + (size_t)rdn * W, ctxs[r + 1]->mig_send[0], (size_t)rup * W * 4,
-                           cudaMemcpyDeviceToDevice, st));
-        if (c->ids[c->cur])
-          CK(cudaMemcpyAsync(c->ids[c->cur] + c->n + rdn, ctxs[r + 1]->mig_send_ids[0], (size_t)rup * 4,
-                             cudaMemcpyDeviceToDevice, st));
-      }
-      arr[r] = rdn + rup;
-      n_live[r] = (uint64_t)c->h_cnt[3] - c->h_cnt[0] - c->h_cnt[1] + rdn + rup;
-    }
-    for (int r = 0; r < n; ++r) {
-      qmpm_status rc = slab_b(ctxs[r], arr[r]);
-      if (rc) return rc;
+      SlabPhases ph{ctxs[r]};
+      if ((rc = ph.sort()) || (rc = ph.p2g(false))) return rc;
     }
     for (int r = 0; r + 1 < n; ++r)
-      CK(cudaMemcpyAsync(ctxs[r + 1]->plane_recv, ctxs[r]->plane_send, ctxs[r]->plane_elems * sizeof(float4),
-                         cudaMemcpyDeviceToDevice, st));
-    for (int r = 0; r < n; ++r) {
-      qmpm_status rc = slab_c(ctxs[r]);
-      if (rc) return rc;
-    }
+      if ((rc = copy(ctxs[r + 1]->plane_recv, ctxs[r]->plane_send, ctxs[r]->plane_elems * sizeof(float4)))) return rc;
+    for (int r = 0; r < n; ++r)
+      if ((rc = SlabPhases{ctxs[r]}.grid())) return rc;
     for (int r = 1; r < n; ++r)
-      CK(cudaMemcpyAsync(ctxs[r - 1]->plane_recv, ctxs[r]->plane_send, ctxs[r]->plane_elems * sizeof(float4),
-                         cudaMemcpyDeviceToDevice, st));
+      if ((rc = copy(ctxs[r - 1]->plane_recv, ctxs[r]->plane_send, ctxs[r]->plane_elems * sizeof(float4)))) return rc;
     for (int r = 0; r < n; ++r) {
-      qmpm_status rc = slab_d(ctxs[r], n_live[r]);
-      if (rc) return rc;
+      if ((rc = SlabPhases{ctxs[r]}.g2p(false))) return rc;
+      finish_step(ctxs[r]);
     }
+    if ((rc = migrate())) return rc;
   }
   return QMPM_OK;
 }
@@ -976,40 +1140,7 @@ qmpm_status qmpm_create_slab(const qmpm_params* params, const qmpm_scheme* schem
   if (slab->z0 < 0 || slab->z1 > nz || slab->z0 >= slab->z1 || slab->z0 % 4 != 0 || (slab->z1 % 4 != 0 && slab->z1 != nz))
     return fail(ctx, QMPM_EINVAL, "slab [%d, %d) must be non-empty, inside [0, %d) and on 4-cell block planes",
                 slab->z0, slab->z1, nz);
-  qmpm_status rc = qmpm_create(params, scheme, cuda_stream, &ctx);
-  if (rc) return rc;
-  ctx->slab = true;
-  ctx->nranks = slab->nranks;
-  ctx->rank = slab->rank;
-  SimDev& S = ctx->S;
-  S.slab_bz0 = slab->z0 / 4;
-  S.slab_bz1 = (slab->z1 + 3) / 4;
-  S.slab_lo = slab->rank > 0;
-  S.slab_hi = slab->rank + 1 < slab->nranks;
-  ctx->mig_cap = slab->migrate_capacity ? slab->migrate_capacity : std::max<uint64_t>(65536, ctx->cap / 64);
-  ctx->plane_elems = (size_t)S.nb[0] * S.nb[1] * 64;
-  const size_t W = ctx->W;
-  cudaError_t e = cudaSuccess;
-  for (int dir = 0; dir < 2 && !e; ++dir) {
-    e = cudaMalloc((void**)&ctx->mig_send[dir], sizeof(uint32_t) * W * ctx->mig_cap);
-    if (!e && ctx->ids[0]) e = cudaMalloc((void**)&ctx->mig_send_ids[dir], sizeof(uint32_t) * ctx->mig_cap);
-  }
-  if (!e) e = cudaMalloc((void**)&ctx->plane_send, sizeof(float4) * ctx->plane_elems);
-  if (!e) e = cudaMalloc((void**)&ctx->plane_recv, sizeof(float4) * ctx->plane_elems);
-  if (!e) e = cudaMalloc((void**)&ctx->d_cnt_recv, 2 * sizeof(uint32_t));
-  if (!e) e = cudaMallocHost((void**)&ctx->h_cnt, 8 * sizeof(uint32_t));
-  if (!e) e = cudaMemsetAsync(ctx->plane_recv, 0, sizeof(float4) * ctx->plane_elems, ctx->stream);
-  if (!e) e = cudaMemsetAsync(ctx->d_cnt_recv, 0, 2 * sizeof(uint32_t), ctx->stream);
-  if (!e) e = cudaStreamSynchronize(ctx->stream);
-  if (e) {
-    cudaGetLastError();
-    qmpm_destroy(ctx);
-    return fail(nullptr, e == cudaErrorMemoryAllocation ? QMPM_ENOMEM : QMPM_ECUDA, "qmpm_create_slab: %s",
-                cudaGetErrorString(e));
-  }
-  memset(ctx->h_cnt, 0, 8 * sizeof(uint32_t));
-  *out = ctx;
-  return QMPM_OK;
+  return create_impl(params, scheme, cuda_stream, slab, out);
 }
 
 qmpm_status qmpm_set_ids(qmpm_ctx* ctx, uint64_t n, const uint32_t* ids) {
@@ -1023,14 +1154,77 @@ qmpm_status qmpm_set_ids(qmpm_ctx* ctx, uint64_t n, const uint32_t* ids) {
   return QMPM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// synchronise and read the device counters; the sticky status becomes the ctx's
+qmpm_status sync_counters(qmpm_ctx* ctx, DevCounters& h) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemcpy(&h, ctx->dc, sizeof(h), cudaMemcpyDeviceToHost));
+  ctx->sticky |= h.status | (h.nonfinite ? kStatusNonfinite : 0u);
+  return QMPM_OK;
+}
+
+// The live record slots: [0, n_slots) minus the slots whose particle left the slab (their
+// records stay until the next sort).  Without leavers the identity (`slots` = null);
+// else the i-th live slot in slot order, written to ctx->perm (scratch between steps).
+qmpm_status live_slots(qmpm_ctx* ctx, const DevCounters& h, const uint32_t** slots, uint64_t* n) {
+  *slots = nullptr;
+  *n = h.n_slots;
+  if (h.n_leave == 0) return QMPM_OK;
+  const uint32_t nd = std::min(h.n_leave, ctx->dead_cap);
+  std::vector<uint32_t> dead(nd);
+  CK(cudaMemcpy(dead.data(), ctx->dead_list, sizeof(uint32_t) * nd, cudaMemcpyDeviceToHost));
+  std::sort(dead.begin(), dead.end());
+  uint32_t* d_dead = nullptr;
+  CK(cudaMalloc((void**)&d_dead, sizeof(uint32_t) * std::max<uint32_t>(nd, 1u)));
+  cudaError_t e = cudaMemcpy(d_dead, dead.data(), sizeof(uint32_t) * nd, cudaMemcpyHostToDevice);
+  if (!e) e = launch_live_slots(d_dead, nd, h.n_slots, ctx->perm, ctx->jit.num_sms, ctx->stream);
+  if (!e) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d_dead);
+  if (e) return fail(ctx, QMPM_ECUDA, "read_state compaction: %s", cudaGetErrorString(e));
+  *slots = ctx->perm;
+  *n = (uint64_t)h.n_slots - nd;
+  return QMPM_OK;
+}
+
+// rows [n][row] of `src` at the live slots (identity when slots == null) -> dst (any memory)
+qmpm_status gather_rows(qmpm_ctx* ctx, const uint32_t* src, const uint32_t* slots, uint64_t n, uint32_t row,
+                        uint32_t* scratch, void* dst) {
+  if (!n) return QMPM_OK;
+  if (!slots) {
+    CK(cudaMemcpyAsync(dst, src, sizeof(uint32_t) * row * n, cudaMemcpyDefault, ctx->stream));
+    return QMPM_OK;
+  }
+  CK(launch_gather_rows(src, slots, (uint32_t)n, row, scratch, ctx->jit.num_sms, ctx->stream));
+  CK(cudaMemcpyAsync(dst, scratch, sizeof(uint32_t) * row * n, cudaMemcpyDefault, ctx->stream));
+  return QMPM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 qmpm_status qmpm_read_state(qmpm_ctx* ctx, float* vals, uint32_t* words, uint32_t* ids, uint64_t capacity,
                             uint64_t* n_out) {
   if (!ctx) return fail(ctx, QMPM_EINVAL, "NULL ctx");
-  const uint64_t n = ctx->n;
+  DevCounters h;
+  qmpm_status rc = sync_counters(ctx, h);
+  if (rc) return rc;
+  const uint32_t* slots = nullptr;
+  uint64_t n = 0;
+  if ((rc = live_slots(ctx, h, &slots, &n))) return rc;
   if (n_out) *n_out = n;
   if (capacity < n) return fail(ctx, QMPM_ECAPACITY, "capacity %llu < n %llu", (unsigned long long)capacity,
                                 (unsigned long long)n);
   if (ids && !ctx->ids[ctx->cur]) return fail(ctx, QMPM_ESTATE, "ids requested without QMPM_TRACK_IDS");
+  // the live records, gathered into the other ping-pong buffer (free between steps)
+  const uint32_t* rec = ctx->rec[ctx->cur];
+  if (slots && n) {
+    CK(launch_gather_rows(rec, slots, (uint32_t)n, ctx->W, ctx->rec[ctx->cur ^ 1], ctx->jit.num_sms, ctx->stream));
+    rec = ctx->rec[ctx->cur ^ 1];
+  }
   if (vals && n) {
     float* dv = vals;
     float* tmp = nullptr;
@@ -1039,32 +1233,38 @@ qmpm_status qmpm_read_state(qmpm_ctx* ctx, float* vals, uint32_t* words, uint32_
       dv = tmp;
     }
     ctx->launches_total += 1;
-    qmpm_status rc = codec_run(ctx, ctx->C, 1, n, nullptr, dv, nullptr, 0u, ctx->rec[ctx->cur], nullptr, nullptr,
-                               nullptr, ctx->stream);
+    rc = codec_run(ctx, ctx->C, 1, n, nullptr, dv, nullptr, 0u, rec, nullptr, nullptr, nullptr, ctx->stream);
     if (rc) return rc;
     if (tmp) {
       CK(cudaMemcpyAsync(vals, tmp, sizeof(float) * ctx->ns * n, cudaMemcpyDefault, ctx->stream));
       CK(cudaFreeAsync(tmp, ctx->stream));
     }
   }
-  if (words && n) CK(cudaMemcpyAsync(words, ctx->rec[ctx->cur], sizeof(uint32_t) * ctx->W * n, cudaMemcpyDefault, ctx->stream));
-  if (ids && n) CK(cudaMemcpyAsync(ids, ctx->ids[ctx->cur], sizeof(uint32_t) * n, cudaMemcpyDefault, ctx->stream));
+  if (words && n) CK(cudaMemcpyAsync(words, rec, sizeof(uint32_t) * ctx->W * n, cudaMemcpyDefault, ctx->stream));
+  if (ids && n && (rc = gather_rows(ctx, ctx->ids[ctx->cur], slots, n, 1, ctx->ids[ctx->cur ^ 1], ids))) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
-  DevCounters h;
-  CK(cudaMemcpy(&h, ctx->dc, sizeof(h), cudaMemcpyDeviceToHost));
   if (h.overflow) return fail(ctx, QMPM_ECAPACITY, "grid pool overflow in %llu step(s): raise pool_blocks",
                               (unsigned long long)h.overflow);
-  return QMPM_OK;
+  return status_error(ctx, ctx->sticky);
 }
 
 qmpm_status qmpm_read_debug(qmpm_ctx* ctx, float* pre, uint64_t capacity, uint64_t* n_out) {
   if (!ctx) return fail(ctx, QMPM_EINVAL, "NULL ctx");
   if (!ctx->dbg) return fail(ctx, QMPM_ESTATE, "QMPM_DEBUG_PREENCODE not set");
   if (!ctx->dbg_valid) return fail(ctx, QMPM_ESTATE, "no step taken since the state was set");
-  const uint64_t n = ctx->n;
+  DevCounters h;
+  qmpm_status rc = sync_counters(ctx, h);
+  if (rc) return rc;
+  const uint32_t* slots = nullptr;
+  uint64_t n = 0;
+  if ((rc = live_slots(ctx, h, &slots, &n))) return rc;
   if (n_out) *n_out = n;
   if (capacity < n) return fail(ctx, QMPM_ECAPACITY, "capacity < n");
-  if (n) CK(cudaMemcpyAsync(pre, ctx->dbg, sizeof(float) * ctx->ns * n, cudaMemcpyDefault, ctx->stream));
+  uint32_t* scratch = nullptr;
+  if (slots && n) CK(cudaMallocAsync((void**)&scratch, sizeof(float) * ctx->ns * n, ctx->stream));
+  rc = gather_rows(ctx, reinterpret_cast<const uint32_t*>(ctx->dbg), slots, n, (uint32_t)ctx->ns, scratch, pre);
+  if (scratch) CK(cudaFreeAsync(scratch, ctx->stream));
+  if (rc) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
   return QMPM_OK;
 }
@@ -1082,12 +1282,12 @@ qmpm_status qmpm_read_ranges(qmpm_ctx* ctx, float* max_abs, int reset) {
 
 qmpm_status qmpm_stats(qmpm_ctx* ctx, qmpm_stats_t* out) {
   if (!ctx || !out) return fail(ctx, QMPM_EINVAL, "NULL argument");
-  CK(cudaStreamSynchronize(ctx->stream));
   DevCounters h;
-  CK(cudaMemcpy(&h, ctx->dc, sizeof(h), cudaMemcpyDeviceToHost));
+  qmpm_status rc = sync_counters(ctx, h);
+  if (rc) return rc;
   memset(out, 0, sizeof(*out));
   out->step = ctx->step;
-  out->n_particles = ctx->n;
+  out->n_particles = (uint64_t)h.n_slots - std::min(h.n_leave, h.n_slots);  // live particles on this rank
   for (int i = 0; i < QMPM_MAX_FIELDS; ++i) {
     out->saturations[i] = h.sat[i];
     out->round_up[i] = h.up[i];
@@ -1098,7 +1298,7 @@ qmpm_status qmpm_stats(qmpm_ctx* ctx, qmpm_stats_t* out) {
   out->active_blocks = h.n_active;
   out->touched_blocks = h.n_touched;
   out->pool_overflow = h.overflow;
-  return QMPM_OK;
+  return status_error(ctx, ctx->sticky);
 }
 
 qmpm_status qmpm_encode(const qmpm_scheme* scheme, uint64_t n, const float* vals, const uint32_t* keys, uint64_t step,

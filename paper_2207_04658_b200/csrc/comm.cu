@@ -24,6 +24,7 @@ struct NcclApi {
   decltype(&ncclGroupStart) groupStart = nullptr;
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclGetErrorString) errstr = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
   bool ok = false;
 };
 
@@ -49,7 +50,8 @@ bool load(std::string& err) {
   g_api.ok = sym(h, "ncclGetUniqueId", g_api.getUniqueId) && sym(h, "ncclCommInitRank", g_api.commInitRank) &&
              sym(h, "ncclCommDestroy", g_api.commDestroy) && sym(h, "ncclSend", g_api.send) &&
              sym(h, "ncclRecv", g_api.recv) && sym(h, "ncclGroupStart", g_api.groupStart) &&
-             sym(h, "ncclGroupEnd", g_api.groupEnd) && sym(h, "ncclGetErrorString", g_api.errstr);
+             sym(h, "ncclGroupEnd", g_api.groupEnd) && sym(h, "ncclGetErrorString", g_api.errstr) &&
+             sym(h, "ncclAllReduce", g_api.allReduce);
   if (!g_api.ok) err = "incomplete libnccl";
   return g_api.ok;
 }
@@ -109,6 +111,15 @@ bool nccl_exchange(NcclComm* c, const P2P& x, cudaStream_t st, std::string& err)
   if (r == ncclSuccess) r = r2;
   if (r != ncclSuccess) {
     err = std::string("NCCL exchange: ") + g_api.errstr(r);
+    return false;
+  }
+  return true;
+}
+
+bool nccl_allreduce_max_u32(NcclComm* c, unsigned int* v, cudaStream_t st, std::string& err) {
+  ncclResult_t r = g_api.allReduce(v, v, 1, ncclUint32, ncclMax, c->comm, st);
+  if (r != ncclSuccess) {
+    err = std::string("NCCL all-reduce: ") + g_api.errstr(r);
     return false;
   }
   return true;

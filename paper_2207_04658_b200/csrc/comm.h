@@ -28,5 +28,7 @@ struct P2P {
   size_t recv_up_bytes;
 };
 bool nccl_exchange(NcclComm* c, const P2P& x, cudaStream_t st, std::string& err);
+// in-place all-reduce (max) of one device uint32 over every rank (the sticky status)
+bool nccl_allreduce_max_u32(NcclComm* c, unsigned int* v, cudaStream_t st, std::string& err);
 
 }  // namespace qmpm

@@ -221,8 +221,8 @@ __device__ __forceinline__ uint32_t senc_fast(const int i, float v, float omr, b
 //   d = y + (s_r - 2), s_r = 1 + r16 2^-16           (s_r - 2 = -(1 - r) exactly)
 //   u = floor(t) + [y >= 1 - r] = bits(s) - bits(M) + 1 + (bits(d) >> 31)
 // sign(d) is exact under round-to-nearest (d = +0 iff y = 1 - r: rounds up, Q6).
-// `flag` as senc_fast (|t| >= 2^b - 1 or NaN: the caller re-encodes exactly); `zero` is
-// raised when some y == 0 (an on-grid value: counted as neither up nor down).
+// `flag` as senc_fast (|t| >= 2^b - 1 or NaN: the caller re-encodes exactly); zi / zj are
+// y == 0 (an on-grid value: counted as neither up nor down).
 constexpr float kFloorMagic = 12582912.0f;  // 1.5 2^23
 constexpr int kFloorMagicBits = 0x4b400000;
 
@@ -252,7 +252,7 @@ __host__ __device__ constexpr int pair_role(int i) {
 template <class SP>
 __device__ __forceinline__ void senc_pair_fast(const int i, const int j, const float vi, const float vj,
                                                const float si, const float sj, int& ui, int& uj, int& sbi, int& sbj,
-                                               bool& flag, bool& zero) {
+                                               bool& flag, bool& zi, bool& zj) {
   float2 a = make_float2(vi, vj);
   if (SP::offset(i) != 0.0f || SP::offset(j) != 0.0f)  // v - offset; adding -0 is the identity
     a = __fadd2_rn(a, make_float2(-SP::offset(i), -SP::offset(j)));
@@ -266,12 +266,13 @@ __device__ __forceinline__ void senc_pair_fast(const int i, const int j, const f
   ui = __float_as_int(s.x) - (kFloorMagicBits - 1) + sbi;
   uj = __float_as_int(s.y) - (kFloorMagicBits - 1) + sbj;
   flag |= !(fabsf(t.x) < enc_lim(SP::width(i))) || !(fabsf(t.y) < enc_lim(SP::width(j)));
-  zero |= (y.x == 0.0f) || (y.y == 0.0f);
+  zi = y.x == 0.0f;
+  zj = y.y == 0.0f;
 }
 
 template <class SP>
 __device__ __forceinline__ int senc1_fast(const int i, const float v, const float si, int& sb, bool& flag,
-                                          bool& zero) {
+                                          bool& z) {
   const float a = (SP::offset(i) != 0.0f) ? __fsub_rn(v, SP::offset(i)) : v;
   const float t = __fmul_rn(a, SP::inv_delta(i));
   const float s = __fadd_rd(t, kFloorMagic);
@@ -279,17 +280,8 @@ __device__ __forceinline__ int senc1_fast(const int i, const float v, const floa
   const float d = __fadd_rn(y, __fsub_rn(si, 2.0f));
   sb = sign_mask(d);
   flag |= !(fabsf(t) < enc_lim(SP::width(i)));
-  zero |= y == 0.0f;
+  z = y == 0.0f;
   return __float_as_int(s) - (kFloorMagicBits - 1) + sb;
-}
-
-// y == 0 of the fast path (the rare recount of on-grid values)
-template <class SP>
-__device__ __forceinline__ bool on_grid_fast(const int i, const float v) {
-  const float a = (SP::offset(i) != 0.0f) ? __fsub_rn(v, SP::offset(i)) : v;
-  const float t = __fmul_rn(a, SP::inv_delta(i));
-  const float s = __fadd_rd(t, kFloorMagic);
-  return __fsub_rn(t, __fsub_rn(s, kFloorMagic)) == 0.0f;
 }
 
 // the integer code of FIXED entry i (sign-extended b+1 bits, reading Q2)

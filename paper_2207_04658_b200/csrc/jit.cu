@@ -261,7 +261,8 @@ cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err) {
   m.module = mod;
   if (g_drv.moduleGetFunction(&m.bin_count, mod, "qmpm_bin_count") != CUDA_SUCCESS ||
       g_drv.moduleGetFunction(&m.p2g, mod, "qmpm_p2g") != CUDA_SUCCESS ||
-      g_drv.moduleGetFunction(&m.g2p, mod, "qmpm_g2p") != CUDA_SUCCESS) {
+      g_drv.moduleGetFunction(&m.g2p, mod, "qmpm_g2p") != CUDA_SUCCESS ||
+      g_drv.moduleGetFunction(&m.append, mod, "qmpm_append") != CUDA_SUCCESS) {
     err = "JIT module lacks a kernel";
     return cudaErrorSymbolNotFound;
   }

@@ -11,7 +11,7 @@ namespace qmpm {
 
 struct JitModule {
   CUmodule module;
-  CUfunction bin_count, p2g, g2p;
+  CUfunction bin_count, p2g, g2p, append;
   int regs_p2g, regs_g2p;
   unsigned smem_warp_p2g, smem_warp_g2p;  // shared memory per warp
   std::string log;

@@ -8,6 +8,8 @@
 //   k_bin_scatter  a1  counting-sort scatter by (block, cell): perm[sorted slot] = record index
 //   k_grid_update  a4  v = p/m + dt g, separating walls; clears (m, p) for next step
 // (the standalone codec is NVRTC-specialised too: codec_kernels.cuh)
+#include <algorithm>
+
 #include <cuda_runtime.h>
 
 #include "jit.h"
@@ -36,7 +38,7 @@ __device__ __forceinline__ void block_flags(uint32_t b, const uint32_t* __restri
 #pragma unroll
   for (int dl = 1; dl < (1 << D); ++dl) {
     int nc[3] = {bc[0] - (dl & 1), bc[1] - ((dl >> 1) & 1), D == 3 ? bc[2] - ((dl >> 2) & 1) : 0};
-    if (nc[0] < 0 || nc[1] < 0 || nc[2] < 0) continue;
+    if (nc[0] < 0 || nc[1] < 0 || (D == 3 && nc[2] < S.tab_bz0)) continue;
     touched |= count[block_id<D>(nc, S)] > 0;
   }
 }
@@ -128,6 +130,7 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(const uint4* __restrict__ t
     ex.z += s.z;
   }
   if (threadIdx.x == 0) {
+    dc->gstep += 1u;  // the step this sort starts (G2P's dither salt)
     dc->n_active = total.y;
     dc->next_p2g = 0u;
     dc->next_g2p = 0u;
@@ -146,7 +149,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __r
                                                              uint32_t* __restrict__ block_slot,
                                                              uint32_t* __restrict__ active_list,
                                                              uint32_t* __restrict__ touched_list,
-                                                             uint32_t pool) {
+                                                             uint32_t pool, DevCounters* __restrict__ dc) {
+  // slab ranks: active blocks below the top owned block plane (the overlap split of P2G/G2P)
+  const uint32_t top_first = D == 3 ? (uint32_t)(S.slab_bz1 - 1 - S.tab_bz0) * (uint32_t)S.nb[0] * (uint32_t)S.nb[1]
+                                    : 0xffffffffu;
   const uint32_t b0 = blockIdx.x * kScanTile + threadIdx.x * kScanPer;
   uint32_t c[kScanPer], a[kScanPer], t[kScanPer];
   uint3 v = make_uint3(0, 0, 0);
@@ -166,6 +172,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __r
 #pragma unroll
   for (int q = 0; q < kScanPer; ++q) {
     const uint32_t b = b0 + q;
+    if (b == top_first) dc->n_active_below = ex.y;
     if (b < S.nblocks) {
       block_start[b] = ex.x;
       if (a[q]) active_list[ex.y] = b;
@@ -214,42 +221,39 @@ __global__ void k_cell_scan(uint32_t* __restrict__ cell_count, uint32_t* __restr
   }
 }
 
-// zero the cell counters of the active blocks (slab sort pass 1 -> recount)
-__global__ void k_cell_reset(uint32_t* __restrict__ cell_count, const uint32_t* __restrict__ active_list,
-                             const DevCounters* __restrict__ dc) {
-  const uint32_t n = dc->n_active * 64u;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-    cell_count[(size_t)active_list[t >> 6] * 64 + (t & 63u)] = 0u;
-}
-
-// Counting-sort scatter by the full key (block, base cell): perm[pos] = record index,
-// pos from a warp-aggregated atomicSub on the key's cell cursor.  kBinItems particles
-// per thread (strided by the CTA size, so loads stay coalesced): the per-particle
-// chain key -> atomic -> store is latency-bound, so several are kept in flight.
+// Counting-sort scatter by the full key (block, base cell): perm[pos] = record slot,
+// pos from a warp-aggregated atomicSub on the key's cell cursor; dead keys (particles a
+// slab rank no longer owns) are skipped.  The slot count comes from the device
+// (DevCounters::n_slots: it includes a slab's appended arrivals, never synchronised to
+// the host).  kBinItems particles per thread in flight (strided by the CTA size, so loads
+// stay coalesced): the per-particle chain key -> atomic -> store is latency-bound.
 constexpr int kBinItems = 4;
-__global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ key, uint32_t n,
+__global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ key, const DevCounters* __restrict__ dc,
                                                       uint32_t* __restrict__ cell_count, uint32_t* __restrict__ perm) {
-  const uint32_t i0 = blockIdx.x * (blockDim.x * kBinItems) + threadIdx.x;
-  uint32_t k[kBinItems], old[kBinItems];
-  unsigned peers[kBinItems];
+  const uint32_t n = dc->n_slots;
+  const uint32_t stride = gridDim.x * blockDim.x * kBinItems;
+  for (uint32_t i0 = blockIdx.x * (blockDim.x * kBinItems) + threadIdx.x; i0 - threadIdx.x < n; i0 += stride) {
+    uint32_t k[kBinItems], old[kBinItems];
+    unsigned peers[kBinItems];
 #pragma unroll
-  for (int u = 0; u < kBinItems; ++u) {
-    const uint32_t i = i0 + u * blockDim.x;
-    k[u] = i < n ? __ldg(key + i) : kDeadKey;
-  }
+    for (int u = 0; u < kBinItems; ++u) {
+      const uint32_t i = i0 + u * blockDim.x;
+      k[u] = i < n ? __ldg(key + i) : kDeadKey;
+    }
 #pragma unroll
-  for (int u = 0; u < kBinItems; ++u) {
-    peers[u] = __match_any_sync(FULL, k[u]);
-    const int leader = __ffs(peers[u]) - 1;
-    old[u] = 0;
-    if (k[u] != kDeadKey && (int)(threadIdx.x & 31) == leader)
-      old[u] = atomicSub(&cell_count[k[u]], (uint32_t)__popc(peers[u]));
-  }
+    for (int u = 0; u < kBinItems; ++u) {
+      peers[u] = __match_any_sync(FULL, k[u]);
+      const int leader = __ffs(peers[u]) - 1;
+      old[u] = 0;
+      if (k[u] != kDeadKey && (int)(threadIdx.x & 31) == leader)
+        old[u] = atomicSub(&cell_count[k[u]], (uint32_t)__popc(peers[u]));
+    }
 #pragma unroll
-  for (int u = 0; u < kBinItems; ++u) {
-    const int leader = __ffs(peers[u]) - 1;
-    const uint32_t top = __shfl_sync(FULL, old[u], leader);
-    if (k[u] != kDeadKey) perm[top - 1 - __popc(peers[u] & lanemask_lt())] = i0 + u * blockDim.x;
+    for (int u = 0; u < kBinItems; ++u) {
+      const int leader = __ffs(peers[u]) - 1;
+      const uint32_t top = __shfl_sync(FULL, old[u], leader);
+      if (k[u] != kDeadKey) perm[top - 1 - __popc(peers[u] & lanemask_lt())] = i0 + u * blockDim.x;
+    }
   }
 }
 
@@ -292,58 +296,6 @@ __global__ void k_grid_update(float4* __restrict__ mp, float4* __restrict__ gv,
 }
 
 // ============================================================== slab exchange (a8)
-// Particles of the sorted ranges [0, lo_end) (below the slab) and [hi_begin, n_sorted)
-// (above it) left this rank: copy their records (and ids) into the send buffers.
-__global__ void k_pack_leavers(const uint32_t* __restrict__ rec, const uint32_t* __restrict__ ids,
-                               const uint32_t* __restrict__ perm, const uint32_t* __restrict__ block_start,
-                               uint32_t lo_block, uint32_t hi_block, uint32_t nblocks, uint32_t W,
-                               uint32_t cap, uint32_t* __restrict__ send_dn, uint32_t* __restrict__ send_up,
-                               uint32_t* __restrict__ ids_dn, uint32_t* __restrict__ ids_up, DevCounters* dc) {
-  const uint32_t lo_end = block_start[lo_block], hi_begin = block_start[hi_block], n = block_start[nblocks];
-  const uint32_t n_up = n - hi_begin;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    dc->mig_dn = lo_end;
-    dc->mig_up = n_up;
-    dc->n_sorted = n;
-    if (lo_end > cap || n_up > cap) dc->mig_overflow += 1u;
-  }
-  const uint32_t total = min(lo_end, cap) + min(n_up, cap);
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total * W; t += gridDim.x * blockDim.x) {
-    const uint32_t q = t / W, w = t - q * W;
-    const bool dn = q < min(lo_end, cap);
-    const uint32_t slot = dn ? q : q - min(lo_end, cap);
-    const uint32_t src = perm[dn ? slot : hi_begin + slot];
-    (dn ? send_dn : send_up)[(size_t)slot * W + w] = rec[(size_t)src * W + w];
-    if (w == 0 && ids) (dn ? ids_dn : ids_up)[slot] = ids[src];
-  }
-}
-
-// Count the particles this rank owns (block inside the slab) for the second sort;
-// keys of the others become kDeadKey so the scatter drops them.
-template <int D>
-__global__ void k_recount(uint32_t* __restrict__ key, uint32_t n, SimDev S, uint32_t* __restrict__ block_count,
-                          uint32_t* __restrict__ cell_count) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t k = 0xffffffffu;
-  if (i < n) {
-    const uint32_t full = key[i];
-    if (full != kDeadKey) {
-      int bc[3];
-      block_coords<D>(full >> 6, S, bc);
-      if (bc[2] >= S.slab_bz0 && bc[2] < S.slab_bz1) {
-        k = full >> 6;
-      } else {
-        key[i] = kDeadKey;
-      }
-    }
-  }
-  const unsigned peers = __match_any_sync(FULL, k);
-  if (k != 0xffffffffu && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
-  const uint32_t full = k != 0xffffffffu ? key[i] : kDeadKey;
-  const unsigned cp = __match_any_sync(FULL, full);
-  if (full != kDeadKey && (threadIdx.x & 31) == (unsigned)(__ffs(cp) - 1)) atomicAdd(&cell_count[full], __popc(cp));
-}
-
 // Dense copy of one z block plane of a float4 node array (all nbx * nby blocks,
 // 64 nodes each; blocks without a pool slot read as zero).
 __global__ void k_plane_pack(const float4* __restrict__ src, const uint32_t* __restrict__ block_slot, SimDev S,
@@ -405,17 +357,14 @@ static cudaError_t sort_d(const StepBuffers& B, const SimDev& S, cudaStream_t st
   H(KScanTiles, 0);
   H(KScanApply, 1);
   k_scan_apply<D><<<B.ntiles, kScanThreads, 0, st>>>(B.block_count, S, B.tile_off, B.block_start, B.block_slot,
-                                                     B.active_list, B.touched_list, B.pool);
+                                                     B.active_list, B.touched_list, B.pool, B.dc);
   H(KScanApply, 0);
-  if (B.n) {
-    H(KCellScan, 1);
-    k_cell_scan<<<B.num_sms * 8, 256, 0, st>>>(B.cell_count, B.block_count, B.block_start, B.active_list, B.dc);
-    H(KCellScan, 0);
-    H(KBinScatter, 1);
-    k_bin_scatter<<<(B.n + 256 * kBinItems - 1) / (256 * kBinItems), 256, 0, st>>>(B.key, B.n, B.cell_count,
-                                                                                  B.perm);
-    H(KBinScatter, 0);
-  }
+  H(KCellScan, 1);
+  k_cell_scan<<<B.num_sms * 8, 256, 0, st>>>(B.cell_count, B.block_count, B.block_start, B.active_list, B.dc);
+  H(KCellScan, 0);
+  H(KBinScatter, 1);
+  k_bin_scatter<<<B.num_sms * 8, 256, 0, st>>>(B.key, B.dc, B.cell_count, B.perm);
+  H(KBinScatter, 0);
   return cudaGetLastError();
 }
 
@@ -423,14 +372,15 @@ cudaError_t launch_sort(int dim, const StepBuffers& B, const SimDev& S, cudaStre
   return dim == 3 ? sort_d<3>(B, S, st, Hk{hook, user}) : sort_d<2>(B, S, st, Hk{hook, user});
 }
 
-cudaError_t launch_p2g(const StepBuffers& B, const SimDev& S, const StepJit& J, cudaStream_t st, KernelHook hook,
-                       void* user) {
+cudaError_t launch_p2g(const StepBuffers& B, const SimDev& S, const StepJit& J, int part, cudaStream_t st,
+                       KernelHook hook, void* user) {
   Hk H{hook, user};
   H(KP2G, 1);
   SimDev Sv = S;
+  int pv = part;
   void* args[] = {(void*)&B.rec_in,      (void*)&B.perm, (void*)&B.cell_count, (void*)&B.block_start,
                   (void*)&B.active_list, (void*)&B.dc,   (void*)&B.block_slot, (void*)&B.mp,
-                  (void*)&Sv};
+                  (void*)&Sv,            (void*)&pv};
   cudaError_t e = jit_launch(J.p2g, J.p2g_ctas, J.p2g_threads, J.p2g_smem, st, args);
   H(KP2G, 0);
   return e;
@@ -448,55 +398,52 @@ cudaError_t launch_grid_update(int dim, const StepBuffers& B, const SimDev& S, c
   return cudaGetLastError();
 }
 
-cudaError_t launch_g2p(const StepBuffers& B, const SimDev& S, uint32_t salt, const StepJit& J, cudaStream_t st,
-                       KernelHook hook, void* user) {
+cudaError_t launch_g2p(const StepBuffers& B, const SimDev& S, const MigDev& M, const StepJit& J, int part,
+                       cudaStream_t st, KernelHook hook, void* user) {
   Hk H{hook, user};
   H(KG2P, 1);
   SimDev Sv = S;
-  uint32_t saltv = salt;
+  MigDev Mv = M;
+  int pv = part;
   void* args[] = {(void*)&B.rec_in, (void*)&B.rec_out, (void*)&B.perm, (void*)&B.ids_in, (void*)&B.ids_out,
                   (void*)&B.dbg, (void*)&B.key, (void*)&B.block_count, (void*)&B.cell_count, (void*)&B.block_start,
                   (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot, (void*)&B.gv, (void*)&Sv,
-                  (void*)&saltv};
+                  (void*)&Mv, (void*)&pv};
   cudaError_t e = jit_launch(J.g2p, J.g2p_ctas, J.g2p_threads, J.g2p_smem, st, args);
   H(KG2P, 0);
   return e;
 }
 
-cudaError_t launch_step(int dim, const StepBuffers& B, const SimDev& S, uint32_t salt, const StepJit& J,
+cudaError_t launch_step(int dim, const StepBuffers& B, const SimDev& S, const MigDev& M, const StepJit& J,
                         cudaStream_t st, KernelHook hook, void* user) {
   cudaError_t e = launch_sort(dim, B, S, st, hook, user);
-  if (!e) e = launch_p2g(B, S, J, st, hook, user);
+  if (!e) e = launch_p2g(B, S, J, 0, st, hook, user);
   if (!e) e = launch_grid_update(dim, B, S, J, st, hook, user);
-  if (!e) e = launch_g2p(B, S, salt, J, st, hook, user);
+  if (!e) e = launch_g2p(B, S, M, J, 0, st, hook, user);
   return e;
 }
 
-cudaError_t launch_bin_count(const uint32_t* rec, uint32_t first, uint32_t n, const SimDev& S, uint32_t* key,
-                             uint32_t* block_count, uint32_t* cell_count, int do_count, const StepJit& J,
-                             cudaStream_t st) {
+cudaError_t launch_bin_count(const uint32_t* rec, const uint32_t* ids, uint32_t first, uint32_t n, const SimDev& S,
+                             uint32_t* key, uint32_t* block_count, uint32_t* cell_count, int do_count,
+                             const MigDev& M, DevCounters* dc, const StepJit& J, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   SimDev Sv = S;
-  void* args[] = {(void*)&rec,         (void*)&first,      (void*)&n,       (void*)&Sv,
-                  (void*)&key,         (void*)&block_count, (void*)&cell_count, (void*)&do_count};
+  MigDev Mv = M;
+  void* args[] = {(void*)&rec, (void*)&ids, (void*)&first, (void*)&n, (void*)&Sv, (void*)&key,
+                  (void*)&block_count, (void*)&cell_count, (void*)&do_count, (void*)&Mv, (void*)&dc};
   return jit_launch(J.bin_count, (n + 255) / 256, 256, 0, st, args);
 }
 
-cudaError_t launch_pack_leavers(const StepBuffers& B, const SimDev& S, uint32_t W, uint32_t cap, uint32_t* send_dn,
-                                uint32_t* send_up, uint32_t* ids_dn, uint32_t* ids_up, int num_sms,
-                                cudaStream_t st) {
-  const uint32_t P = (uint32_t)S.nb[0] * (uint32_t)S.nb[1];
-  k_pack_leavers<<<num_sms * 4, 256, 0, st>>>(B.rec_in, B.ids_in, B.perm, B.block_start, (uint32_t)S.slab_bz0 * P,
-                                               (uint32_t)S.slab_bz1 * P, S.nblocks, W, cap, send_dn, send_up, ids_dn,
-                                               ids_up, B.dc);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_recount(const StepBuffers& B, const SimDev& S, uint32_t n, int num_sms, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  k_cell_reset<<<num_sms * 4, 256, 0, st>>>(B.cell_count, B.active_list, B.dc);  // pass-1 cursors
-  k_recount<3><<<(n + 255) / 256, 256, 0, st>>>(B.key, n, S, B.block_count, B.cell_count);
-  return cudaGetLastError();
+cudaError_t launch_append(uint32_t* rec, uint32_t* ids, float* dbg, uint64_t cap, const SimDev& S, uint32_t* key,
+                          uint32_t* block_count, uint32_t* cell_count, const MigDev& M, DevCounters* dc,
+                          const StepJit& J, cudaStream_t st) {
+  SimDev Sv = S;
+  MigDev Mv = M;
+  uint64_t capv = cap;
+  void* args[] = {(void*)&rec, (void*)&ids, (void*)&dbg, (void*)&capv, (void*)&Sv, (void*)&key,
+                  (void*)&block_count, (void*)&cell_count, (void*)&Mv, (void*)&dc};
+  return jit_launch(J.append, (unsigned)std::min<uint64_t>((2ull * M.cap + 255) / 256, (uint64_t)J.num_sms * 8), 256,
+                    0, st, args);
 }
 
 cudaError_t launch_plane(float4* nodes, const uint32_t* block_slot, const SimDev& S, int bz, float4* buf, int mode,
@@ -505,6 +452,44 @@ cudaError_t launch_plane(float4* nodes, const uint32_t* block_slot, const SimDev
     k_plane_pack<<<num_sms * 4, 256, 0, st>>>(nodes, block_slot, S, bz, buf);
   else
     k_plane_unpack<<<num_sms * 4, 256, 0, st>>>(nodes, block_slot, S, bz, buf, mode == 1);
+  return cudaGetLastError();
+}
+
+// read_state of a slab context: the live record slots (every slot of [0, n_slots) not in
+// the sorted dead list) in slot order: out[i] = the i-th live slot
+__global__ void k_live_slots(const uint32_t* __restrict__ dead_sorted, uint32_t n_dead, uint32_t n_slots,
+                             uint32_t* __restrict__ out) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_slots; s += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = n_dead;  // dead slots below s
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) / 2;
+      if (dead_sorted[mid] < s) lo = mid + 1; else hi = mid;
+    }
+    if (lo < n_dead && dead_sorted[lo] == s) continue;
+    out[s - lo] = s;
+  }
+}
+
+__global__ void k_gather_rows(const uint32_t* __restrict__ src, const uint32_t* __restrict__ slots, uint32_t n,
+                              uint32_t row, uint32_t* __restrict__ dst) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < (uint64_t)n * row;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = t / row, q = t - i * row;
+    dst[t] = src[(uint64_t)slots[i] * row + q];
+  }
+}
+
+cudaError_t launch_live_slots(const uint32_t* dead_sorted, uint32_t n_dead, uint32_t n_slots, uint32_t* out,
+                              int num_sms, cudaStream_t st) {
+  if (n_slots == 0) return cudaSuccess;
+  k_live_slots<<<num_sms * 8, 256, 0, st>>>(dead_sorted, n_dead, n_slots, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows(const uint32_t* src, const uint32_t* slots, uint32_t n, uint32_t row, uint32_t* dst,
+                               int num_sms, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_gather_rows<<<num_sms * 8, 256, 0, st>>>(src, slots, n, row, dst);
   return cudaGetLastError();
 }
 

@@ -44,13 +44,14 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // slab of z block planes [bz0, bz1) is the contiguous id range [bz0 P, bz1 P),
 // P = nbx * nby: after the counting sort, particles that left a rank's slab are the
 // sorted ranges below and above it.
+// (3D: table-local ids, the table starting at block plane S.tab_bz0)
 template <int D>
 __device__ __forceinline__ void block_coords(uint32_t b, const SimDev& S, int bc[3]) {
   if (D == 3) {
     bc[1] = (int)(b % (uint32_t)S.nb[1]);
     const uint32_t r = b / (uint32_t)S.nb[1];
     bc[0] = (int)(r % (uint32_t)S.nb[0]);
-    bc[2] = (int)(r / (uint32_t)S.nb[0]);
+    bc[2] = (int)(r / (uint32_t)S.nb[0]) + S.tab_bz0;
   } else {
     bc[1] = (int)(b % (uint32_t)S.nb[1]);
     bc[0] = (int)(b / (uint32_t)S.nb[1]);
@@ -60,7 +61,8 @@ __device__ __forceinline__ void block_coords(uint32_t b, const SimDev& S, int bc
 
 template <int D>
 __device__ __forceinline__ uint32_t block_id(const int c[3], const SimDev& S) {
-  if (D == 3) return ((uint32_t)c[2] * (uint32_t)S.nb[0] + (uint32_t)c[0]) * (uint32_t)S.nb[1] + (uint32_t)c[1];
+  if (D == 3)
+    return ((uint32_t)(c[2] - S.tab_bz0) * (uint32_t)S.nb[0] + (uint32_t)c[0]) * (uint32_t)S.nb[1] + (uint32_t)c[1];
   return (uint32_t)c[0] * (uint32_t)S.nb[1] + (uint32_t)c[1];
 }
 
@@ -103,6 +105,32 @@ __device__ __forceinline__ uint32_t key_of_fast(const float* x, const SimDev& S,
   return (block_id<D>(c, S) << 6) | local_node<D>(l);
 }
 
+// sort key from the base cell per axis (block id * 64 + cell in block)
+template <int D>
+__device__ __forceinline__ uint32_t key_from_base(const int b[3], const SimDev& S) {
+  int c[3] = {0, 0, 0}, l[3] = {0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    c[a] = b[a] >> Geo<D>::LB;
+    l[a] = b[a] & (Geo<D>::B - 1);
+  }
+  return (block_id<D>(c, S) << 6) | local_node<D>(l);
+}
+
+// z block plane of a full sort key (3D)
+__device__ __forceinline__ int key_bz(uint32_t key, const SimDev& S) {
+  return (int)((key >> 6) / ((uint32_t)S.nb[0] * (uint32_t)S.nb[1])) + S.tab_bz0;
+}
+
+// block plane bz of a particle relative to this rank's slab: 0 owned, -1 / +1 it left
+// downwards / upwards, 2 it jumped further (an error: CFL keeps migration to one hop)
+__device__ __forceinline__ int slab_side(int bz, const SimDev& S) {
+  if (bz >= S.slab_bz0 && bz < S.slab_bz1) return 0;
+  if (bz == S.slab_bz0 - 1 && S.slab_lo) return -1;
+  if (bz == S.slab_bz1 && S.slab_hi) return 1;
+  return 2;
+}
+
 // tile node t -> (global node coordinates) for a block with origin org
 template <int D>
 __device__ __forceinline__ void tile_node(int t, const int org[3], int node[3]) {
@@ -134,20 +162,16 @@ __device__ __forceinline__ void benign_state(float* s, const int org[3], float d
   }
 }
 
-// affine momentum matrix of one particle (Hu et al. 2018; DESIGN.md §2 Q15):
-//   aff = -dt V_p 4/dx^2 P(F)F^T + m_p C
-//   elastic (fixed corotated): P F^T = 2 mu (F - R) F^T + lambda (J - 1) J I
-//   fluid:                     P F^T = E (J - 1) I
+// the stress part of the affine momentum, -dt V_p 4/dx^2 P(F)F^T (Hu et al. 2018;
+// DESIGN.md §2 Q15), from the decoded F (elastic) or J (fluid, diagonal only)
 template <int D, int MAT>
-__device__ __forceinline__ void affine_of(const float* s, const SimDev& S, float aff[D * D]) {
-  constexpr int CO = 2 * D + (MAT == 1 ? 1 : D * D);  // offset of C
+__device__ __forceinline__ void stress_of(const float* s, const SimDev& S, float st[D * D]) {
   if (MAT == 1) {
-    const float J = s[2 * D];
-    const float p = S.stress_scale * S.E * (J - 1.0f);
+    const float p = S.stress_scale * S.E * (s[2 * D] - 1.0f);
 #pragma unroll
-    for (int i = 0; i < D * D; ++i) aff[i] = S.p_mass * s[CO + i];
+    for (int i = 0; i < D * D; ++i) st[i] = 0.0f;
 #pragma unroll
-    for (int a = 0; a < D; ++a) aff[a * D + a] += p;
+    for (int a = 0; a < D; ++a) st[a * D + a] = p;
   } else {
     const float* F = s + 2 * D;
     float R[D * D];
@@ -169,7 +193,7 @@ __device__ __forceinline__ void affine_of(const float* s, const SimDev& S, float
         float acc = 0.0f;
 #pragma unroll
         for (int k = 0; k < D; ++k) acc += (F[a * D + k] - R[a * D + k]) * F[b * D + k];
-        aff[a * D + b] = two_mu * acc + S.p_mass * s[CO + a * D + b] + (a == b ? diag : 0.0f);
+        st[a * D + b] = two_mu * acc + (a == b ? diag : 0.0f);
       }
   }
 }

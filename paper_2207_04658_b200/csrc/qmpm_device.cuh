@@ -72,10 +72,14 @@ struct SimDev {
   float mu, lambda;   // fixed corotated (elastic)
   float E;            // fluid: P F^T = E (J - 1) I
   int bound;
-  uint32_t nblocks;
+  uint32_t nblocks;   // blocks of this context's block table (slab: its planes + the ghost plane)
   // slab decomposition along z (3D): this rank owns block planes
-  // [slab_bz0, slab_bz1); slab_lo / slab_hi = a neighbour rank exists below / above
+  // [slab_bz0, slab_bz1); slab_lo / slab_hi = a neighbour rank exists below / above.
+  // The block table covers the block planes [tab_bz0, tab_bz1): the owned planes plus
+  // the ghost plane above (single GPU: all planes); block ids are table-local.
   int slab_bz0, slab_bz1, slab_lo, slab_hi;
+  int tab_bz0, tab_bz1;
+  uint32_t seed_lo, seed_hi;  // dither seed (reading Q5): G2P derives the step salt on the device
 };
 
 constexpr uint32_t kDeadKey = 0xffffffffu;  // sort key of a particle this rank does not own
@@ -97,8 +101,47 @@ struct DevCounters {
   unsigned int range_bits[kMaxScalars];  // max |value| per state scalar (float bits, >= 0)
   unsigned int next_p2g;      // dynamic work counters of P2G / G2P (active-list position),
   unsigned int next_g2p;      // reset by the scan every step
-  unsigned int pad;
+  unsigned int n_active_below;  // active blocks below the top owned plane (slab overlap split)
+  unsigned int next_p2g_top, next_g2p_top;  // work counters of the top-plane launches
+  // slab migration, all on the device (no host synchronisation per step):
+  unsigned int n_rec;         // record slots written by the last G2P (= its sorted particles)
+  unsigned int n_slots;       // record slots the next sort scans: n_rec + appended arrivals
+  unsigned int n_leave;       // particles that left the slab since the last sort (dead slots)
+  unsigned int status;        // sticky error bits (kStatus*), agreed by every rank each step
+  unsigned int gstep;         // number of the step in flight (1, 2, ...; the scan advances it), so
+  unsigned int pad2;          // a step's launches take no per-step argument (CUDA-graph replays)
 };
+
+// sticky device-side error bits (DevCounters::status; qmpm_read_state / qmpm_stats report them)
+constexpr unsigned kStatusMigOverflow = 1u;  // more leavers than a migration buffer holds
+constexpr unsigned kStatusCapacity = 2u;     // arrivals past max_particles
+constexpr unsigned kStatusTwoHop = 4u;       // a particle moved more than one slab in one step
+constexpr unsigned kStatusNonfinite = 8u;    // (host side) the encoder met non-finite values
+
+// header of a migration buffer (followed by `cap` records of W words): count, status
+struct MigHeader {
+  unsigned int count, status, pad0, pad1;
+};
+
+// Migration buffers of the slab decomposition: per direction
+// one contiguous buffer [MigHeader | cap records of W words | cap ids | cap pre-encode
+// rows of ns floats (QMPM_DEBUG_PREENCODE only)], exchanged whole (fixed size: the
+// exchange schedule never depends on data, so no rank waits on a host-side count and an
+// error on one rank cannot hang the others).
+struct MigDev {
+  unsigned char* send[2];        // [0] to the rank below, [1] to the rank above
+  const unsigned char* recv[2];  // [0] from the rank below, [1] from the rank above
+  uint32_t* dead_list;           // record slots whose particle left (read_state compaction)
+  uint32_t cap, dead_cap, W, ids;
+  uint32_t dbg_ns;               // 0, or the floats per pre-encode row carried along
+  uint32_t pad;
+};
+
+__host__ __device__ inline size_t mig_ids_off(const MigDev& M) { return 16u + (size_t)M.cap * M.W * 4u; }
+__host__ __device__ inline size_t mig_dbg_off(const MigDev& M) {
+  return mig_ids_off(M) + (M.ids ? (size_t)M.cap * 4u : 0u);
+}
+__host__ __device__ inline size_t mig_bytes_of(const MigDev& M) { return mig_dbg_off(M) + (size_t)M.cap * M.dbg_ns * 4u; }
 
 // ---------------------------------------------------------------- hashing (Q5)
 __device__ __forceinline__ uint32_t mix32(uint32_t x) {

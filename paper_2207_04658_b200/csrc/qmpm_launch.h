@@ -54,7 +54,7 @@ enum KernelId {
 
 // the NVRTC-specialised kernels of one layout and their launch configuration
 struct StepJit {
-  CUfunction bin_count, p2g, g2p;
+  CUfunction bin_count, p2g, g2p, append;
   int num_sms;
   unsigned p2g_ctas, g2p_ctas, p2g_threads, g2p_threads;
   size_t p2g_smem, g2p_smem;
@@ -64,27 +64,33 @@ struct StepJit {
 typedef void (*KernelHook)(void* user, int kernel_id, int begin);
 
 // whole step (single GPU)
-cudaError_t launch_step(int dim, const StepBuffers& B, const SimDev& S, uint32_t salt, const StepJit& J,
+cudaError_t launch_step(int dim, const StepBuffers& B, const SimDev& S, const MigDev& M, const StepJit& J,
                         cudaStream_t st, KernelHook hook, void* user);
-// the step's phases, for the slab decomposition (exchanges in between)
+// the step's phases, for the slab decomposition (exchanges in between); part: 0 all
+// active blocks, 1 those below the top owned block plane, 2 the top plane
 cudaError_t launch_sort(int dim, const StepBuffers& B, const SimDev& S, cudaStream_t st, KernelHook hook, void* user);
-cudaError_t launch_p2g(const StepBuffers& B, const SimDev& S, const StepJit& J, cudaStream_t st, KernelHook hook,
-                       void* user);
+cudaError_t launch_p2g(const StepBuffers& B, const SimDev& S, const StepJit& J, int part, cudaStream_t st,
+                       KernelHook hook, void* user);
 cudaError_t launch_grid_update(int dim, const StepBuffers& B, const SimDev& S, const StepJit& J, cudaStream_t st,
                                KernelHook hook, void* user);
-cudaError_t launch_g2p(const StepBuffers& B, const SimDev& S, uint32_t salt, const StepJit& J, cudaStream_t st,
-                       KernelHook hook, void* user);
-// keys (+ optional histogram) of records [first, first + n)
-cudaError_t launch_bin_count(const uint32_t* rec, uint32_t first, uint32_t n, const SimDev& S, uint32_t* key,
-                             uint32_t* block_count, uint32_t* cell_count, int do_count, const StepJit& J,
-                             cudaStream_t st);
-cudaError_t launch_pack_leavers(const StepBuffers& B, const SimDev& S, uint32_t W, uint32_t cap, uint32_t* send_dn,
-                                uint32_t* send_up, uint32_t* ids_dn, uint32_t* ids_up, int num_sms,
-                                cudaStream_t st);
-cudaError_t launch_recount(const StepBuffers& B, const SimDev& S, uint32_t n, int num_sms, cudaStream_t st);
+cudaError_t launch_g2p(const StepBuffers& B, const SimDev& S, const MigDev& M, const StepJit& J, int part,
+                       cudaStream_t st, KernelHook hook, void* user);
+// keys (+ optional histogram) of records [first, first + n); slab: routes out-of-slab records
+cudaError_t launch_bin_count(const uint32_t* rec, const uint32_t* ids, uint32_t first, uint32_t n, const SimDev& S,
+                             uint32_t* key, uint32_t* block_count, uint32_t* cell_count, int do_count,
+                             const MigDev& M, DevCounters* dc, const StepJit& J, cudaStream_t st);
+// append the arrivals of the received migration buffers (keys + histograms)
+cudaError_t launch_append(uint32_t* rec, uint32_t* ids, float* dbg, uint64_t cap, const SimDev& S, uint32_t* key,
+                          uint32_t* block_count, uint32_t* cell_count, const MigDev& M, DevCounters* dc,
+                          const StepJit& J, cudaStream_t st);
 // mode 0: pack plane bz of `nodes` into buf; 1: add buf into the plane; 2: store buf into the plane
 cudaError_t launch_plane(float4* nodes, const uint32_t* block_slot, const SimDev& S, int bz, float4* buf, int mode,
                          int num_sms, cudaStream_t st);
+// read_state compaction of a slab context
+cudaError_t launch_live_slots(const uint32_t* dead_sorted, uint32_t n_dead, uint32_t n_slots, uint32_t* out,
+                              int num_sms, cudaStream_t st);
+cudaError_t launch_gather_rows(const uint32_t* src, const uint32_t* slots, uint32_t n, uint32_t row, uint32_t* dst,
+                               int num_sms, cudaStream_t st);
 
 cudaError_t launch_iota(uint32_t* ids, uint32_t n, uint32_t first, cudaStream_t st);
 

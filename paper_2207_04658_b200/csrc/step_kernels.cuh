@@ -19,12 +19,51 @@
 
 namespace qmpm {
 
+// ------------------------------------------------------------------ slab migration
+// (MigDev / MigHeader: qmpm_device.cuh)
+__device__ __forceinline__ MigHeader* mig_hdr(unsigned char* b) { return reinterpret_cast<MigHeader*>(b); }
+__device__ __forceinline__ const MigHeader* mig_hdr(const unsigned char* b) {
+  return reinterpret_cast<const MigHeader*>(b);
+}
+__device__ __forceinline__ size_t mig_rec_off() { return sizeof(MigHeader); }
+
+// a particle whose base block plane lies outside this rank's slab: its record (and id)
+// go to the neighbour's send buffer; `slot` (nullable) is remembered as a dead slot
+template <int W>
+__device__ __forceinline__ void mig_push(const MigDev& M, DevCounters* dc, int side, const uint32_t* rec,
+                                         uint32_t id, uint32_t slot, const float* dbg_row) {
+  if (side != -1 && side != 1) {
+    atomicOr(&dc->status, kStatusTwoHop);
+    return;
+  }
+  unsigned char* buf = side > 0 ? M.send[1] : M.send[0];  // (no dynamic index into the param)
+  const uint32_t k = atomicAdd(&mig_hdr(buf)->count, 1u);
+  if (k >= M.cap) {
+    atomicOr(&dc->status, kStatusMigOverflow);
+    return;
+  }
+  uint32_t* dst = reinterpret_cast<uint32_t*>(buf + mig_rec_off()) + (size_t)k * W;
+#pragma unroll
+  for (int q = 0; q < W; ++q) dst[q] = rec[q];
+  if (M.ids) reinterpret_cast<uint32_t*>(buf + mig_ids_off(M))[k] = id;
+  if (M.dbg_ns && dbg_row) {
+    float* dd = reinterpret_cast<float*>(buf + mig_dbg_off(M)) + (size_t)k * M.dbg_ns;
+    for (uint32_t q = 0; q < M.dbg_ns; ++q) dd[q] = dbg_row[q];
+  }
+  const uint32_t dk = atomicAdd(&dc->n_leave, 1u);
+  if (dk < M.dead_cap) M.dead_list[dk] = slot;
+}
+
 // ------------------------------------------------------------------ a1: bin count
+// keys (+ histograms) of records [first, first + n); on a slab rank a record whose base
+// lies in a neighbour's slab is routed to it (first step after set_state: reading of
+// qmpm_create_slab, particles may start in an adjacent slab)
 template <class SP>
-__device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec, uint32_t first, uint32_t n,
-                                               const SimDev& S, uint32_t* __restrict__ key,
-                                               uint32_t* __restrict__ block_count,
-                                               uint32_t* __restrict__ cell_count, int do_count) {
+__device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec, const uint32_t* __restrict__ ids,
+                                               uint32_t first, uint32_t n, const SimDev& S,
+                                               uint32_t* __restrict__ key, uint32_t* __restrict__ block_count,
+                                               uint32_t* __restrict__ cell_count, int do_count, MigDev M,
+                                               DevCounters* dc) {
   constexpr int D = SP::D, W = SP::W;
   const uint32_t i = first + blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < first + n;
@@ -32,20 +71,98 @@ __device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec,
   if (valid) {
     uint32_t w[W + 1];
 #pragma unroll
-    for (int q = 0; q < W; ++q) w[q] = ((SP::XMASK >> q) & 1u) ? __ldg(rec + (size_t)i * W + q) : 0u;
+    for (int q = 0; q < W; ++q) w[q] = __ldg(rec + (size_t)i * W + q);
     w[W] = 0u;
     float x[3];
 #pragma unroll
     for (int a = 0; a < D; ++a) x[a] = sdec<SP>(w, a);
-    full = key_of<D>(x, S);
+    int bsv[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float fx;
+      bool o;
+      bsv[a] = base_fx(x[a], S.inv_dx, S.res[a], fx, o);
+    }
+    const int side = (D == 3 && (S.slab_lo | S.slab_hi)) ? slab_side(bsv[2] >> 2, S) : 0;
+    if (side == 0) {
+      full = key_from_base<D>(bsv, S);
+      k = full >> 6;
+    } else {
+      mig_push<W>(M, dc, side, w, ids ? ids[i] : 0u, i, nullptr);
+    }
     key[i] = full;
-    k = full >> 6;
   }
   if (!do_count) return;
   const unsigned peers = __match_any_sync(FULL, k);
-  if (valid && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
+  if (k != 0xffffffffu && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
   const unsigned cp = __match_any_sync(FULL, full);
-  if (valid && (threadIdx.x & 31) == (unsigned)(__ffs(cp) - 1)) atomicAdd(&cell_count[full], __popc(cp));
+  if (full != kDeadKey && (threadIdx.x & 31) == (unsigned)(__ffs(cp) - 1)) atomicAdd(&cell_count[full], __popc(cp));
+}
+
+// Arrivals from the two neighbours (their headers give the counts) are appended at the
+// record slots [n_rec, n_rec + arrivals) with their keys and histogram counts; n_slots
+// (the sort's slot range) becomes n_rec + arrivals.  The statuses the neighbours sent
+// are folded into this rank's sticky status.
+template <class SP>
+__device__ __forceinline__ void append_body(uint32_t* __restrict__ rec, uint32_t* __restrict__ ids, float* __restrict__ dbg,
+                                            uint64_t cap, const SimDev& S, uint32_t* __restrict__ key,
+                                            uint32_t* __restrict__ block_count, uint32_t* __restrict__ cell_count,
+                                            MigDev M, DevCounters* dc) {
+  constexpr int D = SP::D, W = SP::W;
+  const MigHeader* h0 = mig_hdr(M.recv[0]);
+  const MigHeader* h1 = mig_hdr(M.recv[1]);
+  const uint32_t c0 = min(h0->count, M.cap), c1 = min(h1->count, M.cap);
+  const uint32_t n0 = dc->n_rec;
+  const uint32_t arr = c0 + c1;
+  const uint32_t fit = (uint64_t)n0 + arr > cap ? (uint32_t)(cap - n0) : arr;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    dc->n_slots = n0 + fit;
+    const unsigned st = h0->status | h1->status | ((h0->count > M.cap || h1->count > M.cap) ? kStatusMigOverflow : 0u) |
+                        (fit < arr ? kStatusCapacity : 0u);
+    if (st) atomicOr(&dc->status, st);
+  }
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ((fit + 31u) & ~31u); t += gridDim.x * blockDim.x) {
+    const bool valid = t < fit;
+    uint32_t k = 0xffffffffu, full = kDeadKey;
+    if (valid) {
+      const int dir = t < c0 ? 0 : 1;
+      const uint32_t q = dir ? t - c0 : t;
+      const unsigned char* rb = dir ? M.recv[1] : M.recv[0];  // (no dynamic index into the param)
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(rb + mig_rec_off()) + (size_t)q * W;
+      uint32_t w[W + 1];
+#pragma unroll
+      for (int e = 0; e < W; ++e) w[e] = src[e];
+      w[W] = 0u;
+      const uint32_t slot = n0 + t;
+#pragma unroll
+      for (int e = 0; e < W; ++e) rec[(size_t)slot * W + e] = w[e];
+      if (ids) ids[slot] = reinterpret_cast<const uint32_t*>(rb + mig_ids_off(M))[q];
+      if (dbg && M.dbg_ns) {
+        const float* sd = reinterpret_cast<const float*>(rb + mig_dbg_off(M)) + (size_t)q * M.dbg_ns;
+        for (uint32_t e = 0; e < M.dbg_ns; ++e) dbg[(size_t)slot * M.dbg_ns + e] = sd[e];
+      }
+      float x[3];
+      int bsv[3] = {0, 0, 0};
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        x[a] = sdec<SP>(w, a);
+        float fx;
+        bool o;
+        bsv[a] = base_fx(x[a], S.inv_dx, S.res[a], fx, o);
+      }
+      if (slab_side(bsv[2] >> 2, S) == 0) {
+        full = key_from_base<D>(bsv, S);
+        k = full >> 6;
+      } else {
+        atomicOr(&dc->status, kStatusTwoHop);  // (CFL: one hop per step)
+      }
+      key[slot] = full;
+    }
+    const unsigned peers = __match_any_sync(FULL, k);
+    if (k != 0xffffffffu && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&block_count[k], __popc(peers));
+    const unsigned cp = __match_any_sync(FULL, full);
+    if (full != kDeadKey && (threadIdx.x & 31) == (unsigned)(__ffs(cp) - 1)) atomicAdd(&cell_count[full], __popc(cp));
+  }
 }
 
 // per-warp shared-memory footprint of the two step kernels (16-byte multiples)
@@ -165,7 +282,7 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
                                          const uint32_t* __restrict__ block_start,
                                          const uint32_t* __restrict__ active_list, DevCounters* __restrict__ dc,
                                          const uint32_t* __restrict__ block_slot, float4* __restrict__ mp,
-                                         const SimDev& S) {
+                                         const SimDev& S, int part) {
   constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, W = SP::W;
   constexpr int NN = D == 3 ? 27 : 9;  // stencil nodes
   using G = Geo<D>;
@@ -179,12 +296,22 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
   uint32_t* s_lstart = reinterpret_cast<uint32_t*>(wb + LY::LSTART);
   uint16_t* s_seg = reinterpret_cast<uint16_t*>(wb + LY::SEG);
   uint8_t* s_ns = reinterpret_cast<uint8_t*>(wb + LY::NS);
-  const uint32_t n_active = dc->n_active;
+  // part 0: every active block; 1: the blocks below the slab's top block plane; 2: the
+  // top plane only (whose partial sums reach the ghost plane: launched first so the
+  // exchange overlaps part 1)
+  const uint32_t lo = part == 2 ? dc->n_active_below : 0u;
+  const uint32_t hi = part == 1 ? dc->n_active_below : dc->n_active;
+  unsigned* ctr = part == 2 ? &dc->next_p2g_top : &dc->next_p2g;
+  if (part != 2 && blockIdx.x == 0 && threadIdx.x == 0) {
+    // the sort has consumed the slots [0, n_slots): G2P writes the n_sorted particles
+    dc->n_rec = dc->n_slots = dc->n_sorted;
+    dc->n_leave = 0u;
+  }
   for (;;) {  // blocks are taken dynamically (a work counter): no tail from uneven blocks
     uint32_t ab = 0;
-    if (lane == 0) ab = atomicAdd(&dc->next_p2g, 1u);
+    if (lane == 0) ab = lo + atomicAdd(ctr, 1u);
     ab = __shfl_sync(FULL, ab, 0);
-    if (ab >= n_active) break;
+    if (ab >= hi) break;
     const uint32_t b = active_list[ab];
     const uint32_t start = block_start[b], end = block_start[b + 1];
     int bc[3];
@@ -314,31 +441,53 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
         uint32_t w[W + 1];
         read_staged<SP>(ring + slot * 32 * W, w);
         slot = slot == 2 ? 0 : slot + 1;
+        // Decode what P2G needs.  Its values are never re-encoded, so a FIXED field's Eq. 3
+        // scaling u * Delta is folded into its consumer's constant (one multiply by
+        // Delta * p_mass (* dx) instead of two or three), and fx / the base cell come from
+        // the integer x codes (exact, as in G2P's next-step key, Spec::XK)
+        constexpr int CO = 2 * D + (MAT == 1 ? 1 : D * D);  // first C scalar
         float s[NSV];
 #pragma unroll
-        for (int i = 0; i < NSV; ++i) s[i] = sdec<SP>(w, i);
+        for (int i = 0; i < NSV; ++i)
+          if (i >= 2 * D && i < CO) s[i] = sdec<SP>(w, i);  // F or J: the stress
         float fx[3] = {0.f, 0.f, 0.f};
         {
           bool oob = false;
+          if (SP::XK > 0) {
 #pragma unroll
-          for (int a = 0; a < D; ++a) base_fx_fast(s[a], S.inv_dx, S.res[a], fx[a], oob);
+            for (int a = 0; a < D; ++a) {
+              const int u = scode<SP>(w, a);
+              const int bs = (u - (1 << (SP::XK - 1))) >> SP::XK;
+              oob |= (unsigned)bs > (unsigned)(S.res[a] - 3);
+              fx[a] = __fmul_rn(__int2float_rn(u - (bs << SP::XK)), __int_as_float((127 - SP::XK) << 23));
+            }
+          } else {
+#pragma unroll
+            for (int a = 0; a < D; ++a) base_fx_fast(sdec<SP>(w, a), S.inv_dx, S.res[a], fx[a], oob);
+          }
           if (oob) {  // rare (per lane, no warp vote in this divergent loop): reading Q14's clamp
 #pragma unroll
             for (int a = 0; a < D; ++a) {
               bool o;
-              base_fx(s[a], S.inv_dx, S.res[a], fx[a], o);
+              base_fx(sdec<SP>(w, a), S.inv_dx, S.res[a], fx[a], o);
             }
           }
         }
-        float aff[D * D];
-        affine_of<D, MAT>(s, S, aff);
+        auto folds = [](int i) { return SP::kind(i) == kKindFixed && SP::offset(i) == 0.0f; };
+        const float pm = S.p_mass, pmdx = S.p_mass * S.dx;
+        float st[D * D];
+        stress_of<D, MAT>(s, S, st);  // -dt V_p 4/dx^2 P F^T
         float Q[3] = {0.f, 0.f, 0.f}, A[3][3];
 #pragma unroll
         for (int a = 0; a < D; ++a) {
-          Q[a] = S.p_mass * s[D + a];
+          // m_p v
+          Q[a] = folds(D + a) ? __int2float_rn(scode<SP>(w, D + a)) * (SP::delta(D + a) * pm) : pm * sdec<SP>(w, D + a);
 #pragma unroll
           for (int k2 = 0; k2 < D; ++k2) {
-            A[k2][a] = S.dx * aff[a * D + k2];
+            // A[k][a] = dx (stress + m_p C)[a][k] (the APIC/MLS affine momentum)
+            const int ci = CO + a * D + k2;
+            const float mc = folds(ci) ? __int2float_rn(scode<SP>(w, ci)) * (SP::delta(ci) * pmdx) : pmdx * sdec<SP>(w, ci);
+            A[k2][a] = (MAT == 1 && a != k2) ? mc : fmaf(S.dx, st[a * D + k2], mc);
             Q[a] = fmaf(-fx[k2], A[k2][a], Q[a]);
           }
         }
@@ -509,7 +658,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
                                          uint32_t* __restrict__ cell_count, const uint32_t* __restrict__ block_start,
                                          const uint32_t* __restrict__ active_list, DevCounters* __restrict__ dc,
                                          const uint32_t* __restrict__ block_slot, const float4* __restrict__ gv,
-                                         const SimDev& S, uint32_t salt) {
+                                         const SimDev& S, const MigDev& M, int part) {
   constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, W = SP::W;
   constexpr int CO = 2 * D + (MAT == 1 ? 1 : D * D);
   using G = Geo<D>;
@@ -524,14 +673,20 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
   rc.init();
   unsigned rmax = 0u;  // range recording (float bits of max |value|, lane i: scalar i)
   unsigned c_sat = 0, c_nf = 0, c_oob = 0;
-  const uint32_t n_active = dc->n_active;
   const float four_inv_dx = 4.0f * S.inv_dx;
+  // the step's dither salt (reading Q5): steps numbered 1, 2, ... (Q20), advanced by the scan
+  const uint32_t salt = step_salt(S.seed_lo, S.seed_hi, dc->gstep);
+  // part 0: every active block; 1: below the top block plane; 2: the top plane (the one
+  // reading the ghost plane's velocities: launched after the velocity exchange)
+  const uint32_t lo = part == 2 ? dc->n_active_below : 0u;
+  const uint32_t hi = part == 1 ? dc->n_active_below : dc->n_active;
+  unsigned* ctr = part == 2 ? &dc->next_g2p_top : &dc->next_g2p;
 
   for (;;) {  // blocks are taken dynamically (a work counter): no tail from uneven blocks
     uint32_t ab = 0;
-    if (lane == 0) ab = atomicAdd(&dc->next_g2p, 1u);
+    if (lane == 0) ab = lo + atomicAdd(ctr, 1u);
     ab = __shfl_sync(FULL, ab, 0);
-    if (ab >= n_active) break;
+    if (ab >= hi) break;
     const uint32_t b = active_list[ab];
     const uint32_t start = block_start[b], end = block_start[b + 1];
     int bc[3];
@@ -550,7 +705,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
     if (lane < (1 << D)) {
       int nbk[3] = {bc[0] + (lane & 1), bc[1] + ((lane >> 1) & 1), D == 3 ? bc[2] + ((lane >> 2) & 1) : 0};
       uint32_t sl = 0xffffffffu;
-      if (nbk[0] < S.nb[0] && nbk[1] < S.nb[1] && nbk[2] < S.nb[2]) sl = block_slot[block_id<D>(nbk, S)];
+      if (nbk[0] < S.nb[0] && nbk[1] < S.nb[1] && (D == 2 || nbk[2] < S.tab_bz1)) sl = block_slot[block_id<D>(nbk, S)];
       nslot[lane] = sl;
     }
     __syncwarp();
@@ -739,7 +894,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       uint32_t ow[W + 1];
 #pragma unroll
       for (int q = 0; q <= W; ++q) ow[q] = 0u;
-      bool flag = false, zero = false;
+      bool flag = false;
       int xc[3] = {0, 0, 0};  // x codes (next step's key)
       uint32_t pu_save[RoundCounters<SP>::NP], pz_save[RoundCounters<SP>::NP];
       if (SP::COUNTERS) {
@@ -756,8 +911,9 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         if (role == 2) continue;
         if (role == 1) {  // packed pair (i, i + 1), one pair hash when they share one (Q5 rev. 3)
           int ui, uj, sbi, sbj;
+          bool zi, zj;
           senc_pair_fast<SP>(i, i + 1, o[i], o[i + 1], dither_s(h, SP::idx(i)), dither_s(h, SP::idx(i + 1)), ui, uj,
-                             sbi, sbj, flag, zero);
+                             sbi, sbj, flag, zi, zj);
           sput_code<SP>(ow, i, ui);
           sput_code<SP>(ow, i + 1, uj);
           if (i < D) xc[i] = ui;
@@ -765,15 +921,21 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
           if (SP::COUNTERS) {
             rc.pu[i / 4] += (uint32_t)sbi << (8 * (i % 4));
             rc.pu[(i + 1) / 4] += (uint32_t)sbj << (8 * ((i + 1) % 4));
+            if (zi) rc.pz[i / 4] += 1u << (8 * (i % 4));
+            if (zj) rc.pz[(i + 1) / 4] += 1u << (8 * ((i + 1) % 4));
           }
           continue;
         }
         if (fast_ok<SP>(i)) {
           int sb;
-          const int u = senc1_fast<SP>(i, o[i], dither_s(h, SP::idx(i)), sb, flag, zero);
+          bool z;
+          const int u = senc1_fast<SP>(i, o[i], dither_s(h, SP::idx(i)), sb, flag, z);
           sput_code<SP>(ow, i, u);
           if (i < D) xc[i] = u;
-          if (SP::COUNTERS) rc.pu[i / 4] += (uint32_t)sb << (8 * (i % 4));
+          if (SP::COUNTERS) {
+            rc.pu[i / 4] += (uint32_t)sb << (8 * (i % 4));
+            if (z) rc.pz[i / 4] += 1u << (8 * (i % 4));
+          }
           continue;
         }
         if (SP::kind(i) == kKindShared) {  // reading Q4: the whole group at its leader
@@ -828,12 +990,6 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
           if (lane == i) c_sat += __popc(bs);
           if (lane == 0) c_nf += __popc(bn);
         }
-      } else if (SP::COUNTERS && SP::DITHER && __any_sync(FULL, zero)) {
-        // rare (after the first steps): on-grid values of the packed fast path, counted as
-        // neither up nor down (a value on the grid never rounds up: 1 - r > 0)
-#pragma unroll
-        for (int i = 0; i < NSV; ++i)
-          if (fast_ok<SP>(i) && on_grid_fast<SP>(i, o[i])) rc.pz[i / 4] += 1u << (8 * (i % 4));
       }
       if (SP::COUNTERS && ++rc.n_since == 255u) rc.flush(lane);
       if (SP::RANGES) {  // Alg. 1 line 9: max |value| of s_{t+1} per state scalar (lane i keeps scalar i)
@@ -851,38 +1007,52 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       // powers-of-two scalings (Spec::XK = log2(dx / Delta) > 0: base = floor(u 2^-XK - 1/2),
       // bit-identical to floor(fl(fl(u Delta) / dx) - 1/2)), else from the re-decoded x
       uint32_t nkey;
+      bool leave = false;
       {
+        int bsv[3] = {0, 0, 0};
         bool koob = false;
         if (SP::XK > 0) {
-          int c[3] = {0, 0, 0}, l[3] = {0, 0, 0};
 #pragma unroll
           for (int a = 0; a < D; ++a) {
-            const int bs = (xc[a] - (1 << (SP::XK - 1))) >> SP::XK;
-            koob |= (unsigned)bs > (unsigned)(S.res[a] - 3);
-            c[a] = bs >> G::LB;
-            l[a] = bs & (G::B - 1);
+            bsv[a] = (xc[a] - (1 << (SP::XK - 1))) >> SP::XK;
+            koob |= (unsigned)bsv[a] > (unsigned)(S.res[a] - 3);
           }
-          nkey = (block_id<D>(c, S) << 6) | local_node<D>(l);
         } else {
           float xq[3];
 #pragma unroll
-          for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
-          nkey = key_of_fast<D>(xq, S, koob);
+          for (int a = 0; a < D; ++a) {
+            xq[a] = sdec<SP>(ow, a);
+            float fq;
+            bsv[a] = base_fx_fast(xq[a], S.inv_dx, S.res[a], fq, koob);
+          }
         }
         if (__any_sync(FULL, valid && koob)) {  // rare: clamped base (Q14)
           float xq[3];
 #pragma unroll
-          for (int a = 0; a < D; ++a) xq[a] = sdec<SP>(ow, a);
-          nkey = key_of<D>(xq, S);
+          for (int a = 0; a < D; ++a) {
+            xq[a] = sdec<SP>(ow, a);
+            float fq;
+            bool o;
+            bsv[a] = base_fx(xq[a], S.inv_dx, S.res[a], fq, o);
+          }
         }
+        // slab ranks: a particle whose new base block plane is a neighbour's leaves
+        int side = 0;
+        if (D == 3 && (S.slab_lo | S.slab_hi)) side = slab_side(bsv[2] >> G::LB, S);
+        leave = valid && side != 0;
+        nkey = side == 0 ? key_from_base<D>(bsv, S) : kDeadKey;
+        if (__any_sync(FULL, leave) && leave)
+          mig_push<W>(M, dc, side, ow, ids_out != nullptr ? ids_in[r] : 0u, j,
+                   dbg != nullptr ? dbg + (size_t)j * NSV : nullptr);
       }
       if (valid) key_out[j] = nkey;
       {  // next step's histograms, one atomic per distinct key of the warp
-        const uint32_t nk = valid ? (nkey >> 6) : 0xffffffffu;
+        const bool cnt_it = valid && !leave;
+        const uint32_t nk = cnt_it ? (nkey >> 6) : 0xffffffffu;
         const unsigned kp = __match_any_sync(FULL, nk);
-        if (valid && lane == __ffs(kp) - 1) atomicAdd(&block_count[nk], (unsigned)__popc(kp));
-        const unsigned cp = __match_any_sync(FULL, valid ? nkey : kDeadKey);
-        if (valid && lane == __ffs(cp) - 1) atomicAdd(&cell_count[nkey], (unsigned)__popc(cp));
+        if (cnt_it && lane == __ffs(kp) - 1) atomicAdd(&block_count[nk], (unsigned)__popc(kp));
+        const unsigned cp = __match_any_sync(FULL, cnt_it ? nkey : kDeadKey);
+        if (cnt_it && lane == __ffs(cp) - 1) atomicAdd(&cell_count[nkey], (unsigned)__popc(cp));
       }
       if (valid) {
         if (ids_out != nullptr) ids_out[j] = ids_in[r];
@@ -929,24 +1099,32 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
 // per-warp shared-memory bytes of P2G and G2P, read by the host after loading the module
 extern "C" __device__ const unsigned qmpm_smem_per_warp[2] = {(unsigned)qmpm::P2GLayout<Spec>::BYTES,
                                                              (unsigned)qmpm::Smem<Spec>::G2P_WARP};
-extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t* rec, uint32_t first, uint32_t n,
-                                                                 qmpm::SimDev S, uint32_t* key, uint32_t* block_count,
-                                                                 uint32_t* cell_count, int do_count) {
-  qmpm::bin_count_body<Spec>(rec, first, n, S, key, block_count, cell_count, do_count);
+extern "C" __global__ void __launch_bounds__(256) qmpm_bin_count(const uint32_t* rec, const uint32_t* ids, uint32_t first,
+                                                                 uint32_t n, qmpm::SimDev S, uint32_t* key,
+                                                                 uint32_t* block_count, uint32_t* cell_count,
+                                                                 int do_count, qmpm::MigDev M, qmpm::DevCounters* dc) {
+  qmpm::bin_count_body<Spec>(rec, ids, first, n, S, key, block_count, cell_count, do_count, M, dc);
+}
+
+extern "C" __global__ void __launch_bounds__(256) qmpm_append(uint32_t* rec, uint32_t* ids, float* dbg, uint64_t cap,
+                                                              qmpm::SimDev S, uint32_t* key, uint32_t* block_count,
+                                                              uint32_t* cell_count, qmpm::MigDev M,
+                                                              qmpm::DevCounters* dc) {
+  qmpm::append_body<Spec>(rec, ids, dbg, cap, S, key, block_count, cell_count, M, dc);
 }
 
 extern "C" __global__ void __launch_bounds__(Spec::P2G_WARPS * 32, Spec::P2G_MINB)
     qmpm_p2g(const uint32_t* rec, const uint32_t* perm, uint32_t* cell_count, const uint32_t* block_start,
              const uint32_t* active_list, qmpm::DevCounters* dc, const uint32_t* block_slot, float4* mp,
-             qmpm::SimDev S) {
-  qmpm::p2g_body<Spec>(rec, perm, cell_count, block_start, active_list, dc, block_slot, mp, S);
+             qmpm::SimDev S, int part) {
+  qmpm::p2g_body<Spec>(rec, perm, cell_count, block_start, active_list, dc, block_slot, mp, S, part);
 }
 
 extern "C" __global__ void __launch_bounds__(Spec::G2P_WARPS * 32, Spec::G2P_MINB)
     qmpm_g2p(const uint32_t* rec_in, uint32_t* rec_out, const uint32_t* perm, const uint32_t* ids_in,
              uint32_t* ids_out, float* dbg, uint32_t* key_out, uint32_t* block_count, uint32_t* cell_count,
              const uint32_t* block_start, const uint32_t* active_list, qmpm::DevCounters* dc,
-             const uint32_t* block_slot, const float4* gv, qmpm::SimDev S, uint32_t salt) {
+             const uint32_t* block_slot, const float4* gv, qmpm::SimDev S, qmpm::MigDev M, int part) {
   qmpm::g2p_body<Spec>(rec_in, rec_out, perm, ids_in, ids_out, dbg, key_out, block_count, cell_count, block_start,
-                       active_list, dc, block_slot, gv, S, salt);
+                       active_list, dc, block_slot, gv, S, M, part);
 }

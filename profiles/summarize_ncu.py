@@ -1,10 +1,12 @@
 """Summarise an ncu report: key metrics, stall reasons and the SASS opcode mix per kernel.
 
-    python profiles/summarize_ncu.py gpurun_out/prof.ncu-rep [--traffic-json profiles/ncu_traffic.json]
-        > profiles/<round>_<name>.txt
+    python profiles/summarize_ncu.py gpurun_out/prof.ncu-rep [--traffic-json profiles/ncu_traffic.json
+                                                              --config c4] > profiles/<round>_<name>.txt
 
---traffic-json writes dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes)
-for each kernel ("p2g", "g2p", ...), the `traffic` term bench.py reports.
+--traffic-json merges, under the bench config name, per kernel ("p2g", "g2p", ...) the
+dram__bytes_read.sum + dram__bytes_write.sum of one launch (bench.py's roofline `traffic`)
+and its executed warp instructions (bench.py's `issue_frac`: instructions / (launch time x
+148 SMs x 4 schedulers x SM clock)).
 """
 import json
 import collections
@@ -26,7 +28,7 @@ def run(args):
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
-def main(rep, traffic_json=None):
+def main(rep, traffic_json=None, config="c4"):
     traffic = {}
     rows = list(csv.reader(io.StringIO(run(["-i", rep, "--page", "details", "--csv"]))))
     h = rows[0]
@@ -46,7 +48,7 @@ def main(rep, traffic_json=None):
         try:
             tb = sum(float(d[kk].replace(",", "")) * UNIT.get(units.get(kk, "byte"), 1.0)
                      for kk in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-            traffic[k.replace("qmpm_", "").replace("qmpm::k_", "")] = tb
+            traffic[k.replace("qmpm_", "").replace("qmpm::k_", "")] = {"traffic": tb}
             print(f"   {'dram read+write per launch (bytes)':60s} {tb:.4e}")
         except (KeyError, ValueError):
             pass
@@ -93,15 +95,25 @@ def main(rep, traffic_json=None):
                 stl[op] += st
                 tot += ex
                 tst += st
+            kk = k.replace("qmpm_", "").replace("qmpm::k_", "")
+            traffic.setdefault(kk, {})["warp_inst"] = tot
             print(f"   SASS executed (warp instr): {tot}; top opcodes:")
             for op, c in ops.most_common(14):
                 print(f"      {op:10s} {100 * c / max(tot, 1):5.1f}% of instr  {100 * stl[op] / max(tst, 1):5.1f}% of stall samples")
 
 
     if traffic_json:
-        json.dump(traffic, open(traffic_json, "w"), indent=1)
+        try:
+            allc = json.load(open(traffic_json))
+        except (OSError, ValueError):
+            allc = {}
+        if not all(isinstance(v, dict) for v in allc.values()) or any("traffic" in v for v in allc.values()):
+            allc = {}  # (an older per-kernel file)
+        allc[config] = traffic
+        json.dump(allc, open(traffic_json, "w"), indent=1)
 
 
 if __name__ == "__main__":
     tj = sys.argv[sys.argv.index("--traffic-json") + 1] if "--traffic-json" in sys.argv else None
-    main(sys.argv[1], tj)
+    cfg = sys.argv[sys.argv.index("--config") + 1] if "--config" in sys.argv else "c4"
+    main(sys.argv[1], tj, cfg)

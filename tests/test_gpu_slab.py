@@ -137,3 +137,52 @@ def test_slab_validation():
         s.step(1)  # no transport
     assert e.value.code == 9
     s.close()
+
+
+def test_migration_overflow_is_a_sticky_error_not_a_hang():
+    """A migration buffer too small for the step's leavers (migrate_capacity = 1): the
+    exchange still runs its fixed schedule (no rank waits on a count), the device status
+    becomes ECAPACITY at the next synchronising call, and further steps are refused until
+    the state is set again (SURVEY §8(b) error semantics)."""
+    sc, sch = scenes.small_fluid_3d(), schemes.f2()
+    w0, _ = oracle.encode_state(sch, sc.state())
+    slabs = cuts(sc.sim["grid_res"][2], 2)
+    st = oracle.decode_state(sch, w0)
+    own = owner(st, sc.sim, slabs)
+    stream = torch.cuda.Stream()
+    sims = []
+    for r, (z0, z1) in enumerate(slabs):
+        idx = np.nonzero(own == r)[0]
+        s = qmpm.Sim(sc.sim, sch, w0.shape[0], stream=stream, slab=(2, r, z0, z1), migrate_capacity=1)
+        # everything to rank 0: rank 1's particles must all migrate (far more than 1)
+        s.set_words(dev(w0[idx] if r == 0 else w0[idx]), 0)
+        sims.append(s)
+    # rank 1 also gets rank 0's particles: its first step routes them (overflow)
+    sims[1].set_words(dev(w0[np.nonzero(own == 0)[0][:5000]]), 0)
+    qmpm.step_group(sims, 1)  # returns: fixed schedule, no hang
+    with pytest.raises(qmpm.QmpmError) as e:
+        sims[1].stats()
+    assert e.value.code == 8  # ECAPACITY
+    with pytest.raises(qmpm.QmpmError) as e:
+        qmpm.step_group(sims, 1)
+    assert e.value.code == 9  # ESTATE until set_state / set_words
+    for s in sims:
+        s.close()
+
+
+def test_nonfinite_state_is_reported():
+    """a non-finite value is an error value -- it is encoded as code 0 and counted,
+    and read_state reports QMPM_ENONFINITE (the state is still read)."""
+    sc, sch = scenes.small_fluid_3d(), schemes.f2()
+    st = sc.state()
+    st[7, 3] = np.nan
+    sim = qmpm.Sim(sc.sim, sch, st.shape[0])
+    sim.set_state(dev(st))
+    w = np.zeros((st.shape[0], sim.W), np.uint32)
+    with pytest.raises(qmpm.QmpmError) as e:
+        sim.read_state(words=w)
+    assert e.value.code == 6
+    assert oracle.decode_state(sch, w[7:8])[0, 3] == 0.0
+    sim.set_state(dev(sc.state()))  # a fresh state clears it
+    sim.read_state(words=w)
+    sim.close()
