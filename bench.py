@@ -418,7 +418,10 @@ def run_gpu(args):
                    "particles_total": sc.n_particles,
                    "scheme": scheme_name(args), "record_bytes": S, "rounding": args.rounding,
                    "round_counters": not args.no_counters, "scene_warmup_steps": args.scene_warmup,
-                   "l2": f"state {N * S / 1e9:.1f} GB per buffer >> 126 MB L2: no flush needed",
+                   "l2": (f"state {N * S / 1e9:.1f} GB per buffer >> 126 MB L2: no flush needed"
+                          if N * S > 1e9 else
+                          f"state {N * S / 1e6:.1f} MB fits in L2 and is not flushed: a launch/latency-bound "
+                          "side line (BASELINE configs[0]/[1]), not the headline"),
                    "parallelism": "single GPU" if world == 1 else
                    f"z-slab decomposition over {world} GPUs (ghost-plane + velocity halo + migration over NCCL)",
                    "baseline_ref": "vs_baseline = per-GPU value / the paper's RTX 3090 T-large rate for this workload "

@@ -42,10 +42,12 @@ enum {
     QMPM_ENOMEM = 3,     /* device allocation failed */
     QMPM_ECUDA = 4,      /* CUDA runtime error */
     QMPM_ENCCL = 5,      /* NCCL error in the slab exchange */
-    QMPM_ENONFINITE = 6, /* reserved: non-finite values are counted in qmpm_stats */
-    QMPM_EDOMAIN = 7,    /* reserved: out-of-domain particles are counted in qmpm_stats */
-    QMPM_ECAPACITY = 8,  /* n > max_particles, or grid pool overflow during a step */
-    QMPM_ESTATE = 9      /* call not valid in the ctx's current state */
+    QMPM_ENONFINITE = 6, /* the encoder met non-finite values (encoded as code 0, counted) */
+    QMPM_EDOMAIN = 7,    /* a particle moved more than one slab in a step; the error-bounded
+                            solver cannot meet its bound within b_max.  (Particles whose base
+                            leaves the grid are clamped and only counted: S:263, Q14.) */
+    QMPM_ECAPACITY = 8,  /* n > max_particles, grid pool or migration buffer overflow */
+    QMPM_ESTATE = 9      /* call not valid in the ctx's current state (e.g. a sticky error) */
 };
 
 /* Field kinds.  FIXED: Eq. 3, u = round(v/Delta) stored as frac_bits+1-bit
@@ -169,26 +171,35 @@ qmpm_status qmpm_set_words(qmpm_ctx* ctx, uint64_t n, const uint32_t* words, uin
 qmpm_status qmpm_set_ids(qmpm_ctx* ctx, uint64_t n, const uint32_t* ids);
 
 /* Advance n_steps MLS-MPM steps (decode -> bin -> P2G -> grid update -> G2P ->
- * dithered encode), asynchronously on the ctx stream; allocates nothing. */
+ * dithered encode), asynchronously on the ctx stream; allocates nothing and never
+ * synchronises.  Single GPU: one CUDA-graph launch per step (captured on first use per
+ * ping-pong parity; QMPM_NO_GRAPH=1 or qmpm_set_profiling(1) launch kernel by kernel).
+ * Device-side conditions (non-finite values met by the encoder, migration overflow,
+ * capacity, a two-slab jump) set a sticky status that the next synchronising call
+ * (qmpm_read_state, qmpm_stats) reports as QMPM_ENONFINITE / QMPM_ECAPACITY /
+ * QMPM_EDOMAIN; qmpm_step then returns QMPM_ESTATE until qmpm_set_state / set_words. */
 qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps);
 
 /* Read the current particles (synchronizes).  vals: [n][n_scalars] decoded fp32
  * (nullable); words: [n][W] packed records (nullable); ids: [n] (nullable; needs
  * QMPM_TRACK_IDS).  All host or device.  Particles are in the library's storage
- * order (sorted by grid block after a step); use ids to match them.  *n_out = n;
- * QMPM_ECAPACITY if capacity < n. */
+ * order (sorted by grid block after a step); use ids to match them.  *n_out = n
+ * (a slab rank: the particles it owns now, migrants received, leavers excluded);
+ * QMPM_ECAPACITY if capacity < n.  The outputs are filled before a sticky error
+ * (see qmpm_step) is returned. */
 qmpm_status qmpm_read_state(qmpm_ctx* ctx, float* vals, uint32_t* words, uint32_t* ids,
                             uint64_t capacity, uint64_t* n_out);
 /* The last step's fp32 state BEFORE the encode (needs QMPM_DEBUG_PREENCODE), in
  * the same order as qmpm_read_state.  Synchronizes. */
 qmpm_status qmpm_read_debug(qmpm_ctx* ctx, float* pre_encode_vals, uint64_t capacity,
                             uint64_t* n_out);
-qmpm_status qmpm_stats(qmpm_ctx* ctx, qmpm_stats_t* out); /* synchronizes */
+qmpm_status qmpm_stats(qmpm_ctx* ctx, qmpm_stats_t* out); /* synchronizes; fills *out, then
+                                                            returns the sticky error if any */
 
 /* Standalone codec (Eq. 3 / Eq. 11 + bit pack) on device arrays, enqueued on
  * cuda_stream.  vals: [n][n_fields] fp32 in PACKING order; words: [n][W].
  * keys: nullable => round-half-even; else dithered with r24(seed, step, keys[i],
- * field) when scheme->rounding == QMPM_DITHER.  The scheme's dim/material are not
+ * field) of reading Q5 rev. 3 when scheme->rounding == QMPM_DITHER.  The scheme's dim/material are not
  * used and attr/comp are not checked.  counters (nullable, device, 3*64 u64,
  * accumulated): saturations, round-ups, round-downs per field. */
 qmpm_status qmpm_encode(const qmpm_scheme* scheme, uint64_t n, const float* vals,
@@ -209,7 +220,7 @@ qmpm_status qmpm_codec_matmul3(const qmpm_scheme* scheme, uint64_t n, const uint
  * kernel with CUDA events on the ctx stream.  qmpm_kernel_times (synchronizes)
  * returns, for each of the QMPM_NUM_KERNELS kernels in the order of
  * qmpm_kernel_name(i), the summed milliseconds and launch count since enabling. */
-#define QMPM_NUM_KERNELS 8
+#define QMPM_NUM_KERNELS 9
 qmpm_status qmpm_set_profiling(qmpm_ctx* ctx, int enabled);
 qmpm_status qmpm_kernel_times(qmpm_ctx* ctx, double* ms, uint64_t* launches);
 const char* qmpm_kernel_name(int i);
@@ -225,7 +236,8 @@ uint64_t qmpm_launch_count(const qmpm_ctx* ctx);
 typedef struct {
     int32_t nranks, rank;
     int32_t z0, z1;            /* owned cell planes [z0, z1): multiples of 4 (z1 may be grid_res[2]) */
-    uint64_t migrate_capacity; /* particles per direction per step; 0 = max(65536, max_particles/64) */
+    uint64_t migrate_capacity; /* particles per direction per step (the fixed migration buffer);
+                                  0 = max(65536, min(max_particles / 256, 2^22)) */
 } qmpm_slab;
 
 /* Like qmpm_create, for rank `slab->rank` of `slab->nranks` (3D only).  Particles
@@ -235,9 +247,12 @@ qmpm_status qmpm_create_slab(const qmpm_params* params, const qmpm_scheme* schem
                              const qmpm_slab* slab, qmpm_ctx** out);
 /* NCCL transport (one process per GPU): rank 0 creates the unique id, the caller
  * broadcasts it (e.g. torch.distributed), every rank connects; qmpm_step then
- * exchanges halos and migrants with grouped ncclSend/ncclRecv on the ctx stream
- * (host-synchronising once per step for the migration counts).  QMPM_ENCCL on
- * failure (including a missing libnccl.so.2). */
+ * exchanges, with grouped ncclSend/ncclRecv of FIXED sizes (the schedule never depends
+ * on data; no host synchronisation): the ghost-plane partial sums (on a comm stream,
+ * overlapping the interior P2G), the velocity plane (overlapping the interior G2P) and
+ * the migration buffers, plus an all-reduce of the sticky status so that every rank
+ * reports an error at its next synchronising call.  QMPM_ENCCL on failure (including a
+ * missing libnccl.so.2). */
 qmpm_status qmpm_get_unique_id(uint8_t id[128]);
 qmpm_status qmpm_connect_nccl(qmpm_ctx* ctx, const uint8_t id[128]);
 /* The one-call form: qmpm_create_slab for rank `rank` of `nranks` with

@@ -403,7 +403,8 @@ qmpm_status encode_rows(qmpm_ctx* ctx, uint64_t first, uint64_t n, const float* 
     CK(cudaMemcpyAsync(tmp, vals, sizeof(float) * ctx->ns * n, cudaMemcpyDefault, ctx->stream));
     dv = tmp;
   }
-  ctx->launches_total += 1;
+  ctx->launches_total += 2;
+  CK(launch_count_nonfinite(dv, n * (uint64_t)ctx->ns, &ctx->dc->nonfinite, ctx->jit.num_sms, ctx->stream));
   qmpm_status rc = codec_run(ctx, ctx->C, 0, n, dv, nullptr, nullptr, 0u, nullptr, ctx->rec[ctx->cur] + first * ctx->W,
                              (unsigned long long*)ctx->dc, nullptr, ctx->stream);
   if (rc) return rc;
@@ -668,7 +669,8 @@ qmpm_status create_impl(const qmpm_params* params, const qmpm_scheme* scheme, vo
     const int kP2GMinBlocks = env_int("QMPM_P2G_MINB", ctx->material == QMPM_FLUID_J ? 5 : 6),
               kG2PMinBlocks = env_int("QMPM_G2P_MINB", (d == 3 && ctx->material == QMPM_ELASTIC_FCR) ? 3 : 4);
     const int xk = env_int("QMPM_FLOAT_KEY", 0) ? 0 : integer_key_shift(d, ctx->L, S.inv_dx);
-    ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps, kP2GMinBlocks, kG2PMinBlocks, xk);
+    ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps, kP2GMinBlocks, kG2PMinBlocks, xk,
+                               slab != nullptr && slab->nranks > 1);
     JitModule m;
     std::string jerr;
     e = jit_get(ctx->jit_src, m, jerr);
@@ -1000,7 +1002,8 @@ qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps) {
       qmpm_status rc = rebin(ctx);
       if (rc) return rc;
     }
-    if (!ctx->prof && ctx->use_graphs) {
+    if (!ctx->prof && ctx->use_graphs && ctx->stream != nullptr && ctx->stream != cudaStreamLegacy &&
+        ctx->stream != cudaStreamPerThread) {
       // one CUDA-graph launch per step: the step's launches take no per-step argument
       // (the dither salt comes from the device step counter), so one graph per ping-pong
       // parity replays for the ctx's lifetime
@@ -1014,9 +1017,14 @@ qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps) {
         if (!e) e = e2;
         if (!e) e = cudaGraphInstantiate(&g, graph, 0);
         if (graph) cudaGraphDestroy(graph);
-        if (e) {
+        if (e) {  // (e.g. a stream already being captured by the caller): plain launches
+          cudaGetLastError();
           g = nullptr;
-          return fail(ctx, QMPM_ECUDA, "step graph capture: %s", cudaGetErrorString(e));
+          ctx->use_graphs = false;
+          StepBuffers B2 = buffers(ctx, ctx->n);
+          CK(launch_step(ctx->dim, B2, ctx->S, mig_of(ctx), ctx->jit, ctx->stream, hook_fn, ctx));
+          finish_step(ctx);
+          continue;
         }
       }
       CK(cudaGraphLaunch(g, ctx->stream));

@@ -136,7 +136,7 @@ int integer_key_shift(int dim, const LayoutDev& L, float inv_dx) {
 }
 
 std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps, int g2p_warps, int p2g_minb,
-                        int g2p_minb, int xk) {
+                        int g2p_minb, int xk, bool slab) {
   std::string s;
   char buf[1024];
   const int ns = (int)L.ns;
@@ -144,8 +144,10 @@ std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps
            "struct Spec {\n  static constexpr int D = %d, MAT = %d, NS = %d, W = %u, SW = %u;\n"
            "  static constexpr int P2G_WARPS = %d, G2P_WARPS = %d, P2G_MINB = %d, G2P_MINB = %d;\n"
            "  static constexpr unsigned XMASK = %uu;\n  static constexpr int XK = %d;\n"
+           "  static constexpr bool SLAB = %s;\n"
            "  static constexpr bool DITHER = %s, COUNTERS = %s, RANGES = %s;\n",
            dim, material, ns, L.W, L.SW, p2g_warps, g2p_warps, p2g_minb, g2p_minb, L.xword_mask, xk,
+           slab ? "true" : "false",
            L.dither ? "true" : "false",
            L.counters ? "true" : "false", L.ranges ? "true" : "false");
   s += buf;

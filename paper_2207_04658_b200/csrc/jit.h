@@ -20,7 +20,7 @@ struct JitModule {
 // the generated preamble + #include of step_kernels.cuh for one layout; xk = log2(dx / Delta_x)
 // when the next-step key can come from the integer x codes (0: from the decoded floats)
 std::string spec_source(int dim, int material, const LayoutDev& L, int p2g_warps, int g2p_warps, int p2g_minb,
-                        int g2p_minb, int xk);
+                        int g2p_minb, int xk, bool slab);
 // xk of spec_source for a layout and a cell size (api.cu)
 int integer_key_shift(int dim, const LayoutDev& L, float inv_dx);
 cudaError_t jit_get(const std::string& src, JitModule& out, std::string& err);

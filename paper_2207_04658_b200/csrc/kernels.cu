@@ -493,6 +493,23 @@ cudaError_t launch_gather_rows(const uint32_t* src, const uint32_t* slots, uint3
   return cudaGetLastError();
 }
 
+// qmpm_set_state / append_state: non-finite input values (an error value; the
+// encoder stores code 0) are counted into DevCounters::nonfinite
+__global__ void k_count_nonfinite(const float* __restrict__ v, uint64_t n, unsigned long long* __restrict__ out) {
+  unsigned c = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    c += !isfinite(v[i]);
+  c = __reduce_add_sync(FULL, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+cudaError_t launch_count_nonfinite(const float* vals, uint64_t n, unsigned long long* out, int num_sms,
+                                   cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_count_nonfinite<<<num_sms * 4, 256, 0, st>>>(vals, n, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_iota(uint32_t* ids, uint32_t n, uint32_t first, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   k_iota<<<(n + 255) / 256, 256, 0, st>>>(ids, n, first);

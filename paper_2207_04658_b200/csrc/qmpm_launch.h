@@ -93,5 +93,7 @@ cudaError_t launch_gather_rows(const uint32_t* src, const uint32_t* slots, uint3
                                int num_sms, cudaStream_t st);
 
 cudaError_t launch_iota(uint32_t* ids, uint32_t n, uint32_t first, cudaStream_t st);
+cudaError_t launch_count_nonfinite(const float* vals, uint64_t n, unsigned long long* out, int num_sms,
+                                   cudaStream_t st);
 
 }  // namespace qmpm

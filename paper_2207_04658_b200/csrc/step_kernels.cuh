@@ -83,7 +83,7 @@ __device__ __forceinline__ void bin_count_body(const uint32_t* __restrict__ rec,
       bool o;
       bsv[a] = base_fx(x[a], S.inv_dx, S.res[a], fx, o);
     }
-    const int side = (D == 3 && (S.slab_lo | S.slab_hi)) ? slab_side(bsv[2] >> 2, S) : 0;
+    const int side = (SP::SLAB && D == 3) ? slab_side(bsv[2] >> 2, S) : 0;
     if (side == 0) {
       full = key_from_base<D>(bsv, S);
       k = full >> 6;
@@ -395,14 +395,19 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     // ---- 2. the fetch cursor walks this lane's segments of all groups ahead of the
     // compute: fidx = pidx[fk] is loaded one fetch ahead, and the next segment's first
     // index (nidx) a whole segment ahead (it starts a new cache line)
-    uint32_t fk, fe, fidx = 0u, nk, ne, nidx = 0u, fg = 1;
+    // fidx / fidx1: the record indices of particles fk and fk + 1 (two fetches ahead: the
+    // index load's latency is covered by two particles' compute, not one -- measured, the
+    // one-ahead form stalled on it); nidx / nidx1 the same for the next segment
+    uint32_t fk, fe, fidx = 0u, fidx1 = 0u, nk, ne, nidx = 0u, nidx1 = 0u, fg = 1;
     int fslot = 0, slot = 0;
     {
       int c_;
       seg_range(lane, fk, fe, c_);
       if (fk < fe) fidx = __ldg(pidx + fk);
+      if (fk + 1 < fe) fidx1 = __ldg(pidx + fk + 1);
       seg_range(32 + lane, nk, ne, c_);
       if (nk < ne) nidx = __ldg(pidx + nk);
+      if (nk + 1 < ne) nidx1 = __ldg(pidx + nk + 1);
     }
     auto fetch = [&]() {
       if (fk < fe) {
@@ -412,12 +417,15 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
           fk = nk;
           fe = ne;
           fidx = nidx;
+          fidx1 = nidx1;
           fg += 1;
           int c_;
           seg_range(fg * 32 + lane, nk, ne, c_);
           if (nk < ne) nidx = __ldg(pidx + nk);
+          if (nk + 1 < ne) nidx1 = __ldg(pidx + nk + 1);
         } else {
-          fidx = __ldg(pidx + fk);
+          fidx = fidx1;
+          if (fk + 1 < fe) fidx1 = __ldg(pidx + fk + 1);
         }
       }
       cp_async_commit();
@@ -1038,10 +1046,10 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         }
         // slab ranks: a particle whose new base block plane is a neighbour's leaves
         int side = 0;
-        if (D == 3 && (S.slab_lo | S.slab_hi)) side = slab_side(bsv[2] >> G::LB, S);
+        if (SP::SLAB && D == 3) side = slab_side(bsv[2] >> G::LB, S);  // (compiled out on one GPU)
         leave = valid && side != 0;
         nkey = side == 0 ? key_from_base<D>(bsv, S) : kDeadKey;
-        if (__any_sync(FULL, leave) && leave)
+        if (SP::SLAB && __any_sync(FULL, leave) && leave)
           mig_push<W>(M, dc, side, ow, ids_out != nullptr ? ids_in[r] : 0u, j,
                    dbg != nullptr ? dbg + (size_t)j * NSV : nullptr);
       }

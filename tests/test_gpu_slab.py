@@ -155,10 +155,14 @@ def test_migration_overflow_is_a_sticky_error_not_a_hang():
         idx = np.nonzero(own == r)[0]
         s = qmpm.Sim(sc.sim, sch, w0.shape[0], stream=stream, slab=(2, r, z0, z1), migrate_capacity=1)
         # everything to rank 0: rank 1's particles must all migrate (far more than 1)
-        s.set_words(dev(w0[idx] if r == 0 else w0[idx]), 0)
+        s.set_words(dev(w0[idx]), 0)
         sims.append(s)
-    # rank 1 also gets rank 0's particles: its first step routes them (overflow)
-    sims[1].set_words(dev(w0[np.nonzero(own == 0)[0][:5000]]), 0)
+    # rank 1 gets particles of rank 0's top block plane (one hop down): its first step
+    # routes thousands of them into a buffer of one record
+    zb = np.floor(st[:, 2].astype(np.float64) / sc.sim["dx"] - 0.5).astype(np.int64)
+    top0 = np.nonzero((own == 0) & (zb >= slabs[0][1] - 4))[0]
+    assert top0.size > 100
+    sims[1].set_words(dev(w0[top0]), 0)
     qmpm.step_group(sims, 1)  # returns: fixed schedule, no hang
     with pytest.raises(qmpm.QmpmError) as e:
         sims[1].stats()
