@@ -395,19 +395,14 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     // ---- 2. the fetch cursor walks this lane's segments of all groups ahead of the
     // compute: fidx = pidx[fk] is loaded one fetch ahead, and the next segment's first
     // index (nidx) a whole segment ahead (it starts a new cache line)
-    // fidx / fidx1: the record indices of particles fk and fk + 1 (two fetches ahead: the
-    // index load's latency is covered by two particles' compute, not one -- measured, the
-    // one-ahead form stalled on it); nidx / nidx1 the same for the next segment
-    uint32_t fk, fe, fidx = 0u, fidx1 = 0u, nk, ne, nidx = 0u, nidx1 = 0u, fg = 1;
+    uint32_t fk, fe, fidx = 0u, nk, ne, nidx = 0u, fg = 1;
     int fslot = 0, slot = 0;
     {
       int c_;
       seg_range(lane, fk, fe, c_);
       if (fk < fe) fidx = __ldg(pidx + fk);
-      if (fk + 1 < fe) fidx1 = __ldg(pidx + fk + 1);
       seg_range(32 + lane, nk, ne, c_);
       if (nk < ne) nidx = __ldg(pidx + nk);
-      if (nk + 1 < ne) nidx1 = __ldg(pidx + nk + 1);
     }
     auto fetch = [&]() {
       if (fk < fe) {
@@ -417,15 +412,12 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
           fk = nk;
           fe = ne;
           fidx = nidx;
-          fidx1 = nidx1;
           fg += 1;
           int c_;
           seg_range(fg * 32 + lane, nk, ne, c_);
           if (nk < ne) nidx = __ldg(pidx + nk);
-          if (nk + 1 < ne) nidx1 = __ldg(pidx + nk + 1);
         } else {
-          fidx = fidx1;
-          if (fk + 1 < fe) fidx1 = __ldg(pidx + fk + 1);
+          fidx = __ldg(pidx + fk);
         }
       }
       cp_async_commit();

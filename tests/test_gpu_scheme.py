@@ -34,10 +34,38 @@ def test_record_ranges_equal_max_of_preencode_state(case):
         np.testing.assert_array_equal(r, step_max if t == 3 else run_max)
         if t == 2:
             run_max[:] = 0.0
-    # against the oracle's pre-encode state of the same step (P2 tolerance of the values)
-    w = np.zeros((n, sim.W), np.uint32)
-    sim.read_state(words=w)
     sim.close()
+
+
+@pytest.mark.parametrize("case", ["c1", "fluid", "elastic"])
+def test_record_ranges_match_oracle_preencode_maxima(case):
+    """Alg. 1 line 9 against the ORACLE: one step from oracle-warmed words; the recorded
+    max |value| per state scalar equals the maximum over particles of the fp64 oracle's
+    pre-encode state within the P2 tolerance of the values (1e-5 of the conditioning-aware
+    scale): a range recorded from the wrong stage (decoded input, post-encode) or the
+    wrong scalar misses it by far more."""
+    from test_gpu_step import REL, scales
+    if case == "c1":
+        sc, sch = scenes.c1(), schemes.x16()
+    elif case == "fluid":
+        sc, sch = scenes.small_fluid_3d(), schemes.f2()
+    else:
+        sc, sch = scenes.small_elastic_3d(), schemes.e01()
+    w0, _ = oracle.encode_state(sch, sc.state())
+    w_in, _ = oracle.run(sc.sim, sch, w0, 1, 12)
+    o_pre, _, _ = oracle.step(sc.sim, sch, w_in, 13)
+    n = w_in.shape[0]
+    sim = qmpm.Sim(sc.sim, sch, n, flags=qmpm.RECORD_RANGES)
+    sim.set_words(dev(w_in.view(np.int32)), 12)
+    sim.step(1)
+    r = sim.read_ranges(reset=True).astype(np.float64)
+    sim.close()
+    o_max = np.abs(o_pre).max(axis=0)
+    s_h = scales(sc.sim, o_pre, oracle.decode_state(sch, w_in))
+    assert np.all(np.abs(r - o_max) <= REL * np.maximum(o_max, s_h)), (r, o_max)
+    # and it is not the decoded input's maximum (the state did change)
+    i_max = np.abs(oracle.decode_state(sch, w_in)).max(axis=0)
+    assert np.any(np.abs(i_max - o_max) > REL * np.maximum(o_max, s_h))
 
 
 def test_scheme_derivation_pipeline():
