@@ -250,15 +250,16 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 // Momentum at stencil node o of a particle: m v + aff (o - fx) dx = Q + sum_k o_k a_k,
 // a_k = dx aff[:, k], Q = m v - sum_k fx_k a_k (Hu et al. 2018 APIC/MLS form).
 #ifndef QMPM_SEG_L
-#define QMPM_SEG_L 16
+#define QMPM_SEG_L 32
 #endif
 #ifndef QMPM_SEG_LMIN
-#define QMPM_SEG_LMIN 16
+#define QMPM_SEG_LMIN 32
 #endif
 // particles per P2G segment (one lane, one group): n_blk / 128 clamped to [kSegLmin, kSegL]
 // (QMPM_SEG_LMIN < QMPM_SEG_L shortens the segments of sparse blocks so every lane gets
-// work; measured on B200 the fixed length 16 is as fast at C4 and 2.5 % faster at C3,
-// 8 ppc, than a floor of 8 -- fewer per-group flushes beat the better lane balance)
+// work; measured on B200: at C4 (~72 ppc) P2G takes 7.15 / 7.07 / 6.99 ms with segments
+// of 16 / 24 / 32 particles -- fewer per-group tile updates; at 8 ppc every cell is one
+// tail segment whatever the length, and a floor of 8 was 2.5 % slower there than 16)
 constexpr int kSegL = QMPM_SEG_L;
 constexpr int kSegLmin = QMPM_SEG_LMIN < QMPM_SEG_L ? QMPM_SEG_LMIN : QMPM_SEG_L;
 constexpr int kSegLev = 32;        // segments per cell at most (the last one takes the rest)

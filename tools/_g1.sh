@@ -1,16 +1,11 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-timeout 1800 python -m pytest tests/test_gpu_slab.py tests/test_gpu_step.py -q -p no:cacheprovider > gpurun_out/t1.log 2>&1; echo "tests rc=$?"
-grep -E "passed|failed|FAILED|Error" gpurun_out/t1.log | tail -10
-for mb in 5 6; do
-QMPM_P2G_MINB=$mb timeout 900 python bench.py --steps 20 --warmup 5 --no-e2e --cpu-sample 1000 --cpu-steps 1 > gpurun_out/b_mb$mb.log 2>&1; echo "bench minb=$mb rc=$?"
-tail -1 gpurun_out/b_mb$mb.log | python -c "
+run() { tag=$1; shift; env "$@" timeout 900 python bench.py --steps 20 --warmup 5 --no-e2e --cpu-sample 1000 --cpu-steps 1 > gpurun_out/tune_$tag.log 2>&1
+tail -1 gpurun_out/tune_$tag.log | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); k=d['kernels']
-print('%.3e'%d['value'], 'ms %.2f'%d['ms_per_step'], 'p2g %.3f g2p %.3f'%(k['p2g']['ms_per_step'], k['g2p']['ms_per_step']))"
-done
-QMPM_P2G_MINB=6 timeout 900 python bench.py --config c3 --steps 20 --warmup 5 --no-e2e --cpu-sample 1000 --cpu-steps 1 > gpurun_out/b_c3mb6.log 2>&1; echo "bench c3 minb6 rc=$?"
-timeout 900 python bench.py --config c3 --steps 20 --warmup 5 --no-e2e --cpu-sample 1000 --cpu-steps 1 > gpurun_out/b_c3.log 2>&1; echo "bench c3 rc=$?"
-for f in c3mb6 c3; do tail -1 gpurun_out/b_$f.log | python -c "
-import json,sys
-d=json.loads(sys.stdin.read()); k=d['kernels']
-print('$f', '%.3e'%d['value'], 'ms %.2f'%d['ms_per_step'], 'p2g %.3f g2p %.3f'%(k['p2g']['ms_per_step'], k['g2p']['ms_per_step']))"; done
+print('$tag', '%.4e'%d['value'], 'ms %.3f'%d['ms_per_step'], 'p2g %.3f g2p %.3f scat %.3f'%(k['p2g']['ms_per_step'], k['g2p']['ms_per_step'], k['bin_scatter']['ms_per_step']))" ; }
+run base X=1
+run g2p5 QMPM_G2P_MINB=5
+run segl24 "QMPM_JIT_OPTS=-DQMPM_SEG_L=24 -DQMPM_SEG_LMIN=24"
+run segl32 "QMPM_JIT_OPTS=-DQMPM_SEG_L=32 -DQMPM_SEG_LMIN=32"
+run p2g7 QMPM_P2G_MINB=7
