@@ -665,8 +665,9 @@ qmpm_status create_impl(const qmpm_params* params, const qmpm_scheme* scheme, vo
       return (v && *v) ? atoi(v) : dflt;
     };
     // (3D elastic G2P holds F and C: 3 CTAs x 168 registers beat 4 x 128 with spills;
-    // P2G measured: fluid C4 7.21 ms at 5 vs 7.32 at 6, elastic C3 12.6 ms at 6 vs 13.0 at 5)
-    const int kP2GMinBlocks = env_int("QMPM_P2G_MINB", ctx->material == QMPM_FLUID_J ? 5 : 6),
+    // P2G: 6 CTAs x 168 registers -- at 5 ptxas also stops at 168 but spills 20 bytes
+    // (measured equal, 7.33 ms at C4), at 7 it spills heavily (14.7 ms))
+    const int kP2GMinBlocks = env_int("QMPM_P2G_MINB", 6),
               kG2PMinBlocks = env_int("QMPM_G2P_MINB", (d == 3 && ctx->material == QMPM_ELASTIC_FCR) ? 3 : 4);
     const int xk = env_int("QMPM_FLOAT_KEY", 0) ? 0 : integer_key_shift(d, ctx->L, S.inv_dx);
     ctx->jit_src = spec_source(d, ctx->material, ctx->L, kP2GWarps, kG2PWarps, kP2GMinBlocks, kG2PMinBlocks, xk,

@@ -416,7 +416,14 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
           fg += 1;
           int c_;
           seg_range(fg * 32 + lane, nk, ne, c_);
-          if (nk < ne) nidx = __ldg(pidx + nk);
+          if (nk < ne) {
+            nidx = __ldg(pidx + nk);
+            // the next segment's indices (contiguous, <= L): into L1 a segment ahead, so the
+            // one-ahead index loads of its particles hit (ncu: the index latency was the top
+            // stall of the loop; records bypass L1 with cp.async.cg)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pidx + nk + 1));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pidx + ne - 1));
+          }
         } else {
           fidx = __ldg(pidx + fk);
         }
@@ -785,55 +792,59 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       float Sv[3] = {0.f, 0.f, 0.f}, T[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
       const int base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
       if (D == 3) {
-        // packed FP32x2 (sm_100 FFMA2 / FMUL2): pair 0 = (v_x, v_y), pair 1 = (v_z, 0) of a
-        // node; each lane is the same IEEE op the scalar form does
+        // packed FP32x2 (sm_100 FFMA2 / FMUL2; each lane is the IEEE op the scalar form does):
+        // (v_x, v_y) of a node as one pair through every level; v_z, which would waste half
+        // a pair, carries its two z-moments instead: (sum_oz w v_z, sum_oz w oz v_z) with the
+        // weight pairs (w0, 0), (w1, w1), (w2, 2 w2), then (S, T_z) pairs up the y and x levels
         const float wz0 = wt[2][0], wz1 = wt[2][1], wz2 = wt[2][2], wz2x2 = 2.0f * wt[2][2];
-        float2 sv[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        float2 tx[2] = {sv[0], sv[0]}, tyy[2] = {sv[0], sv[0]}, tzz[2] = {sv[0], sv[0]};
+        const float2 wzp0 = make_float2(wz0, 0.0f), wzp1 = make_float2(wz1, wz1), wzp2 = make_float2(wz2, wz2x2);
+        float2 sv = make_float2(0.f, 0.f), tx = sv, tyy = sv, tzz = sv;
+        float2 svz = sv;  // (sum w v_z, T[2][2])
+        float tyz = 0.f, txz = 0.f;
 #pragma unroll
         for (int ox = 0; ox < 3; ++ox) {
-          float2 sy[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, ty[2] = {sy[0], sy[0]},
-                 tzy[2] = {sy[0], sy[0]};
+          float2 sy = make_float2(0.f, 0.f), ty = sy, tzy = sy, syz = sy;
+          float tyzo = 0.f;
 #pragma unroll
           for (int oy = 0; oy < 3; ++oy) {
             const int idx = base_idx + (ox * G::T + oy) * G::T;
             const float4 g0 = tile[idx], g1 = tile[idx + 1], g2 = tile[idx + 2];
-            const float2 ga[3][2] = {{make_float2(g0.x, g0.y), make_float2(g0.z, g0.w)},
-                                     {make_float2(g1.x, g1.y), make_float2(g1.z, g1.w)},
-                                     {make_float2(g2.x, g2.y), make_float2(g2.z, g2.w)}};
             const float wy = wt[1][oy], wyo = wt[1][oy] * oy;
-#pragma unroll
-            for (int pp = 0; pp < 2; ++pp) {
-              const float2 p1 = __fmul2_rn(make_float2(wz1, wz1), ga[1][pp]);
-              const float2 tz = __ffma2_rn(make_float2(wz2x2, wz2x2), ga[2][pp], p1);  // sum_oz w oz g
-              const float2 sz = __ffma2_rn(make_float2(wz0, wz0), ga[0][pp],
-                                           __ffma2_rn(make_float2(wz2, wz2), ga[2][pp], p1));  // sum_oz w g
-              sy[pp] = __ffma2_rn(make_float2(wy, wy), sz, sy[pp]);
-              tzy[pp] = __ffma2_rn(make_float2(wy, wy), tz, tzy[pp]);
-              if (oy) ty[pp] = __ffma2_rn(make_float2(wyo, wyo), sz, ty[pp]);
-            }
+            const float2 a0 = make_float2(g0.x, g0.y), a1 = make_float2(g1.x, g1.y), a2 = make_float2(g2.x, g2.y);
+            const float2 p1 = __fmul2_rn(make_float2(wz1, wz1), a1);
+            const float2 tz = __ffma2_rn(make_float2(wz2x2, wz2x2), a2, p1);  // sum_oz w oz g
+            const float2 sz = __ffma2_rn(make_float2(wz0, wz0), a0,
+                                         __ffma2_rn(make_float2(wz2, wz2), a2, p1));  // sum_oz w g
+            sy = __ffma2_rn(make_float2(wy, wy), sz, sy);
+            tzy = __ffma2_rn(make_float2(wy, wy), tz, tzy);
+            if (oy) ty = __ffma2_rn(make_float2(wyo, wyo), sz, ty);
+            const float2 z = __ffma2_rn(wzp2, make_float2(g2.z, g2.z),
+                                        __ffma2_rn(wzp1, make_float2(g1.z, g1.z),
+                                                   __fmul2_rn(wzp0, make_float2(g0.z, g0.z))));
+            syz = __ffma2_rn(make_float2(wy, wy), z, syz);
+            if (oy) tyzo = fmaf(wyo, z.x, tyzo);
           }
           const float wx = wt[0][ox], wxo = wt[0][ox] * ox;
-#pragma unroll
-          for (int pp = 0; pp < 2; ++pp) {
-            sv[pp] = __ffma2_rn(make_float2(wx, wx), sy[pp], sv[pp]);
-            tyy[pp] = __ffma2_rn(make_float2(wx, wx), ty[pp], tyy[pp]);
-            tzz[pp] = __ffma2_rn(make_float2(wx, wx), tzy[pp], tzz[pp]);
-            if (ox) tx[pp] = __ffma2_rn(make_float2(wxo, wxo), sy[pp], tx[pp]);
-          }
+          sv = __ffma2_rn(make_float2(wx, wx), sy, sv);
+          tyy = __ffma2_rn(make_float2(wx, wx), ty, tyy);
+          tzz = __ffma2_rn(make_float2(wx, wx), tzy, tzz);
+          if (ox) tx = __ffma2_rn(make_float2(wxo, wxo), sy, tx);
+          svz = __ffma2_rn(make_float2(wx, wx), syz, svz);
+          tyz = fmaf(wx, tyzo, tyz);
+          if (ox) txz = fmaf(wxo, syz.x, txz);
         }
-        Sv[0] = sv[0].x;
-        Sv[1] = sv[0].y;
-        Sv[2] = sv[1].x;
-        T[0][0] = tx[0].x;
-        T[1][0] = tx[0].y;
-        T[2][0] = tx[1].x;
-        T[0][1] = tyy[0].x;
-        T[1][1] = tyy[0].y;
-        T[2][1] = tyy[1].x;
-        T[0][2] = tzz[0].x;
-        T[1][2] = tzz[0].y;
-        T[2][2] = tzz[1].x;
+        Sv[0] = sv.x;
+        Sv[1] = sv.y;
+        Sv[2] = svz.x;
+        T[0][0] = tx.x;
+        T[1][0] = tx.y;
+        T[2][0] = txz;
+        T[0][1] = tyy.x;
+        T[1][1] = tyy.y;
+        T[2][1] = tyz;
+        T[0][2] = tzz.x;
+        T[1][2] = tzz.y;
+        T[2][2] = svz.y;
       } else {
 #pragma unroll
         for (int ox = 0; ox < 3; ++ox) {
