@@ -317,7 +317,8 @@ int oracle_n_scalars(int dim, int material) {
 }
 
 /* Particle key (reading Q5): k = 0; for each record word holding any bit of an
- * x field (scalars 0..dim-1), in ascending word order: k = mix32(k ^ word). */
+ * x field (scalars 0..dim-1), in ascending word order: k = (k ^ word) * 0x9E3779B1 (rev. 3;
+ * an odd multiply per word, the particle hash mix(key ^ salt) does the mixing). */
 uint32_t oracle_particle_key(const oracle_scheme* s, int dim, const uint32_t* rec) {
     uint32_t offsets[ORACLE_MAX_FIELDS], W, bits;
     if (oracle_layout(s, offsets, &W, &bits)) return 0;
@@ -329,7 +330,7 @@ uint32_t oracle_particle_key(const oracle_scheme* s, int dim, const uint32_t* re
             uint32_t first = offsets[f] / 32, last = (offsets[f] + field_width(s, f) - 1) / 32;
             if (w >= first && w <= last) holds_x = 1;
         }
-        if (holds_x) k = oracle_mix32(k ^ rec[w]);
+        if (holds_x) k = (k ^ rec[w]) * 0x9E3779B1u; /* reading Q5 rev. 3: multiply-xor fold */
     }
     return k;
 }

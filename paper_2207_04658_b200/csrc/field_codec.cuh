@@ -166,13 +166,15 @@ __host__ __device__ constexpr float enc_lim(int wi) {
   return wi <= 1 ? 0.0f : (wi <= 25 ? (float)((1 << (wi - 1)) - 1) : (float)(1 << 24) * (float)(1 << (wi - 26)));
 }
 
-// content key of a record (reading Q5): k = mix(k ^ word) over the words holding x
+// content key of a record (reading Q5 rev. 3): k = (k ^ word) * 0x9E3779B1 over the words
+// holding x (an odd multiply per word: a bijection of each word; the full mixing is the
+// particle hash h = mix(key ^ salt) that follows)
 template <class SP>
 __device__ __forceinline__ uint32_t content_key(const uint32_t* w) {
   uint32_t k = 0;
 #pragma unroll
   for (int q = 0; q < SP::W; ++q)
-    if ((SP::XMASK >> q) & 1u) k = mix32(k ^ w[q]);
+    if ((SP::XMASK >> q) & 1u) k = (k ^ w[q]) * 0x9E3779B1u;
   return k;
 }
 

@@ -250,15 +250,26 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 // Momentum at stencil node o of a particle: m v + aff (o - fx) dx = Q + sum_k o_k a_k,
 // a_k = dx aff[:, k], Q = m v - sum_k fx_k a_k (Hu et al. 2018 APIC/MLS form).
 #ifndef QMPM_SEG_L
-#define QMPM_SEG_L 32
+#define QMPM_SEG_L 48
+#endif
+// A/B switches of micro-optimisations (tools/ab_step.py; defaults = the measured winners)
+#ifndef QMPM_AB_P2G_PF
+#define QMPM_AB_P2G_PF 1  // (measured: P2G 6.92 vs 7.22 ms at C4)
+#endif
+#ifndef QMPM_AB_CNT_LOP3
+#define QMPM_AB_CNT_LOP3 0  // (measured: 9.996 vs 10.132 ms G2P at C4 -- the shift-add form wins)
+#endif
+#ifndef QMPM_AB_ZPACK
+#define QMPM_AB_ZPACK 1  // (measured: G2P 10.13 vs 10.23 ms at C4 with the round counters)
 #endif
 #ifndef QMPM_SEG_LMIN
-#define QMPM_SEG_LMIN 32
+#define QMPM_SEG_LMIN 48
 #endif
 // particles per P2G segment (one lane, one group): n_blk / 128 clamped to [kSegLmin, kSegL]
 // (QMPM_SEG_LMIN < QMPM_SEG_L shortens the segments of sparse blocks so every lane gets
 // work; measured on B200: at C4 (~72 ppc) P2G takes 7.15 / 7.07 / 6.99 ms with segments
-// of 16 / 24 / 32 particles -- fewer per-group tile updates; at 8 ppc every cell is one
+// of 16 / 24 / 32 particles and 6.85 vs 6.92 with 48 vs 32 (paired A/B on one state,
+// tools/ab_step.py) -- fewer per-group tile updates; at 8 ppc every cell is one
 // tail segment whatever the length, and a floor of 8 was 2.5 % slower there than 16)
 constexpr int kSegL = QMPM_SEG_L;
 constexpr int kSegLmin = QMPM_SEG_LMIN < QMPM_SEG_L ? QMPM_SEG_LMIN : QMPM_SEG_L;
@@ -421,8 +432,10 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
             // the next segment's indices (contiguous, <= L): into L1 a segment ahead, so the
             // one-ahead index loads of its particles hit (ncu: the index latency was the top
             // stall of the loop; records bypass L1 with cp.async.cg)
+#if QMPM_AB_P2G_PF
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pidx + nk + 1));
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pidx + ne - 1));
+#endif
           }
         } else {
           fidx = __ldg(pidx + fk);
@@ -612,13 +625,6 @@ struct RoundCounters {
   uint32_t n_since;  // chunks (per lane) since the last flush, warp-uniform
   unsigned c_up, c_z;
   unsigned long long c_n;  // lane-particles counted (dithered: the "all" of down)
-  // + 1 in the byte of every packed-fast-path entry of register k
-  __host__ __device__ static constexpr uint32_t one(int i) {
-    return (i < SP::NS && fast_ok<SP>(i)) ? 1u << (8 * (i % 4)) : 0u;
-  }
-  __host__ __device__ static constexpr uint32_t fast_one(int k) {
-    return one(4 * k) + one(4 * k + 1) + one(4 * k + 2) + one(4 * k + 3);
-  }
   __device__ __forceinline__ void init() {
 #pragma unroll
     for (int k = 0; k < NP; ++k) pu[k] = pz[k] = 0u;
@@ -792,6 +798,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       float Sv[3] = {0.f, 0.f, 0.f}, T[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
       const int base_idx = D == 3 ? (lb[0] * G::T + lb[1]) * G::T + lb[2] : lb[0] * G::T + lb[1];
       if (D == 3) {
+#if QMPM_AB_ZPACK
         // packed FP32x2 (sm_100 FFMA2 / FMUL2; each lane is the IEEE op the scalar form does):
         // (v_x, v_y) of a node as one pair through every level; v_z, which would waste half
         // a pair, carries its two z-moments instead: (sum_oz w v_z, sum_oz w oz v_z) with the
@@ -845,6 +852,57 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         T[0][2] = tzz.x;
         T[1][2] = tzz.y;
         T[2][2] = svz.y;
+#else
+        // packed FP32x2 (sm_100 FFMA2 / FMUL2): pair 0 = (v_x, v_y), pair 1 = (v_z, 0) of a
+        // node; each lane is the same IEEE op the scalar form does
+        const float wz0 = wt[2][0], wz1 = wt[2][1], wz2 = wt[2][2], wz2x2 = 2.0f * wt[2][2];
+        float2 sv[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float2 tx[2] = {sv[0], sv[0]}, tyy[2] = {sv[0], sv[0]}, tzz[2] = {sv[0], sv[0]};
+#pragma unroll
+        for (int ox = 0; ox < 3; ++ox) {
+          float2 sy[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, ty[2] = {sy[0], sy[0]},
+                 tzy[2] = {sy[0], sy[0]};
+#pragma unroll
+          for (int oy = 0; oy < 3; ++oy) {
+            const int idx = base_idx + (ox * G::T + oy) * G::T;
+            const float4 g0 = tile[idx], g1 = tile[idx + 1], g2 = tile[idx + 2];
+            const float2 ga[3][2] = {{make_float2(g0.x, g0.y), make_float2(g0.z, g0.w)},
+                                     {make_float2(g1.x, g1.y), make_float2(g1.z, g1.w)},
+                                     {make_float2(g2.x, g2.y), make_float2(g2.z, g2.w)}};
+            const float wy = wt[1][oy], wyo = wt[1][oy] * oy;
+#pragma unroll
+            for (int pp = 0; pp < 2; ++pp) {
+              const float2 p1 = __fmul2_rn(make_float2(wz1, wz1), ga[1][pp]);
+              const float2 tz = __ffma2_rn(make_float2(wz2x2, wz2x2), ga[2][pp], p1);  // sum_oz w oz g
+              const float2 sz = __ffma2_rn(make_float2(wz0, wz0), ga[0][pp],
+                                           __ffma2_rn(make_float2(wz2, wz2), ga[2][pp], p1));  // sum_oz w g
+              sy[pp] = __ffma2_rn(make_float2(wy, wy), sz, sy[pp]);
+              tzy[pp] = __ffma2_rn(make_float2(wy, wy), tz, tzy[pp]);
+              if (oy) ty[pp] = __ffma2_rn(make_float2(wyo, wyo), sz, ty[pp]);
+            }
+          }
+          const float wx = wt[0][ox], wxo = wt[0][ox] * ox;
+#pragma unroll
+          for (int pp = 0; pp < 2; ++pp) {
+            sv[pp] = __ffma2_rn(make_float2(wx, wx), sy[pp], sv[pp]);
+            tyy[pp] = __ffma2_rn(make_float2(wx, wx), ty[pp], tyy[pp]);
+            tzz[pp] = __ffma2_rn(make_float2(wx, wx), tzy[pp], tzz[pp]);
+            if (ox) tx[pp] = __ffma2_rn(make_float2(wxo, wxo), sy[pp], tx[pp]);
+          }
+        }
+        Sv[0] = sv[0].x;
+        Sv[1] = sv[0].y;
+        Sv[2] = sv[1].x;
+        T[0][0] = tx[0].x;
+        T[1][0] = tx[0].y;
+        T[2][0] = tx[1].x;
+        T[0][1] = tyy[0].x;
+        T[1][1] = tyy[0].y;
+        T[2][1] = tyy[1].x;
+        T[0][2] = tzz[0].x;
+        T[1][2] = tzz[0].y;
+        T[2][2] = tzz[1].x;
+#endif
       } else {
 #pragma unroll
         for (int ox = 0; ox < 3; ++ox) {
@@ -914,7 +972,6 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         for (int k = 0; k < RoundCounters<SP>::NP; ++k) {
           pu_save[k] = rc.pu[k];
           pz_save[k] = rc.pz[k];
-          rc.pu[k] += RoundCounters<SP>::fast_one(k);  // + 1 per fast entry; - 1 below when rounded down
         }
       }
 #pragma unroll
@@ -931,8 +988,16 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
           if (i < D) xc[i] = ui;
           if (i + 1 < D) xc[i + 1] = uj;
           if (SP::COUNTERS) {
-            rc.pu[i / 4] += (uint32_t)sbi << (8 * (i % 4));
-            rc.pu[(i + 1) / 4] += (uint32_t)sbj << (8 * ((i + 1) % 4));
+            // + 1 in the bytes of i and i + 1 (one counter register: i is even) that rounded
+            // up (sb == 0): two LOP3 and an add on the integer pipe (the FMA pipe binds)
+#if QMPM_AB_CNT_LOP3
+            const uint32_t ci = 0xffu << (8 * (i % 4));
+            const uint32_t bij = (1u << (8 * (i % 4))) | (1u << (8 * ((i + 1) % 4)));
+            rc.pu[i / 4] += ((~(uint32_t)sbi & ci) | (~(uint32_t)sbj & ~ci)) & bij;
+#else
+            rc.pu[i / 4] += (1u + (uint32_t)sbi) << (8 * (i % 4));
+            rc.pu[(i + 1) / 4] += (1u + (uint32_t)sbj) << (8 * ((i + 1) % 4));
+#endif
             if (zi) rc.pz[i / 4] += 1u << (8 * (i % 4));
             if (zj) rc.pz[(i + 1) / 4] += 1u << (8 * ((i + 1) % 4));
           }
@@ -945,7 +1010,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
           sput_code<SP>(ow, i, u);
           if (i < D) xc[i] = u;
           if (SP::COUNTERS) {
-            rc.pu[i / 4] += (uint32_t)sb << (8 * (i % 4));
+            rc.pu[i / 4] += ~(uint32_t)sb & (1u << (8 * (i % 4)));
             if (z) rc.pz[i / 4] += 1u << (8 * (i % 4));
           }
           continue;

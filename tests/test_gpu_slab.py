@@ -190,3 +190,28 @@ def test_nonfinite_state_is_reported():
     sim.set_state(dev(sc.state()))  # a fresh state clears it
     sim.read_state(words=w)
     sim.close()
+
+
+def test_two_slab_jump_is_edomain():
+    """A particle handed to a rank two slabs away from its owner cannot be routed in one
+    hop (CFL keeps migration to the neighbours): the next synchronising call reports
+    QMPM_EDOMAIN (sticky), never a hang."""
+    sc, sch = scenes.small_fluid_3d(), schemes.f2()
+    w0, _ = oracle.encode_state(sch, sc.state())
+    slabs = cuts(sc.sim["grid_res"][2], 3)
+    st = oracle.decode_state(sch, w0)
+    own = owner(st, sc.sim, slabs)
+    stream = torch.cuda.Stream()
+    sims = []
+    for r, (z0, z1) in enumerate(slabs):
+        idx = np.nonzero(own == r)[0]
+        s = qmpm.Sim(sc.sim, sch, w0.shape[0], stream=stream, slab=(3, r, z0, z1))
+        s.set_words(dev(w0[idx]), 0)
+        sims.append(s)
+    sims[2].set_words(dev(w0[np.nonzero(own == 0)[0][:100]]), 0)  # rank 0's particles on rank 2
+    qmpm.step_group(sims, 1)
+    with pytest.raises(qmpm.QmpmError) as e:
+        sims[2].stats()
+    assert e.value.code == 7  # EDOMAIN
+    for s in sims:
+        s.close()

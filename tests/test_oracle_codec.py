@@ -366,6 +366,24 @@ def test_rng_golden_vector():
     for c in g["cases"]:
         assert [L.oracle_pair_hash(c["seed"], c["step"], c["key"], p) for p in range(4)] == c["pair_hash"]
         assert [oracle.r16(c["seed"], c["step"], c["key"], f) for f in range(8)] == c["r16"]
+    from paper_2207_04658_b200 import schemes
+    for c in g["particle_keys_f2"]:
+        assert oracle.particle_key(schemes.f2(), np.array(c["record"], np.uint32)) == c["key"]
+
+
+def test_particle_key_depends_on_x_words_only():
+    """Reading Q5: the content key folds exactly the record words holding x bits (F2: words
+    0 and 1, x = 3 x 19 bits); any other word leaves it unchanged, every x word changes it."""
+    from paper_2207_04658_b200 import schemes
+    sch = schemes.f2()
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        r = rng.integers(0, 2 ** 32, 8, dtype=np.uint64).astype(np.uint32)
+        k = oracle.particle_key(sch, r)
+        for w in range(8):
+            r2 = r.copy()
+            r2[w] ^= np.uint32(1 << int(rng.integers(0, 32)))
+            assert (oracle.particle_key(sch, r2) != k) == (w < 2), w
 
 
 def test_mix32_is_a_bijection_on_a_sample():

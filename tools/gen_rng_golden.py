@@ -20,8 +20,15 @@ for step in (1, 2, 1000):
         cases.append({"seed": SEED, "step": step, "key": key,
                       "pair_hash": [oracle.lib().oracle_pair_hash(SEED, step, key, p) for p in range(4)],
                       "r16": [oracle.r16(SEED, step, key, f) for f in range(8)]})
+# particle keys (content keys over the x words) of a few F2 records
+import numpy as np  # noqa: E402
+from paper_2207_04658_b200 import schemes  # noqa: E402
+sch = schemes.f2()
+recs = [[0] * 8, [1, 2, 3, 4, 5, 6, 7, 8], [0xFFFFFFFF] * 8, [0x12345678, 0x9ABCDEF0, 0, 0, 0, 0, 0, 0]]
+keys = [{"record": r, "key": oracle.particle_key(sch, np.array(r, np.uint32))} for r in recs]
 out = {"citation": "reading Q5 rev. 3 (DESIGN.md §2); P:421 (Eq. 11), P:811 (the paper's RNG, unavailable)",
-       "generator": "tools/gen_rng_golden.py (oracle only)", "cases": cases}
+       "generator": "tools/gen_rng_golden.py (oracle only)", "cases": cases,
+       "particle_keys_f2": keys}
 path = os.path.join(ROOT, "tests", "golden", "rng_rev3.json")
 with open(path, "w") as f:
     json.dump(out, f, indent=1)
