@@ -162,6 +162,86 @@ __device__ __forceinline__ void benign_state(float* s, const int org[3], float d
   }
 }
 
+#ifndef QMPM_AB_VSQRT
+#define QMPM_AB_VSQRT 1  // 3D fixed corotated through B - sqrt(B) instead of the Newton polar
+#endif
+
+// (F - R) F^T of the polar decomposition F = R S (det F > 0), in 3D without R:
+// R F^T = R S R^T = V = sqrt(B), B = F F^T, so (F - R) F^T = B - V.  With E = B - I and
+// mu_i its eigenvalues (closed form, trigonometric), sigma_i = sqrt(1 + mu_i), the
+// matrix function G = V - I = g(E), g(mu) = sqrt(1 + mu) - 1, is the quadratic that
+// interpolates g at the mu_i, G = a0 I + a1 E + a2 E^2, from the divided differences
+//   g[mu_i, mu_j] = 1 / (sigma_i + sigma_j),
+//   g[mu_1, mu_2, mu_3] = -1 / ((sigma_1 + sigma_2)(sigma_2 + sigma_3)(sigma_3 + sigma_1)),
+// closed forms without cancellation, so B - V = E - G keeps its relative accuracy when
+// the strain is small (no 1 - 1 differences anywhere).  Out: K = (F - R) F^T symmetric
+// as {00, 11, 22, 01, 02, 12}.
+__device__ __forceinline__ float sqrt_apx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_apx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// arccos on [-1, 1] to ~2e-8 absolute: acos(x) = sqrt(1 - x) P(x) for x >= 0 (the
+// degree-7 fit of Abramowitz & Stegun 4.4.46), acos(-x) = pi - acos(x)
+__device__ __forceinline__ float acos_apx(float r) {
+  const float x = fabsf(r);
+  float p = -0.0012624911f;
+  p = fmaf(p, x, 0.0066700901f);
+  p = fmaf(p, x, -0.0170881256f);
+  p = fmaf(p, x, 0.0308918810f);
+  p = fmaf(p, x, -0.0501743046f);
+  p = fmaf(p, x, 0.0889789874f);
+  p = fmaf(p, x, -0.2145988016f);
+  p = fmaf(p, x, 1.5707963050f);
+  const float a = sqrt_apx(1.0f - x) * p;
+  return r < 0.0f ? 3.14159265f - a : a;
+}
+
+__device__ __forceinline__ void corot_kernel3(const float F[9], float K[6]) {
+  float E[6];
+  E[0] = fmaf(F[0], F[0], fmaf(F[1], F[1], fmaf(F[2], F[2], -1.0f)));
+  E[1] = fmaf(F[3], F[3], fmaf(F[4], F[4], fmaf(F[5], F[5], -1.0f)));
+  E[2] = fmaf(F[6], F[6], fmaf(F[7], F[7], fmaf(F[8], F[8], -1.0f)));
+  E[3] = fmaf(F[0], F[3], fmaf(F[1], F[4], F[2] * F[5]));
+  E[4] = fmaf(F[0], F[6], fmaf(F[1], F[7], F[2] * F[8]));
+  E[5] = fmaf(F[3], F[6], fmaf(F[4], F[7], F[5] * F[8]));
+  const float q = (E[0] + E[1] + E[2]) * (1.0f / 3.0f);
+  const float d0 = E[0] - q, d1 = E[1] - q, d2 = E[2] - q;
+  const float off2 = fmaf(E[3], E[3], fmaf(E[4], E[4], E[5] * E[5]));
+  const float p2 = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, 2.0f * off2))) * (1.0f / 6.0f);
+  float m1 = q, m2 = q, m3 = q;
+  if (p2 > 1e-20f) {  // (below: eigenvalue spread under fp32 resolution, all = q)
+    const float ip = rsqrtf(p2), p = p2 * ip;
+    const float detD = d0 * fmaf(d1, d2, -E[5] * E[5]) - E[3] * fmaf(E[3], d2, -E[5] * E[4]) +
+                       E[4] * fmaf(E[3], E[5], -d1 * E[4]);
+    const float r = fminf(fmaxf(((detD * ip) * ip) * ip * 0.5f, -1.0f), 1.0f);
+    const float phi = acos_apx(r) * (1.0f / 3.0f);
+    m1 = fmaf(2.0f * p, __cosf(phi), q);
+    m3 = fmaf(2.0f * p, __cosf(phi + 2.09439510f), q);
+    m2 = 3.0f * q - m1 - m3;
+  }
+  const float s1 = sqrt_apx(fmaxf(1.0f + m1, 1e-30f)), s2 = sqrt_apx(fmaxf(1.0f + m2, 1e-30f)),
+              s3 = sqrt_apx(fmaxf(1.0f + m3, 1e-30f));
+  const float s12 = s1 + s2, s23 = s2 + s3, s31 = s3 + s1;
+  const float i12 = rcp_apx(s12);
+  const float a2 = -rcp_apx(s12 * s23 * s31);
+  const float a1 = fmaf(-(m1 + m2), a2, i12);
+  const float a0 = fmaf(m1 * m2, a2, m1 * (rcp_apx(1.0f + s1) - i12));
+  // E^2 (symmetric)
+  const float Q[6] = {fmaf(E[0], E[0], fmaf(E[3], E[3], E[4] * E[4])), fmaf(E[1], E[1], fmaf(E[3], E[3], E[5] * E[5])),
+                      fmaf(E[2], E[2], fmaf(E[4], E[4], E[5] * E[5])),
+                      fmaf(E[0], E[3], fmaf(E[3], E[1], E[4] * E[5])),
+                      fmaf(E[0], E[4], fmaf(E[3], E[5], E[4] * E[2])),
+                      fmaf(E[3], E[4], fmaf(E[1], E[5], E[5] * E[2]))};
+#pragma unroll
+  for (int i = 0; i < 6; ++i) K[i] = E[i] - fmaf(a2, Q[i], (i < 3 ? a0 : 0.0f) + a1 * E[i]);
+}
+
 // the stress part of the affine momentum, -dt V_p 4/dx^2 P(F)F^T (Hu et al. 2018;
 // DESIGN.md §2 Q15), from the decoded F (elastic) or J (fluid, diagonal only)
 template <int D, int MAT>
@@ -172,6 +252,19 @@ __device__ __forceinline__ void stress_of(const float* s, const SimDev& S, float
     for (int i = 0; i < D * D; ++i) st[i] = 0.0f;
 #pragma unroll
     for (int a = 0; a < D; ++a) st[a * D + a] = p;
+  } else if (D == 3 && QMPM_AB_VSQRT) {
+    const float* F = s + 2 * D;
+    float K[6];
+    corot_kernel3(F, K);
+    const float J = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
+                    F[2] * (F[3] * F[7] - F[4] * F[6]);
+    const float two_mu = 2.0f * S.mu * S.stress_scale;
+    const float diag = S.lambda * (J - 1.0f) * J * S.stress_scale;
+    constexpr int SI[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) st[a * D + b] = fmaf(two_mu, K[SI[a][b]], a == b ? diag : 0.0f);
   } else {
     const float* F = s + 2 * D;
     float R[D * D];

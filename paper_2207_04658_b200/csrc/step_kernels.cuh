@@ -259,6 +259,9 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 #ifndef QMPM_AB_CNT_LOP3
 #define QMPM_AB_CNT_LOP3 0  // (measured: 9.996 vs 10.132 ms G2P at C4 -- the shift-add form wins)
 #endif
+#ifndef QMPM_AB_BCNT
+#define QMPM_AB_BCNT 1  // G2P: the next step's count of the current block summed per block
+#endif
 #ifndef QMPM_AB_ZPACK
 #define QMPM_AB_ZPACK 1  // (measured: G2P 10.13 vs 10.23 ms at C4 with the round counters)
 #endif
@@ -435,10 +438,17 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
 #if QMPM_AB_P2G_PF
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pidx + nk + 1));
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pidx + ne - 1));
+#if QMPM_AB_P2G_PF == 2
+            // (a 48-index segment can straddle three 128-byte lines)
+            if (ne - nk > 32u) asm volatile("prefetch.global.L1 [%0];" ::"l"(pidx + nk + 24));
+#endif
 #endif
           }
         } else {
           fidx = __ldg(pidx + fk);
+#if QMPM_AB_P2G_PF == 3
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(pidx + fk + 8));
+#endif
         }
       }
       cp_async_commit();
@@ -750,6 +760,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
     }
     __syncwarp();
 
+    unsigned stay = 0;  // (QMPM_AB_BCNT) particles of this chunk loop staying in block b
     for (uint32_t j0 = start; j0 < end; j0 += 32) {
       const uint32_t cnt = min(32u, end - j0);
       const bool valid = (uint32_t)lane < cnt;
@@ -1125,9 +1136,17 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       if (valid) key_out[j] = nkey;
       {  // next step's histograms, one atomic per distinct key of the warp
         const bool cnt_it = valid && !leave;
+#if QMPM_AB_BCNT
+        // most particles stay in their block: those are summed over the block's chunks
+        // (one atomic per block below), the others count themselves
+        const bool same = cnt_it && (nkey >> 6) == b;
+        stay += (unsigned)__popc(__ballot_sync(FULL, same));
+        if (cnt_it && !same) atomicAdd(&block_count[nkey >> 6], 1u);
+#else
         const uint32_t nk = cnt_it ? (nkey >> 6) : 0xffffffffu;
         const unsigned kp = __match_any_sync(FULL, nk);
         if (cnt_it && lane == __ffs(kp) - 1) atomicAdd(&block_count[nk], (unsigned)__popc(kp));
+#endif
         const unsigned cp = __match_any_sync(FULL, cnt_it ? nkey : kDeadKey);
         if (cnt_it && lane == __ffs(cp) - 1) atomicAdd(&cell_count[nkey], (unsigned)__popc(cp));
       }
@@ -1147,6 +1166,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         }
       }
     }
+    if (QMPM_AB_BCNT && lane == 0 && stay != 0u) atomicAdd(&block_count[b], stay);
     __syncwarp();
   }
   if (SP::COUNTERS) rc.flush(lane);
