@@ -170,9 +170,31 @@ template <class SP>
 struct Smem {
   static constexpr int TN = Geo<SP::D>::TN;
   static constexpr int TILE = 16 * TN;
-  // velocity tile + 8 neighbour slots + double-buffered record stage
-  static constexpr int G2P_WARP = TILE + 32 + (2 * 32 * 4 * SP::W + 15) / 16 * 16;
+  // velocity tile + 8 neighbour slots + double-buffered record stage + tile node table
+  static constexpr int STAGE = TILE + 32;
+  static constexpr int TNODE = STAGE + (2 * 32 * 4 * SP::W + 15) / 16 * 16;
+  static constexpr int G2P_WARP = TNODE + (2 * TN + 15) / 16 * 16;
 };
+
+// tile node t -> which of the 2^d blocks a (B+2)^d tile spans it lies in (bit a: the +a
+// neighbour) and its node inside that block: u16 (sel << 6 | node), the same for every
+// block, built once per warp
+template <int D>
+__device__ __forceinline__ void build_tile_nodes(uint16_t* tn, int lane) {
+  using G = Geo<D>;
+  for (int t = lane; t < G::TN; t += 32) {
+    int node[3];
+    const int zero[3] = {0, 0, 0};
+    tile_node<D>(t, zero, node);
+    int sel = 0, ln[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      sel |= (node[a] >= G::B) << a;
+      ln[a] = node[a] & (G::B - 1);
+    }
+    tn[t] = (uint16_t)((sel << 6) | (int)local_node<D>(ln));
+  }
+}
 
 // Per-lane asynchronous copy of record r (W words) into shared memory (cp.async, no
 // registers held while in flight; 16-byte granules when the record size allows).
@@ -254,10 +276,19 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 #endif
 // A/B switches of micro-optimisations (tools/ab_step.py; defaults = the measured winners)
 #ifndef QMPM_AB_P2G_PF
-#define QMPM_AB_P2G_PF 1  // (measured: P2G 6.92 vs 7.22 ms at C4)
+#define QMPM_AB_P2G_PF 0  // (measured: 6.92 vs 7.22 ms at C4 before IDX_FIRST; with it 6.24 vs 6.28-6.33 without the prefetch)
 #endif
 #ifndef QMPM_AB_CNT_LOP3
 #define QMPM_AB_CNT_LOP3 0  // (measured: 9.996 vs 10.132 ms G2P at C4 -- the shift-add form wins)
+#endif
+#ifndef QMPM_AB_P2G_PACK
+#define QMPM_AB_P2G_PACK 1  // P2G: packed weight products and node momenta (3D)
+#endif
+#ifndef QMPM_AB_G2P_IDX_FIRST
+#define QMPM_AB_G2P_IDX_FIRST 0  // G2P: the chunk-after-next's indices load before the next chunk's copies
+#endif
+#ifndef QMPM_AB_IDX_FIRST
+#define QMPM_AB_IDX_FIRST 1  // P2G: the next record index loads before the current record's copy (C4 P2G 6.90 -> 6.39 ms)
 #endif
 #ifndef QMPM_AB_BCNT
 #define QMPM_AB_BCNT 1  // G2P: the next step's count of the current block summed per block
@@ -288,7 +319,9 @@ struct P2GLayout {
   static constexpr int LSTART = START + 4 * 68;                // u32[kSegLev]
   static constexpr int SEG = LSTART + 4 * kSegLev;             // u16[64 * kSegLev]
   static constexpr int NS = SEG + 2 * 64 * kSegLev;            // u8[64]
-  static constexpr int BYTES = (NS + 64 + 15) / 16 * 16;
+  static constexpr int NSLOT = (NS + 64 + 15) / 16 * 16;       // u32[8] the 2^d blocks a tile spans
+  static constexpr int TNODE = NSLOT + 32;                     // u16[TN] tile node -> (block << 6 | node)
+  static constexpr int BYTES = (TNODE + 2 * TN + 15) / 16 * 16;
 };
 
 template <class SP>
@@ -311,6 +344,9 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
   uint32_t* s_lstart = reinterpret_cast<uint32_t*>(wb + LY::LSTART);
   uint16_t* s_seg = reinterpret_cast<uint16_t*>(wb + LY::SEG);
   uint8_t* s_ns = reinterpret_cast<uint8_t*>(wb + LY::NS);
+  uint32_t* s_nslot = reinterpret_cast<uint32_t*>(wb + LY::NSLOT);
+  uint16_t* s_tnode = reinterpret_cast<uint16_t*>(wb + LY::TNODE);
+  build_tile_nodes<D>(s_tnode, lane);  // (for the flush)
   // part 0: every active block; 1: the blocks below the slab's top block plane; 2: the
   // top plane only (whose partial sums reach the ghost plane: launched first so the
   // exchange overlaps part 1)
@@ -333,6 +369,12 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     block_coords<D>(b, S, bc);
     const int org[3] = {bc[0] * G::B, bc[1] * G::B, bc[2] * G::B};
     for (int t = lane; t < G::TN; t += 32) tile[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lane < (1 << D)) {  // slots of the block and its +x/+y(/+z) neighbours (flush)
+      const int nbk[3] = {bc[0] + (lane & 1), bc[1] + ((lane >> 1) & 1), D == 3 ? bc[2] + ((lane >> 2) & 1) : 0};
+      uint32_t sl = 0xffffffffu;
+      if (nbk[0] < S.nb[0] && nbk[1] < S.nb[1] && (D == 2 || nbk[2] < S.tab_bz1)) sl = block_slot[block_id<D>(nbk, S)];
+      s_nslot[lane] = sl;
+    }
     // cell starts (the scatter left them in cell_count); zeroed for the next step
     uint32_t* cc = cell_count + (size_t)b * 64;
     const uint32_t st0 = cc[lane] - start, st1 = cc[lane + 32] - start;
@@ -381,7 +423,9 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     {  // tails, by key = min(length, L) descending, ties in cell order
       const uint32_t k0 = min(tl0, L), k1 = min(tl1, L);
       uint32_t above = 0;
-      for (uint32_t v = L; v >= 1u; --v) {
+      // (from the longest tail present: at 8 ppc the tails are short and a loop from L
+      // was 10 % of the kernel's instructions)
+      for (uint32_t v = __reduce_max_sync(FULL, max(k0, k1)); v >= 1u; --v) {
         const unsigned b0 = __ballot_sync(FULL, k0 == v), b1 = __ballot_sync(FULL, k1 == v);
         if (k0 == v) s_seg[nfull + above + __popc(b0 & lanemask_lt())] = (uint16_t)((lane << 8) | nf0);
         if (k1 == v)
@@ -421,8 +465,12 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     }
     auto fetch = [&]() {
       if (fk < fe) {
+#if QMPM_AB_IDX_FIRST
+        const uint32_t cur = fidx;  // (the next index's load goes out before this copy)
+#else
         record_async<SP>(rec, fidx, ring + fslot * 32 * W);
         fslot = fslot == 2 ? 0 : fslot + 1;
+#endif
         if (++fk == fe) {
           fk = nk;
           fe = ne;
@@ -448,8 +496,16 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
           fidx = __ldg(pidx + fk);
 #if QMPM_AB_P2G_PF == 3
           asm volatile("prefetch.global.L1 [%0];" ::"l"(pidx + fk + 8));
+#elif QMPM_AB_P2G_PF == 4
+          // the segment's next 128-byte index line, 8 particles before it is needed
+          if ((((unsigned long long)(pidx + fk + 8)) & 127ull) < 4ull && fk + 8 < fe)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pidx + fk + 8));
 #endif
         }
+#if QMPM_AB_IDX_FIRST
+        record_async<SP>(rec, cur, ring + fslot * 32 * W);
+        fslot = fslot == 2 ? 0 : fslot + 1;
+#endif
       }
       cp_async_commit();
     };
@@ -525,7 +581,49 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
         float wt[3][3];
 #pragma unroll
         for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
-        if (D == 3) {
+        if (D == 3 && QMPM_AB_P2G_PACK) {
+          // the same sums with the weight products in FMUL2 pairs and each node's momentum
+          // per unit weight built by packed adds of A's columns (row, then column, then
+          // node: Q + ox A_x + oy A_y + oz A_z)
+          const float2 a0xy = make_float2(A[0][0], A[0][1]), a0z0 = make_float2(A[0][2], 0.0f);
+          const float2 a1xy = make_float2(A[1][0], A[1][1]), a1z0 = make_float2(A[1][2], 0.0f);
+          const float2 a2xy = make_float2(A[2][0], A[2][1]), a2z0 = make_float2(A[2][2], 0.0f);
+          const float2 wy01 = make_float2(wt[1][0], wt[1][1]), wz01 = make_float2(wt[2][0], wt[2][1]);
+          float2 rxy = make_float2(Q[0], Q[1]), rz1 = make_float2(Q[2], 1.0f);
+#pragma unroll
+          for (int ox = 0; ox < 3; ++ox) {
+            const float2 wxy01 = __fmul2_rn(make_float2(wt[0][ox], wt[0][ox]), wy01);
+            const float wxy2 = wt[0][ox] * wt[1][2];
+            float2 mxy = rxy, mz1 = rz1;
+#pragma unroll
+            for (int oy = 0; oy < 3; ++oy) {
+              const float wxy = oy == 0 ? wxy01.x : (oy == 1 ? wxy01.y : wxy2);
+              const float2 ww01 = __fmul2_rn(make_float2(wxy, wxy), wz01);
+              const float ww2 = wxy * wt[2][2];
+              float2 nxy = mxy, nz1 = mz1;
+#pragma unroll
+              for (int oz = 0; oz < 3; ++oz) {
+                const int q = (ox * 3 + oy) * 3 + oz;
+                const float ww = oz == 0 ? ww01.x : (oz == 1 ? ww01.y : ww2);
+                const float2 w2 = make_float2(ww, ww);
+                axy[q] = __ffma2_rn(w2, nxy, axy[q]);
+                azm[q] = __ffma2_rn(w2, nz1, azm[q]);  // .y: sum w + ww * 1 (exact product)
+                if (oz < 2) {
+                  nxy = __fadd2_rn(nxy, a2xy);
+                  nz1 = __fadd2_rn(nz1, a2z0);
+                }
+              }
+              if (oy < 2) {
+                mxy = __fadd2_rn(mxy, a1xy);
+                mz1 = __fadd2_rn(mz1, a1z0);
+              }
+            }
+            if (ox < 2) {
+              rxy = __fadd2_rn(rxy, a0xy);
+              rz1 = __fadd2_rn(rz1, a0z0);
+            }
+          }
+        } else if (D == 3) {
           const float2 a2xy = make_float2(A[2][0], A[2][1]), a2z0 = make_float2(A[2][2], 0.0f);
 #pragma unroll
           for (int ox = 0; ox < 3; ++ox) {
@@ -607,16 +705,9 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     for (int t = lane; t < G::TN; t += 32) {
       const float4 acc = tile[t];
       if (acc.x != 0.0f) {
-        int node[3];
-        tile_node<D>(t, org, node);
-        int nbk[3], ln[3];
-#pragma unroll
-        for (int a2 = 0; a2 < 3; ++a2) {
-          nbk[a2] = node[a2] >> G::LB;
-          ln[a2] = node[a2] & (G::B - 1);
-        }
-        const uint32_t slot = block_slot[block_id<D>(nbk, S)];
-        if (slot != 0xffffffffu) atomicAdd(&mp[(size_t)slot * 64 + local_node<D>(ln)], acc);
+        const uint32_t e = s_tnode[t];
+        const uint32_t slot = s_nslot[e >> 6];
+        if (slot != 0xffffffffu) atomicAdd(&mp[(size_t)slot * 64 + (e & 63u)], acc);
       }
     }
     __syncwarp();
@@ -692,7 +783,9 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
   char* wbase = reinterpret_cast<char*>(smem4) + warp * SM::G2P_WARP;
   float4* tile = reinterpret_cast<float4*>(wbase);
   uint32_t* nslot = reinterpret_cast<uint32_t*>(wbase + SM::TILE);  // [4] / [8] neighbour slots
-  uint32_t* wring = reinterpret_cast<uint32_t*>(wbase + SM::TILE + 32);  // [2][32][W] record stage
+  uint32_t* wring = reinterpret_cast<uint32_t*>(wbase + SM::STAGE);  // [2][32][W] record stage
+  uint16_t* s_tnode = reinterpret_cast<uint16_t*>(wbase + SM::TNODE);
+  build_tile_nodes<D>(s_tnode, lane);
   RoundCounters<SP> rc;
   rc.init();
   unsigned rmax = 0u;  // range recording (float bits of max |value|, lane i: scalar i)
@@ -741,17 +834,9 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
         const int t = lane + 32 * u;
         v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (t < G::TN) {
-          int node[3];
-          tile_node<D>(t, org, node);
-          int sel = 0, ln[3] = {0, 0, 0};
-#pragma unroll
-          for (int a = 0; a < D; ++a) {
-            const int hi = (node[a] - org[a]) >= G::B;
-            sel |= hi << a;
-            ln[a] = node[a] & (G::B - 1);
-          }
-          const uint32_t slot = nslot[sel];
-          if (slot != 0xffffffffu) v[u] = gv[(size_t)slot * 64 + local_node<D>(ln)];
+          const uint32_t e = s_tnode[t];
+          const uint32_t slot = nslot[e >> 6];
+          if (slot != 0xffffffffu) v[u] = gv[(size_t)slot * 64 + (e & 63u)];
         }
       }
 #pragma unroll
@@ -767,12 +852,22 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
       const uint32_t r = r_next;
       {  // the next chunk's records go in flight while this one computes
         const uint32_t jn = j0 + 32 + lane;
+#if QMPM_AB_G2P_IDX_FIRST
+        const uint32_t ra = r_after;
+        if (jn + 32 < end) r_after = perm[jn + 32];  // (issued before the copies, as in P2G)
+        if (jn < end) {
+          r_next = ra;
+          record_async<SP>(rec_in, r_next, wring + ((buf ^ 1) * 32 + lane) * W);
+        }
+        cp_async_commit();
+#else
         if (jn < end) {
           r_next = r_after;
           record_async<SP>(rec_in, r_next, wring + ((buf ^ 1) * 32 + lane) * W);
         }
         cp_async_commit();
         if (jn + 32 < end) r_after = perm[jn + 32];
+#endif
       }
       cp_async_wait<1>();
       uint32_t w[W + 1];

@@ -25,6 +25,8 @@ ap.add_argument("--variant", action="append", default=[], help="NVRTC options of
 a = ap.parse_args()
 if a.config == "c3":
     sc, sch = scenes.c3(), schemes.e001()
+elif a.config == "c4_8ppc":
+    sc, sch = scenes.c4(res=512, dt=5e-5), schemes.f2()
 else:
     sc, sch = scenes.c4(), schemes.f2()
 flags = qmpm.NO_ROUND_COUNTERS if a.no_counters else 0
