@@ -276,7 +276,7 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 #endif
 // A/B switches of micro-optimisations (tools/ab_step.py; defaults = the measured winners)
 #ifndef QMPM_AB_P2G_PF
-#define QMPM_AB_P2G_PF 0  // (measured: 6.92 vs 7.22 ms at C4 before IDX_FIRST; with it 6.24 vs 6.28-6.33 without the prefetch)
+#define QMPM_AB_P2G_PF 0  // (measured at C4: 6.92 with vs 7.22 ms without before IDX_FIRST; after it 6.24 without vs 6.28-6.33 with)
 #endif
 #ifndef QMPM_AB_CNT_LOP3
 #define QMPM_AB_CNT_LOP3 0  // (measured: 9.996 vs 10.132 ms G2P at C4 -- the shift-add form wins)
