@@ -366,14 +366,14 @@ def run_gpu(args):
     achieved = ab[dom](N) / (avg_ms / 1e3) / 1e9
     # ncu `--set full` capture of this config's kernels (profiles/ncu_traffic.json, written
     # by profiles/summarize_ncu.py --config): DRAM bytes and warp instructions per launch
-    traffic, winst = None, None
+    traffic, winst, fma_frac = None, None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath) and not args.n and args.scaling == "weak" and args.z_extent == 1.0:
         try:
             rec = _json.load(open(tpath)).get(args.config, {}).get(dom, {})
-            traffic, winst = rec.get("traffic"), rec.get("warp_inst")
+            traffic, winst, fma_frac = rec.get("traffic"), rec.get("warp_inst"), rec.get("fma_pipe")
         except Exception:
-            traffic, winst = None, None
+            traffic, winst, fma_frac = None, None, None
     # issue-rate roofline: the step kernels are bound by the warp
     # schedulers, not by bytes -- warp instructions per launch / (launch time x SMs x 4
     # schedulers x SM clock under load)
@@ -389,7 +389,12 @@ def run_gpu(args):
                 "issue_frac": issue_frac,
                 "issue_note": "warp instructions per launch (ncu, profiles/ncu_traffic.json, this config) / "
                               "(avg launch time x SMs x 4 schedulers x median SM clock): the binding roofline "
-                              "of the issue-bound step kernels (SURVEY §8(d) M4)"}
+                              "of the issue-bound step kernels (SURVEY §8(d) M4)",
+                "fma_pipe_frac": fma_frac,
+                "fma_pipe_note": "ncu sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active of this kernel "
+                                 "(this config): FFMA/FMUL/FADD, their packed FP32x2 forms and IMAD share the FMA "
+                                 "pipe at one warp instruction per 2 cycles per scheduler -- the unit that binds "
+                                 "P2G and G2P (DESIGN.md §6)"}
     kshare = {k: {"ms_per_step": v[0] / max(v[1], 1) * (v[1] / args.steps), "launches": v[1]}
               for k, v in ktimes.items()}
 

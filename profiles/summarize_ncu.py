@@ -4,9 +4,9 @@
                                                               --config c4] > profiles/<round>_<name>.txt
 
 --traffic-json merges, under the bench config name, per kernel ("p2g", "g2p", ...) the
-dram__bytes_read.sum + dram__bytes_write.sum of one launch (bench.py's roofline `traffic`)
-and its executed warp instructions (bench.py's `issue_frac`: instructions / (launch time x
-148 SMs x 4 schedulers x SM clock)).
+dram__bytes_read.sum + dram__bytes_write.sum of one launch (bench.py's roofline `traffic`),
+its executed warp instructions (bench.py's `issue_frac`: instructions / (launch time x
+148 SMs x 4 schedulers x SM clock)) and its FMA-pipe active fraction (`fma_pipe_frac`).
 """
 import json
 import collections
@@ -61,6 +61,12 @@ def main(rep, traffic_json=None, config="c4"):
                     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"):
             if key in d:
                 print(f"   {key:60s} {d[key]}")
+        try:  # the FMA pipe's active fraction (the binding unit of the step kernels)
+            kk = k.replace("qmpm_", "").replace("qmpm::k_", "")
+            traffic.setdefault(kk, {})["fma_pipe"] = float(
+                d["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"].replace(",", "")) / 100.0
+        except (KeyError, ValueError):
+            pass
         stalls = []
         for key, v in d.items():
             if key.startswith("smsp__average_warps_issue_stalled_") and key.endswith("_per_issue_active.ratio"):

@@ -5,7 +5,7 @@ every variant (NVRTC options in QMPM_JIT_OPTS, e.g. -DQMPM_AB_ZPACK=0) starts fr
 kernel times over --steps steps with per-launch events, the baseline repeated first and
 last.  Prints one line per variant.
 
-    python tools/ab_step.py --warm 2000 --steps 20 --variant=-DQMPM_AB_ZPACK=0 ...
+    python tools/ab_step.py --warm 2000 --steps 20 --variant=-DQMPM_AB_ZPACK=0 --variant=ENV:QMPM_G2P_MINB=3 ...
 """
 import argparse
 import os
@@ -48,6 +48,14 @@ with torch.cuda.stream(stream):
     torch.cuda.empty_cache()
 
     def measure(opts):
+        # "ENV:NAME=VALUE[,NAME=VALUE]" sets environment variables (e.g. QMPM_G2P_MINB) instead
+        envs = {}
+        if opts.startswith("ENV:"):
+            envs = dict(kv.split("=", 1) for kv in opts[4:].split(","))
+            opts = ""
+        for k in ("QMPM_G2P_MINB", "QMPM_P2G_MINB", "QMPM_SEG_L"):
+            os.environ.pop(k, None)
+        os.environ.update(envs)
         if opts:
             os.environ["QMPM_JIT_OPTS"] = opts
         else:
