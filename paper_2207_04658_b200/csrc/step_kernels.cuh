@@ -281,6 +281,15 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 #ifndef QMPM_AB_CNT_LOP3
 #define QMPM_AB_CNT_LOP3 0  // (measured: 9.996 vs 10.132 ms G2P at C4 -- the shift-add form wins)
 #endif
+#ifndef QMPM_AB_P2G_NEXT
+#define QMPM_AB_P2G_NEXT 0  // P2G: claim the next block one block ahead (measured: C3 P2G 10.60 vs
+                            // 10.66 ms, 8 ppc 9.01 vs 9.06, C4 6.44 vs 6.33-6.38 -- noise-level, off)
+#endif
+#ifndef QMPM_AB_CNT_NEG
+#define QMPM_AB_CNT_NEG 0  // G2P round counters: count not-up from 255 down (one LEA per field);
+                           // 2: fluid specs only (measured within noise: C4 G2P 9.645 vs 9.72-9.74 ms on
+                           // one box, 9.78-9.86 vs 9.75 on another; C3 11.41 vs 11.34)
+#endif
 #ifndef QMPM_AB_P2G_PACK
 #define QMPM_AB_P2G_PACK 1  // P2G: packed weight products and node momenta (3D)
 #endif
@@ -358,12 +367,28 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
     dc->n_rec = dc->n_slots = dc->n_sorted;
     dc->n_leave = 0u;
   }
+#if QMPM_AB_P2G_NEXT
+  // the next block is claimed while this one runs and its id loaded before this one's
+  // flush, so the dependent chain counter -> active_list -> block_start / cell_count
+  // is not all exposed at each block start (at 8 ppc blocks are short)
+  uint32_t nx_ab = 0, nx_claim = 0;
+  if (lane == 0) nx_ab = lo + atomicAdd(ctr, 1u);
+  nx_ab = __shfl_sync(FULL, nx_ab, 0);
+  uint32_t nx_b = nx_ab < hi ? active_list[nx_ab] : 0u;
+#endif
   for (;;) {  // blocks are taken dynamically (a work counter): no tail from uneven blocks
+#if QMPM_AB_P2G_NEXT
+    const uint32_t ab = nx_ab;
+    if (ab >= hi) break;
+    const uint32_t b = nx_b;
+    if (lane == 0) nx_claim = lo + atomicAdd(ctr, 1u);  // (consumed before the flush)
+#else
     uint32_t ab = 0;
     if (lane == 0) ab = lo + atomicAdd(ctr, 1u);
     ab = __shfl_sync(FULL, ab, 0);
     if (ab >= hi) break;
     const uint32_t b = active_list[ab];
+#endif
     const uint32_t start = block_start[b], end = block_start[b + 1];
     int bc[3];
     block_coords<D>(b, S, bc);
@@ -699,6 +724,10 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
         }
       }
     }
+#if QMPM_AB_P2G_NEXT
+    nx_ab = __shfl_sync(FULL, nx_claim, 0);
+    nx_b = nx_ab < hi ? active_list[nx_ab] : 0u;
+#endif
     cp_async_wait<0>();
     __syncwarp();
     // ---- 4. flush: one vector reduction per non-empty node
@@ -722,27 +751,44 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
 template <class SP>
 struct RoundCounters {
   static constexpr int NP = (SP::NS + 3) / 4;
+  // QMPM_AB_CNT_NEG: pu's bytes start at 255 and count DOWN once per chunk in which the
+  // scalar did not round up, so the fast encode adds its sign mask sb (0 up, -1 not)
+  // shifted into place -- one LEA per field; no byte reaches 0 within the 255 chunks
+  // between flushes, so no borrow crosses bytes
+  static constexpr bool NEG = QMPM_AB_CNT_NEG == 2 ? SP::MAT == 1 : QMPM_AB_CNT_NEG != 0;
+  static constexpr uint32_t PU0 = NEG ? 0xffffffffu : 0u;
   uint32_t pu[NP], pz[NP];
   uint32_t n_since;  // chunks (per lane) since the last flush, warp-uniform
   unsigned c_up, c_z;
   unsigned long long c_n;  // lane-particles counted (dithered: the "all" of down)
   __device__ __forceinline__ void init() {
 #pragma unroll
-    for (int k = 0; k < NP; ++k) pu[k] = pz[k] = 0u;
+    for (int k = 0; k < NP; ++k) {
+      pu[k] = PU0;
+      pz[k] = 0u;
+    }
     n_since = 0u;
     c_up = c_z = 0u;
     c_n = 0ull;
   }
+  // the fast encode's up flag of scalar i as its sign mask sb (0: rounded up, -1: not)
+  __device__ __forceinline__ void count_sb(int i, int sb) {
+    if (NEG)
+      pu[i / 4] += (uint32_t)sb << (8 * (i % 4));
+    else
+      pu[i / 4] += (1u + (uint32_t)sb) << (8 * (i % 4));
+  }
   // exact flags of scalar i: dithered counts on-grid (neither), RNE counts downs
   __device__ __forceinline__ void count(int i, bool up, bool down) {
-    if (up) pu[i / 4] += 1u << (8 * (i % 4));
+    count_sb(i, up ? 0 : -1);
     if (SP::DITHER ? (!up && !down) : down) pz[i / 4] += 1u << (8 * (i % 4));
   }
   __device__ __forceinline__ void flush(int lane) {
 #pragma unroll
     for (int i = 0; i < SP::NS; ++i) {
       if (SP::kind(i) == kKindRaw) continue;
-      const unsigned tu = __reduce_add_sync(FULL, (pu[i / 4] >> (8 * (i % 4))) & 255u);
+      unsigned tu = __reduce_add_sync(FULL, (pu[i / 4] >> (8 * (i % 4))) & 255u);
+      if (NEG) tu -= 32u * (255u - n_since);  // sum over lanes of n_since - (255 - byte)
       const unsigned tz = __reduce_add_sync(FULL, (pz[i / 4] >> (8 * (i % 4))) & 255u);
       if (lane == i) {
         c_up += tu;
@@ -751,7 +797,10 @@ struct RoundCounters {
     }
     c_n += 32ull * n_since;
 #pragma unroll
-    for (int k = 0; k < NP; ++k) pu[k] = pz[k] = 0u;
+    for (int k = 0; k < NP; ++k) {
+      pu[k] = PU0;
+      pz[k] = 0u;
+    }
     n_since = 0u;
   }
   // (up, down) of this lane's scalar after the last flush
@@ -1096,14 +1145,14 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
           if (SP::COUNTERS) {
             // + 1 in the bytes of i and i + 1 (one counter register: i is even) that rounded
             // up (sb == 0): two LOP3 and an add on the integer pipe (the FMA pipe binds)
-#if QMPM_AB_CNT_LOP3
-            const uint32_t ci = 0xffu << (8 * (i % 4));
-            const uint32_t bij = (1u << (8 * (i % 4))) | (1u << (8 * ((i + 1) % 4)));
-            rc.pu[i / 4] += ((~(uint32_t)sbi & ci) | (~(uint32_t)sbj & ~ci)) & bij;
-#else
-            rc.pu[i / 4] += (1u + (uint32_t)sbi) << (8 * (i % 4));
-            rc.pu[(i + 1) / 4] += (1u + (uint32_t)sbj) << (8 * ((i + 1) % 4));
-#endif
+            if (QMPM_AB_CNT_LOP3 && !RoundCounters<SP>::NEG) {
+              const uint32_t ci = 0xffu << (8 * (i % 4));
+              const uint32_t bij = (1u << (8 * (i % 4))) | (1u << (8 * ((i + 1) % 4)));
+              rc.pu[i / 4] += ((~(uint32_t)sbi & ci) | (~(uint32_t)sbj & ~ci)) & bij;
+            } else {
+              rc.count_sb(i, sbi);
+              rc.count_sb(i + 1, sbj);
+            }
             if (zi) rc.pz[i / 4] += 1u << (8 * (i % 4));
             if (zj) rc.pz[(i + 1) / 4] += 1u << (8 * ((i + 1) % 4));
           }
@@ -1116,7 +1165,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
           sput_code<SP>(ow, i, u);
           if (i < D) xc[i] = u;
           if (SP::COUNTERS) {
-            rc.pu[i / 4] += ~(uint32_t)sb & (1u << (8 * (i % 4)));
+            rc.count_sb(i, sb);
             if (z) rc.pz[i / 4] += 1u << (8 * (i % 4));
           }
           continue;
