@@ -227,6 +227,8 @@ __global__ void k_cell_scan(uint32_t* __restrict__ cell_count, uint32_t* __restr
 // (DevCounters::n_slots: it includes a slab's appended arrivals, never synchronised to
 // the host).  kBinItems particles per thread in flight (strided by the CTA size, so loads
 // stay coalesced): the per-particle chain key -> atomic -> store is latency-bound.
+// (Measured at C4, 0.91 ms: 2 or 8 items per thread and 4 or 16 CTAs per SM all within
+// noise of this configuration.)
 constexpr int kBinItems = 4;
 __global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ key, const DevCounters* __restrict__ dc,
                                                       uint32_t* __restrict__ cell_count, uint32_t* __restrict__ perm) {

@@ -53,7 +53,7 @@ with torch.cuda.stream(stream):
         if opts.startswith("ENV:"):
             envs = dict(kv.split("=", 1) for kv in opts[4:].split(","))
             opts = ""
-        for k in ("QMPM_G2P_MINB", "QMPM_P2G_MINB", "QMPM_SEG_L"):
+        for k in ("QMPM_G2P_MINB", "QMPM_P2G_MINB"):
             os.environ.pop(k, None)
         os.environ.update(envs)
         if opts:
