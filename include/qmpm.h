@@ -198,8 +198,8 @@ qmpm_status qmpm_stats(qmpm_ctx* ctx, qmpm_stats_t* out); /* synchronizes; fills
 
 /* Standalone codec (Eq. 3 / Eq. 11 + bit pack) on device arrays, enqueued on
  * cuda_stream.  vals: [n][n_fields] fp32 in PACKING order; words: [n][W].
- * keys: nullable => round-half-even; else dithered with r24(seed, step, keys[i],
- * field) of reading Q5 rev. 3 when scheme->rounding == QMPM_DITHER.  The scheme's dim/material are not
+ * keys: nullable => round-half-even; else dithered with the 16-bit draw r16(seed, step,
+ * keys[i], field) of reading Q5 rev. 3 when scheme->rounding == QMPM_DITHER.  The scheme's dim/material are not
  * used and attr/comp are not checked.  counters (nullable, device, 3*64 u64,
  * accumulated): saturations, round-ups, round-downs per field. */
 qmpm_status qmpm_encode(const qmpm_scheme* scheme, uint64_t n, const float* vals,

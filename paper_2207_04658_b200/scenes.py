@@ -336,7 +336,7 @@ def developed_fluid(seed=0, res=64, cells=(14, 12, 14), ppc_axis=4.1, swirl=1.5,
     `ppc_axis`^3 particles per cell (C4 has ~4.2^3 = 72 ppc), a smooth swirling and
     converging initial flow (|v| ~ 1-2 m/s) so that after ~100 steps the block holds
     compression (J != 1), pressure and shear (C != 0) -- the P2G's full per-cell segments
-    (16 particles) then carry non-trivial momentum and stress."""
+    (48 particles) then carry non-trivial momentum and stress."""
     dx = 1.0 / res
     spacing = dx / ppc_axis
     counts = tuple(int(round(c * ppc_axis)) for c in cells)
