@@ -91,7 +91,6 @@ struct qmpm_ctx {
 };
 
 // kernels one single-GPU step launches (sort: 5, P2G, grid update, G2P)
-constexpr uint64_t kStepLaunches = 8;
 
 namespace qmpm {
 // the thread-local message qmpm_last_error(NULL) returns (used by solver.cu too)
@@ -817,6 +816,7 @@ StepBuffers buffers(qmpm_ctx* ctx, uint64_t n) {
   B.dc = ctx->dc;
   B.dbg = ctx->dbg;
   B.n = (uint32_t)n;
+  B.cap = (uint32_t)std::min<uint64_t>(ctx->cap, 0xffffffffull);
   B.pool = (uint32_t)ctx->pool;
   B.ntiles = ctx->ntiles;
   return B;
@@ -1029,7 +1029,7 @@ qmpm_status qmpm_step(qmpm_ctx* ctx, uint32_t n_steps) {
         }
       }
       CK(cudaGraphLaunch(g, ctx->stream));
-      ctx->launches_total += kStepLaunches;
+      ctx->launches_total += (uint64_t)step_launches(buffers(ctx, ctx->n));
     } else {
       StepBuffers B = buffers(ctx, ctx->n);
       CK(launch_step(ctx->dim, B, ctx->S, mig_of(ctx), ctx->jit, ctx->stream, hook_fn, ctx));

@@ -194,31 +194,96 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __r
 // block_start[b] + inclusive prefix; the scatter's atomicSub leaves each at its cell's
 // START, which P2G reads (and zeroes for the next step's counts).  The block's count
 // has been consumed by the scan: it is zeroed here for the next step's histogram.
+__device__ __forceinline__ void cell_scan_block(uint32_t b, uint32_t lane, uint32_t* __restrict__ cell_count,
+                                                uint32_t* __restrict__ block_count,
+                                                const uint32_t* __restrict__ block_start) {
+  uint32_t* cc = cell_count + (size_t)b * 64;
+  const uint32_t c0 = cc[lane], c1 = cc[lane + 32];
+  uint32_t i0 = c0, i1 = c1;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t0 = __shfl_up_sync(FULL, i0, d), t1 = __shfl_up_sync(FULL, i1, d);
+    if ((int)lane >= d) {
+      i0 += t0;
+      i1 += t1;
+    }
+  }
+  const uint32_t base = block_start[b];
+  const uint32_t tot0 = __shfl_sync(FULL, i0, 31);
+  cc[lane] = base + i0;
+  cc[lane + 32] = base + tot0 + i1;
+  if (lane == 0) block_count[b] = 0u;
+}
+
 __global__ void k_cell_scan(uint32_t* __restrict__ cell_count, uint32_t* __restrict__ block_count,
                             const uint32_t* __restrict__ block_start, const uint32_t* __restrict__ active_list,
                             const DevCounters* __restrict__ dc) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t n_active = dc->n_active;
-  for (uint32_t ab = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ab < n_active; ab += warps) {
-    const uint32_t b = active_list[ab];
-    uint32_t* cc = cell_count + (size_t)b * 64;
-    const uint32_t c0 = cc[lane], c1 = cc[lane + 32];
-    uint32_t i0 = c0, i1 = c1;
+  for (uint32_t ab = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ab < n_active; ab += warps)
+    cell_scan_block(active_list[ab], lane, cell_count, block_count, block_start);
+}
+
+// The whole sort front (scan_reduce + scan_tiles + scan_apply + cell_scan) in ONE CTA
+// when the block table fits one scan tile (nblocks <= kScanTile, e.g. C1's 2D 128^2
+// grid): the same arithmetic in the same order, three launches fewer per step (C1 is
+// launch-bound).  The tile offset of the single tile is 0.
+template <int D>
+__global__ void __launch_bounds__(kScanThreads) k_sort_small(uint32_t* __restrict__ count, SimDev S,
+                                                             uint32_t* __restrict__ block_start,
+                                                             uint32_t* __restrict__ block_slot,
+                                                             uint32_t* __restrict__ active_list,
+                                                             uint32_t* __restrict__ touched_list, uint32_t pool,
+                                                             DevCounters* __restrict__ dc,
+                                                             uint32_t* __restrict__ cell_count) {
+  const uint32_t top_first = D == 3 ? (uint32_t)(S.slab_bz1 - 1 - S.tab_bz0) * (uint32_t)S.nb[0] * (uint32_t)S.nb[1]
+                                    : 0xffffffffu;
+  const uint32_t b0 = threadIdx.x * kScanPer;
+  uint32_t c[kScanPer], a[kScanPer], t[kScanPer];
+  uint3 v = make_uint3(0, 0, 0);
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t0 = __shfl_up_sync(FULL, i0, d), t1 = __shfl_up_sync(FULL, i1, d);
-      if ((int)lane >= d) {
-        i0 += t0;
-        i1 += t1;
-      }
-    }
-    const uint32_t base = block_start[b];
-    const uint32_t tot0 = __shfl_sync(FULL, i0, 31);
-    cc[lane] = base + i0;
-    cc[lane + 32] = base + tot0 + i1;
-    if (lane == 0) block_count[b] = 0u;
+  for (int q = 0; q < kScanPer; ++q) {
+    block_flags<D>(b0 + q, count, S, c[q], a[q], t[q]);
+    v.x += c[q];
+    v.y += a[q];
+    v.z += t[q];
   }
+  uint3 total;
+  uint3 ex = block_exclusive_scan3(v, total);  // (ends with a barrier: every count read)
+  if (threadIdx.x == 0) {  // k_scan_tiles' counters
+    dc->gstep += 1u;
+    dc->n_active = total.y;
+    dc->next_p2g = 0u;
+    dc->next_g2p = 0u;
+    dc->n_touched = total.z;
+    dc->n_touched_eff = total.z < pool ? total.z : pool;
+    dc->n_sorted = total.x;
+    if (total.z > pool) dc->overflow += 1ull;
+    block_start[S.nblocks] = total.x;
+  }
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {  // k_scan_apply
+    const uint32_t b = b0 + q;
+    if (b == top_first) dc->n_active_below = ex.y;
+    if (b < S.nblocks) {
+      block_start[b] = ex.x;
+      if (a[q]) active_list[ex.y] = b;
+      uint32_t slot = 0xffffffffu;
+      if (t[q] && ex.z < pool) {
+        slot = ex.z;
+        touched_list[slot] = b;
+      }
+      block_slot[b] = slot;
+    }
+    ex.x += c[q];
+    ex.y += a[q];
+    ex.z += t[q];
+  }
+  __syncthreads();  // block_start / active_list visible to the CTA
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t ab = threadIdx.x >> 5; ab < total.y; ab += kScanThreads / 32)  // k_cell_scan
+    cell_scan_block(active_list[ab], lane, cell_count, count, block_start);
 }
 
 // Counting-sort scatter by the full key (block, base cell): perm[pos] = record slot,
@@ -230,6 +295,19 @@ __global__ void k_cell_scan(uint32_t* __restrict__ cell_count, uint32_t* __restr
 // (Measured at C4, 0.91 ms: 2 or 8 items per thread and 4 or 16 CTAs per SM all within
 // noise of this configuration.)
 constexpr int kBinItems = 4;
+
+// Grid of a grid-stride (or work-counter) kernel: per_sm CTAs per SM, but no more than
+// `work` items at `per_cta` items per CTA need -- the device-side counts are not known
+// on the host (no per-step sync), the capacity / block count / pool bound them.  Small
+// problems (C1: 8K particles) then launch tens of CTAs instead of ~1,200 idle ones.
+inline unsigned grid_for(int num_sms, int per_sm, uint64_t work, uint64_t per_cta = 256) {
+  const uint64_t need = (work + per_cta - 1) / per_cta;
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)num_sms * per_sm, need));
+}
+// active blocks are at most the blocks of the table and at most the particles
+inline uint64_t max_active(const StepBuffers& B, const SimDev& S) {
+  return std::min<uint64_t>((uint64_t)S.nblocks, (uint64_t)B.cap);
+}
 __global__ void __launch_bounds__(256) k_bin_scatter(const uint32_t* __restrict__ key, const DevCounters* __restrict__ dc,
                                                       uint32_t* __restrict__ cell_count, uint32_t* __restrict__ perm) {
   const uint32_t n = dc->n_slots;
@@ -351,6 +429,12 @@ struct Hk {
 
 template <int D>
 static cudaError_t sort_d(const StepBuffers& B, const SimDev& S, cudaStream_t st, Hk H) {
+  if (B.ntiles == 1) {  // one scan tile: the fused single-CTA front (timed as scan_reduce)
+    H(KScanReduce, 1);
+    k_sort_small<D><<<1, kScanThreads, 0, st>>>(B.block_count, S, B.block_start, B.block_slot, B.active_list,
+                                                B.touched_list, B.pool, B.dc, B.cell_count);
+    H(KScanReduce, 0);
+  } else {
   H(KScanReduce, 1);
   k_scan_reduce<D><<<B.ntiles, kScanThreads, 0, st>>>(B.block_count, S, B.tile_sums);
   H(KScanReduce, 0);
@@ -362,13 +446,18 @@ static cudaError_t sort_d(const StepBuffers& B, const SimDev& S, cudaStream_t st
                                                      B.active_list, B.touched_list, B.pool, B.dc);
   H(KScanApply, 0);
   H(KCellScan, 1);
-  k_cell_scan<<<B.num_sms * 8, 256, 0, st>>>(B.cell_count, B.block_count, B.block_start, B.active_list, B.dc);
+  k_cell_scan<<<grid_for(B.num_sms, 8, 32ull * max_active(B, S)), 256, 0, st>>>(B.cell_count, B.block_count,
+                                                                                  B.block_start, B.active_list, B.dc);
   H(KCellScan, 0);
+  }
   H(KBinScatter, 1);
-  k_bin_scatter<<<B.num_sms * 8, 256, 0, st>>>(B.key, B.dc, B.cell_count, B.perm);
+  k_bin_scatter<<<grid_for(B.num_sms, 8, (uint64_t)B.cap, 256 * kBinItems), 256, 0, st>>>(B.key, B.dc, B.cell_count,
+                                                                                           B.perm);
   H(KBinScatter, 0);
   return cudaGetLastError();
 }
+
+int step_launches(const StepBuffers& B) { return B.ntiles == 1 ? 5 : 8; }
 
 cudaError_t launch_sort(int dim, const StepBuffers& B, const SimDev& S, cudaStream_t st, KernelHook hook, void* user) {
   return dim == 3 ? sort_d<3>(B, S, st, Hk{hook, user}) : sort_d<2>(B, S, st, Hk{hook, user});
@@ -383,7 +472,8 @@ cudaError_t launch_p2g(const StepBuffers& B, const SimDev& S, const StepJit& J, 
   void* args[] = {(void*)&B.rec_in,      (void*)&B.perm, (void*)&B.cell_count, (void*)&B.block_start,
                   (void*)&B.active_list, (void*)&B.dc,   (void*)&B.block_slot, (void*)&B.mp,
                   (void*)&Sv,            (void*)&pv};
-  cudaError_t e = jit_launch(J.p2g, J.p2g_ctas, J.p2g_threads, J.p2g_smem, st, args);
+  cudaError_t e = jit_launch(J.p2g, std::min<unsigned>(J.p2g_ctas, grid_for(1, 1 << 30, max_active(B, S), J.p2g_threads / 32)),
+                             J.p2g_threads, J.p2g_smem, st, args);
   H(KP2G, 0);
   return e;
 }
@@ -393,9 +483,9 @@ cudaError_t launch_grid_update(int dim, const StepBuffers& B, const SimDev& S, c
   Hk H{hook, user};
   H(KGridUpdate, 1);
   if (dim == 3)
-    k_grid_update<3><<<J.num_sms * 8, 256, 0, st>>>(B.mp, B.gv, B.touched_list, B.dc, S);
+    k_grid_update<3><<<grid_for(J.num_sms, 8, 64ull * B.pool), 256, 0, st>>>(B.mp, B.gv, B.touched_list, B.dc, S);
   else
-    k_grid_update<2><<<J.num_sms * 8, 256, 0, st>>>(B.mp, B.gv, B.touched_list, B.dc, S);
+    k_grid_update<2><<<grid_for(J.num_sms, 8, 64ull * B.pool), 256, 0, st>>>(B.mp, B.gv, B.touched_list, B.dc, S);
   H(KGridUpdate, 0);
   return cudaGetLastError();
 }
@@ -411,7 +501,8 @@ cudaError_t launch_g2p(const StepBuffers& B, const SimDev& S, const MigDev& M, c
                   (void*)&B.dbg, (void*)&B.key, (void*)&B.block_count, (void*)&B.cell_count, (void*)&B.block_start,
                   (void*)&B.active_list, (void*)&B.dc, (void*)&B.block_slot, (void*)&B.gv, (void*)&Sv,
                   (void*)&Mv, (void*)&pv};
-  cudaError_t e = jit_launch(J.g2p, J.g2p_ctas, J.g2p_threads, J.g2p_smem, st, args);
+  cudaError_t e = jit_launch(J.g2p, std::min<unsigned>(J.g2p_ctas, grid_for(1, 1 << 30, max_active(B, S), J.g2p_threads / 32)),
+                             J.g2p_threads, J.g2p_smem, st, args);
   H(KG2P, 0);
   return e;
 }

@@ -31,6 +31,7 @@ struct StepBuffers {
   DevCounters* dc;
   float* dbg;              // nullable [n][ns]
   uint32_t n;
+  uint32_t cap;             // particle capacity (an upper bound of the device-side counts)
   uint32_t pool;
   uint32_t ntiles;
   int num_sms;
@@ -63,6 +64,8 @@ struct StepJit {
 // one hook per kernel so the runtime can bracket launches with events
 typedef void (*KernelHook)(void* user, int kernel_id, int begin);
 
+// kernels launch_step launches per step (a one-tile block table fuses the sort front)
+int step_launches(const StepBuffers& B);
 // whole step (single GPU)
 cudaError_t launch_step(int dim, const StepBuffers& B, const SimDev& S, const MigDev& M, const StepJit& J,
                         cudaStream_t st, KernelHook hook, void* user);
