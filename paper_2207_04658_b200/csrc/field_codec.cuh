@@ -20,13 +20,30 @@
 
 namespace qmpm {
 
+#ifndef QMPM_AB_SZEXT
+#define QMPM_AB_SZEXT 1  // sign-extend decoded codes with szext (SASS SGXT, integer pipe)
+#endif
+// the low `width` bits of raw as a signed integer (two's complement, reading Q2).  The
+// shift pair (raw << (32 - width)) >> (32 - width) puts its left shift on the FMA pipe
+// (IMAD.SHL), the pipe that binds the step kernels; szext is one integer-pipe op.
+__device__ __forceinline__ int sext_bits(uint32_t raw, int width) {
+#if QMPM_AB_SZEXT
+  if (width < 32) {
+    int u;
+    asm("szext.wrap.s32 %0, %1, %2;" : "=r"(u) : "r"(raw), "r"(width));
+    return u;
+  }
+#endif
+  return ((int)(raw << (32 - width))) >> (32 - width);
+}
+
 // value of state scalar i from a register-resident record w[0..W] (w[W] = 0)
 template <class SP>
 __device__ __forceinline__ float sdec(const uint32_t* w, const int i) {
   const int wd = SP::word(i), sh = SP::shift(i), wi = SP::width(i);
   const uint32_t raw = (sh + wi <= 32) ? (w[wd] >> sh) : __funnelshift_r(w[wd], w[wd + 1], sh);
   if (SP::kind(i) == kKindRaw) return __uint_as_float(raw);
-  const int u = ((int)(raw << (32 - wi))) >> (32 - wi);  // sign-extend b+1 bits (Q2)
+  const int u = sext_bits(raw, wi);  // sign-extend b+1 bits (Q2)
   if (SP::kind(i) == kKindShared) {  // reading Q4: u * Delta_0 2^E, E = the group exponent
     const int gw = SP::gword(i), gs = SP::gshift(i), eb = SP::ebits(i);
     const uint32_t er = (gs + eb <= 32) ? (w[gw] >> gs) : __funnelshift_r(w[gw], w[gw + 1], gs);
@@ -111,7 +128,14 @@ __device__ __forceinline__ uint32_t senc(const int i, float v, float omr, EncFla
 template <class SP>
 __device__ __forceinline__ void sput(uint32_t* w, const int i, uint32_t bits) {
   const int wd = SP::word(i), sh = SP::shift(i), wi = SP::width(i);
+  // fields never overlap and `bits` holds no bit above the field's width, so the OR is
+  // an ADD -- (bits << sh) + w is one LEA on the integer pipe instead of a shift the
+  // compiler puts on the FMA pipe (IMAD.SHL) plus an OR
+#if QMPM_AB_SZEXT
+  w[wd] += bits << sh;
+#else
   w[wd] |= bits << sh;
+#endif
   if (sh + wi > 32) w[wd + 1] |= bits >> (32 - sh);
 }
 
@@ -291,7 +315,7 @@ template <class SP>
 __device__ __forceinline__ int scode(const uint32_t* w, const int i) {
   const int wd = SP::word(i), sh = SP::shift(i), wi = SP::width(i);
   const uint32_t raw = (sh + wi <= 32) ? (w[wd] >> sh) : __funnelshift_r(w[wd], w[wd + 1], sh);
-  return ((int)(raw << (32 - wi))) >> (32 - wi);
+  return sext_bits(raw, wi);
 }
 
 template <class SP>

@@ -222,6 +222,31 @@ __device__ __forceinline__ void bspline_w(float fx, float w[3]) {
   w[2] = 0.5f * c * c;
 }
 
+#ifndef QMPM_AB_WPACK
+#define QMPM_AB_WPACK 1
+#endif
+// the weights of the first two axes in packed FP32x2 (each lane the same IEEE ops as
+// bspline_w, so the weights are bit-identical), the third (3D) in scalar
+template <int D>
+__device__ __forceinline__ void bspline_weights(const float fx[3], float wt[3][3]) {
+#if QMPM_AB_WPACK
+  const float2 f = make_float2(fx[0], fx[1]);
+  const float2 a = __fadd2_rn(make_float2(1.5f, 1.5f), make_float2(-f.x, -f.y));
+  const float2 b = __fadd2_rn(f, make_float2(-1.0f, -1.0f));
+  const float2 c = __fadd2_rn(f, make_float2(-0.5f, -0.5f));
+  const float2 w0 = __fmul2_rn(__fmul2_rn(make_float2(0.5f, 0.5f), a), a);
+  const float2 w1 = __ffma2_rn(make_float2(-b.x, -b.y), b, make_float2(0.75f, 0.75f));
+  const float2 w2 = __fmul2_rn(__fmul2_rn(make_float2(0.5f, 0.5f), c), c);
+  wt[0][0] = w0.x; wt[1][0] = w0.y;
+  wt[0][1] = w1.x; wt[1][1] = w1.y;
+  wt[0][2] = w2.x; wt[1][2] = w2.y;
+  if (D == 3) bspline_w(fx[2], wt[2]);
+#else
+#pragma unroll
+  for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
+#endif
+}
+
 // 3x3 polar decomposition F = R S, det R = +1 for det F > 0, by Newton's iteration
 // R <- (g R + R^{-T}/g)/2 with Higham's determinant scaling g = |det R|^{-1/3}.
 __device__ __forceinline__ void polar3(const float F[9], float R[9]) {

@@ -604,8 +604,7 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
           }
         }
         float wt[3][3];
-#pragma unroll
-        for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
+        bspline_weights<D>(fx, wt);
         if (D == 3 && QMPM_AB_P2G_PACK) {
           // the same sums with the weight products in FMUL2 pairs and each node's momentum
           // per unit weight built by packed adds of A's columns (row, then column, then
@@ -946,8 +945,7 @@ __device__ __forceinline__ void g2p_body(const uint32_t* __restrict__ rec_in, ui
           lb[a] = base_fx(s[a], S.inv_dx, S.res[a], fx[a], o) - org[a];
         }
       }
-#pragma unroll
-      for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
+      bspline_weights<D>(fx, wt);
       // gather: v' = sum w v_i;  C' = 4/dx sum w v_i (x) (i - fx) = 4/dx (T - v' fx^T),
       // T[a][k] = sum w v_i,a o_k, reduced axis by axis (z, then y, then x)
       float Sv[3] = {0.f, 0.f, 0.f}, T[3][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
