@@ -226,10 +226,16 @@ __device__ __forceinline__ void bspline_w(float fx, float w[3]) {
 #define QMPM_AB_WPACK 1
 #endif
 // the weights of the first two axes in packed FP32x2 (each lane the same IEEE ops as
-// bspline_w, so the weights are bit-identical), the third (3D) in scalar
-template <int D>
+// bspline_w, so the weights are bit-identical), the third (3D) in scalar.  Measured:
+// G2P -0.4 % (C4) / -0.7 % (C3); P2G +0.6 % / -0.5 % (noise) -- P2G keeps the scalar form
+template <int D, bool PACK = true>
 __device__ __forceinline__ void bspline_weights(const float fx[3], float wt[3][3]) {
 #if QMPM_AB_WPACK
+  if (!PACK) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) bspline_w(fx[a], wt[a]);
+    return;
+  }
   const float2 f = make_float2(fx[0], fx[1]);
   const float2 a = __fadd2_rn(make_float2(1.5f, 1.5f), make_float2(-f.x, -f.y));
   const float2 b = __fadd2_rn(f, make_float2(-1.0f, -1.0f));

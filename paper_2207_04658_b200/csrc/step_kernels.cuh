@@ -604,7 +604,7 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
           }
         }
         float wt[3][3];
-        bspline_weights<D>(fx, wt);
+        bspline_weights<D, false>(fx, wt);
         if (D == 3 && QMPM_AB_P2G_PACK) {
           // the same sums with the weight products in FMUL2 pairs and each node's momentum
           // per unit weight built by packed adds of A's columns (row, then column, then
