@@ -20,6 +20,9 @@
 
 namespace qmpm {
 
+#ifndef QMPM_AB_SHFPACK
+#define QMPM_AB_SHFPACK 1  // pack shifts as SHF (integer pipe): G2P -0.4 % (C4), -0.3 % (C3)
+#endif
 #ifndef QMPM_AB_SZEXT
 #define QMPM_AB_SZEXT 1  // sign-extend decoded codes with szext (SASS SGXT, integer pipe)
 #endif
@@ -131,7 +134,15 @@ __device__ __forceinline__ void sput(uint32_t* w, const int i, uint32_t bits) {
   // fields never overlap and `bits` holds no bit above the field's width, so the OR is
   // an ADD -- (bits << sh) + w is one LEA on the integer pipe instead of a shift the
   // compiler puts on the FMA pipe (IMAD.SHL) plus an OR
-#if QMPM_AB_SZEXT
+#if QMPM_AB_SZEXT && QMPM_AB_SHFPACK
+  if (sh > 0 && sh + wi <= 32) {  // (a funnel shift with a zero low word: SHF, integer pipe)
+    uint32_t r;
+    asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(0u), "r"(bits), "r"(sh));
+    w[wd] += r;
+  } else {
+    w[wd] += bits << sh;
+  }
+#elif QMPM_AB_SZEXT
   w[wd] += bits << sh;
 #else
   w[wd] |= bits << sh;
