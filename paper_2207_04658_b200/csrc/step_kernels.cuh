@@ -281,6 +281,9 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 #ifndef QMPM_AB_CNT_LOP3
 #define QMPM_AB_CNT_LOP3 0  // (measured: 9.996 vs 10.132 ms G2P at C4 -- the shift-add form wins)
 #endif
+#ifndef QMPM_AB_DPACK
+#define QMPM_AB_DPACK 0  // P2G: decode scaling of same-Delta scalar pairs as FMUL2 (A/B variant)
+#endif
 #ifndef QMPM_AB_P2G_NEXT
 #define QMPM_AB_P2G_NEXT 0  // P2G: claim the next block one block ahead (measured: C3 P2G 10.60 vs
                             // 10.66 ms, 8 ppc 9.01 vs 9.06, C4 6.44 vs 6.33-6.38 -- noise-level, off)
@@ -590,15 +593,51 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
         float st[D * D];
         stress_of<D, MAT>(s, S, st);  // -dt V_p 4/dx^2 P F^T
         float Q[3] = {0.f, 0.f, 0.f}, A[3][3];
+        // m_p v and m_p dx C, decoded with the scaling folded; consecutive scalars with the
+        // same Delta scale as one FMUL2 pair (the FMA pipe binds; each lane the same op)
+        float mv[3], mcv[D * D];
+        {
+          auto scaled = [&](int i, float m) {
+            return folds(i) ? __int2float_rn(scode<SP>(w, i)) * (SP::delta(i) * m) : m * sdec<SP>(w, i);
+          };
+          auto pair_ok = [&](int i) {
+            return QMPM_AB_DPACK && folds(i) && folds(i + 1) && SP::delta(i) == SP::delta(i + 1);
+          };
+#pragma unroll
+          for (int q = 0; q < D; q += 2) {
+            if (q + 1 < D && pair_ok(D + q)) {
+              const float sc = SP::delta(D + q) * pm;
+              const float2 r = __fmul2_rn(make_float2(__int2float_rn(scode<SP>(w, D + q)),
+                                                      __int2float_rn(scode<SP>(w, D + q + 1))), make_float2(sc, sc));
+              mv[q] = r.x;
+              mv[q + 1] = r.y;
+            } else {
+              mv[q] = scaled(D + q, pm);
+              if (q + 1 < D) mv[q + 1] = scaled(D + q + 1, pm);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < D * D; q += 2) {
+            if (q + 1 < D * D && pair_ok(CO + q)) {
+              const float sc = SP::delta(CO + q) * pmdx;
+              const float2 r = __fmul2_rn(make_float2(__int2float_rn(scode<SP>(w, CO + q)),
+                                                      __int2float_rn(scode<SP>(w, CO + q + 1))), make_float2(sc, sc));
+              mcv[q] = r.x;
+              mcv[q + 1] = r.y;
+            } else {
+              mcv[q] = scaled(CO + q, pmdx);
+              if (q + 1 < D * D) mcv[q + 1] = scaled(CO + q + 1, pmdx);
+            }
+          }
+        }
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           // m_p v
-          Q[a] = folds(D + a) ? __int2float_rn(scode<SP>(w, D + a)) * (SP::delta(D + a) * pm) : pm * sdec<SP>(w, D + a);
+          Q[a] = mv[a];
 #pragma unroll
           for (int k2 = 0; k2 < D; ++k2) {
             // A[k][a] = dx (stress + m_p C)[a][k] (the APIC/MLS affine momentum)
-            const int ci = CO + a * D + k2;
-            const float mc = folds(ci) ? __int2float_rn(scode<SP>(w, ci)) * (SP::delta(ci) * pmdx) : pmdx * sdec<SP>(w, ci);
+            const float mc = mcv[a * D + k2];
             A[k2][a] = (MAT == 1 && a != k2) ? mc : fmaf(S.dx, st[a * D + k2], mc);
             Q[a] = fmaf(-fx[k2], A[k2][a], Q[a]);
           }
