@@ -74,10 +74,12 @@ def gather(sims, ns, W, debug=True):
 
 
 @pytest.mark.parametrize("k", [2, 3])
-@pytest.mark.parametrize("case", ["fluid", "elastic"])
+@pytest.mark.parametrize("case", ["fluid", "elastic", "fluid_res32"])
 def test_slab_step_matches_oracle(case, k):
     if case == "fluid":
         sc, sch = scenes.small_fluid_3d(), schemes.f2()
+    elif case == "fluid_res32":  # slab block tables of one scan tile: the fused sort front
+        sc, sch = scenes.small_fluid_3d(res=32, n_target=20_000), schemes.f2()
     else:
         sc, sch = scenes.small_elastic_3d(), schemes.e01()
     w0, _ = oracle.encode_state(sch, sc.state())

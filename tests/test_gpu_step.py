@@ -90,6 +90,9 @@ CASES = {
     # no field straddles a word (the bit struct's rule; T-bitpack-perf analogue)
     "s3_3d_e0.01_nostraddle": (scenes.small_elastic_3d, lambda: schemes.with_layout(schemes.e001(), "nostraddle"), 20),
     "s4_3d_fluid_f2_nostraddle": (scenes.small_fluid_3d, lambda: schemes.with_layout(schemes.f2(), "nostraddle"), 20),
+    # a 32^3 grid: 512 blocks, one scan tile, so the step's sort front is the fused
+    # one-CTA k_sort_small (C1 takes it in 2D)
+    "s4_3d_fluid_f2_res32": (lambda: scenes.small_fluid_3d(res=32, n_target=20_000), schemes.f2, 20),
 }
 
 
