@@ -237,7 +237,10 @@ typedef struct {
     int32_t nranks, rank;
     int32_t z0, z1;            /* owned cell planes [z0, z1): multiples of 4 (z1 may be grid_res[2]) */
     uint64_t migrate_capacity; /* particles per direction per step (the fixed migration buffer);
-                                  0 = max(65536, min(max_particles / 256, 2^22)) */
+                                  0 = max(65536, min(max_particles / 256, 2^22)).  The exchanges
+                                  are fixed-size, so the ranks of one run agree on ONE capacity:
+                                  qmpm_connect_nccl (one all-reduce) and qmpm_step_group re-size
+                                  every rank's buffers to the largest value of the ranks */
 } qmpm_slab;
 
 /* Like qmpm_create, for rank `slab->rank` of `slab->nranks` (3D only).  Particles

@@ -482,6 +482,28 @@ qmpm_status qmpm_destroy(qmpm_ctx* ctx) {
 namespace {
 // qmpm_create, and qmpm_create_slab with `slab` set: the block table then covers the
 // rank's own block planes plus the ghost plane above (table-local block ids)
+// (Re)allocate a slab ctx's migration buffers for `cap` particles per direction.
+static cudaError_t alloc_migration(qmpm_ctx* ctx, uint64_t cap) {
+  for (int b = 0; b < 4; ++b)
+    if (ctx->mig_buf[b]) {
+      cudaFree(ctx->mig_buf[b]);
+      ctx->mig_buf[b] = nullptr;
+    }
+  if (ctx->dead_list) {
+    cudaFree(ctx->dead_list);
+    ctx->dead_list = nullptr;
+  }
+  ctx->mig_cap = cap;
+  ctx->dead_cap = (uint32_t)std::min<uint64_t>(2 * ctx->mig_cap, 0xffffffffull);
+  ctx->mig_bytes = mig_bytes_of(mig_of(ctx));
+  cudaError_t e = cudaSuccess;
+  for (int b = 0; b < 4 && !e; ++b) e = cudaMalloc((void**)&ctx->mig_buf[b], ctx->mig_bytes);
+  if (!e) e = cudaMalloc((void**)&ctx->dead_list, sizeof(uint32_t) * ctx->dead_cap);
+  for (int b = 0; b < 4 && !e; ++b) e = cudaMemsetAsync(ctx->mig_buf[b], 0, sizeof(MigHeader), ctx->stream);
+  if (!e) e = cudaStreamSynchronize(ctx->stream);
+  return e;
+}
+
 qmpm_status create_impl(const qmpm_params* params, const qmpm_scheme* scheme, void* cuda_stream,
                         const qmpm_slab* slab, qmpm_ctx** out) {
   qmpm_ctx* ctx = nullptr;
@@ -707,15 +729,10 @@ qmpm_status create_impl(const qmpm_params* params, const qmpm_scheme* scheme, vo
     // step; the first step may route up to half a plane (particles loaded by position)
     ctx->mig_cap = slab->migrate_capacity ? slab->migrate_capacity
                                           : std::max<uint64_t>(65536, std::min<uint64_t>(ctx->cap / 256, 1u << 22));
-    ctx->dead_cap = (uint32_t)std::min<uint64_t>(2 * ctx->mig_cap, 0xffffffffull);
-    ctx->mig_bytes = mig_bytes_of(mig_of(ctx));
     ctx->plane_elems = (size_t)S.nb[0] * S.nb[1] * 64;
-    cudaError_t e2 = cudaSuccess;
-    for (int b = 0; b < 4 && !e2; ++b) e2 = cudaMalloc((void**)&ctx->mig_buf[b], ctx->mig_bytes);
-    if (!e2) e2 = cudaMalloc((void**)&ctx->dead_list, sizeof(uint32_t) * ctx->dead_cap);
+    cudaError_t e2 = alloc_migration(ctx, ctx->mig_cap);
     if (!e2) e2 = cudaMalloc((void**)&ctx->plane_send, sizeof(float4) * ctx->plane_elems);
     if (!e2) e2 = cudaMalloc((void**)&ctx->plane_recv, sizeof(float4) * ctx->plane_elems);
-    for (int b = 0; b < 4 && !e2; ++b) e2 = cudaMemsetAsync(ctx->mig_buf[b], 0, sizeof(MigHeader), ctx->stream);
     if (!e2) e2 = cudaMemsetAsync(ctx->plane_recv, 0, sizeof(float4) * ctx->plane_elems, ctx->stream);
     if (!e2) e2 = cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking);
     for (int b = 0; b < 4 && !e2; ++b) e2 = cudaEventCreateWithFlags(&ctx->ev[b], cudaEventDisableTiming);
@@ -1047,10 +1064,19 @@ qmpm_status qmpm_step_group(qmpm_ctx* const* ctxs, int n, uint32_t n_steps) {
     if (!ctxs[r] || !ctxs[r]->slab || ctxs[r]->nranks != n || ctxs[r]->rank != r)
       return fail(ctx, QMPM_EINVAL, "qmpm_step_group: ctxs[%d] must be the slab ctx of rank %d of %d", r, r, n);
     if (ctxs[r]->stream != ctxs[0]->stream) return fail(ctx, QMPM_EINVAL, "qmpm_step_group: one stream for all ctxs");
-    if ((ctxs[r]->ids[0] != nullptr) != (ctxs[0]->ids[0] != nullptr) || ctxs[r]->W != ctxs[0]->W ||
-        ctxs[r]->mig_cap != ctxs[0]->mig_cap)
-      return fail(ctx, QMPM_EINVAL, "qmpm_step_group: ctxs differ in scheme, flags or migration capacity");
+    if ((ctxs[r]->ids[0] != nullptr) != (ctxs[0]->ids[0] != nullptr) || ctxs[r]->W != ctxs[0]->W)
+      return fail(ctx, QMPM_EINVAL, "qmpm_step_group: ctxs differ in scheme or flags");
     if (ctxs[r]->sticky) return fail(ctxs[r], QMPM_ESTATE, "ctx %d is in error", r);
+  }
+  {  // one migration capacity for the group (as qmpm_connect_nccl agrees on over NCCL)
+    uint64_t mc = 0;
+    for (int r = 0; r < n; ++r) mc = std::max<uint64_t>(mc, ctxs[r]->mig_cap);
+    for (int r = 0; r < n; ++r)
+      if (ctxs[r]->mig_cap != mc) {
+        const cudaError_t e = alloc_migration(ctxs[r], mc);
+        if (e) return fail(ctxs[r], e == cudaErrorMemoryAllocation ? QMPM_ENOMEM : QMPM_ECUDA, "qmpm_step_group: %s",
+                           cudaGetErrorString(e));
+      }
   }
   cudaStream_t st = ctxs[0]->stream;
   auto copy = [&](void* dst, const void* src, size_t bytes) -> qmpm_status {
@@ -1109,6 +1135,31 @@ qmpm_status qmpm_connect_nccl(qmpm_ctx* ctx, const uint8_t id[128]) {
   std::string err;
   ctx->nccl = nccl_connect(id, ctx->nranks, ctx->rank, err);
   if (!ctx->nccl) return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+  // The migration exchanges are fixed-size (no host sync per step), so every rank must
+  // post buffers of ONE capacity.  The default capacity follows each rank's own particle
+  // capacity, which differs between slabs: agree on the largest over the ranks (one
+  // all-reduce, here only) and re-size this rank's buffers to it.
+  {
+    unsigned int* d = nullptr;
+    unsigned int v = (unsigned int)std::min<uint64_t>(ctx->mig_cap, 0xffffffffull);
+    cudaError_t e = cudaMalloc((void**)&d, sizeof(unsigned int));
+    if (!e) e = cudaMemcpyAsync(d, &v, sizeof(v), cudaMemcpyHostToDevice, ctx->stream);
+    if (e) {
+      if (d) cudaFree(d);
+      return fail(ctx, QMPM_ECUDA, "qmpm_connect_nccl: %s", cudaGetErrorString(e));
+    }
+    if (!nccl_allreduce_max_u32(ctx->nccl, d, ctx->stream, err)) {
+      cudaFree(d);
+      return fail(ctx, QMPM_ENCCL, "%s", err.c_str());
+    }
+    e = cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream);
+    if (!e) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d);
+    if (!e && (uint64_t)v != ctx->mig_cap) e = alloc_migration(ctx, v);
+    if (e)
+      return fail(ctx, e == cudaErrorMemoryAllocation ? QMPM_ENOMEM : QMPM_ECUDA, "qmpm_connect_nccl: %s",
+                  cudaGetErrorString(e));
+  }
   return QMPM_OK;
 }
 

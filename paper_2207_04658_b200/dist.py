@@ -31,11 +31,13 @@ def slab_cuts(nz: int, world: int, weights=None):
 
 
 def rank_zrange(cuts, rank, dx):
-    """The z interval (world units) of a rank's slab: particles are handed to the rank
-    whose cell planes contain their z (the device resolves the half-cell offset of the
-    base cell by routing to the neighbour in the first step)."""
+    """The z interval (world units) of the particles a rank owns: base cell
+    floor(z / dx - 1/2) in its planes [z0, z1), i.e. z in [(z0 + 1/2) dx, (z1 + 1/2) dx)
+    (P:561's base cell), so the first step migrates only the float-rounding strays at
+    the faces instead of half a cell plane (which overflowed the default migration
+    buffer at 4 slabs of 25M particles)."""
     z0, z1 = cuts[rank]
-    return z0 * dx, z1 * dx
+    return (z0 + 0.5) * dx, (z1 + 0.5) * dx
 
 
 def rank_count_bound(scene, cuts, rank):

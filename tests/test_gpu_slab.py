@@ -39,7 +39,7 @@ def owner(state, sim, slabs):
     return o
 
 
-def make_group(sc, sch, words, step0, k, flags):
+def make_group(sc, sch, words, step0, k, flags, mig_caps=None):
     slabs = cuts(sc.sim["grid_res"][2], k)
     st = oracle.decode_state(sch, words)
     own = owner(st, sc.sim, slabs)
@@ -47,7 +47,8 @@ def make_group(sc, sch, words, step0, k, flags):
     sims = []
     for r, (z0, z1) in enumerate(slabs):
         idx = np.nonzero(own == r)[0]
-        s = qmpm.Sim(sc.sim, sch, words.shape[0], flags=flags, stream=stream, slab=(k, r, z0, z1))
+        s = qmpm.Sim(sc.sim, sch, words.shape[0], flags=flags, stream=stream, slab=(k, r, z0, z1),
+                     migrate_capacity=mig_caps[r] if mig_caps else 0)
         s.set_words(dev(words[idx]), step0)
         s.set_ids(dev(idx.astype(np.uint32)))
         sims.append(s)
@@ -97,6 +98,27 @@ def test_slab_step_matches_oracle(case, k):
     assert err.max() <= REL, err.max(axis=0)
     keys = np.array([oracle.particle_key(sch, w_in[i]) for i in range(n)], np.uint32)
     assert np.array_equal(g_words, oracle.encode_state(sch, g_pre, step=11, keys=keys)[0])
+
+
+def test_ranks_agree_on_one_migration_capacity():
+    """The migration exchanges are fixed-size, so ranks whose capacities differ (the
+    default follows each rank's particle capacity, which differs between slabs) are
+    re-sized to the largest before the first exchange -- the in-process group here, the
+    NCCL connect by an all-reduce -- instead of posting mismatched transfers."""
+    sc, sch = scenes.small_fluid_3d(), schemes.f2()
+    w0, _ = oracle.encode_state(sch, sc.state())
+    w_in, _ = oracle.run(sc.sim, sch, w0, 1, 10)
+    o_pre, _, _ = oracle.step(sc.sim, sch, w_in, 11)
+    sims, _ = make_group(sc, sch, w_in, 10, 3, qmpm.TRACK_IDS | qmpm.DEBUG_PREENCODE,
+                         mig_caps=[65536, 90000, 70000])
+    qmpm.step_group(sims, 1)
+    ids, _, g_pre = gather(sims, sims[0].n_scalars, sims[0].W)
+    for s in sims:
+        s.close()
+    assert np.array_equal(ids, np.arange(w_in.shape[0]))
+    s_h = scales(sc.sim, o_pre, oracle.decode_state(sch, w_in))
+    err = np.abs(g_pre.astype(np.float64) - o_pre) / np.maximum(np.abs(o_pre), s_h)
+    assert err.max() <= REL, err.max(axis=0)
 
 
 def test_slab_run_conserves_and_matches_single_gpu():

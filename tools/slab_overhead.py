@@ -1,9 +1,11 @@
 """Per-step overhead of the slab decomposition, measured on ONE GPU with the in-process
 group transport (qmpm_step_group): the C4 scene (n particles) as one context vs k z slabs
-stepping together.  The slab path adds a second sort pass, the migration packing and
-recount, the ghost/velocity plane packs and two host synchronisations per step; with k
-slabs on one GPU their kernels run back to back, so (t_k - t_1) / k estimates the
-per-rank overhead of an N-GPU weak-scaling step.
+stepping together.  The slab path adds the leaver routing in G2P, the device-side
+append of arrivals, the ghost / velocity plane packs and the split P2G / G2P launches
+(no host synchronisation per step since round 2); with k slabs on one GPU their
+kernels and exchange copies run back to back on one stream, so (t_k - t_1) / k
+estimates the per-rank overhead of an N-GPU weak-scaling step (the NCCL transfers
+themselves are not in it).
 
     python tools/slab_overhead.py [--n 200000000] [--k 2] [--steps 10]
 """
@@ -49,10 +51,10 @@ def main():
         sim.close()
         torch.cuda.empty_cache()
         cuts = qdist.slab_cuts(sc.sim["grid_res"][2], args.k)
-        per = sc.n_particles // args.k
         sims = []
         for r in range(args.k):
-            s = qmpm.Sim(sc.sim, sch, int(per * 1.25) + 65536, stream=stream, slab=(args.k, r, cuts[r][0], cuts[r][1]))
+            s = qmpm.Sim(sc.sim, sch, qdist.slab_capacity(sc, cuts, r), stream=stream,
+                         slab=(args.k, r, cuts[r][0], cuts[r][1]))  # (capacities reconciled by the group)
             qdist.load_slab(s, sc, cuts, r, track_ids=False)
             sims.append(s)
         qmpm.step_group(sims, args.warm)
