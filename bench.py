@@ -89,6 +89,8 @@ def make_scene(args, world=1):
         sch = schemes.f2()
     if args.scheme:
         sch = schemes.fp32(sc.dim, sc.material) if args.scheme == "fp32" else schemes.BY_NAME[args.scheme]()
+    # positions over the whole domain (the weak-scaling runs extend C4 along z; a no-op at N = 1)
+    sch = schemes.with_domain(sch, sc.sim)
     sch = schemes.with_layout(schemes.with_rounding(sch, args.rounding), args.layout)
     return sc, sch
 

@@ -58,6 +58,29 @@ def f2():
     return dict(dim=3, material="fluid", rounding="dither", seed=DITHER_SEED, fields=f)
 
 
+def with_domain(sch, sim):
+    """The scheme's position fields widened to the simulation domain: a FIXED x
+    component whose range is below the domain's extent along its axis (grid_res * dx)
+    gets range 2^ceil(log2 extent) and log2 of that many more fraction bits, so
+    Delta = range 2^-b is unchanged (the integer next-step key and the grid stay
+    aligned) and positions beyond 1 do not saturate.  The z-slab weak-scaling runs
+    (bench.py --gpus N) extend C4's domain N times along z: F2's x_z goes from 19 to
+    19 + log2 N bits (253 + 3 = 256 bits = 8 words at N = 8)."""
+    import copy
+    import math
+    out = copy.deepcopy(sch)
+    for f in out["fields"]:
+        if f["attr"] != "x" or f["kind"] != "fixed" or f.get("offset", 0.0) != 0.0:
+            continue
+        ext = float(sim["grid_res"][f["comp"]]) * float(sim["dx"])
+        if ext <= f["range"]:
+            continue
+        k = math.ceil(math.log2(ext / f["range"]))
+        f["range"] = f["range"] * 2.0 ** k
+        f["frac_bits"] = f["frac_bits"] + k
+    return out
+
+
 def ranges_from_record(max_abs, factor=2.0, pow2=True):
     """R_h from a recorded full-precision run ("record the ranges from the full
     precision simulation and multiply the ranges by a factor (e.g., 2)"); rounded up

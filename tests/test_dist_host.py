@@ -90,3 +90,19 @@ def test_c4_slab_capacities_hold_every_rank(world):
         cap = qdist.slab_capacity(sc, cuts, r)
         assert cap >= 1.2 * bounds[r], (r, cap, bounds[r])
         assert cap < 2 ** 32 - 1
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_weak_scaling_scheme_covers_the_domain(k):
+    """bench.py --gpus k extends C4 k times along z; the position fields must cover
+    [0, k) without saturating, with Delta unchanged (the integer next-step key needs
+    Delta_x = 2^-18 on every axis) and F2's record still 8 words."""
+    from paper_2207_04658_b200 import qmpm, schemes
+    sc = scenes.c4(n_target=1000, z_extent=float(k))
+    sch = schemes.with_domain(schemes.f2(), sc.sim)
+    for f in sch["fields"]:
+        if f["attr"] == "x":
+            ext = sc.sim["grid_res"][f["comp"]] * sc.sim["dx"]
+            assert f["range"] >= ext
+            assert f["range"] * 2.0 ** -f["frac_bits"] == 2.0 ** -18
+    assert qmpm.layout(sch)[1] == 8

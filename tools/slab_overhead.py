@@ -25,31 +25,39 @@ def main():
     ap.add_argument("--k", type=int, default=2)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warm", type=int, default=20)
+    ap.add_argument("--weak", action="store_true",
+                    help="the decomposition bench.py --gpus k uses: --n particles PER SLAB, the C4 scene "
+                         "extended k times along z (one 256^3 slab per rank); skips the single-ctx run")
     args = ap.parse_args()
     import torch
     from paper_2207_04658_b200 import dist as qdist
     from paper_2207_04658_b200 import qmpm, scenes, schemes
     torch.cuda.set_device(0)
-    sc, sch = scenes.c4(n_target=args.n), schemes.f2()
+    if args.weak:
+        sc = scenes.c4(n_target=args.n * args.k, z_extent=float(args.k))
+        sch = schemes.with_domain(schemes.f2(), sc.sim)  # (x_z over [0, k), as bench.py)
+    else:
+        sc, sch = scenes.c4(n_target=args.n), schemes.f2()
     stream = torch.cuda.Stream()
-    out = {"n": sc.n_particles, "k": args.k}
+    out = {"n": sc.n_particles, "k": args.k, "weak": args.weak}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
-        sim = qmpm.Sim(sc.sim, sch, sc.n_particles, stream=stream)
-        chunk = 1 << 24
-        for s0 in range(0, sc.n_particles, chunk):
-            st = sc.state_chunk(s0, min(chunk, sc.n_particles - s0), backend="torch", device="cuda")
-            (sim.set_state if s0 == 0 else sim.append_state)(st)
+        if not args.weak:
+            sim = qmpm.Sim(sc.sim, sch, sc.n_particles, stream=stream)
+            chunk = 1 << 24
+            for s0 in range(0, sc.n_particles, chunk):
+                st = sc.state_chunk(s0, min(chunk, sc.n_particles - s0), backend="torch", device="cuda")
+                (sim.set_state if s0 == 0 else sim.append_state)(st)
+                stream.synchronize()
+            sim.step(args.warm)
             stream.synchronize()
-        sim.step(args.warm)
-        stream.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        sim.step(args.steps)
-        e1.record(stream)
-        e1.synchronize()
-        out["single_ms"] = e0.elapsed_time(e1) / args.steps
-        sim.close()
-        torch.cuda.empty_cache()
+            e0.record(stream)
+            sim.step(args.steps)
+            e1.record(stream)
+            e1.synchronize()
+            out["single_ms"] = e0.elapsed_time(e1) / args.steps
+            sim.close()
+            torch.cuda.empty_cache()
         cuts = qdist.slab_cuts(sc.sim["grid_res"][2], args.k)
         sims = []
         for r in range(args.k):
@@ -66,7 +74,8 @@ def main():
         e1.synchronize()
         out["group_ms"] = e0.elapsed_time(e1) / args.steps
         out["group_wall_ms"] = (time.perf_counter() - t0) * 1e3 / args.steps
-        out["overhead_per_slab_ms"] = (out["group_ms"] - out["single_ms"]) / args.k
+        if "single_ms" in out:
+            out["overhead_per_slab_ms"] = (out["group_ms"] - out["single_ms"]) / args.k
         out["n_per_slab"] = [s.stats().n_particles for s in sims]
         for s in sims:
             s.close()
