@@ -81,3 +81,40 @@ def test_two_rank_nccl_matches_one_context():
     ke_1, com_1 = oracle.aggregates(sc.sim, oracle.decode_state(sch, w1))
     assert abs(ke_g - ke_1) <= 1e-3 * abs(ke_1)
     assert np.all(np.abs(com_g - com_1) <= 1e-3 * np.abs(com_1))
+
+
+def test_one_rank_nccl_path_matches_oracle():
+    """The NCCL code path on ONE GPU: a one-rank slab context (a single-rank NCCL
+    communicator is valid) loads NCCL, initialises the communicator, agrees on the
+    migration capacity by the connect-time all-reduce and runs the slab phases with the
+    per-step status all-reduce (no neighbour transfers).  One step meets the P2 bar
+    against the fp64 oracle; ten more keep every particle."""
+    from paper_2207_04658_b200 import qmpm
+    from test_gpu_step import REL, dev, scales
+    sc, sch = scenes.small_fluid_3d(), schemes.f2()
+    w0, _ = oracle.encode_state(sch, sc.state())
+    w_in, _ = oracle.run(sc.sim, sch, w0, 1, 10)
+    o_pre, _, _ = oracle.step(sc.sim, sch, w_in, 11)
+    n = w_in.shape[0]
+    nz = sc.sim["grid_res"][2]
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        sim = qmpm.Sim(sc.sim, sch, n, flags=qmpm.TRACK_IDS | qmpm.DEBUG_PREENCODE, stream=stream,
+                       slab=(1, 0, 0, nz))
+        sim.connect_nccl(qmpm.get_unique_id())
+        sim.set_words(dev(w_in), 10)
+        sim.set_ids(dev(np.arange(n, dtype=np.uint32)))
+        sim.step(1)
+        m = sim.stats().n_particles
+        pre = np.zeros((m, sim.n_scalars), np.float32)
+        ids = np.zeros(m, np.uint32)
+        sim.read_state(ids=ids, capacity=m)
+        sim.read_debug(pre)
+        sim.step(10)
+        st = sim.stats()
+        sim.close()
+    assert m == n and st.n_particles == n and st.step == 21
+    pre = pre[np.argsort(ids)]
+    s_h = scales(sc.sim, o_pre, oracle.decode_state(sch, w_in))
+    err = np.abs(pre.astype(np.float64) - o_pre) / np.maximum(np.abs(o_pre), s_h)
+    assert err.max() <= REL, err.max(axis=0)
