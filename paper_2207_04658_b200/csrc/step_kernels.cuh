@@ -281,6 +281,10 @@ __device__ __forceinline__ void read_staged(const uint32_t* row, uint32_t* w) {
 #ifndef QMPM_AB_CNT_LOP3
 #define QMPM_AB_CNT_LOP3 0  // (measured: 9.996 vs 10.132 ms G2P at C4 -- the shift-add form wins)
 #endif
+#ifndef QMPM_AB_TILE_PACK
+#define QMPM_AB_TILE_PACK 0  // P2G: tile (m, p_z, p_x, p_y) with packed node updates (measured slower:
+                              // C4 P2G 6.54 vs 6.25 ms, C3 10.79 vs 10.60 -- the per-node RMW chain is latency-bound)
+#endif
 #ifndef QMPM_AB_DPACK
 #define QMPM_AB_DPACK 0  // P2G: decode scaling of same-Delta scalar pairs as FMUL2 (A/B variant)
 #endif
@@ -345,6 +349,9 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
                                          const SimDev& S, int part) {
   constexpr int D = SP::D, MAT = SP::MAT, NSV = SP::NS, W = SP::W;
   constexpr int NN = D == 3 ? 27 : 9;  // stencil nodes
+  // the warp tile as (m, p_z, p_x, p_y) (3D, packed accumulators): one FFMA2 + one FADD2
+  // per node update instead of four scalar ops
+  constexpr bool kTP = QMPM_AB_TILE_PACK && D == 3 && QMPM_AB_P2G_PACK;
   using G = Geo<D>;
   using LY = P2GLayout<SP>;
   extern __shared__ float4 smem4[];
@@ -648,11 +655,13 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
           // the same sums with the weight products in FMUL2 pairs and each node's momentum
           // per unit weight built by packed adds of A's columns (row, then column, then
           // node: Q + ox A_x + oy A_y + oz A_z)
-          const float2 a0xy = make_float2(A[0][0], A[0][1]), a0z0 = make_float2(A[0][2], 0.0f);
-          const float2 a1xy = make_float2(A[1][0], A[1][1]), a1z0 = make_float2(A[1][2], 0.0f);
-          const float2 a2xy = make_float2(A[2][0], A[2][1]), a2z0 = make_float2(A[2][2], 0.0f);
+          // (TILE_PACK: the z pair is (1, M_z), so azm accumulates (sum w, p_z) -- the
+          // order of the tile's (m, p_z) pair)
+          const float2 a0xy = make_float2(A[0][0], A[0][1]), a0z0 = kTP ? make_float2(0.0f, A[0][2]) : make_float2(A[0][2], 0.0f);
+          const float2 a1xy = make_float2(A[1][0], A[1][1]), a1z0 = kTP ? make_float2(0.0f, A[1][2]) : make_float2(A[1][2], 0.0f);
+          const float2 a2xy = make_float2(A[2][0], A[2][1]), a2z0 = kTP ? make_float2(0.0f, A[2][2]) : make_float2(A[2][2], 0.0f);
           const float2 wy01 = make_float2(wt[1][0], wt[1][1]), wz01 = make_float2(wt[2][0], wt[2][1]);
-          float2 rxy = make_float2(Q[0], Q[1]), rz1 = make_float2(Q[2], 1.0f);
+          float2 rxy = make_float2(Q[0], Q[1]), rz1 = kTP ? make_float2(1.0f, Q[2]) : make_float2(Q[2], 1.0f);
 #pragma unroll
           for (int ox = 0; ox < 3; ++ox) {
             const float2 wxy01 = __fmul2_rn(make_float2(wt[0][ox], wt[0][ox]), wy01);
@@ -752,10 +761,16 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
           const int idx = base_idx + (D == 3 ? (ox * G::T + oy) * G::T + oz : ox * G::T + oy);
           if (mine && occ == o) {
             float4 t = tile[idx];
-            t.x = fmaf(azm[q].y, S.p_mass, t.x);
-            t.y += axy[q].x;
-            t.z += axy[q].y;
-            t.w += azm[q].x;
+            if (kTP) {  // tile (m, p_z, p_x, p_y): (m, p_z) += (sum w, p_z) * (m_p, 1); (p_x, p_y) += axy
+              const float2 mz = __ffma2_rn(azm[q], make_float2(S.p_mass, 1.0f), make_float2(t.x, t.y));
+              const float2 xy = __fadd2_rn(make_float2(t.z, t.w), axy[q]);
+              t = make_float4(mz.x, mz.y, xy.x, xy.y);
+            } else {
+              t.x = fmaf(azm[q].y, S.p_mass, t.x);
+              t.y += axy[q].x;
+              t.z += axy[q].y;
+              t.w += azm[q].x;
+            }
             tile[idx] = t;
           }
           __syncwarp();
@@ -774,7 +789,8 @@ __device__ __forceinline__ void p2g_body(const uint32_t* __restrict__ rec, const
       if (acc.x != 0.0f) {
         const uint32_t e = s_tnode[t];
         const uint32_t slot = s_nslot[e >> 6];
-        if (slot != 0xffffffffu) atomicAdd(&mp[(size_t)slot * 64 + (e & 63u)], acc);
+        if (slot != 0xffffffffu)
+          atomicAdd(&mp[(size_t)slot * 64 + (e & 63u)], kTP ? make_float4(acc.x, acc.z, acc.w, acc.y) : acc);
       }
     }
     __syncwarp();
