@@ -77,6 +77,19 @@ def main():
         if "single_ms" in out:
             out["overhead_per_slab_ms"] = (out["group_ms"] - out["single_ms"]) / args.k
         out["n_per_slab"] = [s.stats().n_particles for s in sims]
+        # per-kernel device time of the group step (events around every launch), summed
+        # over the slabs, ms per step -- where the extra time of a slab step goes
+        for s in sims:
+            s.set_profiling(True)
+        qmpm.step_group(sims, args.steps)
+        stream.synchronize()
+        kt = {}
+        for s in sims:
+            for name, (ms, cnt) in s.kernel_times().items():
+                if cnt:
+                    kt[name] = kt.get(name, 0.0) + ms / args.steps
+            s.set_profiling(False)
+        out["group_kernel_ms_per_step"] = {k: round(v, 3) for k, v in sorted(kt.items(), key=lambda x: -x[1])}
         for s in sims:
             s.close()
     print(json.dumps(out), flush=True)
